@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the RKC electro-quasistatic hot path (BASELINE.json metric).
+
+One "step" = one RKC time step, path (B) of SURVEY.md §8d: rkc_advance_fixed
+with s = 4 stages and dt = 0.9 beta(4)/rho(x0) on the C3 workload (215^3
+jittered unit cube, 9,984,384 free dofs, nonlinear microvaristor layer), i.e.
+4 F-evaluations, each = fused K(x)x + SPE start vector + AMG-PCG M-solve at
+rel_tol 1e-12, plus the fused stage updates.
+
+value = DOF-stage-updates/s = n_free x F-evaluations / device time (whole job,
+summed over ranks); steps_per_s is reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4] [--impl b200|reference]
+
+--impl reference times the CPU restatement of the reference (oracle/, the
+reference itself needs Eigen and cannot be built here) on a
+bounded sample of the same mesh family, with all host threads for the element
+kernel exactly like the reference (PCG/AMG serial, proj/src/matfree.cpp:105).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RKC time steps/sec & DOF-updates/sec at 1/2/4/8 B200; % HBM roofline vs CPU"
+UNIT = "DOF-stage-updates/s"
+S_STAGES = 4
+
+MATERIALS = {
+    "1": {"eps_r": 3.0, "conductivity": {"kind": "constant", "kappa": 1e-9}},
+    "2": {"eps_r": 12.0, "conductivity": {"kind": "microvaristor", "kappa_lo": 1e-10, "kappa_hi": 3e-6,
+                                          "e_switch": 5e5, "width": 5e4}},
+    "3": {"eps_r": 3.0, "conductivity": {"kind": "constant", "kappa": 1e-9}},
+}
+
+# SURVEY.md §8d configurations (unit cube, hv amplitude scaled from the reference slab)
+CONFIGS = {
+    "c1": dict(n=36, jitter=0.0, planes=[1 / 3, 2 / 3]),
+    "c2": dict(n=99, jitter=0.0, planes=[1 / 3, 2 / 3]),
+    "c3": dict(n=215, jitter=0.1, planes=[0.45, 0.55]),
+    "c4": dict(n=367, jitter=0.1, planes=[0.45, 0.55]),
+}
+# bounded CPU sample of the same family (same physics/planes/jitter, 48^3 cells)
+CPU_SAMPLE = dict(n=48, steps=2)
+
+
+def scenario(n, jitter, planes, estimator="spe"):
+    return {
+        "name": f"bench_cube{n}",
+        "mesh": {"box": {"nx": n, "ny": n, "nz": n, "lx": 1.0, "ly": 1.0, "lz": 1.0, "z_planes": planes,
+                         "regions": [1, 2, 3], "jitter": jitter}},
+        "order": 1,
+        "materials": MATERIALS,
+        "excitations": {"hv": {"kind": "sinusoid", "amplitude": 4e4 / 0.012, "frequency": 50.0},
+                        "ground": {"kind": "constant", "value": 0.0}},
+        "solver": {"preconditioner": "amg", "rel_tol": 1e-12, "max_iter": 500},
+        "estimator": {"mode": estimator, "window": 8},
+    }
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# ------------------------------------------------------------------ CPU (oracle) leg
+def cpu_sample(steps, cores):
+    """Time the CPU restatement of the reference on the bounded sample; returns
+    (DOF-stage-updates/s, steps/s, description)."""
+    from oracle import pyoracle as po  # checker / baseline only (never the measured product)
+
+    cfg = scenario(CPU_SAMPLE["n"], 0.1, [0.45, 0.55])
+    cfg["workers"] = cores
+    o = po.Problem(cfg)
+    x = 2e4 * po.random_vec(o.n_free, 31)
+    rho = o.spectral_radius(0.0, x)
+    dt = 0.9 * 0.653 * (S_STAGES ** 2 - 1) / rho
+    t0 = time.perf_counter()
+    x = o.rkc_advance_fixed(0.0, x, dt, S_STAGES, steps)
+    wall = time.perf_counter() - t0
+    dof_updates = o.n_free * S_STAGES * steps / wall
+    desc = (f"oracle (C++ restatement of the reference, -O3, OpenMP element kernel with {cores} threads, serial "
+            f"PCG/SGS-AMG as in the reference) on {CPU_SAMPLE['n']}^3 jittered cube of the C3 family "
+            f"({o.n_free} free dofs), {steps} RKC steps path B (s=4), stepping time only")
+    return dof_updates, steps / wall, desc
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    from oracle import pyoracle as po
+    cfg = scenario(CPU_SAMPLE["n"], 0.1, [0.45, 0.55])
+    cfg["workers"] = cores
+    o = po.Problem(cfg)
+    x = 2e4 * po.random_vec(o.n_free, 31)
+    rho = o.spectral_radius(0.0, x)
+    dt = 0.9 * 0.653 * (S_STAGES ** 2 - 1) / rho
+    t = 0.0
+    for _ in range(args.warmup):
+        x = o.rkc_advance_fixed(t, x, dt, S_STAGES, 1)
+        t += dt
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x = o.rkc_advance_fixed(t, x, dt, S_STAGES, 1)
+        t += dt
+    wall = time.perf_counter() - t0
+    value = o.n_free * S_STAGES * args.steps / wall
+    sample = (f"{CPU_SAMPLE['n']}^3 jittered cube of the C3 family ({o.n_free} free dofs), RKC path B s=4, "
+              f"{args.steps} timed steps after {args.warmup} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "steps_per_s": args.steps / wall, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cpu sample of {args.config}: {sample}", "n_free": o.n_free},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": "oracle/ C++ restatement (reference unbuildable: Eigen3 absent); " + sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 leg
+def run_b200(args):
+    rank, world, local_rank = dist_env()
+    import torch
+    import paper_1612_09447_b200 as eb
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    spec = CONFIGS[args.config]
+    cfg = scenario(spec["n"], spec["jitter"], spec["planes"])
+    t_setup = time.perf_counter()
+    g = eb.FemSystem(cfg, device=local_rank)
+    t_setup = time.perf_counter() - t_setup
+    n = g.n_free
+    lib = eb.load_library()
+    x0 = np.zeros(n)
+    import ctypes as C
+    lib.eqs_random_vec(C.c_int(n), C.c_uint(31), x0.ctypes.data_as(C.POINTER(C.c_double)))
+    x0 *= 2e4
+    g.set_state(0.0, x0, 0.0)
+    rho = g.spectral_radius()
+    dt = 0.9 * 0.653 * (S_STAGES ** 2 - 1) / rho
+    g.set_state(0.0, x0, dt)
+    stream_ptr = C.c_void_p()
+    lib.eqs_get_stream(g._h, C.byref(stream_ptr))
+    stream = torch.cuda.ExternalStream(stream_ptr.value, device=torch.device("cuda", local_rank))
+
+    for _ in range(args.warmup):
+        g.rkc_advance_fixed(dt, S_STAGES, 1)
+    st0 = g.stats()
+    g.timing(True)
+    g.timing_reset()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.eqs_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            g.rkc_advance_fixed(dt, S_STAGES, 1)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.eqs_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    timing = g.timing()
+    g.timing(False)
+    st1 = g.stats()
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    f_evals = st1["m_solves"] - st0["m_solves"]
+    iters = st1["pcg_iterations"] - st0["pcg_iterations"]
+    value = world * n * f_evals / (ms / 1e3)
+
+    # e2e: the same step through the public API with host buffers (H2D state in, D2H state out)
+    x_host, _ = g.get_state()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    e_steps = max(1, min(args.steps, 5))
+    for _ in range(e_steps):
+        g.set_state(g.get_state()[1]["t"], x_host, dt)
+        g.rkc_advance_fixed(dt, S_STAGES, 1)
+        x_host, _ = g.get_state()
+    e_wall = time.perf_counter() - e0
+    if dist:
+        t = torch.tensor([e_wall], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_wall = float(t.item())
+    e2e_value = world * n * S_STAGES * e_steps / e_wall
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peaks, peak_kind = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    # roofline of the dominant kernel class (TimeClass in gpu_system.hpp): per-class
+    # device time from CUDA events on the library stream, algorithmic bytes per launch
+    names = ["stiffness K(x)x", "pcg spmv+vectors", "v-cycle", "rkc stage/error", "spe estimator", "boundary"]
+    cls = max(range(6), key=lambda c: timing["ms"][c])
+    dom = None
+    spmv_cls = 1
+    if timing["launches"][spmv_cls] and timing["bytes"][spmv_cls]:
+        avg_ms = timing["ms"][spmv_cls] / timing["launches"][spmv_cls]
+        per = timing["bytes"][spmv_cls] / timing["launches"][spmv_cls]
+        ach = per / (avg_ms / 1e3) / 1e9
+        dom = {"kernel": "PCG fine-level M_II SpMV+dot and fused x/r update (k_spmv_red + k_pcg_update)",
+               "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+               "traffic": None, "bytes_per_launch": per, "avg_launch_ms": avg_ms,
+               "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        cv, csps, desc = cpu_sample(CPU_SAMPLE["steps"], cores)
+        cpu = {"value": cv, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "steps_per_s": 1e3 * args.steps / ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated mesh + mt19937 initial state; no dataset)",
+        "config": {"workload": f"{args.config}: {spec['n']}^3 {'jittered ' if spec['jitter'] else ''}unit cube, "
+                               f"{n} free dofs, {g.n_tets} tets, microvaristor layer z in {spec['planes']}, "
+                               f"RKC path B s={S_STAGES} dt=0.9*beta(4)/rho (={dt:.4g}s), SPE(8) + AMG-PCG 1e-12",
+                   "n_free": n, "n_tets": g.n_tets, "nnz_mass_free": g.nnz_mass_free,
+                   "amg_levels": g.amg_levels(), "parallelism": f"replicas x{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (matrices + vectors >> 126 MB), no flush needed"},
+        "pcg_iters_per_solve": iters / max(1, f_evals), "f_evals_per_step": f_evals / args.steps,
+        "setup_s": t_setup, "rho": rho,
+        "clocks": clocks.summary(),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                "steps": e_steps},
+        "gpu_launches": launches,
+        "roofline": dom,
+        "time_by_class_ms": {names[c]: timing["ms"][c] for c in range(6)},
+        "bytes_by_class": {names[c]: timing["bytes"][c] for c in range(6)},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the in-run CPU baseline sample")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

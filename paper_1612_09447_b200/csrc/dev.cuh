@@ -1,0 +1,138 @@
+// Device-side helpers and kernel launcher declarations (sm_100a, fp64 CUDA
+// cores; no tensor cores — the path is sparse and HBM-bound).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace eqsb {
+
+constexpr int kBlock = 256;
+
+// number of kernels this library has launched (bench.py's gpu_launches)
+extern long g_launch_count;
+// Reduction kernels run grid-stride on a fixed grid so that the partial-sum
+// count (and therefore the summation order) is fixed: deterministic results.
+constexpr int kRedGrid = 148 * 8;
+
+// device scalar slots (double) used by the fused PCG / RKC kernels
+enum Slot : int {
+  S_PQ = 0,   // p.q
+  S_RR,       // r.r
+  S_RZ,       // r.z (current)
+  S_RZ_OLD,   // r.z (previous iteration)
+  S_BB,       // b.b
+  S_X0X0,     // x0.x0
+  S_DOT,      // generic dot
+  S_ERR,      // RKC weighted error sum
+  S_NORM,     // generic norm^2
+  S_MDOT,     // first of kMaxMulti multi-dot slots
+  kMaxMulti = 16,
+  S_COUNT = S_MDOT + kMaxMulti
+};
+
+struct Reducer {
+  double* partials;   // [S_COUNT][kRedGrid]
+  unsigned* counters; // [S_COUNT]
+  double* scal;       // [S_COUNT] results
+};
+
+// CSR matrix resident in HBM (int32 indices, fp64 values, sorted columns).
+struct DevCsr {
+  int n_rows = 0, n_cols = 0;
+  long nnz = 0;
+  int* row_ptr = nullptr;
+  int* col_idx = nullptr;
+  double* values = nullptr;
+  int tpr = 4;  // threads per row used by the SpMV kernels
+};
+
+struct ChebCoef {
+  double c0, c1, inv_theta;
+};
+
+// Material table in constant memory (kappa_of_e, proj/src/materials.cpp:25-33)
+struct DevMaterial {
+  int kind;         // 0 constant, 1 microvaristor
+  double kappa;     // constant
+  double lo, hi;    // log10(kappa_lo), log10(kappa_hi) hoisted per material
+  double e_switch, inv_width;
+};
+constexpr int kMaxMaterials = 64;
+
+// ---- stiffness (k_stiffness.cu)
+void set_materials(const DevMaterial* mats, int n, cudaStream_t s);
+// pass 1: per-tet local products (ytet[t][n_local]); x_state and v in device
+// dof numbering; coords [n_dofs][4] (x, y, z, pad)
+void launch_kx_tets(int order, int n_tets, const int* tet_dofs, const unsigned char* tet_mat, const double* coords,
+                    const double* x_state, const double* v, double* ytet, int* geo_error, cudaStream_t s);
+// pass 2: out[d] = base[d] + sign * sum over incident slots (ascending tet)
+void launch_kx_gather(int n_rows, const long* slot_ptr, const int* slots, const double* ytet, const double* base,
+                      double sign, double* out, cudaStream_t s);
+// coloured single pass: y[dof] += local product for one colour batch
+void launch_kx_colored(int order, int n_batch, const int* batch_tets, const int* tet_dofs,
+                       const unsigned char* tet_mat, const double* coords, const double* x_state, const double* v,
+                       double* y, int* geo_error, cudaStream_t s);
+
+// ---- sparse linear algebra (k_sparse.cu)
+void launch_spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s);
+// y = b - A x, and (if red) ||y||^2 into slot
+void launch_residual(const DevCsr& a, const double* b, const double* x, double* y, Reducer* red, int slot,
+                     cudaStream_t s);
+// q = A p ; slot <- p.q
+void launch_spmv_dot(const DevCsr& a, const double* p, double* q, Reducer red, int slot, cudaStream_t s);
+// x += alpha p ; r -= alpha q ; slot_rr <- r.r ; alpha = scal[S_RZ]/scal[S_PQ]
+void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s);
+// p = z + beta p, beta = scal[S_RZ]/scal[S_RZ_OLD]
+void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s);
+// Chebyshev(2) smoother pieces
+void launch_cheb_pre(const DevCsr& a, const double* invd, const double* b, double* z, ChebCoef c, cudaStream_t s);
+void launch_cheb_post2(const DevCsr& a, const double* invd, const double* r0, double* z, ChebCoef c,
+                       const double* b_dot, Reducer* red, int slot, cudaStream_t s);
+// z += P zc
+void launch_prolong_add(const DevCsr& p, const double* zc, double* z, cudaStream_t s);
+// z = Ainv b (dense, n <= 1024)
+void launch_dense_solve(int n, const double* ainv, const double* b, double* z, cudaStream_t s);
+// Jacobi: z = invd .* r (+ dot r.z into slot when red)
+void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s);
+
+// ---- vector kernels (k_sparse.cu)
+void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, cudaStream_t s);
+// slot+k <- V_k . w for k < m (V column-major with leading dim ld)
+void launch_multi_dot(int n, int m, const double* const* V, const double* w, Reducer red, int slot0, cudaStream_t s);
+void launch_axpy(int n, double a, const double* x, double* y, cudaStream_t s);            // y += a x
+void launch_scale(int n, double a, const double* x, double* y, cudaStream_t s);           // y = a x
+void launch_axpy_dev(int n, const double* coef, double sign, const double* x, double* y, cudaStream_t s);  // y += sign*(*coef) x
+// y = sum_k c[k] V_k  (coefficients by value)
+struct CoefPack {
+  double c[kMaxMulti];
+};
+void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s);
+// w = invd .* (A v)   (power iteration on D^-1 A for the smoother bounds)
+void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, double* w, cudaStream_t s);
+void launch_fill(long n, double v, double* y, cudaStream_t s);
+// RKC stage (proj/src/integrators.cpp:167-168): y = a0 y0 + mu y1 + nu y2 + mt f + gt f0
+void launch_rkc_stage(int n, double a0, double mu, double nu, double mt, double gt, const double* y0,
+                      const double* y1, const double* y2, const double* f, const double* f0, double* y,
+                      cudaStream_t s);
+// y = y0 + c f
+void launch_axpby_into(int n, const double* y0, double c, const double* f, double* y, cudaStream_t s);
+// RKC error estimate + weighted RMS sum (integrators.cpp:20-31,201-202)
+void launch_rkc_error(int n, const double* x, const double* xn, const double* f0, const double* fn, double dt,
+                      double atol, double rtol, Reducer red, int slot, cudaStream_t s);
+// permutations: y[i] = x[idx[i]] / y[idx[i]] = x[i]
+void launch_gather(int n, const int* idx, const double* x, double* y, cudaStream_t s);
+void launch_scatter(int n, const int* idx, const double* x, double* y, cudaStream_t s);
+// per-boundary-set scalars passed by value (no H2D copy per stage)
+constexpr int kMaxSets = 16;
+struct SetVals {
+  double v[kMaxSets];
+};
+// boundary lift: full[n_free + i] = set_vals[set_of_fixed[i]]
+void launch_lift_fixed(int n_fixed, const int* set_of_fixed, SetVals vals, double* fixed_part, cudaStream_t s);
+// r[row_k] -= sum_s coef[k][s] * rate[s]  (compressed M_IB xdot_B, fem_system.cpp:65)
+void launch_boundary_load(int n_rows, const int* rows, const double* coef, int n_sets, SetVals rates, double* r,
+                          cudaStream_t s);
+
+}  // namespace eqsb

@@ -1,0 +1,232 @@
+// GpuSystem: the B200-resident counterpart of the reference FemSystem
+// (proj/include/eqs/fem_system.hpp:30-73) plus the integrator state
+// (proj/include/eqs/integrators.hpp:23-29). Host code controls, the device
+// holds every vector and matrix.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <deque>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dev.cuh"
+#include "eqs_internal.hpp"
+
+namespace eqsb {
+
+struct SolveStats {
+  long m_solves = 0, pcg_iterations = 0, rho_solves = 0, rho_pcg_iterations = 0;
+  long precond_setups = 0, assemblies = 0, applies = 0, spe_fallbacks = 0;
+  double t_residual = 0, t_solve = 0, t_setup = 0, t_estimator = 0;
+};
+struct SolveRecord {
+  double t = 0;
+  int estimator_rank = 0, iterations = 0;
+  double initial_rel_residual = 0;
+};
+struct PcgResult {
+  int iterations = 0;
+  double rel_residual = 0, initial_rel_residual = 0;
+  bool converged = false;
+};
+struct StepAttempt {
+  double t_start = 0, dt = 0;
+  bool accepted = false;
+  int stages = 0;
+  double error = 0, rho = 0, dt_next = 0;
+};
+struct RkcOptions {
+  double rtol = 1e-2, atol = 1e-8;
+  int max_stages = 200, rho_refresh_every = 25;
+};
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  ~DevBuf();
+  void alloc(size_t count);
+  void upload(const T* host, size_t count, cudaStream_t s);
+  void download(T* host, size_t count, cudaStream_t s) const;
+};
+
+struct DevLevel {
+  DevCsr A, P, R;
+  DevBuf<int> a_rp, a_ci, p_rp, p_ci, r_rp, r_ci;
+  DevBuf<double> a_v, p_v, r_v;
+  DevBuf<double> invd, b, z, t;
+  ChebCoef cheb{};
+  double lambda_smoother = 0;
+};
+
+// timing classes (eqs_timing in include/eqs_b200.h)
+enum TimeClass { TC_STIFF = 0, TC_PCG = 1, TC_VCYCLE = 2, TC_RKC = 3, TC_SPE = 4, TC_BOUNDARY = 5, TC_COUNT = 8 };
+
+class GpuSystem {
+ public:
+  GpuSystem(Problem&& p, int device);
+  ~GpuSystem();
+
+  // sizes
+  int n_dofs() const { return n_dofs_; }
+  int n_free() const { return n_free_; }
+  int n_fixed() const { return n_fixed_; }
+  int n_tets() const { return n_tets_; }
+  const Problem& problem() const { return prob_; }
+  const HostCsr& mass_ii() const { return m_ii_; }
+  const HostCsr& mass_ib() const { return m_ib_; }
+  const AmgHierarchy& amg() const { return amg_; }
+  const std::vector<int>& colors();  // lazily computed (bit-exact, matfree.cpp:11-38)
+  int n_colors();
+  SolveStats& stats() { return stats_; }
+  std::vector<SolveRecord>& solve_records() { return records_; }
+  cudaStream_t stream() const { return stream_; }
+  bool host_only() const { return device_ < 0; }
+
+  // ---- operators on device buffers (device dof numbering: free first, then fixed)
+  // y = K(x_state) v on full vectors (rows: all dofs)
+  void kx_apply_full_dev(const double* x_state, const double* v, double* y);
+  // r = -(K(x) x)|free + boundary load of rates at t (eval_residual core)
+  void residual_dev(double t, double* x_full, double* r);
+  // x_full tail <- Dirichlet values at t
+  void lift_dev(double t, double* x_full);
+  void mass_apply_dev(const double* v, double* y);
+  // PCG on M_II with the configured preconditioner (x0 may be null)
+  PcgResult pcg_dev(const double* b, const double* x0, double* x, double tol, int max_iter);
+  // f = M^-1 (b - K(x)x) with the estimator; throws NumericalError on failure
+  PcgResult eval_rhs_dev(double t, double* x_full, double* f);
+  void apply_minv_stiffness_dev(double t, double* x_full, const double* v_free, double* y);
+  double estimate_spectral_radius(double t, double* x_full);
+
+  // ---- host-pointer wrappers in reference dof numbering
+  void kx_apply_host(const double* x_state, const double* v, double* y);
+  void kx_residual_host(const double* x_full, const double* b_mass, double* r);
+  void eval_residual_host(double t, const double* x, double* r);
+  PcgResult eval_rhs_host(double t, const double* x, double* f);
+  PcgResult mass_solve_host(const double* b, const double* x0, double tol, int max_iter, double* x);
+  void mass_apply_host(const double* v, double* y);
+  void apply_minv_stiffness_host(double t, const double* x_state, const double* v, double* y);
+  void lift_full_host(double t, const double* x_free, double* x_full);
+
+  // ---- integrator state (device resident)
+  void set_state(double t, const double* x_host, double dt);
+  void get_state(double* x_host);
+  double state_t = 0, state_dt = 0;
+  long st_accepted = 0, st_rejected = 0, st_stages = 0;
+  double rho_value = 0;
+  long rho_age = 0;
+  bool rho_valid = false;
+  double spectral_radius_cached(int refresh_every);
+  StepAttempt rkc_step(const RkcOptions& o);
+  void rkc_advance_fixed(double dt, int s);
+  StepAttempt euler_step(double dt);
+  double* state_dev() { return X_; }
+  double* scratch_full() { return full_[0].p != X_ ? full_[0].p : full_[1].p; }
+
+  // ---- options / timing
+  int stiffness_mode = 0;  // 0 gather, 1 coloured
+  int cheb_degree = 2;
+  double cheb_ratio = 6.0;
+  void set_cheb(double ratio);
+  bool timing_on = false;
+  void tic(int cls);
+  void toc(int cls, double bytes);
+  void timing_resolve(double ms[TC_COUNT], long launches[TC_COUNT], double bytes[TC_COUNT]);
+  void timing_reset();
+  double kx_bytes() const;       // algorithmic bytes of one K(x)v
+  double spmv_bytes(const DevCsr& a) const;
+  int amg_levels() const { return (int)levels_.size(); }
+  const DevLevel& level(int l) const { return levels_[l]; }
+
+ private:
+  void build_device();
+  void vcycle(int l, const double* b, double* z, bool dot_into_rz);
+  void precondition(const double* r, double* z);  // z = M^-1 r, S_RZ <- r.z
+  void kx_tets(const double* x, const double* v);
+  double read_scalar(int slot);
+  void read_scalars(int first, int count, double* out);
+  void check_kernel_flags();
+  void sync();
+  std::vector<double> set_values(double t, bool rates) const;
+  // estimator (start_vector.cpp:84-109,152-164)
+  bool estimator_next(const double* r, double* x0);
+  void estimator_feedback(const double* x);
+  int estimator_rank_ = 0;
+
+  Problem prob_;
+  int device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  int n_dofs_ = 0, n_free_ = 0, n_fixed_ = 0, n_tets_ = 0, n_local_ = 4, order_ = 1, n_sets_ = 0;
+  std::vector<int> dev2ref_, ref2dev_;
+  std::vector<int> colors_;
+  int n_colors_ = -1;
+  HostCsr m_ii_, m_ib_;
+  AmgHierarchy amg_;
+  SolveStats stats_;
+  std::vector<SolveRecord> records_;
+
+  // device mesh data
+  DevBuf<double> coords_;       // [n_dofs][4]
+  DevBuf<int> tet_dofs_;        // [n_tets][n_local] device numbering
+  DevBuf<unsigned char> tet_mat_;
+  DevBuf<long> slot_ptr_;
+  DevBuf<int> slots_;
+  DevBuf<double> ytet_;
+  DevBuf<int> err_;             // kernel error flags
+  DevBuf<int> set_of_fixed_;
+  DevBuf<int> bl_rows_;
+  DevBuf<double> bl_coef_;
+  DevBuf<double> set_vals_;     // [n_sets]
+  int n_bl_rows_ = 0;
+  // colour batches (lazy)
+  DevBuf<int> color_tets_;
+  std::vector<long> color_off_;
+  // matrices
+  DevCsr mii_;
+  DevBuf<int> mii_rp_, mii_ci_;
+  DevBuf<double> mii_v_, mii_invd_;
+  std::vector<DevLevel> levels_;
+  DevBuf<double> coarse_inv_;
+  int coarse_n_ = 0;
+  // reductions
+  DevBuf<double> red_partials_, red_scal_;
+  DevBuf<unsigned> red_counters_;
+  Reducer red_{};
+  double* pinned_ = nullptr;  // host pinned scalar mirror [S_COUNT + 8]
+  // work vectors
+  DevBuf<double> w_r_, w_z_, w_p_, w_q_, w_full_a_, w_full_b_, w_free_a_, w_free_b_;
+  DevBuf<double> full_[4], F0_, F_, Fn_, rho_v_, rho_w_;  // full_: state + 3 stage buffers
+  std::vector<std::unique_ptr<DevBuf<double>>> basis_w_;
+  double* X_ = nullptr;
+  // estimator history (device ring)
+  std::vector<std::unique_ptr<DevBuf<double>>> hist_pool_;
+  std::deque<double*> history_;
+  std::vector<std::unique_ptr<DevBuf<double>>> basis_;
+  // timing
+  struct Ev {
+    cudaEvent_t a, b;
+    int cls;
+    double bytes;
+  };
+  std::vector<Ev> events_;
+  std::vector<cudaEvent_t> ev_pool_;
+  int open_cls_ = -1, nest_ = 0;
+  cudaEvent_t open_ev_ = nullptr;
+  double acc_ms_[TC_COUNT] = {}, acc_bytes_[TC_COUNT] = {};
+  long acc_n_[TC_COUNT] = {};
+  cudaEvent_t get_event();
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+}  // namespace eqsb

@@ -1,0 +1,523 @@
+// Sparse / vector kernels of the M-solve (AMG-PCG) and the RKC recurrence.
+// All HBM-bound: CSR rows are read by TPR-thread groups (TPR chosen per
+// matrix from the mean row length) so that a warp streams contiguous
+// col_idx/values; gathered vectors hit L2. Reductions are fused into the
+// producing kernel and finished deterministically (fixed grid, last-block
+// ordered sum).
+#include <cuda_runtime.h>
+
+#include "dev.cuh"
+
+namespace eqsb {
+
+long g_launch_count = 0;
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum; result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[kBlock / 32];
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = l < (kBlock / 32) ? sh[l] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+// Store this block's partial; the last block to arrive sums all partials in
+// block order and writes the result (deterministic for a fixed grid).
+__device__ __forceinline__ void reduce_finish(double v, Reducer red, int slot) {
+  __shared__ bool last;
+  const double bs = block_sum(v);
+  double* part = red.partials + (size_t)slot * kRedGrid;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = bs;
+    __threadfence();
+    const unsigned prev = atomicAdd(red.counters + slot, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += kBlock) acc += __ldcg(part + i);
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) {
+      red.scal[slot] = acc;
+      red.counters[slot] = 0u;
+    }
+  }
+}
+
+int red_grid(long work_items) {
+  long g = (work_items + kBlock - 1) / kBlock;
+  if (g > kRedGrid) g = kRedGrid;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// Row-group SpMV core: returns sum_k A_ik x_k for `row` in lane 0 of the group.
+// All lanes of the warp must call it (shuffles); rows >= n contribute nothing.
+template <int TPR>
+__device__ __forceinline__ double row_dot(const int* __restrict__ rp, const int* __restrict__ ci,
+                                          const double* __restrict__ v, const double* __restrict__ x, int row,
+                                          int lane, int n) {
+  const bool ok = row < n;
+  const int beg = ok ? rp[row] : 0, end = ok ? rp[row + 1] : 0;
+  double s = 0.0;
+#pragma unroll 4
+  for (int k = beg + lane; k < end; k += TPR) s += v[k] * __ldg(x + ci[k]);
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, TPR);
+  return s;
+}
+// same with the gathered vector scaled on the fly: sum_k A_ik x_k w_k
+template <int TPR>
+__device__ __forceinline__ double row_dot_scaled(const int* __restrict__ rp, const int* __restrict__ ci,
+                                                 const double* __restrict__ v, const double* __restrict__ x,
+                                                 const double* __restrict__ w, int row, int lane, int n) {
+  const bool ok = row < n;
+  const int beg = ok ? rp[row] : 0, end = ok ? rp[row + 1] : 0;
+  double s = 0.0;
+#pragma unroll 4
+  for (int k = beg + lane; k < end; k += TPR) {
+    const int c = ci[k];
+    s += v[k] * (__ldg(x + c) * __ldg(w + c));
+  }
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, TPR);
+  return s;
+}
+
+template <int TPR>
+__global__ void __launch_bounds__(kBlock) k_spmv(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                 const double* __restrict__ v, const double* __restrict__ x,
+                                                 double* __restrict__ y) {
+  const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
+  const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
+  if ((tid & ~31L) / TPR >= n) return;  // warp-uniform exit
+  const double s = row_dot<TPR>(rp, ci, v, x, row, lane, n);
+  if (lane == 0 && row < n) y[row] = s;
+}
+
+// grid-stride over row groups with a fused reduction. MODE 0: q = A p, sum p.q
+// MODE 1: y = b - A x, sum y.y
+template <int TPR, int MODE>
+__global__ void __launch_bounds__(kBlock) k_spmv_red(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                     const double* __restrict__ v, const double* __restrict__ x,
+                                                     const double* __restrict__ b, double* __restrict__ y,
+                                                     Reducer red, int slot, int do_red) {
+  const int lane = threadIdx.x % TPR;
+  const long groups_per_grid = (long)gridDim.x * (kBlock / TPR);
+  // every group iterates the same number of times (shuffles need full warps)
+  const long n_pad = ((n + (long)(kBlock / TPR) - 1) / (kBlock / TPR)) * (kBlock / TPR);
+  double acc = 0.0;
+  for (long row = (long)blockIdx.x * (kBlock / TPR) + threadIdx.x / TPR; row < n_pad; row += groups_per_grid) {
+    const double s = row_dot<TPR>(rp, ci, v, x, (int)row, lane, n);
+    if (lane == 0 && row < n) {
+      if (MODE == 0) {
+        y[row] = s;
+        acc += x[row] * s;
+      } else {
+        const double r = b[row] - s;
+        y[row] = r;
+        acc += r * r;
+      }
+    }
+  }
+  if (do_red) reduce_finish(acc, red, slot);
+}
+
+template <int TPR>
+__global__ void __launch_bounds__(kBlock) k_cheb_pre(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                     const double* __restrict__ v, const double* __restrict__ invd,
+                                                     const double* __restrict__ b, double* __restrict__ z,
+                                                     ChebCoef c) {
+  const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
+  const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
+  if ((tid & ~31L) / TPR >= n) return;
+  const double s = row_dot_scaled<TPR>(rp, ci, v, b, invd, row, lane, n);
+  if (lane == 0 && row < n) {
+    const double bi = b[row], di = invd[row];
+    z[row] = c.c0 * bi * di + c.c1 * di * (bi - s * c.inv_theta);
+  }
+}
+
+// z += c0 D^-1 r0 + c1 D^-1 (r0 - A D^-1 r0 / theta); optional sum b.z
+template <int TPR>
+__global__ void __launch_bounds__(kBlock) k_cheb_post2(int n, const int* __restrict__ rp,
+                                                       const int* __restrict__ ci, const double* __restrict__ v,
+                                                       const double* __restrict__ invd,
+                                                       const double* __restrict__ r0, double* __restrict__ z,
+                                                       ChebCoef c, const double* __restrict__ bdot, Reducer red,
+                                                       int slot, int do_red) {
+  const int lane = threadIdx.x % TPR;
+  const long groups_per_grid = (long)gridDim.x * (kBlock / TPR);
+  const long n_pad = ((n + (long)(kBlock / TPR) - 1) / (kBlock / TPR)) * (kBlock / TPR);
+  double acc = 0.0;
+  for (long row = (long)blockIdx.x * (kBlock / TPR) + threadIdx.x / TPR; row < n_pad; row += groups_per_grid) {
+    const double s = row_dot_scaled<TPR>(rp, ci, v, r0, invd, (int)row, lane, n);
+    if (lane == 0 && row < n) {
+      const double ri = r0[row], di = invd[row];
+      const double zn = z[row] + (c.c0 * ri * di + c.c1 * di * (ri - s * c.inv_theta));
+      z[row] = zn;
+      if (do_red) acc += bdot[row] * zn;
+    }
+  }
+  if (do_red) reduce_finish(acc, red, slot);
+}
+
+template <int TPR>
+__global__ void __launch_bounds__(kBlock) k_prolong_add(int n, const int* __restrict__ rp,
+                                                        const int* __restrict__ ci, const double* __restrict__ v,
+                                                        const double* __restrict__ zc, double* __restrict__ z) {
+  const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
+  const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
+  if ((tid & ~31L) / TPR >= n) return;
+  const double s = row_dot<TPR>(rp, ci, v, zc, row, lane, n);
+  if (lane == 0 && row < n) z[row] += s;
+}
+
+__global__ void k_dense_solve(int n, const double* __restrict__ ainv, const double* __restrict__ b,
+                              double* __restrict__ z) {
+  extern __shared__ double sb[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sb[i] = b[i];
+  __syncthreads();
+  // one warp per row
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int row = w; row < n; row += nw) {
+    double s = 0.0;
+    for (int k = l; k < n; k += 32) s += ainv[(size_t)row * n + k] * sb[k];
+    s = warp_sum(s);
+    if (l == 0) z[row] = s;
+  }
+}
+
+__global__ void k_jacobi(int n, const double* __restrict__ invd, const double* __restrict__ r,
+                         double* __restrict__ z, Reducer red, int slot, int do_red) {
+  double acc = 0.0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    const double zi = invd[i] * r[i];
+    z[i] = zi;
+    acc += r[i] * zi;
+  }
+  if (do_red) reduce_finish(acc, red, slot);
+}
+
+__global__ void k_pcg_update(int n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                             const double* __restrict__ q, Reducer red) {
+  const double alpha = red.scal[S_RZ] / red.scal[S_PQ];
+  double acc = 0.0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    acc += ri * ri;
+  }
+  reduce_finish(acc, red, S_RR);
+}
+
+__global__ void k_pcg_direction(int n, double* __restrict__ p, const double* __restrict__ z,
+                                const double* __restrict__ scal) {
+  const double beta = scal[S_RZ] / scal[S_RZ_OLD];
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
+    p[i] = z[i] + beta * p[i];
+}
+
+__global__ void k_dot(int n, const double* __restrict__ a, const double* __restrict__ b, Reducer red, int slot) {
+  double acc = 0.0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) acc += a[i] * b[i];
+  reduce_finish(acc, red, slot);
+}
+
+struct PtrPack {
+  const double* p[kMaxMulti];
+};
+
+__global__ void k_multi_dot(int n, int m, PtrPack V, const double* __restrict__ w, Reducer red, int slot0) {
+  double acc[kMaxMulti];
+#pragma unroll
+  for (int k = 0; k < kMaxMulti; ++k) acc[k] = 0.0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    const double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < kMaxMulti; ++k)
+      if (k < m) acc[k] += V.p[k][i] * wi;
+  }
+  for (int k = 0; k < m; ++k) reduce_finish(acc[k], red, slot0 + k);
+}
+
+__global__ void k_lincomb(int n, int m, PtrPack V, CoefPack c, double* __restrict__ y) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    double s = 0.0;
+    for (int k = 0; k < m; ++k) s += V.p[k][i] * c.c[k];
+    y[i] = s;
+  }
+}
+
+template <int TPR>
+__global__ void __launch_bounds__(kBlock) k_scaled_spmv(int n, const int* __restrict__ rp,
+                                                        const int* __restrict__ ci, const double* __restrict__ v,
+                                                        const double* __restrict__ invd,
+                                                        const double* __restrict__ x, double* __restrict__ y) {
+  const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
+  const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
+  if ((tid & ~31L) / TPR >= n) return;
+  const double s = row_dot<TPR>(rp, ci, v, x, row, lane, n);
+  if (lane == 0 && row < n) y[row] = s * invd[row];
+}
+
+__global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] += a * x[i];
+}
+__global__ void k_axpy_dev(int n, const double* __restrict__ coef, double sign, const double* __restrict__ x,
+                           double* __restrict__ y) {
+  const double a = sign * coef[0];
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] += a * x[i];
+}
+__global__ void k_scale(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = a * x[i];
+}
+__global__ void k_fill(long n, double v, double* __restrict__ y) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = v;
+}
+
+__global__ void k_rkc_stage(int n, double a0, double mu, double nu, double mt, double gt,
+                            const double* __restrict__ y0, const double* __restrict__ y1,
+                            const double* __restrict__ y2, const double* __restrict__ f,
+                            const double* __restrict__ f0, double* __restrict__ y) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
+    y[i] = a0 * y0[i] + mu * y1[i] + nu * y2[i] + mt * f[i] + gt * f0[i];
+}
+__global__ void k_axpby_into(int n, const double* __restrict__ y0, double c, const double* __restrict__ f,
+                             double* __restrict__ y) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = y0[i] + c * f[i];
+}
+
+__global__ void k_rkc_error(int n, const double* __restrict__ x, const double* __restrict__ xn,
+                            const double* __restrict__ f0, const double* __restrict__ fn, double dt, double atol,
+                            double rtol, Reducer red, int slot) {
+  const double c = 0.4 * dt;
+  double acc = 0.0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    const double xo = x[i], xv = xn[i];
+    const double est = 0.8 * (xo - xv) + c * (f0[i] + fn[i]);
+    const double w = atol + rtol * fmax(fabs(xo), fabs(xv));
+    const double e = est / w;
+    acc += e * e;
+  }
+  reduce_finish(acc, red, slot);
+}
+
+__global__ void k_gather(int n, const int* __restrict__ idx, const double* __restrict__ x, double* __restrict__ y) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = x[idx[i]];
+}
+__global__ void k_scatter(int n, const int* __restrict__ idx, const double* __restrict__ x, double* __restrict__ y) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[idx[i]] = x[i];
+}
+__global__ void k_lift_fixed(int n, const int* __restrict__ set_of, SetVals vals, double* __restrict__ out) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
+    out[i] = vals.v[set_of[i]];
+}
+__global__ void k_boundary_load(int n, const int* __restrict__ rows, const double* __restrict__ coef, int ns,
+                                SetVals rates, double* __restrict__ r) {
+  for (long k = (long)blockIdx.x * kBlock + threadIdx.x; k < n; k += (long)gridDim.x * kBlock) {
+    double s = 0.0;
+    for (int j = 0; j < ns; ++j) s += coef[k * ns + j] * rates.v[j];
+    r[rows[k]] += -s;
+  }
+}
+
+inline int grid_for(long n) {
+  long g = (n + kBlock - 1) / kBlock;
+  const long cap = 148L * 32;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+inline int grid_rows(long n_rows, int tpr) {
+  long g = (n_rows * tpr + kBlock - 1) / kBlock;
+  return (int)(g < 1 ? 1 : g);
+}
+
+#define DISPATCH_TPR(tpr, KERNEL, ...)      \
+  switch (tpr) {                            \
+    case 1: KERNEL<1> __VA_ARGS__; break;   \
+    case 2: KERNEL<2> __VA_ARGS__; break;   \
+    case 4: KERNEL<4> __VA_ARGS__; break;   \
+    case 8: KERNEL<8> __VA_ARGS__; break;   \
+    case 16: KERNEL<16> __VA_ARGS__; break; \
+    default: KERNEL<32> __VA_ARGS__; break; \
+  }
+
+}  // namespace
+
+void launch_spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  if (a.n_rows == 0) return;
+  const int g = grid_rows(a.n_rows, a.tpr);
+  DISPATCH_TPR(a.tpr, k_spmv, <<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, x, y));
+}
+
+void launch_residual(const DevCsr& a, const double* b, const double* x, double* y, Reducer* red, int slot,
+                     cudaStream_t s) {
+  ++g_launch_count;
+  if (a.n_rows == 0) return;
+  const int g = red_grid((long)a.n_rows * a.tpr);
+  Reducer r = red ? *red : Reducer{};
+  const int dr = red ? 1 : 0;
+#define K1(T) k_spmv_red<T, 1><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, x, b, y, r, slot, dr)
+  switch (a.tpr) {
+    case 1: K1(1); break;
+    case 2: K1(2); break;
+    case 4: K1(4); break;
+    case 8: K1(8); break;
+    case 16: K1(16); break;
+    default: K1(32); break;
+  }
+#undef K1
+}
+
+void launch_spmv_dot(const DevCsr& a, const double* p, double* q, Reducer red, int slot, cudaStream_t s) {
+  ++g_launch_count;
+  const int g = red_grid((long)a.n_rows * a.tpr);
+#define K0(T) k_spmv_red<T, 0><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, p, nullptr, q, red, slot, 1)
+  switch (a.tpr) {
+    case 1: K0(1); break;
+    case 2: K0(2); break;
+    case 4: K0(4); break;
+    case 8: K0(8); break;
+    case 16: K0(16); break;
+    default: K0(32); break;
+  }
+#undef K0
+}
+
+void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s) {
+  ++g_launch_count;
+  k_pcg_update<<<red_grid(n), kBlock, 0, s>>>(n, x, r, p, q, red);
+}
+void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s) {
+  ++g_launch_count;
+  k_pcg_direction<<<grid_for(n), kBlock, 0, s>>>(n, p, z, scal);
+}
+
+void launch_cheb_pre(const DevCsr& a, const double* invd, const double* b, double* z, ChebCoef c, cudaStream_t s) {
+  ++g_launch_count;
+  if (a.n_rows == 0) return;
+  const int g = grid_rows(a.n_rows, a.tpr);
+  DISPATCH_TPR(a.tpr, k_cheb_pre, <<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, invd, b, z, c));
+}
+
+void launch_cheb_post2(const DevCsr& a, const double* invd, const double* r0, double* z, ChebCoef c,
+                       const double* b_dot, Reducer* red, int slot, cudaStream_t s) {
+  ++g_launch_count;
+  if (a.n_rows == 0) return;
+  const int g = red_grid((long)a.n_rows * a.tpr);
+  Reducer r = red ? *red : Reducer{};
+  const int dr = red ? 1 : 0;
+  DISPATCH_TPR(a.tpr, k_cheb_post2,
+               <<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, invd, r0, z, c, b_dot, r, slot, dr));
+}
+
+void launch_prolong_add(const DevCsr& p, const double* zc, double* z, cudaStream_t s) {
+  ++g_launch_count;
+  if (p.n_rows == 0) return;
+  const int g = grid_rows(p.n_rows, p.tpr);
+  DISPATCH_TPR(p.tpr, k_prolong_add, <<<g, kBlock, 0, s>>>(p.n_rows, p.row_ptr, p.col_idx, p.values, zc, z));
+}
+
+void launch_dense_solve(int n, const double* ainv, const double* b, double* z, cudaStream_t s) {
+  ++g_launch_count;
+  k_dense_solve<<<1, 1024, n * sizeof(double), s>>>(n, ainv, b, z);
+}
+
+void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s) {
+  ++g_launch_count;
+  Reducer rr = red ? *red : Reducer{};
+  k_jacobi<<<red_grid(n), kBlock, 0, s>>>(n, invd, r, z, rr, slot, red ? 1 : 0);
+}
+
+void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, cudaStream_t s) {
+  ++g_launch_count;
+  k_dot<<<red_grid(n), kBlock, 0, s>>>(n, a, b, red, slot);
+}
+
+void launch_multi_dot(int n, int m, const double* const* V, const double* w, Reducer red, int slot0, cudaStream_t s) {
+  ++g_launch_count;
+  PtrPack pk{};
+  for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
+  k_multi_dot<<<red_grid(n), kBlock, 0, s>>>(n, m, pk, w, red, slot0);
+}
+void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  PtrPack pk{};
+  for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
+  k_lincomb<<<grid_for(n), kBlock, 0, s>>>(n, m, pk, c, y);
+}
+void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, double* w, cudaStream_t s) {
+  ++g_launch_count;
+  if (a.n_rows == 0) return;
+  const int g = grid_rows(a.n_rows, a.tpr);
+  DISPATCH_TPR(a.tpr, k_scaled_spmv, <<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, invd, v, w));
+}
+void launch_axpy(int n, double a, const double* x, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  k_axpy<<<grid_for(n), kBlock, 0, s>>>(n, a, x, y);
+}
+void launch_axpy_dev(int n, const double* coef, double sign, const double* x, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  k_axpy_dev<<<grid_for(n), kBlock, 0, s>>>(n, coef, sign, x, y);
+}
+void launch_scale(int n, double a, const double* x, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  k_scale<<<grid_for(n), kBlock, 0, s>>>(n, a, x, y);
+}
+void launch_fill(long n, double v, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  if (n > 0) k_fill<<<grid_for(n), kBlock, 0, s>>>(n, v, y);
+}
+void launch_rkc_stage(int n, double a0, double mu, double nu, double mt, double gt, const double* y0,
+                      const double* y1, const double* y2, const double* f, const double* f0, double* y,
+                      cudaStream_t s) {
+  ++g_launch_count;
+  k_rkc_stage<<<grid_for(n), kBlock, 0, s>>>(n, a0, mu, nu, mt, gt, y0, y1, y2, f, f0, y);
+}
+void launch_axpby_into(int n, const double* y0, double c, const double* f, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  k_axpby_into<<<grid_for(n), kBlock, 0, s>>>(n, y0, c, f, y);
+}
+void launch_rkc_error(int n, const double* x, const double* xn, const double* f0, const double* fn, double dt,
+                      double atol, double rtol, Reducer red, int slot, cudaStream_t s) {
+  ++g_launch_count;
+  k_rkc_error<<<red_grid(n), kBlock, 0, s>>>(n, x, xn, f0, fn, dt, atol, rtol, red, slot);
+}
+void launch_gather(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  if (n > 0) k_gather<<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
+}
+void launch_scatter(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  if (n > 0) k_scatter<<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
+}
+void launch_lift_fixed(int n_fixed, const int* set_of_fixed, SetVals set_vals, double* fixed_part, cudaStream_t s) {
+  ++g_launch_count;
+  if (n_fixed > 0) k_lift_fixed<<<grid_for(n_fixed), kBlock, 0, s>>>(n_fixed, set_of_fixed, set_vals, fixed_part);
+}
+void launch_boundary_load(int n_rows, const int* rows, const double* coef, int n_sets, SetVals rates, double* r,
+                          cudaStream_t s) {
+  ++g_launch_count;
+  if (n_rows > 0) k_boundary_load<<<grid_for(n_rows), kBlock, 0, s>>>(n_rows, rows, coef, n_sets, rates, r);
+}
+
+}  // namespace eqsb

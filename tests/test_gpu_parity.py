@@ -1,0 +1,219 @@
+"""GPU parity: the B200 path (through the C-ABI) against the CPU oracle.
+
+Tolerances follow the reference's own tests: fused K(x)v vs assembled 1e-12
+(proj/tests/test_matfree.cpp:40-58, acceptance C1), potentials after N RKC
+steps 1e-9 relative with the PCG tolerance identical (BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+
+from helpers import cube, matfree_setup, slab_reference
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+eb = pytest.importorskip("paper_1612_09447_b200")
+
+
+def rel_inf(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("nonlinear", [False, True])
+def test_fused_apply_matches_oracle_and_assembled(order, nonlinear):
+    cfg = matfree_setup(order, nonlinear)
+    g, o = eb.FemSystem(cfg), po.Problem(cfg)
+    x = 2.0 * po.random_vec(g.n_dofs, 101 + order)
+    v = po.random_vec(g.n_dofs, 202 + order)
+    y = g.kx_apply(x, v)
+    assert rel_inf(y, o.assembled_k_apply(x, v)) <= 1e-12
+    assert rel_inf(y, o.kx_apply(x, v)) <= 1e-12
+
+
+def test_ones_vector_vanishes():  # test_matfree.cpp:60-71
+    cfg = matfree_setup(2, True)
+    g, o = eb.FemSystem(cfg), po.Problem(cfg)
+    x = po.random_vec(g.n_dofs, 7)
+    y = g.kx_apply(x, np.ones(g.n_dofs))
+    scale = np.abs(o.kx_apply(x, po.random_vec(g.n_dofs, 9))).max()
+    assert np.abs(y).max() <= 1e-12 * max(scale, 1.0) * 100
+
+
+def test_linearity_in_v():  # test_matfree.cpp:73-87
+    cfg = matfree_setup(1, True)
+    g = eb.FemSystem(cfg)
+    for seed in range(4):
+        x = po.random_vec(g.n_dofs, 1 + 10 * seed)
+        v1 = po.random_vec(g.n_dofs, 2 + 10 * seed)
+        v2 = po.random_vec(g.n_dofs, 3 + 10 * seed)
+        a = -2.75 + seed
+        y12 = g.kx_apply(x, a * v1 + v2)
+        ref = a * g.kx_apply(x, v1) + g.kx_apply(x, v2)
+        assert np.linalg.norm(y12 - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_residual_matches_oracle():  # test_matfree.cpp:89-104
+    cfg = matfree_setup(2, True)
+    g, o = eb.FemSystem(cfg), po.Problem(cfg)
+    x = po.random_vec(g.n_dofs, 31)
+    b = po.random_vec(g.n_free, 32)
+    r = g.kx_residual(x, b)
+    ref = o.kx_residual(x, b)
+    assert np.abs(r - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+def test_coloured_and_gather_modes_agree():
+    cfg = cube(6, jitter=0.1)
+    g = eb.FemSystem(cfg)
+    x = 1e5 * po.random_vec(g.n_dofs, 3)
+    v = po.random_vec(g.n_dofs, 4)
+    y_gather = g.kx_apply(x, v)
+    g.set_option(0, 1)
+    y_col = g.kx_apply(x, v)
+    assert rel_inf(y_col, y_gather) <= 1e-13
+    assert np.array_equal(y_col, g.kx_apply(x, v))  # coloured scatter has a fixed order
+
+
+def test_mass_solve_matches_oracle():
+    cfg = cube(12, jitter=0.1)
+    g, o = eb.FemSystem(cfg), po.Problem(cfg)
+    b = o.mass_apply(po.random_vec(g.n_free, 5))
+    xg, res = g.mass_solve(b, tol=1e-12)
+    xo, it_o, _, conv = o.mass_solve(b, tol=1e-12)
+    assert res.converged and conv
+    assert res.rel_residual <= 1e-12
+    assert np.linalg.norm(xg - xo) <= 1e-10 * np.linalg.norm(xo)
+    assert res.iterations <= 2 * it_o + 2  # GPU smoother differs
+
+
+def test_pcg_semantics():  # test_solvers.cpp:52-116
+    cfg = cube(4)
+    g, o = eb.FemSystem(cfg), po.Problem(cfg)
+    x_star = po.random_vec(g.n_free, 9)
+    b = o.mass_apply(x_star)
+    x, r = g.mass_solve(b, x0=x_star, tol=1e-12)
+    assert r.converged and r.iterations == 0 and r.initial_rel_residual <= 1e-12
+    x, r = g.mass_solve(np.zeros(g.n_free), tol=1e-12)
+    assert r.converged and r.iterations == 0 and np.linalg.norm(x) == 0.0
+    x, r = g.mass_solve(po.random_vec(g.n_free, 3), tol=1e-30, max_iter=2)
+    assert not r.converged and r.iterations == 2
+
+
+def test_eval_rhs_matches_oracle():
+    cfg = cube(10, jitter=0.1, estimator="zero")
+    g, o = eb.FemSystem(cfg), po.Problem(cfg)
+    x = 2e4 * po.random_vec(g.n_free, 31)
+    for t in (0.0, 1.3e-3):
+        assert np.abs(g.eval_residual(t, x) - o.eval_residual(t, x)).max() <= 1e-12 * np.abs(
+            o.eval_residual(t, x)).max()
+        fg, fo = g.eval_rhs(t, x), o.eval_rhs(t, x)
+        assert np.linalg.norm(fg - fo) <= 1e-9 * np.linalg.norm(fo)
+
+
+@pytest.mark.parametrize("estimator", ["zero", "previous", "spe"])
+def test_rkc_fixed_steps_config1(estimator):
+    """SURVEY.md §8d config 1 path (B): 36^3 cube, s = 4, 10 steps from 2e4*random."""
+    n = 36 if estimator == "spe" else 16
+    cfg = cube(n, estimator=estimator)
+    g, o = eb.FemSystem(cfg), po.Problem(cfg)
+    x0 = 2e4 * po.random_vec(g.n_free, 31)
+    g.set_state(0.0, x0, 0.0)
+    rho = g.spectral_radius()
+    rho_o = o.spectral_radius(0.0, x0)
+    assert abs(rho - rho_o) <= 0.05 * rho_o  # loose (1e-4) solves inside, preconditioner-dependent
+    # dt = 0.2 beta(4)/rho: the trajectory's own sensitivity to a 1e-13 relative
+    # perturbation of x0 stays ~1e-14 here (measured with the oracle), so 1e-9 is a
+    # real gate on the solver, not on the problem's conditioning.
+    dt = 0.2 * 0.653 * 15 / rho_o
+    g.set_state(0.0, x0, dt)
+    g.rkc_advance_fixed(dt, 4, 10)
+    xg, info = g.get_state()
+    xo = o.rkc_advance_fixed(0.0, x0, dt, 4, 10)
+    assert info["accepted"] == 10 and abs(info["t"] - 10 * dt) <= 1e-15
+    assert np.linalg.norm(xg - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
+def test_rkc_fixed_steps_at_stability_limit_within_conditioning():
+    """dt = 0.9 beta(4)/rho (the benchmark step): the nonlinear trajectory amplifies
+    a 1e-13 relative perturbation of x0 to ~1e-6 after 10 steps (oracle, measured),
+    so parity is stated relative to the oracle's own perturbation response."""
+    cfg = cube(16, estimator="zero")
+    g, o = eb.FemSystem(cfg), po.Problem(cfg)
+    x0 = 2e4 * po.random_vec(g.n_free, 31)
+    rho_o = o.spectral_radius(0.0, x0)
+    dt = 0.9 * 0.653 * 15 / rho_o
+    g.set_state(0.0, x0, dt)
+    g.rkc_advance_fixed(dt, 4, 10)
+    xg, _ = g.get_state()
+    xo = o.rkc_advance_fixed(0.0, x0, dt, 4, 10)
+    xp = o.rkc_advance_fixed(0.0, x0 * (1 + 1e-12), dt, 4, 10)
+    sens = np.linalg.norm(xp - xo)
+    diff = np.linalg.norm(xg - xo)
+    print(f"gpu-oracle {diff / np.linalg.norm(xo):.3e}  oracle 1e-12-perturbation {sens / np.linalg.norm(xo):.3e}")
+    assert diff <= 10.0 * sens
+
+
+def test_rkc_step_adaptive_matches_oracle_scenario():
+    """Full drop-in run of the reference's committed nonlinear slab scenario."""
+    cfg = slab_reference("slab_nonlinear_rkc_spe")
+    cfg["integrator"]["t_end"] = 0.004
+    rg = eb.run_scenario(cfg)
+    ro = po.run_scenario(cfg, x_cap=10 ** 6)
+    assert rg["exit_code"] == 0, rg.get("error")
+    assert abs(rg["final_t"] - 0.004) <= 1e-15
+    assert rg["stats"]["precond_setups"] == 1  # acceptance C5
+    # The runs agree step by step until the first rho refresh (after 25 accepted
+    # steps); rho comes from 15 power iterations with 1e-4 solves, so it differs
+    # by a few percent between preconditioners, and the step-size controller then
+    # follows a different (equally valid) path. Trajectories agree at the
+    # integration tolerance; exact adaptive parity is pinned by
+    # test_rkc_step_adaptive_pinned_rho.
+    assert np.linalg.norm(rg["x"] - ro["x"]) <= 2e-2 * np.linalg.norm(ro["x"])
+    assert abs(rg["accepted"] - ro["accepted"]) <= 0.3 * ro["accepted"]
+
+
+def test_rkc_step_adaptive_pinned_rho():
+    """rkc_step (integrators.cpp:177-225) with the rho cache pinned to the same
+    value on both sides: stage choice, accept/reject decisions and step sizes
+    follow the reference controller step for step."""
+    cfg = slab_reference("slab_nonlinear_rkc_spe")
+    g, o = eb.FemSystem(cfg), po.Problem(cfg)
+    n = g.n_free
+    t, dt = 0.0, 1e-5
+    x = np.zeros(n)
+    atol = 1e-6 * 4e4
+    rho = o.spectral_radius(0.0, x)
+    g.set_state(t, x, dt)
+    xo = x.copy()
+    for step in range(25):
+        g.set_rho(rho, True, 0)
+        ag = g.rkc_step(rtol=1e-2, atol=atol, rho_refresh_every=1 << 30)
+        xo, ao = o.rkc_step_pinned(t, xo, dt, rho, rtol=1e-2, atol=atol)
+        assert ag.accepted == ao["accepted"] and ag.stages == ao["stages"], step
+        assert abs(ag.dt - ao["dt"]) <= 1e-9 * ao["dt"], step
+        assert abs(ag.error - ao["error"]) <= 1e-5 * max(ao["error"], 1e-3), step
+        t, dt = ao["t"], ao["dt_next"]
+        xg, info = g.get_state()
+        g.set_state(t, xg, dt)  # re-sync dt bit-exactly (controller pow() rounding)
+    assert np.linalg.norm(xg - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
+def test_repeat_runs_bit_identical():  # test_scenario.cpp:133-154
+    cfg = cube(8, jitter=0.1)
+    out = []
+    for _ in range(2):
+        g = eb.FemSystem(cfg)
+        x0 = 2e4 * po.random_vec(g.n_free, 31)
+        g.set_state(0.0, x0, 0.0)
+        g.rkc_advance_fixed(1e-4, 4, 3)
+        out.append(g.get_state()[0])
+    assert np.array_equal(out[0], out[1])
+
+
+def test_nan_field_maps_to_invalid_argument():  # materials.cpp:26 quirk (exit code 1)
+    cfg = cube(4)
+    g = eb.FemSystem(cfg)
+    x = np.full(g.n_free, np.nan)
+    with pytest.raises(eb.InvalidArgument):
+        g.eval_residual(0.0, x)

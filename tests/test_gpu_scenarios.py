@@ -1,0 +1,142 @@
+"""Drop-in scenario runs on the GPU backend: ports of the reference's scenario
+and acceptance checks (proj/tests/test_scenario.cpp, acceptance_main.cpp)."""
+import csv
+import math
+import os
+
+import numpy as np
+import pytest
+
+from helpers import slab_reference, tiny_slab
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+eb = pytest.importorskip("paper_1612_09447_b200")
+EPS0 = 8.8541878128e-12
+
+
+def read_probe(path):
+    rows = list(csv.reader(open(path)))
+    return [(float(r[0]), [float(v) for v in r[1:]]) for r in rows[1:]]
+
+
+def rk4(f, y, t0, t1, n):
+    h = (t1 - t0) / n
+    t = t0
+    for _ in range(n):
+        k1 = f(t, y)
+        k2 = f(t + h / 2, y + h / 2 * k1)
+        k3 = f(t + h / 2, y + h / 2 * k2)
+        k4 = f(t + h, y + h * k3)
+        y += h / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
+        t += h
+    return y
+
+
+def test_start_vector_effectiveness_c6():  # acceptance_main.cpp:249-269
+    its = {}
+    for name in ("slab_linear_rkc", "slab_linear_rkc_previous", "slab_linear_rkc_spe"):
+        cfg = slab_reference(name)
+        cfg["output"] = {"metrics_csv": "", "probe_csv": "", "solves_csv": ""}
+        r = eb.run_scenario(cfg)
+        assert r["exit_code"] == 0, r.get("error")
+        assert r["stats"]["precond_setups"] == 1  # C5: one preconditioner per explicit run
+        its[name] = r["stats"]["pcg_iterations"]
+    zero, prev, spe = its["slab_linear_rkc"], its["slab_linear_rkc_previous"], its["slab_linear_rkc_spe"]
+    print(f"C6 cumulative PCG iterations: zero {zero}, previous {prev}, spe {spe} -> {spe / zero:.2f}")
+    assert spe <= zero / 2
+
+
+def test_order2_rc_divider(tmp_path):  # test_scenario.cpp:290-317
+    cfg = slab_reference("slab_order2_rkc")
+    cfg["output"] = {"metrics_csv": "", "probe_csv": "probe.csv", "solves_csv": ""}
+    r = eb.run_scenario(cfg, out_dir=str(tmp_path))
+    assert r["exit_code"] == 0, r.get("error")
+    d = 0.005
+    c1, c2 = 2.0 * EPS0 / d, 5.0 * EPS0 / d
+    g1, g2 = 1e-8 / d, 5e-9 / d
+    amp, om = 1e4, 2 * math.pi * 50.0
+
+    def rhs(t, phi):
+        return (c2 * amp * om * math.cos(om * t) + g2 * amp * math.sin(om * t) - (g1 + g2) * phi) / (c1 + c2)
+
+    phi, t, max_err, max_ref = 0.0, 0.0, 0.0, 0.0
+    for tp, vals in read_probe(tmp_path / "probe.csv"):
+        phi = rk4(rhs, phi, t, tp, max(1, math.ceil((tp - t) / 2e-7)))
+        t = tp
+        max_err = max(max_err, abs(vals[0] - phi))
+        max_ref = max(max_ref, abs(phi))
+    assert max_err <= 0.02 * max_ref
+
+
+def test_dc_steady_state_divider(tmp_path):  # test_scenario.cpp:120-131
+    cfg = tiny_slab()
+    cfg["excitations"]["hv"] = {"kind": "constant", "value": 90.0}
+    cfg["integrator"]["t_end"] = 5e-2
+    cfg["output"]["probe_csv"] = "probe.csv"
+    r = eb.run_scenario(cfg, out_dir=str(tmp_path))
+    assert r["exit_code"] == 0, r.get("error")
+    last = read_probe(tmp_path / "probe.csv")[-1][1][0]
+    assert last == pytest.approx(30.0, rel=1e-3)
+
+
+def test_zero_excitation_stays_zero(tmp_path):  # test_scenario.cpp:100-118
+    cfg = tiny_slab()
+    cfg["excitations"]["hv"]["amplitude"] = 0.0
+    cfg["output"]["probe_csv"] = "probe.csv"
+    r = eb.run_scenario(cfg, out_dir=str(tmp_path))
+    assert r["exit_code"] == 0
+    assert r["stats"]["pcg_iterations"] == 0 and np.linalg.norm(r["x"]) == 0.0
+    assert all(v == 0.0 for _, vals in read_probe(tmp_path / "probe.csv") for v in vals)
+
+
+def test_euler_scenario_stability_bounded(tmp_path):  # test_scenario.cpp:276-288
+    cfg = tiny_slab()
+    cfg["integrator"] = {"kind": "euler", "tolerance": 1e-2, "t_end": 2e-3, "dt0": 1e-3}
+    cfg["output"]["metrics_csv"] = "metrics.csv"
+    r = eb.run_scenario(cfg, out_dir=str(tmp_path))
+    assert r["exit_code"] == 0 and r["accepted"] > 0 and r["stats"]["precond_setups"] == 1
+    for row in csv.DictReader(open(tmp_path / "metrics.csv")):
+        assert row["accepted"] == "1"
+        rho = float(row["rho"])
+        if rho > 0:
+            assert float(row["dt"]) <= 1.8 / rho + 1e-15
+    ro = po.run_scenario(cfg, x_cap=10 ** 5)
+    assert r["accepted"] == ro["accepted"]
+    assert np.linalg.norm(r["x"] - ro["x"]) <= 1e-9 * np.linalg.norm(ro["x"])
+
+
+def test_identical_runs_bit_identical(tmp_path):  # test_scenario.cpp:133-154
+    cfg = tiny_slab()
+    cfg["output"]["metrics_csv"] = "metrics.csv"
+    a = eb.run_scenario(cfg, out_dir=str(tmp_path / "a"))
+    b = eb.run_scenario(cfg, out_dir=str(tmp_path / "b"))
+    assert np.array_equal(a["x"], b["x"])
+    strip = lambda p: [r[:13] for r in csv.reader(open(p))]  # drop the wall-time columns
+    assert strip(tmp_path / "a" / "metrics.csv") == strip(tmp_path / "b" / "metrics.csv")
+
+
+def test_preconditioner_invariance():  # test_scenario.cpp:227-241
+    out = {}
+    for p in ("amg", "jacobi"):
+        cfg = tiny_slab()
+        cfg["solver"]["preconditioner"] = p
+        out[p] = eb.run_scenario(cfg)
+        assert out[p]["exit_code"] == 0
+    a, j = out["amg"]["x"], out["jacobi"]["x"]
+    assert np.linalg.norm(a - j) <= 1e-8 * np.linalg.norm(a)
+
+
+def test_max_iter_one_maps_to_solver_failure():  # test_scenario.cpp:216-225
+    cfg = tiny_slab()
+    cfg["solver"]["max_iter"] = 1
+    r = eb.run_scenario(cfg)
+    assert r["exit_code"] == 2
+
+
+def test_config_error_exit_code():  # scenario.cpp:353-368
+    cfg = tiny_slab()
+    cfg["estimator"]["mode"] = "bogus"
+    with pytest.raises(eb.ConfigError):
+        eb.run_scenario(cfg)
