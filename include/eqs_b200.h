@@ -239,7 +239,8 @@ int eqs_timing_enable(eqs_ctx* ctx, int on);
 int eqs_timing_get(eqs_ctx* ctx, eqs_timing* out);
 int eqs_timing_reset(eqs_ctx* ctx);
 /* Tuning knobs (not in the reference): 0 = stiffness mode (0 gather, 1 coloured),
- * 1 = chebyshev degree, 2 = chebyshev eig ratio, 3 = use CUDA graphs. */
+ * 1 = fine-level Chebyshev degree (1 or 2), 2 = Chebyshev eigenvalue ratio,
+ * 3 = coarse-level Chebyshev degree (1 or 2), 4 = fp32 V-cycle matrices (0/1). */
 int eqs_set_option(eqs_ctx* ctx, int key, double value);
 /* The CUDA stream (cudaStream_t) every device call of this context runs on. */
 int eqs_get_stream(eqs_ctx* ctx, void** stream);

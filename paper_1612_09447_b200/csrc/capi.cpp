@@ -405,6 +405,11 @@ int eqs_set_option(eqs_ctx* ctx, int key, double value) {
       case 0: g.stiffness_mode = (int)value; break;
       case 1: g.cheb_degree = (int)value; break;
       case 2: g.set_cheb(value); break;
+      case 3: g.coarse_degree = (int)value; break;
+      case 4: g.set_vcycle_fp32(value != 0.0); break;
+      case 5: g.set_level_tpr(0, (int)value); break;
+      case 6: g.set_level_tpr(1, (int)value); break;
+      case 7: g.set_level_tpr(2, (int)value); break;
       default: throw std::invalid_argument("eqs_set_option: unknown key");
     }
   });

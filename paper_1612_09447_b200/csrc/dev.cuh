@@ -45,7 +45,8 @@ struct DevCsr {
   int* row_ptr = nullptr;
   int* col_idx = nullptr;
   double* values = nullptr;
-  int tpr = 4;  // threads per row used by the SpMV kernels
+  float* values_f = nullptr;  // when set, kernels read fp32 values (V-cycle copies only)
+  int tpr = 4;                // threads per row used by the SpMV kernels
 };
 
 struct ChebCoef {
@@ -90,6 +91,12 @@ void launch_pcg_direction(int n, double* p, const double* z, const double* scal,
 void launch_cheb_pre(const DevCsr& a, const double* invd, const double* b, double* z, ChebCoef c, cudaStream_t s);
 void launch_cheb_post2(const DevCsr& a, const double* invd, const double* r0, double* z, ChebCoef c,
                        const double* b_dot, Reducer* red, int slot, cudaStream_t s);
+// Chebyshev(1): z = D^-1 b / theta and t = b - A z in one pass
+void launch_cheb1_pre_resid(const DevCsr& a, const double* invd, const double* b, double* z, double* t, ChebCoef c,
+                            cudaStream_t s);
+// Chebyshev(1) post: z_out = z + D^-1 (b - A z) / theta (z_out != z)
+void launch_cheb1_post(const DevCsr& a, const double* invd, const double* b, const double* z, double* z_out,
+                       ChebCoef c, cudaStream_t s);
 // z += P zc
 void launch_prolong_add(const DevCsr& p, const double* zc, double* z, cudaStream_t s);
 // z = Ainv b (dense, n <= 1024)

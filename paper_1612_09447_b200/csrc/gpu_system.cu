@@ -54,11 +54,13 @@ struct PhaseTimer {
   ~PhaseTimer() { slot += std::chrono::duration<double>(clk::now() - t0).count(); }
 };
 
+// threads per row: enough that each thread handles <= 8 entries (one batch of
+// the row kernels' prefetch), capped at a warp
 int choose_tpr(const HostCsr& a) {
   if (a.n_rows == 0) return 1;
   const double avg = (double)a.nnz() / a.n_rows;
   int t = 1;
-  while (t < 32 && t * 4 < avg) t <<= 1;
+  while (t < 32 && t * 8 < avg) t <<= 1;
   return t;
 }
 
@@ -230,27 +232,38 @@ void GpuSystem::build_device() {
   if (prob_.solver.precond == 2) {
     const int L = (int)amg_.levels.size();
     levels_.resize(L);
+    auto f32 = [&](const std::vector<double>& v, DevBuf<float>& out) {
+      std::vector<float> f(v.begin(), v.end());
+      out.alloc(std::max<size_t>(1, f.size()));
+      out.upload(f.data(), f.size(), s);
+      CK(cudaStreamSynchronize(s));
+    };
     for (int l = 0; l < L; ++l) {
       DevLevel& lv = levels_[l];
       const AmgHostLevel& hl = amg_.levels[l];
       if (l == 0) {
-        lv.A = mii_;
+        lv.A = mii_;  // shares indices / fp64 values with the PCG operator
       } else {
         upload_csr(hl.A, lv.A, lv.a_rp, lv.a_ci, lv.a_v, s);
       }
       const int n = hl.A.n_rows;
       if (l + 1 < L) {
+        f32(hl.A.values, lv.a_vf);
         upload_csr(hl.P, lv.P, lv.p_rp, lv.p_ci, lv.p_v, s);
         upload_csr(hl.R, lv.R, lv.r_rp, lv.r_ci, lv.r_v, s);
+        f32(hl.P.values, lv.p_vf);
+        f32(hl.R.values, lv.r_vf);
         const std::vector<double> invd = inv_diagonal(hl.A);
         lv.invd.alloc(n);
         lv.invd.upload(invd.data(), n, s);
         lv.t.alloc(n);
+        lv.z2.alloc(std::max(1, n));
       }
       lv.z.alloc(std::max(1, n));
       if (l > 0) lv.b.alloc(std::max(1, n));
       CK(cudaStreamSynchronize(s));
     }
+    set_vcycle_fp32(vcycle_fp32_);
     coarse_n_ = amg_.coarse_n;
     coarse_inv_.alloc(amg_.coarse_inverse.size());
     coarse_inv_.upload(amg_.coarse_inverse.data(), amg_.coarse_inverse.size(), s);
@@ -306,6 +319,9 @@ void GpuSystem::build_device() {
   CK(cudaStreamSynchronize(s));
 }
 
+// Chebyshev smoother on [lmax/ratio, lmax] of D^-1 A, lmax = 1.1 x the power
+// estimate. Degree 2: x += c0 D^-1 r0 + c1 D^-1 (r0 - A D^-1 r0 / theta);
+// degree 1: x += D^-1 r0 / theta.
 void GpuSystem::set_cheb(double ratio) {
   cheb_ratio = ratio;
   for (auto& lv : levels_) {
@@ -315,6 +331,23 @@ void GpuSystem::set_cheb(double ratio) {
     lv.cheb.c0 = (1.0 + rho1 * rho0) / theta;
     lv.cheb.c1 = 2.0 * rho1 / delta;
     lv.cheb.inv_theta = 1.0 / theta;
+    lv.cheb1 = ChebCoef{0.0, 0.0, 1.0 / theta};
+  }
+}
+
+void GpuSystem::set_level_tpr(int level, int tpr) {
+  if (tpr < 1 || tpr > 32 || (tpr & (tpr - 1))) throw std::invalid_argument("tpr must be a power of two <= 32");
+  if (level == 0) mii_.tpr = tpr;
+  if (level < (int)levels_.size()) levels_[level].A.tpr = tpr;
+}
+
+void GpuSystem::set_vcycle_fp32(bool on) {
+  vcycle_fp32_ = on;
+  for (size_t l = 0; l + 1 < levels_.size(); ++l) {
+    DevLevel& lv = levels_[l];
+    lv.A.values_f = on ? lv.a_vf.p : nullptr;
+    lv.P.values_f = on ? lv.p_vf.p : nullptr;
+    lv.R.values_f = on ? lv.r_vf.p : nullptr;
   }
 }
 
@@ -507,35 +540,53 @@ void GpuSystem::residual_dev(double t, double* x_full, double* r) {
 
 void GpuSystem::mass_apply_dev(const double* v, double* y) { launch_spmv(mii_, v, y, stream_); }
 
-void GpuSystem::vcycle(int l, const double* b, double* z, bool dot_into_rz) {
+// Symmetric V-cycle (amg.cpp:145-172 structure) with Chebyshev smoothing:
+// degree `cheb_degree` on the fine level, `coarse_degree` below; the same
+// polynomial pre and post keeps the preconditioner symmetric for PCG.
+double* GpuSystem::vcycle(int l, const double* b, bool dot_into_rz) {
   const int L = (int)levels_.size();
-  if (l == L - 1) {
-    launch_dense_solve(coarse_n_, coarse_inv_.p, b, z, stream_);
-    if (dot_into_rz) launch_dot(coarse_n_, b, z, red_, S_RZ, stream_);
-    return;
-  }
   DevLevel& lv = levels_[l];
+  if (l == L - 1) {
+    launch_dense_solve(coarse_n_, coarse_inv_.p, b, lv.z.p, stream_);
+    if (dot_into_rz) launch_dot(coarse_n_, b, lv.z.p, red_, S_RZ, stream_);
+    return lv.z.p;
+  }
   DevLevel& nx = levels_[l + 1];
-  launch_cheb_pre(lv.A, lv.invd.p, b, z, lv.cheb, stream_);
-  launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
+  const int deg = l == 0 ? cheb_degree : coarse_degree;
+  double* z = lv.z.p;
+  if (deg >= 2) {
+    launch_cheb_pre(lv.A, lv.invd.p, b, z, lv.cheb, stream_);
+    launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
+  } else {
+    launch_cheb1_pre_resid(lv.A, lv.invd.p, b, z, lv.t.p, lv.cheb1, stream_);
+  }
   launch_spmv(lv.R, lv.t.p, nx.b.p, stream_);
-  vcycle(l + 1, nx.b.p, nx.z.p, false);
-  launch_prolong_add(lv.P, nx.z.p, z, stream_);
-  launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
-  Reducer r = red_;
-  launch_cheb_post2(lv.A, lv.invd.p, lv.t.p, z, lv.cheb, dot_into_rz ? b : nullptr, dot_into_rz ? &r : nullptr, S_RZ,
-                    stream_);
+  const double* zc = vcycle(l + 1, nx.b.p, false);
+  launch_prolong_add(lv.P, zc, z, stream_);
+  if (deg >= 2) {
+    launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
+    Reducer r = red_;
+    launch_cheb_post2(lv.A, lv.invd.p, lv.t.p, z, lv.cheb, dot_into_rz ? b : nullptr, dot_into_rz ? &r : nullptr,
+                      S_RZ, stream_);
+    return z;
+  }
+  launch_cheb1_post(lv.A, lv.invd.p, b, z, lv.z2.p, lv.cheb1, stream_);
+  if (dot_into_rz) launch_dot(lv.A.n_rows, b, lv.z2.p, red_, S_RZ, stream_);
+  return lv.z2.p;
 }
 
-void GpuSystem::precondition(const double* r, double* z) {
+double* GpuSystem::precondition(const double* r) {
   tic(TC_VCYCLE);
+  double* z;
   if (prob_.solver.precond == 2) {
-    vcycle(0, r, z, true);
+    z = vcycle(0, r, true);
   } else {
     Reducer rr = red_;
+    z = w_z_.p;
     launch_jacobi(n_free_, mii_invd_.p, r, z, &rr, S_RZ, stream_);
   }
   toc(TC_VCYCLE, 0.0);
+  return z;
 }
 
 // pcg_solve (proj/src/pcg.cpp:9-72) with device vectors; host reads three
@@ -556,7 +607,7 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
     use_x0 = read_scalar(S_X0X0) != 0.0;
   }
   double* r = w_r_.p;
-  double* z = w_z_.p;
+  double* z = nullptr;
   double* p = w_p_.p;
   double* q = w_q_.p;
   double rr;
@@ -581,11 +632,11 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
     res.converged = true;
     return res;
   }
-  precondition(r, z);
+  z = precondition(r);
   double sc[3];
   read_scalars(S_RZ, 1, sc);
   if (!std::isfinite(sc[0])) throw NumericalError("pcg: non-finite preconditioned residual");
-  std::swap(p, z);  // p = z
+  CK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));  // p = z
   for (int k = 1; k <= max_iter; ++k) {
     tic(TC_PCG);
     launch_spmv_dot(mii_, p, q, red_, S_PQ, stream_);
@@ -606,7 +657,7 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
     }
     CK(cudaMemcpyAsync(red_scal_.p + S_RZ_OLD, red_scal_.p + S_RZ, sizeof(double), cudaMemcpyDeviceToDevice,
                        stream_));
-    precondition(r, z);
+    z = precondition(r);
     tic(TC_PCG);
     launch_pcg_direction(n, p, z, red_scal_.p, stream_);
     toc(TC_PCG, 24.0 * n);

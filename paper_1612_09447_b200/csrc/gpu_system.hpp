@@ -64,8 +64,9 @@ struct DevLevel {
   DevCsr A, P, R;
   DevBuf<int> a_rp, a_ci, p_rp, p_ci, r_rp, r_ci;
   DevBuf<double> a_v, p_v, r_v;
-  DevBuf<double> invd, b, z, t;
-  ChebCoef cheb{};
+  DevBuf<float> a_vf, p_vf, r_vf;  // fp32 copies for the V-cycle
+  DevBuf<double> invd, b, z, z2, t;
+  ChebCoef cheb{}, cheb1{};          // degree-2 and degree-1 Chebyshev coefficients
   double lambda_smoother = 0;
 };
 
@@ -135,9 +136,13 @@ class GpuSystem {
 
   // ---- options / timing
   int stiffness_mode = 0;  // 0 gather, 1 coloured
-  int cheb_degree = 2;
+  int cheb_degree = 2;     // fine level (1 or 2)
+  int coarse_degree = 1;   // levels >= 1 (1 or 2)
   double cheb_ratio = 6.0;
   void set_cheb(double ratio);
+  void set_vcycle_fp32(bool on);
+  void set_level_tpr(int level, int tpr);  // threads per row of A_l (level 0 also sets M_II)
+  bool vcycle_fp32() const { return vcycle_fp32_; }
   bool timing_on = false;
   void tic(int cls);
   void toc(int cls, double bytes);
@@ -150,8 +155,9 @@ class GpuSystem {
 
  private:
   void build_device();
-  void vcycle(int l, const double* b, double* z, bool dot_into_rz);
-  void precondition(const double* r, double* z);  // z = M^-1 r, S_RZ <- r.z
+  double* vcycle(int l, const double* b, bool dot_into_rz);  // returns the buffer holding z_l
+  double* precondition(const double* r);  // z = M^-1 r (returned buffer), S_RZ <- r.z
+  bool vcycle_fp32_ = true;
   void kx_tets(const double* x, const double* v);
   double read_scalar(int slot);
   void read_scalars(int first, int count, double* out);

@@ -3,7 +3,8 @@
 // matrix from the mean row length) so that a warp streams contiguous
 // col_idx/values; gathered vectors hit L2. Reductions are fused into the
 // producing kernel and finished deterministically (fixed grid, last-block
-// ordered sum).
+// ordered sum). V-cycle matrices may be stored with fp32 values (the
+// preconditioner only; PCG itself is fp64 throughout).
 #include <cuda_runtime.h>
 
 #include "dev.cuh"
@@ -68,126 +69,115 @@ int red_grid(long work_items) {
   return (int)g;
 }
 
-// Row-group SpMV core: returns sum_k A_ik x_k for `row` in lane 0 of the group.
-// All lanes of the warp must call it (shuffles); rows >= n contribute nothing.
-template <int TPR>
+// matrix entries are streamed once per pass: evict-first loads keep L2 for
+// the gathered vectors (ld.global.cs)
+__device__ __forceinline__ double ldv(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ double ldv(const float* p) { return (double)__ldcs(p); }
+
+constexpr int kUnroll = 8;  // independent entries in flight per thread
+
+// Row-group SpMV core: returns sum_k A_ik x_k (x_k w_k when SCALED) for `row`
+// in lane 0 of the group. Entries are fetched kUnroll at a time (indices and
+// values first, then the gathers) so each thread keeps several independent
+// loads in flight. All lanes of the warp must call it (shuffles); rows >= n
+// contribute nothing.
+template <int TPR, class VT, bool SCALED>
 __device__ __forceinline__ double row_dot(const int* __restrict__ rp, const int* __restrict__ ci,
-                                          const double* __restrict__ v, const double* __restrict__ x, int row,
-                                          int lane, int n) {
+                                          const VT* __restrict__ v, const double* __restrict__ x,
+                                          const double* __restrict__ w, int row, int lane, int n) {
   const bool ok = row < n;
-  const int beg = ok ? rp[row] : 0, end = ok ? rp[row + 1] : 0;
+  const int beg = ok ? __ldg(rp + row) : 0, end = ok ? __ldg(rp + row + 1) : 0;
   double s = 0.0;
-#pragma unroll 4
-  for (int k = beg + lane; k < end; k += TPR) s += v[k] * __ldg(x + ci[k]);
+  for (int k0 = beg + lane; k0 < end; k0 += TPR * kUnroll) {
+    int c[kUnroll];
+    double a[kUnroll];
 #pragma unroll
-  for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, TPR);
-  return s;
-}
-// same with the gathered vector scaled on the fly: sum_k A_ik x_k w_k
-template <int TPR>
-__device__ __forceinline__ double row_dot_scaled(const int* __restrict__ rp, const int* __restrict__ ci,
-                                                 const double* __restrict__ v, const double* __restrict__ x,
-                                                 const double* __restrict__ w, int row, int lane, int n) {
-  const bool ok = row < n;
-  const int beg = ok ? rp[row] : 0, end = ok ? rp[row + 1] : 0;
-  double s = 0.0;
-#pragma unroll 4
-  for (int k = beg + lane; k < end; k += TPR) {
-    const int c = ci[k];
-    s += v[k] * (__ldg(x + c) * __ldg(w + c));
+    for (int u = 0; u < kUnroll; ++u) {
+      const int k = k0 + u * TPR;
+      const bool in = k < end;
+      c[u] = in ? __ldcs(ci + k) : 0;
+      a[u] = in ? ldv(v + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const double xv = SCALED ? __ldg(x + c[u]) * __ldg(w + c[u]) : __ldg(x + c[u]);
+      s += a[u] * xv;
+    }
   }
 #pragma unroll
   for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, TPR);
   return s;
 }
 
-template <int TPR>
-__global__ void __launch_bounds__(kBlock) k_spmv(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                 const double* __restrict__ v, const double* __restrict__ x,
-                                                 double* __restrict__ y) {
+// Generic row kernel (one pass over a matrix), warp-uniform early exit.
+// OP 0: y = A x                       (restriction, plain SpMV)
+// OP 1: y = b - A x                   (residual)
+// OP 2: z += A zc                     (prolongation + correction; v = P)
+// OP 3: z = c0 D^-1 b + c1 D^-1 (b - A D^-1 b / theta)          (Chebyshev(2) pre-smoothing from 0)
+// OP 4: z = D^-1 b / theta ; t = b - A z                         (Chebyshev(1) pre-smoothing + residual)
+// OP 5: zo = z + D^-1 (b - A z) / theta                          (Chebyshev(1) post-smoothing, out of place)
+// OP 6: w = D^-1 A x                                             (power iteration on D^-1 A)
+template <int TPR, class VT, int OP>
+__global__ void __launch_bounds__(kBlock) k_row(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                const VT* __restrict__ v, const double* __restrict__ x,
+                                                const double* __restrict__ b, const double* __restrict__ invd,
+                                                double* __restrict__ y, double* __restrict__ y2, ChebCoef c) {
   const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
   const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
   if ((tid & ~31L) / TPR >= n) return;  // warp-uniform exit
-  const double s = row_dot<TPR>(rp, ci, v, x, row, lane, n);
-  if (lane == 0 && row < n) y[row] = s;
+  constexpr bool SC = (OP == 3 || OP == 4);
+  const double s = row_dot<TPR, VT, SC>(rp, ci, v, SC ? b : x, invd, row, lane, n);
+  if (lane != 0 || row >= n) return;
+  if (OP == 0) y[row] = s;
+  if (OP == 1) y[row] = b[row] - s;
+  if (OP == 2) y[row] += s;
+  if (OP == 3) {
+    const double bi = b[row], di = invd[row];
+    y[row] = c.c0 * bi * di + c.c1 * di * (bi - s * c.inv_theta);
+  }
+  if (OP == 4) {
+    const double bi = b[row];
+    y[row] = bi * invd[row] * c.inv_theta;
+    y2[row] = bi - s * c.inv_theta;
+  }
+  if (OP == 5) y2[row] = x[row] + invd[row] * (b[row] - s) * c.inv_theta;
+  if (OP == 6) y[row] = s * invd[row];
 }
 
-// grid-stride over row groups with a fused reduction. MODE 0: q = A p, sum p.q
+// grid-stride row kernels with a fused reduction.
+// MODE 0: q = A p,  sum p.q
 // MODE 1: y = b - A x, sum y.y
-template <int TPR, int MODE>
-__global__ void __launch_bounds__(kBlock) k_spmv_red(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                     const double* __restrict__ v, const double* __restrict__ x,
-                                                     const double* __restrict__ b, double* __restrict__ y,
-                                                     Reducer red, int slot, int do_red) {
+// MODE 2: z += c0 D^-1 r0 + c1 D^-1 (r0 - A D^-1 r0 / theta), sum b.z  (Chebyshev(2) post step 2)
+template <int TPR, class VT, int MODE>
+__global__ void __launch_bounds__(kBlock) k_row_red(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                    const VT* __restrict__ v, const double* __restrict__ x,
+                                                    const double* __restrict__ b, const double* __restrict__ invd,
+                                                    double* __restrict__ y, ChebCoef c, Reducer red, int slot,
+                                                    int do_red) {
   const int lane = threadIdx.x % TPR;
   const long groups_per_grid = (long)gridDim.x * (kBlock / TPR);
   // every group iterates the same number of times (shuffles need full warps)
   const long n_pad = ((n + (long)(kBlock / TPR) - 1) / (kBlock / TPR)) * (kBlock / TPR);
   double acc = 0.0;
   for (long row = (long)blockIdx.x * (kBlock / TPR) + threadIdx.x / TPR; row < n_pad; row += groups_per_grid) {
-    const double s = row_dot<TPR>(rp, ci, v, x, (int)row, lane, n);
+    const double s = row_dot<TPR, VT, MODE == 2>(rp, ci, v, x, invd, (int)row, lane, n);
     if (lane == 0 && row < n) {
       if (MODE == 0) {
         y[row] = s;
         acc += x[row] * s;
-      } else {
+      } else if (MODE == 1) {
         const double r = b[row] - s;
         y[row] = r;
         acc += r * r;
+      } else {
+        const double ri = x[row], di = invd[row];
+        const double zn = y[row] + (c.c0 * ri * di + c.c1 * di * (ri - s * c.inv_theta));
+        y[row] = zn;
+        if (do_red) acc += b[row] * zn;
       }
     }
   }
   if (do_red) reduce_finish(acc, red, slot);
-}
-
-template <int TPR>
-__global__ void __launch_bounds__(kBlock) k_cheb_pre(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                     const double* __restrict__ v, const double* __restrict__ invd,
-                                                     const double* __restrict__ b, double* __restrict__ z,
-                                                     ChebCoef c) {
-  const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
-  const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
-  if ((tid & ~31L) / TPR >= n) return;
-  const double s = row_dot_scaled<TPR>(rp, ci, v, b, invd, row, lane, n);
-  if (lane == 0 && row < n) {
-    const double bi = b[row], di = invd[row];
-    z[row] = c.c0 * bi * di + c.c1 * di * (bi - s * c.inv_theta);
-  }
-}
-
-// z += c0 D^-1 r0 + c1 D^-1 (r0 - A D^-1 r0 / theta); optional sum b.z
-template <int TPR>
-__global__ void __launch_bounds__(kBlock) k_cheb_post2(int n, const int* __restrict__ rp,
-                                                       const int* __restrict__ ci, const double* __restrict__ v,
-                                                       const double* __restrict__ invd,
-                                                       const double* __restrict__ r0, double* __restrict__ z,
-                                                       ChebCoef c, const double* __restrict__ bdot, Reducer red,
-                                                       int slot, int do_red) {
-  const int lane = threadIdx.x % TPR;
-  const long groups_per_grid = (long)gridDim.x * (kBlock / TPR);
-  const long n_pad = ((n + (long)(kBlock / TPR) - 1) / (kBlock / TPR)) * (kBlock / TPR);
-  double acc = 0.0;
-  for (long row = (long)blockIdx.x * (kBlock / TPR) + threadIdx.x / TPR; row < n_pad; row += groups_per_grid) {
-    const double s = row_dot_scaled<TPR>(rp, ci, v, r0, invd, (int)row, lane, n);
-    if (lane == 0 && row < n) {
-      const double ri = r0[row], di = invd[row];
-      const double zn = z[row] + (c.c0 * ri * di + c.c1 * di * (ri - s * c.inv_theta));
-      z[row] = zn;
-      if (do_red) acc += bdot[row] * zn;
-    }
-  }
-  if (do_red) reduce_finish(acc, red, slot);
-}
-
-template <int TPR>
-__global__ void __launch_bounds__(kBlock) k_prolong_add(int n, const int* __restrict__ rp,
-                                                        const int* __restrict__ ci, const double* __restrict__ v,
-                                                        const double* __restrict__ zc, double* __restrict__ z) {
-  const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
-  const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
-  if ((tid & ~31L) / TPR >= n) return;
-  const double s = row_dot<TPR>(rp, ci, v, zc, row, lane, n);
-  if (lane == 0 && row < n) z[row] += s;
 }
 
 __global__ void k_dense_solve(int n, const double* __restrict__ ainv, const double* __restrict__ b,
@@ -195,7 +185,6 @@ __global__ void k_dense_solve(int n, const double* __restrict__ ainv, const doub
   extern __shared__ double sb[];
   for (int i = threadIdx.x; i < n; i += blockDim.x) sb[i] = b[i];
   __syncthreads();
-  // one warp per row
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int row = w; row < n; row += nw) {
     double s = 0.0;
@@ -265,18 +254,6 @@ __global__ void k_lincomb(int n, int m, PtrPack V, CoefPack c, double* __restric
     for (int k = 0; k < m; ++k) s += V.p[k][i] * c.c[k];
     y[i] = s;
   }
-}
-
-template <int TPR>
-__global__ void __launch_bounds__(kBlock) k_scaled_spmv(int n, const int* __restrict__ rp,
-                                                        const int* __restrict__ ci, const double* __restrict__ v,
-                                                        const double* __restrict__ invd,
-                                                        const double* __restrict__ x, double* __restrict__ y) {
-  const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
-  const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
-  if ((tid & ~31L) / TPR >= n) return;
-  const double s = row_dot<TPR>(rp, ci, v, x, row, lane, n);
-  if (lane == 0 && row < n) y[row] = s * invd[row];
 }
 
 __global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
@@ -350,57 +327,93 @@ inline int grid_rows(long n_rows, int tpr) {
   return (int)(g < 1 ? 1 : g);
 }
 
-#define DISPATCH_TPR(tpr, KERNEL, ...)      \
-  switch (tpr) {                            \
-    case 1: KERNEL<1> __VA_ARGS__; break;   \
-    case 2: KERNEL<2> __VA_ARGS__; break;   \
-    case 4: KERNEL<4> __VA_ARGS__; break;   \
-    case 8: KERNEL<8> __VA_ARGS__; break;   \
-    case 16: KERNEL<16> __VA_ARGS__; break; \
-    default: KERNEL<32> __VA_ARGS__; break; \
+template <int OP>
+void row_launch(const DevCsr& a, const double* x, const double* b, const double* invd, double* y, double* y2,
+                ChebCoef c, cudaStream_t s) {
+  if (a.n_rows == 0) return;
+  ++g_launch_count;
+  const int g = grid_rows(a.n_rows, a.tpr);
+#define L_(T, VT, V) \
+  k_row<T, VT, OP><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, y2, c)
+#define D_(VT, V)                \
+  switch (a.tpr) {               \
+    case 1: L_(1, VT, V); break;   \
+    case 2: L_(2, VT, V); break;   \
+    case 4: L_(4, VT, V); break;   \
+    case 8: L_(8, VT, V); break;   \
+    case 16: L_(16, VT, V); break; \
+    default: L_(32, VT, V); break; \
   }
+  if (a.values_f) {
+    D_(float, a.values_f)
+  } else {
+    D_(double, a.values)
+  }
+#undef D_
+#undef L_
+}
+
+template <int MODE>
+void row_red_launch(const DevCsr& a, const double* x, const double* b, const double* invd, double* y, ChebCoef c,
+                    Reducer* red, int slot, cudaStream_t s) {
+  if (a.n_rows == 0) return;
+  ++g_launch_count;
+  const int g = red_grid((long)a.n_rows * a.tpr);
+  Reducer r = red ? *red : Reducer{};
+  const int dr = red ? 1 : 0;
+#define L_(T, VT, V) \
+  k_row_red<T, VT, MODE><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, c, r, slot, dr)
+#define D_(VT, V)                \
+  switch (a.tpr) {               \
+    case 1: L_(1, VT, V); break;   \
+    case 2: L_(2, VT, V); break;   \
+    case 4: L_(4, VT, V); break;   \
+    case 8: L_(8, VT, V); break;   \
+    case 16: L_(16, VT, V); break; \
+    default: L_(32, VT, V); break; \
+  }
+  if (a.values_f) {
+    D_(float, a.values_f)
+  } else {
+    D_(double, a.values)
+  }
+#undef D_
+#undef L_
+}
 
 }  // namespace
 
 void launch_spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s) {
-  ++g_launch_count;
-  if (a.n_rows == 0) return;
-  const int g = grid_rows(a.n_rows, a.tpr);
-  DISPATCH_TPR(a.tpr, k_spmv, <<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, x, y));
+  row_launch<0>(a, x, nullptr, nullptr, y, nullptr, ChebCoef{}, s);
 }
-
 void launch_residual(const DevCsr& a, const double* b, const double* x, double* y, Reducer* red, int slot,
                      cudaStream_t s) {
-  ++g_launch_count;
-  if (a.n_rows == 0) return;
-  const int g = red_grid((long)a.n_rows * a.tpr);
-  Reducer r = red ? *red : Reducer{};
-  const int dr = red ? 1 : 0;
-#define K1(T) k_spmv_red<T, 1><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, x, b, y, r, slot, dr)
-  switch (a.tpr) {
-    case 1: K1(1); break;
-    case 2: K1(2); break;
-    case 4: K1(4); break;
-    case 8: K1(8); break;
-    case 16: K1(16); break;
-    default: K1(32); break;
-  }
-#undef K1
+  if (red) row_red_launch<1>(a, x, b, nullptr, y, ChebCoef{}, red, slot, s);
+  else row_launch<1>(a, x, b, nullptr, y, nullptr, ChebCoef{}, s);
 }
-
 void launch_spmv_dot(const DevCsr& a, const double* p, double* q, Reducer red, int slot, cudaStream_t s) {
-  ++g_launch_count;
-  const int g = red_grid((long)a.n_rows * a.tpr);
-#define K0(T) k_spmv_red<T, 0><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, p, nullptr, q, red, slot, 1)
-  switch (a.tpr) {
-    case 1: K0(1); break;
-    case 2: K0(2); break;
-    case 4: K0(4); break;
-    case 8: K0(8); break;
-    case 16: K0(16); break;
-    default: K0(32); break;
-  }
-#undef K0
+  row_red_launch<0>(a, p, nullptr, nullptr, q, ChebCoef{}, &red, slot, s);
+}
+void launch_prolong_add(const DevCsr& p, const double* zc, double* z, cudaStream_t s) {
+  row_launch<2>(p, zc, nullptr, nullptr, z, nullptr, ChebCoef{}, s);
+}
+void launch_cheb_pre(const DevCsr& a, const double* invd, const double* b, double* z, ChebCoef c, cudaStream_t s) {
+  row_launch<3>(a, nullptr, b, invd, z, nullptr, c, s);
+}
+void launch_cheb_post2(const DevCsr& a, const double* invd, const double* r0, double* z, ChebCoef c,
+                       const double* b_dot, Reducer* red, int slot, cudaStream_t s) {
+  row_red_launch<2>(a, r0, b_dot, invd, z, c, red, slot, s);
+}
+void launch_cheb1_pre_resid(const DevCsr& a, const double* invd, const double* b, double* z, double* t, ChebCoef c,
+                            cudaStream_t s) {
+  row_launch<4>(a, nullptr, b, invd, z, t, c, s);
+}
+void launch_cheb1_post(const DevCsr& a, const double* invd, const double* b, const double* z, double* z_out,
+                       ChebCoef c, cudaStream_t s) {
+  row_launch<5>(a, z, b, invd, nullptr, z_out, c, s);
+}
+void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, double* w, cudaStream_t s) {
+  row_launch<6>(a, v, nullptr, invd, w, nullptr, ChebCoef{}, s);
 }
 
 void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s) {
@@ -411,48 +424,19 @@ void launch_pcg_direction(int n, double* p, const double* z, const double* scal,
   ++g_launch_count;
   k_pcg_direction<<<grid_for(n), kBlock, 0, s>>>(n, p, z, scal);
 }
-
-void launch_cheb_pre(const DevCsr& a, const double* invd, const double* b, double* z, ChebCoef c, cudaStream_t s) {
-  ++g_launch_count;
-  if (a.n_rows == 0) return;
-  const int g = grid_rows(a.n_rows, a.tpr);
-  DISPATCH_TPR(a.tpr, k_cheb_pre, <<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, invd, b, z, c));
-}
-
-void launch_cheb_post2(const DevCsr& a, const double* invd, const double* r0, double* z, ChebCoef c,
-                       const double* b_dot, Reducer* red, int slot, cudaStream_t s) {
-  ++g_launch_count;
-  if (a.n_rows == 0) return;
-  const int g = red_grid((long)a.n_rows * a.tpr);
-  Reducer r = red ? *red : Reducer{};
-  const int dr = red ? 1 : 0;
-  DISPATCH_TPR(a.tpr, k_cheb_post2,
-               <<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, invd, r0, z, c, b_dot, r, slot, dr));
-}
-
-void launch_prolong_add(const DevCsr& p, const double* zc, double* z, cudaStream_t s) {
-  ++g_launch_count;
-  if (p.n_rows == 0) return;
-  const int g = grid_rows(p.n_rows, p.tpr);
-  DISPATCH_TPR(p.tpr, k_prolong_add, <<<g, kBlock, 0, s>>>(p.n_rows, p.row_ptr, p.col_idx, p.values, zc, z));
-}
-
 void launch_dense_solve(int n, const double* ainv, const double* b, double* z, cudaStream_t s) {
   ++g_launch_count;
   k_dense_solve<<<1, 1024, n * sizeof(double), s>>>(n, ainv, b, z);
 }
-
 void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s) {
   ++g_launch_count;
   Reducer rr = red ? *red : Reducer{};
   k_jacobi<<<red_grid(n), kBlock, 0, s>>>(n, invd, r, z, rr, slot, red ? 1 : 0);
 }
-
 void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, cudaStream_t s) {
   ++g_launch_count;
   k_dot<<<red_grid(n), kBlock, 0, s>>>(n, a, b, red, slot);
 }
-
 void launch_multi_dot(int n, int m, const double* const* V, const double* w, Reducer red, int slot0, cudaStream_t s) {
   ++g_launch_count;
   PtrPack pk{};
@@ -464,12 +448,6 @@ void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y,
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
   k_lincomb<<<grid_for(n), kBlock, 0, s>>>(n, m, pk, c, y);
-}
-void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, double* w, cudaStream_t s) {
-  ++g_launch_count;
-  if (a.n_rows == 0) return;
-  const int g = grid_rows(a.n_rows, a.tpr);
-  DISPATCH_TPR(a.tpr, k_scaled_spmv, <<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, a.values, invd, v, w));
 }
 void launch_axpy(int n, double a, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;
@@ -484,8 +462,9 @@ void launch_scale(int n, double a, const double* x, double* y, cudaStream_t s) {
   k_scale<<<grid_for(n), kBlock, 0, s>>>(n, a, x, y);
 }
 void launch_fill(long n, double v, double* y, cudaStream_t s) {
+  if (n <= 0) return;
   ++g_launch_count;
-  if (n > 0) k_fill<<<grid_for(n), kBlock, 0, s>>>(n, v, y);
+  k_fill<<<grid_for(n), kBlock, 0, s>>>(n, v, y);
 }
 void launch_rkc_stage(int n, double a0, double mu, double nu, double mt, double gt, const double* y0,
                       const double* y1, const double* y2, const double* f, const double* f0, double* y,
@@ -503,21 +482,25 @@ void launch_rkc_error(int n, const double* x, const double* xn, const double* f0
   k_rkc_error<<<red_grid(n), kBlock, 0, s>>>(n, x, xn, f0, fn, dt, atol, rtol, red, slot);
 }
 void launch_gather(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
+  if (n <= 0) return;
   ++g_launch_count;
-  if (n > 0) k_gather<<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
+  k_gather<<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
 }
 void launch_scatter(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
+  if (n <= 0) return;
   ++g_launch_count;
-  if (n > 0) k_scatter<<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
+  k_scatter<<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
 }
 void launch_lift_fixed(int n_fixed, const int* set_of_fixed, SetVals set_vals, double* fixed_part, cudaStream_t s) {
+  if (n_fixed <= 0) return;
   ++g_launch_count;
-  if (n_fixed > 0) k_lift_fixed<<<grid_for(n_fixed), kBlock, 0, s>>>(n_fixed, set_of_fixed, set_vals, fixed_part);
+  k_lift_fixed<<<grid_for(n_fixed), kBlock, 0, s>>>(n_fixed, set_of_fixed, set_vals, fixed_part);
 }
 void launch_boundary_load(int n_rows, const int* rows, const double* coef, int n_sets, SetVals rates, double* r,
                           cudaStream_t s) {
+  if (n_rows <= 0) return;
   ++g_launch_count;
-  if (n_rows > 0) k_boundary_load<<<grid_for(n_rows), kBlock, 0, s>>>(n_rows, rows, coef, n_sets, rates, r);
+  k_boundary_load<<<grid_for(n_rows), kBlock, 0, s>>>(n_rows, rows, coef, n_sets, rates, r);
 }
 
 }  // namespace eqsb
