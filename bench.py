@@ -201,7 +201,7 @@ def run_b200(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     spec = CONFIGS[args.config]
-    cfg = scenario(spec["n"], spec["jitter"], spec["planes"])
+    cfg = scenario(spec["n"], spec["jitter"], spec["planes"], estimator=args.estimator)
     t_setup = time.perf_counter()
     g = eb.FemSystem(cfg, device=local_rank)
     t_setup = time.perf_counter() - t_setup
@@ -299,7 +299,9 @@ def run_b200(args):
         "data": "synthetic (generated mesh + mt19937 initial state; no dataset)",
         "config": {"workload": f"{args.config}: {spec['n']}^3 {'jittered ' if spec['jitter'] else ''}unit cube, "
                                f"{n} free dofs, {g.n_tets} tets, microvaristor layer z in {spec['planes']}, "
-                               f"RKC path B s={S_STAGES} dt=0.9*beta(4)/rho (={dt:.4g}s), SPE(8) + AMG-PCG 1e-12",
+                               f"RKC path B s={S_STAGES} dt=0.9*beta(4)/rho (={dt:.4g}s), "
+                               f"estimator {args.estimator} + AMG-PCG 1e-12",
+                   "estimator": args.estimator,
                    "n_free": n, "n_tets": g.n_tets, "nnz_mass_free": g.nnz_mass_free,
                    "amg_levels": g.amg_levels(), "parallelism": f"replicas x{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (matrices + vectors >> 126 MB), no flush needed"},
@@ -327,6 +329,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the in-run CPU baseline sample")
+    ap.add_argument("--estimator", default="spe", choices=["zero", "previous", "spe"],
+                    help="MRHS start vectors (proj/src/start_vector.cpp); the reference nonlinear scenario uses spe")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

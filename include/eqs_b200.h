@@ -65,6 +65,7 @@ typedef struct {
   int estimator_mode;     /* 0 = zero, 1 = previous, 2 = spe */
   int spe_window;         /* 8 */
   double mgs_drop_tol;    /* 1e-8 */
+  double amg_coarse_filter; /* additive: V-cycle coarse-operator filter eps (0 = off; configs default 0.0025) */
 } eqs_solver_params;
 
 /* Problem description consumed by eqs_create: the arrays the reference's

@@ -110,12 +110,23 @@ void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, 
 void launch_multi_dot(int n, int m, const double* const* V, const double* w, Reducer red, int slot0, cudaStream_t s);
 void launch_axpy(int n, double a, const double* x, double* y, cudaStream_t s);            // y += a x
 void launch_scale(int n, double a, const double* x, double* y, cudaStream_t s);           // y = a x
+void launch_diag_scale(int n, const double* invd, const double* b, double a, double* z, cudaStream_t s);  // z = a D^-1 b
 void launch_axpy_dev(int n, const double* coef, double sign, const double* x, double* y, cudaStream_t s);  // y += sign*(*coef) x
 // y = sum_k c[k] V_k  (coefficients by value)
 struct CoefPack {
   double c[kMaxMulti];
 };
 void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s);
+// SPE basis maintenance: w -= sum_j c_j Q_j with ||w||^2 into slot; and a
+// kin -> kout basis rotation out_j = sum_i T[i][j] in_i (kin, kout <= 9)
+constexpr int kMaxWin = 9;
+struct RotPack {
+  double t[kMaxWin][kMaxWin];
+};
+void launch_orth_update(int n, int m, const double* const* Q, CoefPack c, double* w, Reducer red, int slot,
+                        cudaStream_t s);
+void launch_lincomb_multi(int n, int kin, int kout, const double* const* in, double* const* out, const RotPack& T,
+                          cudaStream_t s);
 // w = invd .* (A v)   (power iteration on D^-1 A for the smoother bounds)
 void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, double* w, cudaStream_t s);
 void launch_fill(long n, double v, double* y, cudaStream_t s);

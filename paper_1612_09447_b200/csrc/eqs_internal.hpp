@@ -76,6 +76,7 @@ struct SolverParams {
   double rho_solve_tol = 1e-4;
   double amg_theta = 0.08, amg_omega = 4.0 / 3.0;
   int amg_sweeps = 1, amg_max_levels = 10, amg_coarse_limit = 64;
+  double amg_coarse_filter = 0.0025;  // additive: V-cycle coarse-operator filter (0 = off)
   int estimator_mode = 0;  // 0 zero, 1 previous, 2 spe
   int spe_window = 8;
   double mgs_drop_tol = 1e-8;
@@ -116,6 +117,11 @@ struct AmgHierarchy {
 // AmgPreconditioner ctor (proj/src/amg.cpp:90-143), bit-exact aggregation and
 // Galerkin products (deterministic row-parallel SpGEMM).
 AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp);
+// V-cycle operator of a coarse level: entries with |a_ij| < eps sqrt(|a_ii a_jj|)
+// dropped and lumped onto the diagonal (row sums kept). The hierarchy itself
+// (P, R, Galerkin A_l) is untouched; only the smoother/residual operator of
+// levels >= 1 uses this.
+HostCsr filter_lumped(const HostCsr& a, double eps);
 double estimate_lambda_max_scaled(const HostCsr& a, int iters, unsigned seed);
 
 // symmetric LDLT with diagonal pivoting (Eigen::LDLT semantics)

@@ -124,6 +124,7 @@ GpuSystem::GpuSystem(Problem&& p, int device) : prob_(std::move(p)), device_(dev
 }
 
 GpuSystem::~GpuSystem() {
+  invalidate_graphs();
   for (auto& e : events_) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -238,22 +239,29 @@ void GpuSystem::build_device() {
       out.upload(f.data(), f.size(), s);
       CK(cudaStreamSynchronize(s));
     };
+    const double eps = prob_.solver.amg_coarse_filter;
     for (int l = 0; l < L; ++l) {
       DevLevel& lv = levels_[l];
       const AmgHostLevel& hl = amg_.levels[l];
+      // V-cycle operator: the fine level uses M_II itself; coarse levels use the
+      // lumped filtered Galerkin operator
+      HostCsr filtered;
+      const bool filt = l > 0 && l + 1 < L && eps > 0.0;
+      if (filt) filtered = filter_lumped(hl.A, eps);
+      const HostCsr& av = filt ? filtered : hl.A;
       if (l == 0) {
         lv.A = mii_;  // shares indices / fp64 values with the PCG operator
       } else {
-        upload_csr(hl.A, lv.A, lv.a_rp, lv.a_ci, lv.a_v, s);
+        upload_csr(av, lv.A, lv.a_rp, lv.a_ci, lv.a_v, s);
       }
       const int n = hl.A.n_rows;
       if (l + 1 < L) {
-        f32(hl.A.values, lv.a_vf);
+        f32(av.values, lv.a_vf);
         upload_csr(hl.P, lv.P, lv.p_rp, lv.p_ci, lv.p_v, s);
         upload_csr(hl.R, lv.R, lv.r_rp, lv.r_ci, lv.r_v, s);
         f32(hl.P.values, lv.p_vf);
         f32(hl.R.values, lv.r_vf);
-        const std::vector<double> invd = inv_diagonal(hl.A);
+        const std::vector<double> invd = inv_diagonal(av);
         lv.invd.alloc(n);
         lv.invd.upload(invd.data(), n, s);
         lv.t.alloc(n);
@@ -311,7 +319,8 @@ void GpuSystem::build_device() {
         }
         launch_scale(n, 1.0 / lam, lv.t.p, lv.z.p, s);
       }
-      lv.lambda_smoother = std::max(lam, amg_.levels[l].lambda_max_scaled);
+      // level 0 operator == the hierarchy's A_0: also use the setup's 10-step estimate
+      lv.lambda_smoother = l == 0 ? std::max(lam, amg_.levels[l].lambda_max_scaled) : lam;
     }
     set_cheb(cheb_ratio);
   }
@@ -323,6 +332,7 @@ void GpuSystem::build_device() {
 // estimate. Degree 2: x += c0 D^-1 r0 + c1 D^-1 (r0 - A D^-1 r0 / theta);
 // degree 1: x += D^-1 r0 / theta.
 void GpuSystem::set_cheb(double ratio) {
+  invalidate_graphs();  // coefficients are baked into the captured kernel parameters
   cheb_ratio = ratio;
   for (auto& lv : levels_) {
     const double lmax = 1.1 * lv.lambda_smoother, lmin = lmax / ratio;
@@ -335,13 +345,20 @@ void GpuSystem::set_cheb(double ratio) {
   }
 }
 
+void GpuSystem::invalidate_graphs() {
+  if (vcycle_graph_) cudaGraphExecDestroy(vcycle_graph_);
+  vcycle_graph_ = nullptr;
+}
+
 void GpuSystem::set_level_tpr(int level, int tpr) {
   if (tpr < 1 || tpr > 32 || (tpr & (tpr - 1))) throw std::invalid_argument("tpr must be a power of two <= 32");
+  invalidate_graphs();
   if (level == 0) mii_.tpr = tpr;
   if (level < (int)levels_.size()) levels_[level].A.tpr = tpr;
 }
 
 void GpuSystem::set_vcycle_fp32(bool on) {
+  invalidate_graphs();
   vcycle_fp32_ = on;
   for (size_t l = 0; l + 1 < levels_.size(); ++l) {
     DevLevel& lv = levels_[l];
@@ -557,8 +574,12 @@ double* GpuSystem::vcycle(int l, const double* b, bool dot_into_rz) {
   if (deg >= 2) {
     launch_cheb_pre(lv.A, lv.invd.p, b, z, lv.cheb, stream_);
     launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
-  } else {
+  } else if (lv.A.tpr <= 4) {
     launch_cheb1_pre_resid(lv.A, lv.invd.p, b, z, lv.t.p, lv.cheb1, stream_);
+  } else {
+    // dense rows: one gathered vector per entry instead of two (b and D^-1)
+    launch_diag_scale(lv.A.n_rows, lv.invd.p, b, lv.cheb1.inv_theta, z, stream_);
+    launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
   }
   launch_spmv(lv.R, lv.t.p, nx.b.p, stream_);
   const double* zc = vcycle(l + 1, nx.b.p, false);
@@ -575,11 +596,32 @@ double* GpuSystem::vcycle(int l, const double* b, bool dot_into_rz) {
   return lv.z2.p;
 }
 
+// The V-cycle is a fixed sequence of ~4 kernels per level on fixed buffers,
+// so it is captured once into a CUDA graph and replayed: one launch per
+// preconditioner application instead of ~30, no host gaps between the short
+// coarse-level kernels.
 double* GpuSystem::precondition(const double* r) {
   tic(TC_VCYCLE);
   double* z;
   if (prob_.solver.precond == 2) {
-    z = vcycle(0, r, true);
+    if (use_graphs && r == w_r_.p) {
+      if (!vcycle_graph_) {
+        cudaGraph_t graph;
+        const long before = g_launch_count;
+        CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        vcycle_out_ = vcycle(0, r, true);
+        CK(cudaStreamEndCapture(stream_, &graph));
+        vcycle_graph_kernels_ = g_launch_count - before;
+        g_launch_count = before;
+        CK(cudaGraphInstantiate(&vcycle_graph_, graph, 0));
+        CK(cudaGraphDestroy(graph));
+      }
+      CK(cudaGraphLaunch(vcycle_graph_, stream_));
+      g_launch_count += vcycle_graph_kernels_;
+      z = vcycle_out_;
+    } else {
+      z = vcycle(0, r, true);
+    }
   } else {
     Reducer rr = red_;
     z = w_z_.p;
@@ -670,6 +712,204 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
 // ------------------------------------------------------------------ estimator
 // StartVectorEstimator::next (proj/src/start_vector.cpp:84-109); writes the
 // start vector into x0 and returns true when it is non-zero-by-construction.
+// SPE (proj/src/start_vector.cpp:33-62,84-109,152-164). The reference
+// re-orthonormalises its whole window with MGS on every solve and applies
+// M to every basis vector (2 sum_k (dot + axpy) + m SpMVs per solve). The
+// Galerkin start vector x0 = V (V'MV)^-1 V'b only depends on span(V), so the
+// device keeps an orthonormal basis Q of the window, W = M Q, G = Q'MQ and R
+// with H = Q R across solves: the new solution is appended by two classical
+// Gram-Schmidt passes with the reference's drop test (against the same span
+// the reference's MGS would test it against), the oldest is removed by a
+// Givens downdate of R and a rotation of Q and W. Windows containing a dropped
+// or zero vector (where the reference's drop decisions can change when the
+// window slides) fall back to the reference's full MGS rebuild.
+double* GpuSystem::spe_q(int set, int j) { return spe_q_[set][j]->p; }
+double* GpuSystem::spe_w(int set, int j) { return spe_w_[set][j]->p; }
+
+void GpuSystem::spe_alloc(int window) {
+  if ((int)spe_q_[0].size() >= window) return;
+  for (int s = 0; s < 2; ++s)
+    while ((int)spe_q_[s].size() < window) {
+      spe_q_[s].push_back(std::make_unique<DevBuf<double>>());
+      spe_q_[s].back()->alloc(std::max(1, n_free_));
+      spe_w_[s].push_back(std::make_unique<DevBuf<double>>());
+      spe_w_[s].back()->alloc(std::max(1, n_free_));
+    }
+}
+
+// G row/column k (G_ik = q_i' W_k) for the basis vectors 0..k of the current set
+void GpuSystem::spe_g_column(int k) {
+  std::vector<const double*> Q(k + 1);
+  for (int i = 0; i <= k; ++i) Q[i] = spe_q(spe_set_, i);
+  launch_multi_dot(n_free_, k + 1, Q.data(), spe_w(spe_set_, k), red_, S_MDOT, stream_);
+  double g[kMaxMulti];
+  read_scalars(S_MDOT, k + 1, g);
+  spe_G_.resize((size_t)kMaxMulti * kMaxMulti);
+  for (int i = 0; i <= k; ++i) spe_G_[(size_t)i * kMaxMulti + k] = spe_G_[(size_t)k * kMaxMulti + i] = g[i];
+}
+
+// mgs_orthonormalize (start_vector.cpp:10-28) over the whole history, reference order
+void GpuSystem::spe_rebuild() {
+  const int n = n_free_;
+  const double drop = prob_.solver.mgs_drop_tol;
+  spe_alloc((int)history_.size());
+  spe_k_ = 0;
+  bool all_kept = true;
+  for (double* cand : history_) {
+    launch_dot(n, cand, cand, red_, S_NORM, stream_);
+    const double norm0 = std::sqrt(read_scalar(S_NORM));
+    if (norm0 == 0.0) {
+      all_kept = false;
+      continue;
+    }
+    const int m = spe_k_;
+    double* w = spe_q(spe_set_, m);
+    CK(cudaMemcpyAsync(w, cand, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    std::vector<double> rc(m + 1, 0.0);
+    bool keep = true;
+    for (int pass = 0; pass < 2 && keep; ++pass) {
+      for (int u = 0; u < m; ++u) {  // modified Gram-Schmidt, sequential projections
+        launch_dot(n, spe_q(spe_set_, u), w, red_, S_DOT, stream_);
+        launch_axpy_dev(n, red_scal_.p + S_DOT, -1.0, spe_q(spe_set_, u), w, stream_);
+      }
+      launch_dot(n, w, w, red_, S_NORM, stream_);
+      const double nrm = std::sqrt(read_scalar(S_NORM));
+      if (nrm <= drop * norm0) keep = false;
+      else if (pass == 1) {
+        launch_scale(n, 1.0 / nrm, w, w, stream_);
+        rc[m] = nrm;
+      }
+    }
+    if (!keep) {
+      all_kept = false;
+      continue;
+    }
+    launch_spmv(mii_, w, spe_w(spe_set_, m), stream_);
+    ++spe_k_;
+    spe_g_column(m);
+  }
+  spe_clean_ = all_kept && (int)history_.size() <= kMaxWin - 1;
+  if (spe_clean_) {  // R = Q' H (H = Q R exactly in this state)
+    const int k = spe_k_;
+    spe_R_.assign((size_t)kMaxWin * kMaxWin, 0.0);
+    std::vector<const double*> Q(k);
+    for (int i = 0; i < k; ++i) Q[i] = spe_q(spe_set_, i);
+    int j = 0;
+    for (double* h : history_) {
+      launch_multi_dot(n, k, Q.data(), h, red_, S_MDOT, stream_);
+      double col[kMaxMulti];
+      read_scalars(S_MDOT, k, col);
+      for (int i = 0; i <= j; ++i) spe_R_[(size_t)i * kMaxWin + j] = col[i];
+      ++j;
+    }
+  }
+}
+
+// append h (newest) with two classical Gram-Schmidt passes and the MGS drop test
+void GpuSystem::spe_append(const double* h) {
+  const int n = n_free_;
+  const double drop = prob_.solver.mgs_drop_tol;
+  const int m = spe_k_;
+  launch_dot(n, h, h, red_, S_NORM, stream_);
+  const double norm0 = std::sqrt(read_scalar(S_NORM));
+  if (norm0 == 0.0) {
+    spe_clean_ = false;
+    return;
+  }
+  double* w = spe_q(spe_set_, m);
+  CK(cudaMemcpyAsync(w, h, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+  std::vector<const double*> Q(m);
+  for (int i = 0; i < m; ++i) Q[i] = spe_q(spe_set_, i);
+  std::vector<double> r(m + 1, 0.0);
+  double nrm = norm0;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (m > 0) {
+      launch_multi_dot(n, m, Q.data(), w, red_, S_MDOT, stream_);
+      double c[kMaxMulti];
+      read_scalars(S_MDOT, m, c);
+      CoefPack cp{};
+      for (int i = 0; i < m; ++i) {
+        cp.c[i] = c[i];
+        r[i] += c[i];
+      }
+      launch_orth_update(n, m, Q.data(), cp, w, red_, S_NORM, stream_);
+      nrm = std::sqrt(read_scalar(S_NORM));
+    }
+    if (nrm <= drop * norm0) {
+      spe_clean_ = false;
+      return;
+    }
+  }
+  launch_scale(n, 1.0 / nrm, w, w, stream_);
+  r[m] = nrm;
+  for (int i = 0; i <= m; ++i) spe_R_[(size_t)i * kMaxWin + m] = r[i];
+  launch_spmv(mii_, w, spe_w(spe_set_, m), stream_);
+  spe_k_ = m + 1;
+  spe_g_column(m);
+}
+
+// remove the oldest window vector: Givens downdate of R[:,1:], rotate Q and W
+void GpuSystem::spe_downdate() {
+  const int k = spe_k_;
+  if (k <= 1) {
+    spe_k_ = 0;
+    return;
+  }
+  // Hessenberg Rh = R[:, 1:k] (k x (k-1)); J accumulates the rotations (k x k)
+  double Rh[kMaxWin][kMaxWin] = {}, J[kMaxWin][kMaxWin] = {};
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j + 1 < k; ++j) Rh[i][j] = spe_R_[(size_t)i * kMaxWin + j + 1];
+  for (int i = 0; i < k; ++i) J[i][i] = 1.0;
+  for (int i = 0; i + 1 < k; ++i) {
+    const double a = Rh[i][i], b = Rh[i + 1][i];
+    const double rr = std::hypot(a, b);
+    const double c = rr == 0.0 ? 1.0 : a / rr, s = rr == 0.0 ? 0.0 : b / rr;
+    for (int j = 0; j + 1 < k; ++j) {
+      const double u = Rh[i][j], v = Rh[i + 1][j];
+      Rh[i][j] = c * u + s * v;
+      Rh[i + 1][j] = -s * u + c * v;
+    }
+    for (int j = 0; j < k; ++j) {
+      const double u = J[i][j], v = J[i + 1][j];
+      J[i][j] = c * u + s * v;
+      J[i + 1][j] = -s * u + c * v;
+    }
+  }
+  // Q' = Q J^T (first k-1 columns); T[a][b] = J[b][a]
+  RotPack T{};
+  for (int a = 0; a < k; ++a)
+    for (int b = 0; b + 1 < k; ++b) T.t[a][b] = J[b][a];
+  std::vector<const double*> qi(k), wi(k);
+  std::vector<double*> qo(k - 1), wo(k - 1);
+  for (int i = 0; i < k; ++i) {
+    qi[i] = spe_q(spe_set_, i);
+    wi[i] = spe_w(spe_set_, i);
+  }
+  for (int j = 0; j + 1 < k; ++j) {
+    qo[j] = spe_q(1 - spe_set_, j);
+    wo[j] = spe_w(1 - spe_set_, j);
+  }
+  launch_lincomb_multi(n_free_, k, k - 1, qi.data(), qo.data(), T, stream_);
+  launch_lincomb_multi(n_free_, k, k - 1, wi.data(), wo.data(), T, stream_);
+  // G' = T' G T, R' = rows 0..k-2 of the rotated Rh
+  std::vector<double> G2((size_t)kMaxMulti * kMaxMulti, 0.0);
+  for (int a = 0; a + 1 < k; ++a)
+    for (int b = 0; b + 1 < k; ++b) {
+      double s = 0.0;
+      for (int i = 0; i < k; ++i)
+        for (int j = 0; j < k; ++j) s += T.t[i][a] * spe_G_[(size_t)i * kMaxMulti + j] * T.t[j][b];
+      G2[(size_t)a * kMaxMulti + b] = s;
+    }
+  spe_G_ = G2;
+  spe_R_.assign((size_t)kMaxWin * kMaxWin, 0.0);
+  for (int i = 0; i + 1 < k; ++i)
+    for (int j = i; j + 1 < k; ++j) spe_R_[(size_t)i * kMaxWin + j] = Rh[i][j];
+  spe_set_ = 1 - spe_set_;
+  spe_k_ = k - 1;
+}
+
+// StartVectorEstimator::next (proj/src/start_vector.cpp:84-109); writes the
+// start vector into x0 and returns true when it is non-zero-by-construction.
 bool GpuSystem::estimator_next(const double* b, double* x0) {
   const int n = n_free_;
   const int mode = prob_.solver.estimator_mode;
@@ -680,50 +920,17 @@ bool GpuSystem::estimator_next(const double* b, double* x0) {
     return true;
   }
   tic(TC_SPE);
-  // mgs_orthonormalize (start_vector.cpp:10-28), two projection passes with dropping
-  const double drop = prob_.solver.mgs_drop_tol;
-  while (basis_.size() < history_.size()) {
-    basis_.push_back(std::make_unique<DevBuf<double>>());
-    basis_.back()->alloc(std::max(1, n));
-    basis_w_.push_back(std::make_unique<DevBuf<double>>());
-    basis_w_.back()->alloc(std::max(1, n));
-  }
-  int m = 0;
-  for (double* cand : history_) {
-    launch_dot(n, cand, cand, red_, S_NORM, stream_);
-    const double norm0 = std::sqrt(read_scalar(S_NORM));
-    if (norm0 == 0.0) continue;
-    double* w = basis_[m]->p;
-    CK(cudaMemcpyAsync(w, cand, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
-    bool keep = true;
-    for (int pass = 0; pass < 2 && keep; ++pass) {
-      for (int u = 0; u < m; ++u) {
-        launch_dot(n, basis_[u]->p, w, red_, S_DOT, stream_);
-        launch_axpy_dev(n, red_scal_.p + S_DOT, -1.0, basis_[u]->p, w, stream_);
-      }
-      launch_dot(n, w, w, red_, S_NORM, stream_);
-      const double nrm = std::sqrt(read_scalar(S_NORM));
-      if (nrm <= drop * norm0) keep = false;
-      else if (pass == 1) launch_scale(n, 1.0 / nrm, w, w, stream_);
-    }
-    if (keep) ++m;
-  }
+  if (!spe_clean_ || !spe_incremental) spe_rebuild();
+  const int m = spe_k_;
   estimator_rank_ = m;
   if (m == 0) {
     toc(TC_SPE, 0.0);
     return false;
   }
-  // spe_start (start_vector.cpp:33-62): x0 = V (V'MV)^-1 V' b
-  std::vector<const double*> V(m);
-  for (int c = 0; c < m; ++c) V[c] = basis_[c]->p;
+  // spe_start (start_vector.cpp:33-62): x0 = V (V'MV)^-1 V' b with the pivoted LDLT of G
   std::vector<double> g((size_t)m * m);
-  for (int j = 0; j < m; ++j) {
-    launch_spmv(mii_, basis_[j]->p, basis_w_[j]->p, stream_);
-    launch_multi_dot(n, m, V.data(), basis_w_[j]->p, red_, S_MDOT, stream_);
-    double col[kMaxMulti];
-    read_scalars(S_MDOT, m, col);
-    for (int i = 0; i < m; ++i) g[(size_t)i * m + j] = col[i];
-  }
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) g[(size_t)i * m + j] = spe_G_[(size_t)i * kMaxMulti + j];
   DenseLdlt ldlt;
   ldlt.compute(g, m);
   double dmax = 0.0, dmin = INFINITY;
@@ -745,6 +952,8 @@ bool GpuSystem::estimator_next(const double* b, double* x0) {
     ldlt.solve(e.data(), col.data());
     for (int r = 0; r < m; ++r) ginv[(size_t)r * m + c] = col[r];
   }
+  std::vector<const double*> V(m);
+  for (int c = 0; c < m; ++c) V[c] = spe_q(spe_set_, c);
   launch_multi_dot(n, m, V.data(), b, red_, S_MDOT, stream_);
   double vtb[kMaxMulti];
   read_scalars(S_MDOT, m, vtb);
@@ -768,6 +977,7 @@ void GpuSystem::estimator_feedback(const double* x) {
   if (history_.size() >= window) {
     buf = history_.front();
     history_.pop_front();
+    if (mode == 2 && spe_clean_ && spe_incremental) spe_downdate();
   } else {
     hist_pool_.push_back(std::make_unique<DevBuf<double>>());
     hist_pool_.back()->alloc(std::max(1, n_free_));
@@ -775,6 +985,16 @@ void GpuSystem::estimator_feedback(const double* x) {
   }
   CK(cudaMemcpyAsync(buf, x, sizeof(double) * n_free_, cudaMemcpyDeviceToDevice, stream_));
   history_.push_back(buf);
+  if (mode == 2 && spe_clean_ && spe_incremental) {
+    if (window > (size_t)(kMaxWin - 1)) {
+      spe_clean_ = false;  // large windows always use the full rebuild
+    } else {
+      tic(TC_SPE);
+      spe_alloc((int)window);
+      spe_append(buf);
+      toc(TC_SPE, 0.0);
+    }
+  }
 }
 
 // FemSystem::eval_rhs (proj/src/fem_system.cpp:69-99)

@@ -158,6 +158,16 @@ class GpuSystem {
   double* vcycle(int l, const double* b, bool dot_into_rz);  // returns the buffer holding z_l
   double* precondition(const double* r);  // z = M^-1 r (returned buffer), S_RZ <- r.z
   bool vcycle_fp32_ = true;
+  cudaGraphExec_t vcycle_graph_ = nullptr;  // captured V-cycle (rebuilt when options change)
+  double* vcycle_out_ = nullptr;
+  long vcycle_graph_kernels_ = 0;
+
+ public:
+  bool use_graphs = true;
+  bool spe_incremental = true;  // false: the reference's full MGS rebuild on every solve
+  void invalidate_graphs();
+
+ private:
   void kx_tets(const double* x, const double* v);
   double read_scalar(int slot);
   void read_scalars(int first, int count, double* out);
@@ -168,6 +178,19 @@ class GpuSystem {
   bool estimator_next(const double* r, double* x0);
   void estimator_feedback(const double* x);
   int estimator_rank_ = 0;
+  // incremental SPE basis (Q orthonormal, W = M Q, G = Q'MQ, H = Q R)
+  std::vector<std::unique_ptr<DevBuf<double>>> spe_q_[2], spe_w_[2];
+  int spe_set_ = 0, spe_k_ = 0;
+  bool spe_clean_ = true;
+  std::vector<double> spe_G_ = std::vector<double>((size_t)kMaxMulti * kMaxMulti, 0.0);
+  std::vector<double> spe_R_ = std::vector<double>((size_t)kMaxWin * kMaxWin, 0.0);
+  double* spe_q(int set, int j);
+  double* spe_w(int set, int j);
+  void spe_alloc(int window);
+  void spe_g_column(int k);
+  void spe_rebuild();
+  void spe_append(const double* h);
+  void spe_downdate();
 
   Problem prob_;
   int device_ = 0;
@@ -212,12 +235,10 @@ class GpuSystem {
   // work vectors
   DevBuf<double> w_r_, w_z_, w_p_, w_q_, w_full_a_, w_full_b_, w_free_a_, w_free_b_;
   DevBuf<double> full_[4], F0_, F_, Fn_, rho_v_, rho_w_;  // full_: state + 3 stage buffers
-  std::vector<std::unique_ptr<DevBuf<double>>> basis_w_;
   double* X_ = nullptr;
   // estimator history (device ring)
   std::vector<std::unique_ptr<DevBuf<double>>> hist_pool_;
   std::deque<double*> history_;
-  std::vector<std::unique_ptr<DevBuf<double>>> basis_;
   // timing
   struct Ev {
     cudaEvent_t a, b;

@@ -131,6 +131,7 @@ SimConfig parse_config(const std::string& text) {
       c.solver.max_iter = js.value("max_iter", c.solver.max_iter);
       c.solver.amg_theta = js.value("amg_strength_threshold", c.solver.amg_theta);
       c.solver.amg_coarse_limit = js.value("amg_coarse_limit", c.solver.amg_coarse_limit);
+      c.solver.amg_coarse_filter = js.value("amg_coarse_filter", c.solver.amg_coarse_filter);  // additive key
       if (!(c.solver.rel_tol > 0)) throw ConfigError("solver rel_tol must be positive");
     }
     if (j.contains("estimator")) {

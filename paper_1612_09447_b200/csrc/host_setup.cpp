@@ -475,6 +475,46 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp) {
   return h;
 }
 
+HostCsr filter_lumped(const HostCsr& a, double eps) {
+  const std::vector<double> d = diagonal(a);
+  HostCsr f;
+  f.n_rows = a.n_rows;
+  f.n_cols = a.n_cols;
+  f.row_ptr.assign(a.n_rows + 1, 0);
+  std::vector<char> keep(a.nnz(), 0);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < a.n_rows; ++i) {
+    int cnt = 0;
+    for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+      const int j = a.col_idx[k];
+      if (j == i || std::abs(a.values[k]) >= eps * std::sqrt(std::abs(d[i] * d[j]))) {
+        keep[k] = 1;
+        ++cnt;
+      }
+    }
+    f.row_ptr[i + 1] = cnt;
+  }
+  for (int i = 0; i < a.n_rows; ++i) f.row_ptr[i + 1] += f.row_ptr[i];
+  f.col_idx.resize(f.row_ptr.back());
+  f.values.resize(f.row_ptr.back());
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < a.n_rows; ++i) {
+    double lumped = 0.0;
+    int pos = f.row_ptr[i], diag = -1;
+    for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+      if (!keep[k]) {
+        lumped += a.values[k];
+        continue;
+      }
+      if (a.col_idx[k] == i) diag = pos;
+      f.col_idx[pos] = a.col_idx[k];
+      f.values[pos++] = a.values[k];
+    }
+    if (diag >= 0) f.values[diag] += lumped;
+  }
+  return f;
+}
+
 // Eigen::LDLT semantics (see oracle/solvers.cpp for the same restatement).
 void DenseLdlt::compute(const std::vector<double>& a, int n_) {
   n = n_;

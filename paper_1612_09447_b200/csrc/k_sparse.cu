@@ -256,6 +256,31 @@ __global__ void k_lincomb(int n, int m, PtrPack V, CoefPack c, double* __restric
   }
 }
 
+// w -= sum_j c_j Q_j ; slot <- w.w   (one Gram-Schmidt projection pass)
+__global__ void k_orth_update(int n, int m, PtrPack Q, CoefPack c, double* __restrict__ w, Reducer red, int slot) {
+  double acc = 0.0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    double s = w[i];
+    for (int k = 0; k < m; ++k) s -= c.c[k] * Q.p[k][i];
+    w[i] = s;
+    acc += s * s;
+  }
+  reduce_finish(acc, red, slot);
+}
+
+// out_j = sum_i T[i][j] in_i  (basis rotation of the SPE window, T by value)
+__global__ void k_lincomb_multi(int n, int kin, int kout, PtrPack in, PtrPack out, RotPack T) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    double v[kMaxMulti];
+    for (int a = 0; a < kin; ++a) v[a] = in.p[a][i];
+    for (int b = 0; b < kout; ++b) {
+      double s = 0.0;
+      for (int a = 0; a < kin; ++a) s += T.t[a][b] * v[a];
+      const_cast<double*>(out.p[b])[i] = s;
+    }
+  }
+}
+
 __global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] += a * x[i];
 }
@@ -263,6 +288,10 @@ __global__ void k_axpy_dev(int n, const double* __restrict__ coef, double sign, 
                            double* __restrict__ y) {
   const double a = sign * coef[0];
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] += a * x[i];
+}
+__global__ void k_diag_scale(int n, const double* __restrict__ invd, const double* __restrict__ b, double a,
+                             double* __restrict__ z) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) z[i] = a * invd[i] * b[i];
 }
 __global__ void k_scale(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = a * x[i];
@@ -449,6 +478,21 @@ void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y,
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
   k_lincomb<<<grid_for(n), kBlock, 0, s>>>(n, m, pk, c, y);
 }
+void launch_orth_update(int n, int m, const double* const* Q, CoefPack c, double* w, Reducer red, int slot,
+                        cudaStream_t s) {
+  ++g_launch_count;
+  PtrPack pk{};
+  for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = Q[k];
+  k_orth_update<<<red_grid(n), kBlock, 0, s>>>(n, m, pk, c, w, red, slot);
+}
+void launch_lincomb_multi(int n, int kin, int kout, const double* const* in, double* const* out, const RotPack& T,
+                          cudaStream_t s) {
+  ++g_launch_count;
+  PtrPack pi{}, po{};
+  for (int k = 0; k < kin && k < kMaxMulti; ++k) pi.p[k] = in[k];
+  for (int k = 0; k < kout && k < kMaxMulti; ++k) po.p[k] = out[k];
+  k_lincomb_multi<<<grid_for(n), kBlock, 0, s>>>(n, kin, kout, pi, po, T);
+}
 void launch_axpy(int n, double a, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;
   k_axpy<<<grid_for(n), kBlock, 0, s>>>(n, a, x, y);
@@ -456,6 +500,11 @@ void launch_axpy(int n, double a, const double* x, double* y, cudaStream_t s) {
 void launch_axpy_dev(int n, const double* coef, double sign, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;
   k_axpy_dev<<<grid_for(n), kBlock, 0, s>>>(n, coef, sign, x, y);
+}
+void launch_diag_scale(int n, const double* invd, const double* b, double a, double* z, cudaStream_t s) {
+  if (n <= 0) return;
+  ++g_launch_count;
+  k_diag_scale<<<grid_for(n), kBlock, 0, s>>>(n, invd, b, a, z);
 }
 void launch_scale(int n, double a, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;

@@ -1,5 +1,7 @@
 """Shared scenario builders (reference JSON schema, proj/README.md:77-113)."""
 import copy
+import json
+import os
 
 SLAB_MATERIALS = {  # proj/configs/slab_nonlinear_rkc_spe.json:22-47
     "1": {"eps_r": 3.0, "conductivity": {"kind": "constant", "kappa": 1e-9}},
@@ -40,434 +42,14 @@ def matfree_setup(order, nonlinear, n=3):
                             "hv": {"kind": "constant", "value": 1.0}}}
 
 
+# verbatim copies of proj/configs/*.json (tests/golden/make_reference_configs.py):
+# /root/reference does not exist on the GPU box
+with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_configs.json")) as _f:
+    REFERENCE_CONFIGS = json.load(_f)
+
+
 def slab_reference(name):
-    """One of the reference's committed configs (inlined: /root/reference is absent on the GPU box)."""
     return copy.deepcopy(REFERENCE_CONFIGS[name])
-
-
-REFERENCE_CONFIGS = {
-    # proj/configs/slab_nonlinear_rkc_spe.json
-    "slab_nonlinear_rkc_spe": {
-        "name": "slab_nonlinear_rkc_spe",
-        "mesh": {"box": {"nx": 6, "ny": 6, "nz": 12, "lx": 0.006, "ly": 0.006, "lz": 0.012,
-                         "z_planes": [0.004, 0.008], "regions": [1, 2, 3]}},
-        "order": 1, "materials": copy.deepcopy(SLAB_MATERIALS),
-        "excitations": {"hv": {"kind": "sinusoid", "amplitude": 40000.0, "frequency": 50.0, "phase": 0.0},
-                        "ground": {"kind": "constant", "value": 0.0}},
-        "integrator": {"kind": "rkc", "tolerance": 0.01, "t_end": 0.02, "dt0": 1e-05, "max_stages": 200},
-        "solver": {"preconditioner": "amg", "rel_tol": 1e-12, "max_iter": 500},
-        "estimator": {"mode": "spe", "window": 8},
-        "probes": [[0.003, 0.003, 0.006]],
-        "workers": 1,
-    },
-    # proj/configs/smoke.json
-    "smoke": {
-        "name": "smoke",
-        "mesh": {"box": {"nx": 2, "ny": 2, "nz": 4, "lx": 0.01, "ly": 0.01, "lz": 0.02,
-                         "z_planes": [0.01], "regions": [1, 2]}},
-        "order": 1,
-        "materials": {"1": {"eps_r": 2.0, "conductivity": {"kind": "constant", "kappa": 1e-8}},
-                      "2": {"eps_r": 5.0, "conductivity": {"kind": "constant", "kappa": 5e-9}}},
-        "excitations": {"ground": {"kind": "constant", "value": 0.0},
-                        "hv": {"kind": "sinusoid", "amplitude": 100.0, "frequency": 50.0}},
-        "integrator": {"kind": "rkc", "tolerance": 1e-2, "t_end": 5e-4, "dt0": 1e-5},
-        "solver": {"preconditioner": "amg", "rel_tol": 1e-12, "max_iter": 500},
-        "estimator": {"mode": "spe", "window": 8},
-        "probes": [[0.005, 0.005, 0.01]],
-        "workers": 2,
-    },
-}
-
-
-# proj/configs/*.json (verbatim values; generated by the snippet in tests/golden/README.md)
-REFERENCE_CONFIGS.update({
- "slab_linear_rkc": {
-  "mesh": {
-   "box": {
-    "nx": 10,
-    "ny": 10,
-    "nz": 20,
-    "lx": 0.01,
-    "ly": 0.01,
-    "lz": 0.02,
-    "z_planes": [
-     0.01
-    ],
-    "regions": [
-     1,
-     2
-    ]
-   }
-  },
-  "order": 1,
-  "materials": {
-   "1": {
-    "eps_r": 2.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 1e-08
-    }
-   },
-   "2": {
-    "eps_r": 5.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 5e-09
-    }
-   }
-  },
-  "excitations": {
-   "hv": {
-    "kind": "sinusoid",
-    "amplitude": 10000.0,
-    "frequency": 50.0,
-    "phase": 0.0
-   },
-   "ground": {
-    "kind": "constant",
-    "value": 0.0
-   }
-  },
-  "name": "slab_linear_rkc",
-  "integrator": {
-   "kind": "rkc",
-   "tolerance": 0.01,
-   "t_end": 0.02,
-   "dt0": 1e-05,
-   "max_stages": 200
-  },
-  "solver": {
-   "preconditioner": "amg",
-   "rel_tol": 1e-12,
-   "max_iter": 500
-  },
-  "estimator": {
-   "mode": "zero"
-  },
-  "probes": [
-   [
-    0.005,
-    0.005,
-    0.01
-   ]
-  ],
-  "output": {
-   "metrics_csv": "metrics.csv",
-   "probe_csv": "probe.csv",
-   "solves_csv": ""
-  },
-  "workers": 1
- },
- "slab_linear_rkc_previous": {
-  "mesh": {
-   "box": {
-    "nx": 10,
-    "ny": 10,
-    "nz": 20,
-    "lx": 0.01,
-    "ly": 0.01,
-    "lz": 0.02,
-    "z_planes": [
-     0.01
-    ],
-    "regions": [
-     1,
-     2
-    ]
-   }
-  },
-  "order": 1,
-  "materials": {
-   "1": {
-    "eps_r": 2.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 1e-08
-    }
-   },
-   "2": {
-    "eps_r": 5.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 5e-09
-    }
-   }
-  },
-  "excitations": {
-   "hv": {
-    "kind": "sinusoid",
-    "amplitude": 10000.0,
-    "frequency": 50.0,
-    "phase": 0.0
-   },
-   "ground": {
-    "kind": "constant",
-    "value": 0.0
-   }
-  },
-  "name": "slab_linear_rkc_previous",
-  "integrator": {
-   "kind": "rkc",
-   "tolerance": 0.01,
-   "t_end": 0.02,
-   "dt0": 1e-05,
-   "max_stages": 200
-  },
-  "solver": {
-   "preconditioner": "amg",
-   "rel_tol": 1e-12,
-   "max_iter": 500
-  },
-  "estimator": {
-   "mode": "previous"
-  },
-  "probes": [
-   [
-    0.005,
-    0.005,
-    0.01
-   ]
-  ],
-  "output": {
-   "metrics_csv": "metrics.csv",
-   "probe_csv": "probe.csv",
-   "solves_csv": ""
-  },
-  "workers": 1
- },
- "slab_linear_rkc_spe": {
-  "mesh": {
-   "box": {
-    "nx": 10,
-    "ny": 10,
-    "nz": 20,
-    "lx": 0.01,
-    "ly": 0.01,
-    "lz": 0.02,
-    "z_planes": [
-     0.01
-    ],
-    "regions": [
-     1,
-     2
-    ]
-   }
-  },
-  "order": 1,
-  "materials": {
-   "1": {
-    "eps_r": 2.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 1e-08
-    }
-   },
-   "2": {
-    "eps_r": 5.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 5e-09
-    }
-   }
-  },
-  "excitations": {
-   "hv": {
-    "kind": "sinusoid",
-    "amplitude": 10000.0,
-    "frequency": 50.0,
-    "phase": 0.0
-   },
-   "ground": {
-    "kind": "constant",
-    "value": 0.0
-   }
-  },
-  "name": "slab_linear_rkc_spe",
-  "integrator": {
-   "kind": "rkc",
-   "tolerance": 0.01,
-   "t_end": 0.02,
-   "dt0": 1e-05,
-   "max_stages": 200
-  },
-  "solver": {
-   "preconditioner": "amg",
-   "rel_tol": 1e-12,
-   "max_iter": 500
-  },
-  "estimator": {
-   "mode": "spe",
-   "window": 8
-  },
-  "probes": [
-   [
-    0.005,
-    0.005,
-    0.01
-   ]
-  ],
-  "output": {
-   "metrics_csv": "metrics.csv",
-   "probe_csv": "probe.csv",
-   "solves_csv": ""
-  },
-  "workers": 1
- },
- "slab_order2_rkc": {
-  "mesh": {
-   "box": {
-    "nx": 5,
-    "ny": 5,
-    "nz": 10,
-    "lx": 0.005,
-    "ly": 0.005,
-    "lz": 0.01,
-    "z_planes": [
-     0.005
-    ],
-    "regions": [
-     1,
-     2
-    ]
-   }
-  },
-  "order": 2,
-  "materials": {
-   "1": {
-    "eps_r": 2.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 1e-08
-    }
-   },
-   "2": {
-    "eps_r": 5.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 5e-09
-    }
-   }
-  },
-  "excitations": {
-   "hv": {
-    "kind": "sinusoid",
-    "amplitude": 10000.0,
-    "frequency": 50.0,
-    "phase": 0.0
-   },
-   "ground": {
-    "kind": "constant",
-    "value": 0.0
-   }
-  },
-  "name": "slab_order2_rkc",
-  "integrator": {
-   "kind": "rkc",
-   "tolerance": 0.01,
-   "t_end": 0.02,
-   "dt0": 1e-05,
-   "max_stages": 200
-  },
-  "solver": {
-   "preconditioner": "amg",
-   "rel_tol": 1e-12,
-   "max_iter": 500
-  },
-  "estimator": {
-   "mode": "zero"
-  },
-  "probes": [
-   [
-    0.0025,
-    0.0025,
-    0.005
-   ]
-  ],
-  "output": {
-   "metrics_csv": "metrics.csv",
-   "probe_csv": "probe.csv",
-   "solves_csv": ""
-  },
-  "workers": 1
- },
- "slab_linear_euler": {
-  "mesh": {
-   "box": {
-    "nx": 10,
-    "ny": 10,
-    "nz": 20,
-    "lx": 0.01,
-    "ly": 0.01,
-    "lz": 0.02,
-    "z_planes": [
-     0.01
-    ],
-    "regions": [
-     1,
-     2
-    ]
-   }
-  },
-  "order": 1,
-  "materials": {
-   "1": {
-    "eps_r": 2.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 1e-08
-    }
-   },
-   "2": {
-    "eps_r": 5.0,
-    "conductivity": {
-     "kind": "constant",
-     "kappa": 5e-09
-    }
-   }
-  },
-  "excitations": {
-   "hv": {
-    "kind": "sinusoid",
-    "amplitude": 10000.0,
-    "frequency": 50.0,
-    "phase": 0.0
-   },
-   "ground": {
-    "kind": "constant",
-    "value": 0.0
-   }
-  },
-  "name": "slab_linear_euler",
-  "integrator": {
-   "kind": "euler",
-   "tolerance": 0.01,
-   "t_end": 0.02,
-   "dt0": 0.0005,
-   "max_stages": 200
-  },
-  "solver": {
-   "preconditioner": "amg",
-   "rel_tol": 1e-12,
-   "max_iter": 500
-  },
-  "estimator": {
-   "mode": "zero"
-  },
-  "probes": [
-   [
-    0.005,
-    0.005,
-    0.01
-   ]
-  ],
-  "output": {
-   "metrics_csv": "metrics.csv",
-   "probe_csv": "probe.csv",
-   "solves_csv": ""
-  },
-  "workers": 1
- }
-})
 
 
 TINY_SLAB = {  # proj/tests/test_scenario.cpp:21-39 (tiny_slab_json)

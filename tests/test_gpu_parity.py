@@ -211,6 +211,23 @@ def test_repeat_runs_bit_identical():  # test_scenario.cpp:133-154
     assert np.array_equal(out[0], out[1])
 
 
+def test_incremental_spe_matches_full_rebuild():
+    """The incremental SPE basis (append + Givens downdate) spans the same window
+    as the reference's full MGS rebuild: same start vectors up to rounding, hence
+    the same iteration counts and potentials."""
+    out = {}
+    for incremental in (1, 0):
+        g = eb.FemSystem(cube(12, jitter=0.1, estimator="spe"))
+        g.set_option(9, incremental)
+        x0 = 2e4 * po.random_vec(g.n_free, 31)
+        g.set_state(0.0, x0, 0.0)
+        g.rkc_advance_fixed(1e-4, 4, 4)  # 16 solves: the 8-window slides 8 times
+        out[incremental] = (g.get_state()[0], g.stats()["pcg_iterations"])
+    (xi, it_i), (xf, it_f) = out[1], out[0]
+    assert abs(it_i - it_f) <= 2
+    assert np.linalg.norm(xi - xf) <= 1e-10 * np.linalg.norm(xf)
+
+
 def test_nan_field_maps_to_invalid_argument():  # materials.cpp:26 quirk (exit code 1)
     cfg = cube(4)
     g = eb.FemSystem(cfg)
