@@ -166,6 +166,31 @@ int eqs_create_from_config(const char* json_text, int device, eqs_ctx** out);
 void eqs_destroy(eqs_ctx* ctx);
 int eqs_get_sizes(eqs_ctx* ctx, eqs_sizes* out);
 
+/* ----------------------------------------------------------------- distributed (node ownership) */
+/* One process per GPU: rank 0 calls eqs_nccl_unique_id (128 bytes), shares
+ * it (e.g. torch.distributed broadcast), then every rank calls
+ * eqs_create_distributed. Host vectors of a distributed context are the
+ * owned part (eqs_get_owned). */
+int eqs_nccl_unique_id(char* id128);
+int eqs_create_distributed(const char* json_text, int device, int nranks, int rank, const char* id128,
+                           eqs_ctx** out);
+/* nranks virtual ranks in one process (threads, device-to-device halos);
+ * every later call on these contexts must be made concurrently from one
+ * thread per rank. Used to test the partitioned path on a single GPU. */
+int eqs_create_virtual_group(const char* json_text, int device, int nranks, eqs_ctx** out);
+/* host-only partition plan of `rank` (no device, no collectives) */
+int eqs_create_partition_host(const char* json_text, int nranks, int rank, eqs_ctx** out);
+/* partition of the context's rank: info = {rank, nranks, levels, n_own(level 0)} */
+int eqs_partition_info(eqs_ctx* ctx, long* info4);
+/* level sizes {n_global, n_own, n_ghost, n_peers_recv, n_peers_send, n_local_tets, n_local_fixed} */
+int eqs_partition_level(eqs_ctx* ctx, int level, long* info7);
+/* owner rank per global index of a level; owned / ghost global ids of this rank */
+int eqs_partition_owner(eqs_ctx* ctx, int level, int* owner);
+int eqs_partition_owned(eqs_ctx* ctx, int level, int* ids);
+int eqs_partition_ghosts(eqs_ctx* ctx, int level, int* ids);
+/* global ids this rank sends to `peer` at a level, in the peer's ghost order (returns count) */
+int eqs_partition_send(eqs_ctx* ctx, int level, int peer, int* ids, int* count);
+
 /* ----------------------------------------------------------------- setup artefacts (bit-exact checks) */
 /* color_elements (proj/src/matfree.cpp:11-38): colour of every tet. */
 int eqs_get_colors(eqs_ctx* ctx, int* color_of_tet);

@@ -7,6 +7,8 @@
 #include <memory>
 #include <random>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "eqs_b200.h"
 #include "gpu_system.hpp"
@@ -167,6 +169,123 @@ int eqs_create_from_config(const char* json_text, int device, eqs_ctx** out) {
 }
 
 void eqs_destroy(eqs_ctx* ctx) { delete ctx; }
+
+int eqs_nccl_unique_id(char* id128) {
+  return guard([&] {
+    const std::string id = nccl_unique_id();
+    std::memcpy(id128, id.data(), id.size());
+  });
+}
+
+int eqs_create_distributed(const char* json_text, int device, int nranks, int rank, const char* id128,
+                           eqs_ctx** out) {
+  return guard([&] {
+    if (!json_text || !out || !id128) throw std::invalid_argument("eqs_create_distributed: null argument");
+    SimConfig c = parse_config(json_text);
+    std::unique_ptr<Comm> comm;
+    if (nranks > 1) {
+      cuda_check(cudaSetDevice(device), "cudaSetDevice");
+      comm = make_nccl_comm(std::string(id128, 128), nranks, rank);
+    }
+    auto ctx = std::make_unique<eqs_ctx>();
+    ctx->sys = std::make_unique<GpuSystem>(build_problem(c), device, std::move(comm));
+    *out = ctx.release();
+  });
+}
+
+int eqs_create_virtual_group(const char* json_text, int device, int nranks, eqs_ctx** out) {
+  return guard([&] {
+    if (!json_text || !out || nranks < 1) throw std::invalid_argument("eqs_create_virtual_group: bad argument");
+    SimConfig c = parse_config(json_text);
+    auto group = make_thread_group(nranks);
+    std::vector<std::unique_ptr<eqs_ctx>> ctx(nranks);
+    std::vector<std::string> err(nranks);
+    std::vector<std::thread> th;
+    for (int r = 0; r < nranks; ++r)
+      th.emplace_back([&, r] {
+        try {
+          ctx[r] = std::make_unique<eqs_ctx>();
+          ctx[r]->sys = std::make_unique<GpuSystem>(build_problem(c), device, make_thread_comm(group, r));
+        } catch (const std::exception& e) {
+          err[r] = e.what();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int r = 0; r < nranks; ++r)
+      if (!err[r].empty()) throw std::runtime_error("virtual rank " + std::to_string(r) + ": " + err[r]);
+    for (int r = 0; r < nranks; ++r) out[r] = ctx[r].release();
+  });
+}
+
+int eqs_create_partition_host(const char* json_text, int nranks, int rank, eqs_ctx** out) {
+  return guard([&] {
+    SimConfig c = parse_config(json_text);
+    auto ctx = std::make_unique<eqs_ctx>();
+    ctx->sys = std::make_unique<GpuSystem>(build_problem(c), -1, std::make_unique<StaticComm>(rank, nranks));
+    *out = ctx.release();
+  });
+}
+
+int eqs_partition_info(eqs_ctx* ctx, long* info) {
+  return guard([&] {
+    const PartitionPlan& p = H(ctx).plan();
+    info[0] = p.rank;
+    info[1] = p.nranks;
+    info[2] = (long)p.space.size();
+    info[3] = p.space[0].n_own();
+  });
+}
+
+int eqs_partition_level(eqs_ctx* ctx, int level, long* info) {
+  return guard([&] {
+    const PartitionPlan& p = H(ctx).plan();
+    if (level < 0 || level >= (int)p.space.size()) throw std::invalid_argument("eqs_partition_level: bad level");
+    const LocalSpace& s = p.space[level];
+    info[0] = s.n_global;
+    info[1] = s.n_own();
+    info[2] = s.n_ghost();
+    info[3] = (long)s.recv_ranks.size();
+    info[4] = (long)s.send_ranks.size();
+    info[5] = (long)p.tets.size();
+    info[6] = (long)p.fixed.size();
+  });
+}
+
+int eqs_partition_owner(eqs_ctx* ctx, int level, int* owner) {
+  return guard([&] {
+    const PartitionPlan& p = H(ctx).plan();
+    if (level < 0 || level >= (int)p.owner.size()) throw std::invalid_argument("eqs_partition_owner: bad level");
+    std::memcpy(owner, p.owner[level].data(), sizeof(int) * p.owner[level].size());
+  });
+}
+
+int eqs_partition_owned(eqs_ctx* ctx, int level, int* ids) {
+  return guard([&] {
+    const LocalSpace& s = H(ctx).plan().space.at(level);
+    std::memcpy(ids, s.owned.data(), sizeof(int) * s.owned.size());
+  });
+}
+
+int eqs_partition_ghosts(eqs_ctx* ctx, int level, int* ids) {
+  return guard([&] {
+    const LocalSpace& s = H(ctx).plan().space.at(level);
+    std::memcpy(ids, s.ghosts.data(), sizeof(int) * s.ghosts.size());
+  });
+}
+
+int eqs_partition_send(eqs_ctx* ctx, int level, int peer, int* ids, int* count) {
+  return guard([&] {
+    const LocalSpace& s = H(ctx).plan().space.at(level);
+    *count = 0;
+    for (size_t k = 0; k < s.send_ranks.size(); ++k)
+      if (s.send_ranks[k] == peer) {
+        const auto& l = s.send_local[k];
+        if (ids)
+          for (size_t i = 0; i < l.size(); ++i) ids[i] = s.owned[l[i]];
+        *count = (int)l.size();
+      }
+  });
+}
 
 int eqs_get_sizes(eqs_ctx* ctx, eqs_sizes* o) {
   return guard([&] {

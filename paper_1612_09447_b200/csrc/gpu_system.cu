@@ -1,16 +1,19 @@
-// GpuSystem: device-resident FemSystem + integrator (DESIGN.md §2-§5).
+// GpuSystem: device-resident FemSystem + integrator (DESIGN.md §2-§6).
 //
-// Device dof numbering: free dofs first (in DofMap::free_dofs order), then the
-// fixed dofs. A "full" vector therefore holds the free state in [0, n_free)
-// and the Dirichlet values in the tail, so lifting a stage vector
-// (DofMap::lift, proj/src/dofmap.cpp:11-15) is a write of n_fixed entries and
-// restricting (restrict_free, :17-20) is free.
+// Local numbering of the fine dofs on a rank: [owned free | ghost free |
+// local fixed]. A "full" vector holds the owned state, room for the ghosts
+// that a halo exchange fills, and the Dirichlet values of the fixed dofs used
+// by the local tets, so lifting a stage vector (DofMap::lift,
+// proj/src/dofmap.cpp:11-15) is a write of the fixed tail and restricting
+// (restrict_free, :17-20) is free. With one rank the owned set is every free
+// dof in DofMap::free_dofs order and there are no ghosts.
 #include "gpu_system.hpp"
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <random>
 
 namespace eqsb {
@@ -40,6 +43,7 @@ void DevBuf<T>::download(T* host, size_t count, cudaStream_t s) const {
   if (count) CK(cudaMemcpyAsync(host, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
 }
 template struct DevBuf<double>;
+template struct DevBuf<float>;
 template struct DevBuf<int>;
 template struct DevBuf<long>;
 template struct DevBuf<unsigned>;
@@ -68,7 +72,7 @@ void upload_csr(const HostCsr& h, DevCsr& d, DevBuf<int>& rp, DevBuf<int>& ci, D
   d.n_rows = h.n_rows;
   d.n_cols = h.n_cols;
   d.nnz = h.nnz();
-  rp.alloc(h.row_ptr.size());
+  rp.alloc(std::max<size_t>(1, h.row_ptr.size()));
   ci.alloc(std::max<size_t>(1, h.col_idx.size()));
   v.alloc(std::max<size_t>(1, h.values.size()));
   rp.upload(h.row_ptr.data(), h.row_ptr.size(), s);
@@ -77,9 +81,11 @@ void upload_csr(const HostCsr& h, DevCsr& d, DevBuf<int>& rp, DevBuf<int>& ci, D
   d.row_ptr = rp.p;
   d.col_idx = ci.p;
   d.values = v.p;
+  d.values_f = nullptr;
   d.tpr = choose_tpr(h);
 }
 
+// 1/diag of the owned rows (local row i <-> local column i)
 std::vector<double> inv_diagonal(const HostCsr& a) {
   std::vector<double> d(a.n_rows, 0.0);
   for (int i = 0; i < a.n_rows; ++i)
@@ -89,7 +95,8 @@ std::vector<double> inv_diagonal(const HostCsr& a) {
 }
 }  // namespace
 
-GpuSystem::GpuSystem(Problem&& p, int device) : prob_(std::move(p)), device_(device) {
+GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
+    : prob_(std::move(p)), device_(device), comm_(comm ? std::move(comm) : std::make_unique<SelfComm>()) {
   PhaseTimer timer(stats_.t_setup);
   if (device_ >= 0) {
     CK(cudaSetDevice(device_));
@@ -109,17 +116,32 @@ GpuSystem::GpuSystem(Problem&& p, int device) : prob_(std::move(p)), device_(dev
   for (int t = 0; t < n_tets_; ++t)
     if (!prob_.materials.count(prob_.mesh.region[t]))
       throw ConfigError("no material for region " + std::to_string(prob_.mesh.region[t]));
-  dev2ref_.resize(n_dofs_);
-  ref2dev_.resize(n_dofs_);
-  for (int i = 0; i < n_free_; ++i) dev2ref_[i] = dm.free_dofs[i];
-  for (int i = 0; i < n_fixed_; ++i) dev2ref_[n_free_ + i] = dm.fixed_dofs[i];
-  for (int k = 0; k < n_dofs_; ++k) ref2dev_[dev2ref_[k]] = k;
   // FemSystem ctor: assemble M once (fem_system.cpp:27-36)
   assemble_mass_blocks(prob_, m_ii_, m_ib_);
   ++stats_.assemblies;
   // mass preconditioner (built once; the reference builds it lazily on first use, fem_system.cpp:48-54)
   if (prob_.solver.precond == 2) amg_ = build_amg(m_ii_, prob_.solver);
   ++stats_.precond_setups;
+  // V-cycle operators of the coarse levels: lumped filtered Galerkin matrices
+  // (DESIGN.md §4); the hierarchy reported through the API stays the reference's
+  AmgHierarchy vh;
+  if (prob_.solver.precond == 2) {
+    vh = amg_;
+    const double eps = prob_.solver.amg_coarse_filter;
+    for (size_t l = 1; l + 1 < vh.levels.size(); ++l)
+      if (eps > 0.0) vh.levels[l].A = filter_lumped(amg_.levels[l].A, eps);
+  }
+  plan_ = build_plan(prob_, m_ii_, m_ib_, vh, comm_->size(), comm_->rank());
+  const LocalSpace& s0 = plan_.space[0];
+  n_own_ = s0.n_own();
+  n_ghost_ = s0.n_ghost();
+  n_loc_ = s0.n_local();
+  n_fixloc_ = (int)plan_.fixed.size();
+  n_full_ = n_loc_ + n_fixloc_;
+  n_tets_loc_ = (int)plan_.tets.size();
+  loc2ref_.assign(n_full_, -1);
+  for (int i = 0; i < n_loc_; ++i) loc2ref_[i] = dm.free_dofs[i < n_own_ ? s0.owned[i] : s0.ghosts[i - n_own_]];
+  for (int j = 0; j < n_fixloc_; ++j) loc2ref_[n_loc_ + j] = plan_.fixed[j];
   if (device_ >= 0) build_device();  // device < 0: host-only setup (artefact checks without a GPU)
 }
 
@@ -134,25 +156,72 @@ GpuSystem::~GpuSystem() {
   if (stream_) cudaStreamDestroy(stream_);
 }
 
+void GpuSystem::require_single(const char* what) const {
+  if (comm_->size() != 1)
+    throw std::invalid_argument(std::string(what) + ": host-vector API needs a single-rank context");
+}
+
+void GpuSystem::build_halo(const LocalSpace& sp, DevHalo& h) {
+  h.n_own = sp.n_own();
+  std::map<int, std::pair<int, int>> rel;  // peer -> (send index, recv index)
+  for (size_t k = 0; k < sp.send_ranks.size(); ++k) rel[sp.send_ranks[k]].first = (int)k + 1;
+  for (size_t k = 0; k < sp.recv_ranks.size(); ++k) rel[sp.recv_ranks[k]].second = (int)k + 1;
+  std::vector<int> idx;
+  for (auto& [peer, sr] : rel) {
+    h.peers.push_back(peer);
+    h.send_off.push_back((int)idx.size());
+    if (sr.first) {
+      const auto& l = sp.send_local[sr.first - 1];
+      idx.insert(idx.end(), l.begin(), l.end());
+      h.send_cnt.push_back((int)l.size());
+    } else {
+      h.send_cnt.push_back(0);
+    }
+    if (sr.second) {
+      h.recv_off.push_back(sp.recv_off[sr.second - 1]);
+      h.recv_cnt.push_back(sp.recv_off[sr.second] - sp.recv_off[sr.second - 1]);
+    } else {
+      h.recv_off.push_back(0);
+      h.recv_cnt.push_back(0);
+    }
+  }
+  h.n_send = (int)idx.size();
+  h.send_idx.alloc(std::max<size_t>(1, idx.size()));
+  h.send_idx.upload(idx.data(), idx.size(), stream_);
+  h.send_buf.alloc(std::max<size_t>(1, idx.size()));
+  CK(cudaStreamSynchronize(stream_));
+}
+
+void GpuSystem::halo(DevHalo& h, double* vec) {
+  if (comm_->size() == 1 || h.peers.empty()) return;
+  launch_gather(h.n_send, h.send_idx.p, vec, h.send_buf.p, stream_);
+  std::vector<HaloMsg> msgs;
+  for (size_t k = 0; k < h.peers.size(); ++k)
+    msgs.push_back({h.peers[k], h.send_buf.p + h.send_off[k], h.send_cnt[k], vec + h.n_own + h.recv_off[k],
+                    h.recv_cnt[k]});
+  comm_->exchange(msgs, stream_);
+}
+
+void GpuSystem::allreduce(int slot, int count) {
+  if (comm_->size() > 1) comm_->allreduce(red_scal_.p + slot, count, stream_);
+}
+
 void GpuSystem::build_device() {
   const Dofs& dm = prob_.dm;
   const Mesh& mesh = prob_.mesh;
   cudaStream_t s = stream_;
-  // coordinates per device dof (vertex dofs = nodes; P2 edge dofs = midpoints, unused by K1)
+  // coordinates per local dof (vertex dofs = nodes; P2 edge dofs unused by K1)
   {
-    std::vector<double> c((size_t)n_dofs_ * 4, 0.0);
-    std::vector<std::array<double, 3>> dc(n_dofs_);
-    for (int n = 0; n < mesh.n_nodes; ++n) dc[n] = {mesh.nodes[3L * n], mesh.nodes[3L * n + 1], mesh.nodes[3L * n + 2]};
-    for (int k = 0; k < n_dofs_; ++k) {
-      const int r = dev2ref_[k];
-      if (r < mesh.n_nodes)
-        for (int d = 0; d < 3; ++d) c[4L * k + d] = dc[r][d];
+    std::vector<double> c((size_t)std::max(1, n_full_) * 4, 0.0);
+    for (int k = 0; k < n_full_; ++k) {
+      const int r = loc2ref_[k];
+      if (r >= 0 && r < mesh.n_nodes)
+        for (int d = 0; d < 3; ++d) c[4L * k + d] = mesh.nodes[3L * r + d];
     }
     coords_.alloc(c.size());
     coords_.upload(c.data(), c.size(), s);
     CK(cudaStreamSynchronize(s));
   }
-  // connectivity in device numbering + material index
   std::map<int, int> mat_index;
   std::vector<DevMaterial> mats;
   for (const auto& [region, m] : prob_.materials) {
@@ -170,47 +239,45 @@ void GpuSystem::build_device() {
   }
   set_materials(mats.data(), (int)mats.size(), s);
   {
-    std::vector<int> td((size_t)n_tets_ * n_local_);
-    std::vector<unsigned char> tm(n_tets_);
-#pragma omp parallel for schedule(static)
-    for (long t = 0; t < n_tets_; ++t) {
-      for (int i = 0; i < n_local_; ++i) td[t * n_local_ + i] = ref2dev_[dm.element_dofs[t * n_local_ + i]];
-      tm[t] = (unsigned char)mat_index.at(mesh.region[t]);
-    }
-    tet_dofs_.alloc(td.size());
+    const std::vector<int>& td = plan_.tet_dofs;
+    std::vector<unsigned char> tm(n_tets_loc_);
+    for (int k = 0; k < n_tets_loc_; ++k) tm[k] = (unsigned char)mat_index.at(mesh.region[plan_.tets[k]]);
+    tet_dofs_.alloc(std::max<size_t>(1, td.size()));
     tet_dofs_.upload(td.data(), td.size(), s);
-    tet_mat_.alloc(tm.size());
+    tet_mat_.alloc(std::max<size_t>(1, tm.size()));
     tet_mat_.upload(tm.data(), tm.size(), s);
-    // slot lists: device dof -> (t * n_local + i), ascending t
-    std::vector<long> ptr((size_t)n_dofs_ + 1, 0);
+    // slot lists: local dof -> (local tet * n_local + i), ascending tet
+    std::vector<long> ptr((size_t)n_full_ + 1, 0);
     for (size_t k = 0; k < td.size(); ++k) ++ptr[td[k] + 1];
-    for (int d = 0; d < n_dofs_; ++d) ptr[d + 1] += ptr[d];
+    for (int d = 0; d < n_full_; ++d) ptr[d + 1] += ptr[d];
     if (ptr.back() >= (1L << 31)) throw ConfigError("mesh too large for int32 slot indices");
-    std::vector<int> sl(ptr.back());
+    std::vector<int> sl(std::max<long>(1, ptr.back()));
     std::vector<long> next(ptr.begin(), ptr.end() - 1);
     for (size_t k = 0; k < td.size(); ++k) sl[next[td[k]]++] = (int)k;
     slot_ptr_.alloc(ptr.size());
     slot_ptr_.upload(ptr.data(), ptr.size(), s);
     slots_.alloc(sl.size());
     slots_.upload(sl.data(), sl.size(), s);
-    ytet_.alloc((size_t)n_tets_ * n_local_);
+    ytet_.alloc(std::max<size_t>(1, td.size()));
     CK(cudaStreamSynchronize(s));
   }
   err_.alloc(4);
   CK(cudaMemsetAsync(err_.p, 0, 4 * sizeof(int), s));
-  // Dirichlet data: set of every fixed dof; compressed M_IB rows per set
+  // Dirichlet data: set of every local fixed dof; compressed M_IB rows (owned) per set
   {
-    std::vector<int> sof(std::max(1, n_fixed_));
-    for (int i = 0; i < n_fixed_; ++i) sof[i] = dm.fixed_set[dm.fixed_dofs[i]];
+    std::vector<int> sof(std::max(1, n_fixloc_));
+    for (int j = 0; j < n_fixloc_; ++j) sof[j] = dm.fixed_set[plan_.fixed[j]];
     set_of_fixed_.alloc(sof.size());
     set_of_fixed_.upload(sof.data(), sof.size(), s);
+    const HostCsr& mib = plan_.mib;
     std::vector<int> rows;
     std::vector<double> coef;
-    for (int r = 0; r < m_ib_.n_rows; ++r) {
-      if (m_ib_.row_ptr[r] == m_ib_.row_ptr[r + 1]) continue;
+    for (int r = 0; r < mib.n_rows; ++r) {
+      if (mib.row_ptr[r] == mib.row_ptr[r + 1]) continue;
       rows.push_back(r);
       std::vector<double> c(n_sets_, 0.0);
-      for (int k = m_ib_.row_ptr[r]; k < m_ib_.row_ptr[r + 1]; ++k) c[sof[m_ib_.col_idx[k]]] += m_ib_.values[k];
+      for (int k = mib.row_ptr[r]; k < mib.row_ptr[r + 1]; ++k)
+        c[dm.fixed_set[dm.fixed_dofs[mib.col_idx[k]]]] += mib.values[k];
       coef.insert(coef.end(), c.begin(), c.end());
     }
     n_bl_rows_ = (int)rows.size();
@@ -220,61 +287,17 @@ void GpuSystem::build_device() {
     bl_coef_.upload(coef.data(), coef.size(), s);
     CK(cudaStreamSynchronize(s));
   }
-  // M_II
-  upload_csr(m_ii_, mii_, mii_rp_, mii_ci_, mii_v_, s);
+  // M_II (owned rows, local columns) + level-0 halo
+  upload_csr(plan_.mii, mii_, mii_rp_, mii_ci_, mii_v_, s);
+  build_halo(plan_.space[0], halo0_);
   {
-    const std::vector<double> invd = inv_diagonal(m_ii_);
+    std::vector<double> invd = inv_diagonal(plan_.mii);
     for (double v : invd)
       if (!std::isfinite(v)) throw NumericalError("Jacobi: zero diagonal");
-    mii_invd_.alloc(std::max(1, n_free_));
+    invd.resize(std::max(1, n_loc_), 0.0);
+    mii_invd_.alloc(invd.size());
     mii_invd_.upload(invd.data(), invd.size(), s);
-  }
-  // AMG hierarchy
-  if (prob_.solver.precond == 2) {
-    const int L = (int)amg_.levels.size();
-    levels_.resize(L);
-    auto f32 = [&](const std::vector<double>& v, DevBuf<float>& out) {
-      std::vector<float> f(v.begin(), v.end());
-      out.alloc(std::max<size_t>(1, f.size()));
-      out.upload(f.data(), f.size(), s);
-      CK(cudaStreamSynchronize(s));
-    };
-    const double eps = prob_.solver.amg_coarse_filter;
-    for (int l = 0; l < L; ++l) {
-      DevLevel& lv = levels_[l];
-      const AmgHostLevel& hl = amg_.levels[l];
-      // V-cycle operator: the fine level uses M_II itself; coarse levels use the
-      // lumped filtered Galerkin operator
-      HostCsr filtered;
-      const bool filt = l > 0 && l + 1 < L && eps > 0.0;
-      if (filt) filtered = filter_lumped(hl.A, eps);
-      const HostCsr& av = filt ? filtered : hl.A;
-      if (l == 0) {
-        lv.A = mii_;  // shares indices / fp64 values with the PCG operator
-      } else {
-        upload_csr(av, lv.A, lv.a_rp, lv.a_ci, lv.a_v, s);
-      }
-      const int n = hl.A.n_rows;
-      if (l + 1 < L) {
-        f32(av.values, lv.a_vf);
-        upload_csr(hl.P, lv.P, lv.p_rp, lv.p_ci, lv.p_v, s);
-        upload_csr(hl.R, lv.R, lv.r_rp, lv.r_ci, lv.r_v, s);
-        f32(hl.P.values, lv.p_vf);
-        f32(hl.R.values, lv.r_vf);
-        const std::vector<double> invd = inv_diagonal(av);
-        lv.invd.alloc(n);
-        lv.invd.upload(invd.data(), n, s);
-        lv.t.alloc(n);
-        lv.z2.alloc(std::max(1, n));
-      }
-      lv.z.alloc(std::max(1, n));
-      if (l > 0) lv.b.alloc(std::max(1, n));
-      CK(cudaStreamSynchronize(s));
-    }
-    set_vcycle_fp32(vcycle_fp32_);
-    coarse_n_ = amg_.coarse_n;
-    coarse_inv_.alloc(amg_.coarse_inverse.size());
-    coarse_inv_.upload(amg_.coarse_inverse.data(), amg_.coarse_inverse.size(), s);
+    halo(halo0_, mii_invd_.p);
   }
   // reductions + work vectors
   red_partials_.alloc((size_t)S_COUNT * kRedGrid);
@@ -283,49 +306,116 @@ void GpuSystem::build_device() {
   CK(cudaMemsetAsync(red_counters_.p, 0, sizeof(unsigned) * S_COUNT, s));
   CK(cudaMemsetAsync(red_scal_.p, 0, sizeof(double) * S_COUNT, s));
   red_ = Reducer{red_partials_.p, red_counters_.p, red_scal_.p};
-  const size_t nf = std::max(1, n_free_), nd = std::max(1, n_dofs_);
-  for (auto* b : {&w_r_, &w_z_, &w_p_, &w_q_, &w_free_a_, &w_free_b_, &F0_, &F_, &Fn_, &rho_v_, &rho_w_}) b->alloc(nf);
-  for (auto* b : {&w_full_a_, &w_full_b_}) b->alloc(nd);
+  const size_t nl = std::max(1, n_loc_), nf = std::max(1, n_full_);
+  for (auto* b : {&w_r_, &w_z_, &w_p_, &w_q_, &w_free_a_, &w_free_b_, &F0_, &F_, &Fn_, &rho_v_, &rho_w_}) b->alloc(nl);
+  for (auto* b : {&w_full_a_, &w_full_b_}) b->alloc(nf);
   for (auto& b : full_) {
-    b.alloc(nd);
-    launch_fill((long)nd, 0.0, b.p, s);
+    b.alloc(nf);
+    launch_fill((long)nf, 0.0, b.p, s);
   }
   X_ = full_[0].p;
   CK(cudaStreamSynchronize(s));
-  // smoother bounds: lambda_max(D^-1 A) per level by 20 device power iterations
-  if (prob_.solver.precond == 2) {
-    std::mt19937 rng(12345u);
-    std::uniform_real_distribution<double> uni(-1.0, 1.0);
-    for (int l = 0; l + 1 < (int)levels_.size(); ++l) {
-      DevLevel& lv = levels_[l];
-      const int n = lv.A.n_rows;
-      std::vector<double> v(n);
-      double nrm = 0.0;
-      for (auto& e : v) {
-        e = uni(rng);
-        nrm += e * e;
-      }
-      nrm = std::sqrt(nrm);
-      for (auto& e : v) e /= nrm;
-      lv.z.upload(v.data(), n, s);
-      double lam = 1.0;
-      for (int it = 0; it < 20; ++it) {
-        launch_scaled_spmv(lv.A, lv.invd.p, lv.z.p, lv.t.p, s);
-        launch_dot(n, lv.t.p, lv.t.p, red_, S_NORM, s);
-        lam = std::sqrt(read_scalar(S_NORM));
-        if (lam == 0.0) {
-          lam = 1.0;
-          break;
-        }
-        launch_scale(n, 1.0 / lam, lv.t.p, lv.z.p, s);
-      }
-      // level 0 operator == the hierarchy's A_0: also use the setup's 10-step estimate
-      lv.lambda_smoother = l == 0 ? std::max(lam, amg_.levels[l].lambda_max_scaled) : lam;
-    }
-    set_cheb(cheb_ratio);
-  }
+  if (prob_.solver.precond == 2) build_levels();
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
+}
+
+// AMG levels on this rank: owned rows of A_l (level 0: M_II; coarse levels:
+// the lumped filtered operator), P_l, R_l, fp32 copies, halos, and the
+// replicated dense coarsest solve.
+void GpuSystem::build_levels() {
+  cudaStream_t s = stream_;
+  const int L = (int)amg_.levels.size();
+  levels_.clear();
+  levels_.resize(L);
+  auto f32 = [&](const std::vector<double>& v, DevBuf<float>& out) {
+    std::vector<float> f(v.begin(), v.end());
+    out.alloc(std::max<size_t>(1, f.size()));
+    out.upload(f.data(), f.size(), s);
+    CK(cudaStreamSynchronize(s));
+  };
+  for (int l = 0; l < L; ++l) {
+    DevLevel& lv = levels_[l];
+    const LocalSpace& sp = plan_.space[l];
+    lv.n_own = sp.n_own();
+    lv.n_loc = sp.n_local();
+    lv.n_global = sp.n_global;
+    if (l == 0) {
+      lv.A = mii_;  // shares indices / fp64 values with the PCG operator
+    } else {
+      upload_csr(plan_.A[l], lv.A, lv.a_rp, lv.a_ci, lv.a_v, s);
+    }
+    build_halo(sp, lv.halo);
+    const size_t nloc = std::max(1, lv.n_loc);
+    lv.z.alloc(nloc);
+    lv.b.alloc(nloc);
+    lv.t.alloc(nloc);
+    lv.z2.alloc(nloc);
+    if (l + 1 < L) {
+      f32(plan_.A[l].values, lv.a_vf);
+      upload_csr(plan_.P[l], lv.P, lv.p_rp, lv.p_ci, lv.p_v, s);
+      upload_csr(plan_.R[l], lv.R, lv.r_rp, lv.r_ci, lv.r_v, s);
+      f32(plan_.P[l].values, lv.p_vf);
+      f32(plan_.R[l].values, lv.r_vf);
+      std::vector<double> invd = inv_diagonal(plan_.A[l]);
+      invd.resize(nloc, 0.0);
+      lv.invd.alloc(nloc);
+      lv.invd.upload(invd.data(), invd.size(), s);
+      halo(lv.halo, lv.invd.p);
+    } else {
+      // coarsest: every rank solves the (<= coarse_limit) dense system on the full vector
+      std::vector<int> glob(nloc, 0);
+      for (int i = 0; i < lv.n_loc; ++i) glob[i] = i < lv.n_own ? sp.owned[i] : sp.ghosts[i - lv.n_own];
+      lv.glob.alloc(glob.size());
+      lv.glob.upload(glob.data(), glob.size(), s);
+      lv.full_b.alloc(std::max(1, sp.n_global));
+      lv.full_z.alloc(std::max(1, sp.n_global));
+    }
+    CK(cudaStreamSynchronize(s));
+  }
+  coarse_n_ = amg_.coarse_n;
+  coarse_inv_.alloc(amg_.coarse_inverse.size());
+  coarse_inv_.upload(amg_.coarse_inverse.data(), amg_.coarse_inverse.size(), s);
+  set_vcycle_fp32(vcycle_fp32_);
+  // smoother bounds: lambda_max(D^-1 A_l) by 20 power iterations from a
+  // global random vector (same on every rank), norms reduced over ranks
+  std::mt19937 rng(12345u);
+  std::uniform_real_distribution<double> uni(-1.0, 1.0);
+  for (int l = 0; l + 1 < L; ++l) {
+    DevLevel& lv = levels_[l];
+    const LocalSpace& sp = plan_.space[l];
+    std::vector<double> g(sp.n_global);
+    double nrm = 0.0;
+    for (auto& e : g) {
+      e = uni(rng);
+      nrm += e * e;
+    }
+    nrm = std::sqrt(nrm);
+    std::vector<double> v(std::max(1, lv.n_loc), 0.0);
+    for (int i = 0; i < lv.n_own; ++i) v[i] = g[sp.owned[i]] / nrm;
+    lv.z.upload(v.data(), v.size(), s);
+    double lam = 1.0;
+    for (int it = 0; it < 20; ++it) {
+      halo(lv.halo, lv.z.p);
+      launch_scaled_spmv(lv.A, lv.invd.p, lv.z.p, lv.t.p, s);
+      lam = std::sqrt(dot_n(lv.n_own, lv.t.p, lv.t.p, S_NORM));
+      if (lam == 0.0) {
+        lam = 1.0;
+        break;
+      }
+      launch_scale(lv.n_own, 1.0 / lam, lv.t.p, lv.z.p, s);
+    }
+    // level 0 operator == the hierarchy's A_0: also use the setup's 10-step estimate
+    lv.lambda_smoother = l == 0 ? std::max(lam, amg_.levels[l].lambda_max_scaled) : lam;
+  }
+  set_cheb(cheb_ratio);
+}
+
+// global dot over n owned entries (reduced over ranks), read on the host
+double GpuSystem::dot_n(int n, const double* a, const double* b, int slot) {
+  launch_dot(n, a, b, red_, slot, stream_);
+  allreduce(slot);
+  return read_scalar(slot);
 }
 
 // Chebyshev smoother on [lmax/ratio, lmax] of D^-1 A, lmax = 1.1 x the power
@@ -440,7 +530,7 @@ void GpuSystem::toc(int cls, double bytes) {
   (void)cls;
   cudaEvent_t b = get_event();
   CK(cudaEventRecord(b, stream_));
-  events_.push_back({open_ev_, b, cls, bytes});
+  events_.push_back({open_ev_, b, open_cls_, bytes});
   open_cls_ = -1;
   if (events_.size() > 4096) {
     double ms[TC_COUNT];
@@ -476,10 +566,10 @@ void GpuSystem::timing_reset() {
 }
 
 // K(x)v P1 = 20 n_tets + 48 n_dofs (x, v gathered, coords 24 B,
-// y written); P2 = 44 n_tets + 24 n_nodes + 24 n_dofs.
+// y written); P2 = 44 n_tets + 24 n_nodes + 24 n_dofs (this rank's share).
 double GpuSystem::kx_bytes() const {
-  if (order_ == 1) return 20.0 * n_tets_ + 48.0 * n_dofs_;
-  return 44.0 * n_tets_ + 24.0 * prob_.mesh.n_nodes + 24.0 * n_dofs_;
+  if (order_ == 1) return 20.0 * n_tets_loc_ + 48.0 * n_full_;
+  return 44.0 * n_tets_loc_ + 24.0 * prob_.mesh.n_nodes * ((double)n_full_ / std::max(1, n_dofs_)) + 24.0 * n_full_;
 }
 double GpuSystem::spmv_bytes(const DevCsr& a) const {
   return 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 8.0 * a.n_rows;
@@ -490,64 +580,56 @@ void GpuSystem::lift_dev(double t, double* x_full) {
   const std::vector<double> v = set_values(t, false);
   SetVals sv;
   std::copy(v.begin(), v.end(), sv.v);
-  launch_lift_fixed(n_fixed_, set_of_fixed_.p, sv, x_full + n_free_, stream_);
+  launch_lift_fixed(n_fixloc_, set_of_fixed_.p, sv, x_full + n_loc_, stream_);
 }
 
 void GpuSystem::kx_tets(const double* x, const double* v) {
-  launch_kx_tets(order_, n_tets_, tet_dofs_.p, tet_mat_.p, coords_.p, x, v, ytet_.p, err_.p, stream_);
+  launch_kx_tets(order_, n_tets_loc_, tet_dofs_.p, tet_mat_.p, coords_.p, x, v, ytet_.p, err_.p, stream_);
   ++stats_.applies;
 }
 
-// coloured single-pass scatter (matfree.cpp:100-117): y (n_dofs) = K(x) v
-static void colored_apply(GpuSystem& g, int order, int n_tets, const int* tet_dofs, const unsigned char* tet_mat,
-                          const double* coords, const double* x, const double* v, double* y, int* err, int n_dofs,
-                          const int* color_tets, const std::vector<long>& off, cudaStream_t s) {
-  (void)g;
-  (void)n_tets;
-  launch_fill(n_dofs, 0.0, y, s);
-  for (size_t c = 0; c + 1 < off.size(); ++c)
-    launch_kx_colored(order, (int)(off[c + 1] - off[c]), color_tets + off[c], tet_dofs, tet_mat, coords, x, v, y, err,
-                      s);
-}
-
+// y (all local rows) = K(x) v; x and v carry valid ghost and fixed entries
 void GpuSystem::kx_apply_full_dev(const double* x_state, const double* v, double* y) {
   tic(TC_STIFF);
   if (stiffness_mode == 1) {
-    if (color_off_.empty()) {
+    if (color_off_.empty()) {  // coloured batches of the local tets (matfree.cpp:100-117)
       const std::vector<int>& col = colors();
       std::vector<long> off(n_colors_ + 1, 0);
-      for (int c : col) ++off[c + 1];
+      for (int k = 0; k < n_tets_loc_; ++k) ++off[col[plan_.tets[k]] + 1];
       for (int c = 0; c < n_colors_; ++c) off[c + 1] += off[c];
-      std::vector<int> order_t(n_tets_);
+      std::vector<int> order_t(std::max(1, n_tets_loc_));
       std::vector<long> nx(off.begin(), off.end() - 1);
-      for (int t = 0; t < n_tets_; ++t) order_t[nx[col[t]]++] = t;
+      for (int k = 0; k < n_tets_loc_; ++k) order_t[nx[col[plan_.tets[k]]]++] = k;
       color_tets_.alloc(order_t.size());
       color_tets_.upload(order_t.data(), order_t.size(), stream_);
       color_off_ = off;
     }
-    colored_apply(*this, order_, n_tets_, tet_dofs_.p, tet_mat_.p, coords_.p, x_state, v, y, err_.p, n_dofs_,
-                  color_tets_.p, color_off_, stream_);
+    launch_fill(n_full_, 0.0, y, stream_);
+    for (size_t c = 0; c + 1 < color_off_.size(); ++c)
+      launch_kx_colored(order_, (int)(color_off_[c + 1] - color_off_[c]), color_tets_.p + color_off_[c],
+                        tet_dofs_.p, tet_mat_.p, coords_.p, x_state, v, y, err_.p, stream_);
     ++stats_.applies;
   } else {
     kx_tets(x_state, v);
-    launch_kx_gather(n_dofs_, slot_ptr_.p, slots_.p, ytet_.p, nullptr, 1.0, y, stream_);
+    launch_kx_gather(n_full_, slot_ptr_.p, slots_.p, ytet_.p, nullptr, 1.0, y, stream_);
   }
   toc(TC_STIFF, kx_bytes());
 }
 
 // eval_residual core (fem_system.cpp:62-67 + matfree.cpp:138-143):
-// r = -M_IB xdot_B(t) - (K(x) x)|free with x lifted at t.
+// r = -M_IB xdot_B(t) - (K(x) x)|owned with x lifted at t and its ghosts exchanged.
 void GpuSystem::residual_dev(double t, double* x_full, double* r) {
   lift_dev(t, x_full);
+  halo(halo0_, x_full);
   tic(TC_STIFF);
   if (stiffness_mode == 1) {
     kx_apply_full_dev(x_full, x_full, w_full_a_.p);
-    launch_scale(n_free_, -1.0, w_full_a_.p, r, stream_);
+    launch_scale(n_own_, -1.0, w_full_a_.p, r, stream_);
   } else {
     kx_tets(x_full, x_full);
-    launch_kx_gather(n_free_, slot_ptr_.p, slots_.p, ytet_.p, nullptr, -1.0, r, stream_);
+    launch_kx_gather(n_own_, slot_ptr_.p, slots_.p, ytet_.p, nullptr, -1.0, r, stream_);
   }
-  toc(TC_STIFF, kx_bytes() - 8.0 * n_fixed_);
+  toc(TC_STIFF, kx_bytes() - 8.0 * n_fixloc_);
   const std::vector<double> rt = set_values(t, true);
   SetVals sv;
   std::copy(rt.begin(), rt.end(), sv.v);
@@ -555,56 +637,83 @@ void GpuSystem::residual_dev(double t, double* x_full, double* r) {
   check_kernel_flags();
 }
 
-void GpuSystem::mass_apply_dev(const double* v, double* y) { launch_spmv(mii_, v, y, stream_); }
+void GpuSystem::mass_apply_dev(double* v, double* y) {
+  halo(halo0_, v);
+  launch_spmv(mii_, v, y, stream_);
+}
 
 // Symmetric V-cycle (amg.cpp:145-172 structure) with Chebyshev smoothing:
 // degree `cheb_degree` on the fine level, `coarse_degree` below; the same
-// polynomial pre and post keeps the preconditioner symmetric for PCG.
-double* GpuSystem::vcycle(int l, const double* b, bool dot_into_rz) {
+// polynomial pre and post keeps the preconditioner symmetric for PCG. Every
+// gathered vector has its ghosts exchanged first (no-op on one rank).
+double* GpuSystem::vcycle(int l, const double* b_in, bool dot_into_rz) {
   const int L = (int)levels_.size();
   DevLevel& lv = levels_[l];
+  double* b = const_cast<double*>(b_in);
   if (l == L - 1) {
-    launch_dense_solve(coarse_n_, coarse_inv_.p, b, lv.z.p, stream_);
-    if (dot_into_rz) launch_dot(coarse_n_, b, lv.z.p, red_, S_RZ, stream_);
-    return lv.z.p;
+    // replicated dense solve: assemble the full right-hand side on every rank
+    double* z = lv.z.p;
+    if (comm_->size() == 1) {
+      launch_dense_solve(coarse_n_, coarse_inv_.p, b, z, stream_);
+    } else {
+      launch_fill(coarse_n_, 0.0, lv.full_b.p, stream_);
+      launch_scatter(lv.n_own, lv.glob.p, b, lv.full_b.p, stream_);
+      comm_->allreduce(lv.full_b.p, coarse_n_, stream_);
+      launch_dense_solve(coarse_n_, coarse_inv_.p, lv.full_b.p, lv.full_z.p, stream_);
+      launch_gather(lv.n_loc, lv.glob.p, lv.full_z.p, z, stream_);  // owned + ghosts
+    }
+    if (dot_into_rz) {
+      launch_dot(lv.n_own, b, z, red_, S_RZ, stream_);
+      allreduce(S_RZ);
+    }
+    return z;
   }
   DevLevel& nx = levels_[l + 1];
   const int deg = l == 0 ? cheb_degree : coarse_degree;
   double* z = lv.z.p;
+  halo(lv.halo, b);
   if (deg >= 2) {
     launch_cheb_pre(lv.A, lv.invd.p, b, z, lv.cheb, stream_);
+    halo(lv.halo, z);
     launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
   } else if (lv.A.tpr <= 4) {
     launch_cheb1_pre_resid(lv.A, lv.invd.p, b, z, lv.t.p, lv.cheb1, stream_);
   } else {
     // dense rows: one gathered vector per entry instead of two (b and D^-1)
-    launch_diag_scale(lv.A.n_rows, lv.invd.p, b, lv.cheb1.inv_theta, z, stream_);
+    launch_diag_scale(lv.n_loc, lv.invd.p, b, lv.cheb1.inv_theta, z, stream_);
     launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
   }
+  halo(lv.halo, lv.t.p);
   launch_spmv(lv.R, lv.t.p, nx.b.p, stream_);
-  const double* zc = vcycle(l + 1, nx.b.p, false);
+  double* zc = vcycle(l + 1, nx.b.p, false);
+  if (l + 1 < L - 1) halo(nx.halo, zc);  // the coarsest returns its ghosts already
   launch_prolong_add(lv.P, zc, z, stream_);
+  halo(lv.halo, z);
   if (deg >= 2) {
     launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
+    halo(lv.halo, lv.t.p);
     Reducer r = red_;
     launch_cheb_post2(lv.A, lv.invd.p, lv.t.p, z, lv.cheb, dot_into_rz ? b : nullptr, dot_into_rz ? &r : nullptr,
                       S_RZ, stream_);
+    if (dot_into_rz) allreduce(S_RZ);
     return z;
   }
   launch_cheb1_post(lv.A, lv.invd.p, b, z, lv.z2.p, lv.cheb1, stream_);
-  if (dot_into_rz) launch_dot(lv.A.n_rows, b, lv.z2.p, red_, S_RZ, stream_);
+  if (dot_into_rz) {
+    launch_dot(lv.n_own, b, lv.z2.p, red_, S_RZ, stream_);
+    allreduce(S_RZ);
+  }
   return lv.z2.p;
 }
 
-// The V-cycle is a fixed sequence of ~4 kernels per level on fixed buffers,
-// so it is captured once into a CUDA graph and replayed: one launch per
-// preconditioner application instead of ~30, no host gaps between the short
-// coarse-level kernels.
-double* GpuSystem::precondition(const double* r) {
+// The V-cycle is a fixed sequence of kernels (and, on several ranks, NCCL
+// halo/allreduce calls) on fixed buffers, so it is captured once into a CUDA
+// graph and replayed: one launch per preconditioner application.
+double* GpuSystem::precondition(double* r) {
   tic(TC_VCYCLE);
   double* z;
   if (prob_.solver.precond == 2) {
-    if (use_graphs && r == w_r_.p) {
+    if (use_graphs && comm_->capturable() && r == w_r_.p) {
       if (!vcycle_graph_) {
         cudaGraph_t graph;
         const long before = g_launch_count;
@@ -625,7 +734,8 @@ double* GpuSystem::precondition(const double* r) {
   } else {
     Reducer rr = red_;
     z = w_z_.p;
-    launch_jacobi(n_free_, mii_invd_.p, r, z, &rr, S_RZ, stream_);
+    launch_jacobi(n_own_, mii_invd_.p, r, z, &rr, S_RZ, stream_);
+    allreduce(S_RZ);
   }
   toc(TC_VCYCLE, 0.0);
   return z;
@@ -633,10 +743,12 @@ double* GpuSystem::precondition(const double* r) {
 
 // pcg_solve (proj/src/pcg.cpp:9-72) with device vectors; host reads three
 // scalars per iteration for the stopping rule and the breakdown checks.
+// b, x: owned entries; x0 may be null.
 PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, double tol, int max_iter) {
-  const int n = n_free_;
+  const int n = n_own_;
   PcgResult res;
   launch_dot(n, b, b, red_, S_BB, stream_);
+  allreduce(S_BB);
   const double bnorm = std::sqrt(read_scalar(S_BB));
   if (bnorm == 0.0) {
     launch_fill(n, 0.0, x, stream_);
@@ -646,6 +758,7 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
   bool use_x0 = false;
   if (x0) {
     launch_dot(n, x0, x0, red_, S_X0X0, stream_);
+    allreduce(S_X0X0);
     use_x0 = read_scalar(S_X0X0) != 0.0;
   }
   double* r = w_r_.p;
@@ -656,8 +769,12 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
   tic(TC_PCG);
   if (use_x0) {
     if (x0 != x) CK(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    // the residual gathers x: stage it in p, which has room for ghosts
+    CK(cudaMemcpyAsync(p, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    halo(halo0_, p);
     Reducer rd = red_;
-    launch_residual(mii_, b, x, r, &rd, S_RR, stream_);
+    launch_residual(mii_, b, p, r, &rd, S_RR, stream_);
+    allreduce(S_RR);
     toc(TC_PCG, spmv_bytes(mii_) + 16.0 * n);
     rr = read_scalar(S_RR);
   } else {
@@ -681,8 +798,11 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
   CK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));  // p = z
   for (int k = 1; k <= max_iter; ++k) {
     tic(TC_PCG);
+    halo(halo0_, p);
     launch_spmv_dot(mii_, p, q, red_, S_PQ, stream_);
+    allreduce(S_PQ);
     launch_pcg_update(n, x, r, p, q, red_, stream_);
+    allreduce(S_RR);
     toc(TC_PCG, spmv_bytes(mii_) + 8.0 * n + 48.0 * n);
     read_scalars(S_PQ, 3, sc);  // pq, rr, rz
     const double pq = sc[0];
@@ -710,8 +830,6 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
 }
 
 // ------------------------------------------------------------------ estimator
-// StartVectorEstimator::next (proj/src/start_vector.cpp:84-109); writes the
-// start vector into x0 and returns true when it is non-zero-by-construction.
 // SPE (proj/src/start_vector.cpp:33-62,84-109,152-164). The reference
 // re-orthonormalises its whole window with MGS on every solve and applies
 // M to every basis vector (2 sum_k (dot + axpy) + m SpMVs per solve). The
@@ -731,17 +849,20 @@ void GpuSystem::spe_alloc(int window) {
   for (int s = 0; s < 2; ++s)
     while ((int)spe_q_[s].size() < window) {
       spe_q_[s].push_back(std::make_unique<DevBuf<double>>());
-      spe_q_[s].back()->alloc(std::max(1, n_free_));
+      spe_q_[s].back()->alloc(std::max(1, n_loc_));
       spe_w_[s].push_back(std::make_unique<DevBuf<double>>());
-      spe_w_[s].back()->alloc(std::max(1, n_free_));
+      spe_w_[s].back()->alloc(std::max(1, n_loc_));
     }
 }
+
+double GpuSystem::dot_own(const double* a, const double* b, int slot) { return dot_n(n_own_, a, b, slot); }
 
 // G row/column k (G_ik = q_i' W_k) for the basis vectors 0..k of the current set
 void GpuSystem::spe_g_column(int k) {
   std::vector<const double*> Q(k + 1);
   for (int i = 0; i <= k; ++i) Q[i] = spe_q(spe_set_, i);
-  launch_multi_dot(n_free_, k + 1, Q.data(), spe_w(spe_set_, k), red_, S_MDOT, stream_);
+  launch_multi_dot(n_own_, k + 1, Q.data(), spe_w(spe_set_, k), red_, S_MDOT, stream_);
+  allreduce(S_MDOT, k + 1);
   double g[kMaxMulti];
   read_scalars(S_MDOT, k + 1, g);
   spe_G_.resize((size_t)kMaxMulti * kMaxMulti);
@@ -750,14 +871,13 @@ void GpuSystem::spe_g_column(int k) {
 
 // mgs_orthonormalize (start_vector.cpp:10-28) over the whole history, reference order
 void GpuSystem::spe_rebuild() {
-  const int n = n_free_;
+  const int n = n_own_;
   const double drop = prob_.solver.mgs_drop_tol;
   spe_alloc((int)history_.size());
   spe_k_ = 0;
   bool all_kept = true;
   for (double* cand : history_) {
-    launch_dot(n, cand, cand, red_, S_NORM, stream_);
-    const double norm0 = std::sqrt(read_scalar(S_NORM));
+    const double norm0 = std::sqrt(dot_own(cand, cand, S_NORM));
     if (norm0 == 0.0) {
       all_kept = false;
       continue;
@@ -765,26 +885,22 @@ void GpuSystem::spe_rebuild() {
     const int m = spe_k_;
     double* w = spe_q(spe_set_, m);
     CK(cudaMemcpyAsync(w, cand, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
-    std::vector<double> rc(m + 1, 0.0);
     bool keep = true;
     for (int pass = 0; pass < 2 && keep; ++pass) {
       for (int u = 0; u < m; ++u) {  // modified Gram-Schmidt, sequential projections
         launch_dot(n, spe_q(spe_set_, u), w, red_, S_DOT, stream_);
+        allreduce(S_DOT);
         launch_axpy_dev(n, red_scal_.p + S_DOT, -1.0, spe_q(spe_set_, u), w, stream_);
       }
-      launch_dot(n, w, w, red_, S_NORM, stream_);
-      const double nrm = std::sqrt(read_scalar(S_NORM));
+      const double nrm = std::sqrt(dot_own(w, w, S_NORM));
       if (nrm <= drop * norm0) keep = false;
-      else if (pass == 1) {
-        launch_scale(n, 1.0 / nrm, w, w, stream_);
-        rc[m] = nrm;
-      }
+      else if (pass == 1) launch_scale(n, 1.0 / nrm, w, w, stream_);
     }
     if (!keep) {
       all_kept = false;
       continue;
     }
-    launch_spmv(mii_, w, spe_w(spe_set_, m), stream_);
+    mass_apply_dev(w, spe_w(spe_set_, m));
     ++spe_k_;
     spe_g_column(m);
   }
@@ -797,6 +913,7 @@ void GpuSystem::spe_rebuild() {
     int j = 0;
     for (double* h : history_) {
       launch_multi_dot(n, k, Q.data(), h, red_, S_MDOT, stream_);
+      allreduce(S_MDOT, k);
       double col[kMaxMulti];
       read_scalars(S_MDOT, k, col);
       for (int i = 0; i <= j; ++i) spe_R_[(size_t)i * kMaxWin + j] = col[i];
@@ -806,12 +923,11 @@ void GpuSystem::spe_rebuild() {
 }
 
 // append h (newest) with two classical Gram-Schmidt passes and the MGS drop test
-void GpuSystem::spe_append(const double* h) {
-  const int n = n_free_;
+void GpuSystem::spe_append(double* h) {
+  const int n = n_own_;
   const double drop = prob_.solver.mgs_drop_tol;
   const int m = spe_k_;
-  launch_dot(n, h, h, red_, S_NORM, stream_);
-  const double norm0 = std::sqrt(read_scalar(S_NORM));
+  const double norm0 = std::sqrt(dot_own(h, h, S_NORM));
   if (norm0 == 0.0) {
     spe_clean_ = false;
     return;
@@ -825,6 +941,7 @@ void GpuSystem::spe_append(const double* h) {
   for (int pass = 0; pass < 2; ++pass) {
     if (m > 0) {
       launch_multi_dot(n, m, Q.data(), w, red_, S_MDOT, stream_);
+      allreduce(S_MDOT, m);
       double c[kMaxMulti];
       read_scalars(S_MDOT, m, c);
       CoefPack cp{};
@@ -833,6 +950,7 @@ void GpuSystem::spe_append(const double* h) {
         r[i] += c[i];
       }
       launch_orth_update(n, m, Q.data(), cp, w, red_, S_NORM, stream_);
+      allreduce(S_NORM);
       nrm = std::sqrt(read_scalar(S_NORM));
     }
     if (nrm <= drop * norm0) {
@@ -843,7 +961,7 @@ void GpuSystem::spe_append(const double* h) {
   launch_scale(n, 1.0 / nrm, w, w, stream_);
   r[m] = nrm;
   for (int i = 0; i <= m; ++i) spe_R_[(size_t)i * kMaxWin + m] = r[i];
-  launch_spmv(mii_, w, spe_w(spe_set_, m), stream_);
+  mass_apply_dev(w, spe_w(spe_set_, m));
   spe_k_ = m + 1;
   spe_g_column(m);
 }
@@ -889,8 +1007,8 @@ void GpuSystem::spe_downdate() {
     qo[j] = spe_q(1 - spe_set_, j);
     wo[j] = spe_w(1 - spe_set_, j);
   }
-  launch_lincomb_multi(n_free_, k, k - 1, qi.data(), qo.data(), T, stream_);
-  launch_lincomb_multi(n_free_, k, k - 1, wi.data(), wo.data(), T, stream_);
+  launch_lincomb_multi(n_own_, k, k - 1, qi.data(), qo.data(), T, stream_);
+  launch_lincomb_multi(n_own_, k, k - 1, wi.data(), wo.data(), T, stream_);
   // G' = T' G T, R' = rows 0..k-2 of the rotated Rh
   std::vector<double> G2((size_t)kMaxMulti * kMaxMulti, 0.0);
   for (int a = 0; a + 1 < k; ++a)
@@ -911,7 +1029,7 @@ void GpuSystem::spe_downdate() {
 // StartVectorEstimator::next (proj/src/start_vector.cpp:84-109); writes the
 // start vector into x0 and returns true when it is non-zero-by-construction.
 bool GpuSystem::estimator_next(const double* b, double* x0) {
-  const int n = n_free_;
+  const int n = n_own_;
   const int mode = prob_.solver.estimator_mode;
   if (mode == 0) return false;
   if (history_.empty()) return false;
@@ -955,6 +1073,7 @@ bool GpuSystem::estimator_next(const double* b, double* x0) {
   std::vector<const double*> V(m);
   for (int c = 0; c < m; ++c) V[c] = spe_q(spe_set_, c);
   launch_multi_dot(n, m, V.data(), b, red_, S_MDOT, stream_);
+  allreduce(S_MDOT, m);
   double vtb[kMaxMulti];
   read_scalars(S_MDOT, m, vtb);
   CoefPack y{};
@@ -980,10 +1099,10 @@ void GpuSystem::estimator_feedback(const double* x) {
     if (mode == 2 && spe_clean_ && spe_incremental) spe_downdate();
   } else {
     hist_pool_.push_back(std::make_unique<DevBuf<double>>());
-    hist_pool_.back()->alloc(std::max(1, n_free_));
+    hist_pool_.back()->alloc(std::max(1, n_loc_));
     buf = hist_pool_.back()->p;
   }
-  CK(cudaMemcpyAsync(buf, x, sizeof(double) * n_free_, cudaMemcpyDeviceToDevice, stream_));
+  CK(cudaMemcpyAsync(buf, x, sizeof(double) * n_own_, cudaMemcpyDeviceToDevice, stream_));
   history_.push_back(buf);
   if (mode == 2 && spe_clean_ && spe_incremental) {
     if (window > (size_t)(kMaxWin - 1)) {
@@ -1030,21 +1149,23 @@ PcgResult GpuSystem::eval_rhs_dev(double t, double* x_full, double* f) {
 }
 
 // FemSystem::apply_minv_stiffness (proj/src/fem_system.cpp:103-122)
-void GpuSystem::apply_minv_stiffness_dev(double t, double* x_full, const double* v_free, double* y) {
+void GpuSystem::apply_minv_stiffness_dev(double t, double* x_full, const double* v_own, double* y) {
   double* vfull = w_full_b_.p;
   double* kv = w_free_b_.p;
   {
     PhaseTimer pt(stats_.t_residual);
     lift_dev(t, x_full);
-    CK(cudaMemcpyAsync(vfull, v_free, sizeof(double) * n_free_, cudaMemcpyDeviceToDevice, stream_));
-    launch_fill(n_fixed_, 0.0, vfull + n_free_, stream_);
+    halo(halo0_, x_full);
+    CK(cudaMemcpyAsync(vfull, v_own, sizeof(double) * n_own_, cudaMemcpyDeviceToDevice, stream_));
+    halo(halo0_, vfull);
+    launch_fill(n_fixloc_, 0.0, vfull + n_loc_, stream_);
     tic(TC_STIFF);
     if (stiffness_mode == 1) {
       kx_apply_full_dev(x_full, vfull, w_full_a_.p);
-      CK(cudaMemcpyAsync(kv, w_full_a_.p, sizeof(double) * n_free_, cudaMemcpyDeviceToDevice, stream_));
+      CK(cudaMemcpyAsync(kv, w_full_a_.p, sizeof(double) * n_own_, cudaMemcpyDeviceToDevice, stream_));
     } else {
       kx_tets(x_full, vfull);
-      launch_kx_gather(n_free_, slot_ptr_.p, slots_.p, ytet_.p, nullptr, 1.0, kv, stream_);
+      launch_kx_gather(n_own_, slot_ptr_.p, slots_.p, ytet_.p, nullptr, 1.0, kv, stream_);
     }
     toc(TC_STIFF, kx_bytes());
     check_kernel_flags();
@@ -1055,9 +1176,11 @@ void GpuSystem::apply_minv_stiffness_dev(double t, double* x_full, const double*
   stats_.rho_pcg_iterations += res.iterations;
 }
 
-// estimate_spectral_radius (proj/src/integrators.cpp:49-75)
+// estimate_spectral_radius (proj/src/integrators.cpp:49-75); the start vector
+// is generated in global free order, each rank keeps its owned entries
 double GpuSystem::estimate_spectral_radius(double t, double* x_full) {
   const int n = n_free_;
+  const std::vector<int>& own = plan_.space[0].owned;
   for (int restart = 0; restart < 4; ++restart) {
     std::mt19937 rng(7919u + 31u * (unsigned)restart);
     std::uniform_real_distribution<double> uni(-1.0, 1.0);
@@ -1067,101 +1190,109 @@ double GpuSystem::estimate_spectral_radius(double t, double* x_full) {
     for (double e : v) nrm += e * e;
     nrm = std::sqrt(nrm);
     if (nrm == 0.0) continue;
-    for (double& e : v) e /= nrm;
-    rho_v_.upload(v.data(), n, stream_);
+    std::vector<double> vo(std::max(1, n_own_));
+    for (int i = 0; i < n_own_; ++i) vo[i] = v[own[i]] / nrm;
+    rho_v_.upload(vo.data(), n_own_, stream_);
     double rho = 0.0;
     bool annihilated = false;
     for (int it = 0; it < 15; ++it) {
       apply_minv_stiffness_dev(t, x_full, rho_v_.p, rho_w_.p);
-      launch_dot(n, rho_w_.p, rho_w_.p, red_, S_NORM, stream_);
-      rho = std::sqrt(read_scalar(S_NORM));
+      rho = std::sqrt(dot_own(rho_w_.p, rho_w_.p, S_NORM));
       if (rho == 0.0) {
         annihilated = true;
         break;
       }
-      launch_scale(n, 1.0 / rho, rho_w_.p, rho_v_.p, stream_);
+      launch_scale(n_own_, 1.0 / rho, rho_w_.p, rho_v_.p, stream_);
     }
     if (!annihilated) return 1.2 * rho;
   }
   return 0.0;
 }
 
-// ------------------------------------------------------------------ host wrappers
+// ------------------------------------------------------------------ host wrappers (single rank)
 void GpuSystem::kx_apply_host(const double* x_state, const double* v, double* y) {
-  std::vector<double> xd(n_dofs_), vd(n_dofs_), yd(n_dofs_);
-  for (int k = 0; k < n_dofs_; ++k) {
-    xd[k] = x_state[dev2ref_[k]];
-    vd[k] = v[dev2ref_[k]];
+  require_single("kx_apply");
+  std::vector<double> xd(n_full_), vd(n_full_), yd(n_full_);
+  for (int k = 0; k < n_full_; ++k) {
+    xd[k] = x_state[loc2ref_[k]];
+    vd[k] = v[loc2ref_[k]];
   }
-  w_full_a_.upload(xd.data(), n_dofs_, stream_);
-  w_full_b_.upload(vd.data(), n_dofs_, stream_);
+  w_full_a_.upload(xd.data(), n_full_, stream_);
+  w_full_b_.upload(vd.data(), n_full_, stream_);
   double* out = scratch_full();
   kx_apply_full_dev(w_full_a_.p, w_full_b_.p, out);
-  CK(cudaMemcpyAsync(yd.data(), out, sizeof(double) * n_dofs_, cudaMemcpyDeviceToHost, stream_));
+  CK(cudaMemcpyAsync(yd.data(), out, sizeof(double) * n_full_, cudaMemcpyDeviceToHost, stream_));
   check_kernel_flags();
-  for (int k = 0; k < n_dofs_; ++k) y[dev2ref_[k]] = yd[k];
+  std::fill(y, y + n_dofs_, 0.0);  // dofs in no tet
+  for (int k = 0; k < n_full_; ++k) y[loc2ref_[k]] = yd[k];
 }
 
 // MatFreeStiffness::residual (matfree.cpp:138-143)
 void GpuSystem::kx_residual_host(const double* x_full, const double* b_mass, double* r) {
-  std::vector<double> xd(n_dofs_), yd(n_dofs_);
-  for (int k = 0; k < n_dofs_; ++k) xd[k] = x_full[dev2ref_[k]];
-  w_full_a_.upload(xd.data(), n_dofs_, stream_);
-  w_free_a_.upload(b_mass, n_free_, stream_);
+  require_single("kx_residual");
+  std::vector<double> xd(n_full_);
+  for (int k = 0; k < n_full_; ++k) xd[k] = x_full[loc2ref_[k]];
+  w_full_a_.upload(xd.data(), n_full_, stream_);
+  w_free_a_.upload(b_mass, n_own_, stream_);
   tic(TC_STIFF);
   if (stiffness_mode == 1) {
     kx_apply_full_dev(w_full_a_.p, w_full_a_.p, w_full_b_.p);
-    launch_axpby_into(n_free_, w_free_a_.p, -1.0, w_full_b_.p, w_free_b_.p, stream_);
+    launch_axpby_into(n_own_, w_free_a_.p, -1.0, w_full_b_.p, w_free_b_.p, stream_);
   } else {
     kx_tets(w_full_a_.p, w_full_a_.p);
-    launch_kx_gather(n_free_, slot_ptr_.p, slots_.p, ytet_.p, w_free_a_.p, -1.0, w_free_b_.p, stream_);
+    launch_kx_gather(n_own_, slot_ptr_.p, slots_.p, ytet_.p, w_free_a_.p, -1.0, w_free_b_.p, stream_);
   }
   toc(TC_STIFF, kx_bytes());
-  w_free_b_.download(r, n_free_, stream_);
+  w_free_b_.download(r, n_own_, stream_);
   check_kernel_flags();
 }
 
 void GpuSystem::eval_residual_host(double t, const double* x, double* r) {
+  require_single("eval_residual");
   PhaseTimer pt(stats_.t_residual);
   double* xf = w_full_b_.p;
-  CK(cudaMemcpyAsync(xf, x, sizeof(double) * n_free_, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(xf, x, sizeof(double) * n_own_, cudaMemcpyHostToDevice, stream_));
   residual_dev(t, xf, w_free_b_.p);
-  w_free_b_.download(r, n_free_, stream_);
+  w_free_b_.download(r, n_own_, stream_);
   sync();
 }
 
 PcgResult GpuSystem::eval_rhs_host(double t, const double* x, double* f) {
+  require_single("eval_rhs");
   double* xf = w_full_b_.p;
-  CK(cudaMemcpyAsync(xf, x, sizeof(double) * n_free_, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(xf, x, sizeof(double) * n_own_, cudaMemcpyHostToDevice, stream_));
   PcgResult r = eval_rhs_dev(t, xf, F_.p);
-  F_.download(f, n_free_, stream_);
+  F_.download(f, n_own_, stream_);
   sync();
   return r;
 }
 
 PcgResult GpuSystem::mass_solve_host(const double* b, const double* x0, double tol, int max_iter, double* x) {
-  F0_.upload(b, n_free_, stream_);
-  if (x0) Fn_.upload(x0, n_free_, stream_);
+  require_single("mass_solve");
+  F0_.upload(b, n_own_, stream_);
+  if (x0) Fn_.upload(x0, n_own_, stream_);
   PhaseTimer pt(stats_.t_solve);
   PcgResult r = pcg_dev(F0_.p, x0 ? Fn_.p : nullptr, F_.p, tol, max_iter);
-  F_.download(x, n_free_, stream_);
+  F_.download(x, n_own_, stream_);
   sync();
   return r;
 }
 
 void GpuSystem::mass_apply_host(const double* v, double* y) {
-  F0_.upload(v, n_free_, stream_);
+  require_single("mass_apply");
+  F0_.upload(v, n_own_, stream_);
   mass_apply_dev(F0_.p, F_.p);
-  F_.download(y, n_free_, stream_);
+  F_.download(y, n_own_, stream_);
   sync();
 }
 
 void GpuSystem::apply_minv_stiffness_host(double t, const double* x_state, const double* v, double* y) {
+  require_single("apply_minv_stiffness");
   double* xf = scratch_full();
-  CK(cudaMemcpyAsync(xf, x_state, sizeof(double) * n_free_, cudaMemcpyHostToDevice, stream_));
-  F0_.upload(v, n_free_, stream_);
+  CK(cudaMemcpyAsync(xf, x_state, sizeof(double) * n_own_, cudaMemcpyHostToDevice, stream_));
+  F0_.upload(v, n_own_, stream_);
   apply_minv_stiffness_dev(t, xf, F0_.p, F_.p);
-  F_.download(y, n_free_, stream_);
+  F_.download(y, n_own_, stream_);
   sync();
 }
 
@@ -1172,16 +1303,16 @@ void GpuSystem::lift_full_host(double t, const double* x_free, double* x_full) {
 }
 
 // ------------------------------------------------------------------ integrators
-void GpuSystem::set_state(double t, const double* x_host, double dt) {
+void GpuSystem::set_state(double t, const double* x_own, double dt) {
   state_t = t;
   state_dt = dt;
-  CK(cudaMemcpyAsync(X_, x_host, sizeof(double) * n_free_, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(X_, x_own, sizeof(double) * n_own_, cudaMemcpyHostToDevice, stream_));
   sync();
   rho_valid = false;
   rho_age = 0;
 }
-void GpuSystem::get_state(double* x_host) {
-  CK(cudaMemcpyAsync(x_host, X_, sizeof(double) * n_free_, cudaMemcpyDeviceToHost, stream_));
+void GpuSystem::get_state(double* x_own) {
+  CK(cudaMemcpyAsync(x_own, X_, sizeof(double) * n_own_, cudaMemcpyDeviceToHost, stream_));
   sync();
 }
 
@@ -1203,10 +1334,10 @@ const RkcCoefficients& rkc_coefficients(int s) {  // integrators.cpp:148-153
 }
 }  // namespace
 
-// rkc_stages (proj/src/integrators.cpp:156-173). Returns the buffer holding Y_s.
+// rkc_stages (proj/src/integrators.cpp:156-173) on the owned entries. Returns the buffer holding Y_s.
 static double* rkc_stages(GpuSystem& g, double t, double dt, const RkcCoefficients& k, double* X, double* bufs[3],
                           double* f0, double* f) {
-  const int n = g.n_free();
+  const int n = g.n_own();
   g.eval_rhs_dev(t, X, f0);
   double* jm2 = X;
   double* jm1 = bufs[0];
@@ -1257,8 +1388,9 @@ StepAttempt GpuSystem::rkc_step(const RkcOptions& o) {
     double* x_new = rkc_stages(*this, state_t, dt, k, X_, bufs, F0_.p, F_.p);
     eval_rhs_dev(state_t + dt, x_new, Fn_.p);
     tic(TC_RKC);
-    launch_rkc_error(n_free_, X_, x_new, F0_.p, Fn_.p, dt, o.atol, o.rtol, red_, S_ERR, stream_);
-    toc(TC_RKC, 32.0 * n_free_);
+    launch_rkc_error(n_own_, X_, x_new, F0_.p, Fn_.p, dt, o.atol, o.rtol, red_, S_ERR, stream_);
+    allreduce(S_ERR);
+    toc(TC_RKC, 32.0 * n_own_);
     const double acc = read_scalar(S_ERR);
     att.error = n_free_ == 0 ? 0.0 : std::sqrt(acc / (double)n_free_);
     // step_controller (integrators.cpp:12-18), order 2
@@ -1315,8 +1447,8 @@ StepAttempt GpuSystem::euler_step(double dt) {
   att.dt = dt;
   eval_rhs_dev(state_t + dt, X_, F_.p);
   tic(TC_RKC);
-  launch_axpy(n_free_, dt, F_.p, X_, stream_);
-  toc(TC_RKC, 24.0 * n_free_);
+  launch_axpy(n_own_, dt, F_.p, X_, stream_);
+  toc(TC_RKC, 24.0 * n_own_);
   state_t += dt;
   ++st_accepted;
   ++st_stages;

@@ -1,7 +1,9 @@
 // GpuSystem: the B200-resident counterpart of the reference FemSystem
 // (proj/include/eqs/fem_system.hpp:30-73) plus the integrator state
 // (proj/include/eqs/integrators.hpp:23-29). Host code controls, the device
-// holds every vector and matrix.
+// holds every vector and matrix. With nranks > 1 each instance owns one
+// partition of the node-ownership decomposition (partition.hpp) and talks to
+// its peers through a Comm (comm.hpp); with one rank it is the whole problem.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -12,8 +14,10 @@
 #include <string>
 #include <vector>
 
+#include "comm.hpp"
 #include "dev.cuh"
 #include "eqs_internal.hpp"
+#include "partition.hpp"
 
 namespace eqsb {
 
@@ -60,7 +64,16 @@ struct DevBuf {
   void download(T* host, size_t count, cudaStream_t s) const;
 };
 
+// halo of one level's index space on this rank (partition.hpp LocalSpace)
+struct DevHalo {
+  int n_own = 0, n_send = 0;
+  DevBuf<int> send_idx;      // concatenated per-peer send lists (local owned indices)
+  DevBuf<double> send_buf;
+  std::vector<int> peers, send_off, send_cnt, recv_off, recv_cnt;
+};
+
 struct DevLevel {
+  int n_own = 0, n_loc = 0, n_global = 0;
   DevCsr A, P, R;
   DevBuf<int> a_rp, a_ci, p_rp, p_ci, r_rp, r_ci;
   DevBuf<double> a_v, p_v, r_v;
@@ -68,6 +81,9 @@ struct DevLevel {
   DevBuf<double> invd, b, z, z2, t;
   ChebCoef cheb{}, cheb1{};          // degree-2 and degree-1 Chebyshev coefficients
   double lambda_smoother = 0;
+  DevHalo halo;
+  DevBuf<int> glob;                  // coarsest level: local -> global ids (replicated dense solve)
+  DevBuf<double> full_b, full_z;     // coarsest level: replicated vectors
 };
 
 // timing classes (eqs_timing in include/eqs_b200.h)
@@ -75,14 +91,19 @@ enum TimeClass { TC_STIFF = 0, TC_PCG = 1, TC_VCYCLE = 2, TC_RKC = 3, TC_SPE = 4
 
 class GpuSystem {
  public:
-  GpuSystem(Problem&& p, int device);
+  // comm == nullptr: single rank
+  GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm = nullptr);
   ~GpuSystem();
 
-  // sizes
+  // sizes (global unless noted)
   int n_dofs() const { return n_dofs_; }
   int n_free() const { return n_free_; }
   int n_fixed() const { return n_fixed_; }
   int n_tets() const { return n_tets_; }
+  int n_own() const { return n_own_; }  // free dofs owned by this rank
+  int rank() const { return comm_->rank(); }
+  int nranks() const { return comm_->size(); }
+  const PartitionPlan& plan() const { return plan_; }
   const Problem& problem() const { return prob_; }
   const HostCsr& mass_ii() const { return m_ii_; }
   const HostCsr& mass_ib() const { return m_ib_; }
@@ -94,22 +115,17 @@ class GpuSystem {
   cudaStream_t stream() const { return stream_; }
   bool host_only() const { return device_ < 0; }
 
-  // ---- operators on device buffers (device dof numbering: free first, then fixed)
-  // y = K(x_state) v on full vectors (rows: all dofs)
-  void kx_apply_full_dev(const double* x_state, const double* v, double* y);
-  // r = -(K(x) x)|free + boundary load of rates at t (eval_residual core)
-  void residual_dev(double t, double* x_full, double* r);
-  // x_full tail <- Dirichlet values at t
-  void lift_dev(double t, double* x_full);
-  void mass_apply_dev(const double* v, double* y);
-  // PCG on M_II with the configured preconditioner (x0 may be null)
+  // ---- operators on device buffers (local numbering [owned | ghosts | local fixed])
+  void kx_apply_full_dev(const double* x_state, const double* v, double* y);  // rows: all local
+  void residual_dev(double t, double* x_full, double* r);  // r (owned) = -(K(x)x) - M_IB xdot_B(t)
+  void lift_dev(double t, double* x_full);                  // fixed tail <- x_B(t)
+  void mass_apply_dev(double* v, double* y);                // v with room for ghosts
   PcgResult pcg_dev(const double* b, const double* x0, double* x, double tol, int max_iter);
-  // f = M^-1 (b - K(x)x) with the estimator; throws NumericalError on failure
   PcgResult eval_rhs_dev(double t, double* x_full, double* f);
-  void apply_minv_stiffness_dev(double t, double* x_full, const double* v_free, double* y);
+  void apply_minv_stiffness_dev(double t, double* x_full, const double* v_own, double* y);
   double estimate_spectral_radius(double t, double* x_full);
 
-  // ---- host-pointer wrappers in reference dof numbering
+  // ---- host-pointer wrappers in reference dof numbering (single rank)
   void kx_apply_host(const double* x_state, const double* v, double* y);
   void kx_residual_host(const double* x_full, const double* b_mass, double* r);
   void eval_residual_host(double t, const double* x, double* r);
@@ -119,9 +135,10 @@ class GpuSystem {
   void apply_minv_stiffness_host(double t, const double* x_state, const double* v, double* y);
   void lift_full_host(double t, const double* x_free, double* x_full);
 
-  // ---- integrator state (device resident)
-  void set_state(double t, const double* x_host, double dt);
-  void get_state(double* x_host);
+  // ---- integrator state (device resident). Host vectors are the owned part
+  // (n_own entries, global free order restricted to plan().space[0].owned).
+  void set_state(double t, const double* x_own, double dt);
+  void get_state(double* x_own);
   double state_t = 0, state_dt = 0;
   long st_accepted = 0, st_rejected = 0, st_stages = 0;
   double rho_value = 0;
@@ -139,41 +156,40 @@ class GpuSystem {
   int cheb_degree = 2;     // fine level (1 or 2)
   int coarse_degree = 1;   // levels >= 1 (1 or 2)
   double cheb_ratio = 6.0;
+  bool use_graphs = true;
+  bool spe_incremental = true;  // false: the reference's full MGS rebuild on every solve
   void set_cheb(double ratio);
   void set_vcycle_fp32(bool on);
   void set_level_tpr(int level, int tpr);  // threads per row of A_l (level 0 also sets M_II)
+  void invalidate_graphs();
   bool vcycle_fp32() const { return vcycle_fp32_; }
   bool timing_on = false;
   void tic(int cls);
   void toc(int cls, double bytes);
   void timing_resolve(double ms[TC_COUNT], long launches[TC_COUNT], double bytes[TC_COUNT]);
   void timing_reset();
-  double kx_bytes() const;       // algorithmic bytes of one K(x)v
+  double kx_bytes() const;  // algorithmic bytes of one K(x)v
   double spmv_bytes(const DevCsr& a) const;
   int amg_levels() const { return (int)levels_.size(); }
   const DevLevel& level(int l) const { return levels_[l]; }
 
  private:
   void build_device();
+  void build_levels();
+  void build_halo(const LocalSpace& sp, DevHalo& h);
+  void halo(DevHalo& h, double* vec);  // fill ghosts of vec from the owners
+  void allreduce(int slot, int count = 1);
   double* vcycle(int l, const double* b, bool dot_into_rz);  // returns the buffer holding z_l
-  double* precondition(const double* r);  // z = M^-1 r (returned buffer), S_RZ <- r.z
-  bool vcycle_fp32_ = true;
-  cudaGraphExec_t vcycle_graph_ = nullptr;  // captured V-cycle (rebuilt when options change)
-  double* vcycle_out_ = nullptr;
-  long vcycle_graph_kernels_ = 0;
-
- public:
-  bool use_graphs = true;
-  bool spe_incremental = true;  // false: the reference's full MGS rebuild on every solve
-  void invalidate_graphs();
-
- private:
+  double* precondition(double* r);  // z = M^-1 r (returned buffer), S_RZ <- r.z
   void kx_tets(const double* x, const double* v);
   double read_scalar(int slot);
   void read_scalars(int first, int count, double* out);
+  double dot_n(int n, const double* a, const double* b, int slot);  // global dot over n owned entries
+  double dot_own(const double* a, const double* b, int slot);       // level-0 owned entries
   void check_kernel_flags();
   void sync();
   std::vector<double> set_values(double t, bool rates) const;
+  void require_single(const char* what) const;
   // estimator (start_vector.cpp:84-109,152-164)
   bool estimator_next(const double* r, double* x0);
   void estimator_feedback(const double* x);
@@ -189,14 +205,21 @@ class GpuSystem {
   void spe_alloc(int window);
   void spe_g_column(int k);
   void spe_rebuild();
-  void spe_append(const double* h);
+  void spe_append(double* h);
   void spe_downdate();
+  bool vcycle_fp32_ = true;
+  cudaGraphExec_t vcycle_graph_ = nullptr;  // captured V-cycle (rebuilt when options change)
+  double* vcycle_out_ = nullptr;
+  long vcycle_graph_kernels_ = 0;
 
   Problem prob_;
   int device_ = 0;
+  std::unique_ptr<Comm> comm_;
   cudaStream_t stream_ = nullptr;
   int n_dofs_ = 0, n_free_ = 0, n_fixed_ = 0, n_tets_ = 0, n_local_ = 4, order_ = 1, n_sets_ = 0;
-  std::vector<int> dev2ref_, ref2dev_;
+  int n_own_ = 0, n_ghost_ = 0, n_loc_ = 0, n_fixloc_ = 0, n_full_ = 0, n_tets_loc_ = 0;
+  PartitionPlan plan_;
+  std::vector<int> loc2ref_;  // local full index -> reference dof id
   std::vector<int> colors_;
   int n_colors_ = -1;
   HostCsr m_ii_, m_ib_;
@@ -205,17 +228,16 @@ class GpuSystem {
   std::vector<SolveRecord> records_;
 
   // device mesh data
-  DevBuf<double> coords_;       // [n_dofs][4]
-  DevBuf<int> tet_dofs_;        // [n_tets][n_local] device numbering
+  DevBuf<double> coords_;  // [n_full][4]
+  DevBuf<int> tet_dofs_;   // [n_tets_loc][n_local] local full numbering
   DevBuf<unsigned char> tet_mat_;
   DevBuf<long> slot_ptr_;
   DevBuf<int> slots_;
   DevBuf<double> ytet_;
-  DevBuf<int> err_;             // kernel error flags
+  DevBuf<int> err_;  // kernel error flags
   DevBuf<int> set_of_fixed_;
   DevBuf<int> bl_rows_;
   DevBuf<double> bl_coef_;
-  DevBuf<double> set_vals_;     // [n_sets]
   int n_bl_rows_ = 0;
   // colour batches (lazy)
   DevBuf<int> color_tets_;
@@ -224,6 +246,7 @@ class GpuSystem {
   DevCsr mii_;
   DevBuf<int> mii_rp_, mii_ci_;
   DevBuf<double> mii_v_, mii_invd_;
+  DevHalo halo0_;  // level-0 (fine dof) halo
   std::vector<DevLevel> levels_;
   DevBuf<double> coarse_inv_;
   int coarse_n_ = 0;
@@ -232,7 +255,7 @@ class GpuSystem {
   DevBuf<unsigned> red_counters_;
   Reducer red_{};
   double* pinned_ = nullptr;  // host pinned scalar mirror [S_COUNT + 8]
-  // work vectors
+  // work vectors (level-0 vectors that are gathered carry room for ghosts)
   DevBuf<double> w_r_, w_z_, w_p_, w_q_, w_full_a_, w_full_b_, w_free_a_, w_free_b_;
   DevBuf<double> full_[4], F0_, F_, Fn_, rho_v_, rho_w_;  // full_: state + 3 stage buffers
   double* X_ = nullptr;

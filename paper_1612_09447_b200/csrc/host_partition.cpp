@@ -1,0 +1,216 @@
+// Deterministic node-ownership partition of the fine dofs and of the AMG
+// hierarchy: owner-computes for the stiffness operator, owned
+// rows + ghost columns for every CSR operator, halo lists per peer.
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "partition.hpp"
+
+namespace eqsb {
+
+namespace {
+
+// coordinates of every dof (vertex dofs: nodes; P2 edge dofs: midpoint of the edge)
+std::vector<double> dof_coords(const Problem& p) {
+  const Dofs& dm = p.dm;
+  const Mesh& m = p.mesh;
+  std::vector<double> c((size_t)dm.n_dofs * 3, 0.0);
+  std::copy(m.nodes.begin(), m.nodes.end(), c.begin());
+  if (dm.order == 2) {
+    for (int t = 0; t < m.n_tets; ++t)
+      for (int e = 0; e < 6; ++e) {
+        const int d = dm.element_dofs[10L * t + 4 + e];
+        const int a = m.tets[4L * t + kTetEdgeVertices[e][0]], b = m.tets[4L * t + kTetEdgeVertices[e][1]];
+        for (int k = 0; k < 3; ++k) c[3L * d + k] = 0.5 * (m.nodes[3L * a + k] + m.nodes[3L * b + k]);
+      }
+  }
+  return c;
+}
+
+HostCsr local_rows(const HostCsr& a, const std::vector<int>& rows, const std::vector<int>& g2l_cols) {
+  HostCsr out;
+  out.n_rows = (int)rows.size();
+  out.row_ptr.assign(rows.size() + 1, 0);
+  for (size_t r = 0; r < rows.size(); ++r) out.row_ptr[r + 1] = out.row_ptr[r] + (a.row_ptr[rows[r] + 1] - a.row_ptr[rows[r]]);
+  out.col_idx.resize(out.row_ptr.back());
+  out.values.resize(out.row_ptr.back());
+  int max_col = -1, bad = 0;
+#pragma omp parallel for schedule(static) reduction(max : max_col, bad)
+  for (long r = 0; r < (long)rows.size(); ++r) {
+    int pos = out.row_ptr[r];
+    for (int k = a.row_ptr[rows[r]]; k < a.row_ptr[rows[r] + 1]; ++k) {
+      const int lc = g2l_cols.empty() ? a.col_idx[k] : g2l_cols[a.col_idx[k]];
+      if (lc < 0) bad = 1;
+      out.col_idx[pos] = lc;
+      out.values[pos++] = a.values[k];
+      max_col = std::max(max_col, lc);
+    }
+  }
+  if (bad) throw std::logic_error("partition: column without a local index");
+  out.n_cols = max_col + 1;
+  return out;
+}
+
+}  // namespace
+
+std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out) {
+  const Dofs& dm = p.dm;
+  const int nf = dm.n_free();
+  const std::vector<double> c = dof_coords(p);
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int n = 0; n < p.mesh.n_nodes; ++n)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = std::min(lo[k], p.mesh.nodes[3L * n + k]);
+      hi[k] = std::max(hi[k], p.mesh.nodes[3L * n + k]);
+    }
+  int axis = 2;
+  for (int k : {1, 0})
+    if (hi[k] - lo[k] > hi[axis] - lo[axis]) axis = k;
+  if (axis_out) *axis_out = axis;
+  std::vector<int> order(nf);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return c[3L * dm.free_dofs[a] + axis] < c[3L * dm.free_dofs[b] + axis];
+  });
+  std::vector<int> owner(nf);
+  for (long k = 0; k < nf; ++k) owner[order[k]] = (int)(k * nranks / std::max(1, nf));
+  return owner;
+}
+
+PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m_ib, const AmgHierarchy& h,
+                         int nranks, int rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("build_plan: bad rank/nranks");
+  PartitionPlan plan;
+  plan.nranks = nranks;
+  plan.rank = rank;
+  const int L = h.levels.empty() ? 1 : (int)h.levels.size();
+  auto A_of = [&](int l) -> const HostCsr& { return h.levels.empty() ? m_ii : h.levels[l].A; };
+  // ownership per level
+  plan.owner.resize(L);
+  plan.owner[0] = partition_free_dofs(p, nranks, &plan.axis);
+  for (int l = 0; l + 1 < L; ++l) {
+    const std::vector<int>& agg = h.levels[l].aggregates;
+    const int nc = A_of(l + 1).n_rows;
+    std::vector<int> first(nc, -1);
+    for (int i = 0; i < (int)agg.size(); ++i)
+      if (first[agg[i]] < 0) first[agg[i]] = i;
+    plan.owner[l + 1].resize(nc);
+    for (int j = 0; j < nc; ++j) plan.owner[l + 1][j] = plan.owner[l][first[j]];
+  }
+  // rows owned by every rank, per level
+  std::vector<std::vector<std::vector<int>>> rows_of(L, std::vector<std::vector<int>>(nranks));
+  for (int l = 0; l < L; ++l)
+    for (int i = 0; i < (int)plan.owner[l].size(); ++i) rows_of[l][plan.owner[l][i]].push_back(i);
+  // ghost sets of every rank per level: columns (level l) of A_l[own_l], R_l[own_l+1], P_l-1[own_l-1]
+  plan.space.resize(L);
+  std::vector<std::vector<int>> g2l(L);
+  for (int l = 0; l < L; ++l) {
+    const std::vector<int>& own = plan.owner[l];
+    std::vector<std::vector<int>> ghosts(nranks);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int q = 0; q < nranks; ++q) {
+      std::vector<int>& gs = ghosts[q];
+      auto scan = [&](const HostCsr& m, const std::vector<int>& rows) {
+        for (int r : rows)
+          for (int k = m.row_ptr[r]; k < m.row_ptr[r + 1]; ++k)
+            if (own[m.col_idx[k]] != q) gs.push_back(m.col_idx[k]);
+      };
+      scan(A_of(l), rows_of[l][q]);
+      if (l + 1 < L) scan(h.levels[l].R, rows_of[l + 1][q]);
+      if (l >= 1) scan(h.levels[l - 1].P, rows_of[l - 1][q]);
+      std::sort(gs.begin(), gs.end());
+      gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
+      std::stable_sort(gs.begin(), gs.end(), [&](int a, int b) { return own[a] < own[b]; });
+    }
+    LocalSpace& sp = plan.space[l];
+    sp.n_global = (int)own.size();
+    sp.owned = rows_of[l][rank];
+    sp.ghosts = ghosts[rank];
+    g2l[l].assign(own.size(), -1);
+    for (int i = 0; i < sp.n_own(); ++i) g2l[l][sp.owned[i]] = i;
+    for (int i = 0; i < sp.n_ghost(); ++i) g2l[l][sp.ghosts[i]] = sp.n_own() + i;
+    sp.recv_off.push_back(0);
+    for (int i = 0; i < sp.n_ghost(); ++i) {
+      const int q = own[sp.ghosts[i]];
+      if (sp.recv_ranks.empty() || sp.recv_ranks.back() != q) {
+        if (!sp.recv_ranks.empty()) sp.recv_off.push_back(i);
+        sp.recv_ranks.push_back(q);
+      }
+    }
+    if (!sp.recv_ranks.empty()) sp.recv_off.push_back(sp.n_ghost());
+    for (int q = 0; q < nranks; ++q) {
+      if (q == rank) continue;
+      std::vector<int> s;
+      for (int gid : ghosts[q])
+        if (own[gid] == rank) s.push_back(g2l[l][gid]);
+      if (!s.empty()) {
+        sp.send_ranks.push_back(q);
+        sp.send_local.push_back(std::move(s));
+      }
+    }
+  }
+  // local operators
+  plan.A.resize(L);
+  plan.P.resize(L);
+  plan.R.resize(L);
+  for (int l = 0; l < L; ++l) {
+    plan.A[l] = local_rows(A_of(l), plan.space[l].owned, g2l[l]);
+    plan.A[l].n_cols = plan.space[l].n_local();
+    if (l + 1 < L) {
+      plan.P[l] = local_rows(h.levels[l].P, plan.space[l].owned, g2l[l + 1]);
+      plan.P[l].n_cols = plan.space[l + 1].n_local();
+      plan.R[l] = local_rows(h.levels[l].R, plan.space[l + 1].owned, g2l[l]);
+      plan.R[l].n_cols = plan.space[l].n_local();
+    }
+  }
+  plan.mii = h.levels.empty() ? plan.A[0] : local_rows(m_ii, plan.space[0].owned, g2l[0]);
+  plan.mii.n_cols = plan.space[0].n_local();
+  plan.mib = local_rows(m_ib, plan.space[0].owned, {});
+  plan.mib.n_cols = m_ib.n_cols;
+  // stiffness operator: tets touching an owned free dof, local full numbering
+  const Dofs& dm = p.dm;
+  const int nl = dm.n_local;
+  std::vector<int> free_index(dm.n_dofs, -1), fixed_index(dm.n_dofs, -1);
+  for (int i = 0; i < dm.n_free(); ++i) free_index[dm.free_dofs[i]] = i;
+  for (int i = 0; i < dm.n_fixed(); ++i) fixed_index[dm.fixed_dofs[i]] = i;
+  std::vector<char> fixed_used(dm.n_dofs, 0);
+  for (int t = 0; t < p.mesh.n_tets; ++t) {
+    bool mine = false;
+    for (int i = 0; i < nl && !mine; ++i) {
+      const int fi = free_index[dm.element_dofs[(size_t)nl * t + i]];
+      mine = fi >= 0 && plan.owner[0][fi] == rank;
+    }
+    if (!mine) continue;
+    plan.tets.push_back(t);
+    for (int i = 0; i < nl; ++i) {
+      const int d = dm.element_dofs[(size_t)nl * t + i];
+      if (free_index[d] < 0) fixed_used[d] = 1;
+    }
+  }
+  std::vector<int> fixed_pos(dm.n_dofs, -1);
+  for (int d = 0; d < dm.n_dofs; ++d)
+    if (fixed_used[d]) {
+      fixed_pos[d] = (int)plan.fixed.size();
+      plan.fixed.push_back(d);
+    }
+  const int base = plan.space[0].n_local();
+  plan.tet_dofs.resize(plan.tets.size() * nl);
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+  for (long k = 0; k < (long)plan.tets.size(); ++k)
+    for (int i = 0; i < nl; ++i) {
+      const int d = dm.element_dofs[(size_t)nl * plan.tets[k] + i];
+      const int fi = free_index[d];
+      const int loc = fi >= 0 ? g2l[0][fi] : base + fixed_pos[d];
+      if (loc < 0) bad = 1;
+      plan.tet_dofs[k * nl + i] = loc;
+    }
+  if (bad) throw std::logic_error("partition: tet dof without a local index");
+  (void)fixed_index;
+  return plan;
+}
+
+}  // namespace eqsb

@@ -7,6 +7,9 @@
 // preconditioner only; PCG itself is fp64 throughout).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <unordered_map>
+
 #include "dev.cuh"
 
 namespace eqsb {
@@ -62,11 +65,30 @@ __device__ __forceinline__ void reduce_finish(double v, Reducer red, int slot) {
   }
 }
 
-int red_grid(long work_items) {
+// Grid of a grid-stride reduction kernel: exactly one wave of resident blocks
+// (SMs x blocks-per-SM at this kernel's register use), so no tail wave; the
+// grid (hence the summation order) is fixed per kernel: deterministic.
+template <class K>
+int red_grid(K kernel, long work_items) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static std::unordered_map<const void*, int> bps_cache;
+  const void* key = (const void*)kernel;
+  auto it = bps_cache.find(key);
+  int bps;
+  if (it == bps_cache.end()) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, kBlock, 0) != cudaSuccess || bps < 1) bps = 1;
+    bps_cache[key] = bps;
+  } else {
+    bps = it->second;
+  }
   long g = (work_items + kBlock - 1) / kBlock;
-  if (g > kRedGrid) g = kRedGrid;
-  if (g < 1) g = 1;
-  return (int)g;
+  g = std::min<long>(g, std::min<long>((long)sms * bps, kRedGrid));
+  return (int)std::max<long>(g, 1);
 }
 
 // matrix entries are streamed once per pass: evict-first loads keep L2 for
@@ -387,11 +409,12 @@ void row_red_launch(const DevCsr& a, const double* x, const double* b, const dou
                     Reducer* red, int slot, cudaStream_t s) {
   if (a.n_rows == 0) return;
   ++g_launch_count;
-  const int g = red_grid((long)a.n_rows * a.tpr);
+  const long work = (long)a.n_rows * a.tpr;
   Reducer r = red ? *red : Reducer{};
   const int dr = red ? 1 : 0;
-#define L_(T, VT, V) \
-  k_row_red<T, VT, MODE><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, c, r, slot, dr)
+#define L_(T, VT, V)                                                                                       \
+  k_row_red<T, VT, MODE><<<red_grid(k_row_red<T, VT, MODE>, work), kBlock, 0, s>>>(                         \
+      a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, c, r, slot, dr)
 #define D_(VT, V)                \
   switch (a.tpr) {               \
     case 1: L_(1, VT, V); break;   \
@@ -447,7 +470,7 @@ void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, do
 
 void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s) {
   ++g_launch_count;
-  k_pcg_update<<<red_grid(n), kBlock, 0, s>>>(n, x, r, p, q, red);
+  k_pcg_update<<<red_grid(k_pcg_update, n), kBlock, 0, s>>>(n, x, r, p, q, red);
 }
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s) {
   ++g_launch_count;
@@ -460,17 +483,17 @@ void launch_dense_solve(int n, const double* ainv, const double* b, double* z, c
 void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s) {
   ++g_launch_count;
   Reducer rr = red ? *red : Reducer{};
-  k_jacobi<<<red_grid(n), kBlock, 0, s>>>(n, invd, r, z, rr, slot, red ? 1 : 0);
+  k_jacobi<<<red_grid(k_jacobi, n), kBlock, 0, s>>>(n, invd, r, z, rr, slot, red ? 1 : 0);
 }
 void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, cudaStream_t s) {
   ++g_launch_count;
-  k_dot<<<red_grid(n), kBlock, 0, s>>>(n, a, b, red, slot);
+  k_dot<<<red_grid(k_dot, n), kBlock, 0, s>>>(n, a, b, red, slot);
 }
 void launch_multi_dot(int n, int m, const double* const* V, const double* w, Reducer red, int slot0, cudaStream_t s) {
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
-  k_multi_dot<<<red_grid(n), kBlock, 0, s>>>(n, m, pk, w, red, slot0);
+  k_multi_dot<<<red_grid(k_multi_dot, n), kBlock, 0, s>>>(n, m, pk, w, red, slot0);
 }
 void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s) {
   ++g_launch_count;
@@ -483,7 +506,7 @@ void launch_orth_update(int n, int m, const double* const* Q, CoefPack c, double
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = Q[k];
-  k_orth_update<<<red_grid(n), kBlock, 0, s>>>(n, m, pk, c, w, red, slot);
+  k_orth_update<<<red_grid(k_orth_update, n), kBlock, 0, s>>>(n, m, pk, c, w, red, slot);
 }
 void launch_lincomb_multi(int n, int kin, int kout, const double* const* in, double* const* out, const RotPack& T,
                           cudaStream_t s) {
@@ -528,7 +551,7 @@ void launch_axpby_into(int n, const double* y0, double c, const double* f, doubl
 void launch_rkc_error(int n, const double* x, const double* xn, const double* f0, const double* fn, double dt,
                       double atol, double rtol, Reducer red, int slot, cudaStream_t s) {
   ++g_launch_count;
-  k_rkc_error<<<red_grid(n), kBlock, 0, s>>>(n, x, xn, f0, fn, dt, atol, rtol, red, slot);
+  k_rkc_error<<<red_grid(k_rkc_error, n), kBlock, 0, s>>>(n, x, xn, f0, fn, dt, atol, rtol, red, slot);
 }
 void launch_gather(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
   if (n <= 0) return;

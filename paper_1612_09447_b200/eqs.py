@@ -169,17 +169,73 @@ class FemSystem:
     reference's dof numbering.
     """
 
-    def __init__(self, config, device: int = 0):
+    def __init__(self, config, device: int = 0, _handle=None):
         L = load_library()
-        text = config if isinstance(config, str) else json.dumps(config)
-        h = C.c_void_p()
-        _check(L.eqs_create_from_config(text.encode(), C.c_int(device), C.byref(h)))
+        if _handle is None:
+            text = config if isinstance(config, str) else json.dumps(config)
+            h = C.c_void_p()
+            _check(L.eqs_create_from_config(text.encode(), C.c_int(device), C.byref(h)))
+        else:
+            h = _handle
         self._h = h
         s = _Sizes()
         _check(L.eqs_get_sizes(h, C.byref(s)))
         self.n_nodes, self.n_tets, self.n_dofs = s.n_nodes, s.n_tets, s.n_dofs
         self.n_free, self.n_fixed, self.n_local, self.order = s.n_free, s.n_fixed, s.n_local, s.order
         self.nnz_mass_free, self.nnz_mass_ib, self.amg_n_levels = s.nnz_mass_free, s.nnz_mass_ib, s.amg_levels
+        info = np.zeros(4, dtype=np.int64)
+        _check(L.eqs_partition_info(h, info.ctypes.data_as(C.POINTER(C.c_long))))
+        self.rank, self.nranks, self.partition_levels, self.n_own = (int(v) for v in info)
+
+    # --- distributed contexts (node ownership, SURVEY.md §8e)
+    @classmethod
+    def distributed(cls, config, device: int, nranks: int, rank: int, nccl_id: bytes):
+        """One rank of a multi-GPU run (NCCL); nccl_id from nccl_unique_id() on rank 0."""
+        text = config if isinstance(config, str) else json.dumps(config)
+        h = C.c_void_p()
+        _check(load_library().eqs_create_distributed(text.encode(), C.c_int(device), C.c_int(nranks),
+                                                     C.c_int(rank), C.create_string_buffer(nccl_id, 128),
+                                                     C.byref(h)))
+        return cls(None, _handle=h)
+
+    @classmethod
+    def virtual_group(cls, config, nranks: int, device: int = 0):
+        """nranks partitions in this process (threads); drive them concurrently, one thread per rank."""
+        text = config if isinstance(config, str) else json.dumps(config)
+        hs = (C.c_void_p * nranks)()
+        _check(load_library().eqs_create_virtual_group(text.encode(), C.c_int(device), C.c_int(nranks), hs))
+        return [cls(None, _handle=C.c_void_p(hs[r])) for r in range(nranks)]
+
+    @classmethod
+    def partition_host(cls, config, nranks: int, rank: int):
+        """Host-only partition plan of one rank (no device)."""
+        text = config if isinstance(config, str) else json.dumps(config)
+        h = C.c_void_p()
+        _check(load_library().eqs_create_partition_host(text.encode(), C.c_int(nranks), C.c_int(rank),
+                                                        C.byref(h)))
+        return cls(None, _handle=h)
+
+    def partition(self, level: int = 0) -> dict:
+        L = load_library()
+        info = np.zeros(7, dtype=np.int64)
+        _check(L.eqs_partition_level(self._h, C.c_int(level), info.ctypes.data_as(C.POINTER(C.c_long))))
+        n_global, n_own, n_ghost = int(info[0]), int(info[1]), int(info[2])
+        owner = np.zeros(n_global, dtype=np.int32)
+        owned = np.zeros(max(1, n_own), dtype=np.int32)
+        ghosts = np.zeros(max(1, n_ghost), dtype=np.int32)
+        _check(L.eqs_partition_owner(self._h, C.c_int(level), _ip(owner)))
+        _check(L.eqs_partition_owned(self._h, C.c_int(level), _ip(owned)))
+        _check(L.eqs_partition_ghosts(self._h, C.c_int(level), _ip(ghosts)))
+        sends = {}
+        for q in range(self.nranks):
+            cnt = C.c_int()
+            _check(L.eqs_partition_send(self._h, C.c_int(level), C.c_int(q), None, C.byref(cnt)))
+            if cnt.value:
+                ids = np.zeros(cnt.value, dtype=np.int32)
+                _check(L.eqs_partition_send(self._h, C.c_int(level), C.c_int(q), _ip(ids), C.byref(cnt)))
+                sends[q] = ids
+        return dict(n_global=n_global, owner=owner, owned=owned[:n_own], ghosts=ghosts[:n_ghost], sends=sends,
+                    n_local_tets=int(info[5]), n_local_fixed=int(info[6]))
 
     def close(self):
         if getattr(self, "_h", None) is not None and _lib is not None:
@@ -291,7 +347,8 @@ class FemSystem:
         _check(load_library().eqs_set_state(self._h, C.c_double(t), _dp(_f64(x)), C.c_double(dt)))
 
     def get_state(self):
-        x = np.zeros(self.n_free)
+        """Owned part of the resident state (all free dofs on a single rank)."""
+        x = np.zeros(self.n_own)
         info = _StateInfo()
         _check(load_library().eqs_get_state(self._h, _dp(x), C.byref(info)))
         return x, {n: getattr(info, n) for n, _ in _StateInfo._fields_}
@@ -334,6 +391,12 @@ class FemSystem:
 
     def timing_reset(self):
         _check(load_library().eqs_timing_reset(self._h))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load_library().eqs_nccl_unique_id(buf))
+    return buf.raw
 
 
 def run_scenario(config, out_dir: str = "", device: int = 0, x_cap: int = 1 << 26) -> dict:

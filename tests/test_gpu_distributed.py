@@ -1,0 +1,96 @@
+"""Partitioned (node-ownership) path on one GPU via virtual ranks.
+
+Each virtual rank is a full GpuSystem partition (owner-computes K(x)x, owned
+rows of M_II and of every AMG level, halo exchanges before every gathered
+vector, allreduce of every dot) driven by its own host thread; the exchange
+backend is device-to-device copies instead of NCCL. Results must match the
+single-partition run to rounding (only the dot-product summation order
+differs) and the oracle to the usual 1e-9.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from helpers import cube
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+eb = pytest.importorskip("paper_1612_09447_b200")
+
+
+def run_concurrently(ctxs, fn):
+    out = [None] * len(ctxs)
+    errs = []
+
+    def work(r):
+        try:
+            out[r] = fn(ctxs[r], r)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(len(ctxs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("estimator", ["zero", "spe"])
+def test_virtual_ranks_match_single_partition(nranks, estimator):
+    cfg = cube(12, jitter=0.1, planes=(0.45, 0.55), estimator=estimator)
+    single = eb.FemSystem(cfg)
+    x0 = 2e4 * po.random_vec(single.n_free, 31)
+    single.set_state(0.0, x0, 0.0)
+    rho = single.spectral_radius()
+    dt = 0.2 * 0.653 * 15 / rho
+    single.set_state(0.0, x0, dt)
+    single.rkc_advance_fixed(dt, 4, 3)
+    xs, _ = single.get_state()
+    its_single = single.stats()["pcg_iterations"]
+
+    ctxs = eb.FemSystem.virtual_group(cfg, nranks)
+    owned = [c.partition(0)["owned"] for c in ctxs]
+    assert sorted(np.concatenate(owned).tolist()) == list(range(single.n_free))
+
+    def step(c, r):
+        c.set_state(0.0, x0[owned[r]], dt)
+        rho_r = c.spectral_radius()
+        c.rkc_advance_fixed(dt, 4, 3)
+        return rho_r, c.get_state()[0], c.stats()["pcg_iterations"]
+
+    res = run_concurrently(ctxs, step)
+    x = np.zeros(single.n_free)
+    for r, (rho_r, xr, _) in enumerate(res):
+        assert rho_r == pytest.approx(rho, rel=1e-9)
+        x[owned[r]] = xr
+    assert np.linalg.norm(x - xs) <= 1e-11 * np.linalg.norm(xs)
+    its = [it for _, _, it in res]
+    assert len(set(its)) == 1 and abs(its[0] - its_single) <= 2
+
+
+def test_virtual_ranks_match_oracle():
+    cfg = cube(10, jitter=0.1, planes=(0.45, 0.55), estimator="previous")
+    o = po.Problem(cfg)
+    x0 = 2e4 * po.random_vec(o.n_free, 31)
+    rho = o.spectral_radius(0.0, x0)
+    dt = 0.2 * 0.653 * 15 / rho
+    xo = o.rkc_advance_fixed(0.0, x0, dt, 4, 2)
+    ctxs = eb.FemSystem.virtual_group(cfg, 4)
+    owned = [c.partition(0)["owned"] for c in ctxs]
+
+    def step(c, r):
+        c.set_state(0.0, x0[owned[r]], dt)
+        c.rkc_advance_fixed(dt, 4, 2)
+        return c.get_state()[0]
+
+    res = run_concurrently(ctxs, step)
+    x = np.zeros(o.n_free)
+    for r, xr in enumerate(res):
+        x[owned[r]] = xr
+    assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)

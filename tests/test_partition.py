@@ -1,0 +1,113 @@
+"""Node-ownership partition, host logic without a GPU.
+
+The plan must be a deterministic function of the problem, bit-identical to an
+independent CPU recomputation, and consistent across ranks (what rank r sends
+to q is exactly q's ghosts owned by r, in q's order). The world-size-2 test
+runs two gloo processes that exchange their halo lists.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from helpers import cube, slab_reference
+from oracle import pyoracle as po
+
+import paper_1612_09447_b200 as eb
+
+
+def recompute_fine_owner(cfg, nranks):
+    """numpy restatement of partition_free_dofs (csrc/host_partition.cpp)."""
+    o = po.Problem(cfg)
+    nodes, tets, _ = o.mesh()
+    _, free, _, _ = o.dofs()
+    lo, hi = nodes.min(axis=0), nodes.max(axis=0)
+    ext = hi - lo
+    axis = 2
+    for k in (1, 0):
+        if ext[k] > ext[axis]:
+            axis = k
+    coord = nodes[free, axis]  # P1: dofs are nodes
+    order = np.argsort(coord, kind="stable")
+    owner = np.empty(len(free), dtype=np.int64)
+    owner[order] = (np.arange(len(free)) * nranks) // len(free)
+    return owner
+
+
+def coarse_owner(fine_owner, agg):
+    first = {}
+    for i, a in enumerate(agg):
+        first.setdefault(int(a), i)
+    return np.array([fine_owner[first[j]] for j in range(len(first))])
+
+
+CFGS = [cube(10), cube(8, jitter=0.1, planes=(0.45, 0.55)), slab_reference("slab_nonlinear_rkc_spe")]
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: c.get("name", "cfg"))
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_partition_bit_exact_and_consistent(cfg, nranks):
+    plans = [eb.FemSystem.partition_host(cfg, nranks, r) for r in range(nranks)]
+    ref = recompute_fine_owner(cfg, nranks)
+    n_levels = plans[0].partition_levels
+    for lvl in range(n_levels):
+        parts = [p.partition(lvl) for p in plans]
+        owner = parts[0]["owner"]
+        for part in parts[1:]:
+            assert np.array_equal(part["owner"], owner)  # every rank computes the same plan
+        if lvl == 0:
+            assert np.array_equal(owner, ref)
+        else:
+            agg = plans[0].amg_aggregates(lvl - 1)
+            assert np.array_equal(owner, coarse_owner(plans[0].partition(lvl - 1)["owner"], agg))
+        owned = np.concatenate([p["owned"] for p in parts])
+        assert np.array_equal(np.sort(owned), np.arange(parts[0]["n_global"]))  # a partition
+        for r, pr in enumerate(parts):
+            assert np.all(owner[pr["owned"]] == r)
+            assert np.all(owner[pr["ghosts"]] != r)
+            for q, pq in enumerate(parts):
+                if q == r:
+                    continue
+                expect = pq["ghosts"][owner[pq["ghosts"]] == r]  # q's ghosts owned by r, q's order
+                got = pr["sends"].get(q, np.zeros(0, dtype=np.int32))
+                assert np.array_equal(got, expect)
+    # owner computes: every tet with an owned free dof is local to that owner
+    tets_total = sum(p.partition(0)["n_local_tets"] for p in plans)
+    assert tets_total >= plans[0].n_tets
+
+
+def _gloo_worker(rank, world, port, cfg, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = eb.FemSystem.partition_host(cfg, world, rank)
+        mine = plan.partition(0)
+        payload = {"ghosts": mine["ghosts"].tolist(), "owner": mine["owner"].tolist(),
+                   "sends": {q: v.tolist() for q, v in mine["sends"].items()}}
+        allp = [None] * world
+        dist.all_gather_object(allp, payload)
+        ok = allp[0]["owner"] == payload["owner"]
+        for q in range(world):
+            if q == rank:
+                continue
+            expect = [g for g in allp[q]["ghosts"] if payload["owner"][g] == rank]
+            ok = ok and payload["sends"].get(q, []) == expect
+        out[rank] = bool(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world_size_2_gloo_halo_lists_agree():
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gloo_worker, args=(2, port, cube(8, jitter=0.1), out), nprocs=2, join=True)
+    assert out[0] and out[1]
