@@ -182,8 +182,9 @@ int eqs_create_virtual_group(const char* json_text, int device, int nranks, eqs_
 int eqs_create_partition_host(const char* json_text, int nranks, int rank, eqs_ctx** out);
 /* partition of the context's rank: info = {rank, nranks, levels, n_own(level 0)} */
 int eqs_partition_info(eqs_ctx* ctx, long* info4);
-/* level sizes {n_global, n_own, n_ghost, n_peers_recv, n_peers_send, n_local_tets, n_local_fixed} */
-int eqs_partition_level(eqs_ctx* ctx, int level, long* info7);
+/* level sizes {n_global, n_own, n_ghost, n_peers_recv, n_peers_send, n_local_tets, n_local_fixed,
+   replicated (1: the level is held whole on every rank)} */
+int eqs_partition_level(eqs_ctx* ctx, int level, long* info8);
 /* owner rank per global index of a level; owned / ghost global ids of this rank */
 int eqs_partition_owner(eqs_ctx* ctx, int level, int* owner);
 int eqs_partition_owned(eqs_ctx* ctx, int level, int* ids);

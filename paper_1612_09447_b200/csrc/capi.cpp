@@ -248,6 +248,7 @@ int eqs_partition_level(eqs_ctx* ctx, int level, long* info) {
     info[4] = (long)s.send_ranks.size();
     info[5] = (long)p.tets.size();
     info[6] = (long)p.fixed.size();
+    info[7] = level >= p.rep_level ? 1 : 0;
   });
 }
 

@@ -77,6 +77,7 @@ struct SolverParams {
   double amg_theta = 0.08, amg_omega = 4.0 / 3.0;
   int amg_sweeps = 1, amg_max_levels = 10, amg_coarse_limit = 64;
   double amg_coarse_filter = 0.0025;  // additive: V-cycle coarse-operator filter (0 = off)
+  int amg_replicate_rows = 32768;     // additive: coarse levels up to this size are replicated on every rank
   int estimator_mode = 0;  // 0 zero, 1 previous, 2 spe
   int spe_window = 8;
   double mgs_drop_tol = 1e-8;

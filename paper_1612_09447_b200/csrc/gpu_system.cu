@@ -131,7 +131,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     for (size_t l = 1; l + 1 < vh.levels.size(); ++l)
       if (eps > 0.0) vh.levels[l].A = filter_lumped(amg_.levels[l].A, eps);
   }
-  plan_ = build_plan(prob_, m_ii_, m_ib_, vh, comm_->size(), comm_->rank());
+  plan_ = build_plan(prob_, m_ii_, m_ib_, vh, comm_->size(), comm_->rank(), prob_.solver.amg_replicate_rows);
   const LocalSpace& s0 = plan_.space[0];
   n_own_ = s0.n_own();
   n_ghost_ = s0.n_ghost();
@@ -340,6 +340,7 @@ void GpuSystem::build_levels() {
     lv.n_own = sp.n_own();
     lv.n_loc = sp.n_local();
     lv.n_global = sp.n_global;
+    lv.replicated = l >= plan_.rep_level;
     if (l == 0) {
       lv.A = mii_;  // shares indices / fp64 values with the PCG operator
     } else {
@@ -362,8 +363,9 @@ void GpuSystem::build_levels() {
       lv.invd.alloc(nloc);
       lv.invd.upload(invd.data(), invd.size(), s);
       halo(lv.halo, lv.invd.p);
-    } else {
-      // coarsest: every rank solves the (<= coarse_limit) dense system on the full vector
+    } else if (!lv.replicated) {
+      // partitioned coarsest (single-level hierarchy): every rank solves the
+      // dense system on the full vector assembled by scatter + allreduce
       std::vector<int> glob(nloc, 0);
       for (int i = 0; i < lv.n_loc; ++i) glob[i] = i < lv.n_own ? sp.owned[i] : sp.ghosts[i - lv.n_own];
       lv.glob.alloc(glob.size());
@@ -398,7 +400,8 @@ void GpuSystem::build_levels() {
     for (int it = 0; it < 20; ++it) {
       halo(lv.halo, lv.z.p);
       launch_scaled_spmv(lv.A, lv.invd.p, lv.z.p, lv.t.p, s);
-      lam = std::sqrt(dot_n(lv.n_own, lv.t.p, lv.t.p, S_NORM));
+      lam = std::sqrt(lv.replicated ? dot_local(lv.n_own, lv.t.p, lv.t.p, S_NORM)
+                                    : dot_n(lv.n_own, lv.t.p, lv.t.p, S_NORM));
       if (lam == 0.0) {
         lam = 1.0;
         break;
@@ -409,6 +412,12 @@ void GpuSystem::build_levels() {
     lv.lambda_smoother = l == 0 ? std::max(lam, amg_.levels[l].lambda_max_scaled) : lam;
   }
   set_cheb(cheb_ratio);
+}
+
+// dot over n local entries of a replicated level (no reduction), read on the host
+double GpuSystem::dot_local(int n, const double* a, const double* b, int slot) {
+  launch_dot(n, a, b, red_, slot, stream_);
+  return read_scalar(slot);
 }
 
 // global dot over n owned entries (reduced over ranks), read on the host
@@ -651,9 +660,9 @@ double* GpuSystem::vcycle(int l, const double* b_in, bool dot_into_rz) {
   DevLevel& lv = levels_[l];
   double* b = const_cast<double*>(b_in);
   if (l == L - 1) {
-    // replicated dense solve: assemble the full right-hand side on every rank
+    // dense solve on the full vector (replicated level: b is already whole)
     double* z = lv.z.p;
-    if (comm_->size() == 1) {
+    if (comm_->size() == 1 || lv.replicated) {
       launch_dense_solve(coarse_n_, coarse_inv_.p, b, z, stream_);
     } else {
       launch_fill(coarse_n_, 0.0, lv.full_b.p, stream_);
@@ -685,8 +694,11 @@ double* GpuSystem::vcycle(int l, const double* b_in, bool dot_into_rz) {
   }
   halo(lv.halo, lv.t.p);
   launch_spmv(lv.R, lv.t.p, nx.b.p, stream_);
+  // entering the replicated levels: every rank holds the partial restriction
+  // of its owned rows for all coarse rows; the sum is the coarse right-hand side
+  if (nx.replicated && !lv.replicated && comm_->size() > 1) comm_->allreduce(nx.b.p, nx.n_loc, stream_);
   double* zc = vcycle(l + 1, nx.b.p, false);
-  if (l + 1 < L - 1) halo(nx.halo, zc);  // the coarsest returns its ghosts already
+  halo(nx.halo, zc);  // no-op on replicated levels
   launch_prolong_add(lv.P, zc, z, stream_);
   halo(lv.halo, z);
   if (deg >= 2) {

@@ -74,6 +74,7 @@ struct DevHalo {
 
 struct DevLevel {
   int n_own = 0, n_loc = 0, n_global = 0;
+  bool replicated = false;           // held whole on every rank (partition.hpp rep_level)
   DevCsr A, P, R;
   DevBuf<int> a_rp, a_ci, p_rp, p_ci, r_rp, r_ci;
   DevBuf<double> a_v, p_v, r_v;
@@ -82,8 +83,8 @@ struct DevLevel {
   ChebCoef cheb{}, cheb1{};          // degree-2 and degree-1 Chebyshev coefficients
   double lambda_smoother = 0;
   DevHalo halo;
-  DevBuf<int> glob;                  // coarsest level: local -> global ids (replicated dense solve)
-  DevBuf<double> full_b, full_z;     // coarsest level: replicated vectors
+  DevBuf<int> glob;                  // partitioned coarsest level: local -> global ids
+  DevBuf<double> full_b, full_z;     // partitioned coarsest level: whole vectors for the dense solve
 };
 
 // timing classes (eqs_timing in include/eqs_b200.h)
@@ -185,6 +186,7 @@ class GpuSystem {
   double read_scalar(int slot);
   void read_scalars(int first, int count, double* out);
   double dot_n(int n, const double* a, const double* b, int slot);  // global dot over n owned entries
+  double dot_local(int n, const double* a, const double* b, int slot);  // no reduction over ranks
   double dot_own(const double* a, const double* b, int slot);       // level-0 owned entries
   void check_kernel_flags();
   void sync();

@@ -1,6 +1,7 @@
 // Deterministic node-ownership partition of the fine dofs and of the AMG
 // hierarchy: owner-computes for the stiffness operator, owned
-// rows + ghost columns for every CSR operator, halo lists per peer.
+// rows + ghost columns for every CSR operator, halo lists per peer, and
+// replicated (agglomerated) small coarse levels.
 #include <omp.h>
 
 #include <algorithm>
@@ -30,27 +31,44 @@ std::vector<double> dof_coords(const Problem& p) {
   return c;
 }
 
-HostCsr local_rows(const HostCsr& a, const std::vector<int>& rows, const std::vector<int>& g2l_cols) {
+// rows `rows` of a (all rows when rows == nullptr); columns mapped through
+// g2l (identity when empty); entries whose column maps to -1 are an error
+// unless drop_unmapped (then they are skipped)
+HostCsr local_rows(const HostCsr& a, const std::vector<int>* rows, const std::vector<int>& g2l, int n_cols,
+                   bool drop_unmapped = false) {
   HostCsr out;
-  out.n_rows = (int)rows.size();
-  out.row_ptr.assign(rows.size() + 1, 0);
-  for (size_t r = 0; r < rows.size(); ++r) out.row_ptr[r + 1] = out.row_ptr[r] + (a.row_ptr[rows[r] + 1] - a.row_ptr[rows[r]]);
+  const long nr = rows ? (long)rows->size() : a.n_rows;
+  auto row_of = [&](long r) { return rows ? (*rows)[r] : (int)r; };
+  out.n_rows = (int)nr;
+  out.n_cols = n_cols;
+  out.row_ptr.assign(nr + 1, 0);
+#pragma omp parallel for schedule(static)
+  for (long r = 0; r < nr; ++r) {
+    int cnt = 0;
+    const int i = row_of(r);
+    for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k)
+      if (g2l.empty() || !drop_unmapped || g2l[a.col_idx[k]] >= 0) ++cnt;
+    out.row_ptr[r + 1] = cnt;
+  }
+  for (long r = 0; r < nr; ++r) out.row_ptr[r + 1] += out.row_ptr[r];
   out.col_idx.resize(out.row_ptr.back());
   out.values.resize(out.row_ptr.back());
-  int max_col = -1, bad = 0;
-#pragma omp parallel for schedule(static) reduction(max : max_col, bad)
-  for (long r = 0; r < (long)rows.size(); ++r) {
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+  for (long r = 0; r < nr; ++r) {
     int pos = out.row_ptr[r];
-    for (int k = a.row_ptr[rows[r]]; k < a.row_ptr[rows[r] + 1]; ++k) {
-      const int lc = g2l_cols.empty() ? a.col_idx[k] : g2l_cols[a.col_idx[k]];
-      if (lc < 0) bad = 1;
+    const int i = row_of(r);
+    for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+      const int lc = g2l.empty() ? a.col_idx[k] : g2l[a.col_idx[k]];
+      if (lc < 0) {
+        if (!drop_unmapped) bad = 1;
+        continue;
+      }
       out.col_idx[pos] = lc;
       out.values[pos++] = a.values[k];
-      max_col = std::max(max_col, lc);
     }
   }
   if (bad) throw std::logic_error("partition: column without a local index");
-  out.n_cols = max_col + 1;
   return out;
 }
 
@@ -70,24 +88,37 @@ std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out
   for (int k : {1, 0})
     if (hi[k] - lo[k] > hi[axis] - lo[axis]) axis = k;
   if (axis_out) *axis_out = axis;
+  std::vector<int> owner(nf, 0);
+  if (nranks == 1) return owner;
   std::vector<int> order(nf);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     return c[3L * dm.free_dofs[a] + axis] < c[3L * dm.free_dofs[b] + axis];
   });
-  std::vector<int> owner(nf);
   for (long k = 0; k < nf; ++k) owner[order[k]] = (int)(k * nranks / std::max(1, nf));
   return owner;
 }
 
 PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m_ib, const AmgHierarchy& h,
-                         int nranks, int rank) {
+                         int nranks, int rank, int rep_threshold) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("build_plan: bad rank/nranks");
   PartitionPlan plan;
   plan.nranks = nranks;
   plan.rank = rank;
   const int L = h.levels.empty() ? 1 : (int)h.levels.size();
   auto A_of = [&](int l) -> const HostCsr& { return h.levels.empty() ? m_ii : h.levels[l].A; };
+  // first replicated level: small coarse levels (and always the dense coarsest)
+  // are held whole on every rank; a single level (no hierarchy) stays partitioned
+  int rep = L;
+  if (L > 1) {
+    rep = L - 1;
+    for (int l = 1; l < L; ++l)
+      if (A_of(l).n_rows <= rep_threshold) {
+        rep = l;
+        break;
+      }
+  }
+  plan.rep_level = rep;
   // ownership per level
   plan.owner.resize(L);
   plan.owner[0] = partition_free_dofs(p, nranks, &plan.axis);
@@ -100,15 +131,24 @@ PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m
     plan.owner[l + 1].resize(nc);
     for (int j = 0; j < nc; ++j) plan.owner[l + 1][j] = plan.owner[l][first[j]];
   }
-  // rows owned by every rank, per level
+  // rows owned by every rank, per partitioned level
   std::vector<std::vector<std::vector<int>>> rows_of(L, std::vector<std::vector<int>>(nranks));
-  for (int l = 0; l < L; ++l)
+  for (int l = 0; l < std::min(rep, L); ++l)
     for (int i = 0; i < (int)plan.owner[l].size(); ++i) rows_of[l][plan.owner[l][i]].push_back(i);
-  // ghost sets of every rank per level: columns (level l) of A_l[own_l], R_l[own_l+1], P_l-1[own_l-1]
   plan.space.resize(L);
   std::vector<std::vector<int>> g2l(L);
   for (int l = 0; l < L; ++l) {
     const std::vector<int>& own = plan.owner[l];
+    LocalSpace& sp = plan.space[l];
+    sp.n_global = (int)own.size();
+    if (l >= rep) {  // replicated: every rank holds the whole level, no halo
+      sp.owned.resize(sp.n_global);
+      std::iota(sp.owned.begin(), sp.owned.end(), 0);
+      g2l[l] = sp.owned;
+      continue;
+    }
+    // ghost sets of every rank: columns (level l) of A_l[own_l], R_l[own_l+1]
+    // (when l+1 is partitioned), P_l-1[own_l-1]
     std::vector<std::vector<int>> ghosts(nranks);
 #pragma omp parallel for schedule(dynamic, 1)
     for (int q = 0; q < nranks; ++q) {
@@ -119,14 +159,12 @@ PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m
             if (own[m.col_idx[k]] != q) gs.push_back(m.col_idx[k]);
       };
       scan(A_of(l), rows_of[l][q]);
-      if (l + 1 < L) scan(h.levels[l].R, rows_of[l + 1][q]);
+      if (l + 1 < rep) scan(h.levels[l].R, rows_of[l + 1][q]);
       if (l >= 1) scan(h.levels[l - 1].P, rows_of[l - 1][q]);
       std::sort(gs.begin(), gs.end());
       gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
       std::stable_sort(gs.begin(), gs.end(), [&](int a, int b) { return own[a] < own[b]; });
     }
-    LocalSpace& sp = plan.space[l];
-    sp.n_global = (int)own.size();
     sp.owned = rows_of[l][rank];
     sp.ghosts = ghosts[rank];
     g2l[l].assign(own.size(), -1);
@@ -157,25 +195,33 @@ PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m
   plan.P.resize(L);
   plan.R.resize(L);
   for (int l = 0; l < L; ++l) {
-    plan.A[l] = local_rows(A_of(l), plan.space[l].owned, g2l[l]);
-    plan.A[l].n_cols = plan.space[l].n_local();
+    const LocalSpace& sp = plan.space[l];
+    const bool part = l < rep;
+    plan.A[l] = part ? local_rows(A_of(l), &sp.owned, g2l[l], sp.n_local()) : local_rows(A_of(l), nullptr, {}, sp.n_global);
     if (l + 1 < L) {
-      plan.P[l] = local_rows(h.levels[l].P, plan.space[l].owned, g2l[l + 1]);
-      plan.P[l].n_cols = plan.space[l + 1].n_local();
-      plan.R[l] = local_rows(h.levels[l].R, plan.space[l + 1].owned, g2l[l]);
-      plan.R[l].n_cols = plan.space[l].n_local();
+      const LocalSpace& sc = plan.space[l + 1];
+      plan.P[l] = part ? local_rows(h.levels[l].P, &sp.owned, g2l[l + 1], sc.n_local())
+                       : local_rows(h.levels[l].P, nullptr, {}, sc.n_global);
+      if (l + 1 < rep) {
+        plan.R[l] = local_rows(h.levels[l].R, &sc.owned, g2l[l], sp.n_local());
+      } else if (part) {
+        // restriction into a replicated level: all coarse rows, owned fine
+        // columns only; the ranks' partial results are summed by allreduce
+        std::vector<int> own_only(sp.n_global, -1);
+        for (int i = 0; i < sp.n_own(); ++i) own_only[sp.owned[i]] = i;
+        plan.R[l] = local_rows(h.levels[l].R, nullptr, own_only, sp.n_local(), true);
+      } else {
+        plan.R[l] = local_rows(h.levels[l].R, nullptr, {}, sp.n_global);
+      }
     }
   }
-  plan.mii = h.levels.empty() ? plan.A[0] : local_rows(m_ii, plan.space[0].owned, g2l[0]);
-  plan.mii.n_cols = plan.space[0].n_local();
-  plan.mib = local_rows(m_ib, plan.space[0].owned, {});
-  plan.mib.n_cols = m_ib.n_cols;
+  plan.mii = h.levels.empty() ? plan.A[0] : local_rows(m_ii, &plan.space[0].owned, g2l[0], plan.space[0].n_local());
+  plan.mib = local_rows(m_ib, &plan.space[0].owned, {}, m_ib.n_cols);
   // stiffness operator: tets touching an owned free dof, local full numbering
   const Dofs& dm = p.dm;
   const int nl = dm.n_local;
-  std::vector<int> free_index(dm.n_dofs, -1), fixed_index(dm.n_dofs, -1);
+  std::vector<int> free_index(dm.n_dofs, -1);
   for (int i = 0; i < dm.n_free(); ++i) free_index[dm.free_dofs[i]] = i;
-  for (int i = 0; i < dm.n_fixed(); ++i) fixed_index[dm.fixed_dofs[i]] = i;
   std::vector<char> fixed_used(dm.n_dofs, 0);
   for (int t = 0; t < p.mesh.n_tets; ++t) {
     bool mine = false;
@@ -209,7 +255,6 @@ PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m
       plan.tet_dofs[k * nl + i] = loc;
     }
   if (bad) throw std::logic_error("partition: tet dof without a local index");
-  (void)fixed_index;
   return plan;
 }
 

@@ -27,6 +27,7 @@ struct LocalSpace {
 
 struct PartitionPlan {
   int nranks = 1, rank = 0, axis = 2;
+  int rep_level = 1;                    // levels >= rep_level are replicated whole on every rank
   std::vector<std::vector<int>> owner;  // per level: global id -> rank
   std::vector<LocalSpace> space;        // per level, this rank
   // this rank's rows with local column ids
@@ -45,8 +46,12 @@ struct PartitionPlan {
 // contiguous equal chunks
 std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out = nullptr);
 
-// full plan for `rank` (levels from the AMG hierarchy; a single level when h is empty)
+// full plan for `rank` (levels from the AMG hierarchy; a single level when h
+// is empty). Coarse levels with at most rep_threshold rows, and always the
+// dense coarsest level, are replicated: every rank holds all rows, the
+// restriction into the first replicated level sums the ranks' partial
+// products (allreduce), and no halo is exchanged below it.
 PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m_ib, const AmgHierarchy& h,
-                         int nranks, int rank);
+                         int nranks, int rank, int rep_threshold);
 
 }  // namespace eqsb

@@ -217,7 +217,7 @@ class FemSystem:
 
     def partition(self, level: int = 0) -> dict:
         L = load_library()
-        info = np.zeros(7, dtype=np.int64)
+        info = np.zeros(8, dtype=np.int64)
         _check(L.eqs_partition_level(self._h, C.c_int(level), info.ctypes.data_as(C.POINTER(C.c_long))))
         n_global, n_own, n_ghost = int(info[0]), int(info[1]), int(info[2])
         owner = np.zeros(n_global, dtype=np.int32)
@@ -235,7 +235,7 @@ class FemSystem:
                 _check(L.eqs_partition_send(self._h, C.c_int(level), C.c_int(q), _ip(ids), C.byref(cnt)))
                 sends[q] = ids
         return dict(n_global=n_global, owner=owner, owned=owned[:n_own], ghosts=ghosts[:n_ghost], sends=sends,
-                    n_local_tets=int(info[5]), n_local_fixed=int(info[6]))
+                    n_local_tets=int(info[5]), n_local_fixed=int(info[6]), replicated=bool(info[7]))
 
     def close(self):
         if getattr(self, "_h", None) is not None and _lib is not None:

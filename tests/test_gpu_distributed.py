@@ -41,9 +41,12 @@ def run_concurrently(ctxs, fn):
 
 
 @pytest.mark.parametrize("nranks", [2, 3])
-@pytest.mark.parametrize("estimator", ["zero", "spe"])
-def test_virtual_ranks_match_single_partition(nranks, estimator):
+@pytest.mark.parametrize("estimator,replicate", [("zero", 32768), ("spe", 32768), ("zero", 0)])
+def test_virtual_ranks_match_single_partition(nranks, estimator, replicate):
+    """replicate: coarse levels up to this many rows are held whole on every
+    rank (0: only the dense coarsest)."""
     cfg = cube(12, jitter=0.1, planes=(0.45, 0.55), estimator=estimator)
+    cfg["solver"]["amg_replicate_rows"] = replicate
     single = eb.FemSystem(cfg)
     x0 = 2e4 * po.random_vec(single.n_free, 31)
     single.set_state(0.0, x0, 0.0)

@@ -5,6 +5,7 @@ independent CPU recomputation, and consistent across ranks (what rank r sends
 to q is exactly q's ghosts owned by r, in q's order). The world-size-2 test
 runs two gloo processes that exchange their halo lists.
 """
+import copy
 import os
 import socket
 
@@ -42,15 +43,31 @@ def coarse_owner(fine_owner, agg):
     return np.array([fine_owner[first[j]] for j in range(len(first))])
 
 
-CFGS = [cube(10), cube(8, jitter=0.1, planes=(0.45, 0.55)), slab_reference("slab_nonlinear_rkc_spe")]
+def with_replication(cfg, rows):
+    cfg = copy.deepcopy(cfg)
+    cfg.setdefault("solver", {})["amg_replicate_rows"] = rows
+    return cfg
 
 
-@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: c.get("name", "cfg"))
+CFGS = [cube(10), with_replication(cube(10), 0), with_replication(cube(8, jitter=0.1, planes=(0.45, 0.55)), 200),
+        slab_reference("slab_nonlinear_rkc_spe")]
+
+
+def expected_rep_level(sizes, rows):
+    """First coarse level with at most `rows` rows, else the coarsest (csrc/host_partition.cpp)."""
+    if len(sizes) == 1:
+        return 1
+    return next((l for l in range(1, len(sizes)) if sizes[l] <= rows), len(sizes) - 1)
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=lambda c: f'{c.get("name", "cfg")}-rep{c.get("solver", {}).get("amg_replicate_rows", "default")}')
 @pytest.mark.parametrize("nranks", [2, 3, 4])
 def test_partition_bit_exact_and_consistent(cfg, nranks):
     plans = [eb.FemSystem.partition_host(cfg, nranks, r) for r in range(nranks)]
     ref = recompute_fine_owner(cfg, nranks)
     n_levels = plans[0].partition_levels
+    sizes = [plans[0].partition(l)["n_global"] for l in range(n_levels)]
+    rep = expected_rep_level(sizes, cfg.get("solver", {}).get("amg_replicate_rows", 32768))
     for lvl in range(n_levels):
         parts = [p.partition(lvl) for p in plans]
         owner = parts[0]["owner"]
@@ -61,6 +78,13 @@ def test_partition_bit_exact_and_consistent(cfg, nranks):
         else:
             agg = plans[0].amg_aggregates(lvl - 1)
             assert np.array_equal(owner, coarse_owner(plans[0].partition(lvl - 1)["owner"], agg))
+        if lvl >= rep:  # replicated: whole level on every rank, no halo
+            for pr in parts:
+                assert pr["replicated"]
+                assert np.array_equal(pr["owned"], np.arange(pr["n_global"]))
+                assert len(pr["ghosts"]) == 0 and not pr["sends"]
+            continue
+        assert not any(pr["replicated"] for pr in parts)
         owned = np.concatenate([p["owned"] for p in parts])
         assert np.array_equal(np.sort(owned), np.arange(parts[0]["n_global"]))  # a partition
         for r, pr in enumerate(parts):
