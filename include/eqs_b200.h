@@ -267,7 +267,11 @@ int eqs_timing_get(eqs_ctx* ctx, eqs_timing* out);
 int eqs_timing_reset(eqs_ctx* ctx);
 /* Tuning knobs (not in the reference): 0 = stiffness mode (0 gather, 1 coloured),
  * 1 = fine-level Chebyshev degree (1 or 2), 2 = Chebyshev eigenvalue ratio,
- * 3 = coarse-level Chebyshev degree (1 or 2), 4 = fp32 V-cycle matrices (0/1). */
+ * 3 = coarse-level Chebyshev degree (1 or 2), 4 = V-cycle matrix values
+ * (0 fp64, 1 fp32, 2 bf16; default 2), 5/6/7 = CSR threads per row of levels
+ * 0/1/2, 8 = CUDA graphs (0/1), 9 = incremental SPE (0/1), 10 = SELL-16
+ * operators (0/1; default 1), 11 = fp32 V-cycle vectors (0/1; default 1).
+ * The PCG operator and vectors are fp64 in every setting. */
 int eqs_set_option(eqs_ctx* ctx, int key, double value);
 /* The CUDA stream (cudaStream_t) every device call of this context runs on. */
 int eqs_get_stream(eqs_ctx* ctx, void** stream);

@@ -527,12 +527,14 @@ int eqs_set_option(eqs_ctx* ctx, int key, double value) {
       case 1: g.cheb_degree = (int)value; g.invalidate_graphs(); break;
       case 2: g.set_cheb(value); break;
       case 3: g.coarse_degree = (int)value; g.invalidate_graphs(); break;
-      case 4: g.set_vcycle_fp32(value != 0.0); break;
+      case 4: g.set_vcycle_precision((int)value); break;
       case 5: g.set_level_tpr(0, (int)value); break;
       case 6: g.set_level_tpr(1, (int)value); break;
       case 7: g.set_level_tpr(2, (int)value); break;
       case 8: g.use_graphs = value != 0.0; g.invalidate_graphs(); break;
       case 9: g.spe_incremental = value != 0.0; break;
+      case 10: g.set_sell(value != 0.0); break;
+      case 11: g.set_vcycle_vectors_f32(value != 0.0); break;
       default: throw std::invalid_argument("eqs_set_option: unknown key");
     }
   });

@@ -95,17 +95,21 @@ class ThreadComm final : public Comm {
   bool capturable() const override { return false; }
   void barrier() override { g_->barrier(); }
   // deterministic: every rank sums the contributions in rank order
-  void allreduce(double* dev, int count, cudaStream_t s) override {
+  void allreduce(double* dev, int count, cudaStream_t s) override { sum_in_rank_order(dev, count, s); }
+  void allreduce(float* dev, int count, cudaStream_t s) override { sum_in_rank_order(dev, count, s); }
+  template <class T>
+  void sum_in_rank_order(T* dev, int count, cudaStream_t s) {
     std::vector<double>& mine = g_->partial[rank_];
-    mine.resize(count);
-    ck(cudaMemcpyAsync(mine.data(), dev, sizeof(double) * count, cudaMemcpyDeviceToHost, s), "allreduce d2h");
+    std::vector<T> buf(count);
+    ck(cudaMemcpyAsync(buf.data(), dev, sizeof(T) * count, cudaMemcpyDeviceToHost, s), "allreduce d2h");
     ck(cudaStreamSynchronize(s), "allreduce sync");
+    mine.assign(buf.begin(), buf.end());
     g_->barrier();
-    std::vector<double> sum(count, 0.0);
+    std::vector<T> sum(count, T(0));
     for (int r = 0; r < g_->n; ++r)
-      for (int i = 0; i < count; ++i) sum[i] += g_->partial[r][i];
+      for (int i = 0; i < count; ++i) sum[i] += (T)g_->partial[r][i];
     g_->barrier();
-    ck(cudaMemcpyAsync(dev, sum.data(), sizeof(double) * count, cudaMemcpyHostToDevice, s), "allreduce h2d");
+    ck(cudaMemcpyAsync(dev, sum.data(), sizeof(T) * count, cudaMemcpyHostToDevice, s), "allreduce h2d");
     ck(cudaStreamSynchronize(s), "allreduce sync");
   }
   void exchange(const std::vector<HaloMsg>& msgs, cudaStream_t s) override {
@@ -118,7 +122,7 @@ class ThreadComm final : public Comm {
       for (const HaloMsg& o : g_->posted[m.peer])
         if (o.peer == rank_) src = &o;
       if (!src || src->send_count != m.recv_count) throw std::logic_error("thread comm: unmatched halo message");
-      ck(cudaMemcpyAsync(m.recv, src->send, sizeof(double) * m.recv_count, cudaMemcpyDefault, s), "halo copy");
+      ck(cudaMemcpyAsync(m.recv, src->send, (size_t)m.elem_bytes * m.recv_count, cudaMemcpyDefault, s), "halo copy");
     }
     ck(cudaStreamSynchronize(s), "exchange sync");
     g_->barrier();  // peers may reuse their send buffers now
@@ -152,14 +156,18 @@ class NcclComm final : public Comm {
     ck(cudaStreamSynchronize(0), "barrier sync");
     cudaFree(d);
   }
+  void allreduce(float* dev, int count, cudaStream_t s) override {
+    nck(nccl().AllReduce(dev, dev, count, ncclFloat, ncclSum, comm_, s), "ncclAllReduce");
+  }
   void allreduce(double* dev, int count, cudaStream_t s) override {
     nck(nccl().AllReduce(dev, dev, count, ncclDouble, ncclSum, comm_, s), "ncclAllReduce");
   }
   void exchange(const std::vector<HaloMsg>& msgs, cudaStream_t s) override {
     nck(nccl().GroupStart(), "ncclGroupStart");
     for (const HaloMsg& m : msgs) {
-      if (m.send_count > 0) nck(nccl().Send(m.send, m.send_count, ncclDouble, m.peer, comm_, s), "ncclSend");
-      if (m.recv_count > 0) nck(nccl().Recv(m.recv, m.recv_count, ncclDouble, m.peer, comm_, s), "ncclRecv");
+      const ncclDataType_t t = m.elem_bytes == 4 ? ncclFloat : ncclDouble;
+      if (m.send_count > 0) nck(nccl().Send(m.send, m.send_count, t, m.peer, comm_, s), "ncclSend");
+      if (m.recv_count > 0) nck(nccl().Recv(m.recv, m.recv_count, t, m.peer, comm_, s), "ncclRecv");
     }
     nck(nccl().GroupEnd(), "ncclGroupEnd");
   }

@@ -19,10 +19,11 @@ namespace eqsb {
 
 struct HaloMsg {
   int peer;
-  const double* send;  // device
-  int send_count;
-  double* recv;        // device
+  const void* send;    // device
+  int send_count;      // elements
+  void* recv;          // device
   int recv_count;
+  int elem_bytes = 8;  // 8: fp64 vectors, 4: fp32 (V-cycle) vectors
 };
 
 class Comm {
@@ -33,6 +34,7 @@ class Comm {
   virtual bool capturable() const = 0;  // may be recorded into a CUDA graph
   // in-place sum over ranks of `count` doubles in device memory
   virtual void allreduce(double* dev, int count, cudaStream_t s) = 0;
+  virtual void allreduce(float* dev, int count, cudaStream_t s) = 0;
   // point-to-point exchange: every message's send buffer goes to `peer`,
   // every recv buffer is filled from `peer` (pairs must match on both sides)
   virtual void exchange(const std::vector<HaloMsg>& msgs, cudaStream_t s) = 0;
@@ -45,6 +47,7 @@ class SelfComm final : public Comm {
   int size() const override { return 1; }
   bool capturable() const override { return true; }
   void allreduce(double*, int, cudaStream_t) override {}
+  void allreduce(float*, int, cudaStream_t) override {}
   void exchange(const std::vector<HaloMsg>&, cudaStream_t) override {}
   void barrier() override {}
 };
@@ -58,6 +61,7 @@ class StaticComm final : public Comm {
   int size() const override { return size_; }
   bool capturable() const override { return false; }
   void allreduce(double*, int, cudaStream_t) override { throw std::logic_error("StaticComm: no collectives"); }
+  void allreduce(float*, int, cudaStream_t) override { throw std::logic_error("StaticComm: no collectives"); }
   void exchange(const std::vector<HaloMsg>&, cudaStream_t) override {
     throw std::logic_error("StaticComm: no collectives");
   }

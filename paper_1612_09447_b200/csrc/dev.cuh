@@ -12,6 +12,8 @@ constexpr int kBlock = 256;
 
 // number of kernels this library has launched (bench.py's gpu_launches)
 extern long g_launch_count;
+// algorithmic HBM bytes of the sparse row kernels launched so far (roofline accounting)
+extern double g_algo_bytes;
 // Reduction kernels run grid-stride on a fixed grid so that the partial-sum
 // count (and therefore the summation order) is fixed: deterministic results.
 constexpr int kRedGrid = 148 * 8;
@@ -38,15 +40,33 @@ struct Reducer {
   double* scal;       // [S_COUNT] results
 };
 
-// CSR matrix resident in HBM (int32 indices, fp64 values, sorted columns).
+// Sliced-ELL copy with packed 16-bit columns (sell.hpp); tpr == 0: absent.
+struct DevSell {
+  int tpr = 0, n_chunks = 0;
+  long padded = 0;                   // stored entries (nnz + padding)
+  const long* chunk_ptr = nullptr;   // [n_chunks + 1]
+  const int* bases = nullptr;        // [n_chunks][8]
+  const uint16_t* code = nullptr;    // (window << 13) | (column - base)
+  const double* v64 = nullptr;
+  const float* v32 = nullptr;
+  const uint16_t* v16 = nullptr;     // bf16 bit patterns
+};
+
+// CSR matrix resident in HBM (int32 indices, fp64 values, sorted columns),
+// optionally with reduced-precision value copies and a SELL copy that the
+// kernels use instead when `use_sell` is set.
 struct DevCsr {
   int n_rows = 0, n_cols = 0;
   long nnz = 0;
   int* row_ptr = nullptr;
   int* col_idx = nullptr;
   double* values = nullptr;
-  float* values_f = nullptr;  // when set, kernels read fp32 values (V-cycle copies only)
-  int tpr = 4;                // threads per row used by the SpMV kernels
+  float* values_f = nullptr;  // fp32 copy (V-cycle operators only)
+  int tpr = 4;                // threads per row used by the CSR kernels
+  int prec = 0;               // values read by the kernels: 0 fp64, 1 fp32, 2 bf16 (SELL only; CSR reads fp32)
+  bool use_sell = false;
+  DevSell sell;
+  int lanes() const { return use_sell ? sell.tpr : tpr; }
 };
 
 struct ChebCoef {
@@ -76,33 +96,55 @@ void launch_kx_colored(int order, int n_batch, const int* batch_tets, const int*
                        const unsigned char* tet_mat, const double* coords, const double* x_state, const double* v,
                        double* y, int* geo_error, cudaStream_t s);
 
-// ---- sparse linear algebra (k_sparse.cu)
-void launch_spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s);
+// ---- matrix row kernels (k_rows.cu). XT is the vector type: fp64 for the PCG
+// operator, fp32 or fp64 for the V-cycle; matrix values per
+// DevCsr::prec. Every launcher adds its algorithmic bytes to g_algo_bytes.
+// algorithmic bytes of one pass over `a` (resident format) with `gathered`
+// column vectors and `streamed` row vectors of `xbytes` each
+double matrix_pass_bytes(const DevCsr& a, int gathered, int streamed, int xbytes = 8);
+template <class XT>
+void launch_spmv(const DevCsr& a, const XT* x, XT* y, cudaStream_t s);
 // y = b - A x, and (if red) ||y||^2 into slot
-void launch_residual(const DevCsr& a, const double* b, const double* x, double* y, Reducer* red, int slot,
-                     cudaStream_t s);
+template <class XT>
+void launch_residual(const DevCsr& a, const XT* b, const XT* x, XT* y, Reducer* red, int slot, cudaStream_t s);
 // q = A p ; slot <- p.q
 void launch_spmv_dot(const DevCsr& a, const double* p, double* q, Reducer red, int slot, cudaStream_t s);
-// x += alpha p ; r -= alpha q ; slot_rr <- r.r ; alpha = scal[S_RZ]/scal[S_PQ]
-void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s);
+// Chebyshev(2) smoother pieces (DESIGN.md §4)
+template <class XT>
+void launch_cheb_pre(const DevCsr& a, const XT* invd, const XT* b, XT* z, ChebCoef c, cudaStream_t s);
+template <class XT>
+void launch_cheb_post2(const DevCsr& a, const XT* invd, const XT* r0, XT* z, ChebCoef c, const XT* b_dot,
+                       Reducer* red, int slot, cudaStream_t s);
+// fp32 V-cycle, fine level: z_out (fp64) = z + Chebyshev(2) post step ; slot <- b64.z_out
+void launch_cheb_post2_out64(const DevCsr& a, const float* invd, const float* r0, const float* z, ChebCoef c,
+                             double* z_out, const double* b_dot, Reducer* red, int slot, cudaStream_t s);
+// Chebyshev(1): z = D^-1 b / theta and t = b - A z in one pass
+template <class XT>
+void launch_cheb1_pre_resid(const DevCsr& a, const XT* invd, const XT* b, XT* z, XT* t, ChebCoef c, cudaStream_t s);
+// Chebyshev(1) post: z_out = z + D^-1 (b - A z) / theta (z_out != z)
+template <class XT>
+void launch_cheb1_post(const DevCsr& a, const XT* invd, const XT* b, const XT* z, XT* z_out, ChebCoef c,
+                       cudaStream_t s);
+// z += P zc
+template <class XT>
+void launch_prolong_add(const DevCsr& p, const XT* zc, XT* z, cudaStream_t s);
+// w = invd .* (A v)   (power iteration on D^-1 A for the smoother bounds)
+void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, double* w, cudaStream_t s);
+
+// ---- PCG / dense (k_sparse.cu)
+// x += alpha p ; r -= alpha q ; slot_rr <- r.r ; alpha = scal[S_RZ]/scal[S_PQ]; r32 (optional) = (float) r
+void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s,
+                       float* r32 = nullptr);
 // p = z + beta p, beta = scal[S_RZ]/scal[S_RZ_OLD]
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s);
-// Chebyshev(2) smoother pieces (DESIGN.md §4)
-void launch_cheb_pre(const DevCsr& a, const double* invd, const double* b, double* z, ChebCoef c, cudaStream_t s);
-void launch_cheb_post2(const DevCsr& a, const double* invd, const double* r0, double* z, ChebCoef c,
-                       const double* b_dot, Reducer* red, int slot, cudaStream_t s);
-// Chebyshev(1): z = D^-1 b / theta and t = b - A z in one pass
-void launch_cheb1_pre_resid(const DevCsr& a, const double* invd, const double* b, double* z, double* t, ChebCoef c,
-                            cudaStream_t s);
-// Chebyshev(1) post: z_out = z + D^-1 (b - A z) / theta (z_out != z)
-void launch_cheb1_post(const DevCsr& a, const double* invd, const double* b, const double* z, double* z_out,
-                       ChebCoef c, cudaStream_t s);
-// z += P zc
-void launch_prolong_add(const DevCsr& p, const double* zc, double* z, cudaStream_t s);
-// z = Ainv b (dense, n <= 1024)
-void launch_dense_solve(int n, const double* ainv, const double* b, double* z, cudaStream_t s);
+// z = Ainv b (dense, n <= 1024, fp64 inverse)
+template <class XT>
+void launch_dense_solve(int n, const double* ainv, const XT* b, XT* z, cudaStream_t s);
 // Jacobi: z = invd .* r (+ dot r.z into slot when red)
 void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s);
+// precision conversions at the fp32 V-cycle boundary
+void launch_to_f32(long n, const double* x, float* y, cudaStream_t s);
+void launch_to_f64_dot(int n, const float* z32, double* z64, const double* b, Reducer* red, int slot, cudaStream_t s);
 
 // ---- vector kernels (k_sparse.cu)
 void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, cudaStream_t s);
@@ -110,7 +152,8 @@ void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, 
 void launch_multi_dot(int n, int m, const double* const* V, const double* w, Reducer red, int slot0, cudaStream_t s);
 void launch_axpy(int n, double a, const double* x, double* y, cudaStream_t s);            // y += a x
 void launch_scale(int n, double a, const double* x, double* y, cudaStream_t s);           // y = a x
-void launch_diag_scale(int n, const double* invd, const double* b, double a, double* z, cudaStream_t s);  // z = a D^-1 b
+template <class XT>
+void launch_diag_scale(int n, const XT* invd, const XT* b, double a, XT* z, cudaStream_t s);  // z = a D^-1 b
 void launch_axpy_dev(int n, const double* coef, double sign, const double* x, double* y, cudaStream_t s);  // y += sign*(*coef) x
 // y = sum_k c[k] V_k  (coefficients by value)
 struct CoefPack {
@@ -141,6 +184,7 @@ void launch_rkc_error(int n, const double* x, const double* xn, const double* f0
                       double atol, double rtol, Reducer red, int slot, cudaStream_t s);
 // permutations: y[i] = x[idx[i]] / y[idx[i]] = x[i]
 void launch_gather(int n, const int* idx, const double* x, double* y, cudaStream_t s);
+void launch_gather_f(int n, const int* idx, const float* x, float* y, cudaStream_t s);
 void launch_scatter(int n, const int* idx, const double* x, double* y, cudaStream_t s);
 // per-boundary-set scalars passed by value (no H2D copy per stage)
 constexpr int kMaxSets = 16;

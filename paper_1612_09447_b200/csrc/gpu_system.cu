@@ -8,6 +8,7 @@
 // (restrict_free, :17-20) is free. With one rank the owned set is every free
 // dof in DofMap::free_dofs order and there are no ghosts.
 #include "gpu_system.hpp"
+#include "sell.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -15,6 +16,7 @@
 #include <cstring>
 #include <map>
 #include <random>
+#include <type_traits>
 
 namespace eqsb {
 
@@ -48,6 +50,7 @@ template struct DevBuf<int>;
 template struct DevBuf<long>;
 template struct DevBuf<unsigned>;
 template struct DevBuf<unsigned char>;
+template struct DevBuf<unsigned short>;
 
 namespace {
 using clk = std::chrono::steady_clock;
@@ -83,6 +86,64 @@ void upload_csr(const HostCsr& h, DevCsr& d, DevBuf<int>& rp, DevBuf<int>& ci, D
   d.values = v.p;
   d.values_f = nullptr;
   d.tpr = choose_tpr(h);
+}
+
+uint16_t to_bf16(double d) {  // round to nearest even
+  const float f = (float)d;
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+// SELL copy of h (sell.hpp) with fp64/fp32/bf16 values; d.sell stays absent
+// when some chunk cannot be encoded
+void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
+  d.sell = DevSell{};
+  HostSell hs;
+  if (h.n_rows == 0 || !build_sell(h, choose_sell_tpr(h), hs)) return;
+  const size_t np = std::max<long>(1, hs.padded());
+  // chunk pointers and bases padded past the end: the pipelined kernels copy
+  // whole tiles of metadata (10 pointers, 64 bases) with bulk copies
+  std::vector<long> cp = hs.chunk_ptr;
+  cp.resize(cp.size() + 16, cp.back());
+  std::vector<int> bases = hs.bases;
+  bases.resize(bases.size() + 64, 0);
+  b.cp.alloc(cp.size());
+  b.cp.upload(cp.data(), cp.size(), s);
+  b.bases.alloc(bases.size());
+  b.bases.upload(bases.data(), bases.size(), s);
+  b.code.alloc(np);
+  b.code.upload(hs.code.data(), hs.code.size(), s);
+  {
+    const std::vector<double> v = sell_values<double>(hs, h.values);
+    b.v64.alloc(np);
+    b.v64.upload(v.data(), v.size(), s);
+    CK(cudaStreamSynchronize(s));
+  }
+  {
+    const std::vector<float> v = sell_values<float>(hs, h.values);
+    b.v32.alloc(np);
+    b.v32.upload(v.data(), v.size(), s);
+    CK(cudaStreamSynchronize(s));
+  }
+  {
+    std::vector<uint16_t> v(hs.src.size());
+    for (size_t k = 0; k < v.size(); ++k) v[k] = hs.src[k] >= 0 ? to_bf16(h.values[hs.src[k]]) : 0;
+    b.v16.alloc(np);
+    b.v16.upload(v.data(), v.size(), s);
+    CK(cudaStreamSynchronize(s));
+  }
+  d.sell.tpr = hs.tpr;
+  d.sell.n_chunks = hs.n_chunks;
+  d.sell.padded = hs.padded();
+  d.sell.chunk_ptr = b.cp.p;
+  d.sell.bases = b.bases.p;
+  d.sell.code = b.code.p;
+  d.sell.v64 = b.v64.p;
+  d.sell.v32 = b.v32.p;
+  d.sell.v16 = b.v16.p;
 }
 
 // 1/diag of the owned rows (local row i <-> local column i)
@@ -189,18 +250,29 @@ void GpuSystem::build_halo(const LocalSpace& sp, DevHalo& h) {
   h.send_idx.alloc(std::max<size_t>(1, idx.size()));
   h.send_idx.upload(idx.data(), idx.size(), stream_);
   h.send_buf.alloc(std::max<size_t>(1, idx.size()));
+  h.send_buf32.alloc(std::max<size_t>(1, idx.size()));
   CK(cudaStreamSynchronize(stream_));
 }
 
-void GpuSystem::halo(DevHalo& h, double* vec) {
+template <class T>
+void GpuSystem::halo(DevHalo& h, T* vec) {
   if (comm_->size() == 1 || h.peers.empty()) return;
-  launch_gather(h.n_send, h.send_idx.p, vec, h.send_buf.p, stream_);
+  T* buf;
+  if constexpr (std::is_same_v<T, double>) {
+    buf = h.send_buf.p;
+    launch_gather(h.n_send, h.send_idx.p, vec, buf, stream_);
+  } else {
+    buf = h.send_buf32.p;
+    launch_gather_f(h.n_send, h.send_idx.p, vec, buf, stream_);
+  }
   std::vector<HaloMsg> msgs;
   for (size_t k = 0; k < h.peers.size(); ++k)
-    msgs.push_back({h.peers[k], h.send_buf.p + h.send_off[k], h.send_cnt[k], vec + h.n_own + h.recv_off[k],
-                    h.recv_cnt[k]});
+    msgs.push_back({h.peers[k], buf + h.send_off[k], h.send_cnt[k], vec + h.n_own + h.recv_off[k], h.recv_cnt[k],
+                    (int)sizeof(T)});
   comm_->exchange(msgs, stream_);
 }
+template void GpuSystem::halo<double>(DevHalo&, double*);
+template void GpuSystem::halo<float>(DevHalo&, float*);
 
 void GpuSystem::allreduce(int slot, int count) {
   if (comm_->size() > 1) comm_->allreduce(red_scal_.p + slot, count, stream_);
@@ -289,6 +361,8 @@ void GpuSystem::build_device() {
   }
   // M_II (owned rows, local columns) + level-0 halo
   upload_csr(plan_.mii, mii_, mii_rp_, mii_ci_, mii_v_, s);
+  upload_sell(plan_.mii, mii_, mii_s_, s);
+  set_sell(sell_on_);
   build_halo(plan_.space[0], halo0_);
   {
     std::vector<double> invd = inv_diagonal(plan_.mii);
@@ -316,6 +390,7 @@ void GpuSystem::build_device() {
   X_ = full_[0].p;
   CK(cudaStreamSynchronize(s));
   if (prob_.solver.precond == 2) build_levels();
+  set_sell(sell_on_);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
 }
@@ -345,6 +420,7 @@ void GpuSystem::build_levels() {
       lv.A = mii_;  // shares indices / fp64 values with the PCG operator
     } else {
       upload_csr(plan_.A[l], lv.A, lv.a_rp, lv.a_ci, lv.a_v, s);
+      if (l + 1 < L) upload_sell(plan_.A[l], lv.A, lv.a_s, s);
     }
     build_halo(sp, lv.halo);
     const size_t nloc = std::max(1, lv.n_loc);
@@ -352,17 +428,25 @@ void GpuSystem::build_levels() {
     lv.b.alloc(nloc);
     lv.t.alloc(nloc);
     lv.z2.alloc(nloc);
+    lv.z32.alloc(nloc);
+    lv.b32.alloc(nloc);
+    lv.t32.alloc(nloc);
+    lv.z2_32.alloc(nloc);
     if (l + 1 < L) {
       f32(plan_.A[l].values, lv.a_vf);
       upload_csr(plan_.P[l], lv.P, lv.p_rp, lv.p_ci, lv.p_v, s);
       upload_csr(plan_.R[l], lv.R, lv.r_rp, lv.r_ci, lv.r_v, s);
       f32(plan_.P[l].values, lv.p_vf);
       f32(plan_.R[l].values, lv.r_vf);
+      upload_sell(plan_.P[l], lv.P, lv.p_s, s);
+      upload_sell(plan_.R[l], lv.R, lv.r_s, s);
       std::vector<double> invd = inv_diagonal(plan_.A[l]);
       invd.resize(nloc, 0.0);
       lv.invd.alloc(nloc);
       lv.invd.upload(invd.data(), invd.size(), s);
       halo(lv.halo, lv.invd.p);
+      lv.invd32.alloc(nloc);
+      launch_to_f32(lv.n_loc, lv.invd.p, lv.invd32.p, s);  // owned + ghosts
     } else if (!lv.replicated) {
       // partitioned coarsest (single-level hierarchy): every rank solves the
       // dense system on the full vector assembled by scatter + allreduce
@@ -378,7 +462,8 @@ void GpuSystem::build_levels() {
   coarse_n_ = amg_.coarse_n;
   coarse_inv_.alloc(amg_.coarse_inverse.size());
   coarse_inv_.upload(amg_.coarse_inverse.data(), amg_.coarse_inverse.size(), s);
-  set_vcycle_fp32(vcycle_fp32_);
+  set_vcycle_precision(vcycle_prec_);
+  set_sell(sell_on_);
   // smoother bounds: lambda_max(D^-1 A_l) by 20 power iterations from a
   // global random vector (same on every rank), norms reduced over ranks
   std::mt19937 rng(12345u);
@@ -456,14 +541,28 @@ void GpuSystem::set_level_tpr(int level, int tpr) {
   if (level < (int)levels_.size()) levels_[level].A.tpr = tpr;
 }
 
-void GpuSystem::set_vcycle_fp32(bool on) {
+// V-cycle operators only: the PCG operator M_II stays fp64. bf16 is read from
+// the SELL copies; a matrix without one falls back to its fp32 CSR values.
+void GpuSystem::set_vcycle_precision(int prec) {
+  if (prec < 0 || prec > 2) throw std::invalid_argument("V-cycle precision must be 0 (fp64), 1 (fp32) or 2 (bf16)");
   invalidate_graphs();
-  vcycle_fp32_ = on;
+  vcycle_prec_ = prec;
   for (size_t l = 0; l + 1 < levels_.size(); ++l) {
     DevLevel& lv = levels_[l];
-    lv.A.values_f = on ? lv.a_vf.p : nullptr;
-    lv.P.values_f = on ? lv.p_vf.p : nullptr;
-    lv.R.values_f = on ? lv.r_vf.p : nullptr;
+    lv.A.values_f = lv.a_vf.p;
+    lv.P.values_f = lv.p_vf.p;
+    lv.R.values_f = lv.r_vf.p;
+    lv.A.prec = lv.P.prec = lv.R.prec = prec;
+  }
+}
+
+void GpuSystem::set_sell(bool on) {
+  invalidate_graphs();
+  sell_on_ = on;
+  mii_.use_sell = on && mii_.sell.tpr > 0;
+  for (size_t l = 0; l < levels_.size(); ++l) {
+    DevLevel& lv = levels_[l];
+    for (DevCsr* m : {&lv.A, &lv.P, &lv.R}) m->use_sell = on && m->sell.tpr > 0;
   }
 }
 
@@ -580,9 +679,7 @@ double GpuSystem::kx_bytes() const {
   if (order_ == 1) return 20.0 * n_tets_loc_ + 48.0 * n_full_;
   return 44.0 * n_tets_loc_ + 24.0 * prob_.mesh.n_nodes * ((double)n_full_ / std::max(1, n_dofs_)) + 24.0 * n_full_;
 }
-double GpuSystem::spmv_bytes(const DevCsr& a) const {
-  return 12.0 * a.nnz + 4.0 * (a.n_rows + 1) + 8.0 * a.n_cols + 8.0 * a.n_rows;
-}
+double GpuSystem::spmv_bytes(const DevCsr& a) const { return matrix_pass_bytes(a, 1, 1); }
 
 // ------------------------------------------------------------------ operators
 void GpuSystem::lift_dev(double t, double* x_full) {
@@ -651,71 +748,134 @@ void GpuSystem::mass_apply_dev(double* v, double* y) {
   launch_spmv(mii_, v, y, stream_);
 }
 
+// level buffers of the V-cycle vector type
+template <class XT>
+struct VBufs;
+template <>
+struct VBufs<double> {
+  static double* b(DevLevel& l) { return l.b.p; }
+  static double* z(DevLevel& l) { return l.z.p; }
+  static double* z2(DevLevel& l) { return l.z2.p; }
+  static double* t(DevLevel& l) { return l.t.p; }
+  static double* invd(DevLevel& l) { return l.invd.p; }
+};
+template <>
+struct VBufs<float> {
+  static float* b(DevLevel& l) { return l.b32.p; }
+  static float* z(DevLevel& l) { return l.z32.p; }
+  static float* z2(DevLevel& l) { return l.z2_32.p; }
+  static float* t(DevLevel& l) { return l.t32.p; }
+  static float* invd(DevLevel& l) { return l.invd32.p; }
+};
+
 // Symmetric V-cycle (amg.cpp:145-172 structure) with Chebyshev smoothing:
 // degree `cheb_degree` on the fine level, `coarse_degree` below; the same
 // polynomial pre and post keeps the preconditioner symmetric for PCG. Every
-// gathered vector has its ghosts exchanged first (no-op on one rank).
-double* GpuSystem::vcycle(int l, const double* b_in, bool dot_into_rz) {
+// gathered vector has its ghosts exchanged first (no-op on one rank). XT is
+// the vector type of the levels (fp32 by default). With fp32
+// vectors the fine level reads the fp32 copy of r (b) and its last kernel
+// writes z in fp64 (out64, with r64 . z when dot_into_rz).
+template <class XT>
+XT* GpuSystem::vcycle_t(int l, const XT* b_in, bool dot_into_rz, const double* r64, double* out64) {
+  using V = VBufs<XT>;
   const int L = (int)levels_.size();
   DevLevel& lv = levels_[l];
-  double* b = const_cast<double*>(b_in);
+  XT* b = const_cast<XT*>(b_in);
   if (l == L - 1) {
     // dense solve on the full vector (replicated level: b is already whole)
-    double* z = lv.z.p;
+    XT* z = V::z(lv);
     if (comm_->size() == 1 || lv.replicated) {
-      launch_dense_solve(coarse_n_, coarse_inv_.p, b, z, stream_);
+      launch_dense_solve<XT>(coarse_n_, coarse_inv_.p, b, z, stream_);
     } else {
-      launch_fill(coarse_n_, 0.0, lv.full_b.p, stream_);
-      launch_scatter(lv.n_own, lv.glob.p, b, lv.full_b.p, stream_);
-      comm_->allreduce(lv.full_b.p, coarse_n_, stream_);
-      launch_dense_solve(coarse_n_, coarse_inv_.p, lv.full_b.p, lv.full_z.p, stream_);
-      launch_gather(lv.n_loc, lv.glob.p, lv.full_z.p, z, stream_);  // owned + ghosts
+      if constexpr (std::is_same_v<XT, double>) {
+        launch_fill(coarse_n_, 0.0, lv.full_b.p, stream_);
+        launch_scatter(lv.n_own, lv.glob.p, b, lv.full_b.p, stream_);
+        comm_->allreduce(lv.full_b.p, coarse_n_, stream_);
+        launch_dense_solve<double>(coarse_n_, coarse_inv_.p, lv.full_b.p, lv.full_z.p, stream_);
+        launch_gather(lv.n_loc, lv.glob.p, lv.full_z.p, z, stream_);  // owned + ghosts
+      } else {
+        throw std::logic_error("fp32 V-cycle needs a replicated coarsest level");
+      }
     }
     if (dot_into_rz) {
-      launch_dot(lv.n_own, b, z, red_, S_RZ, stream_);
-      allreduce(S_RZ);
+      if constexpr (std::is_same_v<XT, double>) {
+        launch_dot(lv.n_own, b, z, red_, S_RZ, stream_);
+        allreduce(S_RZ);
+      }
     }
     return z;
   }
   DevLevel& nx = levels_[l + 1];
   const int deg = l == 0 ? cheb_degree : coarse_degree;
-  double* z = lv.z.p;
+  XT* z = V::z(lv);
+  XT* t = V::t(lv);
+  XT* invd = V::invd(lv);
   halo(lv.halo, b);
   if (deg >= 2) {
-    launch_cheb_pre(lv.A, lv.invd.p, b, z, lv.cheb, stream_);
+    launch_cheb_pre<XT>(lv.A, invd, b, z, lv.cheb, stream_);
     halo(lv.halo, z);
-    launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
-  } else if (lv.A.tpr <= 4) {
-    launch_cheb1_pre_resid(lv.A, lv.invd.p, b, z, lv.t.p, lv.cheb1, stream_);
+    launch_residual<XT>(lv.A, b, z, t, nullptr, 0, stream_);
+  } else if (lv.A.lanes() <= 4) {
+    launch_cheb1_pre_resid<XT>(lv.A, invd, b, z, t, lv.cheb1, stream_);
   } else {
     // dense rows: one gathered vector per entry instead of two (b and D^-1)
-    launch_diag_scale(lv.n_loc, lv.invd.p, b, lv.cheb1.inv_theta, z, stream_);
-    launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
+    launch_diag_scale<XT>(lv.n_loc, invd, b, lv.cheb1.inv_theta, z, stream_);
+    launch_residual<XT>(lv.A, b, z, t, nullptr, 0, stream_);
   }
-  halo(lv.halo, lv.t.p);
-  launch_spmv(lv.R, lv.t.p, nx.b.p, stream_);
+  halo(lv.halo, t);
+  XT* bc = V::b(nx);
+  launch_spmv<XT>(lv.R, t, bc, stream_);
   // entering the replicated levels: every rank holds the partial restriction
   // of its owned rows for all coarse rows; the sum is the coarse right-hand side
-  if (nx.replicated && !lv.replicated && comm_->size() > 1) comm_->allreduce(nx.b.p, nx.n_loc, stream_);
-  double* zc = vcycle(l + 1, nx.b.p, false);
+  if (nx.replicated && !lv.replicated && comm_->size() > 1) comm_->allreduce(bc, nx.n_loc, stream_);
+  XT* zc = vcycle_t<XT>(l + 1, bc, false, nullptr, nullptr);
   halo(nx.halo, zc);  // no-op on replicated levels
-  launch_prolong_add(lv.P, zc, z, stream_);
+  launch_prolong_add<XT>(lv.P, zc, z, stream_);
   halo(lv.halo, z);
+  const bool to64 = out64 != nullptr;  // fine level of an fp32 V-cycle
+  Reducer r = red_;
   if (deg >= 2) {
-    launch_residual(lv.A, b, z, lv.t.p, nullptr, 0, stream_);
-    halo(lv.halo, lv.t.p);
-    Reducer r = red_;
-    launch_cheb_post2(lv.A, lv.invd.p, lv.t.p, z, lv.cheb, dot_into_rz ? b : nullptr, dot_into_rz ? &r : nullptr,
-                      S_RZ, stream_);
+    launch_residual<XT>(lv.A, b, z, t, nullptr, 0, stream_);
+    halo(lv.halo, t);
+    if constexpr (std::is_same_v<XT, float>) {
+      if (to64) {
+        launch_cheb_post2_out64(lv.A, invd, t, z, lv.cheb, out64, r64, dot_into_rz ? &r : nullptr, S_RZ, stream_);
+        if (dot_into_rz) allreduce(S_RZ);
+        return nullptr;
+      }
+    }
+    launch_cheb_post2<XT>(lv.A, invd, t, z, lv.cheb, dot_into_rz ? b : nullptr, dot_into_rz ? &r : nullptr, S_RZ,
+                          stream_);
     if (dot_into_rz) allreduce(S_RZ);
     return z;
   }
-  launch_cheb1_post(lv.A, lv.invd.p, b, z, lv.z2.p, lv.cheb1, stream_);
-  if (dot_into_rz) {
-    launch_dot(lv.n_own, b, lv.z2.p, red_, S_RZ, stream_);
-    allreduce(S_RZ);
+  XT* z2 = V::z2(lv);
+  launch_cheb1_post<XT>(lv.A, invd, b, z, z2, lv.cheb1, stream_);
+  if constexpr (std::is_same_v<XT, float>) {
+    if (to64) {
+      launch_to_f64_dot(lv.n_own, z2, out64, r64, dot_into_rz ? &r : nullptr, S_RZ, stream_);
+      if (dot_into_rz) allreduce(S_RZ);
+      return nullptr;
+    }
   }
-  return lv.z2.p;
+  if (dot_into_rz) {
+    if constexpr (std::is_same_v<XT, double>) {
+      launch_dot(lv.n_own, b, z2, red_, S_RZ, stream_);
+      allreduce(S_RZ);
+    }
+  }
+  return z2;
+}
+
+// V-cycle on the fine residual r (fp64): returns z (fp64) and r.z in S_RZ
+double* GpuSystem::vcycle(const double* r) {
+  if (vcycle_f32_ && levels_.size() >= 2) {
+    DevLevel& f = levels_[0];
+    launch_to_f32(n_own_, r, f.b32.p, stream_);
+    vcycle_t<float>(0, f.b32.p, true, r, f.z.p);
+    return f.z.p;
+  }
+  return vcycle_t<double>(0, r, true, nullptr, nullptr);
 }
 
 // The V-cycle is a fixed sequence of kernels (and, on several ranks, NCCL
@@ -723,33 +883,39 @@ double* GpuSystem::vcycle(int l, const double* b_in, bool dot_into_rz) {
 // graph and replayed: one launch per preconditioner application.
 double* GpuSystem::precondition(double* r) {
   tic(TC_VCYCLE);
+  const double bytes0 = g_algo_bytes;
   double* z;
   if (prob_.solver.precond == 2) {
     if (use_graphs && comm_->capturable() && r == w_r_.p) {
       if (!vcycle_graph_) {
         cudaGraph_t graph;
         const long before = g_launch_count;
+        const double bytes_before = g_algo_bytes;
         CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-        vcycle_out_ = vcycle(0, r, true);
+        vcycle_out_ = vcycle(r);
         CK(cudaStreamEndCapture(stream_, &graph));
         vcycle_graph_kernels_ = g_launch_count - before;
+        vcycle_graph_bytes_ = g_algo_bytes - bytes_before;
         g_launch_count = before;
+        g_algo_bytes = bytes_before;
         CK(cudaGraphInstantiate(&vcycle_graph_, graph, 0));
         CK(cudaGraphDestroy(graph));
       }
       CK(cudaGraphLaunch(vcycle_graph_, stream_));
       g_launch_count += vcycle_graph_kernels_;
+      g_algo_bytes += vcycle_graph_bytes_;
       z = vcycle_out_;
     } else {
-      z = vcycle(0, r, true);
+      z = vcycle(r);
     }
   } else {
     Reducer rr = red_;
     z = w_z_.p;
     launch_jacobi(n_own_, mii_invd_.p, r, z, &rr, S_RZ, stream_);
     allreduce(S_RZ);
+    g_algo_bytes += 24.0 * n_own_;
   }
-  toc(TC_VCYCLE, 0.0);
+  toc(TC_VCYCLE, g_algo_bytes - bytes0);
   return z;
 }
 

@@ -69,7 +69,18 @@ struct DevHalo {
   int n_own = 0, n_send = 0;
   DevBuf<int> send_idx;      // concatenated per-peer send lists (local owned indices)
   DevBuf<double> send_buf;
+  DevBuf<float> send_buf32;
   std::vector<int> peers, send_off, send_cnt, recv_off, recv_cnt;
+};
+
+// device buffers of a SELL copy (sell.hpp), all three value precisions
+struct SellBufs {
+  DevBuf<long> cp;
+  DevBuf<int> bases;
+  DevBuf<uint16_t> code;
+  DevBuf<double> v64;
+  DevBuf<float> v32;
+  DevBuf<uint16_t> v16;
 };
 
 struct DevLevel {
@@ -79,7 +90,9 @@ struct DevLevel {
   DevBuf<int> a_rp, a_ci, p_rp, p_ci, r_rp, r_ci;
   DevBuf<double> a_v, p_v, r_v;
   DevBuf<float> a_vf, p_vf, r_vf;  // fp32 copies for the V-cycle
+  SellBufs a_s, p_s, r_s;          // SELL copies (level 0: A shares the PCG operator's)
   DevBuf<double> invd, b, z, z2, t;
+  DevBuf<float> invd32, b32, z32, z2_32, t32;  // fp32 V-cycle vectors
   ChebCoef cheb{}, cheb1{};          // degree-2 and degree-1 Chebyshev coefficients
   double lambda_smoother = 0;
   DevHalo halo;
@@ -160,10 +173,16 @@ class GpuSystem {
   bool use_graphs = true;
   bool spe_incremental = true;  // false: the reference's full MGS rebuild on every solve
   void set_cheb(double ratio);
-  void set_vcycle_fp32(bool on);
+  void set_vcycle_precision(int prec);  // V-cycle matrix values: 0 fp64, 1 fp32, 2 bf16
+  void set_sell(bool on);               // SELL-16 copies instead of CSR where available
+  void set_vcycle_vectors_f32(bool on) {  // V-cycle vectors fp32 (default) or fp64
+    invalidate_graphs();
+    vcycle_f32_ = on;
+  }
   void set_level_tpr(int level, int tpr);  // threads per row of A_l (level 0 also sets M_II)
   void invalidate_graphs();
-  bool vcycle_fp32() const { return vcycle_fp32_; }
+  int vcycle_precision() const { return vcycle_prec_; }
+  bool sell_on() const { return sell_on_; }
   bool timing_on = false;
   void tic(int cls);
   void toc(int cls, double bytes);
@@ -178,9 +197,12 @@ class GpuSystem {
   void build_device();
   void build_levels();
   void build_halo(const LocalSpace& sp, DevHalo& h);
-  void halo(DevHalo& h, double* vec);  // fill ghosts of vec from the owners
+  template <class T>
+  void halo(DevHalo& h, T* vec);  // fill ghosts of vec from the owners
   void allreduce(int slot, int count = 1);
-  double* vcycle(int l, const double* b, bool dot_into_rz);  // returns the buffer holding z_l
+  template <class XT>
+  XT* vcycle_t(int l, const XT* b, bool dot_into_rz, const double* r64, double* out64);
+  double* vcycle(const double* r);  // fine-level V-cycle: z (fp64), r.z in S_RZ
   double* precondition(double* r);  // z = M^-1 r (returned buffer), S_RZ <- r.z
   void kx_tets(const double* x, const double* v);
   double read_scalar(int slot);
@@ -209,10 +231,13 @@ class GpuSystem {
   void spe_rebuild();
   void spe_append(double* h);
   void spe_downdate();
-  bool vcycle_fp32_ = true;
+  int vcycle_prec_ = 2;
+  bool vcycle_f32_ = true;
+  bool sell_on_ = true;
   cudaGraphExec_t vcycle_graph_ = nullptr;  // captured V-cycle (rebuilt when options change)
   double* vcycle_out_ = nullptr;
   long vcycle_graph_kernels_ = 0;
+  double vcycle_graph_bytes_ = 0.0;
 
   Problem prob_;
   int device_ = 0;
@@ -248,6 +273,7 @@ class GpuSystem {
   DevCsr mii_;
   DevBuf<int> mii_rp_, mii_ci_;
   DevBuf<double> mii_v_, mii_invd_;
+  SellBufs mii_s_;
   DevHalo halo0_;  // level-0 (fine dof) halo
   std::vector<DevLevel> levels_;
   DevBuf<double> coarse_inv_;

@@ -1,0 +1,81 @@
+// SELL-16 encoder (sell.hpp). Deterministic; chunks are independent, so the
+// window search and the per-chunk layout run in parallel.
+#include <omp.h>
+
+#include <algorithm>
+#include <climits>
+
+#include "sell.hpp"
+
+namespace eqsb {
+
+int choose_sell_tpr(const HostCsr& a) {
+  if (a.n_rows == 0) return 1;
+  const double avg = (double)a.nnz() / a.n_rows;
+  int t = 1;
+  while (t < 32 && t * 16 < avg) t <<= 1;
+  return t;
+}
+
+bool build_sell(const HostCsr& a, int tpr, HostSell& out) {
+  const int rows_per_chunk = 32 / tpr;
+  const int n_chunks = (a.n_rows + rows_per_chunk - 1) / rows_per_chunk;
+  std::vector<long> len(n_chunks + 1, 0);
+  std::vector<int> bases((size_t)n_chunks * kSellWindows, 0);
+  int fail = 0;
+#pragma omp parallel
+  {
+    std::vector<int> cols;
+#pragma omp for schedule(static) reduction(max : fail)
+    for (int c = 0; c < n_chunks; ++c) {
+      const int r0 = c * rows_per_chunk, r1 = std::min(a.n_rows, r0 + rows_per_chunk);
+      int maxlen = 0;
+      cols.assign(a.col_idx.begin() + a.row_ptr[r0], a.col_idx.begin() + a.row_ptr[r1]);
+      for (int r = r0; r < r1; ++r) maxlen = std::max(maxlen, a.row_ptr[r + 1] - a.row_ptr[r]);
+      std::sort(cols.begin(), cols.end());
+      int w = 0;
+      for (size_t i = 0; i < cols.size();) {
+        if (w == kSellWindows) {
+          fail = 1;
+          break;
+        }
+        const int b = cols[i];
+        bases[(size_t)c * kSellWindows + w++] = b;
+        while (i < cols.size() && cols[i] < b + kSellSpan) ++i;
+      }
+      for (int k = w; k < kSellWindows; ++k) bases[(size_t)c * kSellWindows + k] = INT_MAX;  // unused
+      len[c + 1] = 32L * ((maxlen + tpr - 1) / tpr);
+    }
+  }
+  if (fail) return false;
+  for (int c = 0; c < n_chunks; ++c) len[c + 1] += len[c];
+  HostSell s;
+  s.tpr = tpr;
+  s.n_rows = a.n_rows;
+  s.n_chunks = n_chunks;
+  s.chunk_ptr = std::move(len);
+  s.bases = std::move(bases);
+  s.code.assign(s.padded(), 0);
+  s.src.assign(s.padded(), -1);
+#pragma omp parallel for schedule(static)
+  for (int c = 0; c < n_chunks; ++c) {
+    const int* wb = &s.bases[(size_t)c * kSellWindows];
+    const int r0 = c * rows_per_chunk, r1 = std::min(a.n_rows, r0 + rows_per_chunk);
+    for (int r = r0; r < r1; ++r) {
+      const int q = r - r0;
+      for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
+        const int j = k - a.row_ptr[r], col = a.col_idx[k];
+        // windows ascend (unused ones are INT_MAX): the owner is the last base <= col
+        int w = kSellWindows - 1;
+        while (w > 0 && wb[w] > col) --w;
+        const long pos = s.chunk_ptr[c] + 32L * (j / tpr) + q * tpr + j % tpr;
+        s.code[pos] = (uint16_t)((w << kSellShift) | (col - wb[w]));
+        s.src[pos] = k;
+      }
+    }
+  }
+  out = std::move(s);
+  return true;
+}
+
+}  // namespace eqsb

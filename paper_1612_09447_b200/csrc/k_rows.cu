@@ -1,0 +1,418 @@
+// Matrix row kernels: one pass over a sparse operator with the AMG/PCG
+// epilogue fused (SpMV, residual, Chebyshev smoothing steps, prolongation,
+// fused dot products). HBM-bound. Two resident formats:
+//   * CSR: TPR-thread groups per row (TPR from the mean row length);
+//   * SELL-16 (sell.hpp): one warp per chunk of 32/TPR rows, slice-major
+//     storage so every load instruction reads 32 consecutive entries, 16-bit
+//     packed columns decoded through per-chunk window bases.
+// Matrix values are fp64, fp32 or bf16 (DevCsr::prec); the vector type XT is
+// fp64 for the PCG operator and fp32 (default) or fp64 inside the V-cycle.
+// Row operands of the epilogue are loaded before the matrix pass so that
+// their latency overlaps it.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <type_traits>
+
+#include "dev.cuh"
+#include "reduce.cuh"
+
+namespace eqsb {
+
+// Algorithmic HBM bytes of one pass over `a` in its resident format: matrix
+// stream (indices + values + row/chunk pointers), the gathered vector(s) once
+// (n_cols each) and the streamed row vectors (n_rows each).
+double matrix_pass_bytes(const DevCsr& a, int gathered, int streamed, int xbytes) {
+  double m;
+  if (a.use_sell) {
+    const double vs = a.prec == 2 ? 2.0 : a.prec == 1 ? 4.0 : 8.0;
+    m = (double)a.sell.padded * (2.0 + vs) + 40.0 * a.sell.n_chunks;  // padded entries are read too
+  } else {
+    const double vs = (a.prec >= 1 && a.values_f) ? 4.0 : 8.0;
+    m = (double)a.nnz * (4.0 + vs) + 4.0 * (a.n_rows + 1);
+  }
+  return m + (double)xbytes * ((double)gathered * a.n_cols + (double)streamed * a.n_rows);
+}
+
+namespace {
+
+constexpr int kUnroll = 8;  // independent entries in flight per lane
+
+// matrix entries are streamed once per pass: evict-first loads keep L2 for
+// the gathered vectors (ld.global.cs). bf16 values are stored as uint16 bit
+// patterns; bf16 -> fp32 is a 16-bit shift.
+__device__ __forceinline__ double ldv(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ float ldv(const float* p) { return __ldcs(p); }
+__device__ __forceinline__ float ldv(const uint16_t* p) { return __uint_as_float((unsigned)__ldcs(p) << 16); }
+
+// CSR row-group core: sum_k A_ik x_k (x_k w_k when SCALED) in lane 0 of the
+// group. All lanes of the warp must call it (shuffles); rows >= n contribute nothing.
+template <int TPR, class VT, class XT, bool SCALED>
+__device__ __forceinline__ XT row_dot(const int* __restrict__ rp, const int* __restrict__ ci,
+                                      const VT* __restrict__ v, const XT* __restrict__ x, const XT* __restrict__ w,
+                                      int row, int lane, int n) {
+  const bool ok = row < n;
+  const int beg = ok ? __ldg(rp + row) : 0, end = ok ? __ldg(rp + row + 1) : 0;
+  XT s = 0;
+  for (int k0 = beg + lane; k0 < end; k0 += TPR * kUnroll) {
+    int c[kUnroll];
+    XT a[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int k = k0 + u * TPR;
+      const bool in = k < end;
+      c[u] = in ? __ldcs(ci + k) : 0;
+      a[u] = in ? (XT)ldv(v + k) : (XT)0;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const XT xv = SCALED ? __ldg(x + c[u]) * __ldg(w + c[u]) : __ldg(x + c[u]);
+      s += a[u] * xv;
+    }
+  }
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, TPR);
+  return s;
+}
+
+// SELL core: the chunk's slices are read with 32-bit offsets from the chunk
+// base (immediate-offset loads inside a batch); window bases sit in lanes 0..7
+// and are fetched per entry by a shuffle. Result in lane (row_in_chunk * TPR).
+template <int TPR, class VT, class XT, bool SCALED>
+__device__ __forceinline__ XT sell_dot(const DevSell& m, const VT* __restrict__ v, int chunk, int lane,
+                                       const XT* __restrict__ x, const XT* __restrict__ w) {
+  const long beg = __ldg(m.chunk_ptr + chunk);
+  const int S = (int)((__ldg(m.chunk_ptr + chunk + 1) - beg) >> 5);  // slices (warp-uniform)
+  const int mybase = lane < 8 ? __ldg(m.bases + 8L * chunk + lane) : 0;
+  const uint16_t* cp = m.code + beg + lane;
+  const VT* vp = v + beg + lane;
+  XT s = 0;
+  for (int s0 = 0; s0 < S; s0 += kUnroll) {
+    unsigned cd[kUnroll];
+    XT a[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const bool in = s0 + u < S;
+      cd[u] = in ? (unsigned)__ldcs(cp + 32 * (s0 + u)) : 0u;
+      a[u] = in ? (XT)ldv(vp + 32 * (s0 + u)) : (XT)0;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int c = __shfl_sync(0xffffffffu, mybase, (int)(cd[u] >> 13)) + (int)(cd[u] & 0x1fffu);
+      if (s0 + u < S) {
+        const XT xv = SCALED ? __ldg(x + c) * __ldg(w + c) : __ldg(x + c);
+        s += a[u] * xv;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, TPR);
+  return s;
+}
+
+// Row epilogues (load before the pass, store after).
+// Row ops (MODE < 0):
+// OP 0: y = A x                       (restriction, plain SpMV)
+// OP 1: y = b - A x                   (residual)
+// OP 2: z += A zc                     (prolongation + correction; v = P)
+// OP 3: z = c0 D^-1 b + c1 D^-1 (b - A D^-1 b / theta)          (Chebyshev(2) pre-smoothing from 0)
+// OP 4: z = D^-1 b / theta ; t = b - A z                         (Chebyshev(1) pre-smoothing + residual)
+// OP 5: zo = z + D^-1 (b - A z) / theta                          (Chebyshev(1) post-smoothing, out of place)
+// OP 6: w = D^-1 A x                                             (power iteration on D^-1 A)
+// Reduction modes (MODE >= 0; the dot is accumulated in fp64):
+// MODE 0: q = A p,  p.q
+// MODE 1: y = b - A x, y.y
+// MODE 2: z += c0 D^-1 r0 + c1 D^-1 (r0 - A D^-1 r0 / theta), b.z   (Chebyshev(2) post step 2; x = r0)
+// MODE 3: as MODE 2 but z_out64 = z + ... in fp64 and b64.z_out64   (fine level of the fp32 V-cycle)
+template <int OP, int MODE, class XT>
+struct Epi {
+  XT p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+  double q = 0.0;
+  __device__ __forceinline__ void load(int row, const XT* __restrict__ x, const XT* __restrict__ b,
+                                       const XT* __restrict__ invd, const XT* y, const double* __restrict__ b64,
+                                       int do_red) {
+    if constexpr (MODE < 0) {
+      if (OP == 1 || OP == 3 || OP == 4 || OP == 5) p0 = b[row];
+      if (OP == 3 || OP == 4 || OP == 5 || OP == 6) p1 = invd[row];
+      if (OP == 5) p2 = x[row];
+      if (OP == 2) p2 = y[row];
+    } else {
+      if (MODE == 0 || MODE >= 2) p0 = x[row];
+      if (MODE == 1 || (MODE == 2 && do_red)) p1 = b[row];
+      if (MODE == 3 && do_red) q = b64[row];
+      if (MODE >= 2) {
+        p2 = invd[row];
+        p3 = y[row];
+      }
+    }
+  }
+  __device__ __forceinline__ double store(int row, XT s, XT* __restrict__ y, XT* __restrict__ y2,
+                                          double* __restrict__ out64, const ChebCoef& c, int do_red) const {
+    const XT c0 = (XT)c.c0, c1 = (XT)c.c1, it = (XT)c.inv_theta;
+    if constexpr (MODE < 0) {
+      if (OP == 0) y[row] = s;
+      if (OP == 1) y[row] = p0 - s;
+      if (OP == 2) y[row] = p2 + s;
+      if (OP == 3) y[row] = c0 * p0 * p1 + c1 * p1 * (p0 - s * it);
+      if (OP == 4) {
+        y[row] = p0 * p1 * it;
+        y2[row] = p0 - s * it;
+      }
+      if (OP == 5) y2[row] = p2 + p1 * (p0 - s) * it;
+      if (OP == 6) y[row] = s * p1;
+      return 0.0;
+    } else if (MODE == 0) {
+      y[row] = s;
+      return (double)p0 * (double)s;
+    } else if (MODE == 1) {
+      const XT r = p1 - s;
+      y[row] = r;
+      return (double)r * (double)r;
+    } else if (MODE == 2) {
+      const XT zn = p3 + (c0 * p0 * p2 + c1 * p2 * (p0 - s * it));
+      y[row] = zn;
+      return do_red ? (double)p1 * (double)zn : 0.0;
+    } else {
+      const double zn = (double)p3 + (double)(c0 * p0 * p2 + c1 * p2 * (p0 - s * it));
+      out64[row] = zn;
+      return do_red ? q * zn : 0.0;
+    }
+  }
+};
+template <int OP, int MODE>
+constexpr bool kScaled = MODE < 0 ? (OP == 3 || OP == 4) : (MODE >= 2);
+
+template <int TPR, class VT, class XT, int OP>
+__global__ void __launch_bounds__(kBlock) k_row(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                const VT* __restrict__ v, const XT* __restrict__ x,
+                                                const XT* __restrict__ b, const XT* __restrict__ invd,
+                                                XT* __restrict__ y, XT* __restrict__ y2, ChebCoef c) {
+  const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
+  const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
+  if ((tid & ~31L) / TPR >= n) return;  // warp-uniform exit
+  constexpr bool SC = kScaled<OP, -1>;
+  const bool act = lane == 0 && row < n;
+  Epi<OP, -1, XT> e;
+  if (act) e.load(row, x, b, invd, y, nullptr, 0);
+  const XT s = row_dot<TPR, VT, XT, SC>(rp, ci, v, SC ? b : x, invd, row, lane, n);
+  if (act) e.store(row, s, y, y2, nullptr, c, 0);
+}
+
+template <int TPR, class VT, class XT, int OP>
+__global__ void __launch_bounds__(kBlock) k_sell(int n, DevSell m, const VT* __restrict__ v,
+                                                 const XT* __restrict__ x, const XT* __restrict__ b,
+                                                 const XT* __restrict__ invd, XT* __restrict__ y,
+                                                 XT* __restrict__ y2, ChebCoef c) {
+  const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (chunk >= m.n_chunks) return;  // warp-uniform exit
+  constexpr bool SC = kScaled<OP, -1>;
+  const int row = chunk * (32 / TPR) + lane / TPR;
+  const bool act = lane % TPR == 0 && row < n;
+  Epi<OP, -1, XT> e;
+  if (act) e.load(row, x, b, invd, y, nullptr, 0);
+  const XT s = sell_dot<TPR, VT, XT, SC>(m, v, chunk, lane, SC ? b : x, invd);
+  if (act) e.store(row, s, y, y2, nullptr, c, 0);
+}
+
+// grid-stride kernels with a fused reduction (fixed grid: deterministic)
+template <int TPR, class VT, class XT, int MODE>
+__global__ void __launch_bounds__(kBlock) k_row_red(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                    const VT* __restrict__ v, const XT* __restrict__ x,
+                                                    const XT* __restrict__ b, const XT* __restrict__ invd,
+                                                    XT* __restrict__ y, double* __restrict__ out64,
+                                                    const double* __restrict__ b64, ChebCoef c, Reducer red,
+                                                    int slot, int do_red) {
+  const int lane = threadIdx.x % TPR;
+  const long groups_per_grid = (long)gridDim.x * (kBlock / TPR);
+  // every group iterates the same number of times (shuffles need full warps)
+  const long n_pad = ((n + (long)(kBlock / TPR) - 1) / (kBlock / TPR)) * (kBlock / TPR);
+  double acc = 0.0;
+  for (long row = (long)blockIdx.x * (kBlock / TPR) + threadIdx.x / TPR; row < n_pad; row += groups_per_grid) {
+    const bool act = lane == 0 && row < n;
+    Epi<0, MODE, XT> e;
+    if (act) e.load((int)row, x, b, invd, y, b64, do_red);
+    const XT s = row_dot<TPR, VT, XT, kScaled<0, MODE>>(rp, ci, v, x, invd, (int)row, lane, n);
+    if (act) acc += e.store((int)row, s, y, nullptr, out64, c, do_red);
+  }
+  if (do_red) reduce_finish(acc, red, slot);
+}
+
+template <int TPR, class VT, class XT, int MODE>
+__global__ void __launch_bounds__(kBlock) k_sell_red(int n, DevSell m, const VT* __restrict__ v,
+                                                     const XT* __restrict__ x, const XT* __restrict__ b,
+                                                     const XT* __restrict__ invd, XT* __restrict__ y,
+                                                     double* __restrict__ out64, const double* __restrict__ b64,
+                                                     ChebCoef c, Reducer red, int slot, int do_red) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (kBlock / 32);
+  double acc = 0.0;
+  for (int chunk = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); chunk < m.n_chunks; chunk += warps) {
+    const int row = chunk * (32 / TPR) + lane / TPR;
+    const bool act = lane % TPR == 0 && row < n;
+    Epi<0, MODE, XT> e;
+    if (act) e.load(row, x, b, invd, y, b64, do_red);
+    const XT s = sell_dot<TPR, VT, XT, kScaled<0, MODE>>(m, v, chunk, lane, x, invd);
+    if (act) acc += e.store(row, s, y, nullptr, out64, c, do_red);
+  }
+  if (do_red) reduce_finish(acc, red, slot);
+}
+
+#define TPR_SWITCH_(tpr, L_, VT, V) \
+  switch (tpr) {                    \
+    case 1: L_(1, VT, V); break;    \
+    case 2: L_(2, VT, V); break;    \
+    case 4: L_(4, VT, V); break;    \
+    case 8: L_(8, VT, V); break;    \
+    case 16: L_(16, VT, V); break;  \
+    default: L_(32, VT, V); break;  \
+  }
+
+// value array per format and precision; fp32 vectors never read fp64 values
+// (the V-cycle then uses the fp32 copy)
+template <class XT>
+int eff_prec(const DevCsr& a) {
+  int p = a.prec;
+  if (std::is_same_v<XT, float> && p == 0) p = 1;
+  if (!a.use_sell && p == 2) p = 1;  // CSR has no bf16 copy
+  if (!a.use_sell && p == 1 && !a.values_f) p = 0;
+  return p;
+}
+
+template <class XT, int OP>
+void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y, XT* y2, ChebCoef c, cudaStream_t s) {
+  if (a.n_rows == 0) return;
+  ++g_launch_count;
+  // gathered / streamed row vectors per op (Epi)
+  constexpr int kG[7] = {1, 1, 1, 2, 2, 1, 1}, kS[7] = {1, 2, 2, 1, 2, 3, 2};
+  const int p = eff_prec<XT>(a);
+  if (a.use_sell) {
+    const DevSell& m = a.sell;
+    DevCsr view = a;
+    view.prec = p;
+    g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
+    const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
+#define S_(T, VT, V) k_sell<T, VT, XT, OP><<<g, kBlock, 0, s>>>(a.n_rows, m, V, x, b, invd, y, y2, c)
+    if (p == 2) {
+      TPR_SWITCH_(m.tpr, S_, uint16_t, m.v16)
+    } else if (p == 1 || std::is_same_v<XT, float>) {
+      TPR_SWITCH_(m.tpr, S_, float, m.v32)
+    } else {
+      if constexpr (std::is_same_v<XT, double>) TPR_SWITCH_(m.tpr, S_, double, m.v64)
+    }
+#undef S_
+    return;
+  }
+  DevCsr view = a;
+  view.prec = p;
+  g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
+  const int g = grid_rows(a.n_rows, a.tpr);
+#define L_(T, VT, V) k_row<T, VT, XT, OP><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, y2, c)
+  if (p >= 1 || std::is_same_v<XT, float>) {
+    TPR_SWITCH_(a.tpr, L_, float, a.values_f)
+  } else {
+    if constexpr (std::is_same_v<XT, double>) TPR_SWITCH_(a.tpr, L_, double, a.values)
+  }
+#undef L_
+}
+
+template <class XT, int MODE>
+void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y, double* out64,
+                    const double* b64, ChebCoef c, Reducer* red, int slot, cudaStream_t s) {
+  if (a.n_rows == 0) return;
+  ++g_launch_count;
+  Reducer r = red ? *red : Reducer{};
+  const int dr = red ? 1 : 0;
+  constexpr int kG[4] = {1, 1, 2, 2}, kS[4] = {1, 2, 3, 2};
+  const int p = eff_prec<XT>(a);
+  DevCsr view = a;
+  view.prec = p;
+  double bytes = matrix_pass_bytes(view, kG[MODE], kS[MODE], sizeof(XT));
+  if (MODE == 2 && red) bytes += sizeof(XT) * (double)a.n_rows;
+  if (MODE == 3) bytes += (red ? 16.0 : 8.0) * a.n_rows;
+  g_algo_bytes += bytes;
+  if (a.use_sell) {
+    const DevSell& m = a.sell;
+    const long work = (long)m.n_chunks * 32;
+#define S_(T, VT, V)                                                                                              \
+  k_sell_red<T, VT, XT, MODE><<<red_grid(k_sell_red<T, VT, XT, MODE>, work), kBlock, 0, s>>>(                      \
+      a.n_rows, m, V, x, b, invd, y, out64, b64, c, r, slot, dr)
+    if (p == 2) {
+      TPR_SWITCH_(m.tpr, S_, uint16_t, m.v16)
+    } else if (p == 1 || std::is_same_v<XT, float>) {
+      TPR_SWITCH_(m.tpr, S_, float, m.v32)
+    } else {
+      if constexpr (std::is_same_v<XT, double>) TPR_SWITCH_(m.tpr, S_, double, m.v64)
+    }
+#undef S_
+    return;
+  }
+  const long work = (long)a.n_rows * a.tpr;
+#define L_(T, VT, V)                                                                                             \
+  k_row_red<T, VT, XT, MODE><<<red_grid(k_row_red<T, VT, XT, MODE>, work), kBlock, 0, s>>>(                       \
+      a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, out64, b64, c, r, slot, dr)
+  if (p >= 1 || std::is_same_v<XT, float>) {
+    TPR_SWITCH_(a.tpr, L_, float, a.values_f)
+  } else {
+    if constexpr (std::is_same_v<XT, double>) TPR_SWITCH_(a.tpr, L_, double, a.values)
+  }
+#undef L_
+}
+
+}  // namespace
+
+template <class XT>
+void launch_spmv(const DevCsr& a, const XT* x, XT* y, cudaStream_t s) {
+  row_launch<XT, 0>(a, x, nullptr, nullptr, y, nullptr, ChebCoef{}, s);
+}
+template <class XT>
+void launch_residual(const DevCsr& a, const XT* b, const XT* x, XT* y, Reducer* red, int slot, cudaStream_t s) {
+  if (red) row_red_launch<XT, 1>(a, x, b, nullptr, y, nullptr, nullptr, ChebCoef{}, red, slot, s);
+  else row_launch<XT, 1>(a, x, b, nullptr, y, nullptr, ChebCoef{}, s);
+}
+void launch_spmv_dot(const DevCsr& a, const double* p, double* q, Reducer red, int slot, cudaStream_t s) {
+  row_red_launch<double, 0>(a, p, nullptr, nullptr, q, nullptr, nullptr, ChebCoef{}, &red, slot, s);
+}
+template <class XT>
+void launch_prolong_add(const DevCsr& p, const XT* zc, XT* z, cudaStream_t s) {
+  row_launch<XT, 2>(p, zc, nullptr, nullptr, z, nullptr, ChebCoef{}, s);
+}
+template <class XT>
+void launch_cheb_pre(const DevCsr& a, const XT* invd, const XT* b, XT* z, ChebCoef c, cudaStream_t s) {
+  row_launch<XT, 3>(a, nullptr, b, invd, z, nullptr, c, s);
+}
+template <class XT>
+void launch_cheb_post2(const DevCsr& a, const XT* invd, const XT* r0, XT* z, ChebCoef c, const XT* b_dot,
+                       Reducer* red, int slot, cudaStream_t s) {
+  row_red_launch<XT, 2>(a, r0, b_dot, invd, z, nullptr, nullptr, c, red, slot, s);
+}
+void launch_cheb_post2_out64(const DevCsr& a, const float* invd, const float* r0, const float* z, ChebCoef c,
+                             double* z_out, const double* b_dot, Reducer* red, int slot, cudaStream_t s) {
+  row_red_launch<float, 3>(a, r0, nullptr, invd, const_cast<float*>(z), z_out, b_dot, c, red, slot, s);
+}
+template <class XT>
+void launch_cheb1_pre_resid(const DevCsr& a, const XT* invd, const XT* b, XT* z, XT* t, ChebCoef c, cudaStream_t s) {
+  row_launch<XT, 4>(a, nullptr, b, invd, z, t, c, s);
+}
+template <class XT>
+void launch_cheb1_post(const DevCsr& a, const XT* invd, const XT* b, const XT* z, XT* z_out, ChebCoef c,
+                       cudaStream_t s) {
+  row_launch<XT, 5>(a, z, b, invd, nullptr, z_out, c, s);
+}
+void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, double* w, cudaStream_t s) {
+  row_launch<double, 6>(a, v, nullptr, invd, w, nullptr, ChebCoef{}, s);
+}
+
+#define INST_(XT)                                                                                              \
+  template void launch_spmv<XT>(const DevCsr&, const XT*, XT*, cudaStream_t);                                  \
+  template void launch_residual<XT>(const DevCsr&, const XT*, const XT*, XT*, Reducer*, int, cudaStream_t);     \
+  template void launch_prolong_add<XT>(const DevCsr&, const XT*, XT*, cudaStream_t);                           \
+  template void launch_cheb_pre<XT>(const DevCsr&, const XT*, const XT*, XT*, ChebCoef, cudaStream_t);          \
+  template void launch_cheb_post2<XT>(const DevCsr&, const XT*, const XT*, XT*, ChebCoef, const XT*, Reducer*,  \
+                                      int, cudaStream_t);                                                      \
+  template void launch_cheb1_pre_resid<XT>(const DevCsr&, const XT*, const XT*, XT*, XT*, ChebCoef, cudaStream_t); \
+  template void launch_cheb1_post<XT>(const DevCsr&, const XT*, const XT*, const XT*, XT*, ChebCoef, cudaStream_t);
+INST_(double)
+INST_(float)
+#undef INST_
+
+}  // namespace eqsb

@@ -1,218 +1,34 @@
-// Sparse / vector kernels of the M-solve (AMG-PCG) and the RKC recurrence.
-// All HBM-bound: CSR rows are read by TPR-thread groups (TPR chosen per
-// matrix from the mean row length) so that a warp streams contiguous
-// col_idx/values; gathered vectors hit L2. Reductions are fused into the
-// producing kernel and finished deterministically (fixed grid, last-block
-// ordered sum). V-cycle matrices may be stored with fp32 values (the
-// preconditioner only; PCG itself is fp64 throughout).
+// Vector kernels of the M-solve (AMG-PCG), the SPE estimator and the RKC
+// recurrence (the matrix row kernels are in k_rows.cu). All HBM-bound,
+// grid-stride; reductions are fused into the producing kernel and finished
+// deterministically (fixed grid, last-block ordered sum).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <unordered_map>
 
 #include "dev.cuh"
+#include "reduce.cuh"
 
 namespace eqsb {
 
 long g_launch_count = 0;
+double g_algo_bytes = 0.0;
 
 namespace {
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Block-wide sum; result valid in thread 0.
-__device__ __forceinline__ double block_sum(double v) {
-  __shared__ double sh[kBlock / 32];
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) sh[w] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (w == 0) {
-    r = l < (kBlock / 32) ? sh[l] : 0.0;
-    r = warp_sum(r);
-  }
-  return r;
-}
-
-// Store this block's partial; the last block to arrive sums all partials in
-// block order and writes the result (deterministic for a fixed grid).
-__device__ __forceinline__ void reduce_finish(double v, Reducer red, int slot) {
-  __shared__ bool last;
-  const double bs = block_sum(v);
-  double* part = red.partials + (size_t)slot * kRedGrid;
-  if (threadIdx.x == 0) {
-    part[blockIdx.x] = bs;
-    __threadfence();
-    const unsigned prev = atomicAdd(red.counters + slot, 1u);
-    last = (prev == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last) {
-    __threadfence();
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += kBlock) acc += __ldcg(part + i);
-    acc = block_sum(acc);
-    if (threadIdx.x == 0) {
-      red.scal[slot] = acc;
-      red.counters[slot] = 0u;
-    }
-  }
-}
-
-// Grid of a grid-stride reduction kernel: exactly one wave of resident blocks
-// (SMs x blocks-per-SM at this kernel's register use), so no tail wave; the
-// grid (hence the summation order) is fixed per kernel: deterministic.
-template <class K>
-int red_grid(K kernel, long work_items) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  static std::unordered_map<const void*, int> bps_cache;
-  const void* key = (const void*)kernel;
-  auto it = bps_cache.find(key);
-  int bps;
-  if (it == bps_cache.end()) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, kBlock, 0) != cudaSuccess || bps < 1) bps = 1;
-    bps_cache[key] = bps;
-  } else {
-    bps = it->second;
-  }
-  long g = (work_items + kBlock - 1) / kBlock;
-  g = std::min<long>(g, std::min<long>((long)sms * bps, kRedGrid));
-  return (int)std::max<long>(g, 1);
-}
-
-// matrix entries are streamed once per pass: evict-first loads keep L2 for
-// the gathered vectors (ld.global.cs)
-__device__ __forceinline__ double ldv(const double* p) { return __ldcs(p); }
-__device__ __forceinline__ double ldv(const float* p) { return (double)__ldcs(p); }
-
-constexpr int kUnroll = 8;  // independent entries in flight per thread
-
-// Row-group SpMV core: returns sum_k A_ik x_k (x_k w_k when SCALED) for `row`
-// in lane 0 of the group. Entries are fetched kUnroll at a time (indices and
-// values first, then the gathers) so each thread keeps several independent
-// loads in flight. All lanes of the warp must call it (shuffles); rows >= n
-// contribute nothing.
-template <int TPR, class VT, bool SCALED>
-__device__ __forceinline__ double row_dot(const int* __restrict__ rp, const int* __restrict__ ci,
-                                          const VT* __restrict__ v, const double* __restrict__ x,
-                                          const double* __restrict__ w, int row, int lane, int n) {
-  const bool ok = row < n;
-  const int beg = ok ? __ldg(rp + row) : 0, end = ok ? __ldg(rp + row + 1) : 0;
-  double s = 0.0;
-  for (int k0 = beg + lane; k0 < end; k0 += TPR * kUnroll) {
-    int c[kUnroll];
-    double a[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int k = k0 + u * TPR;
-      const bool in = k < end;
-      c[u] = in ? __ldcs(ci + k) : 0;
-      a[u] = in ? ldv(v + k) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const double xv = SCALED ? __ldg(x + c[u]) * __ldg(w + c[u]) : __ldg(x + c[u]);
-      s += a[u] * xv;
-    }
-  }
-#pragma unroll
-  for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, TPR);
-  return s;
-}
-
-// Generic row kernel (one pass over a matrix), warp-uniform early exit.
-// OP 0: y = A x                       (restriction, plain SpMV)
-// OP 1: y = b - A x                   (residual)
-// OP 2: z += A zc                     (prolongation + correction; v = P)
-// OP 3: z = c0 D^-1 b + c1 D^-1 (b - A D^-1 b / theta)          (Chebyshev(2) pre-smoothing from 0)
-// OP 4: z = D^-1 b / theta ; t = b - A z                         (Chebyshev(1) pre-smoothing + residual)
-// OP 5: zo = z + D^-1 (b - A z) / theta                          (Chebyshev(1) post-smoothing, out of place)
-// OP 6: w = D^-1 A x                                             (power iteration on D^-1 A)
-template <int TPR, class VT, int OP>
-__global__ void __launch_bounds__(kBlock) k_row(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                const VT* __restrict__ v, const double* __restrict__ x,
-                                                const double* __restrict__ b, const double* __restrict__ invd,
-                                                double* __restrict__ y, double* __restrict__ y2, ChebCoef c) {
-  const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
-  const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
-  if ((tid & ~31L) / TPR >= n) return;  // warp-uniform exit
-  constexpr bool SC = (OP == 3 || OP == 4);
-  const double s = row_dot<TPR, VT, SC>(rp, ci, v, SC ? b : x, invd, row, lane, n);
-  if (lane != 0 || row >= n) return;
-  if (OP == 0) y[row] = s;
-  if (OP == 1) y[row] = b[row] - s;
-  if (OP == 2) y[row] += s;
-  if (OP == 3) {
-    const double bi = b[row], di = invd[row];
-    y[row] = c.c0 * bi * di + c.c1 * di * (bi - s * c.inv_theta);
-  }
-  if (OP == 4) {
-    const double bi = b[row];
-    y[row] = bi * invd[row] * c.inv_theta;
-    y2[row] = bi - s * c.inv_theta;
-  }
-  if (OP == 5) y2[row] = x[row] + invd[row] * (b[row] - s) * c.inv_theta;
-  if (OP == 6) y[row] = s * invd[row];
-}
-
-// grid-stride row kernels with a fused reduction.
-// MODE 0: q = A p,  sum p.q
-// MODE 1: y = b - A x, sum y.y
-// MODE 2: z += c0 D^-1 r0 + c1 D^-1 (r0 - A D^-1 r0 / theta), sum b.z  (Chebyshev(2) post step 2)
-template <int TPR, class VT, int MODE>
-__global__ void __launch_bounds__(kBlock) k_row_red(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                                                    const VT* __restrict__ v, const double* __restrict__ x,
-                                                    const double* __restrict__ b, const double* __restrict__ invd,
-                                                    double* __restrict__ y, ChebCoef c, Reducer red, int slot,
-                                                    int do_red) {
-  const int lane = threadIdx.x % TPR;
-  const long groups_per_grid = (long)gridDim.x * (kBlock / TPR);
-  // every group iterates the same number of times (shuffles need full warps)
-  const long n_pad = ((n + (long)(kBlock / TPR) - 1) / (kBlock / TPR)) * (kBlock / TPR);
-  double acc = 0.0;
-  for (long row = (long)blockIdx.x * (kBlock / TPR) + threadIdx.x / TPR; row < n_pad; row += groups_per_grid) {
-    const double s = row_dot<TPR, VT, MODE == 2>(rp, ci, v, x, invd, (int)row, lane, n);
-    if (lane == 0 && row < n) {
-      if (MODE == 0) {
-        y[row] = s;
-        acc += x[row] * s;
-      } else if (MODE == 1) {
-        const double r = b[row] - s;
-        y[row] = r;
-        acc += r * r;
-      } else {
-        const double ri = x[row], di = invd[row];
-        const double zn = y[row] + (c.c0 * ri * di + c.c1 * di * (ri - s * c.inv_theta));
-        y[row] = zn;
-        if (do_red) acc += b[row] * zn;
-      }
-    }
-  }
-  if (do_red) reduce_finish(acc, red, slot);
-}
-
-__global__ void k_dense_solve(int n, const double* __restrict__ ainv, const double* __restrict__ b,
-                              double* __restrict__ z) {
+template <class XT>
+__global__ void k_dense_solve(int n, const double* __restrict__ ainv, const XT* __restrict__ b,
+                              XT* __restrict__ z) {
   extern __shared__ double sb[];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sb[i] = b[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sb[i] = (double)b[i];
   __syncthreads();
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int row = w; row < n; row += nw) {
     double s = 0.0;
     for (int k = l; k < n; k += 32) s += ainv[(size_t)row * n + k] * sb[k];
     s = warp_sum(s);
-    if (l == 0) z[row] = s;
+    if (l == 0) z[row] = (XT)s;
   }
 }
 
@@ -227,17 +43,34 @@ __global__ void k_jacobi(int n, const double* __restrict__ invd, const double* _
   if (do_red) reduce_finish(acc, red, slot);
 }
 
+// x += alpha p ; r -= alpha q ; r.r ; r32 = (float) r for an fp32 V-cycle
 __global__ void k_pcg_update(int n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                             const double* __restrict__ q, Reducer red) {
+                             const double* __restrict__ q, float* __restrict__ r32, Reducer red) {
   const double alpha = red.scal[S_RZ] / red.scal[S_PQ];
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     x[i] += alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
+    if (r32) r32[i] = (float)ri;
     acc += ri * ri;
   }
   reduce_finish(acc, red, S_RR);
+}
+
+__global__ void k_to_f32(long n, const double* __restrict__ x, float* __restrict__ y) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = (float)x[i];
+}
+// z64 = z32 ; slot <- b.z64
+__global__ void k_to_f64_dot(int n, const float* __restrict__ z32, double* __restrict__ z64,
+                             const double* __restrict__ b, Reducer red, int slot, int do_red) {
+  double acc = 0.0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    const double zi = (double)z32[i];
+    z64[i] = zi;
+    acc += b[i] * zi;
+  }
+  if (do_red) reduce_finish(acc, red, slot);
 }
 
 __global__ void k_pcg_direction(int n, double* __restrict__ p, const double* __restrict__ z,
@@ -311,9 +144,11 @@ __global__ void k_axpy_dev(int n, const double* __restrict__ coef, double sign, 
   const double a = sign * coef[0];
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] += a * x[i];
 }
-__global__ void k_diag_scale(int n, const double* __restrict__ invd, const double* __restrict__ b, double a,
-                             double* __restrict__ z) {
-  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) z[i] = a * invd[i] * b[i];
+template <class XT>
+__global__ void k_diag_scale(int n, const XT* __restrict__ invd, const XT* __restrict__ b, double a,
+                             XT* __restrict__ z) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
+    z[i] = (XT)(a * invd[i] * b[i]);
 }
 __global__ void k_scale(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = a * x[i];
@@ -349,7 +184,8 @@ __global__ void k_rkc_error(int n, const double* __restrict__ x, const double* _
   reduce_finish(acc, red, slot);
 }
 
-__global__ void k_gather(int n, const int* __restrict__ idx, const double* __restrict__ x, double* __restrict__ y) {
+template <class T>
+__global__ void k_gather(int n, const int* __restrict__ idx, const T* __restrict__ x, T* __restrict__ y) {
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = x[idx[i]];
 }
 __global__ void k_scatter(int n, const int* __restrict__ idx, const double* __restrict__ x, double* __restrict__ y) {
@@ -368,118 +204,37 @@ __global__ void k_boundary_load(int n, const int* __restrict__ rows, const doubl
   }
 }
 
-inline int grid_for(long n) {
-  long g = (n + kBlock - 1) / kBlock;
-  const long cap = 148L * 32;
-  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
-}
-inline int grid_rows(long n_rows, int tpr) {
-  long g = (n_rows * tpr + kBlock - 1) / kBlock;
-  return (int)(g < 1 ? 1 : g);
-}
-
-template <int OP>
-void row_launch(const DevCsr& a, const double* x, const double* b, const double* invd, double* y, double* y2,
-                ChebCoef c, cudaStream_t s) {
-  if (a.n_rows == 0) return;
-  ++g_launch_count;
-  const int g = grid_rows(a.n_rows, a.tpr);
-#define L_(T, VT, V) \
-  k_row<T, VT, OP><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, y2, c)
-#define D_(VT, V)                \
-  switch (a.tpr) {               \
-    case 1: L_(1, VT, V); break;   \
-    case 2: L_(2, VT, V); break;   \
-    case 4: L_(4, VT, V); break;   \
-    case 8: L_(8, VT, V); break;   \
-    case 16: L_(16, VT, V); break; \
-    default: L_(32, VT, V); break; \
-  }
-  if (a.values_f) {
-    D_(float, a.values_f)
-  } else {
-    D_(double, a.values)
-  }
-#undef D_
-#undef L_
-}
-
-template <int MODE>
-void row_red_launch(const DevCsr& a, const double* x, const double* b, const double* invd, double* y, ChebCoef c,
-                    Reducer* red, int slot, cudaStream_t s) {
-  if (a.n_rows == 0) return;
-  ++g_launch_count;
-  const long work = (long)a.n_rows * a.tpr;
-  Reducer r = red ? *red : Reducer{};
-  const int dr = red ? 1 : 0;
-#define L_(T, VT, V)                                                                                       \
-  k_row_red<T, VT, MODE><<<red_grid(k_row_red<T, VT, MODE>, work), kBlock, 0, s>>>(                         \
-      a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, c, r, slot, dr)
-#define D_(VT, V)                \
-  switch (a.tpr) {               \
-    case 1: L_(1, VT, V); break;   \
-    case 2: L_(2, VT, V); break;   \
-    case 4: L_(4, VT, V); break;   \
-    case 8: L_(8, VT, V); break;   \
-    case 16: L_(16, VT, V); break; \
-    default: L_(32, VT, V); break; \
-  }
-  if (a.values_f) {
-    D_(float, a.values_f)
-  } else {
-    D_(double, a.values)
-  }
-#undef D_
-#undef L_
-}
-
 }  // namespace
 
-void launch_spmv(const DevCsr& a, const double* x, double* y, cudaStream_t s) {
-  row_launch<0>(a, x, nullptr, nullptr, y, nullptr, ChebCoef{}, s);
-}
-void launch_residual(const DevCsr& a, const double* b, const double* x, double* y, Reducer* red, int slot,
-                     cudaStream_t s) {
-  if (red) row_red_launch<1>(a, x, b, nullptr, y, ChebCoef{}, red, slot, s);
-  else row_launch<1>(a, x, b, nullptr, y, nullptr, ChebCoef{}, s);
-}
-void launch_spmv_dot(const DevCsr& a, const double* p, double* q, Reducer red, int slot, cudaStream_t s) {
-  row_red_launch<0>(a, p, nullptr, nullptr, q, ChebCoef{}, &red, slot, s);
-}
-void launch_prolong_add(const DevCsr& p, const double* zc, double* z, cudaStream_t s) {
-  row_launch<2>(p, zc, nullptr, nullptr, z, nullptr, ChebCoef{}, s);
-}
-void launch_cheb_pre(const DevCsr& a, const double* invd, const double* b, double* z, ChebCoef c, cudaStream_t s) {
-  row_launch<3>(a, nullptr, b, invd, z, nullptr, c, s);
-}
-void launch_cheb_post2(const DevCsr& a, const double* invd, const double* r0, double* z, ChebCoef c,
-                       const double* b_dot, Reducer* red, int slot, cudaStream_t s) {
-  row_red_launch<2>(a, r0, b_dot, invd, z, c, red, slot, s);
-}
-void launch_cheb1_pre_resid(const DevCsr& a, const double* invd, const double* b, double* z, double* t, ChebCoef c,
-                            cudaStream_t s) {
-  row_launch<4>(a, nullptr, b, invd, z, t, c, s);
-}
-void launch_cheb1_post(const DevCsr& a, const double* invd, const double* b, const double* z, double* z_out,
-                       ChebCoef c, cudaStream_t s) {
-  row_launch<5>(a, z, b, invd, nullptr, z_out, c, s);
-}
-void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, double* w, cudaStream_t s) {
-  row_launch<6>(a, v, nullptr, invd, w, nullptr, ChebCoef{}, s);
-}
-
-void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s) {
+void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s,
+                       float* r32) {
   ++g_launch_count;
-  k_pcg_update<<<red_grid(k_pcg_update, n), kBlock, 0, s>>>(n, x, r, p, q, red);
+  k_pcg_update<<<red_grid(k_pcg_update, n), kBlock, 0, s>>>(n, x, r, p, q, r32, red);
+}
+void launch_to_f32(long n, const double* x, float* y, cudaStream_t s) {
+  if (n <= 0) return;
+  ++g_launch_count;
+  g_algo_bytes += 12.0 * n;
+  k_to_f32<<<grid_for(n), kBlock, 0, s>>>(n, x, y);
+}
+void launch_to_f64_dot(int n, const float* z32, double* z64, const double* b, Reducer* red, int slot, cudaStream_t s) {
+  ++g_launch_count;
+  g_algo_bytes += (red ? 20.0 : 12.0) * n;
+  Reducer rr = red ? *red : Reducer{};
+  k_to_f64_dot<<<red_grid(k_to_f64_dot, n), kBlock, 0, s>>>(n, z32, z64, b, rr, slot, red ? 1 : 0);
 }
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s) {
   ++g_launch_count;
   k_pcg_direction<<<grid_for(n), kBlock, 0, s>>>(n, p, z, scal);
 }
-void launch_dense_solve(int n, const double* ainv, const double* b, double* z, cudaStream_t s) {
+template <class XT>
+void launch_dense_solve(int n, const double* ainv, const XT* b, XT* z, cudaStream_t s) {
   ++g_launch_count;
-  k_dense_solve<<<1, 1024, n * sizeof(double), s>>>(n, ainv, b, z);
+  g_algo_bytes += 8.0 * n * n;
+  k_dense_solve<XT><<<1, 1024, n * sizeof(double), s>>>(n, ainv, b, z);
 }
+template void launch_dense_solve<double>(int, const double*, const double*, double*, cudaStream_t);
+template void launch_dense_solve<float>(int, const double*, const float*, float*, cudaStream_t);
 void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s) {
   ++g_launch_count;
   Reducer rr = red ? *red : Reducer{};
@@ -524,11 +279,15 @@ void launch_axpy_dev(int n, const double* coef, double sign, const double* x, do
   ++g_launch_count;
   k_axpy_dev<<<grid_for(n), kBlock, 0, s>>>(n, coef, sign, x, y);
 }
-void launch_diag_scale(int n, const double* invd, const double* b, double a, double* z, cudaStream_t s) {
+template <class XT>
+void launch_diag_scale(int n, const XT* invd, const XT* b, double a, XT* z, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launch_count;
-  k_diag_scale<<<grid_for(n), kBlock, 0, s>>>(n, invd, b, a, z);
+  g_algo_bytes += 3.0 * sizeof(XT) * n;
+  k_diag_scale<XT><<<grid_for(n), kBlock, 0, s>>>(n, invd, b, a, z);
 }
+template void launch_diag_scale<double>(int, const double*, const double*, double, double*, cudaStream_t);
+template void launch_diag_scale<float>(int, const float*, const float*, double, float*, cudaStream_t);
 void launch_scale(int n, double a, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;
   k_scale<<<grid_for(n), kBlock, 0, s>>>(n, a, x, y);
@@ -556,7 +315,12 @@ void launch_rkc_error(int n, const double* x, const double* xn, const double* f0
 void launch_gather(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launch_count;
-  k_gather<<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
+  k_gather<double><<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
+}
+void launch_gather_f(int n, const int* idx, const float* x, float* y, cudaStream_t s) {
+  if (n <= 0) return;
+  ++g_launch_count;
+  k_gather<float><<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
 }
 void launch_scatter(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
   if (n <= 0) return;
@@ -576,3 +340,4 @@ void launch_boundary_load(int n_rows, const int* rows, const double* coef, int n
 }
 
 }  // namespace eqsb
+

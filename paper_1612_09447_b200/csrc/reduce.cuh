@@ -1,0 +1,100 @@
+// Deterministic reduction helpers and grid sizing shared by the kernel files
+// (fixed grid, last-block ordered sum: the summation order never changes).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <unordered_map>
+
+#include "dev.cuh"
+
+namespace eqsb {
+namespace {
+
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum; result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[kBlock / 32];
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = l < (kBlock / 32) ? sh[l] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+// Store this block's partial; the last block to arrive sums all partials in
+// block order and writes the result (deterministic for a fixed grid).
+__device__ __forceinline__ void reduce_finish(double v, Reducer red, int slot) {
+  __shared__ bool last;
+  const double bs = block_sum(v);
+  double* part = red.partials + (size_t)slot * kRedGrid;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = bs;
+    __threadfence();
+    const unsigned prev = atomicAdd(red.counters + slot, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += kBlock) acc += __ldcg(part + i);
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) {
+      red.scal[slot] = acc;
+      red.counters[slot] = 0u;
+    }
+  }
+}
+
+// Grid of a grid-stride reduction kernel: exactly one wave of resident blocks
+// (SMs x blocks-per-SM at this kernel's register use), so no tail wave; the
+// grid (hence the summation order) is fixed per kernel: deterministic.
+template <class K>
+int red_grid(K kernel, long work_items) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static std::unordered_map<const void*, int> bps_cache;
+  const void* key = (const void*)kernel;
+  auto it = bps_cache.find(key);
+  int bps;
+  if (it == bps_cache.end()) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, kBlock, 0) != cudaSuccess || bps < 1) bps = 1;
+    bps_cache[key] = bps;
+  } else {
+    bps = it->second;
+  }
+  long g = (work_items + kBlock - 1) / kBlock;
+  g = std::min<long>(g, std::min<long>((long)sms * bps, kRedGrid));
+  return (int)std::max<long>(g, 1);
+}
+
+inline int grid_for(long n) {
+  long g = (n + kBlock - 1) / kBlock;
+  const long cap = 148L * 32;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+inline int grid_rows(long n_rows, int tpr) {
+  long g = (n_rows * tpr + kBlock - 1) / kBlock;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+}  // namespace eqsb

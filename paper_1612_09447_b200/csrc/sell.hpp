@@ -1,0 +1,47 @@
+// Sliced-ELL copy of a CSR operator with packed 16-bit column indices
+// (DESIGN.md §3 "SELL-16"). The fine-level operators are read 5-6 times per
+// PCG iteration and their 32-bit column indices are half of every V-cycle
+// pass, so the resident format trades them for 16-bit codes:
+//   - a chunk is the 32/tpr consecutive rows one warp processes (tpr lanes per
+//     row); its rows are padded to the chunk's longest row (rounded up to tpr)
+//     and stored slice-major, so every warp load reads 32 consecutive entries;
+//   - the chunk's columns are covered by at most kSellWindows windows of
+//     kSellSpan columns starting at `bases`; an entry stores
+//     (window << kSellShift) | (column - base);
+//   - padding entries hold code 0 (column = bases[0], a valid column) and value 0.
+// A matrix that has a chunk needing more windows keeps the plain CSR kernels.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "eqs_internal.hpp"
+
+namespace eqsb {
+
+constexpr int kSellWindows = 8;
+constexpr int kSellShift = 13;
+constexpr int kSellSpan = 1 << kSellShift;
+
+struct HostSell {
+  int tpr = 0, n_rows = 0, n_chunks = 0;
+  std::vector<long> chunk_ptr;   // [n_chunks + 1] entry offsets (multiples of 32)
+  std::vector<int> bases;        // [n_chunks][kSellWindows]
+  std::vector<uint16_t> code;    // packed column per entry
+  std::vector<long> src;         // CSR entry of every position (-1: padding)
+  long padded() const { return chunk_ptr.empty() ? 0 : chunk_ptr.back(); }
+};
+
+// lanes per row: each lane handles about 16 entries of the mean row
+int choose_sell_tpr(const HostCsr& a);
+// false (and `out` untouched) when some chunk's columns need more than kSellWindows windows
+bool build_sell(const HostCsr& a, int tpr, HostSell& out);
+// values in SELL order (padding 0), as T
+template <class T>
+std::vector<T> sell_values(const HostSell& s, const std::vector<double>& v) {
+  std::vector<T> out(s.src.size());
+  for (size_t k = 0; k < s.src.size(); ++k) out[k] = s.src[k] >= 0 ? (T)v[s.src[k]] : (T)0.0;
+  return out;
+}
+
+}  // namespace eqsb
