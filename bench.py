@@ -188,6 +188,121 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ B200 leg
+def apply_options(g, args):
+    if args.vcycle_values:
+        g.set_option(4, {"fp64": 0, "fp32": 1, "bf16": 2}[args.vcycle_values])
+
+
+def single_gpu_system(args, estimator=None):
+    import torch
+    import paper_1612_09447_b200 as eb
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("bench.py needs a CUDA device (no CPU fallback)")
+    spec = CONFIGS[args.config]
+    cfg = scenario(spec["n"], spec["jitter"], spec["planes"], estimator=estimator or args.estimator)
+    t0 = time.perf_counter()
+    g = eb.FemSystem(cfg, device=0)
+    apply_options(g, args)
+    return g, time.perf_counter() - t0, eb
+
+
+def run_euler_vs_rkc(args):
+    """Config 2: explicit Euler at dt = min(dt0, 1.8/rho)
+    (scenario.cpp:286-293) against RKC path B (s = 4, dt = 0.9 beta(4)/rho) on
+    the same state, one GPU. Both report simulated seconds per wall second and
+    DOF-stage-updates/s (device time, CUDA events)."""
+    import ctypes as C
+    import torch
+
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    g, t_setup, eb = single_gpu_system(args)
+    n = g.n_free
+    lib = eb.load_library()
+    x0 = np.zeros(n)
+    lib.eqs_random_vec(C.c_int(n), C.c_uint(31), x0.ctypes.data_as(C.POINTER(C.c_double)))
+    x0 *= 2e4
+    g.set_state(0.0, x0, 0.0)
+    rho = g.spectral_radius()
+    sp = C.c_void_p()
+    lib.eqs_get_stream(g._h, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value, device=torch.device("cuda", 0))
+    out = {}
+    for name, dt, run in (("euler", min(1e-5, 1.8 / rho), lambda dt: g.euler_step(dt)),
+                          ("rkc", 0.9 * 0.653 * (S_STAGES ** 2 - 1) / rho,
+                           lambda dt: g.rkc_advance_fixed(dt, S_STAGES, 1))):
+        g.set_state(0.0, x0, dt)
+        for _ in range(args.warmup):
+            run(dt)
+        st0 = g.stats()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            run(dt)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        st1 = g.stats()
+        fe = st1["m_solves"] - st0["m_solves"]
+        out[name] = {"dt": dt, "ms_per_step": ms / args.steps, "f_evals_per_step": fe / args.steps,
+                     "pcg_iters_per_solve": (st1["pcg_iterations"] - st0["pcg_iterations"]) / max(1, fe),
+                     "simulated_s_per_wall_s": dt * args.steps / (ms / 1e3),
+                     "dof_stage_updates_per_s": n * fe / (ms / 1e3)}
+    line = {"metric": "config 2: Euler vs RKC, simulated seconds per wall second (RKC path B vs Euler at 1.8/rho)",
+            "value": out["rkc"]["simulated_s_per_wall_s"], "unit": "simulated s / wall s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
+            "data": "synthetic", "rho": rho, "rkc_over_euler": out["rkc"]["simulated_s_per_wall_s"]
+            / out["euler"]["simulated_s_per_wall_s"],
+            "config": {"workload": f"{args.config} cube, x0 = 2e4*random_vec(31), {n} free dofs",
+                       "n_free": n}, "setup_s": t_setup, **out}
+    print(json.dumps(line), flush=True)
+
+
+def mrhs_rhs(g, n_rhs=40):
+    """Config 5 right-hand sides: b_k = M_II x*_k, x*_k = sum_{m=1..3} cos(2 pi m k/40) phi_m,
+    phi_m = sin(m pi z) cos(pi x) cos(pi y) at the free dofs."""
+    nodes, _, _ = g.mesh()
+    _, free, _ = g.dofs()
+    xyz = nodes[free]
+    phi = [np.sin(m * np.pi * xyz[:, 2]) * np.cos(np.pi * xyz[:, 0]) * np.cos(np.pi * xyz[:, 1]) for m in (1, 2, 3)]
+    X = np.stack([sum(np.cos(2 * np.pi * m * k / 40) * phi[m - 1] for m in (1, 2, 3)) for k in range(n_rhs)])
+    B = np.stack([g.mass_apply(X[k]) for k in range(n_rhs)])
+    return X, B
+
+
+def run_mrhs(args):
+    """Config 5: the 40-RHS sequence solved to 1e-12 with zero / previous /
+    SPE(8) start vectors, inputs resident (eqs_mass_solve_sequence)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    g, t_setup, eb = single_gpu_system(args)
+    X, B = mrhs_rhs(g)
+    n = g.n_free
+    res = {}
+    for mode, key in (("zero", 0), ("previous", 1), ("spe", 2)):
+        g.set_option(12, key)
+        g.mass_solve_sequence(B[:4])  # warm-up (graphs, buffers)
+        g.set_option(12, key)
+        its, ms, Xs = g.mass_solve_sequence(B, want_x=(mode == "spe"))
+        res[mode] = {"iters_total": int(its.sum()), "iters_per_solve": float(its.mean()),
+                     "iters_per_solve_k_ge_8": float(its[8:].mean()), "ms_total": ms,
+                     "solves_per_s": len(its) / (ms / 1e3), "iterations": its.tolist()}
+        if Xs is not None:
+            res[mode]["max_rel_err"] = float(max(np.linalg.norm(Xs[k] - X[k]) / np.linalg.norm(X[k])
+                                                 for k in range(len(X))))
+    line = {"metric": "config 5: MRHS sequence (40 RHS, PCG+AMG 1e-12), solves/s with SPE(8) starts",
+            "value": res["spe"]["solves_per_s"], "unit": "solves/s", "n_gpus": 1, "higher_is_better": True,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"M_II of {args.config} ({n} free dofs), b_k = M_II x*_k, k = 0..39"},
+            "spe_iters_vs_zero": res["spe"]["iters_total"] / res["zero"]["iters_total"],
+            "setup_s": t_setup, **res}
+    print(json.dumps(line), flush=True)
+
+
 def run_b200(args):
     rank, world, local_rank = dist_env()
     if world > 1 and "OMP_NUM_THREADS" not in os.environ:
@@ -216,6 +331,7 @@ def run_b200(args):
     else:
         g = eb.FemSystem(cfg, device=local_rank)
         owned = None
+    apply_options(g, args)
     t_setup = time.perf_counter() - t_setup
     n = g.n_free
     lib = eb.load_library()
@@ -359,9 +475,18 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the in-run CPU baseline sample")
     ap.add_argument("--estimator", default="spe", choices=["zero", "previous", "spe"],
                     help="MRHS start vectors (proj/src/start_vector.cpp); the reference nonlinear scenario uses spe")
+    ap.add_argument("--vcycle-values", default=None, choices=["fp64", "fp32", "bf16"],
+                    help="V-cycle matrix value precision (library default when omitted)")
+    ap.add_argument("--mode", default="rkc", choices=["rkc", "euler", "mrhs"],
+                    help="rkc: the headline line (default); euler: config 2 Euler vs RKC on --config (c2); "
+                         "mrhs: config 5 multiple-right-hand-side sequence on --config")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "euler":
+        run_euler_vs_rkc(args)
+    elif args.mode == "mrhs":
+        run_mrhs(args)
     else:
         run_b200(args)
 

@@ -219,6 +219,15 @@ int eqs_mass_apply(eqs_ctx* ctx, const double* v, double* y);
  * reported in res->converged, not as an error (test_solvers.cpp:108-116). */
 int eqs_mass_solve(eqs_ctx* ctx, const double* b, const double* x0, double tol, int max_iter, double* x,
                    eqs_pcg_result* res);
+/* Multiple-right-hand-side sequence (no reference
+ * counterpart beyond the eval_rhs solve path): the k right-hand sides
+ * B[k][n_free] are uploaded, then solved in order on the device with the
+ * context's start-vector estimator (x0 = estimator.next(b), PCG, feedback),
+ * exactly as eval_rhs does (fem_system.cpp:80-90). X[k][n_free] may be NULL;
+ * iterations[k] receives the PCG iterations; *device_ms the device time of
+ * the k solves. Non-convergence is a NumericalError. */
+int eqs_mass_solve_sequence(eqs_ctx* ctx, const double* B, int k, double tol, int max_iter, double* X,
+                            int* iterations, double* device_ms);
 
 /* ----------------------------------------------------------------- OdeSystem (proj/include/eqs/ode_system.hpp:45-73) */
 /* FemSystem::eval_residual (fem_system.cpp:62-67). */
@@ -270,7 +279,8 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * 3 = coarse-level Chebyshev degree (1 or 2), 4 = V-cycle matrix values
  * (0 fp64, 1 fp32, 2 bf16; default 2), 5/6/7 = CSR threads per row of levels
  * 0/1/2, 8 = CUDA graphs (0/1), 9 = incremental SPE (0/1), 10 = SELL-16
- * operators (0/1; default 1), 11 = fp32 V-cycle vectors (0/1; default 1).
+ * operators (0/1; default 1), 11 = fp32 V-cycle vectors (0/1; default 1),
+ * 12 = start-vector estimator (0 zero, 1 previous, 2 spe; resets its history).
  * The PCG operator and vectors are fp64 in every setting. */
 int eqs_set_option(eqs_ctx* ctx, int key, double value);
 /* The CUDA stream (cudaStream_t) every device call of this context runs on. */

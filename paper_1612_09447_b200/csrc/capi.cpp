@@ -389,6 +389,14 @@ int eqs_mass_solve(eqs_ctx* ctx, const double* b, const double* x0, double tol, 
                    eqs_pcg_result* res) {
   return guard([&] { fill_pcg(S(ctx).mass_solve_host(b, x0, tol, max_iter, x), res); });
 }
+int eqs_mass_solve_sequence(eqs_ctx* ctx, const double* B, int k, double tol, int max_iter, double* X,
+                            int* iterations, double* device_ms) {
+  return guard([&] {
+    if (k < 1 || !B) throw std::invalid_argument("eqs_mass_solve_sequence: need k >= 1 right-hand sides");
+    const double ms = S(ctx).mass_solve_sequence(B, k, tol, max_iter, X, iterations);
+    if (device_ms) *device_ms = ms;
+  });
+}
 int eqs_eval_residual(eqs_ctx* ctx, double t, const double* x, double* r) {
   return guard([&] { S(ctx).eval_residual_host(t, x, r); });
 }
@@ -535,6 +543,7 @@ int eqs_set_option(eqs_ctx* ctx, int key, double value) {
       case 9: g.spe_incremental = value != 0.0; break;
       case 10: g.set_sell(value != 0.0); break;
       case 11: g.set_vcycle_vectors_f32(value != 0.0); break;
+      case 12: g.reset_estimator((int)value); break;
       default: throw std::invalid_argument("eqs_set_option: unknown key");
     }
   });

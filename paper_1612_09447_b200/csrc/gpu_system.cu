@@ -147,6 +147,22 @@ void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
 }
 
 // 1/diag of the owned rows (local row i <-> local column i)
+// EQS_MEMTRACE=1: host RSS / peak at setup checkpoints (stderr)
+void memtrace(const char* tag) {
+  static const bool on = getenv("EQS_MEMTRACE") != nullptr;
+  if (!on) return;
+  FILE* f = fopen("/proc/self/status", "r");
+  if (!f) return;
+  char line[256];
+  long rss = 0, hwm = 0;
+  while (fgets(line, sizeof line, f)) {
+    if (!strncmp(line, "VmRSS:", 6)) rss = atol(line + 6);
+    if (!strncmp(line, "VmHWM:", 6)) hwm = atol(line + 6);
+  }
+  fclose(f);
+  fprintf(stderr, "[memtrace] %-28s rss %7.2f GB  peak %7.2f GB\n", tag, rss / 1048576.0, hwm / 1048576.0);
+}
+
 std::vector<double> inv_diagonal(const HostCsr& a) {
   std::vector<double> d(a.n_rows, 0.0);
   for (int i = 0; i < a.n_rows; ++i)
@@ -177,22 +193,30 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
   for (int t = 0; t < n_tets_; ++t)
     if (!prob_.materials.count(prob_.mesh.region[t]))
       throw ConfigError("no material for region " + std::to_string(prob_.mesh.region[t]));
+  memtrace("problem");
   // FemSystem ctor: assemble M once (fem_system.cpp:27-36)
   assemble_mass_blocks(prob_, m_ii_, m_ib_);
+  memtrace("mass assembled");
   ++stats_.assemblies;
   // mass preconditioner (built once; the reference builds it lazily on first use, fem_system.cpp:48-54)
   if (prob_.solver.precond == 2) amg_ = build_amg(m_ii_, prob_.solver);
   ++stats_.precond_setups;
+  memtrace("amg built");
   // V-cycle operators of the coarse levels: lumped filtered Galerkin matrices
   // (DESIGN.md §4); the hierarchy reported through the API stays the reference's
-  AmgHierarchy vh;
-  if (prob_.solver.precond == 2) {
-    vh = amg_;
-    const double eps = prob_.solver.amg_coarse_filter;
-    for (size_t l = 1; l + 1 < vh.levels.size(); ++l)
-      if (eps > 0.0) vh.levels[l].A = filter_lumped(amg_.levels[l].A, eps);
+  {
+    std::vector<HostCsr> filtered;
+    if (prob_.solver.precond == 2) {
+      filtered.resize(amg_.levels.size());
+      const double eps = prob_.solver.amg_coarse_filter;
+      for (size_t l = 1; l + 1 < amg_.levels.size(); ++l)
+        if (eps > 0.0) filtered[l] = filter_lumped(amg_.levels[l].A, eps);
+    }
+    memtrace("coarse filter");
+    plan_ = build_plan(prob_, m_ii_, m_ib_, amg_, comm_->size(), comm_->rank(), prob_.solver.amg_replicate_rows,
+                       &filtered);
   }
-  plan_ = build_plan(prob_, m_ii_, m_ib_, vh, comm_->size(), comm_->rank(), prob_.solver.amg_replicate_rows);
+  memtrace("plan");
   const LocalSpace& s0 = plan_.space[0];
   n_own_ = s0.n_own();
   n_ghost_ = s0.n_ghost();
@@ -203,7 +227,20 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
   loc2ref_.assign(n_full_, -1);
   for (int i = 0; i < n_loc_; ++i) loc2ref_[i] = dm.free_dofs[i < n_own_ ? s0.owned[i] : s0.ghosts[i - n_own_]];
   for (int j = 0; j < n_fixloc_; ++j) loc2ref_[n_loc_ + j] = plan_.fixed[j];
-  if (device_ >= 0) build_device();  // device < 0: host-only setup (artefact checks without a GPU)
+  if (device_ >= 0) {
+    build_device();
+    // the rank's operators now live in HBM: drop their host copies (the index
+    // spaces stay for the partition queries)
+    for (auto* v : {&plan_.A, &plan_.P, &plan_.R}) std::vector<HostCsr>().swap(*v);
+    plan_.mii = HostCsr{};
+    plan_.mib = HostCsr{};
+    std::vector<int>().swap(plan_.tet_dofs);
+    if (comm_->size() > 1) {
+      // the global hierarchy is only needed for single-rank API queries
+      for (auto& lv : amg_.levels) lv.A = lv.P = lv.R = HostCsr{};
+    }
+  }
+  memtrace("device built");
 }
 
 GpuSystem::~GpuSystem() {
@@ -1454,6 +1491,46 @@ PcgResult GpuSystem::mass_solve_host(const double* b, const double* x0, double t
   F_.download(x, n_own_, stream_);
   sync();
   return r;
+}
+
+// Config-5 MRHS microbenchmark: k right-hand sides solved in
+// sequence on the device with the configured start-vector estimator (the
+// eval_rhs solve path without K(x)x). B and X are host [k][n_free]; X may be
+// null. Returns the device time of the k solves (CUDA events, inputs resident).
+double GpuSystem::mass_solve_sequence(const double* B, int k, double tol, int max_iter, double* X, int* its) {
+  require_single("mass_solve_sequence");
+  const size_t n = (size_t)n_own_;
+  DevBuf<double> Bd, Xd;
+  Bd.alloc(std::max<size_t>(1, n * k));
+  Xd.alloc(std::max<size_t>(1, n * k));
+  Bd.upload(B, n * k, stream_);
+  sync();
+  cudaEvent_t e0 = get_event(), e1 = get_event();
+  CK(cudaEventRecord(e0, stream_));
+  for (int j = 0; j < k; ++j) {
+    const double* b = Bd.p + n * j;
+    double* x = Xd.p + n * j;
+    const bool has_x0 = estimator_next(b, x);
+    const PcgResult r = pcg_dev(b, has_x0 ? x : nullptr, x, tol, max_iter);
+    if (!r.converged) throw NumericalError("mass_solve_sequence: PCG did not converge");
+    estimator_feedback(x);
+    if (its) its[j] = r.iterations;
+  }
+  CK(cudaEventRecord(e1, stream_));
+  sync();
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  if (X) Xd.download(X, n * k, stream_);
+  sync();
+  return ms;
+}
+
+void GpuSystem::reset_estimator(int mode) {
+  if (mode < 0 || mode > 2) throw std::invalid_argument("estimator mode must be 0 (zero), 1 (previous) or 2 (spe)");
+  prob_.solver.estimator_mode = mode;
+  history_.clear();
+  hist_pool_.clear();
+  spe_clean_ = false;
 }
 
 void GpuSystem::mass_apply_host(const double* v, double* y) {

@@ -145,6 +145,8 @@ class GpuSystem {
   void eval_residual_host(double t, const double* x, double* r);
   PcgResult eval_rhs_host(double t, const double* x, double* f);
   PcgResult mass_solve_host(const double* b, const double* x0, double tol, int max_iter, double* x);
+  double mass_solve_sequence(const double* B, int k, double tol, int max_iter, double* X, int* its);
+  void reset_estimator(int mode);  // switch zero/previous/spe and drop the history
   void mass_apply_host(const double* v, double* y);
   void apply_minv_stiffness_host(double t, const double* x_state, const double* v, double* y);
   void lift_full_host(double t, const double* x_free, double* x_full);

@@ -100,13 +100,17 @@ std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out
 }
 
 PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m_ib, const AmgHierarchy& h,
-                         int nranks, int rank, int rep_threshold) {
+                         int nranks, int rank, int rep_threshold, const std::vector<HostCsr>* level_A) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("build_plan: bad rank/nranks");
   PartitionPlan plan;
   plan.nranks = nranks;
   plan.rank = rank;
   const int L = h.levels.empty() ? 1 : (int)h.levels.size();
-  auto A_of = [&](int l) -> const HostCsr& { return h.levels.empty() ? m_ii : h.levels[l].A; };
+  auto A_of = [&](int l) -> const HostCsr& {
+    if (h.levels.empty()) return m_ii;
+    if (level_A && l < (int)level_A->size() && (*level_A)[l].n_rows > 0) return (*level_A)[l];
+    return h.levels[l].A;
+  };
   // first replicated level: small coarse levels (and always the dense coarsest)
   // are held whole on every rank; a single level (no hierarchy) stays partitioned
   int rep = L;

@@ -37,6 +37,13 @@ double matrix_pass_bytes(const DevCsr& a, int gathered, int streamed, int xbytes
 namespace {
 
 constexpr int kUnroll = 8;  // independent entries in flight per lane
+#ifndef SELL_UNROLL1
+#define SELL_UNROLL1 8
+#endif
+#ifndef SELL_MINB
+#define SELL_MINB 1
+#endif
+constexpr int kSellUnroll1 = SELL_UNROLL1;
 
 // matrix entries are streamed once per pass: evict-first loads keep L2 for
 // the gathered vectors (ld.global.cs). bf16 values are stored as uint16 bit
@@ -86,18 +93,20 @@ __device__ __forceinline__ XT sell_dot(const DevSell& m, const VT* __restrict__ 
   const int mybase = lane < 8 ? __ldg(m.bases + 8L * chunk + lane) : 0;
   const uint16_t* cp = m.code + beg + lane;
   const VT* vp = v + beg + lane;
+  // one batch covers a whole fine-level row (<= 16 slices at TPR 1)
+  constexpr int U = TPR == 1 ? kSellUnroll1 : kUnroll;
   XT s = 0;
-  for (int s0 = 0; s0 < S; s0 += kUnroll) {
-    unsigned cd[kUnroll];
-    XT a[kUnroll];
+  for (int s0 = 0; s0 < S; s0 += U) {
+    unsigned cd[U];
+    XT a[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const bool in = s0 + u < S;
       cd[u] = in ? (unsigned)__ldcs(cp + 32 * (s0 + u)) : 0u;
       a[u] = in ? (XT)ldv(vp + 32 * (s0 + u)) : (XT)0;
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int c = __shfl_sync(0xffffffffu, mybase, (int)(cd[u] >> 13)) + (int)(cd[u] & 0x1fffu);
       if (s0 + u < S) {
         const XT xv = SCALED ? __ldg(x + c) * __ldg(w + c) : __ldg(x + c);
@@ -199,7 +208,7 @@ __global__ void __launch_bounds__(kBlock) k_row(int n, const int* __restrict__ r
 }
 
 template <int TPR, class VT, class XT, int OP>
-__global__ void __launch_bounds__(kBlock) k_sell(int n, DevSell m, const VT* __restrict__ v,
+__global__ void __launch_bounds__(kBlock, SELL_MINB) k_sell(int n, DevSell m, const VT* __restrict__ v,
                                                  const XT* __restrict__ x, const XT* __restrict__ b,
                                                  const XT* __restrict__ invd, XT* __restrict__ y,
                                                  XT* __restrict__ y2, ChebCoef c) {

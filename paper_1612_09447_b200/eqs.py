@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libeqs_b200.so")
+LIB_PATH = os.environ.get("EQS_B200_LIB") or os.path.join(_HERE, "libeqs_b200.so")
 _lib = None
 
 
@@ -317,6 +317,19 @@ class FemSystem:
         y = np.zeros(self.n_free)
         _check(load_library().eqs_mass_apply(self._h, _dp(_f64(v)), _dp(y)))
         return y
+
+    def mass_solve_sequence(self, B, tol: float = 1e-12, max_iter: int = 500, want_x: bool = False):
+        """Solve the rows of B (k x n_free) in order with the configured start-vector
+        estimator on the device; returns (iterations[k], device_ms, X or None)."""
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        k = B.shape[0]
+        its = np.zeros(k, dtype=np.int32)
+        ms = C.c_double()
+        X = np.zeros_like(B) if want_x else None
+        _check(load_library().eqs_mass_solve_sequence(
+            self._h, _dp(B), C.c_int(k), C.c_double(tol), C.c_int(max_iter), _dp(X) if want_x else None,
+            its.ctypes.data_as(C.POINTER(C.c_int)), C.byref(ms)))
+        return its, ms.value, X
 
     def mass_solve(self, b, x0=None, tol: float = 1e-12, max_iter: int = 500):
         x = np.zeros(self.n_free)
