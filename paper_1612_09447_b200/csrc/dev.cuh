@@ -52,6 +52,16 @@ struct DevSell {
   const uint16_t* v16 = nullptr;     // bf16 bit patterns
 };
 
+// Packed SELL copy (sell.hpp "SELL-P"): bf16 value | 16-bit column code per
+// 32-bit word, 16-byte groups; tpr == 0: absent.
+struct DevSellP {
+  int tpr = 0, n_chunks = 0, shift = 13, windows = 8;
+  long padded = 0;                  // stored entries (nnz + padding)
+  const int* chunk_ptr = nullptr;   // [n_chunks + 1] in 16-byte groups
+  const int* bases = nullptr;       // [n_chunks][windows]
+  const uint4* words = nullptr;
+};
+
 // CSR matrix resident in HBM (int32 indices, fp64 values, sorted columns),
 // optionally with reduced-precision value copies and a SELL copy that the
 // kernels use instead when `use_sell` is set.
@@ -66,7 +76,10 @@ struct DevCsr {
   int prec = 0;               // values read by the kernels: 0 fp64, 1 fp32, 2 bf16 (SELL only; CSR reads fp32)
   bool use_sell = false;
   DevSell sell;
-  int lanes() const { return use_sell ? sell.tpr : tpr; }
+  DevSellP pk;  // used instead of `sell` for bf16 values (prec 2) when present
+  bool packed() const { return use_sell && prec == 2 && pk.tpr > 0; }
+  bool sell16() const { return use_sell && sell.tpr > 0 && !packed(); }
+  int lanes() const { return packed() ? pk.tpr : sell16() ? sell.tpr : tpr; }
 };
 
 struct ChebCoef {

@@ -88,21 +88,7 @@ void upload_csr(const HostCsr& h, DevCsr& d, DevBuf<int>& rp, DevBuf<int>& ci, D
   d.tpr = choose_tpr(h);
 }
 
-uint16_t to_bf16(double d) {  // round to nearest even
-  const float f = (float)d;
-  uint32_t u;
-  std::memcpy(&u, &f, 4);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
-  u += 0x7fffu + ((u >> 16) & 1u);
-  return (uint16_t)(u >> 16);
-}
-
-// SELL copy of h (sell.hpp) with fp64/fp32/bf16 values; d.sell stays absent
-// when some chunk cannot be encoded
-void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
-  d.sell = DevSell{};
-  HostSell hs;
-  if (h.n_rows == 0 || !build_sell(h, choose_sell_tpr(h), hs)) return;
+void upload_sell16(const HostCsr& h, const HostSell& hs, DevCsr& d, SellBufs& b, cudaStream_t s) {
   const size_t np = std::max<long>(1, hs.padded());
   // chunk pointers and bases padded past the end: the pipelined kernels copy
   // whole tiles of metadata (10 pointers, 64 bases) with bulk copies
@@ -144,6 +130,35 @@ void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.sell.v64 = b.v64.p;
   d.sell.v32 = b.v32.p;
   d.sell.v16 = b.v16.p;
+}
+
+// SELL copies of h (sell.hpp): SELL-16 with fp64/fp32/bf16 values and the
+// packed bf16 SELL-P; each stays absent when some chunk cannot be encoded
+void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
+  d.sell = DevSell{};
+  d.pk = DevSellP{};
+  if (h.n_rows == 0) return;
+  HostSell hs;
+  if (build_sell(h, choose_sell_tpr(h), hs)) upload_sell16(h, hs, d, b, s);
+  // packed bf16 copy for the V-cycle kernels (sell.hpp "SELL-P")
+  HostSellP hp;
+  if (!build_sell_packed(h, choose_sell_tpr(h), hp)) return;
+  std::vector<int> pcp = hp.chunk_ptr;
+  b.pk_cp.alloc(pcp.size());
+  b.pk_cp.upload(pcp.data(), pcp.size(), s);
+  b.pk_bases.alloc(std::max<size_t>(1, hp.bases.size()));
+  b.pk_bases.upload(hp.bases.data(), hp.bases.size(), s);
+  b.pk_words.alloc(std::max<size_t>(4, hp.words.size()));
+  b.pk_words.upload(hp.words.data(), hp.words.size(), s);
+  CK(cudaStreamSynchronize(s));
+  d.pk.tpr = hp.tpr;
+  d.pk.n_chunks = hp.n_chunks;
+  d.pk.shift = hp.shift;
+  d.pk.windows = hp.windows;
+  d.pk.padded = hp.padded();
+  d.pk.chunk_ptr = b.pk_cp.p;
+  d.pk.bases = b.pk_bases.p;
+  d.pk.words = reinterpret_cast<const uint4*>(b.pk_words.p);
 }
 
 // 1/diag of the owned rows (local row i <-> local column i)
@@ -599,7 +614,7 @@ void GpuSystem::set_sell(bool on) {
   mii_.use_sell = on && mii_.sell.tpr > 0;
   for (size_t l = 0; l < levels_.size(); ++l) {
     DevLevel& lv = levels_[l];
-    for (DevCsr* m : {&lv.A, &lv.P, &lv.R}) m->use_sell = on && m->sell.tpr > 0;
+    for (DevCsr* m : {&lv.A, &lv.P, &lv.R}) m->use_sell = on && (m->sell.tpr > 0 || m->pk.tpr > 0);
   }
 }
 

@@ -81,6 +81,8 @@ struct SellBufs {
   DevBuf<double> v64;
   DevBuf<float> v32;
   DevBuf<uint16_t> v16;
+  DevBuf<int> pk_cp, pk_bases;  // packed bf16 copy (sell.hpp SELL-P)
+  DevBuf<uint32_t> pk_words;
 };
 
 struct DevLevel {

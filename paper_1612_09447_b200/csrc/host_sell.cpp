@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstring>
 
 #include "sell.hpp"
 
@@ -76,6 +77,89 @@ bool build_sell(const HostCsr& a, int tpr, HostSell& out) {
   }
   out = std::move(s);
   return true;
+}
+
+
+uint16_t to_bf16(double d) {
+  const float f = (float)d;
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+namespace {
+// windows of `span` columns covering the sorted columns of one chunk; false if
+// more than `max_w` are needed
+bool chunk_windows(std::vector<int>& cols, int span, int max_w, int* out) {
+  std::sort(cols.begin(), cols.end());
+  int w = 0;
+  for (size_t i = 0; i < cols.size();) {
+    if (w == max_w) return false;
+    const int b = cols[i];
+    out[w++] = b;
+    while (i < cols.size() && cols[i] < b + span) ++i;
+  }
+  for (int k = w; k < max_w; ++k) out[k] = INT_MAX;  // unused
+  return true;
+}
+}  // namespace
+
+bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out) {
+  const int rows_per_chunk = 32 / tpr;
+  const int n_chunks = (a.n_rows + rows_per_chunk - 1) / rows_per_chunk;
+  for (int shift = 13; shift >= 11; --shift) {
+    const int windows = 1 << (16 - shift), span = 1 << shift;
+    std::vector<int> len(n_chunks + 1, 0);
+    std::vector<int> bases((size_t)n_chunks * windows, 0);
+    int fail = 0;
+#pragma omp parallel
+    {
+      std::vector<int> cols;
+#pragma omp for schedule(static) reduction(max : fail)
+      for (int c = 0; c < n_chunks; ++c) {
+        const int r0 = c * rows_per_chunk, r1 = std::min(a.n_rows, r0 + rows_per_chunk);
+        int maxlen = 0;
+        for (int r = r0; r < r1; ++r) maxlen = std::max(maxlen, a.row_ptr[r + 1] - a.row_ptr[r]);
+        cols.assign(a.col_idx.begin() + a.row_ptr[r0], a.col_idx.begin() + a.row_ptr[r1]);
+        if (!chunk_windows(cols, span, windows, &bases[(size_t)c * windows])) fail = 1;
+        const int groups = (maxlen + kPackGroup - 1) / kPackGroup;
+        len[c + 1] = 32 * ((groups + tpr - 1) / tpr);
+      }
+    }
+    if (fail) continue;
+    for (int c = 0; c < n_chunks; ++c) len[c + 1] += len[c];
+    HostSellP s;
+    s.tpr = tpr;
+    s.n_rows = a.n_rows;
+    s.n_chunks = n_chunks;
+    s.shift = shift;
+    s.windows = windows;
+    s.chunk_ptr = std::move(len);
+    s.bases = std::move(bases);
+    s.words.assign(s.padded(), 0u);
+#pragma omp parallel for schedule(static)
+    for (int c = 0; c < n_chunks; ++c) {
+      const int* wb = &s.bases[(size_t)c * windows];
+      const int r0 = c * rows_per_chunk, r1 = std::min(a.n_rows, r0 + rows_per_chunk);
+      for (int r = r0; r < r1; ++r) {
+        const int q = r - r0;
+        for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
+          const int j = k - a.row_ptr[r], col = a.col_idx[k];
+          const int g = j / kPackGroup, e = j % kPackGroup;
+          int w = windows - 1;  // windows ascend: the owner is the last base <= col
+          while (w > 0 && wb[w] > col) --w;
+          const long pos = 4L * (s.chunk_ptr[c] + 32L * (g / tpr) + q * tpr + g % tpr) + e;
+          const uint32_t code = ((uint32_t)w << shift) | (uint32_t)(col - wb[w]);
+          s.words[pos] = ((uint32_t)to_bf16(a.values[k]) << 16) | code;
+        }
+      }
+    }
+    out = std::move(s);
+    return true;
+  }
+  return false;
 }
 
 }  // namespace eqsb

@@ -24,7 +24,9 @@ namespace eqsb {
 // (n_cols each) and the streamed row vectors (n_rows each).
 double matrix_pass_bytes(const DevCsr& a, int gathered, int streamed, int xbytes) {
   double m;
-  if (a.use_sell) {
+  if (a.packed()) {
+    m = 4.0 * (double)a.pk.padded + (4.0 + 4.0 * a.pk.windows) * a.pk.n_chunks;
+  } else if (a.sell16()) {
     const double vs = a.prec == 2 ? 2.0 : a.prec == 1 ? 4.0 : 8.0;
     m = (double)a.sell.padded * (2.0 + vs) + 40.0 * a.sell.n_chunks;  // padded entries are read too
   } else {
@@ -111,6 +113,45 @@ __device__ __forceinline__ XT sell_dot(const DevSell& m, const VT* __restrict__ 
       if (s0 + u < S) {
         const XT xv = SCALED ? __ldg(x + c) * __ldg(w + c) : __ldg(x + c);
         s += a[u] * xv;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, TPR);
+  return s;
+}
+
+// SELL-P core (sell.hpp): per step every lane reads one 16-byte group of four
+// packed entries (bf16 value in the high half: decoding is a mask). Steps are
+// batched by 4 (a whole fine-level row per batch at TPR 1). Result in lane
+// (row_in_chunk * TPR).
+template <int TPR, class XT, bool SCALED>
+__device__ __forceinline__ XT sellp_dot(const DevSellP& m, int chunk, int lane, const XT* __restrict__ x,
+                                        const XT* __restrict__ w) {
+  const int beg = __ldg(m.chunk_ptr + chunk);
+  const int S = (__ldg(m.chunk_ptr + chunk + 1) - beg) >> 5;  // steps (warp-uniform)
+  const int mybase = lane < m.windows ? __ldg(m.bases + (long)m.windows * chunk + lane) : 0;
+  const unsigned mask = (1u << m.shift) - 1u;
+  const int shift = m.shift;
+  const uint4* p = m.words + beg + lane;
+  constexpr int U = 4;
+  XT s = 0;
+  for (int s0 = 0; s0 < S; s0 += U) {
+    uint4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) q[u] = s0 + u < S ? __ldcs(p + 32 * (s0 + u)) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned wd[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const unsigned code = wd[e] & 0xffffu;
+        const int c = __shfl_sync(0xffffffffu, mybase, (int)(code >> shift)) + (int)(code & mask);
+        if (s0 + u < S) {
+          const XT a = (XT)__uint_as_float(wd[e] & 0xffff0000u);
+          const XT xv = SCALED ? __ldg(x + c) * __ldg(w + c) : __ldg(x + c);
+          s += a * xv;
+        }
       }
     }
   }
@@ -223,6 +264,41 @@ __global__ void __launch_bounds__(kBlock, SELL_MINB) k_sell(int n, DevSell m, co
   if (act) e.store(row, s, y, y2, nullptr, c, 0);
 }
 
+template <int TPR, class XT, int OP>
+__global__ void __launch_bounds__(kBlock) k_sellp(int n, DevSellP m, const XT* __restrict__ x,
+                                                  const XT* __restrict__ b, const XT* __restrict__ invd,
+                                                  XT* __restrict__ y, XT* __restrict__ y2, ChebCoef c) {
+  const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (chunk >= m.n_chunks) return;  // warp-uniform exit
+  constexpr bool SC = kScaled<OP, -1>;
+  const int row = chunk * (32 / TPR) + lane / TPR;
+  const bool act = lane % TPR == 0 && row < n;
+  Epi<OP, -1, XT> e;
+  if (act) e.load(row, x, b, invd, y, nullptr, 0);
+  const XT s = sellp_dot<TPR, XT, SC>(m, chunk, lane, SC ? b : x, invd);
+  if (act) e.store(row, s, y, y2, nullptr, c, 0);
+}
+
+template <int TPR, class XT, int MODE>
+__global__ void __launch_bounds__(kBlock) k_sellp_red(int n, DevSellP m, const XT* __restrict__ x,
+                                                      const XT* __restrict__ b, const XT* __restrict__ invd,
+                                                      XT* __restrict__ y, double* __restrict__ out64,
+                                                      const double* __restrict__ b64, ChebCoef c, Reducer red,
+                                                      int slot, int do_red) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (kBlock / 32);
+  double acc = 0.0;
+  for (int chunk = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); chunk < m.n_chunks; chunk += warps) {
+    const int row = chunk * (32 / TPR) + lane / TPR;
+    const bool act = lane % TPR == 0 && row < n;
+    Epi<0, MODE, XT> e;
+    if (act) e.load(row, x, b, invd, y, b64, do_red);
+    const XT s = sellp_dot<TPR, XT, kScaled<0, MODE>>(m, chunk, lane, x, invd);
+    if (act) acc += e.store(row, s, y, nullptr, out64, c, do_red);
+  }
+  if (do_red) reduce_finish(acc, red, slot);
+}
+
 // grid-stride kernels with a fused reduction (fixed grid: deterministic)
 template <int TPR, class VT, class XT, int MODE>
 __global__ void __launch_bounds__(kBlock) k_row_red(int n, const int* __restrict__ rp, const int* __restrict__ ci,
@@ -282,8 +358,9 @@ template <class XT>
 int eff_prec(const DevCsr& a) {
   int p = a.prec;
   if (std::is_same_v<XT, float> && p == 0) p = 1;
-  if (!a.use_sell && p == 2) p = 1;  // CSR has no bf16 copy
-  if (!a.use_sell && p == 1 && !a.values_f) p = 0;
+  const bool has16 = a.use_sell && a.sell.tpr > 0, hasp = a.use_sell && a.pk.tpr > 0;
+  if (p == 2 && !has16 && !hasp) p = 1;  // CSR has no bf16 copy
+  if (p == 1 && !has16 && !a.values_f) p = 0;
   return p;
 }
 
@@ -294,10 +371,19 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
   // gathered / streamed row vectors per op (Epi)
   constexpr int kG[7] = {1, 1, 1, 2, 2, 1, 1}, kS[7] = {1, 2, 2, 1, 2, 3, 2};
   const int p = eff_prec<XT>(a);
-  if (a.use_sell) {
+  DevCsr view = a;
+  view.prec = p;
+  if (view.packed()) {
+    g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
+    const DevSellP& m = a.pk;
+    const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
+#define P_(T, VT, V) k_sellp<T, XT, OP><<<g, kBlock, 0, s>>>(a.n_rows, m, x, b, invd, y, y2, c)
+    TPR_SWITCH_(m.tpr, P_, void, 0)
+#undef P_
+    return;
+  }
+  if (view.sell16()) {
     const DevSell& m = a.sell;
-    DevCsr view = a;
-    view.prec = p;
     g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
     const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
 #define S_(T, VT, V) k_sell<T, VT, XT, OP><<<g, kBlock, 0, s>>>(a.n_rows, m, V, x, b, invd, y, y2, c)
@@ -311,8 +397,6 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
 #undef S_
     return;
   }
-  DevCsr view = a;
-  view.prec = p;
   g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
   const int g = grid_rows(a.n_rows, a.tpr);
 #define L_(T, VT, V) k_row<T, VT, XT, OP><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, y2, c)
@@ -339,7 +423,17 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
   if (MODE == 2 && red) bytes += sizeof(XT) * (double)a.n_rows;
   if (MODE == 3) bytes += (red ? 16.0 : 8.0) * a.n_rows;
   g_algo_bytes += bytes;
-  if (a.use_sell) {
+  if (view.packed()) {
+    const DevSellP& m = a.pk;
+    const long work = (long)m.n_chunks * 32;
+#define P_(T, VT, V)                                                                                              \
+  k_sellp_red<T, XT, MODE><<<red_grid(k_sellp_red<T, XT, MODE>, work), kBlock, 0, s>>>(a.n_rows, m, x, b, invd, y, \
+                                                                                      out64, b64, c, r, slot, dr)
+    TPR_SWITCH_(m.tpr, P_, void, 0)
+#undef P_
+    return;
+  }
+  if (view.sell16()) {
     const DevSell& m = a.sell;
     const long work = (long)m.n_chunks * 32;
 #define S_(T, VT, V)                                                                                              \

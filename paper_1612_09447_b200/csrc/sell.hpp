@@ -45,3 +45,29 @@ std::vector<T> sell_values(const HostSell& s, const std::vector<double>& v) {
 }
 
 }  // namespace eqsb
+
+namespace eqsb {
+
+// Packed SELL ("SELL-P") for the bf16 V-cycle operators: one
+// 32-bit word per entry, bf16 value in the high half and the 16-bit column
+// code in the low half. Four consecutive entries of a row form a 16-byte
+// group, so each lane reads a whole group with one vector load and a warp
+// load instruction moves 512 contiguous bytes (SELL-16 moves 64). Group g of
+// row q of a chunk sits at step g / tpr in lane q * tpr + g % tpr; a chunk is
+// `steps` x 32 groups. The column code is (window << shift) | (column - base)
+// with shift 13, 12 or 11 (8, 16 or 32 windows per chunk, the first that fits).
+constexpr int kPackGroup = 4;
+
+struct HostSellP {
+  int tpr = 0, n_rows = 0, n_chunks = 0, shift = 13, windows = 8;
+  std::vector<int> chunk_ptr;    // [n_chunks + 1] offsets in 16-byte groups (multiples of 32)
+  std::vector<int> bases;        // [n_chunks][windows]
+  std::vector<uint32_t> words;   // 4 * chunk_ptr.back() packed entries (padding: 0)
+  long padded() const { return chunk_ptr.empty() ? 0 : 4L * chunk_ptr.back(); }
+};
+
+uint16_t to_bf16(double d);  // round to nearest even
+// false when some chunk's columns need more than 32 windows
+bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out);
+
+}  // namespace eqsb

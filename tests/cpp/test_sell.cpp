@@ -1,0 +1,138 @@
+// CPU check of the SELL-16 and packed SELL-P encoders (sell.hpp): every CSR
+// entry is recovered bit-exactly (column) / as its bf16 rounding (value) by
+// the same index arithmetic the kernels use (k_rows.cu sell_dot / sellp_dot),
+// and padding decodes to value 0 at a valid column. Built and run by
+// tests/test_sell_format.py.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "sell.hpp"
+
+using namespace eqsb;
+
+static float bf16_to_float(uint32_t hi) {
+  float f;
+  uint32_t u = hi & 0xffff0000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+static int check_packed(const HostCsr& a, const HostSellP& p) {
+  const int rpc = 32 / p.tpr;
+  const unsigned mask = (1u << p.shift) - 1u;
+  std::vector<char> seen(a.nnz(), 0);
+  for (int c = 0; c < p.n_chunks; ++c) {
+    const int S = (p.chunk_ptr[c + 1] - p.chunk_ptr[c]) / 32;
+    for (int lane = 0; lane < 32; ++lane) {
+      const int q = lane / p.tpr, sub = lane % p.tpr, r = c * rpc + q;
+      for (int st = 0; st < S; ++st)
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t w = p.words[4L * (p.chunk_ptr[c] + 32L * st + lane) + e];
+          const unsigned code = w & 0xffffu;
+          const int col = p.bases[(size_t)c * p.windows + (code >> p.shift)] + (int)(code & mask);
+          const int j = 4 * (st * p.tpr + sub) + e;  // entry index within the row
+          if (r < a.n_rows && j < a.row_ptr[r + 1] - a.row_ptr[r]) {
+            const long k = a.row_ptr[r] + j;
+            if (col != a.col_idx[k]) return printf("col mismatch c%d lane%d st%d e%d\n", c, lane, st, e), 1;
+            if (bf16_to_float(w) != bf16_to_float((uint32_t)to_bf16(a.values[k]) << 16)) return printf("val\n"), 1;
+            seen[k] = 1;
+          } else {
+            if ((w >> 16) != 0) return printf("padding value nonzero\n"), 1;
+            if (col < 0 || col >= a.n_cols) return printf("padding column out of range\n"), 1;
+          }
+        }
+    }
+  }
+  for (char s : seen)
+    if (!s) return printf("entry not encoded\n"), 1;
+  return 0;
+}
+
+static int check_sell16(const HostCsr& a, const HostSell& h) {
+  const int rpc = 32 / h.tpr;
+  for (int c = 0; c < h.n_chunks; ++c) {
+    const long beg = h.chunk_ptr[c];
+    const int S = (int)((h.chunk_ptr[c + 1] - beg) >> 5);
+    for (int lane = 0; lane < 32; ++lane)
+      for (int s = 0; s < S; ++s) {
+        const long pos = beg + 32L * s + lane;
+        const unsigned code = h.code[pos];
+        const int col = h.bases[(size_t)c * kSellWindows + (code >> kSellShift)] + (int)(code & (kSellSpan - 1));
+        if (h.src[pos] >= 0 && col != a.col_idx[h.src[pos]]) return printf("sell16 col mismatch\n"), 1;
+        const int r = c * rpc + lane / h.tpr;
+        if (h.src[pos] >= 0 && (h.src[pos] < a.row_ptr[r] || h.src[pos] >= a.row_ptr[r + 1]))
+          return printf("sell16 row mismatch\n"), 1;
+      }
+  }
+  return 0;
+}
+
+int main() {
+  std::mt19937 g(20261017u);
+  int fails = 0;
+  // row lengths: fine-level like (15), ragged, empty rows, long coarse rows;
+  // column spread: local (one window) to wide (needs 16 or 32 windows)
+  const int lens[] = {15, 40, 0, 200, 7};
+  const int spreads[] = {3000, 30000, 60000, 120000};
+  for (int li = 0; li < 5; ++li)
+    for (int si = 0; si < 4; ++si) {
+      HostCsr a;
+      a.n_rows = 3000 + 97 * li + 13 * si;
+      a.n_cols = 400000;
+      a.row_ptr.push_back(0);
+      for (int i = 0; i < a.n_rows; ++i) {
+        const int len = lens[li] == 0 ? (i % 5 == 0 ? 0 : (int)(g() % 20)) : lens[li] - (int)(g() % 3);
+        std::vector<int> cols;
+        for (int k = 0; k < len; ++k) cols.push_back((i * 97 + (int)(g() % spreads[si])) % a.n_cols);
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        for (int col : cols) {
+          a.col_idx.push_back(col);
+          a.values.push_back(std::uniform_real_distribution<double>(-1.0, 1.0)(g));
+        }
+        a.row_ptr.push_back((int)a.col_idx.size());
+      }
+      const int tpr = choose_sell_tpr(a);
+      HostSellP p;
+      const bool okp = build_sell_packed(a, tpr, p);
+      HostSell h;
+      const bool ok16 = build_sell(a, tpr, h);
+      const int fp = okp ? check_packed(a, p) : 0;
+      const int f16 = ok16 ? check_sell16(a, h) : 0;
+      printf("len %3d spread %6d tpr %2d packed %d (shift %d, padded %ld / nnz %ld) sell16 %d -> %s\n", lens[li],
+             spreads[si], tpr, okp, p.shift, p.padded(), a.nnz(), ok16, fp || f16 ? "FAIL" : "ok");
+      fails += fp + f16;
+      if (!okp && spreads[si] <= 30000) ++fails, printf("packed encoding unexpectedly failed\n");
+    }
+  // clustered columns (restriction-like rows: a few node planes each): 12
+  // clusters 20000 apart need 16 windows of 4096 (shift 12), 24 need 32 (shift 11)
+  for (int nclus : {12, 24}) {
+    HostCsr a;
+    a.n_rows = 2000;
+    a.n_cols = 600000;
+    a.row_ptr.push_back(0);
+    for (int i = 0; i < a.n_rows; ++i) {
+      std::vector<int> cols;
+      for (int cl = 0; cl < nclus; ++cl)
+        for (int k = 0; k < 4; ++k) cols.push_back(cl * 20000 + (i / 8) * 4 + (int)(g() % 1000));
+      std::sort(cols.begin(), cols.end());
+      cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+      for (int col : cols) {
+        a.col_idx.push_back(col);
+        a.values.push_back(1.0 + col % 7);
+      }
+      a.row_ptr.push_back((int)a.col_idx.size());
+    }
+    HostSellP p;
+    const int tpr = choose_sell_tpr(a);
+    const bool okp = build_sell_packed(a, tpr, p);
+    const int want_shift = nclus == 12 ? 12 : 11;
+    const int fp = okp ? check_packed(a, p) : 1;
+    printf("clusters %d tpr %d packed %d shift %d -> %s\n", nclus, tpr, okp, p.shift,
+           fp || p.shift != want_shift ? "FAIL" : "ok");
+    fails += fp + (p.shift != want_shift);
+  }
+  return fails ? 1 : 0;
+}

@@ -1,0 +1,18 @@
+"""CPU test of the resident sparse formats (SELL-16, packed SELL-P): the host
+encoders in paper_1612_09447_b200/csrc/host_sell.cpp round-trip every CSR entry
+through the kernels' index arithmetic (tests/cpp/test_sell.cpp)."""
+import os
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_sell_encoders_round_trip(tmp_path):
+    exe = tmp_path / "test_sell"
+    csrc = os.path.join(ROOT, "paper_1612_09447_b200", "csrc")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-fopenmp", "-I" + csrc, "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_sell.cpp"), os.path.join(csrc, "host_sell.cpp"),
+                    "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
