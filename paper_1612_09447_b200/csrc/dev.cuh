@@ -122,18 +122,29 @@ template <class XT>
 void launch_residual(const DevCsr& a, const XT* b, const XT* x, XT* y, Reducer* red, int slot, cudaStream_t s);
 // q = A p ; slot <- p.q
 void launch_spmv_dot(const DevCsr& a, const double* p, double* q, Reducer red, int slot, cudaStream_t s);
-// Chebyshev(2) smoother pieces
+// y = b - A x and y2 = D^-1 y ; y = A x and y2 = W y (restriction with the
+// next level's D^-1): the scaled copies are the `pre` inputs below
 template <class XT>
-void launch_cheb_pre(const DevCsr& a, const XT* invd, const XT* b, XT* z, ChebCoef c, cudaStream_t s);
+void launch_residual_scaled(const DevCsr& a, const XT* b, const XT* x, const XT* invd, XT* y, XT* y2, cudaStream_t s);
+template <class XT>
+void launch_spmv_scaled(const DevCsr& a, const XT* x, const XT* w, XT* y, XT* y2, cudaStream_t s);
+// Chebyshev(2) smoother pieces. `pre` (optional) = D^-1 of the
+// vector the op scales (b for the pre-smoother, r0 for the post step): the
+// packed kernels then gather it instead of the vector and D^-1.
+template <class XT>
+void launch_cheb_pre(const DevCsr& a, const XT* invd, const XT* b, XT* z, ChebCoef c, cudaStream_t s,
+                     const XT* pre = nullptr);
 template <class XT>
 void launch_cheb_post2(const DevCsr& a, const XT* invd, const XT* r0, XT* z, ChebCoef c, const XT* b_dot,
-                       Reducer* red, int slot, cudaStream_t s);
+                       Reducer* red, int slot, cudaStream_t s, const XT* pre = nullptr);
 // fp32 V-cycle, fine level: z_out (fp64) = z + Chebyshev(2) post step ; slot <- b64.z_out
 void launch_cheb_post2_out64(const DevCsr& a, const float* invd, const float* r0, const float* z, ChebCoef c,
-                             double* z_out, const double* b_dot, Reducer* red, int slot, cudaStream_t s);
+                             double* z_out, const double* b_dot, Reducer* red, int slot, cudaStream_t s,
+                             const float* pre = nullptr);
 // Chebyshev(1): z = D^-1 b / theta and t = b - A z in one pass
 template <class XT>
-void launch_cheb1_pre_resid(const DevCsr& a, const XT* invd, const XT* b, XT* z, XT* t, ChebCoef c, cudaStream_t s);
+void launch_cheb1_pre_resid(const DevCsr& a, const XT* invd, const XT* b, XT* z, XT* t, ChebCoef c, cudaStream_t s,
+                            const XT* pre = nullptr);
 // Chebyshev(1) post: z_out = z + D^-1 (b - A z) / theta (z_out != z)
 template <class XT>
 void launch_cheb1_post(const DevCsr& a, const XT* invd, const XT* b, const XT* z, XT* z_out, ChebCoef c,
@@ -146,8 +157,9 @@ void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, do
 
 // ---- PCG / dense (k_sparse.cu)
 // x += alpha p ; r -= alpha q ; slot_rr <- r.r ; alpha = scal[S_RZ]/scal[S_PQ]; r32 (optional) = (float) r
+// and d32 = invd32 .* r32 (the next fp32 V-cycle's inputs)
 void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s,
-                       float* r32 = nullptr);
+                       float* r32 = nullptr, const float* invd32 = nullptr, float* d32 = nullptr);
 // p = z + beta p, beta = scal[S_RZ]/scal[S_RZ_OLD]
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s);
 // z = Ainv b (dense, n <= 1024, fp64 inverse)
@@ -157,6 +169,8 @@ void launch_dense_solve(int n, const double* ainv, const XT* b, XT* z, cudaStrea
 void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s);
 // precision conversions at the fp32 V-cycle boundary
 void launch_to_f32(long n, const double* x, float* y, cudaStream_t s);
+// y = (float) x and d = invd .* y (the fine level's b and D^-1 b of an fp32 V-cycle)
+void launch_to_f32_scaled(long n, const double* x, const float* invd, float* y, float* d, cudaStream_t s);
 void launch_to_f64_dot(int n, const float* z32, double* z64, const double* b, Reducer* red, int slot, cudaStream_t s);
 
 // ---- vector kernels (k_sparse.cu)

@@ -142,7 +142,7 @@ void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   if (build_sell(h, choose_sell_tpr(h), hs)) upload_sell16(h, hs, d, b, s);
   // packed bf16 copy for the V-cycle kernels (sell.hpp "SELL-P")
   HostSellP hp;
-  if (!build_sell_packed(h, choose_sell_tpr(h), hp)) return;
+  if (!build_sell_packed(h, choose_sellp_tpr(h), hp)) return;
   std::vector<int> pcp = hp.chunk_ptr;
   b.pk_cp.alloc(pcp.size());
   b.pk_cp.upload(pcp.data(), pcp.size(), s);
@@ -484,6 +484,10 @@ void GpuSystem::build_levels() {
     lv.b32.alloc(nloc);
     lv.t32.alloc(nloc);
     lv.z2_32.alloc(nloc);
+    lv.db.alloc(nloc);
+    lv.dt.alloc(nloc);
+    lv.db32.alloc(nloc);
+    lv.dt32.alloc(nloc);
     if (l + 1 < L) {
       f32(plan_.A[l].values, lv.a_vf);
       upload_csr(plan_.P[l], lv.P, lv.p_rp, lv.p_ci, lv.p_v, s);
@@ -810,6 +814,8 @@ struct VBufs<double> {
   static double* z2(DevLevel& l) { return l.z2.p; }
   static double* t(DevLevel& l) { return l.t.p; }
   static double* invd(DevLevel& l) { return l.invd.p; }
+  static double* db(DevLevel& l) { return l.db.p; }
+  static double* dt(DevLevel& l) { return l.dt.p; }
 };
 template <>
 struct VBufs<float> {
@@ -818,6 +824,8 @@ struct VBufs<float> {
   static float* z2(DevLevel& l) { return l.z2_32.p; }
   static float* t(DevLevel& l) { return l.t32.p; }
   static float* invd(DevLevel& l) { return l.invd32.p; }
+  static float* db(DevLevel& l) { return l.db32.p; }
+  static float* dt(DevLevel& l) { return l.dt32.p; }
 };
 
 // Symmetric V-cycle (amg.cpp:145-172 structure) with Chebyshev smoothing:
@@ -828,7 +836,7 @@ struct VBufs<float> {
 // vectors the fine level reads the fp32 copy of r (b) and its last kernel
 // writes z in fp64 (out64, with r64 . z when dot_into_rz).
 template <class XT>
-XT* GpuSystem::vcycle_t(int l, const XT* b_in, bool dot_into_rz, const double* r64, double* out64) {
+XT* GpuSystem::vcycle_t(int l, const XT* b_in, bool dot_into_rz, const double* r64, double* out64, const XT* pre) {
   using V = VBufs<XT>;
   const int L = (int)levels_.size();
   DevLevel& lv = levels_[l];
@@ -862,42 +870,56 @@ XT* GpuSystem::vcycle_t(int l, const XT* b_in, bool dot_into_rz, const double* r
   XT* z = V::z(lv);
   XT* t = V::t(lv);
   XT* invd = V::invd(lv);
-  halo(lv.halo, b);
+  // pre: D^-1 b, written by the producer of b (PCG update or the restriction),
+  // gathered by the smoother instead of b and D^-1 (k_rows.cu OP 8/9)
   if (deg >= 2) {
-    launch_cheb_pre<XT>(lv.A, invd, b, z, lv.cheb, stream_);
+    halo(lv.halo, pre ? const_cast<XT*>(pre) : b);
+    launch_cheb_pre<XT>(lv.A, invd, b, z, lv.cheb, stream_, pre);
     halo(lv.halo, z);
     launch_residual<XT>(lv.A, b, z, t, nullptr, 0, stream_);
-  } else if (lv.A.lanes() <= 4) {
-    launch_cheb1_pre_resid<XT>(lv.A, invd, b, z, t, lv.cheb1, stream_);
+  } else if (pre || lv.A.lanes() <= 4) {
+    halo(lv.halo, pre ? const_cast<XT*>(pre) : b);
+    launch_cheb1_pre_resid<XT>(lv.A, invd, b, z, t, lv.cheb1, stream_, pre);
   } else {
     // dense rows: one gathered vector per entry instead of two (b and D^-1)
+    halo(lv.halo, b);
     launch_diag_scale<XT>(lv.n_loc, invd, b, lv.cheb1.inv_theta, z, stream_);
     launch_residual<XT>(lv.A, b, z, t, nullptr, 0, stream_);
   }
   halo(lv.halo, t);
   XT* bc = V::b(nx);
-  launch_spmv<XT>(lv.R, t, bc, stream_);
   // entering the replicated levels: every rank holds the partial restriction
   // of its owned rows for all coarse rows; the sum is the coarse right-hand side
-  if (nx.replicated && !lv.replicated && comm_->size() > 1) comm_->allreduce(bc, nx.n_loc, stream_);
-  XT* zc = vcycle_t<XT>(l + 1, bc, false, nullptr, nullptr);
+  const bool to_rep = nx.replicated && !lv.replicated && comm_->size() > 1;
+  XT* prec = (!to_rep && level_takes_pre(l + 1)) ? V::db(nx) : nullptr;
+  if (prec)
+    launch_spmv_scaled<XT>(lv.R, t, V::invd(nx), bc, prec, stream_);
+  else
+    launch_spmv<XT>(lv.R, t, bc, stream_);
+  if (to_rep) comm_->allreduce(bc, nx.n_loc, stream_);
+  XT* zc = vcycle_t<XT>(l + 1, bc, false, nullptr, nullptr, prec);
   halo(nx.halo, zc);  // no-op on replicated levels
   launch_prolong_add<XT>(lv.P, zc, z, stream_);
   halo(lv.halo, z);
   const bool to64 = out64 != nullptr;  // fine level of an fp32 V-cycle
   Reducer r = red_;
   if (deg >= 2) {
-    launch_residual<XT>(lv.A, b, z, t, nullptr, 0, stream_);
-    halo(lv.halo, t);
+    XT* dtp = lv.A.packed() ? V::dt(lv) : nullptr;  // D^-1 t for the post step's gather
+    if (dtp)
+      launch_residual_scaled<XT>(lv.A, b, z, invd, t, dtp, stream_);
+    else
+      launch_residual<XT>(lv.A, b, z, t, nullptr, 0, stream_);
+    halo(lv.halo, dtp ? dtp : t);
     if constexpr (std::is_same_v<XT, float>) {
       if (to64) {
-        launch_cheb_post2_out64(lv.A, invd, t, z, lv.cheb, out64, r64, dot_into_rz ? &r : nullptr, S_RZ, stream_);
+        launch_cheb_post2_out64(lv.A, invd, t, z, lv.cheb, out64, r64, dot_into_rz ? &r : nullptr, S_RZ, stream_,
+                                dtp);
         if (dot_into_rz) allreduce(S_RZ);
         return nullptr;
       }
     }
     launch_cheb_post2<XT>(lv.A, invd, t, z, lv.cheb, dot_into_rz ? b : nullptr, dot_into_rz ? &r : nullptr, S_RZ,
-                          stream_);
+                          stream_, dtp);
     if (dot_into_rz) allreduce(S_RZ);
     return z;
   }
@@ -919,25 +941,41 @@ XT* GpuSystem::vcycle_t(int l, const XT* b_in, bool dot_into_rz, const double* r
   return z2;
 }
 
-// V-cycle on the fine residual r (fp64): returns z (fp64) and r.z in S_RZ
+// level l's pre-smoother gathers D^-1 b (packed operator with a scaled-gather op)
+bool GpuSystem::level_takes_pre(int l) const {
+  if (l <= 0 || l + 1 >= (int)levels_.size()) return false;
+  const DevLevel& lv = levels_[l];
+  return lv.A.packed();
+}
+
+// fp32 V-cycle inputs of the fine level: b32 = (float) r, db32 = D^-1 b32
+void GpuSystem::vcycle_prepare(const double* r) {
+  if (vcycle_f32_ && levels_.size() >= 2) {
+    DevLevel& f = levels_[0];
+    launch_to_f32_scaled(n_own_, r, f.invd32.p, f.b32.p, f.db32.p, stream_);
+  }
+}
+
+// V-cycle on the fine residual r (fp64): returns z (fp64) and r.z in S_RZ.
+// The fp32 V-cycle reads b32/db32, prepared by vcycle_prepare or the PCG update.
 double* GpuSystem::vcycle(const double* r) {
   if (vcycle_f32_ && levels_.size() >= 2) {
     DevLevel& f = levels_[0];
-    launch_to_f32(n_own_, r, f.b32.p, stream_);
-    vcycle_t<float>(0, f.b32.p, true, r, f.z.p);
+    vcycle_t<float>(0, f.b32.p, true, r, f.z.p, f.A.packed() ? f.db32.p : nullptr);
     return f.z.p;
   }
-  return vcycle_t<double>(0, r, true, nullptr, nullptr);
+  return vcycle_t<double>(0, r, true, nullptr, nullptr, nullptr);
 }
 
 // The V-cycle is a fixed sequence of kernels (and, on several ranks, NCCL
 // halo/allreduce calls) on fixed buffers, so it is captured once into a CUDA
 // graph and replayed: one launch per preconditioner application.
-double* GpuSystem::precondition(double* r) {
+double* GpuSystem::precondition(double* r, bool prepared) {
   tic(TC_VCYCLE);
   const double bytes0 = g_algo_bytes;
   double* z;
   if (prob_.solver.precond == 2) {
+    if (!prepared) vcycle_prepare(r);
     if (use_graphs && comm_->capturable() && r == w_r_.p) {
       if (!vcycle_graph_) {
         cudaGraph_t graph;
@@ -1031,7 +1069,12 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
     halo(halo0_, p);
     launch_spmv_dot(mii_, p, q, red_, S_PQ, stream_);
     allreduce(S_PQ);
-    launch_pcg_update(n, x, r, p, q, red_, stream_);
+    const bool f32 = prob_.solver.precond == 2 && vcycle_f32_ && levels_.size() >= 2;
+    DevLevel& f0 = levels_.empty() ? dummy_level_ : levels_[0];
+    if (f32)  // the next V-cycle's fp32 inputs come out of the update
+      launch_pcg_update(n, x, r, p, q, red_, stream_, f0.b32.p, f0.invd32.p, f0.db32.p);
+    else
+      launch_pcg_update(n, x, r, p, q, red_, stream_);
     allreduce(S_RR);
     toc(TC_PCG, spmv_bytes(mii_) + 8.0 * n + 48.0 * n);
     read_scalars(S_PQ, 3, sc);  // pq, rr, rz
@@ -1049,7 +1092,7 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
     }
     CK(cudaMemcpyAsync(red_scal_.p + S_RZ_OLD, red_scal_.p + S_RZ, sizeof(double), cudaMemcpyDeviceToDevice,
                        stream_));
-    z = precondition(r);
+    z = precondition(r, f32);
     tic(TC_PCG);
     launch_pcg_direction(n, p, z, red_scal_.p, stream_);
     toc(TC_PCG, 24.0 * n);

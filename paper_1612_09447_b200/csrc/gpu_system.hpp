@@ -93,8 +93,8 @@ struct DevLevel {
   DevBuf<double> a_v, p_v, r_v;
   DevBuf<float> a_vf, p_vf, r_vf;  // fp32 copies for the V-cycle
   SellBufs a_s, p_s, r_s;          // SELL copies (level 0: A shares the PCG operator's)
-  DevBuf<double> invd, b, z, z2, t;
-  DevBuf<float> invd32, b32, z32, z2_32, t32;  // fp32 V-cycle vectors
+  DevBuf<double> invd, b, z, z2, t, db, dt;
+  DevBuf<float> invd32, b32, z32, z2_32, t32, db32, dt32;  // fp32 V-cycle vectors
   ChebCoef cheb{}, cheb1{};          // degree-2 and degree-1 Chebyshev coefficients
   double lambda_smoother = 0;
   DevHalo halo;
@@ -205,9 +205,13 @@ class GpuSystem {
   void halo(DevHalo& h, T* vec);  // fill ghosts of vec from the owners
   void allreduce(int slot, int count = 1);
   template <class XT>
-  XT* vcycle_t(int l, const XT* b, bool dot_into_rz, const double* r64, double* out64);
+  XT* vcycle_t(int l, const XT* b, bool dot_into_rz, const double* r64, double* out64, const XT* pre);
+  bool level_takes_pre(int l) const;
+  void vcycle_prepare(const double* r);  // fp32 V-cycle: b32, db32 of the fine level from r
   double* vcycle(const double* r);  // fine-level V-cycle: z (fp64), r.z in S_RZ
-  double* precondition(double* r);  // z = M^-1 r (returned buffer), S_RZ <- r.z
+  // z = M^-1 r (returned buffer), S_RZ <- r.z; prepared: the PCG update already
+  // wrote the fp32 V-cycle inputs
+  double* precondition(double* r, bool prepared = false);
   void kx_tets(const double* x, const double* v);
   double read_scalar(int slot);
   void read_scalars(int first, int count, double* out);
@@ -278,6 +282,7 @@ class GpuSystem {
   DevBuf<int> mii_rp_, mii_ci_;
   DevBuf<double> mii_v_, mii_invd_;
   SellBufs mii_s_;
+  DevLevel dummy_level_;
   DevHalo halo0_;  // level-0 (fine dof) halo
   std::vector<DevLevel> levels_;
   DevBuf<double> coarse_inv_;

@@ -4,18 +4,24 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
 #include "sell.hpp"
 
 namespace eqsb {
 
-int choose_sell_tpr(const HostCsr& a) {
+int choose_sell_tpr(const HostCsr& a, int per_lane) {
   if (a.n_rows == 0) return 1;
   const double avg = (double)a.nnz() / a.n_rows;
   int t = 1;
-  while (t < 32 && t * 16 < avg) t <<= 1;
+  while (t < 32 && t * per_lane < avg) t <<= 1;
   return t;
+}
+
+int choose_sellp_tpr(const HostCsr& a) {
+  static const int per_lane = getenv("EQS_SELLP_LANE_ENTRIES") ? atoi(getenv("EQS_SELLP_LANE_ENTRIES")) : 32;
+  return choose_sell_tpr(a, per_lane);
 }
 
 bool build_sell(const HostCsr& a, int tpr, HostSell& out) {
@@ -147,10 +153,13 @@ bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out) {
         const int q = r - r0;
         for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
           const int j = k - a.row_ptr[r], col = a.col_idx[k];
-          const int g = j / kPackGroup, e = j % kPackGroup;
+          // entry j of the (column-sorted) row goes to lane j % tpr, slot
+          // (j / tpr) % 4 of step j / (4 tpr): one gather instruction of the
+          // row's lanes reads tpr consecutive columns
+          const int sub = j % tpr, rest = j / tpr, e = rest % kPackGroup, st = rest / kPackGroup;
           int w = windows - 1;  // windows ascend: the owner is the last base <= col
           while (w > 0 && wb[w] > col) --w;
-          const long pos = 4L * (s.chunk_ptr[c] + 32L * (g / tpr) + q * tpr + g % tpr) + e;
+          const long pos = 4L * (s.chunk_ptr[c] + 32L * st + q * tpr + sub) + e;
           const uint32_t code = ((uint32_t)w << shift) | (uint32_t)(col - wb[w]);
           s.words[pos] = ((uint32_t)to_bf16(a.values[k]) << 16) | code;
         }

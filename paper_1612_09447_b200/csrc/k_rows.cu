@@ -169,6 +169,11 @@ __device__ __forceinline__ XT sellp_dot(const DevSellP& m, int chunk, int lane, 
 // OP 4: z = D^-1 b / theta ; t = b - A z                         (Chebyshev(1) pre-smoothing + residual)
 // OP 5: zo = z + D^-1 (b - A z) / theta                          (Chebyshev(1) post-smoothing, out of place)
 // OP 6: w = D^-1 A x                                             (power iteration on D^-1 A)
+// OP 8: y = b - A x ; y2 = D^-1 y                                (residual + its scaled copy)
+// OP 9: y = A x ; y2 = W y  (W: the next level's D^-1)          (restriction + its scaled copy)
+// The scaled copies feed the PRE kernels: ops that gather D^-1 v (OP 3, 4,
+// MODE 2, 3) then gather the one prescaled vector instead of v and D^-1,
+// with bit-identical products.
 // Reduction modes (MODE >= 0; the dot is accumulated in fp64):
 // MODE 0: q = A p,  p.q
 // MODE 1: y = b - A x, y.y
@@ -182,8 +187,8 @@ struct Epi {
                                        const XT* __restrict__ invd, const XT* y, const double* __restrict__ b64,
                                        int do_red) {
     if constexpr (MODE < 0) {
-      if (OP == 1 || OP == 3 || OP == 4 || OP == 5) p0 = b[row];
-      if (OP == 3 || OP == 4 || OP == 5 || OP == 6) p1 = invd[row];
+      if (OP == 1 || OP == 3 || OP == 4 || OP == 5 || OP == 8) p0 = b[row];
+      if (OP == 3 || OP == 4 || OP == 5 || OP == 6 || OP == 8 || OP == 9) p1 = invd[row];
       if (OP == 5) p2 = x[row];
       if (OP == 2) p2 = y[row];
     } else {
@@ -210,6 +215,15 @@ struct Epi {
       }
       if (OP == 5) y2[row] = p2 + p1 * (p0 - s) * it;
       if (OP == 6) y[row] = s * p1;
+      if (OP == 8) {
+        const XT r = p0 - s;
+        y[row] = r;
+        y2[row] = p1 * r;
+      }
+      if (OP == 9) {
+        y[row] = s;
+        y2[row] = p1 * s;
+      }
       return 0.0;
     } else if (MODE == 0) {
       y[row] = s;
@@ -264,10 +278,11 @@ __global__ void __launch_bounds__(kBlock, SELL_MINB) k_sell(int n, DevSell m, co
   if (act) e.store(row, s, y, y2, nullptr, c, 0);
 }
 
-template <int TPR, class XT, int OP>
+template <int TPR, class XT, int OP, bool PRE>
 __global__ void __launch_bounds__(kBlock) k_sellp(int n, DevSellP m, const XT* __restrict__ x,
                                                   const XT* __restrict__ b, const XT* __restrict__ invd,
-                                                  XT* __restrict__ y, XT* __restrict__ y2, ChebCoef c) {
+                                                  XT* __restrict__ y, XT* __restrict__ y2, ChebCoef c,
+                                                  const XT* __restrict__ pre) {
   const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (chunk >= m.n_chunks) return;  // warp-uniform exit
   constexpr bool SC = kScaled<OP, -1>;
@@ -275,16 +290,16 @@ __global__ void __launch_bounds__(kBlock) k_sellp(int n, DevSellP m, const XT* _
   const bool act = lane % TPR == 0 && row < n;
   Epi<OP, -1, XT> e;
   if (act) e.load(row, x, b, invd, y, nullptr, 0);
-  const XT s = sellp_dot<TPR, XT, SC>(m, chunk, lane, SC ? b : x, invd);
+  const XT s = sellp_dot<TPR, XT, SC && !PRE>(m, chunk, lane, SC ? (PRE ? pre : b) : x, invd);
   if (act) e.store(row, s, y, y2, nullptr, c, 0);
 }
 
-template <int TPR, class XT, int MODE>
+template <int TPR, class XT, int MODE, bool PRE>
 __global__ void __launch_bounds__(kBlock) k_sellp_red(int n, DevSellP m, const XT* __restrict__ x,
                                                       const XT* __restrict__ b, const XT* __restrict__ invd,
                                                       XT* __restrict__ y, double* __restrict__ out64,
                                                       const double* __restrict__ b64, ChebCoef c, Reducer red,
-                                                      int slot, int do_red) {
+                                                      int slot, int do_red, const XT* __restrict__ pre) {
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kBlock / 32);
   double acc = 0.0;
@@ -293,7 +308,7 @@ __global__ void __launch_bounds__(kBlock) k_sellp_red(int n, DevSellP m, const X
     const bool act = lane % TPR == 0 && row < n;
     Epi<0, MODE, XT> e;
     if (act) e.load(row, x, b, invd, y, b64, do_red);
-    const XT s = sellp_dot<TPR, XT, kScaled<0, MODE>>(m, chunk, lane, x, invd);
+    const XT s = sellp_dot<TPR, XT, kScaled<0, MODE> && !PRE>(m, chunk, lane, PRE ? pre : x, invd);
     if (act) acc += e.store(row, s, y, nullptr, out64, c, do_red);
   }
   if (do_red) reduce_finish(acc, red, slot);
@@ -365,19 +380,27 @@ int eff_prec(const DevCsr& a) {
 }
 
 template <class XT, int OP>
-void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y, XT* y2, ChebCoef c, cudaStream_t s) {
+void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y, XT* y2, ChebCoef c, cudaStream_t s,
+                const XT* pre = nullptr) {
   if (a.n_rows == 0) return;
   ++g_launch_count;
   // gathered / streamed row vectors per op (Epi)
-  constexpr int kG[7] = {1, 1, 1, 2, 2, 1, 1}, kS[7] = {1, 2, 2, 1, 2, 3, 2};
+  constexpr int kG[10] = {1, 1, 1, 2, 2, 1, 1, 0, 1, 1}, kS[10] = {1, 2, 2, 1, 2, 3, 2, 0, 4, 3};
   const int p = eff_prec<XT>(a);
   DevCsr view = a;
   view.prec = p;
   if (view.packed()) {
-    g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
     const DevSellP& m = a.pk;
     const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
-#define P_(T, VT, V) k_sellp<T, XT, OP><<<g, kBlock, 0, s>>>(a.n_rows, m, x, b, invd, y, y2, c)
+    if (pre && kScaled<OP, -1>) {  // one prescaled gather; b and D^-1 read per row
+      g_algo_bytes += matrix_pass_bytes(view, 1, kS[OP] + 2, sizeof(XT));
+#define P_(T, VT, V) k_sellp<T, XT, OP, true><<<g, kBlock, 0, s>>>(a.n_rows, m, x, b, invd, y, y2, c, pre)
+      TPR_SWITCH_(m.tpr, P_, void, 0)
+#undef P_
+      return;
+    }
+    g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
+#define P_(T, VT, V) k_sellp<T, XT, OP, false><<<g, kBlock, 0, s>>>(a.n_rows, m, x, b, invd, y, y2, c, nullptr)
     TPR_SWITCH_(m.tpr, P_, void, 0)
 #undef P_
     return;
@@ -410,7 +433,7 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
 
 template <class XT, int MODE>
 void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y, double* out64,
-                    const double* b64, ChebCoef c, Reducer* red, int slot, cudaStream_t s) {
+                    const double* b64, ChebCoef c, Reducer* red, int slot, cudaStream_t s, const XT* pre = nullptr) {
   if (a.n_rows == 0) return;
   ++g_launch_count;
   Reducer r = red ? *red : Reducer{};
@@ -419,16 +442,26 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
   const int p = eff_prec<XT>(a);
   DevCsr view = a;
   view.prec = p;
-  double bytes = matrix_pass_bytes(view, kG[MODE], kS[MODE], sizeof(XT));
+  const bool use_pre = pre && kScaled<0, MODE> && view.packed();
+  double bytes = use_pre ? matrix_pass_bytes(view, 1, kS[MODE] + 2, sizeof(XT))
+                         : matrix_pass_bytes(view, kG[MODE], kS[MODE], sizeof(XT));
   if (MODE == 2 && red) bytes += sizeof(XT) * (double)a.n_rows;
   if (MODE == 3) bytes += (red ? 16.0 : 8.0) * a.n_rows;
   g_algo_bytes += bytes;
   if (view.packed()) {
     const DevSellP& m = a.pk;
     const long work = (long)m.n_chunks * 32;
-#define P_(T, VT, V)                                                                                              \
-  k_sellp_red<T, XT, MODE><<<red_grid(k_sellp_red<T, XT, MODE>, work), kBlock, 0, s>>>(a.n_rows, m, x, b, invd, y, \
-                                                                                      out64, b64, c, r, slot, dr)
+    if (use_pre) {
+#define P_(T, VT, V)                                                                                   \
+  k_sellp_red<T, XT, MODE, true><<<red_grid(k_sellp_red<T, XT, MODE, true>, work), kBlock, 0, s>>>(     \
+      a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, pre)
+      TPR_SWITCH_(m.tpr, P_, void, 0)
+#undef P_
+      return;
+    }
+#define P_(T, VT, V)                                                                                   \
+  k_sellp_red<T, XT, MODE, false><<<red_grid(k_sellp_red<T, XT, MODE, false>, work), kBlock, 0, s>>>(   \
+      a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, nullptr)
     TPR_SWITCH_(m.tpr, P_, void, 0)
 #undef P_
     return;
@@ -480,21 +513,31 @@ void launch_prolong_add(const DevCsr& p, const XT* zc, XT* z, cudaStream_t s) {
   row_launch<XT, 2>(p, zc, nullptr, nullptr, z, nullptr, ChebCoef{}, s);
 }
 template <class XT>
-void launch_cheb_pre(const DevCsr& a, const XT* invd, const XT* b, XT* z, ChebCoef c, cudaStream_t s) {
-  row_launch<XT, 3>(a, nullptr, b, invd, z, nullptr, c, s);
+void launch_residual_scaled(const DevCsr& a, const XT* b, const XT* x, const XT* invd, XT* y, XT* y2, cudaStream_t s) {
+  row_launch<XT, 8>(a, x, b, invd, y, y2, ChebCoef{}, s);
+}
+template <class XT>
+void launch_spmv_scaled(const DevCsr& a, const XT* x, const XT* w, XT* y, XT* y2, cudaStream_t s) {
+  row_launch<XT, 9>(a, x, nullptr, w, y, y2, ChebCoef{}, s);
+}
+template <class XT>
+void launch_cheb_pre(const DevCsr& a, const XT* invd, const XT* b, XT* z, ChebCoef c, cudaStream_t s, const XT* pre) {
+  row_launch<XT, 3>(a, nullptr, b, invd, z, nullptr, c, s, pre);
 }
 template <class XT>
 void launch_cheb_post2(const DevCsr& a, const XT* invd, const XT* r0, XT* z, ChebCoef c, const XT* b_dot,
-                       Reducer* red, int slot, cudaStream_t s) {
-  row_red_launch<XT, 2>(a, r0, b_dot, invd, z, nullptr, nullptr, c, red, slot, s);
+                       Reducer* red, int slot, cudaStream_t s, const XT* pre) {
+  row_red_launch<XT, 2>(a, r0, b_dot, invd, z, nullptr, nullptr, c, red, slot, s, pre);
 }
 void launch_cheb_post2_out64(const DevCsr& a, const float* invd, const float* r0, const float* z, ChebCoef c,
-                             double* z_out, const double* b_dot, Reducer* red, int slot, cudaStream_t s) {
-  row_red_launch<float, 3>(a, r0, nullptr, invd, const_cast<float*>(z), z_out, b_dot, c, red, slot, s);
+                             double* z_out, const double* b_dot, Reducer* red, int slot, cudaStream_t s,
+                             const float* pre) {
+  row_red_launch<float, 3>(a, r0, nullptr, invd, const_cast<float*>(z), z_out, b_dot, c, red, slot, s, pre);
 }
 template <class XT>
-void launch_cheb1_pre_resid(const DevCsr& a, const XT* invd, const XT* b, XT* z, XT* t, ChebCoef c, cudaStream_t s) {
-  row_launch<XT, 4>(a, nullptr, b, invd, z, t, c, s);
+void launch_cheb1_pre_resid(const DevCsr& a, const XT* invd, const XT* b, XT* z, XT* t, ChebCoef c, cudaStream_t s,
+                            const XT* pre) {
+  row_launch<XT, 4>(a, nullptr, b, invd, z, t, c, s, pre);
 }
 template <class XT>
 void launch_cheb1_post(const DevCsr& a, const XT* invd, const XT* b, const XT* z, XT* z_out, ChebCoef c,
@@ -509,10 +552,13 @@ void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, do
   template void launch_spmv<XT>(const DevCsr&, const XT*, XT*, cudaStream_t);                                  \
   template void launch_residual<XT>(const DevCsr&, const XT*, const XT*, XT*, Reducer*, int, cudaStream_t);     \
   template void launch_prolong_add<XT>(const DevCsr&, const XT*, XT*, cudaStream_t);                           \
-  template void launch_cheb_pre<XT>(const DevCsr&, const XT*, const XT*, XT*, ChebCoef, cudaStream_t);          \
+  template void launch_residual_scaled<XT>(const DevCsr&, const XT*, const XT*, const XT*, XT*, XT*, cudaStream_t); \
+  template void launch_spmv_scaled<XT>(const DevCsr&, const XT*, const XT*, XT*, XT*, cudaStream_t);          \
+  template void launch_cheb_pre<XT>(const DevCsr&, const XT*, const XT*, XT*, ChebCoef, cudaStream_t, const XT*); \
   template void launch_cheb_post2<XT>(const DevCsr&, const XT*, const XT*, XT*, ChebCoef, const XT*, Reducer*,  \
-                                      int, cudaStream_t);                                                      \
-  template void launch_cheb1_pre_resid<XT>(const DevCsr&, const XT*, const XT*, XT*, XT*, ChebCoef, cudaStream_t); \
+                                      int, cudaStream_t, const XT*);                                           \
+  template void launch_cheb1_pre_resid<XT>(const DevCsr&, const XT*, const XT*, XT*, XT*, ChebCoef, cudaStream_t, \
+                                           const XT*);                                                         \
   template void launch_cheb1_post<XT>(const DevCsr&, const XT*, const XT*, const XT*, XT*, ChebCoef, cudaStream_t);
 INST_(double)
 INST_(float)

@@ -44,22 +44,65 @@ __global__ void k_jacobi(int n, const double* __restrict__ invd, const double* _
 }
 
 // x += alpha p ; r -= alpha q ; r.r ; r32 = (float) r for an fp32 V-cycle
-__global__ void k_pcg_update(int n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                             const double* __restrict__ q, float* __restrict__ r32, Reducer red) {
+// x += alpha p ; r -= alpha q ; r.r ; and for an fp32 V-cycle r32 = (float) r,
+// d32 = invd32 .* r32 (its fine-level b and D^-1 b). VEC: pairs of entries per
+// thread with 16-byte loads (all arrays 16-byte aligned); the odd tail entry
+// is handled by thread 0.
+template <bool F32, bool VEC>
+__global__ void __launch_bounds__(kBlock, 6)
+    k_pcg_update(int n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                 const double* __restrict__ q, float* __restrict__ r32, const float* __restrict__ invd32,
+                 float* __restrict__ d32, Reducer red) {
   const double alpha = red.scal[S_RZ] / red.scal[S_PQ];
   double acc = 0.0;
-  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+  auto one = [&](long i) {
     x[i] += alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
-    if (r32) r32[i] = (float)ri;
+    if constexpr (F32) {
+      const float rf = (float)ri;
+      r32[i] = rf;
+      d32[i] = invd32[i] * rf;
+    }
     acc += ri * ri;
+  };
+  if constexpr (VEC) {
+    const long n2 = n / 2;
+    for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (long)gridDim.x * kBlock) {
+      const double2 pi = reinterpret_cast<const double2*>(p)[i], qi = reinterpret_cast<const double2*>(q)[i];
+      double2 xi = reinterpret_cast<double2*>(x)[i], ri = reinterpret_cast<double2*>(r)[i];
+      xi.x += alpha * pi.x;
+      xi.y += alpha * pi.y;
+      ri.x -= alpha * qi.x;
+      ri.y -= alpha * qi.y;
+      reinterpret_cast<double2*>(x)[i] = xi;
+      reinterpret_cast<double2*>(r)[i] = ri;
+      if constexpr (F32) {
+        const float2 w = reinterpret_cast<const float2*>(invd32)[i];
+        const float2 rf = make_float2((float)ri.x, (float)ri.y);
+        reinterpret_cast<float2*>(r32)[i] = rf;
+        reinterpret_cast<float2*>(d32)[i] = make_float2(w.x * rf.x, w.y * rf.y);
+      }
+      acc += ri.x * ri.x;
+      acc += ri.y * ri.y;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) one(n - 1);
+  } else {
+    for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) one(i);
   }
   reduce_finish(acc, red, S_RR);
 }
 
 __global__ void k_to_f32(long n, const double* __restrict__ x, float* __restrict__ y) {
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = (float)x[i];
+}
+__global__ void k_to_f32_scaled(long n, const double* __restrict__ x, const float* __restrict__ invd,
+                                float* __restrict__ y, float* __restrict__ d) {
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    const float f = (float)x[i];
+    y[i] = f;
+    d[i] = invd[i] * f;
+  }
 }
 // z64 = z32 ; slot <- b.z64
 __global__ void k_to_f64_dot(int n, const float* __restrict__ z32, double* __restrict__ z64,
@@ -207,9 +250,26 @@ __global__ void k_boundary_load(int n, const int* __restrict__ rows, const doubl
 }  // namespace
 
 void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s,
-                       float* r32) {
+                       float* r32, const float* invd32, float* d32) {
   ++g_launch_count;
-  k_pcg_update<<<red_grid(k_pcg_update, n), kBlock, 0, s>>>(n, x, r, p, q, r32, red);
+  auto al = [](const void* ptr, int a) { return ((uintptr_t)ptr % a) == 0; };
+  const bool vec = al(x, 16) && al(r, 16) && al(p, 16) && al(q, 16) &&
+                   (!r32 || (al(r32, 8) && al(invd32, 8) && al(d32, 8)));
+  const long work = vec ? std::max(1, n / 2) : n;
+#define U_(F, V) \
+  k_pcg_update<F, V><<<red_grid(k_pcg_update<F, V>, work), kBlock, 0, s>>>(n, x, r, p, q, r32, invd32, d32, red)
+  if (r32) {
+    if (vec) U_(true, true); else U_(true, false);
+  } else {
+    if (vec) U_(false, true); else U_(false, false);
+  }
+#undef U_
+}
+void launch_to_f32_scaled(long n, const double* x, const float* invd, float* y, float* d, cudaStream_t s) {
+  if (n <= 0) return;
+  ++g_launch_count;
+  g_algo_bytes += 20.0 * n;
+  k_to_f32_scaled<<<grid_for(n), kBlock, 0, s>>>(n, x, invd, y, d);
 }
 void launch_to_f32(long n, const double* x, float* y, cudaStream_t s) {
   if (n <= 0) return;

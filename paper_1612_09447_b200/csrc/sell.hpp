@@ -32,8 +32,8 @@ struct HostSell {
   long padded() const { return chunk_ptr.empty() ? 0 : chunk_ptr.back(); }
 };
 
-// lanes per row: each lane handles about 16 entries of the mean row
-int choose_sell_tpr(const HostCsr& a);
+// lanes per row: each lane handles about `per_lane` entries of the mean row
+int choose_sell_tpr(const HostCsr& a, int per_lane = 16);
 // false (and `out` untouched) when some chunk's columns need more than kSellWindows windows
 bool build_sell(const HostCsr& a, int tpr, HostSell& out);
 // values in SELL order (padding 0), as T
@@ -52,9 +52,10 @@ namespace eqsb {
 // 32-bit word per entry, bf16 value in the high half and the 16-bit column
 // code in the low half. Four consecutive entries of a row form a 16-byte
 // group, so each lane reads a whole group with one vector load and a warp
-// load instruction moves 512 contiguous bytes (SELL-16 moves 64). Group g of
-// row q of a chunk sits at step g / tpr in lane q * tpr + g % tpr; a chunk is
-// `steps` x 32 groups. The column code is (window << shift) | (column - base)
+// load instruction moves 512 contiguous bytes (SELL-16 moves 64). Entry j of
+// row q of a chunk sits in lane q * tpr + j % tpr, slot (j / tpr) % 4 of step
+// j / (4 tpr), so the tpr lanes of a row gather consecutive columns; a chunk
+// is `steps` x 32 groups. The column code is (window << shift) | (column - base)
 // with shift 13, 12 or 11 (8, 16 or 32 windows per chunk, the first that fits).
 constexpr int kPackGroup = 4;
 
@@ -67,6 +68,9 @@ struct HostSellP {
 };
 
 uint16_t to_bf16(double d);  // round to nearest even
+// lanes per row of the packed format: about 32 entries per lane (fewer
+// shuffle-reduction steps and more loads in flight per lane on coarse levels)
+int choose_sellp_tpr(const HostCsr& a);
 // false when some chunk's columns need more than 32 windows
 bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out);
 

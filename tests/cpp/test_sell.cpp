@@ -32,7 +32,7 @@ static int check_packed(const HostCsr& a, const HostSellP& p) {
           const uint32_t w = p.words[4L * (p.chunk_ptr[c] + 32L * st + lane) + e];
           const unsigned code = w & 0xffffu;
           const int col = p.bases[(size_t)c * p.windows + (code >> p.shift)] + (int)(code & mask);
-          const int j = 4 * (st * p.tpr + sub) + e;  // entry index within the row
+          const int j = (st * 4 + e) * p.tpr + sub;  // entry index within the row
           if (r < a.n_rows && j < a.row_ptr[r + 1] - a.row_ptr[r]) {
             const long k = a.row_ptr[r] + j;
             if (col != a.col_idx[k]) return printf("col mismatch c%d lane%d st%d e%d\n", c, lane, st, e), 1;
