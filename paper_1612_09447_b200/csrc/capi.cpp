@@ -544,6 +544,8 @@ int eqs_set_option(eqs_ctx* ctx, int key, double value) {
       case 10: g.set_sell(value != 0.0); break;
       case 11: g.set_vcycle_vectors_f32(value != 0.0); break;
       case 12: g.reset_estimator((int)value); break;
+      case 13: g.cheb_kind = (int)value; g.set_cheb(g.cheb_ratio); break;
+      case 14: g.cheb_scale = value; g.set_cheb(g.cheb_ratio); break;
       default: throw std::invalid_argument("eqs_set_option: unknown key");
     }
   });

@@ -571,11 +571,27 @@ double GpuSystem::dot_n(int n, const double* a, const double* b, int slot) {
 // Chebyshev smoother on [lmax/ratio, lmax] of D^-1 A, lmax = 1.1 x the power
 // estimate. Degree 2: x += c0 D^-1 r0 + c1 D^-1 (r0 - A D^-1 r0 / theta);
 // degree 1: x += D^-1 r0 / theta.
+//
+// cheb_kind 1: fourth-kind Chebyshev smoother (no lower bound), same kernels:
+// d1 = 4/(3 lmax) D^-1 r, d2 = d1/5 + 12/(5 lmax) D^-1 (r - A d1), z = d1 + d2;
+// degree 1 is z = 4/(3 lmax) D^-1 r. cheb_scale multiplies the power estimate.
 void GpuSystem::set_cheb(double ratio) {
   invalidate_graphs();  // coefficients are baked into the captured kernel parameters
   cheb_ratio = ratio;
   for (auto& lv : levels_) {
-    const double lmax = 1.1 * lv.lambda_smoother, lmin = lmax / ratio;
+    const double lmax = cheb_scale * lv.lambda_smoother;
+    if (cheb_kind >= 1) {
+      // kind 2: Lottes' optimised weights z = sum_k beta_k d_k (residual
+      // recurrence unweighted): degree 1 beta 1.125; degree 2 (1.0239, 1.2641)
+      const double b1 = cheb_kind == 2 ? 1.02387287570313 : 1.0, b2 = cheb_kind == 2 ? 1.26408905371085 : 1.0;
+      const double b11 = cheb_kind == 2 ? 1.125 : 1.0;
+      lv.cheb.c0 = (b1 + b2 / 5.0) * 4.0 / (3.0 * lmax);
+      lv.cheb.c1 = b2 * 12.0 / (5.0 * lmax);
+      lv.cheb.inv_theta = 4.0 / (3.0 * lmax);
+      lv.cheb1 = ChebCoef{0.0, 0.0, b11 * 4.0 / (3.0 * lmax)};
+      continue;
+    }
+    const double lmin = lmax / ratio;
     const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
     const double sigma = theta / delta, rho0 = 1.0 / sigma, rho1 = 1.0 / (2.0 * sigma - rho0);
     lv.cheb.c0 = (1.0 + rho1 * rho0) / theta;

@@ -174,6 +174,8 @@ class GpuSystem {
   int cheb_degree = 2;     // fine level (1 or 2)
   int coarse_degree = 1;   // levels >= 1 (1 or 2)
   double cheb_ratio = 6.0;
+  int cheb_kind = 0;          // 0 first-kind Chebyshev on [lmax/ratio, lmax], 1 fourth-kind
+  double cheb_scale = 1.1;    // lmax = cheb_scale x the power estimate of lambda_max(D^-1 A)
   bool use_graphs = true;
   bool spe_incremental = true;  // false: the reference's full MGS rebuild on every solve
   void set_cheb(double ratio);
