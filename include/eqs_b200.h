@@ -66,6 +66,8 @@ typedef struct {
   int spe_window;         /* 8 */
   double mgs_drop_tol;    /* 1e-8 */
   double amg_coarse_filter; /* additive: V-cycle coarse-operator filter eps (0 = off; configs default 0.0025) */
+  int amg_dense_coarse;     /* additive: direct (dense) solve of the first coarse level with at most this many
+                               rows in the device V-cycle; <= 0 (default) = recurse to the coarsest */
 } eqs_solver_params;
 
 /* Problem description consumed by eqs_create: the arrays the reference's
@@ -280,7 +282,9 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * (0 fp64, 1 fp32, 2 bf16; default 2), 5/6/7 = CSR threads per row of levels
  * 0/1/2, 8 = CUDA graphs (0/1), 9 = incremental SPE (0/1), 10 = SELL-16
  * operators (0/1; default 1), 11 = fp32 V-cycle vectors (0/1; default 1),
- * 12 = start-vector estimator (0 zero, 1 previous, 2 spe; resets its history).
+ * 12 = start-vector estimator (0 zero, 1 previous, 2 spe; resets its history),
+ * 13 = smoother polynomial (0 first-kind Chebyshev, 1 fourth-kind, 2 fourth-kind
+ * with optimised weights), 14 = lambda_max safety factor (default 1.1).
  * The PCG operator and vectors are fp64 in every setting. */
 int eqs_set_option(eqs_ctx* ctx, int key, double value);
 /* The CUDA stream (cudaStream_t) every device call of this context runs on. */

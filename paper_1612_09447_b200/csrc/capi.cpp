@@ -75,6 +75,7 @@ SolverParams solver_from(const eqs_solver_params& s) {
   p.spe_window = s.spe_window;
   p.mgs_drop_tol = s.mgs_drop_tol;
   p.amg_coarse_filter = s.amg_coarse_filter;
+  p.amg_dense_coarse = s.amg_dense_coarse;
   return p;
 }
 

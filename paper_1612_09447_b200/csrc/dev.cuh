@@ -164,7 +164,7 @@ void launch_pcg_update(int n, double* x, double* r, const double* p, const doubl
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s);
 // z = Ainv b (dense, n <= 1024, fp64 inverse)
 template <class XT>
-void launch_dense_solve(int n, const double* ainv, const XT* b, XT* z, cudaStream_t s);
+void launch_dense_solve(int n, const double* ainv, const float* ainv32, const XT* b, XT* z, cudaStream_t s);
 // Jacobi: z = invd .* r (+ dot r.z into slot when red)
 void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s);
 // precision conversions at the fp32 V-cycle boundary

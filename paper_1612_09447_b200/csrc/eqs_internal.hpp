@@ -78,6 +78,9 @@ struct SolverParams {
   int amg_sweeps = 1, amg_max_levels = 10, amg_coarse_limit = 64;
   double amg_coarse_filter = 0.0025;  // additive: V-cycle coarse-operator filter (0 = off)
   int amg_replicate_rows = 32768;     // additive: coarse levels up to this size are replicated on every rank
+  int amg_dense_coarse = 0;           // additive: the device V-cycle solves the first coarse level with at most
+                                      // this many rows directly (dense inverse); <= 0 (default): recurse to the
+                                      // hierarchy's coarsest
   int estimator_mode = 0;  // 0 zero, 1 previous, 2 spe
   int spe_window = 8;
   double mgs_drop_tol = 1e-8;
@@ -118,6 +121,10 @@ struct AmgHierarchy {
 // AmgPreconditioner ctor (proj/src/amg.cpp:90-143), bit-exact aggregation and
 // Galerkin products (deterministic row-parallel SpGEMM).
 AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp);
+// explicit inverse (row-major) of a symmetric matrix through the pivoted LDLT
+// below (the coarsest-level solve, amg.cpp:140); threaded for the larger
+// dense coarse levels of the device V-cycle (SolverParams::amg_dense_coarse)
+std::vector<double> dense_inverse(const HostCsr& a);
 // V-cycle operator of a coarse level: entries with |a_ij| < eps sqrt(|a_ii a_jj|)
 // dropped and lumped onto the diagonal (row sums kept). The hierarchy itself
 // (P, R, Galerkin A_l) is untouched; only the smoother/residual operator of

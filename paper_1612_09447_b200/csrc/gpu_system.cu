@@ -217,6 +217,24 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
   if (prob_.solver.precond == 2) amg_ = build_amg(m_ii_, prob_.solver);
   ++stats_.precond_setups;
   memtrace("amg built");
+  // device V-cycle depth: the first coarse level with at most amg_dense_coarse
+  // rows is solved directly (explicit inverse of its Galerkin operator) instead
+  // of recursing through the remaining latency-bound levels
+  dev_levels_ = (int)amg_.levels.size();
+  if (prob_.solver.precond == 2 && prob_.solver.amg_dense_coarse > 0)
+    for (int l = 1; l + 1 < (int)amg_.levels.size(); ++l)
+      if (amg_.levels[l].A.n_rows <= prob_.solver.amg_dense_coarse) {
+        dev_levels_ = l + 1;
+        break;
+      }
+  if (prob_.solver.precond == 2 && dev_levels_ < (int)amg_.levels.size()) {
+    dev_coarse_n_ = amg_.levels[dev_levels_ - 1].A.n_rows;
+    dev_coarse_inv_ = dense_inverse(amg_.levels[dev_levels_ - 1].A);
+  } else {
+    dev_coarse_n_ = amg_.coarse_n;
+    dev_coarse_inv_ = amg_.coarse_inverse;
+  }
+  memtrace("dense coarse");
   // V-cycle operators of the coarse levels: lumped filtered Galerkin matrices
   // (DESIGN.md §4); the hierarchy reported through the API stays the reference's
   {
@@ -229,7 +247,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     }
     memtrace("coarse filter");
     plan_ = build_plan(prob_, m_ii_, m_ib_, amg_, comm_->size(), comm_->rank(), prob_.solver.amg_replicate_rows,
-                       &filtered);
+                       &filtered, dev_levels_);
   }
   memtrace("plan");
   const LocalSpace& s0 = plan_.space[0];
@@ -452,7 +470,7 @@ void GpuSystem::build_device() {
 // replicated dense coarsest solve.
 void GpuSystem::build_levels() {
   cudaStream_t s = stream_;
-  const int L = (int)amg_.levels.size();
+  const int L = std::min((int)amg_.levels.size(), dev_levels_);
   levels_.clear();
   levels_.resize(L);
   auto f32 = [&](const std::vector<double>& v, DevBuf<float>& out) {
@@ -515,9 +533,16 @@ void GpuSystem::build_levels() {
     }
     CK(cudaStreamSynchronize(s));
   }
-  coarse_n_ = amg_.coarse_n;
-  coarse_inv_.alloc(amg_.coarse_inverse.size());
-  coarse_inv_.upload(amg_.coarse_inverse.data(), amg_.coarse_inverse.size(), s);
+  coarse_n_ = dev_coarse_n_;
+  coarse_inv_.alloc(std::max<size_t>(1, dev_coarse_inv_.size()));
+  coarse_inv_.upload(dev_coarse_inv_.data(), dev_coarse_inv_.size(), s);
+  {
+    std::vector<float> f(dev_coarse_inv_.begin(), dev_coarse_inv_.end());
+    coarse_inv32_.alloc(std::max<size_t>(1, f.size()));
+    coarse_inv32_.upload(f.data(), f.size(), s);
+    CK(cudaStreamSynchronize(s));
+  }
+  std::vector<double>().swap(dev_coarse_inv_);
   set_vcycle_precision(vcycle_prec_);
   set_sell(sell_on_);
   // smoother bounds: lambda_max(D^-1 A_l) by 20 power iterations from a
@@ -861,13 +886,13 @@ XT* GpuSystem::vcycle_t(int l, const XT* b_in, bool dot_into_rz, const double* r
     // dense solve on the full vector (replicated level: b is already whole)
     XT* z = V::z(lv);
     if (comm_->size() == 1 || lv.replicated) {
-      launch_dense_solve<XT>(coarse_n_, coarse_inv_.p, b, z, stream_);
+      launch_dense_solve<XT>(coarse_n_, coarse_inv_.p, coarse_inv32_.p, b, z, stream_);
     } else {
       if constexpr (std::is_same_v<XT, double>) {
         launch_fill(coarse_n_, 0.0, lv.full_b.p, stream_);
         launch_scatter(lv.n_own, lv.glob.p, b, lv.full_b.p, stream_);
         comm_->allreduce(lv.full_b.p, coarse_n_, stream_);
-        launch_dense_solve<double>(coarse_n_, coarse_inv_.p, lv.full_b.p, lv.full_z.p, stream_);
+        launch_dense_solve<double>(coarse_n_, coarse_inv_.p, nullptr, lv.full_b.p, lv.full_z.p, stream_);
         launch_gather(lv.n_loc, lv.glob.p, lv.full_z.p, z, stream_);  // owned + ghosts
       } else {
         throw std::logic_error("fp32 V-cycle needs a replicated coarsest level");

@@ -288,7 +288,11 @@ class GpuSystem {
   DevHalo halo0_;  // level-0 (fine dof) halo
   std::vector<DevLevel> levels_;
   DevBuf<double> coarse_inv_;
+  DevBuf<float> coarse_inv32_;  // fp32 copy for the fp32 V-cycle's dense coarse solve
   int coarse_n_ = 0;
+  int dev_levels_ = 1;          // levels of the device V-cycle (<= the hierarchy's)
+  int dev_coarse_n_ = 0;
+  std::vector<double> dev_coarse_inv_;  // host staging of the dense coarse inverse
   // reductions
   DevBuf<double> red_partials_, red_scal_;
   DevBuf<unsigned> red_counters_;

@@ -100,12 +100,13 @@ std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out
 }
 
 PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m_ib, const AmgHierarchy& h,
-                         int nranks, int rank, int rep_threshold, const std::vector<HostCsr>* level_A) {
+                         int nranks, int rank, int rep_threshold, const std::vector<HostCsr>* level_A,
+                         int max_levels) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("build_plan: bad rank/nranks");
   PartitionPlan plan;
   plan.nranks = nranks;
   plan.rank = rank;
-  const int L = h.levels.empty() ? 1 : (int)h.levels.size();
+  const int L = h.levels.empty() ? 1 : std::min((int)h.levels.size(), std::max(1, max_levels));
   auto A_of = [&](int l) -> const HostCsr& {
     if (h.levels.empty()) return m_ii;
     if (level_A && l < (int)level_A->size() && (*level_A)[l].n_rows > 0) return (*level_A)[l];

@@ -454,7 +454,14 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp) {
     h.levels.push_back({std::move(coarse), {}, {}, {}, 0.0});
   }
   // coarsest: LDLT (amg.cpp:140) then an explicit inverse for a one-kernel dense solve
+  h.coarse_n = h.levels.back().A.n_rows;
+  h.coarse_inverse = dense_inverse(h.levels.back().A);
   const HostCsr& c = h.levels.back().A;
+  if (h.levels.size() > 1) h.levels.back().lambda_max_scaled = estimate_lambda_max_scaled(c, 10, 20240811u);
+  return h;
+}
+
+std::vector<double> dense_inverse(const HostCsr& c) {
   const int n = c.n_rows;
   std::vector<double> dense((size_t)n * n, 0.0);
   for (int i = 0; i < n; ++i)
@@ -462,17 +469,19 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp) {
   DenseLdlt ldlt;
   ldlt.compute(dense, n);
   if (!ldlt.ok) throw NumericalError("amg: coarsest-level factorization failed");
-  h.coarse_n = n;
-  h.coarse_inverse.assign((size_t)n * n, 0.0);
-  std::vector<double> e(n), col(n);
-  for (int j = 0; j < n; ++j) {
-    std::fill(e.begin(), e.end(), 0.0);
-    e[j] = 1.0;
-    ldlt.solve(e.data(), col.data());
-    for (int i = 0; i < n; ++i) h.coarse_inverse[(size_t)i * n + j] = col[i];
+  std::vector<double> inv((size_t)n * n, 0.0);
+#pragma omp parallel if (n > 256)
+  {
+    std::vector<double> e(n), col(n);
+#pragma omp for schedule(static)
+    for (int j = 0; j < n; ++j) {
+      std::fill(e.begin(), e.end(), 0.0);
+      e[j] = 1.0;
+      ldlt.solve(e.data(), col.data());
+      for (int i = 0; i < n; ++i) inv[(size_t)i * n + j] = col[i];
+    }
   }
-  if (h.levels.size() > 1) h.levels.back().lambda_max_scaled = estimate_lambda_max_scaled(c, 10, 20240811u);
-  return h;
+  return inv;
 }
 
 HostCsr filter_lumped(const HostCsr& a, double eps) {
@@ -541,6 +550,8 @@ void DenseLdlt::compute(const std::vector<double>& a, int n_) {
       double s = 0.0;
       for (int j = 0; j < k; ++j) s += M(k, j) * temp[j];
       M(k, k) -= s;
+      // rows are independent: same per-row summation order at any thread count
+#pragma omp parallel for schedule(static) if ((long)(n - k) * k > 200000)
       for (int i = k + 1; i < n; ++i) {
         double t = 0.0;
         for (int j = 0; j < k; ++j) t += M(i, j) * temp[j];

@@ -125,7 +125,14 @@ __device__ __forceinline__ XT sell_dot(const DevSell& m, const VT* __restrict__ 
 // packed entries (bf16 value in the high half: decoding is a mask). Steps are
 // batched by 4 (a whole fine-level row per batch at TPR 1). Result in lane
 // (row_in_chunk * TPR).
-template <int TPR, class XT, bool SCALED>
+// CG: gathers bypass L1 (for vectors written earlier in the same kernel)
+template <bool CG, class T>
+__device__ __forceinline__ T ldvec(const T* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return __ldg(p);
+}
+
+template <int TPR, class XT, bool SCALED, bool CG = false>
 __device__ __forceinline__ XT sellp_dot(const DevSellP& m, int chunk, int lane, const XT* __restrict__ x,
                                         const XT* __restrict__ w) {
   const int beg = __ldg(m.chunk_ptr + chunk);
@@ -149,7 +156,7 @@ __device__ __forceinline__ XT sellp_dot(const DevSellP& m, int chunk, int lane, 
         const int c = __shfl_sync(0xffffffffu, mybase, (int)(code >> shift)) + (int)(code & mask);
         if (s0 + u < S) {
           const XT a = (XT)__uint_as_float(wd[e] & 0xffff0000u);
-          const XT xv = SCALED ? __ldg(x + c) * __ldg(w + c) : __ldg(x + c);
+          const XT xv = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
           s += a * xv;
         }
       }
@@ -179,18 +186,22 @@ __device__ __forceinline__ XT sellp_dot(const DevSellP& m, int chunk, int lane, 
 // MODE 1: y = b - A x, y.y
 // MODE 2: z += c0 D^-1 r0 + c1 D^-1 (r0 - A D^-1 r0 / theta), b.z   (Chebyshev(2) post step 2; x = r0)
 // MODE 3: as MODE 2 but z_out64 = z + ... in fp64 and b64.z_out64   (fine level of the fp32 V-cycle)
-template <int OP, int MODE, class XT>
+template <int OP, int MODE, class XT, bool CG = false>
 struct Epi {
   XT p0 = 0, p1 = 0, p2 = 0, p3 = 0;
   double q = 0.0;
+  static __device__ __forceinline__ XT ld(const XT* p) {
+    if constexpr (CG) return __ldcg(p);
+    else return *p;
+  }
   __device__ __forceinline__ void load(int row, const XT* __restrict__ x, const XT* __restrict__ b,
                                        const XT* __restrict__ invd, const XT* y, const double* __restrict__ b64,
                                        int do_red) {
     if constexpr (MODE < 0) {
-      if (OP == 1 || OP == 3 || OP == 4 || OP == 5 || OP == 8) p0 = b[row];
-      if (OP == 3 || OP == 4 || OP == 5 || OP == 6 || OP == 8 || OP == 9) p1 = invd[row];
-      if (OP == 5) p2 = x[row];
-      if (OP == 2) p2 = y[row];
+      if (OP == 1 || OP == 3 || OP == 4 || OP == 5 || OP == 8) p0 = ld(b + row);
+      if (OP == 3 || OP == 4 || OP == 5 || OP == 6 || OP == 8 || OP == 9) p1 = ld(invd + row);
+      if (OP == 5) p2 = ld(x + row);
+      if (OP == 2) p2 = ld(y + row);
     } else {
       if (MODE == 0 || MODE >= 2) p0 = x[row];
       if (MODE == 1 || (MODE == 2 && do_red)) p1 = b[row];

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <unordered_map>
 
 #include "dev.cuh"
@@ -30,6 +31,21 @@ __global__ void k_dense_solve(int n, const double* __restrict__ ainv, const XT* 
     s = warp_sum(s);
     if (l == 0) z[row] = (XT)s;
   }
+}
+
+// z = Ainv b for the larger dense coarse levels: one warp per row, coalesced
+// row reads (fp32 inverse for the fp32 V-cycle), fp64 accumulation
+template <class MT, class XT>
+__global__ void __launch_bounds__(kBlock) k_dense_gemv(int n, const MT* __restrict__ a, const XT* __restrict__ b,
+                                                      XT* __restrict__ z) {
+  const int row = (int)((blockIdx.x * (long)kBlock + threadIdx.x) >> 5), l = threadIdx.x & 31;
+  if (row >= n) return;
+  const MT* ar = a + (size_t)row * n;
+  double s = 0.0;
+#pragma unroll 8
+  for (int k = l; k < n; k += 32) s += (double)__ldcs(ar + k) * (double)__ldg(b + k);
+  s = warp_sum(s);
+  if (l == 0) z[row] = (XT)s;
 }
 
 __global__ void k_jacobi(int n, const double* __restrict__ invd, const double* __restrict__ r,
@@ -288,13 +304,24 @@ void launch_pcg_direction(int n, double* p, const double* z, const double* scal,
   k_pcg_direction<<<grid_for(n), kBlock, 0, s>>>(n, p, z, scal);
 }
 template <class XT>
-void launch_dense_solve(int n, const double* ainv, const XT* b, XT* z, cudaStream_t s) {
+void launch_dense_solve(int n, const double* ainv, const float* ainv32, const XT* b, XT* z, cudaStream_t s) {
   ++g_launch_count;
-  g_algo_bytes += 8.0 * n * n;
-  k_dense_solve<XT><<<1, 1024, n * sizeof(double), s>>>(n, ainv, b, z);
+  if (n <= 256) {  // the hierarchy's own <= 64-row coarsest (amg.hpp:17): one block
+    g_algo_bytes += 8.0 * n * n;
+    k_dense_solve<XT><<<1, 1024, n * sizeof(double), s>>>(n, ainv, b, z);
+    return;
+  }
+  const int g = (int)(((long)n * 32 + kBlock - 1) / kBlock);
+  if (std::is_same_v<XT, float> && ainv32) {
+    g_algo_bytes += 4.0 * n * n + 8.0 * n;
+    k_dense_gemv<float, XT><<<g, kBlock, 0, s>>>(n, ainv32, b, z);
+  } else {
+    g_algo_bytes += 8.0 * n * n + 2.0 * sizeof(XT) * n;
+    k_dense_gemv<double, XT><<<g, kBlock, 0, s>>>(n, ainv, b, z);
+  }
 }
-template void launch_dense_solve<double>(int, const double*, const double*, double*, cudaStream_t);
-template void launch_dense_solve<float>(int, const double*, const float*, float*, cudaStream_t);
+template void launch_dense_solve<double>(int, const double*, const float*, const double*, double*, cudaStream_t);
+template void launch_dense_solve<float>(int, const double*, const float*, const float*, float*, cudaStream_t);
 void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s) {
   ++g_launch_count;
   Reducer rr = red ? *red : Reducer{};

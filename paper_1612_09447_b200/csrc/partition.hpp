@@ -53,6 +53,7 @@ std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out
 // products (allreduce), and no halo is exchanged below it.
 // level_A (optional): replacement operators per level (entries with n_rows == 0 keep h's)
 PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m_ib, const AmgHierarchy& h,
-                         int nranks, int rank, int rep_threshold, const std::vector<HostCsr>* level_A = nullptr);
+                         int nranks, int rank, int rep_threshold, const std::vector<HostCsr>* level_A = nullptr,
+                         int max_levels = 1 << 30);
 
 }  // namespace eqsb

@@ -111,6 +111,7 @@ def load_library():
         L.eqs_last_error.restype = C.c_char_p
         L.eqs_destroy.restype = None
         L.eqs_destroy.argtypes = [C.c_void_p]
+        L.eqs_launch_count.restype = C.c_long
         for fn in ("eqs_eval_rhs", "eqs_eval_residual", "eqs_apply_minv_stiffness", "eqs_lift_full",
                    "eqs_set_state", "eqs_mass_solve", "eqs_rkc_advance_fixed", "eqs_euler_step",
                    "eqs_set_option"):

@@ -234,3 +234,23 @@ def test_nan_field_maps_to_invalid_argument():  # materials.cpp:26 quirk (exit c
     x = np.full(g.n_free, np.nan)
     with pytest.raises(eb.InvalidArgument):
         g.eval_residual(0.0, x)
+
+
+
+def test_dense_coarse_truncation():
+    """amg_dense_coarse: the device V-cycle stops at the first coarse level
+    with at most that many rows and solves it with its dense inverse; the
+    M-solve still converges to the oracle's solution."""
+    cfg = cube(24, jitter=0.1, planes=(0.45, 0.55))
+    o = po.Problem(cfg)
+    b = po.random_vec(o.n_free, 11)
+    xo = o.mass_solve(b)[0]
+    g0 = eb.FemSystem(cfg)
+    x0, r0 = g0.mass_solve(b)
+    cfg["solver"]["amg_dense_coarse"] = 4096
+    g1 = eb.FemSystem(cfg)
+    x1, r1 = g1.mass_solve(b)
+    assert r0.converged and r1.converged
+    assert r1.iterations <= r0.iterations + 1
+    for x in (x0, x1):
+        assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
