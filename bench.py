@@ -55,6 +55,9 @@ CONFIGS = {
 CPU_SAMPLE = dict(n=48, steps=2)
 
 
+COARSE_FILTER = None  # --coarse-filter: solver.amg_coarse_filter override (additive key)
+
+
 def scenario(n, jitter, planes, estimator="spe"):
     return {
         "name": f"bench_cube{n}",
@@ -64,7 +67,8 @@ def scenario(n, jitter, planes, estimator="spe"):
         "materials": MATERIALS,
         "excitations": {"hv": {"kind": "sinusoid", "amplitude": 4e4 / 0.012, "frequency": 50.0},
                         "ground": {"kind": "constant", "value": 0.0}},
-        "solver": {"preconditioner": "amg", "rel_tol": 1e-12, "max_iter": 500},
+        "solver": dict({"preconditioner": "amg", "rel_tol": 1e-12, "max_iter": 500},
+                       **({} if COARSE_FILTER is None else {"amg_coarse_filter": COARSE_FILTER})),
         "estimator": {"mode": estimator, "window": 8},
     }
 
@@ -118,6 +122,16 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+def ncu_traffic(config_name):
+    """DRAM bytes per launch of each timing class from the committed ncu launch
+    list of this workload (tools/ncu_traffic.py -> profiles/ncu_traffic_<config>.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{config_name}.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch", {})
+    except OSError:
+        return {}
 
 
 def measured_peaks():
@@ -405,6 +419,7 @@ def run_b200(args):
         return
     peaks, peak_kind = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = ncu_traffic(args.config)
     # roofline of the dominant kernel class (TimeClass in gpu_system.hpp): per-class
     # device time from CUDA events on the library stream, algorithmic bytes per launch
     names = ["stiffness K(x)x", "pcg spmv+vectors", "v-cycle", "rkc stage/error", "spe estimator", "boundary"]
@@ -418,8 +433,10 @@ def run_b200(args):
         avg_ms = timing["ms"][c] / timing["launches"][c]
         per = timing["bytes"][c] / timing["launches"][c]
         ach = per / (avg_ms / 1e3) / 1e9
+        tr = traffic.get(names[c])
         return {"kernel": kernels[c], "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "traffic": None, "bytes_per_launch": per, "avg_launch_ms": avg_ms,
+                "frac": ach / hbm, "traffic": tr, "traffic_source": f"profiles/ncu_traffic_{args.config}.json"
+                if tr else None, "bytes_per_launch": per, "avg_launch_ms": avg_ms,
                 "share_of_step": timing["ms"][c] / sum(timing["ms"][:6]),
                 "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"}
 
@@ -472,6 +489,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--coarse-filter", type=float, default=None,
+                    help="solver.amg_coarse_filter (V-cycle coarse-operator filter, DESIGN.md §4)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the in-run CPU baseline sample")
     ap.add_argument("--estimator", default="spe", choices=["zero", "previous", "spe"],
                     help="MRHS start vectors (proj/src/start_vector.cpp); the reference nonlinear scenario uses spe")
@@ -481,6 +500,8 @@ def main():
                     help="rkc: the headline line (default); euler: config 2 Euler vs RKC on --config (c2); "
                          "mrhs: config 5 multiple-right-hand-side sequence on --config")
     args = ap.parse_args()
+    global COARSE_FILTER
+    COARSE_FILTER = args.coarse_filter
     if args.impl == "reference":
         run_reference(args)
     elif args.mode == "euler":
