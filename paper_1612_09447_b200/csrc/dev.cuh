@@ -104,6 +104,23 @@ void launch_kx_tets(int order, int n_tets, const int* tet_dofs, const unsigned c
 // pass 2: out[d] = base[d] + sign * sum over incident slots (ascending tet)
 void launch_kx_gather(int n_rows, const long* slot_ptr, const int* slots, const double* ytet, const double* base,
                       double sign, double* out, cudaStream_t s);
+// blocked single pass + boundary partials (kxblock.hpp): out[d] = base[d] +
+// sign * (K(x) v)[d] for d < n_out (base may be null)
+struct KxDev {
+  int nl = 4, n_blocks = 0, max_block_tets = 0, max_block_dofs = 0, max_block_slots = 0, n_bdof = 0;
+  const int* blk_tet0 = nullptr;
+  const int* tets = nullptr;           // blocked order: P1 ushort4 block-local dof ids, P2 [tets][10] dof ids
+  const int* ldof_dof = nullptr;       // dof of every block-dof entry
+  const unsigned char* mat = nullptr;  // blocked order
+  const int* blk_dof0 = nullptr;
+  const int* sptr = nullptr;
+  const uint16_t* slots = nullptr;
+  const int* lout = nullptr;
+  double* partials = nullptr;
+  const int *bdof = nullptr, *bptr = nullptr, *bpart = nullptr;
+};
+void launch_kx_blocked(const KxDev& k, const double* coords, const double* x_state, const double* v,
+                       const double* base, double sign, int n_out, double* out, int* geo_error, cudaStream_t s);
 // coloured single pass: y[dof] += local product for one colour batch
 void launch_kx_colored(int order, int n_batch, const int* batch_tets, const int* tet_dofs,
                        const unsigned char* tet_mat, const double* coords, const double* x_state, const double* v,

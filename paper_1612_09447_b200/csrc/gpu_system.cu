@@ -8,6 +8,7 @@
 // (restrict_free, :17-20) is free. With one rank the owned set is every free
 // dof in DofMap::free_dofs order and there are no ghosts.
 #include "gpu_system.hpp"
+#include "kxblock.hpp"
 #include "sell.hpp"
 
 #include <algorithm>
@@ -388,20 +389,63 @@ void GpuSystem::build_device() {
     tet_dofs_.upload(td.data(), td.size(), s);
     tet_mat_.alloc(std::max<size_t>(1, tm.size()));
     tet_mat_.upload(tm.data(), tm.size(), s);
-    // slot lists: local dof -> (local tet * n_local + i), ascending tet
-    std::vector<long> ptr((size_t)n_full_ + 1, 0);
-    for (size_t k = 0; k < td.size(); ++k) ++ptr[td[k] + 1];
-    for (int d = 0; d < n_full_; ++d) ptr[d + 1] += ptr[d];
-    if (ptr.back() >= (1L << 31)) throw ConfigError("mesh too large for int32 slot indices");
-    std::vector<int> sl(std::max<long>(1, ptr.back()));
-    std::vector<long> next(ptr.begin(), ptr.end() - 1);
-    for (size_t k = 0; k < td.size(); ++k) sl[next[td[k]]++] = (int)k;
-    slot_ptr_.alloc(ptr.size());
-    slot_ptr_.upload(ptr.data(), ptr.size(), s);
-    slots_.alloc(sl.size());
-    slots_.upload(sl.data(), sl.size(), s);
-    ytet_.alloc(std::max<size_t>(1, td.size()));
     CK(cudaStreamSynchronize(s));
+    // blocked deterministic scatter (kxblock.hpp)
+    const int nl = order_ == 1 ? 4 : 10;
+    static const int env_bt = getenv("EQS_KX_BLOCK_TETS") ? atoi(getenv("EQS_KX_BLOCK_TETS")) : 0;
+    const int bt = env_bt > 0 ? env_bt : (order_ == 1 ? 1024 : 512);
+    std::vector<double> c4((size_t)std::max(1, n_full_) * 4, 0.0);
+    CK(cudaMemcpy(c4.data(), coords_.p, sizeof(double) * c4.size(), cudaMemcpyDeviceToHost));
+    KxBlocks kb = build_kx_blocks(td, nl, n_tets_loc_, c4, n_full_, bt);
+    std::vector<int> btd((size_t)std::max(1, n_tets_loc_) * nl);
+    std::vector<unsigned char> btm(std::max(1, n_tets_loc_));
+    for (int k = 0; k < n_tets_loc_; ++k) {
+      const int t = kb.tet_perm[k];
+      for (int i = 0; i < nl; ++i) btd[(size_t)nl * k + i] = td[(size_t)nl * t + i];
+      btm[k] = tm[t];
+    }
+    auto up = [&](auto& buf, const auto& v) {
+      buf.alloc(std::max<size_t>(1, v.size()));
+      buf.upload(v.data(), v.size(), s);
+    };
+    if (nl == 4) {
+      up(kb_tloc_, kb.tet_local);
+    } else {
+      up(kb_tets_, btd);
+    }
+    up(kb_ldof_, kb.ldof_dof);
+    up(kb_mat_, btm);
+    up(kb_tet0_, kb.blk_tet0);
+    up(kb_dof0_, kb.blk_dof0);
+    up(kb_sptr_, kb.ldof_sptr);
+    up(kb_slots_, kb.slots);
+    up(kb_lout_, kb.ldof_out);
+    up(kb_bdof_, kb.bdof);
+    up(kb_bptr_, kb.bptr);
+    up(kb_bpart_, kb.bpart);
+    kb_partials_.alloc(std::max(1, kb.n_partials));
+    CK(cudaStreamSynchronize(s));
+    kxd_.nl = nl;
+    kxd_.n_blocks = kb.n_blocks;
+    kxd_.max_block_tets = kb.max_block_tets;
+    kxd_.max_block_dofs = kb.max_block_dofs;
+    kxd_.max_block_slots = kb.max_block_slots;
+    kxd_.n_bdof = (int)kb.bdof.size();
+    kxd_.blk_tet0 = kb_tet0_.p;
+    kxd_.tets = nl == 4 ? reinterpret_cast<const int*>(kb_tloc_.p) : kb_tets_.p;
+    kxd_.ldof_dof = kb_ldof_.p;
+    kxd_.mat = kb_mat_.p;
+    kxd_.blk_dof0 = kb_dof0_.p;
+    kxd_.sptr = kb_sptr_.p;
+    kxd_.slots = kb_slots_.p;
+    kxd_.lout = kb_lout_.p;
+    kxd_.partials = kb_partials_.p;
+    kxd_.bdof = kb_bdof_.p;
+    kxd_.bptr = kb_bptr_.p;
+    kxd_.bpart = kb_bpart_.p;
+    kx_partials_ = kb.n_partials;
+    kx_ldofs_ = (long)kb.ldof_out.size();
+    kx_slots_ = (long)kb.slots.size();
   }
   err_.alloc(4);
   CK(cudaMemsetAsync(err_.p, 0, 4 * sizeof(int), s));
@@ -786,6 +830,50 @@ void GpuSystem::lift_dev(double t, double* x_full) {
   launch_lift_fixed(n_fixloc_, set_of_fixed_.p, sv, x_full + n_loc_, stream_);
 }
 
+// two-pass gather mode (stiffness_mode 2): per-tet products through HBM, then
+// one thread per dof over an ascending-tet slot list; built on first use
+void GpuSystem::build_kx_gather() {
+  if (slots_built_) return;
+  const std::vector<int>& td = tet_dofs_host();
+  std::vector<long> ptr((size_t)n_full_ + 1, 0);
+  for (size_t k = 0; k < td.size(); ++k) ++ptr[td[k] + 1];
+  for (int d = 0; d < n_full_; ++d) ptr[d + 1] += ptr[d];
+  if (ptr.back() >= (1L << 31)) throw ConfigError("mesh too large for int32 slot indices");
+  std::vector<int> sl(std::max<long>(1, ptr.back()));
+  std::vector<long> next(ptr.begin(), ptr.end() - 1);
+  for (size_t k = 0; k < td.size(); ++k) sl[next[td[k]]++] = (int)k;
+  slot_ptr_.alloc(ptr.size());
+  slot_ptr_.upload(ptr.data(), ptr.size(), stream_);
+  slots_.alloc(sl.size());
+  slots_.upload(sl.data(), sl.size(), stream_);
+  ytet_.alloc(std::max<size_t>(1, td.size()));
+  CK(cudaStreamSynchronize(stream_));
+  slots_built_ = true;
+}
+
+// tet dofs in the tet_dofs_ (unblocked) order, read back from the device
+const std::vector<int>& GpuSystem::tet_dofs_host() {
+  if (tet_dofs_h_.empty()) {
+    tet_dofs_h_.resize((size_t)std::max(1, n_tets_loc_) * (order_ == 1 ? 4 : 10));
+    CK(cudaMemcpy(tet_dofs_h_.data(), tet_dofs_.p, sizeof(int) * tet_dofs_h_.size(), cudaMemcpyDeviceToHost));
+    tet_dofs_h_.resize((size_t)n_tets_loc_ * (order_ == 1 ? 4 : 10));
+  }
+  return tet_dofs_h_;
+}
+
+// out[d] = base[d] + sign * (K(x) v)[d] for the first n_out local dofs
+// (blocked scatter by default, the two-pass gather in stiffness_mode 2)
+void GpuSystem::kx_into(const double* x, const double* v, const double* base, double sign, double* out, int n_out) {
+  if (stiffness_mode == 2) {
+    build_kx_gather();
+    kx_tets(x, v);
+    launch_kx_gather(n_out, slot_ptr_.p, slots_.p, ytet_.p, base, sign, out, stream_);
+    return;
+  }
+  launch_kx_blocked(kxd_, coords_.p, x, v, base, sign, n_out, out, err_.p, stream_);
+  ++stats_.applies;
+}
+
 void GpuSystem::kx_tets(const double* x, const double* v) {
   launch_kx_tets(order_, n_tets_loc_, tet_dofs_.p, tet_mat_.p, coords_.p, x, v, ytet_.p, err_.p, stream_);
   ++stats_.applies;
@@ -813,8 +901,7 @@ void GpuSystem::kx_apply_full_dev(const double* x_state, const double* v, double
                         tet_dofs_.p, tet_mat_.p, coords_.p, x_state, v, y, err_.p, stream_);
     ++stats_.applies;
   } else {
-    kx_tets(x_state, v);
-    launch_kx_gather(n_full_, slot_ptr_.p, slots_.p, ytet_.p, nullptr, 1.0, y, stream_);
+    kx_into(x_state, v, nullptr, 1.0, y, n_full_);
   }
   toc(TC_STIFF, kx_bytes());
 }
@@ -829,8 +916,7 @@ void GpuSystem::residual_dev(double t, double* x_full, double* r) {
     kx_apply_full_dev(x_full, x_full, w_full_a_.p);
     launch_scale(n_own_, -1.0, w_full_a_.p, r, stream_);
   } else {
-    kx_tets(x_full, x_full);
-    launch_kx_gather(n_own_, slot_ptr_.p, slots_.p, ytet_.p, nullptr, -1.0, r, stream_);
+    kx_into(x_full, x_full, nullptr, -1.0, r, n_own_);
   }
   toc(TC_STIFF, kx_bytes() - 8.0 * n_fixloc_);
   const std::vector<double> rt = set_values(t, true);
@@ -1478,8 +1564,7 @@ void GpuSystem::apply_minv_stiffness_dev(double t, double* x_full, const double*
       kx_apply_full_dev(x_full, vfull, w_full_a_.p);
       CK(cudaMemcpyAsync(kv, w_full_a_.p, sizeof(double) * n_own_, cudaMemcpyDeviceToDevice, stream_));
     } else {
-      kx_tets(x_full, vfull);
-      launch_kx_gather(n_own_, slot_ptr_.p, slots_.p, ytet_.p, nullptr, 1.0, kv, stream_);
+      kx_into(x_full, vfull, nullptr, 1.0, kv, n_own_);
     }
     toc(TC_STIFF, kx_bytes());
     check_kernel_flags();
@@ -1553,8 +1638,7 @@ void GpuSystem::kx_residual_host(const double* x_full, const double* b_mass, dou
     kx_apply_full_dev(w_full_a_.p, w_full_a_.p, w_full_b_.p);
     launch_axpby_into(n_own_, w_free_a_.p, -1.0, w_full_b_.p, w_free_b_.p, stream_);
   } else {
-    kx_tets(w_full_a_.p, w_full_a_.p);
-    launch_kx_gather(n_own_, slot_ptr_.p, slots_.p, ytet_.p, w_free_a_.p, -1.0, w_free_b_.p, stream_);
+    kx_into(w_full_a_.p, w_full_a_.p, w_free_a_.p, -1.0, w_free_b_.p, n_own_);
   }
   toc(TC_STIFF, kx_bytes());
   w_free_b_.download(r, n_own_, stream_);

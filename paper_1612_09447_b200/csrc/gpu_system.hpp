@@ -170,7 +170,7 @@ class GpuSystem {
   double* scratch_full() { return full_[0].p != X_ ? full_[0].p : full_[1].p; }
 
   // ---- options / timing
-  int stiffness_mode = 0;  // 0 gather, 1 coloured
+  int stiffness_mode = 0;  // 0 blocked scatter, 1 coloured, 2 two-pass gather
   int cheb_degree = 2;     // fine level (1 or 2)
   int coarse_degree = 1;   // levels >= 1 (1 or 2)
   double cheb_ratio = 6.0;
@@ -214,6 +214,9 @@ class GpuSystem {
   // z = M^-1 r (returned buffer), S_RZ <- r.z; prepared: the PCG update already
   // wrote the fp32 V-cycle inputs
   double* precondition(double* r, bool prepared = false);
+  void build_kx_gather();
+  const std::vector<int>& tet_dofs_host();
+  void kx_into(const double* x, const double* v, const double* base, double sign, double* out, int n_out);
   void kx_tets(const double* x, const double* v);
   double read_scalar(int slot);
   void read_scalars(int first, int count, double* out);
@@ -268,9 +271,19 @@ class GpuSystem {
   DevBuf<double> coords_;  // [n_full][4]
   DevBuf<int> tet_dofs_;   // [n_tets_loc][n_local] local full numbering
   DevBuf<unsigned char> tet_mat_;
-  DevBuf<long> slot_ptr_;
+  DevBuf<long> slot_ptr_;  // two-pass gather mode (stiffness_mode 2), built on first use
   DevBuf<int> slots_;
   DevBuf<double> ytet_;
+  bool slots_built_ = false;
+  std::vector<int> tet_dofs_h_;
+  // blocked scatter (kxblock.hpp, default)
+  DevBuf<int> kb_tets_, kb_tet0_, kb_dof0_, kb_sptr_, kb_lout_, kb_bdof_, kb_bptr_, kb_bpart_;
+  DevBuf<unsigned char> kb_mat_;
+  DevBuf<uint16_t> kb_slots_, kb_tloc_;
+  DevBuf<int> kb_ldof_;
+  DevBuf<double> kb_partials_;
+  KxDev kxd_;
+  long kx_partials_ = 0, kx_ldofs_ = 0, kx_slots_ = 0;
   DevBuf<int> err_;  // kernel error flags
   DevBuf<int> set_of_fixed_;
   DevBuf<int> bl_rows_;

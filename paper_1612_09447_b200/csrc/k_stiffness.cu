@@ -70,18 +70,11 @@ __device__ __forceinline__ bool geometry(const double p[4][3], double g[4][3], d
   return det != 0.0;
 }
 
-// local product of one P1 tet; returns false on a degenerate tet
-__device__ __forceinline__ void p1_local(int4 n, int m, const double* __restrict__ coords,
-                                         const double* __restrict__ x, const double* __restrict__ v, bool same,
-                                         double y[4], int* err) {
-  double p[4][3];
-  load_xyz(coords, n.x, p[0]);
-  load_xyz(coords, n.y, p[1]);
-  load_xyz(coords, n.z, p[2]);
-  load_xyz(coords, n.w, p[3]);
+// local product of one P1 tet from its vertex coordinates and x / v values
+__device__ __forceinline__ void p1_compute(const double p[4][3], const double xl[4], const double vl[4], bool same,
+                                           int m, double y[4], int* err) {
   double g[4][3], vol;
   if (!geometry(p, g, vol)) atomicOr(err, 1);
-  const double xl[4] = {__ldg(x + n.x), __ldg(x + n.y), __ldg(x + n.z), __ldg(x + n.w)};
   double gx[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -96,7 +89,6 @@ __device__ __forceinline__ void p1_local(int4 n, int m, const double* __restrict
     gv[1] = gx[1];
     gv[2] = gx[2];
   } else {
-    const double vl[4] = {__ldg(v + n.x), __ldg(v + n.y), __ldg(v + n.z), __ldg(v + n.w)};
     gv[0] = gv[1] = gv[2] = 0.0;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -106,6 +98,26 @@ __device__ __forceinline__ void p1_local(int4 n, int m, const double* __restrict
   const double c = vol * kap;
 #pragma unroll
   for (int i = 0; i < 4; ++i) y[i] = c * (g[i][0] * gv[0] + g[i][1] * gv[1] + g[i][2] * gv[2]);
+}
+
+// local product of one P1 tet gathered from global memory
+__device__ __forceinline__ void p1_local(int4 n, int m, const double* __restrict__ coords,
+                                         const double* __restrict__ x, const double* __restrict__ v, bool same,
+                                         double y[4], int* err) {
+  double p[4][3];
+  load_xyz(coords, n.x, p[0]);
+  load_xyz(coords, n.y, p[1]);
+  load_xyz(coords, n.z, p[2]);
+  load_xyz(coords, n.w, p[3]);
+  const double xl[4] = {__ldg(x + n.x), __ldg(x + n.y), __ldg(x + n.z), __ldg(x + n.w)};
+  double vl[4] = {0.0, 0.0, 0.0, 0.0};
+  if (!same) {
+    vl[0] = __ldg(v + n.x);
+    vl[1] = __ldg(v + n.y);
+    vl[2] = __ldg(v + n.z);
+    vl[3] = __ldg(v + n.w);
+  }
+  p1_compute(p, xl, vl, same, m, y, err);
 }
 
 // P2: 10 dofs, 4-point degree-2 rule (assembly.cpp:13-18, 69-85, 97-116)
@@ -236,7 +248,144 @@ __global__ void __launch_bounds__(kBlock) k_kx_colored_p2(int nb, const int* __r
   for (int i = 0; i < 10; ++i) y[dofs[i]] += yl[i];
 }
 
+// Blocked deterministic scatter (kxblock.hpp): one CTA per tet block. The
+// block's dof lists (slot ranges, slots, outputs) are staged into shared
+// memory first, overlapping the element phase; the element phase computes the
+// local products into shared memory (next tet's indices prefetched); the sum
+// phase adds them per block-dof in slot order. Interior dofs are final (out =
+// base + sign * sum for dofs < n_out), boundary dofs leave a partial for pass 2.
+template <int NL>
+__global__ void __launch_bounds__(kBlock, NL == 4 ? 4 : 1) k_kx_block(const int* __restrict__ blk_tet0, const int* __restrict__ tets,
+                                                     const unsigned char* __restrict__ mat,
+                                                     const double* __restrict__ coords, const double* __restrict__ x,
+                                                     const double* __restrict__ v, const int* __restrict__ blk_dof0,
+                                                     const int* __restrict__ sptr, const uint16_t* __restrict__ slots,
+                                                     const int* __restrict__ lout, double* __restrict__ partials,
+                                                     const double* __restrict__ base, double sign, int n_out,
+                                                     double* __restrict__ out, int* err, int max_tets, int max_dofs,
+                                                     int max_slots, const int* __restrict__ ldof_dof) {
+  // shared memory: [NL][max_tets] products; P1: staged coordinates [max_dofs][3],
+  // x and v [max_dofs]; then the dof lists (slot ranges, outputs, slots)
+  extern __shared__ double ysm[];
+  double* s_xyz = ysm + (size_t)max_tets * NL;
+  double* s_x = s_xyz + 3L * max_dofs;
+  int* s_sptr = reinterpret_cast<int*>(NL == 4 ? s_x + 2L * max_dofs : s_xyz);  // [max_dofs + 1]
+  int* s_out = s_sptr + max_dofs + 1;                                             // [max_dofs]
+  uint16_t* s_slot = reinterpret_cast<uint16_t*>(s_out + max_dofs);               // [max_slots]
+  const int b = blockIdx.x;
+  const int t0 = blk_tet0[b], nt = blk_tet0[b + 1] - t0;
+  const int d0 = blk_dof0[b], nd = blk_dof0[b + 1] - d0;
+  const int sbase = sptr[d0], nsl = sptr[d0 + nd] - sbase;
+  // stage the dof lists (independent loads, in flight during the element phase)
+  for (int i = threadIdx.x; i <= nd; i += kBlock) s_sptr[i] = __ldcs(sptr + d0 + i) - sbase;
+  for (int i = threadIdx.x; i < nd; i += kBlock) s_out[i] = __ldcs(lout + d0 + i);
+  for (int i = threadIdx.x; i < nsl; i += kBlock) s_slot[i] = __ldcs(slots + sbase + i);
+  const bool same = x == v;
+  if constexpr (NL == 4) {
+    // stage the block-dofs' coordinates and x (v) values once per dof; the
+    // element phase then reads them through the tets' 16-bit block-local ids
+    double* s_v = same ? s_x : s_x + max_dofs;
+    for (int i = threadIdx.x; i < nd; i += kBlock) {
+      const int gd = __ldcs(ldof_dof + d0 + i);
+      double p[3];
+      load_xyz(coords, gd, p);
+      s_xyz[3 * i] = p[0];
+      s_xyz[3 * i + 1] = p[1];
+      s_xyz[3 * i + 2] = p[2];
+      s_x[i] = __ldg(x + gd);
+      if (!same) s_v[i] = __ldg(v + gd);
+    }
+    __syncthreads();
+    const ushort4* tt = reinterpret_cast<const ushort4*>(tets) + t0;
+    for (int tl = threadIdx.x; tl < nt; tl += kBlock) {
+      const ushort4 n = __ldcs(tt + tl);
+      const int li[4] = {n.x, n.y, n.z, n.w};
+      double p[4][3], xl[4], vl[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) p[k][d] = s_xyz[3 * li[k] + d];
+        xl[k] = s_x[li[k]];
+        vl[k] = s_v[li[k]];
+      }
+      double y[4];
+      p1_compute(p, xl, vl, same, __ldcs(mat + t0 + tl), y, err);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ysm[i * max_tets + tl] = y[i];
+    }
+  } else {
+    for (int tl = threadIdx.x; tl < nt; tl += kBlock) {
+      const long t = (long)t0 + tl;
+      int dofs[10];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) dofs[i] = __ldg(tets + 10L * t + i);
+      double y[10];
+      p2_local(dofs, mat[t], coords, x, v, same, y, err);
+#pragma unroll
+      for (int i = 0; i < 10; ++i) ysm[i * max_tets + tl] = y[i];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nd; e += kBlock) {
+    double s = 0.0;
+    const int k1 = s_sptr[e + 1];
+    for (int k = s_sptr[e]; k < k1; ++k) s += ysm[s_slot[k]];
+    const int o = s_out[e];
+    if (o >= 0) {
+      if (o < n_out) out[o] = base ? base[o] + sign * s : sign * s;
+    } else {
+      partials[-o - 1] = s;
+    }
+  }
+}
+
+// pass 2: boundary dofs, partials summed in block order
+__global__ void __launch_bounds__(kBlock) k_kx_partials(int nb, const int* __restrict__ bdof,
+                                                        const int* __restrict__ bptr, const int* __restrict__ bpart,
+                                                        const double* __restrict__ partials,
+                                                        const double* __restrict__ base, double sign, int n_out,
+                                                        double* __restrict__ out) {
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= nb) return;
+  const int d = bdof[i];
+  if (d >= n_out) return;
+  double s = 0.0;
+  for (int k = bptr[i]; k < bptr[i + 1]; ++k) s += partials[bpart[k]];
+  out[d] = base ? base[d] + sign * s : sign * s;
+}
+
 }  // namespace
+
+void launch_kx_blocked(const KxDev& k, const double* coords, const double* x_state, const double* v,
+                       const double* base, double sign, int n_out, double* out, int* geo_error, cudaStream_t s) {
+  if (k.n_blocks == 0) return;
+  g_launch_count += 2;
+  size_t smem = sizeof(double) * k.nl * k.max_block_tets + sizeof(int) * (2L * k.max_block_dofs + 1) +
+                sizeof(uint16_t) * k.max_block_slots + 16;
+  if (k.nl == 4) smem += sizeof(double) * 5L * k.max_block_dofs;  // staged coordinates, x, v
+  if (k.nl == 4) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_kx_block<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    k_kx_block<4><<<k.n_blocks, kBlock, smem, s>>>(k.blk_tet0, k.tets, k.mat, coords, x_state, v, k.blk_dof0, k.sptr,
+                                                   k.slots, k.lout, k.partials, base, sign, n_out, out, geo_error,
+                                                   k.max_block_tets, k.max_block_dofs, k.max_block_slots, k.ldof_dof);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_kx_block<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    k_kx_block<10><<<k.n_blocks, kBlock, smem, s>>>(k.blk_tet0, k.tets, k.mat, coords, x_state, v, k.blk_dof0,
+                                                    k.sptr, k.slots, k.lout, k.partials, base, sign, n_out, out,
+                                                    geo_error, k.max_block_tets, k.max_block_dofs, k.max_block_slots, k.ldof_dof);
+  }
+  if (k.n_bdof > 0)
+    k_kx_partials<<<(k.n_bdof + kBlock - 1) / kBlock, kBlock, 0, s>>>(k.n_bdof, k.bdof, k.bptr, k.bpart, k.partials,
+                                                                      base, sign, n_out, out);
+}
 
 void set_materials(const DevMaterial* mats, int n, cudaStream_t s) {
   cudaMemcpyToSymbolAsync(c_mat, mats, sizeof(DevMaterial) * n, 0, cudaMemcpyHostToDevice, s);

@@ -63,16 +63,29 @@ def test_residual_matches_oracle():  # test_matfree.cpp:89-104
     assert np.abs(r - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
 
 
-def test_coloured_and_gather_modes_agree():
-    cfg = cube(6, jitter=0.1)
+@pytest.mark.parametrize("order", [1, 2])
+def test_scatter_modes_agree(order):
+    """blocked (default), coloured and two-pass gather scatters of K1 agree to
+    rounding and each is bit-reproducible (fixed summation orders)."""
+    cfg = cube(10, jitter=0.1)
+    cfg["order"] = order
     g = eb.FemSystem(cfg)
     x = 1e5 * po.random_vec(g.n_dofs, 3)
     v = po.random_vec(g.n_dofs, 4)
-    y_gather = g.kx_apply(x, v)
+    y_block = g.kx_apply(x, v)
+    assert np.array_equal(y_block, g.kx_apply(x, v))
     g.set_option(0, 1)
     y_col = g.kx_apply(x, v)
-    assert rel_inf(y_col, y_gather) <= 1e-13
-    assert np.array_equal(y_col, g.kx_apply(x, v))  # coloured scatter has a fixed order
+    assert rel_inf(y_col, y_block) <= 1e-13
+    assert np.array_equal(y_col, g.kx_apply(x, v))
+    g.set_option(0, 2)
+    y_gather = g.kx_apply(x, v)
+    assert rel_inf(y_gather, y_block) <= 1e-13
+    assert np.array_equal(y_gather, g.kx_apply(x, v))
+    g.set_option(0, 0)
+    r_block = g.kx_residual(x, y_block[:g.n_free])
+    g.set_option(0, 2)
+    assert rel_inf(g.kx_residual(x, y_block[:g.n_free]), r_block) <= 1e-13
 
 
 def test_mass_solve_matches_oracle():
