@@ -393,17 +393,20 @@ def run_b200(args):
     iters = st1["pcg_iterations"] - st0["pcg_iterations"]
     value = n * f_evals / (ms / 1e3)  # n = global free dofs: all ranks together
 
-    # e2e: the same step through the public API with host buffers (H2D state in, D2H state out)
-    x_host, _ = g.get_state()
+    # e2e: the same step through the public API with host buffers: every step
+    # copies the state in from pinned host memory (H2D) and back out (D2H)
+    x_host = torch.empty(g.n_own, dtype=torch.float64, pin_memory=True).numpy()
+    g.get_state(out=x_host)
+    t_host = g.get_state(want_x=False)[1]["t"]
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     e0 = time.perf_counter()
     e_steps = max(1, min(args.steps, 5))
     for _ in range(e_steps):
-        g.set_state(g.get_state()[1]["t"], x_host, dt)
+        g.set_state(t_host, x_host, dt)
         g.rkc_advance_fixed(dt, S_STAGES, 1)
-        x_host, _ = g.get_state()
+        t_host = g.get_state(out=x_host)[1]["t"]
     e_wall = time.perf_counter() - e0
     if dist:
         t = torch.tensor([e_wall], device="cuda")

@@ -56,6 +56,7 @@ struct DevSell {
 // 32-bit word, 16-byte groups; tpr == 0: absent.
 struct DevSellP {
   int tpr = 0, n_chunks = 0, shift = 13, windows = 8;
+  int uniform = 0;                  // > 0: steps of every chunk (no chunk-pointer load)
   long padded = 0;                  // stored entries (nnz + padding)
   const int* chunk_ptr = nullptr;   // [n_chunks + 1] in 16-byte groups
   const int* bases = nullptr;       // [n_chunks][windows]

@@ -156,6 +156,7 @@ void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.pk.n_chunks = hp.n_chunks;
   d.pk.shift = hp.shift;
   d.pk.windows = hp.windows;
+  d.pk.uniform = hp.uniform;
   d.pk.padded = hp.padded();
   d.pk.chunk_ptr = b.pk_cp.p;
   d.pk.bases = b.pk_bases.p;

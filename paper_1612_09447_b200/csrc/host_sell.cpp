@@ -135,8 +135,19 @@ bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out) {
       }
     }
     if (fail) continue;
+    // uniform chunks when padding every chunk to the longest costs <= 5% more entries
+    long tot = 0;
+    int smax = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      tot += len[c + 1];
+      smax = std::max(smax, len[c + 1] / 32);
+    }
+    const bool uni = smax > 0 && (double)smax * 32 * n_chunks <= 1.05 * (double)tot;
+    if (uni)
+      for (int c = 0; c < n_chunks; ++c) len[c + 1] = 32 * smax;
     for (int c = 0; c < n_chunks; ++c) len[c + 1] += len[c];
     HostSellP s;
+    s.uniform = uni ? smax : 0;
     s.tpr = tpr;
     s.n_rows = a.n_rows;
     s.n_chunks = n_chunks;

@@ -135,8 +135,8 @@ __device__ __forceinline__ T ldvec(const T* p) {
 template <int TPR, class XT, bool SCALED, bool CG = false>
 __device__ __forceinline__ XT sellp_dot(const DevSellP& m, int chunk, int lane, const XT* __restrict__ x,
                                         const XT* __restrict__ w) {
-  const int beg = __ldg(m.chunk_ptr + chunk);
-  const int S = (__ldg(m.chunk_ptr + chunk + 1) - beg) >> 5;  // steps (warp-uniform)
+  const int beg = m.uniform ? chunk * m.uniform * 32 : __ldg(m.chunk_ptr + chunk);
+  const int S = m.uniform ? m.uniform : (__ldg(m.chunk_ptr + chunk + 1) - beg) >> 5;  // steps (warp-uniform)
   const int mybase = lane < m.windows ? __ldg(m.bases + (long)m.windows * chunk + lane) : 0;
   const unsigned mask = (1u << m.shift) - 1u;
   const int shift = m.shift;

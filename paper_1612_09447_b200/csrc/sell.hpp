@@ -61,6 +61,8 @@ constexpr int kPackGroup = 4;
 
 struct HostSellP {
   int tpr = 0, n_rows = 0, n_chunks = 0, shift = 13, windows = 8;
+  int uniform = 0;  // > 0: every chunk has this many steps (chunk c starts at c * uniform * 32):
+                    // the kernels skip the chunk-pointer load (one dependent round trip less)
   std::vector<int> chunk_ptr;    // [n_chunks + 1] offsets in 16-byte groups (multiples of 32)
   std::vector<int> bases;        // [n_chunks][windows]
   std::vector<uint32_t> words;   // 4 * chunk_ptr.back() packed entries (padding: 0)

@@ -360,11 +360,18 @@ class FemSystem:
     def set_state(self, t: float, x, dt: float = 0.0):
         _check(load_library().eqs_set_state(self._h, C.c_double(t), _dp(_f64(x)), C.c_double(dt)))
 
-    def get_state(self):
-        """Owned part of the resident state (all free dofs on a single rank)."""
-        x = np.zeros(self.n_own)
+    def get_state(self, out=None, want_x: bool = True):
+        """Owned part of the resident state (all free dofs on a single rank).
+        out: optional preallocated float64 array (e.g. pinned host memory) that
+        receives x; want_x=False returns (None, info) without the copy."""
+        if want_x:
+            x = np.zeros(self.n_own) if out is None else out
+            if x.dtype != np.float64 or not x.flags.c_contiguous or x.size < self.n_own:
+                raise ValueError("get_state: out must be a contiguous float64 array of n_own entries")
+        else:
+            x = None
         info = _StateInfo()
-        _check(load_library().eqs_get_state(self._h, _dp(x), C.byref(info)))
+        _check(load_library().eqs_get_state(self._h, _dp(x) if want_x else None, C.byref(info)))
         return x, {n: getattr(info, n) for n, _ in _StateInfo._fields_}
 
     def set_rho(self, value: float, valid: bool = True, age: int = 0):

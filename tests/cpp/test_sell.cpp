@@ -101,9 +101,11 @@ int main() {
       const bool ok16 = build_sell(a, tpr, h);
       const int fp = okp ? check_packed(a, p) : 0;
       const int f16 = ok16 ? check_sell16(a, h) : 0;
-      printf("len %3d spread %6d tpr %2d packed %d (shift %d, padded %ld / nnz %ld) sell16 %d -> %s\n", lens[li],
-             spreads[si], tpr, okp, p.shift, p.padded(), a.nnz(), ok16, fp || f16 ? "FAIL" : "ok");
+      printf("len %3d spread %6d tpr %2d packed %d (shift %d, uniform %d, padded %ld / nnz %ld) sell16 %d -> %s\n",
+             lens[li], spreads[si], tpr, okp, p.shift, p.uniform, p.padded(), a.nnz(), ok16, fp || f16 ? "FAIL" : "ok");
       fails += fp + f16;
+      if (okp && lens[li] == 15 && p.uniform != 4) ++fails, printf("fine-level-like rows should be uniform\n");
+      if (okp && p.uniform && p.padded() != 128L * p.uniform * p.n_chunks) ++fails, printf("uniform size\n");
       if (!okp && spreads[si] <= 30000) ++fails, printf("packed encoding unexpectedly failed\n");
     }
   // clustered columns (restriction-like rows: a few node planes each): 12
