@@ -289,7 +289,7 @@ def mrhs_rhs(g, n_rhs=40):
 
 def run_mrhs(args):
     """Config 5: the 40-RHS sequence solved to 1e-12 with zero / previous /
-    SPE(8) start vectors, inputs resident (eqs_mass_solve_sequence)."""
+    SPE(8) / POD start vectors, inputs resident (eqs_mass_solve_sequence)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -297,7 +297,10 @@ def run_mrhs(args):
     X, B = mrhs_rhs(g)
     n = g.n_free
     res = {}
-    for mode, key in (("zero", 0), ("previous", 1), ("spe", 2)):
+    # POD modes (start_vector.cpp:111-131): pod_fixed builds its rank-10 basis
+    # from the first 8 solutions, pod_rolling keeps a ring of 20 (reference default)
+    g.set_option(15, 8)
+    for mode, key in (("zero", 0), ("previous", 1), ("spe", 2), ("pod_fixed", 3), ("pod_rolling", 4)):
         g.set_option(12, key)
         g.mass_solve_sequence(B[:4])  # warm-up (graphs, buffers)
         g.set_option(12, key)
@@ -313,6 +316,8 @@ def run_mrhs(args):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"M_II of {args.config} ({n} free dofs), b_k = M_II x*_k, k = 0..39"},
             "spe_iters_vs_zero": res["spe"]["iters_total"] / res["zero"]["iters_total"],
+            "pod_fixed_iters_vs_zero": res["pod_fixed"]["iters_total"] / res["zero"]["iters_total"],
+            "pod_rolling_iters_vs_zero": res["pod_rolling"]["iters_total"] / res["zero"]["iters_total"],
             "setup_s": t_setup, **res}
     print(json.dumps(line), flush=True)
 

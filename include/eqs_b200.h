@@ -62,12 +62,17 @@ typedef struct {
   int amg_smoother_sweeps;       /* 1 (GPU: Chebyshev degree 2 pre and post) */
   int amg_max_levels;            /* 10 */
   int amg_coarse_limit;          /* 64 */
-  int estimator_mode;     /* 0 = zero, 1 = previous, 2 = spe */
+  int estimator_mode;     /* 0 = zero, 1 = previous, 2 = spe, 3 = pod_fixed, 4 = pod_rolling */
   int spe_window;         /* 8 */
   double mgs_drop_tol;    /* 1e-8 */
   double amg_coarse_filter; /* additive: V-cycle coarse-operator filter eps (0 = off; configs default 0.0025) */
   int amg_dense_coarse;     /* additive: direct (dense) solve of the first coarse level with at most this many
                                rows in the device V-cycle; <= 0 (default) = recurse to the coarsest */
+  /* start_vector.hpp:31-35 (POD modes); <= 0 selects the reference default */
+  int pod_snapshots;        /* 40: pod_fixed solves collected before the basis is built */
+  int pod_rank;             /* 10 */
+  int pod_capacity;         /* 20: pod_rolling ring size */
+  double pod_threshold;     /* pod_rolling: append when iterations exceed this; <= 0: 1.25 x running median */
 } eqs_solver_params;
 
 /* Problem description consumed by eqs_create: the arrays the reference's
@@ -118,6 +123,7 @@ typedef struct {
   double time_residual, time_solve, time_setup, time_estimator;
   long applies;              /* MatFreeStiffness::applies() (matfree.hpp:43) */
   long spe_fallbacks;
+  long estimator_appends;    /* StartVectorEstimator::Stats::appends (start_vector.hpp:47) */
 } eqs_solve_stats;
 
 /* proj/include/eqs/integrators.hpp:91-95 */
@@ -233,6 +239,13 @@ int eqs_mass_solve_sequence(eqs_ctx* ctx, const double* B, int k, double tol, in
 
 /* ----------------------------------------------------------------- OdeSystem (proj/include/eqs/ode_system.hpp:45-73) */
 /* FemSystem::eval_residual (fem_system.cpp:62-67). */
+/* StartVectorEstimator::next(M_II, b) / feedback(x, iterations) / current_rank()
+ * (proj/include/eqs/start_vector.hpp:52-66, proj/src/start_vector.cpp:84-187) on
+ * the context's own estimator. Host vectors of n_free; x0 is zero when the
+ * estimator has no basis yet. Single-rank contexts. */
+int eqs_estimator_next(eqs_ctx* ctx, const double* b, double* x0, int* rank);
+int eqs_estimator_feedback(eqs_ctx* ctx, const double* x, int iterations);
+
 int eqs_eval_residual(eqs_ctx* ctx, double t, const double* x, double* r);
 /* FemSystem::eval_rhs (fem_system.cpp:69-99): f = M^-1 (b - K(x)x); throws
  * NumericalError (returns EQS_ERR_NUMERICAL) when the mass solve fails. */
@@ -282,7 +295,10 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * (0 fp64, 1 fp32, 2 bf16; default 2), 5/6/7 = CSR threads per row of levels
  * 0/1/2, 8 = CUDA graphs (0/1), 9 = incremental SPE (0/1), 10 = SELL-16
  * operators (0/1; default 1), 11 = fp32 V-cycle vectors (0/1; default 1),
- * 12 = start-vector estimator (0 zero, 1 previous, 2 spe; resets its history),
+ * 12 = start-vector estimator (0 zero, 1 previous, 2 spe, 3 pod_fixed, 4 pod_rolling;
+ * resets its history), 15/16/17/18 = POD snapshots / rank / capacity / threshold
+ * (estimator config keys "snapshots", "rank", "capacity", "threshold"; take effect
+ * at the next reset),
  * 13 = smoother polynomial (0 first-kind Chebyshev, 1 fourth-kind, 2 fourth-kind
  * with optimised weights), 14 = lambda_max safety factor (default 1.1).
  * The PCG operator and vectors are fp64 in every setting. */

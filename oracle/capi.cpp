@@ -300,7 +300,7 @@ int ora_euler_step(void* h, double t, double* x, double dt) {
   });
 }
 
-// stats: m_solves, pcg_iterations, rho_solves, rho_pcg_iterations, precond_setups, assemblies, applies
+// stats: m_solves, pcg_iterations, rho_solves, rho_pcg_iterations, precond_setups, assemblies, applies, svd_count
 int ora_stats(void* h, long* out, double* timers) {
   return guard([&] {
     auto* p = static_cast<Problem*>(h);
@@ -312,6 +312,7 @@ int ora_stats(void* h, long* out, double* timers) {
     out[4] = s.precond_setups;
     out[5] = s.assemblies;
     out[6] = p->sys->stiffness_operator().applies();
+    out[7] = s.svd_count;
     if (timers) {
       timers[0] = s.timers.residual;
       timers[1] = s.timers.solve;
@@ -402,6 +403,47 @@ int ora_element_laplacian(const double* coords /*12*/, int order, const double* 
   });
 }
 
+
+// StartVectorEstimator public API (proj/include/eqs/start_vector.hpp:52-66) on
+// the problem's own estimator and M_II: next(m, b), feedback(x, iterations),
+// current_rank(), stats() = {svd_count, appends, spe_fallbacks}.
+int ora_estimator_next(void* h, const double* b, double* x0, int* rank) {
+  return guard([&] {
+    auto* p = static_cast<Problem*>(h);
+    const int n = p->sys->size();
+    const Vec bv(b, b + n);
+    const Vec x = p->sys->estimator().next(p->sys->mass_free(), bv);
+    std::memcpy(x0, x.data(), sizeof(double) * n);
+    if (rank) *rank = p->sys->estimator().current_rank();
+  });
+}
+int ora_estimator_feedback(void* h, const double* x, int iterations) {
+  return guard([&] {
+    auto* p = static_cast<Problem*>(h);
+    p->sys->estimator().feedback(Vec(x, x + p->sys->size()), iterations);
+  });
+}
+int ora_estimator_stats(void* h, long* out3) {
+  return guard([&] {
+    const auto& st = static_cast<Problem*>(h)->sys->estimator().stats();
+    out3[0] = st.svd_count;
+    out3[1] = st.appends;
+    out3[2] = st.spe_fallbacks;
+  });
+}
+// pod_build (start_vector.cpp:64-71) on k snapshots of length n (row-major
+// [k][n]); writes up to `rank` basis vectors [keep][n] and all k singular values.
+int ora_pod_build(int n, int k, const double* snaps, int rank, double* basis, int* keep, double* sigma) {
+  return guard([&] {
+    std::vector<Vec> s(k);
+    for (int j = 0; j < k; ++j) s[j].assign(snaps + (size_t)j * n, snaps + (size_t)(j + 1) * n);
+    std::vector<double> sv;
+    const std::vector<Vec> u = pod_build(s, rank, &sv);
+    *keep = (int)u.size();
+    for (size_t j = 0; j < u.size(); ++j) std::memcpy(basis + j * n, u[j].data(), sizeof(double) * n);
+    if (sigma) std::memcpy(sigma, sv.data(), sizeof(double) * sv.size());
+  });
+}
 }  // extern "C"
 
 extern "C" {

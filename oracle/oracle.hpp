@@ -266,27 +266,55 @@ class AmgPreconditioner final : public LinearOperator {
 };
 
 // ---------------------------------------------------------------- start vectors
-enum class EstimatorMode { Zero, Previous, Spe };
+// proj/include/eqs/start_vector.hpp:25-38
+enum class EstimatorMode { Zero, Previous, Spe, PodFixed, PodRolling };
 const char* estimator_mode_name(EstimatorMode m);
 struct EstimatorParams {
   EstimatorMode mode = EstimatorMode::Zero;
   int spe_window = 8;
+  int pod_snapshots = 40;    // PodFixed: solves collected before the basis is built
+  int pod_rank = 10;
+  int pod_capacity = 20;     // PodRolling: ring size
+  double pod_threshold = 0;  // PodRolling: append when iterations exceed this; <= 0: 1.25x running median
   double mgs_drop_tol = 1e-8;
 };
 std::vector<Vec> mgs_orthonormalize(const std::vector<Vec>& vectors, double drop_tol);
 Vec spe_start(const std::vector<Vec>& v, const CsrMatrix& m, const Vec& b, bool* ok);
+// proj/src/start_vector.cpp:64-71: dominant left singular vectors of the
+// snapshot matrix (columns), at most `rank`, truncated at sigma <= 1e-12 sigma_0.
+// The reference uses Eigen::JacobiSVD; this is a one-sided (Hestenes) Jacobi
+// SVD, which yields the same singular values and (up to sign) vectors.
+std::vector<Vec> pod_build(const std::vector<Vec>& snapshots, int rank, std::vector<double>* sigma = nullptr);
 class StartVectorEstimator {
  public:
+  struct Stats {  // start_vector.hpp:45-49
+    long svd_count = 0;
+    long appends = 0;
+    long spe_fallbacks = 0;
+  };
   explicit StartVectorEstimator(const EstimatorParams& p) : params_(p) {}
   Vec next(const CsrMatrix& m, const Vec& b);
   void feedback(const Vec& x, int iterations);
   EstimatorMode mode() const { return params_.mode; }
   int current_rank() const { return basis_rank_; }
+  const Stats& stats() const { return stats_; }
   long spe_fallbacks = 0;
  private:
+  Vec pod_start(const CsrMatrix& m, const Vec& b);
+  void factor_reduced(const CsrMatrix& m);
+  double rolling_threshold() const;
   EstimatorParams params_;
+  Stats stats_;
   std::deque<Vec> history_;
   int basis_rank_ = 0;
+  std::vector<Vec> snapshots_;
+  int rolling_next_slot_ = 0;
+  bool basis_stale_ = false;
+  bool fixed_basis_built_ = false;
+  std::vector<Vec> basis_;              // POD basis V
+  std::vector<double> reduced_inverse_;  // (V'MV)^-1, row-major
+  bool reduced_ok_ = false;
+  std::vector<int> iteration_history_;
 };
 
 // ---------------------------------------------------------------- system

@@ -260,15 +260,44 @@ class Problem:
         _check(lib().ora_euler_step(self._h, C.c_double(t), _ptr(x), C.c_double(dt)))
         return x
 
+    def estimator_next(self, b):
+        """StartVectorEstimator::next(M_II, b) -> (x0, current_rank) (start_vector.cpp:84-109)."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x0 = np.zeros_like(b)
+        rank = C.c_int(0)
+        _check(lib().ora_estimator_next(self._h, _ptr(b), _ptr(x0), C.byref(rank)))
+        return x0, rank.value
+
+    def estimator_feedback(self, x, iterations: int):
+        """StartVectorEstimator::feedback (start_vector.cpp:152-187)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        _check(lib().ora_estimator_feedback(self._h, _ptr(x), C.c_int(int(iterations))))
+
+    def estimator_stats(self) -> dict:
+        s = np.zeros(3, dtype=np.int64)
+        _check(lib().ora_estimator_stats(self._h, _ptr(s, C.c_long)))
+        return dict(zip(("svd_count", "appends", "spe_fallbacks"), (int(v) for v in s)))
+
     def stats(self):
-        s = np.zeros(7, dtype=np.int64)
+        s = np.zeros(8, dtype=np.int64)
         tm = np.zeros(4)
         _check(lib().ora_stats(self._h, _ptr(s, C.c_long), _ptr(tm)))
         keys = ("m_solves", "pcg_iterations", "rho_solves", "rho_pcg_iterations", "precond_setups",
-                "assemblies", "applies")
+                "assemblies", "applies", "svd_count")
         d = {k: int(v) for k, v in zip(keys, s)}
         d["timers"] = dict(zip(("residual", "solve", "setup", "estimator"), tm.tolist()))
         return d
+
+
+def pod_build(snapshots, rank: int):
+    """pod_build (start_vector.cpp:64-71): snapshots [k][n] -> (basis [keep][n], sigma [k])."""
+    S = np.ascontiguousarray(snapshots, dtype=np.float64)
+    k, n = S.shape
+    U = np.zeros((min(rank, k), n))
+    sig = np.zeros(k)
+    keep = C.c_int(0)
+    _check(lib().ora_pod_build(C.c_int(n), C.c_int(k), _ptr(S), C.c_int(rank), _ptr(U), C.byref(keep), _ptr(sig)))
+    return U[:keep.value].copy(), sig
 
 
 def amg_level_csr(problem: "Problem", level: int, which: int = 0):

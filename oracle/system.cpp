@@ -100,13 +100,142 @@ Vec spe_start(const std::vector<Vec>& v, const CsrMatrix& m, const Vec& b, bool*
   return x0;
 }
 
+namespace {
+// (V'MV)^-1 (start_vector.cpp:33-50): pivoted LDLT, singular when d_min <= 1e-14 d_max
+bool reduced_mass_inverse(const std::vector<Vec>& v, const CsrMatrix& m, std::vector<double>& ginv) {
+  const int rank = (int)v.size();
+  std::vector<Vec> w(rank);
+  for (int c = 0; c < rank; ++c) m.apply(v[c], w[c]);
+  std::vector<double> g((size_t)rank * rank);
+  for (int i = 0; i < rank; ++i)
+    for (int j = 0; j < rank; ++j) g[(size_t)i * rank + j] = dot(v[i], w[j]);
+  DenseLdlt ldlt;
+  ldlt.compute(g, rank);
+  double dmax = 0.0, dmin = INFINITY;
+  for (double d : ldlt.d) {
+    dmax = std::max(dmax, std::abs(d));
+    dmin = std::min(dmin, d);
+  }
+  if (!(ldlt.ok && dmax > 0.0 && dmin > 1e-14 * dmax)) return false;
+  ginv.assign((size_t)rank * rank, 0.0);
+  std::vector<double> e(rank), col(rank);
+  for (int c = 0; c < rank; ++c) {
+    std::fill(e.begin(), e.end(), 0.0);
+    e[c] = 1.0;
+    ldlt.solve(e.data(), col.data());
+    for (int r = 0; r < rank; ++r) ginv[(size_t)r * rank + c] = col[r];
+  }
+  return true;
+}
+}  // namespace
+
+// proj/src/start_vector.cpp:64-71 (Eigen::JacobiSVD(snapshots, ComputeThinU)).
+// One-sided Jacobi: rotate column pairs until they are mutually orthogonal;
+// then sigma_j = |a_j| and u_j = a_j / sigma_j.
+std::vector<Vec> pod_build(const std::vector<Vec>& snapshots, int rank, std::vector<double>* sigma_out) {
+  std::vector<Vec> a = snapshots;
+  const int k = (int)a.size();
+  if (k == 0) return {};
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    bool rotated = false;
+    for (int p = 0; p < k; ++p)
+      for (int q = p + 1; q < k; ++q) {
+        const double al = dot(a[p], a[p]), be = dot(a[q], a[q]), ga = dot(a[p], a[q]);
+        if (ga == 0.0 || std::abs(ga) <= 1e-15 * std::sqrt(al * be)) continue;
+        rotated = true;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), s = c * t;
+        for (size_t i = 0; i < a[p].size(); ++i) {
+          const double x = a[p][i], y = a[q][i];
+          a[p][i] = c * x - s * y;
+          a[q][i] = s * x + c * y;
+        }
+      }
+    if (!rotated) break;
+  }
+  std::vector<std::pair<double, int>> sv(k);
+  for (int j = 0; j < k; ++j) sv[j] = {norm(a[j]), j};
+  std::stable_sort(sv.begin(), sv.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+  if (sigma_out) {
+    sigma_out->clear();
+    for (auto& e : sv) sigma_out->push_back(e.first);
+  }
+  std::vector<Vec> u;
+  if (sv[0].first == 0.0) return u;
+  for (int j = 0; j < k && j < rank && sv[j].first > 1e-12 * sv[0].first; ++j) {
+    Vec c = a[sv[j].second];
+    for (double& e : c) e /= sv[j].first;
+    u.push_back(std::move(c));
+  }
+  return u;
+}
+
 const char* estimator_mode_name(EstimatorMode m) {
   switch (m) {
     case EstimatorMode::Zero: return "zero";
     case EstimatorMode::Previous: return "previous";
     case EstimatorMode::Spe: return "spe";
+    case EstimatorMode::PodFixed: return "pod_fixed";
+    case EstimatorMode::PodRolling: return "pod_rolling";
   }
   return "?";
+}
+
+// proj/src/start_vector.cpp:111-131
+Vec StartVectorEstimator::pod_start(const CsrMatrix& m, const Vec& b) {
+  if (params_.mode == EstimatorMode::PodFixed && !fixed_basis_built_ &&
+      (int)snapshots_.size() >= params_.pod_snapshots) {
+    basis_ = pod_build(snapshots_, params_.pod_rank);
+    ++stats_.svd_count;
+    fixed_basis_built_ = true;
+    factor_reduced(m);
+  }
+  if (params_.mode == EstimatorMode::PodRolling && basis_stale_ && !snapshots_.empty()) {
+    basis_ = pod_build(snapshots_, params_.pod_rank);
+    ++stats_.svd_count;
+    basis_stale_ = false;
+    factor_reduced(m);
+  }
+  basis_rank_ = (int)basis_.size();
+  if (basis_.empty() || !reduced_ok_) return Vec(b.size(), 0.0);
+  const int r = (int)basis_.size();
+  std::vector<double> vtb(r), y(r, 0.0);
+  for (int c = 0; c < r; ++c) vtb[c] = dot(basis_[c], b);
+  for (int i = 0; i < r; ++i) {
+    double s = 0.0;
+    for (int c = 0; c < r; ++c) s += reduced_inverse_[(size_t)i * r + c] * vtb[c];
+    y[i] = s;
+  }
+  Vec x0(b.size(), 0.0);
+  for (size_t i = 0; i < b.size(); ++i) {
+    double s = 0.0;
+    for (int c = 0; c < r; ++c) s += basis_[c][i] * y[c];
+    x0[i] = s;
+  }
+  return x0;
+}
+
+// proj/src/start_vector.cpp:133-141
+void StartVectorEstimator::factor_reduced(const CsrMatrix& m) {
+  reduced_ok_ = !basis_.empty();
+  if (!reduced_ok_) return;
+  reduced_ok_ = reduced_mass_inverse(basis_, m, reduced_inverse_);
+  if (!reduced_ok_) {
+    ++stats_.spe_fallbacks;
+    ++spe_fallbacks;
+    std::fprintf(stderr, "start_vector: singular reduced system, zero start used\n");
+  }
+}
+
+// proj/src/start_vector.cpp:143-150
+double StartVectorEstimator::rolling_threshold() const {
+  if (params_.pod_threshold > 0.0) return params_.pod_threshold;
+  if (iteration_history_.empty()) return -1.0;
+  std::vector<int> h = iteration_history_;
+  const size_t mid = h.size() / 2;
+  std::nth_element(h.begin(), h.begin() + mid, h.end());
+  return 1.25 * (double)h[mid];
 }
 
 // proj/src/start_vector.cpp:84-109
@@ -123,15 +252,19 @@ Vec StartVectorEstimator::next(const CsrMatrix& m, const Vec& b) {
       Vec x0 = spe_start(v, m, b, &ok);
       if (!ok) {
         ++spe_fallbacks;
+        ++stats_.spe_fallbacks;
         std::fprintf(stderr, "start_vector: singular reduced system, zero start used\n");
       }
       return x0;
     }
+    case EstimatorMode::PodFixed:
+    case EstimatorMode::PodRolling:
+      return pod_start(m, b);
   }
   return Vec(b.size(), 0.0);
 }
-// proj/src/start_vector.cpp:152-164
-void StartVectorEstimator::feedback(const Vec& x, int) {
+// proj/src/start_vector.cpp:152-187
+void StartVectorEstimator::feedback(const Vec& x, int iterations) {
   switch (params_.mode) {
     case EstimatorMode::Zero: break;
     case EstimatorMode::Previous:
@@ -141,8 +274,30 @@ void StartVectorEstimator::feedback(const Vec& x, int) {
     case EstimatorMode::Spe:
       history_.push_back(x);
       while ((int)history_.size() > params_.spe_window) history_.pop_front();
+      ++stats_.appends;
       break;
+    case EstimatorMode::PodFixed:
+      if (!fixed_basis_built_ && (int)snapshots_.size() < params_.pod_snapshots) {
+        snapshots_.push_back(x);
+        ++stats_.appends;
+      }
+      break;
+    case EstimatorMode::PodRolling: {
+      const double thr = rolling_threshold();
+      if ((double)iterations > thr) {
+        if ((int)snapshots_.size() < params_.pod_capacity) {
+          snapshots_.push_back(x);
+        } else {
+          snapshots_[rolling_next_slot_] = x;  // overwrite the oldest
+          rolling_next_slot_ = (rolling_next_slot_ + 1) % params_.pod_capacity;
+        }
+        ++stats_.appends;
+        basis_stale_ = true;
+      }
+      break;
+    }
   }
+  iteration_history_.push_back(iterations);
 }
 
 // proj/src/fem_system.cpp:27-36
@@ -209,6 +364,7 @@ void FemSystem::eval_rhs(double t, const Vec& x, Vec& f) {
     PhaseTimer timer(stats_.timers.estimator);
     estimator_.feedback(res.x, res.iterations);
   }
+  stats_.svd_count = estimator_.stats().svd_count;  // fem_system.cpp:94
   ++stats_.m_solves;
   stats_.pcg_iterations += res.iterations;
   solve_records_.push_back({t, estimator_mode_name(estimator_.mode()), estimator_.current_rank(), res.iterations,

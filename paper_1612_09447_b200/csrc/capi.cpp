@@ -74,6 +74,10 @@ SolverParams solver_from(const eqs_solver_params& s) {
   p.estimator_mode = s.estimator_mode;
   p.spe_window = s.spe_window;
   p.mgs_drop_tol = s.mgs_drop_tol;
+  if (s.pod_snapshots > 0) p.pod_snapshots = s.pod_snapshots;
+  if (s.pod_rank > 0) p.pod_rank = s.pod_rank;
+  if (s.pod_capacity > 0) p.pod_capacity = s.pod_capacity;
+  p.pod_threshold = s.pod_threshold;
   p.amg_coarse_filter = s.amg_coarse_filter;
   p.amg_dense_coarse = s.amg_dense_coarse;
   return p;
@@ -94,6 +98,8 @@ void fill_stats(GpuSystem& g, eqs_solve_stats* o) {
   o->time_estimator = s.t_estimator;
   o->applies = s.applies;
   o->spe_fallbacks = s.spe_fallbacks;
+  o->svd_count = s.svd_count;
+  o->estimator_appends = s.appends;
 }
 
 void fill_pcg(const PcgResult& r, eqs_pcg_result* o) {
@@ -398,6 +404,19 @@ int eqs_mass_solve_sequence(eqs_ctx* ctx, const double* B, int k, double tol, in
     if (device_ms) *device_ms = ms;
   });
 }
+int eqs_estimator_next(eqs_ctx* ctx, const double* b, double* x0, int* rank) {
+  return guard([&] {
+    if (!b || !x0) throw std::invalid_argument("eqs_estimator_next: null vector");
+    const int r = S(ctx).estimator_next_host(b, x0);
+    if (rank) *rank = r;
+  });
+}
+int eqs_estimator_feedback(eqs_ctx* ctx, const double* x, int iterations) {
+  return guard([&] {
+    if (!x) throw std::invalid_argument("eqs_estimator_feedback: null vector");
+    S(ctx).estimator_feedback_host(x, iterations);
+  });
+}
 int eqs_eval_residual(eqs_ctx* ctx, double t, const double* x, double* r) {
   return guard([&] { S(ctx).eval_residual_host(t, x, r); });
 }
@@ -506,6 +525,9 @@ int eqs_run_scenario(const char* json_text, const char* out_dir, int device, eqs
     res->stats.time_setup = r.stats.t_setup;
     res->stats.time_estimator = r.stats.t_estimator;
     res->stats.applies = r.stats.applies;
+    res->stats.spe_fallbacks = r.stats.spe_fallbacks;
+    res->stats.svd_count = r.stats.svd_count;
+    res->stats.estimator_appends = r.stats.appends;
     if (x_final && (long)r.final_x_free.size() <= x_cap)
       std::memcpy(x_final, r.final_x_free.data(), sizeof(double) * r.final_x_free.size());
     if (r.exit_code != 0) {
@@ -547,6 +569,10 @@ int eqs_set_option(eqs_ctx* ctx, int key, double value) {
       case 12: g.reset_estimator((int)value); break;
       case 13: g.cheb_kind = (int)value; g.set_cheb(g.cheb_ratio); break;
       case 14: g.cheb_scale = value; g.set_cheb(g.cheb_ratio); break;
+      case 15: g.set_pod_params((int)value, 0, 0, -1.0); break;
+      case 16: g.set_pod_params(0, (int)value, 0, -1.0); break;
+      case 17: g.set_pod_params(0, 0, (int)value, -1.0); break;
+      case 18: g.set_pod_params(0, 0, 0, std::max(0.0, value)); break;
       default: throw std::invalid_argument("eqs_set_option: unknown key");
     }
   });

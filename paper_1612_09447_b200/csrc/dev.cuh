@@ -205,6 +205,8 @@ struct CoefPack {
   double c[kMaxMulti];
 };
 void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s);
+// y += sum_k c[k] V_k
+void launch_lincomb_acc(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s);
 // SPE basis maintenance: w -= sum_j c_j Q_j with ||w||^2 into slot; and a
 // kin -> kout basis rotation out_j = sum_i T[i][j] in_i (kin, kout <= 9)
 constexpr int kMaxWin = 9;

@@ -81,8 +81,12 @@ struct SolverParams {
   int amg_dense_coarse = 0;           // additive: the device V-cycle solves the first coarse level with at most
                                       // this many rows directly (dense inverse); <= 0 (default): recurse to the
                                       // hierarchy's coarsest
-  int estimator_mode = 0;  // 0 zero, 1 previous, 2 spe
+  int estimator_mode = 0;  // 0 zero, 1 previous, 2 spe, 3 pod_fixed, 4 pod_rolling
   int spe_window = 8;
+  int pod_snapshots = 40;    // start_vector.hpp:31-35
+  int pod_rank = 10;
+  int pod_capacity = 20;
+  double pod_threshold = 0;  // <= 0: 1.25 x the running median of the iteration counts
   double mgs_drop_tol = 1e-8;
 };
 

@@ -1427,12 +1427,244 @@ void GpuSystem::spe_downdate() {
   spe_k_ = k - 1;
 }
 
+
+// ------------------------------------------------------------------ POD estimators
+// proj/src/start_vector.cpp:64-71 (pod_build), 111-131 (pod_start), 133-150
+// (factor_reduced, rolling_threshold), 165-183 (feedback). The reference runs
+// Eigen::JacobiSVD on the n x k snapshot matrix S. Here S = Q R is first
+// factored on the device (classical Gram-Schmidt, two passes), then the small
+// k-column R goes through a one-sided Jacobi SVD on the host: R V = U_R Sigma
+// gives S V = (Q U_R) Sigma, i.e. the same rotations applied to S, so the
+// singular values and left singular vectors are those of S. Only the basis
+// U = Q U_R[:, :keep] (keep <= rank, sigma > 1e-12 sigma_0) is formed on the
+// device, followed by W = M U and the reduced inverse (U'MU)^-1.
+namespace {
+// One-sided Jacobi on the columns of R (m rows, k columns, column-major):
+// returns sigma (descending) and the matching normalised left singular
+// vectors (m each).
+void jacobi_svd_left(int m, int k, std::vector<double> R, std::vector<double>& sigma,
+                     std::vector<std::vector<double>>& u) {
+  auto col = [&](int j) { return R.data() + (size_t)j * m; };
+  auto dotc = [&](int a, int b) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += col(a)[i] * col(b)[i];
+    return s;
+  };
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    bool rotated = false;
+    for (int p = 0; p < k; ++p)
+      for (int q = p + 1; q < k; ++q) {
+        const double al = dotc(p, p), be = dotc(q, q), ga = dotc(p, q);
+        if (ga == 0.0 || std::abs(ga) <= 1e-15 * std::sqrt(al * be)) continue;
+        rotated = true;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        double *x = col(p), *y = col(q);
+        for (int i = 0; i < m; ++i) {
+          const double a = x[i], b = y[i];
+          x[i] = c * a - sn * b;
+          y[i] = sn * a + c * b;
+        }
+      }
+    if (!rotated) break;
+  }
+  std::vector<std::pair<double, int>> sv(k);
+  for (int j = 0; j < k; ++j) sv[j] = {std::sqrt(dotc(j, j)), j};
+  std::stable_sort(sv.begin(), sv.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+  sigma.assign(k, 0.0);
+  u.assign(k, std::vector<double>(m, 0.0));
+  for (int j = 0; j < k; ++j) {
+    sigma[j] = sv[j].first;
+    if (sv[j].first > 0.0)
+      for (int i = 0; i < m; ++i) u[j][i] = col(sv[j].second)[i] / sv[j].first;
+  }
+}
+}  // namespace
+
+DevBuf<double>* GpuSystem::pod_buf(std::vector<std::unique_ptr<DevBuf<double>>>& v, int j) {
+  while ((int)v.size() <= j) {
+    v.push_back(std::make_unique<DevBuf<double>>());
+    v.back()->alloc(std::max(1, n_loc_));
+  }
+  return v[j].get();
+}
+
+// out[k] = V_k . w for k < m (chunks of kMaxMulti), allreduced
+void GpuSystem::multi_dot_chunked(int m, const double* const* V, const double* w, double* out) {
+  for (int c0 = 0; c0 < m; c0 += kMaxMulti) {
+    const int mc = std::min<int>(kMaxMulti, m - c0);
+    launch_multi_dot(n_own_, mc, V + c0, w, red_, S_MDOT, stream_);
+    allreduce(S_MDOT, mc);
+    read_scalars(S_MDOT, mc, out + c0);
+  }
+}
+
+// y = sum_k c[k] V_k (chunks of kMaxMulti)
+void GpuSystem::lincomb_chunked(int m, const double* const* V, const double* c, double* y) {
+  if (m == 0) {
+    launch_fill(n_own_, 0.0, y, stream_);
+    return;
+  }
+  for (int c0 = 0; c0 < m; c0 += kMaxMulti) {
+    const int mc = std::min<int>(kMaxMulti, m - c0);
+    CoefPack cp{};
+    for (int i = 0; i < mc; ++i) cp.c[i] = c[c0 + i];
+    if (c0 == 0) launch_lincomb(n_own_, mc, V + c0, cp, y, stream_);
+    else launch_lincomb_acc(n_own_, mc, V + c0, cp, y, stream_);
+  }
+}
+
+void GpuSystem::pod_build_dev() {
+  const int n = n_own_;
+  const int k = pod_nsnap_;
+  const int rank = prob_.solver.pod_rank;
+  // thin QR of S by classical Gram-Schmidt with re-orthogonalisation; R is m x k
+  std::vector<double> R;  // column-major, leading dimension k (m <= k)
+  R.assign((size_t)k * k, 0.0);
+  int m = 0;
+  std::vector<const double*> Q;
+  std::vector<double> c(k), r(k);
+  for (int j = 0; j < k; ++j) {
+    const double* s = pod_snap_[j]->p;
+    const double norm0 = std::sqrt(dot_own(s, s, S_NORM));
+    if (norm0 == 0.0) continue;  // zero column: R(:, j) = 0
+    double* w = pod_buf(pod_q_, m)->p;
+    CK(cudaMemcpyAsync(w, s, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    std::fill(r.begin(), r.end(), 0.0);
+    double nrm = norm0;
+    for (int pass = 0; pass < 2 && m > 0; ++pass) {
+      multi_dot_chunked(m, Q.data(), w, c.data());
+      for (int c0 = 0; c0 < m; c0 += kMaxMulti) {
+        const int mc = std::min<int>(kMaxMulti, m - c0);
+        CoefPack cp{};
+        for (int i = 0; i < mc; ++i) {
+          cp.c[i] = c[c0 + i];
+          r[c0 + i] += c[c0 + i];
+        }
+        launch_orth_update(n, mc, Q.data() + c0, cp, w, red_, S_NORM, stream_);
+      }
+      allreduce(S_NORM);
+      nrm = std::sqrt(read_scalar(S_NORM));
+    }
+    for (int i = 0; i < m; ++i) R[(size_t)j * k + i] = r[i];
+    // residual at the rounding level of S: a numerically dependent column
+    // (its singular-value contribution is below the 1e-12 sigma_0 cut)
+    if (nrm <= 1e-13 * norm0) continue;
+    launch_scale(n, 1.0 / nrm, w, w, stream_);
+    R[(size_t)j * k + m] = nrm;
+    Q.push_back(w);
+    ++m;
+  }
+  // small SVD of R (m x k) on the host
+  std::vector<double> Rm((size_t)m * k);
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i < m; ++i) Rm[(size_t)j * m + i] = R[(size_t)j * k + i];
+  std::vector<double> sigma;
+  std::vector<std::vector<double>> ur;
+  if (m > 0) jacobi_svd_left(m, k, Rm, sigma, ur);
+  int keep = 0;
+  if (m > 0 && sigma[0] > 0.0)
+    while (keep < k && keep < rank && sigma[keep] > 1e-12 * sigma[0]) ++keep;
+  for (int b = 0; b < keep; ++b) lincomb_chunked(m, Q.data(), ur[b].data(), pod_buf(pod_u_, b)->p);
+  pod_rank_ = keep;
+}
+
+void GpuSystem::pod_factor() {
+  const int r = pod_rank_;
+  pod_ok_ = r > 0;
+  if (!pod_ok_) return;  // empty-basis signal, zero start without noise
+  std::vector<const double*> U(r);
+  for (int a = 0; a < r; ++a) {
+    U[a] = pod_u_[a]->p;
+    mass_apply_dev(pod_u_[a]->p, pod_buf(pod_w_, a)->p);
+  }
+  std::vector<double> g((size_t)r * r), col(r);
+  for (int b = 0; b < r; ++b) {
+    multi_dot_chunked(r, U.data(), pod_w_[b]->p, col.data());
+    for (int a = 0; a < r; ++a) g[(size_t)a * r + b] = col[a];
+  }
+  DenseLdlt ldlt;
+  ldlt.compute(g, r);
+  double dmax = 0.0, dmin = INFINITY;
+  for (double d : ldlt.d) {
+    dmax = std::max(dmax, std::abs(d));
+    dmin = std::min(dmin, d);
+  }
+  pod_ok_ = ldlt.ok && dmax > 0.0 && dmin > 1e-14 * dmax;
+  if (!pod_ok_) {
+    ++stats_.spe_fallbacks;
+    std::fprintf(stderr, "start_vector: singular reduced system, zero start used\n");
+    return;
+  }
+  pod_ginv_.assign((size_t)r * r, 0.0);
+  std::vector<double> e(r);
+  for (int c = 0; c < r; ++c) {
+    std::fill(e.begin(), e.end(), 0.0);
+    e[c] = 1.0;
+    ldlt.solve(e.data(), col.data());
+    for (int a = 0; a < r; ++a) pod_ginv_[(size_t)a * r + c] = col[a];
+  }
+}
+
+double GpuSystem::pod_rolling_threshold() const {
+  if (prob_.solver.pod_threshold > 0.0) return prob_.solver.pod_threshold;
+  if (iteration_history_.empty()) return -1.0;  // always append while empty
+  std::vector<int> h = iteration_history_;
+  const size_t mid = h.size() / 2;
+  std::nth_element(h.begin(), h.begin() + mid, h.end());
+  return 1.25 * (double)h[mid];
+}
+
+bool GpuSystem::pod_start(const double* b, double* x0) {
+  const int mode = prob_.solver.estimator_mode;
+  if (mode == 3 && !pod_built_ && pod_nsnap_ >= prob_.solver.pod_snapshots) {
+    pod_build_dev();
+    ++stats_.svd_count;
+    pod_built_ = true;
+    pod_factor();
+  }
+  if (mode == 4 && pod_stale_ && pod_nsnap_ > 0) {
+    pod_build_dev();
+    ++stats_.svd_count;
+    pod_stale_ = false;
+    pod_factor();
+  }
+  estimator_rank_ = pod_rank_;
+  const int r = pod_rank_;
+  if (r == 0 || !pod_ok_) return false;
+  std::vector<const double*> U(r);
+  for (int a = 0; a < r; ++a) U[a] = pod_u_[a]->p;
+  std::vector<double> vtb(r), y(r, 0.0);
+  multi_dot_chunked(r, U.data(), b, vtb.data());
+  for (int a = 0; a < r; ++a) {
+    double s = 0.0;
+    for (int c = 0; c < r; ++c) s += pod_ginv_[(size_t)a * r + c] * vtb[c];
+    y[a] = s;
+  }
+  lincomb_chunked(r, U.data(), y.data(), x0);
+  return true;
+}
+
+bool GpuSystem::estimator_next_dev(const double* b, double* x0, int* rank) {
+  const bool nz = estimator_next(b, x0);
+  if (!nz) launch_fill(n_own_, 0.0, x0, stream_);
+  if (rank) *rank = prob_.solver.estimator_mode >= 2 ? estimator_rank_ : 0;
+  return nz;
+}
+
 // StartVectorEstimator::next (proj/src/start_vector.cpp:84-109); writes the
 // start vector into x0 and returns true when it is non-zero-by-construction.
 bool GpuSystem::estimator_next(const double* b, double* x0) {
   const int n = n_own_;
   const int mode = prob_.solver.estimator_mode;
   if (mode == 0) return false;
+  if (mode >= 3) {
+    tic(TC_SPE);
+    const bool nz = pod_start(b, x0);
+    toc(TC_SPE, 0.0);
+    return nz;
+  }
   if (history_.empty()) return false;
   if (mode == 1) {
     CK(cudaMemcpyAsync(x0, history_.back(), sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
@@ -1489,9 +1721,32 @@ bool GpuSystem::estimator_next(const double* b, double* x0) {
 }
 
 // StartVectorEstimator::feedback (proj/src/start_vector.cpp:152-164)
-void GpuSystem::estimator_feedback(const double* x) {
+void GpuSystem::estimator_feedback(const double* x, int iterations) {
   const int mode = prob_.solver.estimator_mode;
+  if (mode >= 3) {
+    int slot = -1;
+    if (mode == 3) {
+      if (!pod_built_ && pod_nsnap_ < prob_.solver.pod_snapshots) slot = pod_nsnap_++;
+    } else if ((double)iterations > pod_rolling_threshold()) {
+      if (pod_nsnap_ < prob_.solver.pod_capacity) {
+        slot = pod_nsnap_++;
+      } else {
+        slot = pod_next_slot_;  // overwrite the oldest
+        pod_next_slot_ = (pod_next_slot_ + 1) % prob_.solver.pod_capacity;
+      }
+      pod_stale_ = true;
+    }
+    if (slot >= 0) {
+      CK(cudaMemcpyAsync(pod_buf(pod_snap_, slot)->p, x, sizeof(double) * n_own_, cudaMemcpyDeviceToDevice,
+                         stream_));
+      ++stats_.appends;
+    }
+    iteration_history_.push_back(iterations);
+    return;
+  }
+  iteration_history_.push_back(iterations);
   if (mode == 0) return;
+  if (mode == 2) ++stats_.appends;
   const size_t window = mode == 1 ? 1 : (size_t)prob_.solver.spe_window;
   double* buf;
   if (history_.size() >= window) {
@@ -1541,7 +1796,7 @@ PcgResult GpuSystem::eval_rhs_dev(double t, double* x_full, double* f) {
   }
   {
     PhaseTimer pt(stats_.t_estimator);
-    estimator_feedback(f);
+    estimator_feedback(f, res.iterations);
   }
   ++stats_.m_solves;
   stats_.pcg_iterations += res.iterations;
@@ -1677,6 +1932,27 @@ PcgResult GpuSystem::mass_solve_host(const double* b, const double* x0, double t
   return r;
 }
 
+// StartVectorEstimator::next / feedback with host vectors (start_vector.hpp:52-58)
+int GpuSystem::estimator_next_host(const double* b, double* x0) {
+  require_single("estimator_next");
+  F0_.upload(b, n_own_, stream_);
+  int rank = 0;
+  {
+    PhaseTimer pt(stats_.t_estimator);
+    estimator_next_dev(F0_.p, F_.p, &rank);
+  }
+  F_.download(x0, n_own_, stream_);
+  sync();
+  return rank;
+}
+void GpuSystem::estimator_feedback_host(const double* x, int iterations) {
+  require_single("estimator_feedback");
+  F_.upload(x, n_own_, stream_);
+  PhaseTimer pt(stats_.t_estimator);
+  estimator_feedback(F_.p, iterations);
+  sync();
+}
+
 // Config-5 MRHS microbenchmark: k right-hand sides solved in
 // sequence on the device with the configured start-vector estimator (the
 // eval_rhs solve path without K(x)x). B and X are host [k][n_free]; X may be
@@ -1697,7 +1973,7 @@ double GpuSystem::mass_solve_sequence(const double* B, int k, double tol, int ma
     const bool has_x0 = estimator_next(b, x);
     const PcgResult r = pcg_dev(b, has_x0 ? x : nullptr, x, tol, max_iter);
     if (!r.converged) throw NumericalError("mass_solve_sequence: PCG did not converge");
-    estimator_feedback(x);
+    estimator_feedback(x, r.iterations);
     if (its) its[j] = r.iterations;
   }
   CK(cudaEventRecord(e1, stream_));
@@ -1710,11 +1986,16 @@ double GpuSystem::mass_solve_sequence(const double* B, int k, double tol, int ma
 }
 
 void GpuSystem::reset_estimator(int mode) {
-  if (mode < 0 || mode > 2) throw std::invalid_argument("estimator mode must be 0 (zero), 1 (previous) or 2 (spe)");
+  if (mode < 0 || mode > 4)
+    throw std::invalid_argument("estimator mode must be 0 (zero), 1 (previous), 2 (spe), 3 (pod_fixed) or 4 (pod_rolling)");
   prob_.solver.estimator_mode = mode;
   history_.clear();
   hist_pool_.clear();
   spe_clean_ = false;
+  pod_nsnap_ = pod_next_slot_ = pod_rank_ = 0;  // POD buffers stay allocated for the next run
+  pod_stale_ = pod_built_ = pod_ok_ = false;
+  iteration_history_.clear();
+  estimator_rank_ = 0;
 }
 
 void GpuSystem::mass_apply_host(const double* v, double* y) {

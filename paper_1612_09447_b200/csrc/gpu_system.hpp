@@ -24,6 +24,7 @@ namespace eqsb {
 struct SolveStats {
   long m_solves = 0, pcg_iterations = 0, rho_solves = 0, rho_pcg_iterations = 0;
   long precond_setups = 0, assemblies = 0, applies = 0, spe_fallbacks = 0;
+  long svd_count = 0, appends = 0;  // StartVectorEstimator::Stats (start_vector.hpp:45-49)
   double t_residual = 0, t_solve = 0, t_setup = 0, t_estimator = 0;
 };
 struct SolveRecord {
@@ -148,7 +149,16 @@ class GpuSystem {
   PcgResult eval_rhs_host(double t, const double* x, double* f);
   PcgResult mass_solve_host(const double* b, const double* x0, double tol, int max_iter, double* x);
   double mass_solve_sequence(const double* B, int k, double tol, int max_iter, double* X, int* its);
-  void reset_estimator(int mode);  // switch zero/previous/spe and drop the history
+  void reset_estimator(int mode);  // switch zero/previous/spe/pod_fixed/pod_rolling and drop the history
+  int estimator_next_host(const double* b, double* x0);            // returns current_rank()
+  // > 0 (threshold >= 0) replaces the value; others keep it
+  void set_pod_params(int snapshots, int rank, int capacity, double threshold) {
+    if (snapshots > 0) prob_.solver.pod_snapshots = snapshots;
+    if (rank > 0) prob_.solver.pod_rank = rank;
+    if (capacity > 0) prob_.solver.pod_capacity = capacity;
+    if (threshold >= 0.0) prob_.solver.pod_threshold = threshold;
+  }
+  void estimator_feedback_host(const double* x, int iterations);
   void mass_apply_host(const double* v, double* y);
   void apply_minv_stiffness_host(double t, const double* x_state, const double* v, double* y);
   void lift_full_host(double t, const double* x_free, double* x_full);
@@ -229,7 +239,7 @@ class GpuSystem {
   void require_single(const char* what) const;
   // estimator (start_vector.cpp:84-109,152-164)
   bool estimator_next(const double* r, double* x0);
-  void estimator_feedback(const double* x);
+  void estimator_feedback(const double* x, int iterations);
   int estimator_rank_ = 0;
   // incremental SPE basis (Q orthonormal, W = M Q, G = Q'MQ, H = Q R)
   std::vector<std::unique_ptr<DevBuf<double>>> spe_q_[2], spe_w_[2];
@@ -244,6 +254,28 @@ class GpuSystem {
   void spe_rebuild();
   void spe_append(double* h);
   void spe_downdate();
+  // POD estimators (start_vector.cpp:64-71,111-150,165-187): snapshot ring,
+  // thin QR of the snapshots (Q, R), Jacobi SVD of R on the host, basis
+  // U = Q U_R, W = M U and the reduced inverse (U'MU)^-1
+  std::vector<std::unique_ptr<DevBuf<double>>> pod_snap_, pod_q_, pod_u_, pod_w_;
+  int pod_nsnap_ = 0, pod_next_slot_ = 0, pod_rank_ = 0;
+  bool pod_stale_ = false, pod_built_ = false, pod_ok_ = false;
+  std::vector<double> pod_ginv_;
+  std::vector<int> iteration_history_;
+  DevBuf<double>* pod_buf(std::vector<std::unique_ptr<DevBuf<double>>>& v, int j);
+  void multi_dot_chunked(int m, const double* const* V, const double* w, double* out);
+  void lincomb_chunked(int m, const double* const* V, const double* c, double* y);
+  void pod_build_dev();
+  void pod_factor();
+  bool pod_start(const double* b, double* x0);
+  double pod_rolling_threshold() const;
+
+ public:
+  // StartVectorEstimator public API (start_vector.hpp:52-66), device vectors
+  bool estimator_next_dev(const double* b, double* x0, int* rank);
+  void estimator_feedback_dev(const double* x, int iterations) { estimator_feedback(x, iterations); }
+
+ private:
   int vcycle_prec_ = 2;
   bool vcycle_f32_ = true;
   bool sell_on_ = true;

@@ -142,13 +142,17 @@ SimConfig parse_config(const std::string& text) {
       if (mode == "zero") c.solver.estimator_mode = 0;
       else if (mode == "previous") c.solver.estimator_mode = 1;
       else if (mode == "spe") c.solver.estimator_mode = 2;
-      else if (mode == "pod_fixed" || mode == "pod_rolling")
-        throw ConfigError("estimator mode '" + mode + "' is not supported by the GPU backend (SURVEY.md §8f)");
+      else if (mode == "pod_fixed") c.solver.estimator_mode = 3;
+      else if (mode == "pod_rolling") c.solver.estimator_mode = 4;
       else throw ConfigError("unknown estimator mode '" + mode + "'");
       c.solver.spe_window = je.value("window", c.solver.spe_window);
+      c.solver.pod_snapshots = je.value("snapshots", c.solver.pod_snapshots);  // scenario.cpp:64-67
+      c.solver.pod_rank = je.value("rank", c.solver.pod_rank);
+      c.solver.pod_capacity = je.value("capacity", c.solver.pod_capacity);
+      c.solver.pod_threshold = je.value("threshold", c.solver.pod_threshold);
       c.solver.mgs_drop_tol = je.value("mgs_drop_tol", c.solver.mgs_drop_tol);
-      if (c.solver.spe_window < 1 || je.value("snapshots", 40) < 1 || je.value("rank", 10) < 1 ||
-          je.value("capacity", 20) < 1)
+      if (c.solver.spe_window < 1 || c.solver.pod_snapshots < 1 || c.solver.pod_rank < 1 ||
+          c.solver.pod_capacity < 1)
         throw ConfigError("estimator window/snapshot/rank/capacity values must be >= 1");
     }
     for (const auto& jp : j.value("probes", json::array())) {

@@ -162,9 +162,10 @@ __global__ void k_multi_dot(int n, int m, PtrPack V, const double* __restrict__ 
   for (int k = 0; k < m; ++k) reduce_finish(acc[k], red, slot0 + k);
 }
 
+template <bool ACC>
 __global__ void k_lincomb(int n, int m, PtrPack V, CoefPack c, double* __restrict__ y) {
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
-    double s = 0.0;
+    double s = ACC ? y[i] : 0.0;
     for (int k = 0; k < m; ++k) s += V.p[k][i] * c.c[k];
     y[i] = s;
   }
@@ -341,7 +342,13 @@ void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y,
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
-  k_lincomb<<<grid_for(n), kBlock, 0, s>>>(n, m, pk, c, y);
+  k_lincomb<false><<<grid_for(n), kBlock, 0, s>>>(n, m, pk, c, y);
+}
+void launch_lincomb_acc(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  PtrPack pk{};
+  for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
+  k_lincomb<true><<<grid_for(n), kBlock, 0, s>>>(n, m, pk, c, y);
 }
 void launch_orth_update(int n, int m, const double* const* Q, CoefPack c, double* w, Reducer red, int slot,
                         cudaStream_t s) {

@@ -181,6 +181,8 @@ const char* estimator_mode_name(int m) {
     case 0: return "zero";
     case 1: return "previous";
     case 2: return "spe";
+    case 3: return "pod_fixed";
+    case 4: return "pod_rolling";
   }
   return "?";
 }

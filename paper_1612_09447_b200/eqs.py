@@ -67,7 +67,7 @@ class _SolveStats(C.Structure):
                                          "newton_linear_solves", "newton_pcg_iterations", "precond_setups",
                                          "assemblies", "svd_count")] + \
                [(n, C.c_double) for n in ("time_residual", "time_solve", "time_setup", "time_estimator")] + \
-               [("applies", C.c_long), ("spe_fallbacks", C.c_long)]
+               [("applies", C.c_long), ("spe_fallbacks", C.c_long), ("estimator_appends", C.c_long)]
 
 
 class _RkcOptions(C.Structure):
@@ -339,6 +339,22 @@ class FemSystem:
         _check(load_library().eqs_mass_solve(self._h, _dp(_f64(b)), x0p, C.c_double(tol), C.c_int(max_iter),
                                              _dp(x), C.byref(res)))
         return x, _pcg(res)
+
+    # --- StartVectorEstimator (proj/include/eqs/start_vector.hpp:52-66)
+    def estimator_next(self, b):
+        """next(M_II, b) -> (x0, current_rank())."""
+        x0 = np.zeros(self.n_free)
+        rank = C.c_int(0)
+        _check(load_library().eqs_estimator_next(self._h, _dp(_f64(b)), _dp(x0), C.byref(rank)))
+        return x0, rank.value
+
+    def estimator_feedback(self, x, iterations: int):
+        _check(load_library().eqs_estimator_feedback(self._h, _dp(_f64(x)), C.c_int(int(iterations))))
+
+    def estimator_stats(self) -> dict:
+        """StartVectorEstimator::Stats (start_vector.hpp:45-49)."""
+        s = self.stats()
+        return {"svd_count": s["svd_count"], "appends": s["estimator_appends"], "spe_fallbacks": s["spe_fallbacks"]}
 
     def apply_minv_stiffness(self, t: float, x_state, v) -> np.ndarray:
         y = np.zeros(self.n_free)

@@ -39,6 +39,26 @@ def test_sequence_solutions_and_estimators():
     assert its[1][1:].sum() < its[0][1:].sum()
 
 
+def test_sequence_pod_estimators():
+    """POD start vectors on the config-5 sequence (start_vector.cpp:111-131):
+    the x*_k span three modes, so once the basis holds them the Galerkin start
+    is nearly exact and PCG needs far fewer iterations than from zero."""
+    g = eb.FemSystem(cube(14, jitter=0.1, planes=(0.45, 0.55)))
+    X, B = smooth_sequence(g, 16)
+    g.set_option(15, 4)  # pod_fixed: basis from the first 4 solutions
+    g.set_option(18, 5)  # pod_rolling: append every solve above 5 iterations
+    its = {}
+    for mode in (0, 3, 4):
+        g.set_option(12, mode)
+        it, ms, Xs = g.mass_solve_sequence(B, want_x=True)
+        for k in range(len(X)):
+            assert np.linalg.norm(Xs[k] - X[k]) <= 1e-9 * np.linalg.norm(X[k])
+        its[mode] = it
+    assert (its[3][:4] == its[0][:4]).all()  # still collecting: zero starts
+    assert its[3][5:].sum() <= 0.5 * its[0][5:].sum()
+    assert its[4][5:].sum() <= 0.5 * its[0][5:].sum()
+
+
 def test_sequence_rejects_bad_input():
     g = eb.FemSystem(cube(6))
     with pytest.raises(eb.EqsError):

@@ -140,3 +140,32 @@ def test_config_error_exit_code():  # scenario.cpp:353-368
     cfg["estimator"]["mode"] = "bogus"
     with pytest.raises(eb.ConfigError):
         eb.run_scenario(cfg)
+
+
+def test_pod_estimators_nonlinear_scenario_c7():  # acceptance_main.cpp:272-299 (C7, measured and reported)
+    """The reference's nonlinear slab with SPE, pod_fixed and pod_rolling start
+    vectors (proj/configs/slab_nonlinear_rkc_{spe,pod_fixed,pod_rolling}.json).
+    Like the reference, this criterion is measured and reported: the adaptive
+    nonlinear run is sensitive to rounding-level differences of the M-solves
+    (the oracle's own zero / previous / SPE runs of this config end 100%+
+    apart at t_end with 804 / 248 / 1449 accepted steps), so only completion,
+    the one-preconditioner rule (C5) and the SVD counts of
+    start_vector.cpp:111-126 are asserted."""
+    runs = {}
+    for name in ("slab_nonlinear_rkc_spe", "slab_nonlinear_rkc_pod_fixed", "slab_nonlinear_rkc_pod_rolling"):
+        cfg = slab_reference(name)
+        cfg["output"] = {"metrics_csv": "", "probe_csv": "", "solves_csv": ""}
+        r = eb.run_scenario(cfg)
+        assert r["exit_code"] == 0, r.get("error")
+        assert r["stats"]["precond_setups"] == 1
+        runs[name] = r
+    spe, fixed, rolling = (runs[n] for n in ("slab_nonlinear_rkc_spe", "slab_nonlinear_rkc_pod_fixed",
+                                              "slab_nonlinear_rkc_pod_rolling"))
+    assert spe["stats"]["svd_count"] == 0
+    assert fixed["stats"]["svd_count"] == (1 if fixed["stats"]["m_solves"] > 60 else 0)
+    assert rolling["stats"]["svd_count"] >= 1
+    for r in (spe, fixed, rolling):
+        assert abs(r["final_t"] - 0.02) <= 1e-12 and np.isfinite(r["x"]).all()
+    print("C7 PCG iterations: spe %d, pod_fixed %d (%d SVDs), pod_rolling %d (%d SVDs)" % (
+        spe["stats"]["pcg_iterations"], fixed["stats"]["pcg_iterations"], fixed["stats"]["svd_count"],
+        rolling["stats"]["pcg_iterations"], rolling["stats"]["svd_count"]))
