@@ -212,6 +212,10 @@ int eqs_get_mass(eqs_ctx* ctx, int which, int* row_ptr, int* col_idx, double* va
  * aggregates of level l (proj/src/amg.cpp:49-88). */
 int eqs_amg_levels(eqs_ctx* ctx, int* n_levels, long* rows_nnz);
 int eqs_amg_aggregates(eqs_ctx* ctx, int level, int* agg);
+/* A (which 0), P (1) or R (2) of an AMG level in CSR (AmgPreconditioner levels,
+ * proj/include/eqs/amg.hpp:40-50). Call with null arrays to get dims =
+ * {rows, cols, nnz}. Single-rank contexts. */
+int eqs_amg_level_csr(eqs_ctx* ctx, int level, int which, int* dims, int* row_ptr, int* col_idx, double* values);
 
 /* ----------------------------------------------------------------- operators */
 /* MatFreeStiffness::apply (proj/src/matfree.cpp:90-98): y = K(x_state) v, full dof vectors. */

@@ -368,6 +368,26 @@ int eqs_amg_aggregates(eqs_ctx* ctx, int level, int* agg) {
   });
 }
 
+int eqs_amg_level_csr(eqs_ctx* ctx, int level, int which, int* dims, int* row_ptr, int* col_idx, double* values) {
+  return guard([&] {
+    const AmgHierarchy& h = H(ctx).amg();
+    if (level < 0 || level >= (int)h.levels.size() || which < 0 || which > 2)
+      throw std::invalid_argument("eqs_amg_level_csr: bad level or matrix");
+    const AmgHostLevel& lv = h.levels[level];
+    const HostCsr& m = which == 0 ? lv.A : which == 1 ? lv.P : lv.R;
+    if (m.row_ptr.empty() && !(which > 0 && level + 1 == (int)h.levels.size()))
+      throw std::invalid_argument("eqs_amg_level_csr: host copy released (multi-rank context)");
+    dims[0] = m.n_rows;
+    dims[1] = m.n_cols;
+    dims[2] = (int)m.nnz();
+    if (row_ptr) {
+      std::memcpy(row_ptr, m.row_ptr.data(), sizeof(int) * m.row_ptr.size());
+      std::memcpy(col_idx, m.col_idx.data(), sizeof(int) * m.nnz());
+      std::memcpy(values, m.values.data(), sizeof(double) * m.nnz());
+    }
+  });
+}
+
 int eqs_kx_apply(eqs_ctx* ctx, const double* x_state, const double* v, double* y) {
   return guard([&] { S(ctx).kx_apply_host(x_state, v, y); });
 }

@@ -123,8 +123,14 @@ struct AmgHierarchy {
   int coarse_n = 0;
 };
 // AmgPreconditioner ctor (proj/src/amg.cpp:90-143), bit-exact aggregation and
-// Galerkin products (deterministic row-parallel SpGEMM).
-AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp);
+// Galerkin products (deterministic row-parallel SpGEMM). device >= 0: the
+// smoothed prolongator and the Galerkin products run on that GPU
+// (spgemm_device), bit-identical to the host products.
+AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device = -1);
+// C = A B on the GPU with the host product's per-row arithmetic order
+// (k_spgemm.cu). With diag, A is replaced by I - omega D^-1 A on the fly.
+HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std::vector<double>* diag = nullptr,
+                      double omega = 0.0, long long batch_products = 1ll << 28);
 // explicit inverse (row-major) of a symmetric matrix through the pivoted LDLT
 // below (the coarsest-level solve, amg.cpp:140); threaded for the larger
 // dense coarse levels of the device V-cycle (SolverParams::amg_dense_coarse)

@@ -52,6 +52,7 @@ template struct DevBuf<long>;
 template struct DevBuf<unsigned>;
 template struct DevBuf<unsigned char>;
 template struct DevBuf<unsigned short>;
+template struct DevBuf<unsigned long long>;
 
 namespace {
 using clk = std::chrono::steady_clock;
@@ -177,7 +178,11 @@ void memtrace(const char* tag) {
     if (!strncmp(line, "VmHWM:", 6)) hwm = atol(line + 6);
   }
   fclose(f);
-  fprintf(stderr, "[memtrace] %-28s rss %7.2f GB  peak %7.2f GB\n", tag, rss / 1048576.0, hwm / 1048576.0);
+  static auto last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  fprintf(stderr, "[memtrace] %-28s rss %7.2f GB  peak %7.2f GB  +%.2f s\n", tag, rss / 1048576.0, hwm / 1048576.0,
+          std::chrono::duration<double>(now - last).count());
+  last = now;
 }
 
 std::vector<double> inv_diagonal(const HostCsr& a) {
@@ -216,7 +221,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
   memtrace("mass assembled");
   ++stats_.assemblies;
   // mass preconditioner (built once; the reference builds it lazily on first use, fem_system.cpp:48-54)
-  if (prob_.solver.precond == 2) amg_ = build_amg(m_ii_, prob_.solver);
+  if (prob_.solver.precond == 2) amg_ = build_amg(m_ii_, prob_.solver, device_);
   ++stats_.precond_setups;
   memtrace("amg built");
   // device V-cycle depth: the first coarse level with at most amg_dense_coarse
@@ -450,6 +455,7 @@ void GpuSystem::build_device() {
   }
   err_.alloc(4);
   CK(cudaMemsetAsync(err_.p, 0, 4 * sizeof(int), s));
+  memtrace("dev: coords + kx blocks");
   // Dirichlet data: set of every local fixed dof; compressed M_IB rows (owned) per set
   {
     std::vector<int> sof(std::max(1, n_fixloc_));
@@ -474,6 +480,7 @@ void GpuSystem::build_device() {
     bl_coef_.upload(coef.data(), coef.size(), s);
     CK(cudaStreamSynchronize(s));
   }
+  memtrace("dev: dirichlet");
   // M_II (owned rows, local columns) + level-0 halo
   upload_csr(plan_.mii, mii_, mii_rp_, mii_ci_, mii_v_, s);
   upload_sell(plan_.mii, mii_, mii_s_, s);
@@ -488,6 +495,7 @@ void GpuSystem::build_device() {
     mii_invd_.upload(invd.data(), invd.size(), s);
     halo(halo0_, mii_invd_.p);
   }
+  memtrace("dev: M_II sell");
   // reductions + work vectors
   red_partials_.alloc((size_t)S_COUNT * kRedGrid);
   red_scal_.alloc(S_COUNT);
@@ -590,6 +598,7 @@ void GpuSystem::build_levels() {
   std::vector<double>().swap(dev_coarse_inv_);
   set_vcycle_precision(vcycle_prec_);
   set_sell(sell_on_);
+  memtrace("dev: levels uploaded");
   // smoother bounds: lambda_max(D^-1 A_l) by 20 power iterations from a
   // global random vector (same on every rank), norms reduced over ranks
   std::mt19937 rng(12345u);

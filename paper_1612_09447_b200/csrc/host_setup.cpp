@@ -6,6 +6,9 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -408,7 +411,7 @@ double estimate_lambda_max_scaled(const HostCsr& a, int iters, unsigned seed) {
 }
 
 // proj/src/amg.cpp:90-143
-AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp) {
+AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device) {
   if (a.n_rows != a.n_cols) throw std::invalid_argument("amg: matrix must be square");
   if (symmetry_error(a) > 1e-10) throw std::invalid_argument("amg: matrix is not symmetric");
   check_diagonal(a);
@@ -417,7 +420,16 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp) {
   while ((int)h.levels.size() < sp.amg_max_levels && h.levels.back().A.n_rows > sp.amg_coarse_limit) {
     AmgHostLevel& lv = h.levels.back();
     const HostCsr& fine = lv.A;
+    auto T0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      static const bool on = getenv("EQS_MEMTRACE") != nullptr;
+      const auto now = std::chrono::steady_clock::now();
+      if (on) fprintf(stderr, "[amg] level %zu %-12s %.2f s\n", h.levels.size() - 1, what,
+                      std::chrono::duration<double>(now - T0).count());
+      T0 = now;
+    };
     std::vector<int> agg = aggregate(fine, sp.amg_theta);
+    lap("aggregate");
     const int n_agg = *std::max_element(agg.begin(), agg.end()) + 1;
     if (n_agg >= fine.n_rows) break;
     std::vector<int> agg_size(n_agg, 0);
@@ -434,19 +446,33 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp) {
       p_tent.values[i] = 1.0 / std::sqrt((double)agg_size[agg[i]]);
     }
     p_tent.row_ptr[fine.n_rows] = fine.n_rows;
+    lap("p_tent");
     lv.lambda_max_scaled = estimate_lambda_max_scaled(fine, 10, 20240811u);
+    lap("lambda");
     const double omega = sp.amg_omega / lv.lambda_max_scaled;
-    HostCsr scaled = fine;
     const std::vector<double> d = diagonal(fine);
+    // EQS_SPGEMM_BATCH: products per device batch (tests force many batches)
+    const long long batch = getenv("EQS_SPGEMM_BATCH") ? atoll(getenv("EQS_SPGEMM_BATCH")) : (1ll << 28);
+    HostCsr p;
+    if (device >= 0) {
+      p = spgemm_device(fine, p_tent, device, &d, omega, batch);  // (I - omega D^-1 A) P_tent on the device
+    } else {
+      HostCsr scaled = fine;
 #pragma omp parallel for schedule(static)
-    for (int i = 0; i < fine.n_rows; ++i)
-      for (int k = scaled.row_ptr[i]; k < scaled.row_ptr[i + 1]; ++k) {
-        scaled.values[k] = -omega * scaled.values[k] / d[i];
-        if (scaled.col_idx[k] == i) scaled.values[k] += 1.0;
-      }
-    HostCsr p = multiply(scaled, p_tent);
+      for (int i = 0; i < fine.n_rows; ++i)
+        for (int k = scaled.row_ptr[i]; k < scaled.row_ptr[i + 1]; ++k) {
+          scaled.values[k] = -omega * scaled.values[k] / d[i];
+          if (scaled.col_idx[k] == i) scaled.values[k] += 1.0;
+        }
+      p = multiply(scaled, p_tent);
+    }
+    lap("P");
     HostCsr r = transposed(p);
-    HostCsr coarse = multiply(r, multiply(fine, p));
+    lap("R");
+    HostCsr ap = device >= 0 ? spgemm_device(fine, p, device, nullptr, 0.0, batch) : multiply(fine, p);
+    lap("AP");
+    HostCsr coarse = device >= 0 ? spgemm_device(r, ap, device, nullptr, 0.0, batch) : multiply(r, ap);
+    lap("RAP");
     lv.P = std::move(p);
     lv.R = std::move(r);
     lv.aggregates = std::move(agg);

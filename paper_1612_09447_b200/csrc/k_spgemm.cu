@@ -1,0 +1,228 @@
+// Device Galerkin products for the SA-AMG setup:
+// C = A B with the reference's per-row arithmetic (proj/src/csr.cpp:133-166),
+// bit-identical to the host Gustavson product.
+//
+// The host accumulates row i as accum[j] += a_ik * b_kj in encounter order
+// (ka ascending, then kb ascending), starting from 0.0, products and sums
+// rounded separately (-ffp-contract=off). The device reproduces exactly that
+// order with expand-sort-compress:
+//   1. expand: one warp per row writes every product (key = local row << jbits
+//      | j, value = __dmul_rn(a, b)) at its encounter position;
+//   2. a stable LSD radix sort on the key (cub::DeviceRadixSort) groups equal
+//      (row, j) while keeping encounter order inside each group, and orders
+//      the columns of each row ascending, as the host's std::sort does;
+//   3. compress: the first entry of every group sums its group sequentially
+//      with __dadd_rn from 0.0.
+// Rows are processed in batches that bound the product buffers. Optionally A
+// is replaced on the fly by the damped-Jacobi smoother I - omega D^-1 A with
+// the host's expression order ((-omega * a) / d, then + 1 on the diagonal;
+// amg.cpp:121-126), so P = (I - omega D^-1 A) P_tent needs no host copy of A.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
+#include "eqs_internal.hpp"
+#include "gpu_system.hpp"
+
+namespace eqsb {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string("spgemm: ") + what + ": " + cudaGetErrorString(e));
+}
+
+__global__ void k_spgemm_count(int m, const int* __restrict__ arp, const int* __restrict__ aci,
+                               const int* __restrict__ brp, long long* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  long long s = 0;
+  for (int ka = arp[i]; ka < arp[i + 1]; ++ka) {
+    const int k = aci[ka];
+    s += brp[k + 1] - brp[k];
+  }
+  cnt[i] = s;
+}
+
+template <bool SCALED>
+__global__ void k_spgemm_expand(int r0, int r1, long long base, const long long* __restrict__ off,
+                                const int* __restrict__ arp, const int* __restrict__ aci,
+                                const double* __restrict__ av, const int* __restrict__ brp,
+                                const int* __restrict__ bci, const double* __restrict__ bv,
+                                const double* __restrict__ diag, double neg_omega, int jbits,
+                                unsigned long long* __restrict__ keys, double* __restrict__ vals) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int i = r0 + warp;
+  if (i >= r1) return;
+  long long pos = off[i] - base;
+  const unsigned long long rowkey = (unsigned long long)(i - r0) << jbits;
+  for (int ka = arp[i]; ka < arp[i + 1]; ++ka) {
+    const int k = aci[ka];
+    double a = av[ka];
+    if (SCALED) {
+      a = __ddiv_rn(__dmul_rn(neg_omega, a), diag[i]);
+      if (k == i) a = __dadd_rn(a, 1.0);
+    }
+    const int b0 = brp[k], len = brp[k + 1] - b0;
+    for (int t = lane; t < len; t += 32) {
+      keys[pos + t] = rowkey | (unsigned)bci[b0 + t];
+      vals[pos + t] = __dmul_rn(a, bv[b0 + t]);
+    }
+    pos += len;
+  }
+}
+
+__global__ void k_spgemm_heads(long long n, const unsigned long long* __restrict__ keys, int* __restrict__ head) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    head[t] = (t == 0 || keys[t] != keys[t - 1]) ? 1 : 0;
+}
+
+__global__ void k_spgemm_reduce(long long n, const unsigned long long* __restrict__ keys,
+                                const double* __restrict__ vals, const int* __restrict__ head,
+                                const int* __restrict__ idx, int jbits, int* __restrict__ out_col,
+                                double* __restrict__ out_val, int* __restrict__ row_cnt) {
+  const unsigned long long jmask = (1ull << jbits) - 1;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    if (!head[t]) continue;
+    const unsigned long long key = keys[t];
+    double s = 0.0;
+    for (long long u = t; u < n && keys[u] == key; ++u) s = __dadd_rn(s, vals[u]);
+    out_col[idx[t]] = (int)(key & jmask);
+    out_val[idx[t]] = s;
+    atomicAdd(&row_cnt[key >> jbits], 1);
+  }
+}
+
+int bits_for(long long v) {  // bits to represent 0..v
+  int b = 1;
+  while (b < 62 && (1ll << b) <= v) ++b;
+  return b;
+}
+
+template <class T>
+void up(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
+  d.alloc(std::max<size_t>(1, h.size()));
+  if (!h.empty()) d.upload(h.data(), h.size(), s);
+}
+
+}  // namespace
+
+HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std::vector<double>* diag,
+                      double omega, long long batch_products) {
+  if (a.n_cols != b.n_rows) throw NumericalError("csr multiply: dimension mismatch");
+  ck(cudaSetDevice(device), "set device");
+  cudaStream_t s;
+  ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  const int m = a.n_rows;
+  HostCsr c;
+  c.n_rows = m;
+  c.n_cols = b.n_cols;
+  c.row_ptr.assign(m + 1, 0);
+  DevBuf<int> arp, aci, brp, bci;
+  DevBuf<double> av, bv, dg;
+  up(arp, a.row_ptr, s);
+  up(aci, a.col_idx, s);
+  up(av, a.values, s);
+  up(brp, b.row_ptr, s);
+  up(bci, b.col_idx, s);
+  up(bv, b.values, s);
+  if (diag) up(dg, *diag, s);
+  // per-row product counts -> offsets
+  DevBuf<long> cnt, off;
+  cnt.alloc(std::max(1, m));
+  off.alloc(m + 1);
+  if (m > 0) k_spgemm_count<<<(m + 255) / 256, 256, 0, s>>>(m, arp.p, aci.p, brp.p, (long long*)cnt.p);
+  ck(cudaMemsetAsync(off.p, 0, sizeof(long), s), "memset");
+  size_t tmp_bytes = 0;
+  ck(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, (long long*)cnt.p, (long long*)off.p + 1, m, s), "scan size");
+  DevBuf<unsigned char> tmp;
+  tmp.alloc(std::max<size_t>(1, tmp_bytes));
+  if (m > 0) ck(cub::DeviceScan::InclusiveSum(tmp.p, tmp_bytes, (long long*)cnt.p, (long long*)off.p + 1, m, s), "scan");
+  std::vector<long> hoff(m + 1);
+  off.download(hoff.data(), m + 1, s);
+  ck(cudaStreamSynchronize(s), "offsets");
+  const int jbits = bits_for(std::max(1, b.n_cols - 1));
+  const int kMaxBatchRows = 1 << 22;
+  long long max_batch = 0;
+  std::vector<std::pair<int, int>> batches;
+  for (int r0 = 0; r0 < m;) {
+    int r1 = r0 + 1;
+    while (r1 < m && r1 - r0 < kMaxBatchRows && hoff[r1 + 1] - hoff[r0] <= batch_products) ++r1;
+    batches.push_back({r0, r1});
+    max_batch = std::max<long long>(max_batch, hoff[r1] - hoff[r0]);
+    r0 = r1;
+  }
+  if (max_batch >= (1ll << 31)) throw CudaError("spgemm: a single row has more than 2^31 products");
+  const size_t cap = std::max<long long>(1, max_batch);
+  DevBuf<unsigned long long> k_in, k_out;
+  DevBuf<double> v_in, v_out, o_val;
+  DevBuf<int> head, idx, o_col, rcnt;
+  k_in.alloc(cap);
+  k_out.alloc(cap);
+  v_in.alloc(cap);
+  v_out.alloc(cap);
+  head.alloc(cap);
+  idx.alloc(cap);
+  o_col.alloc(cap);
+  o_val.alloc(cap);
+  rcnt.alloc(std::min(m, kMaxBatchRows) + 1);
+  // temp storage for the largest batch (sizes grow with n)
+  size_t sort_bytes = 0, scan_bytes = 0;
+  ck(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, k_in.p, k_out.p, v_in.p, v_out.p, (int)cap, 0, 64, s),
+     "sort size");
+  ck(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, head.p, idx.p, (int)cap, s), "scan size");
+  tmp.alloc(std::max<size_t>({1, sort_bytes, scan_bytes}));
+  c.col_idx.reserve((size_t)std::min<long long>(hoff[m], (1ll << 31) - 1));
+  c.values.reserve(c.col_idx.capacity());
+  std::vector<int> rc;
+  const double neg_omega = -omega;
+  for (auto [r0, r1] : batches) {
+    const long long base = hoff[r0], n = hoff[r1] - base;
+    const int nr = r1 - r0;
+    if (n == 0) continue;  // empty rows: row_ptr already zero-length
+    const int warps_per_block = 8;
+    const int blocks = (nr + warps_per_block - 1) / warps_per_block;
+    if (diag)
+      k_spgemm_expand<true><<<blocks, 32 * warps_per_block, 0, s>>>(r0, r1, base, (const long long*)off.p, arp.p, aci.p,
+                                                                    av.p, brp.p, bci.p, bv.p, dg.p, neg_omega, jbits,
+                                                                    k_in.p, v_in.p);
+    else
+      k_spgemm_expand<false><<<blocks, 32 * warps_per_block, 0, s>>>(r0, r1, base, (const long long*)off.p, arp.p,
+                                                                     aci.p, av.p, brp.p, bci.p, bv.p, nullptr, 0.0,
+                                                                     jbits, k_in.p, v_in.p);
+    ck(cudaGetLastError(), "expand");
+    const int end_bit = jbits + bits_for(std::max(1, nr - 1));
+    size_t tb = tmp.n;
+    ck(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in.p, k_out.p, v_in.p, v_out.p, (int)n, 0, end_bit, s), "sort");
+    const int grid = (int)std::min<long long>((n + 255) / 256, 148 * 16);
+    k_spgemm_heads<<<grid, 256, 0, s>>>(n, k_out.p, head.p);
+    tb = tmp.n;
+    ck(cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.p, idx.p, (int)n, s), "scan");
+    ck(cudaMemsetAsync(rcnt.p, 0, sizeof(int) * nr, s), "memset");
+    k_spgemm_reduce<<<grid, 256, 0, s>>>(n, k_out.p, v_out.p, head.p, idx.p, jbits, o_col.p, o_val.p, rcnt.p);
+    ck(cudaGetLastError(), "reduce");
+    int last_idx = 0, last_head = 0;
+    ck(cudaMemcpyAsync(&last_idx, idx.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaMemcpyAsync(&last_head, head.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "batch");
+    const long long nu = (long long)last_idx + last_head;
+    if ((long long)c.col_idx.size() + nu >= (1ll << 31)) throw CudaError("spgemm: product has more than 2^31 entries");
+    const size_t at = c.col_idx.size();
+    c.col_idx.resize(at + nu);
+    c.values.resize(at + nu);
+    rc.resize(nr);
+    o_col.download(c.col_idx.data() + at, nu, s);
+    o_val.download(c.values.data() + at, nu, s);
+    rcnt.download(rc.data(), nr, s);
+    ck(cudaStreamSynchronize(s), "download");
+    for (int r = 0; r < nr; ++r) c.row_ptr[r0 + r + 1] = rc[r];
+  }
+  for (int i = 0; i < m; ++i) c.row_ptr[i + 1] += c.row_ptr[i];
+  ck(cudaStreamDestroy(s), "stream destroy");
+  return c;
+}
+
+}  // namespace eqsb

@@ -290,6 +290,18 @@ class FemSystem:
         _check(load_library().eqs_amg_aggregates(self._h, C.c_int(level), _ip(a)))
         return a
 
+    def amg_level_csr(self, level: int, which: int = 0):
+        """(rows, cols, row_ptr, col_idx, values) of A (0), P (1) or R (2) at a level."""
+        L = load_library()
+        dims = np.zeros(3, dtype=np.int32)
+        _check(L.eqs_amg_level_csr(self._h, C.c_int(level), C.c_int(which), _ip(dims), None, None, None))
+        rows, cols, nnz = (int(v) for v in dims)
+        rp = np.zeros(rows + 1, dtype=np.int32)
+        ci = np.zeros(nnz, dtype=np.int32)
+        v = np.zeros(nnz)
+        _check(L.eqs_amg_level_csr(self._h, C.c_int(level), C.c_int(which), _ip(dims), _ip(rp), _ip(ci), _dp(v)))
+        return rows, cols, rp, ci, v
+
     # --- MatFreeStiffness (proj/src/matfree.cpp:90-143)
     def kx_apply(self, x_state, v) -> np.ndarray:
         y = np.zeros(self.n_dofs)

@@ -126,3 +126,18 @@ def test_msh_roundtrip_loads_same_mesh(tmp_path):
     assert np.array_equal(g.colors(), o2.colors())
     for a, b in zip(o2.mass(0), g.mass(0)):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("cfg", [cube(10, jitter=0.1), cube(3, jitter=0.1, order=2),
+                                 slab_reference("slab_nonlinear_rkc_spe")], ids=lambda c: c.get("name", "setup"))
+def test_amg_hierarchy_values_bit_exact(cfg):
+    """Galerkin hierarchy A_l, P_l, R_l (amg.cpp:90-143) of the host setup
+    (row-parallel SpGEMM) == the oracle's, bit for bit."""
+    g, o = eb.FemSystem(cfg, device=-1), po.Problem(cfg)
+    n_levels = len(o.amg_levels())
+    for lvl in range(n_levels):
+        for which in ((0, 1, 2) if lvl + 1 < n_levels else (0,)):
+            a, b = po.amg_level_csr(o, lvl, which), g.amg_level_csr(lvl, which)
+            assert a[:2] == b[:2]
+            for x, y in zip(a[2:], b[2:]):
+                assert np.array_equal(x, y), (lvl, which)
