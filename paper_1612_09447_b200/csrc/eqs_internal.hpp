@@ -6,6 +6,7 @@
 #include <array>
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -131,6 +132,22 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device = -1
 // (k_spgemm.cu). With diag, A is replaced by I - omega D^-1 A on the fly.
 HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std::vector<double>* diag = nullptr,
                       double omega = 0.0, long long batch_products = 1ll << 28);
+// Device-resident Galerkin chain of build_amg: the fine operator and P stay on
+// the GPU; only P (for R = P^T on the host) and the coarse operator come back.
+class AmgDeviceBuilder {
+ public:
+  explicit AmgDeviceBuilder(int device);
+  ~AmgDeviceBuilder();
+  // P = (I - omega D^-1 A) P_tent (fine is uploaded on the first call only)
+  HostCsr prolongator(const HostCsr& fine, const HostCsr& p_tent, const std::vector<double>& d, double omega,
+                      long long batch);
+  // R (A P) with A and P resident; the result becomes the next fine operator
+  HostCsr galerkin(const HostCsr& r, long long batch);
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
 // explicit inverse (row-major) of a symmetric matrix through the pivoted LDLT
 // below (the coarsest-level solve, amg.cpp:140); threaded for the larger
 // dense coarse levels of the device V-cycle (SolverParams::amg_dense_coarse)

@@ -118,7 +118,8 @@ void upload_sell16(const HostCsr& h, const HostSell& hs, DevCsr& d, SellBufs& b,
   }
   {
     std::vector<uint16_t> v(hs.src.size());
-    for (size_t k = 0; k < v.size(); ++k) v[k] = hs.src[k] >= 0 ? to_bf16(h.values[hs.src[k]]) : 0;
+#pragma omp parallel for schedule(static)
+    for (long k = 0; k < (long)v.size(); ++k) v[k] = hs.src[k] >= 0 ? to_bf16(h.values[hs.src[k]]) : 0;
     b.v16.alloc(np);
     b.v16.upload(v.data(), v.size(), s);
     CK(cudaStreamSynchronize(s));

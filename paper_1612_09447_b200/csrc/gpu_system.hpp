@@ -59,6 +59,11 @@ struct DevBuf {
     o.p = nullptr;
     o.n = 0;
   }
+  DevBuf& operator=(DevBuf&& o) noexcept {  // swap: the old buffer is freed with o
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    return *this;
+  }
   ~DevBuf();
   void alloc(size_t count);
   void upload(const T* host, size_t count, cudaStream_t s);

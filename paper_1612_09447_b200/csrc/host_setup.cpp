@@ -319,23 +319,51 @@ HostCsr multiply(const HostCsr& a, const HostCsr& b) {
   return c;
 }
 
-// proj/src/csr.cpp:52-70
+// proj/src/csr.cpp:52-70. Threads own contiguous row ranges; each column's
+// entries are laid out thread by thread, so the result (entries of a column in
+// ascending row order) is the serial one.
 HostCsr transposed(const HostCsr& a) {
   HostCsr t;
   t.n_rows = a.n_cols;
   t.n_cols = a.n_rows;
   t.row_ptr.assign(a.n_cols + 1, 0);
-  for (int c : a.col_idx) ++t.row_ptr[c + 1];
-  for (int i = 0; i < a.n_cols; ++i) t.row_ptr[i + 1] += t.row_ptr[i];
   t.col_idx.resize(a.col_idx.size());
   t.values.resize(a.values.size());
-  std::vector<int> next(t.row_ptr.begin(), t.row_ptr.end() - 1);
-  for (int i = 0; i < a.n_rows; ++i)
-    for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
-      const int pos = next[a.col_idx[k]]++;
-      t.col_idx[pos] = i;
-      t.values[pos] = a.values[k];
+  const int nt = std::max(1, std::min(omp_get_max_threads(), a.n_rows / 4096 + 1));
+  std::vector<std::vector<int>> cnt(nt);
+#pragma omp parallel num_threads(nt)
+  {
+    const int tid = omp_get_thread_num();
+    const long lo = (long)a.n_rows * tid / nt, hi = (long)a.n_rows * (tid + 1) / nt;
+    std::vector<int>& c = cnt[tid];
+    c.assign(a.n_cols, 0);
+    for (long i = lo; i < hi; ++i)
+      for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) ++c[a.col_idx[k]];
+#pragma omp barrier
+#pragma omp for schedule(static)
+    for (int col = 0; col < a.n_cols; ++col) {
+      int s = 0;
+      for (int q = 0; q < nt; ++q) s += cnt[q][col];
+      t.row_ptr[col + 1] = s;
     }
+#pragma omp single
+    for (int col = 0; col < a.n_cols; ++col) t.row_ptr[col + 1] += t.row_ptr[col];
+#pragma omp for schedule(static)
+    for (int col = 0; col < a.n_cols; ++col) {  // per-thread start of each column: row_ptr + earlier threads
+      int s = t.row_ptr[col];
+      for (int q = 0; q < nt; ++q) {
+        const int c = cnt[q][col];
+        cnt[q][col] = s;
+        s += c;
+      }
+    }
+    for (long i = lo; i < hi; ++i)
+      for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+        const int pos = c[a.col_idx[k]]++;
+        t.col_idx[pos] = (int)i;
+        t.values[pos] = a.values[k];
+      }
+  }
   return t;
 }
 
@@ -416,6 +444,7 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device) {
   if (symmetry_error(a) > 1e-10) throw std::invalid_argument("amg: matrix is not symmetric");
   check_diagonal(a);
   AmgHierarchy h;
+  std::unique_ptr<AmgDeviceBuilder> dev_builder;
   h.levels.push_back({a, {}, {}, {}, 0.0});
   while ((int)h.levels.size() < sp.amg_max_levels && h.levels.back().A.n_rows > sp.amg_coarse_limit) {
     AmgHostLevel& lv = h.levels.back();
@@ -455,7 +484,8 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device) {
     const long long batch = getenv("EQS_SPGEMM_BATCH") ? atoll(getenv("EQS_SPGEMM_BATCH")) : (1ll << 28);
     HostCsr p;
     if (device >= 0) {
-      p = spgemm_device(fine, p_tent, device, &d, omega, batch);  // (I - omega D^-1 A) P_tent on the device
+      if (!dev_builder) dev_builder = std::make_unique<AmgDeviceBuilder>(device);
+      p = dev_builder->prolongator(fine, p_tent, d, omega, batch);  // (I - omega D^-1 A) P_tent on the device
     } else {
       HostCsr scaled = fine;
 #pragma omp parallel for schedule(static)
@@ -469,9 +499,7 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device) {
     lap("P");
     HostCsr r = transposed(p);
     lap("R");
-    HostCsr ap = device >= 0 ? spgemm_device(fine, p, device, nullptr, 0.0, batch) : multiply(fine, p);
-    lap("AP");
-    HostCsr coarse = device >= 0 ? spgemm_device(r, ap, device, nullptr, 0.0, batch) : multiply(r, ap);
+    HostCsr coarse = device >= 0 ? dev_builder->galerkin(r, batch) : multiply(r, multiply(fine, p));
     lap("RAP");
     lv.P = std::move(p);
     lv.R = std::move(r);

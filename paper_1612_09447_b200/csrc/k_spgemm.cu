@@ -92,7 +92,7 @@ __global__ void k_spgemm_reduce(long long n, const unsigned long long* __restric
     for (long long u = t; u < n && keys[u] == key; ++u) s = __dadd_rn(s, vals[u]);
     out_col[idx[t]] = (int)(key & jmask);
     out_val[idx[t]] = s;
-    atomicAdd(&row_cnt[key >> jbits], 1);
+    atomicAdd(&row_cnt[key >> jbits], 1);  // row_cnt points at the batch's first row
   }
 }
 
@@ -102,39 +102,79 @@ int bits_for(long long v) {  // bits to represent 0..v
   return b;
 }
 
+}  // namespace
+
 template <class T>
 void up(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
   d.alloc(std::max<size_t>(1, h.size()));
   if (!h.empty()) d.upload(h.data(), h.size(), s);
 }
+template void up(DevBuf<double>&, const std::vector<double>&, cudaStream_t);
 
-}  // namespace
+// ---------------------------------------------------------------- device CSR products
+struct DCsr {
+  int rows = 0, cols = 0;
+  long long nnz = 0;
+  DevBuf<int> rp, ci;
+  DevBuf<double> v;
+};
+class SpgemmDevice {
+ public:
+  SpgemmDevice() = default;
+  ~SpgemmDevice();
+  void init(int device);
+  cudaStream_t stream() const { return s_; }
+  void upload(const HostCsr& h, DCsr& d);
+  void download(const DCsr& d, HostCsr& h);
+  void multiply(const DCsr& a, const DCsr& b, DCsr& c, const double* diag_dev, double omega, long long batch);
 
-HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std::vector<double>* diag,
-                      double omega, long long batch_products) {
-  if (a.n_cols != b.n_rows) throw NumericalError("csr multiply: dimension mismatch");
+ private:
+  int device_ = -1;
+  cudaStream_t s_ = nullptr;
+};
+
+void SpgemmDevice::init(int device) {
+  device_ = device;
   ck(cudaSetDevice(device), "set device");
-  cudaStream_t s;
-  ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-  const int m = a.n_rows;
-  HostCsr c;
-  c.n_rows = m;
-  c.n_cols = b.n_cols;
-  c.row_ptr.assign(m + 1, 0);
-  DevBuf<int> arp, aci, brp, bci;
-  DevBuf<double> av, bv, dg;
-  up(arp, a.row_ptr, s);
-  up(aci, a.col_idx, s);
-  up(av, a.values, s);
-  up(brp, b.row_ptr, s);
-  up(bci, b.col_idx, s);
-  up(bv, b.values, s);
-  if (diag) up(dg, *diag, s);
+  ck(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
+}
+SpgemmDevice::~SpgemmDevice() {
+  if (s_) cudaStreamDestroy(s_);
+}
+
+void SpgemmDevice::upload(const HostCsr& h, DCsr& d) {
+  d.rows = h.n_rows;
+  d.cols = h.n_cols;
+  d.nnz = h.nnz();
+  up(d.rp, h.row_ptr, s_);
+  up(d.ci, h.col_idx, s_);
+  up(d.v, h.values, s_);
+}
+
+void SpgemmDevice::download(const DCsr& d, HostCsr& h) {
+  h.n_rows = d.rows;
+  h.n_cols = d.cols;
+  h.row_ptr.resize(d.rows + 1);
+  h.col_idx.resize(d.nnz);
+  h.values.resize(d.nnz);
+  d.rp.download(h.row_ptr.data(), d.rows + 1, s_);
+  d.ci.download(h.col_idx.data(), d.nnz, s_);
+  d.v.download(h.values.data(), d.nnz, s_);
+  ck(cudaStreamSynchronize(s_), "download");
+}
+
+void SpgemmDevice::multiply(const DCsr& a, const DCsr& b, DCsr& c, const double* diag_dev, double omega,
+                            long long batch_products) {
+  if (a.cols != b.rows) throw NumericalError("csr multiply: dimension mismatch");
+  cudaStream_t s = s_;
+  const int m = a.rows;
+  c.rows = m;
+  c.cols = b.cols;
   // per-row product counts -> offsets
   DevBuf<long> cnt, off;
   cnt.alloc(std::max(1, m));
   off.alloc(m + 1);
-  if (m > 0) k_spgemm_count<<<(m + 255) / 256, 256, 0, s>>>(m, arp.p, aci.p, brp.p, (long long*)cnt.p);
+  if (m > 0) k_spgemm_count<<<(m + 255) / 256, 256, 0, s>>>(m, a.rp.p, a.ci.p, b.rp.p, (long long*)cnt.p);
   ck(cudaMemsetAsync(off.p, 0, sizeof(long), s), "memset");
   size_t tmp_bytes = 0;
   ck(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, (long long*)cnt.p, (long long*)off.p + 1, m, s), "scan size");
@@ -144,7 +184,7 @@ HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std:
   std::vector<long> hoff(m + 1);
   off.download(hoff.data(), m + 1, s);
   ck(cudaStreamSynchronize(s), "offsets");
-  const int jbits = bits_for(std::max(1, b.n_cols - 1));
+  const int jbits = bits_for(std::max(1, b.cols - 1));
   const int kMaxBatchRows = 1 << 22;
   long long max_batch = 0;
   std::vector<std::pair<int, int>> batches;
@@ -158,41 +198,40 @@ HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std:
   if (max_batch >= (1ll << 31)) throw CudaError("spgemm: a single row has more than 2^31 products");
   const size_t cap = std::max<long long>(1, max_batch);
   DevBuf<unsigned long long> k_in, k_out;
-  DevBuf<double> v_in, v_out, o_val;
-  DevBuf<int> head, idx, o_col, rcnt;
+  DevBuf<double> v_in, v_out;
+  DevBuf<int> head, idx, rcnt;
   k_in.alloc(cap);
   k_out.alloc(cap);
   v_in.alloc(cap);
   v_out.alloc(cap);
   head.alloc(cap);
   idx.alloc(cap);
-  o_col.alloc(cap);
-  o_val.alloc(cap);
-  rcnt.alloc(std::min(m, kMaxBatchRows) + 1);
-  // temp storage for the largest batch (sizes grow with n)
+  rcnt.alloc(m + 1);
+  ck(cudaMemsetAsync(rcnt.p, 0, sizeof(int) * (m + 1), s), "memset");
   size_t sort_bytes = 0, scan_bytes = 0;
   ck(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, k_in.p, k_out.p, v_in.p, v_out.p, (int)cap, 0, 64, s),
      "sort size");
   ck(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, head.p, idx.p, (int)cap, s), "scan size");
   tmp.alloc(std::max<size_t>({1, sort_bytes, scan_bytes}));
-  c.col_idx.reserve((size_t)std::min<long long>(hoff[m], (1ll << 31) - 1));
-  c.values.reserve(c.col_idx.capacity());
-  std::vector<int> rc;
-  const double neg_omega = -omega;
+  // batch outputs (compressed entries in row-major, column-sorted order)
+  std::vector<DevBuf<int>> out_c;
+  std::vector<DevBuf<double>> out_v;
+  std::vector<long long> out_n;
+  long long total = 0;
   for (auto [r0, r1] : batches) {
     const long long base = hoff[r0], n = hoff[r1] - base;
     const int nr = r1 - r0;
-    if (n == 0) continue;  // empty rows: row_ptr already zero-length
+    if (n == 0) continue;
     const int warps_per_block = 8;
     const int blocks = (nr + warps_per_block - 1) / warps_per_block;
-    if (diag)
-      k_spgemm_expand<true><<<blocks, 32 * warps_per_block, 0, s>>>(r0, r1, base, (const long long*)off.p, arp.p, aci.p,
-                                                                    av.p, brp.p, bci.p, bv.p, dg.p, neg_omega, jbits,
-                                                                    k_in.p, v_in.p);
+    if (diag_dev)
+      k_spgemm_expand<true><<<blocks, 32 * warps_per_block, 0, s>>>(r0, r1, base, (const long long*)off.p, a.rp.p,
+                                                                    a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, diag_dev,
+                                                                    -omega, jbits, k_in.p, v_in.p);
     else
-      k_spgemm_expand<false><<<blocks, 32 * warps_per_block, 0, s>>>(r0, r1, base, (const long long*)off.p, arp.p,
-                                                                     aci.p, av.p, brp.p, bci.p, bv.p, nullptr, 0.0,
-                                                                     jbits, k_in.p, v_in.p);
+      k_spgemm_expand<false><<<blocks, 32 * warps_per_block, 0, s>>>(r0, r1, base, (const long long*)off.p, a.rp.p,
+                                                                     a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, nullptr,
+                                                                     0.0, jbits, k_in.p, v_in.p);
     ck(cudaGetLastError(), "expand");
     const int end_bit = jbits + bits_for(std::max(1, nr - 1));
     size_t tb = tmp.n;
@@ -201,27 +240,96 @@ HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std:
     k_spgemm_heads<<<grid, 256, 0, s>>>(n, k_out.p, head.p);
     tb = tmp.n;
     ck(cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.p, idx.p, (int)n, s), "scan");
-    ck(cudaMemsetAsync(rcnt.p, 0, sizeof(int) * nr, s), "memset");
-    k_spgemm_reduce<<<grid, 256, 0, s>>>(n, k_out.p, v_out.p, head.p, idx.p, jbits, o_col.p, o_val.p, rcnt.p);
-    ck(cudaGetLastError(), "reduce");
     int last_idx = 0, last_head = 0;
     ck(cudaMemcpyAsync(&last_idx, idx.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
     ck(cudaMemcpyAsync(&last_head, head.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
     ck(cudaStreamSynchronize(s), "batch");
     const long long nu = (long long)last_idx + last_head;
-    if ((long long)c.col_idx.size() + nu >= (1ll << 31)) throw CudaError("spgemm: product has more than 2^31 entries");
-    const size_t at = c.col_idx.size();
-    c.col_idx.resize(at + nu);
-    c.values.resize(at + nu);
-    rc.resize(nr);
-    o_col.download(c.col_idx.data() + at, nu, s);
-    o_val.download(c.values.data() + at, nu, s);
-    rcnt.download(rc.data(), nr, s);
-    ck(cudaStreamSynchronize(s), "download");
-    for (int r = 0; r < nr; ++r) c.row_ptr[r0 + r + 1] = rc[r];
+    out_c.emplace_back();
+    out_v.emplace_back();
+    out_c.back().alloc(nu);
+    out_v.back().alloc(nu);
+    k_spgemm_reduce<<<grid, 256, 0, s>>>(n, k_out.p, v_out.p, head.p, idx.p, jbits, out_c.back().p, out_v.back().p,
+                                         rcnt.p + 1 + r0);
+    ck(cudaGetLastError(), "reduce");
+    out_n.push_back(nu);
+    total += nu;
   }
-  for (int i = 0; i < m; ++i) c.row_ptr[i + 1] += c.row_ptr[i];
-  ck(cudaStreamDestroy(s), "stream destroy");
+  if (total >= (1ll << 31)) throw CudaError("spgemm: product has more than 2^31 entries");
+  // free the batch work space before the result is assembled
+  k_in.alloc(0);
+  k_out.alloc(0);
+  v_in.alloc(0);
+  v_out.alloc(0);
+  head.alloc(0);
+  idx.alloc(0);
+  c.nnz = total;
+  c.ci.alloc(std::max<long long>(1, total));
+  c.v.alloc(std::max<long long>(1, total));
+  long long at = 0;
+  for (size_t q = 0; q < out_n.size(); ++q) {
+    if (out_n[q] == 0) continue;
+    ck(cudaMemcpyAsync(c.ci.p + at, out_c[q].p, sizeof(int) * out_n[q], cudaMemcpyDeviceToDevice, s), "d2d");
+    ck(cudaMemcpyAsync(c.v.p + at, out_v[q].p, sizeof(double) * out_n[q], cudaMemcpyDeviceToDevice, s), "d2d");
+    at += out_n[q];
+  }
+  // row_ptr = inclusive scan of the per-row counts (rcnt[0] = 0)
+  c.rp.alloc(m + 1);
+  size_t sb = 0;
+  ck(cub::DeviceScan::InclusiveSum(nullptr, sb, rcnt.p, c.rp.p, m + 1, s), "scan size");
+  tmp.alloc(std::max<size_t>(1, sb));
+  ck(cub::DeviceScan::InclusiveSum(tmp.p, sb, rcnt.p, c.rp.p, m + 1, s), "row_ptr");
+  ck(cudaStreamSynchronize(s), "assemble");
+}
+
+struct AmgDeviceBuilder::Impl {
+  SpgemmDevice sd;
+  DCsr fine, p;
+  bool has_fine = false;
+};
+AmgDeviceBuilder::AmgDeviceBuilder(int device) : impl_(std::make_unique<Impl>()) { impl_->sd.init(device); }
+AmgDeviceBuilder::~AmgDeviceBuilder() = default;
+
+HostCsr AmgDeviceBuilder::prolongator(const HostCsr& fine, const HostCsr& p_tent, const std::vector<double>& d,
+                                      double omega, long long batch) {
+  Impl& m = *impl_;
+  if (!m.has_fine) m.sd.upload(fine, m.fine);  // level 0; coarser levels are the previous R A P
+  m.has_fine = true;
+  DCsr pt;
+  m.sd.upload(p_tent, pt);
+  DevBuf<double> dg;
+  up(dg, d, m.sd.stream());
+  m.sd.multiply(m.fine, pt, m.p, dg.p, omega, batch);
+  HostCsr p;
+  m.sd.download(m.p, p);
+  return p;
+}
+
+HostCsr AmgDeviceBuilder::galerkin(const HostCsr& r, long long batch) {
+  Impl& m = *impl_;
+  DCsr ap, dr, coarse;
+  m.sd.multiply(m.fine, m.p, ap, nullptr, 0.0, batch);
+  m.p = DCsr();
+  m.sd.upload(r, dr);
+  m.sd.multiply(dr, ap, coarse, nullptr, 0.0, batch);
+  HostCsr c;
+  m.sd.download(coarse, c);
+  m.fine = std::move(coarse);  // next level's fine operator stays resident
+  return c;
+}
+
+HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std::vector<double>* diag,
+                      double omega, long long batch_products) {
+  SpgemmDevice sd;
+  sd.init(device);
+  DCsr da, db, dc;
+  sd.upload(a, da);
+  sd.upload(b, db);
+  DevBuf<double> dg;
+  if (diag) up(dg, *diag, sd.stream());
+  sd.multiply(da, db, dc, diag ? dg.p : nullptr, omega, batch_products);
+  HostCsr c;
+  sd.download(dc, c);
   return c;
 }
 

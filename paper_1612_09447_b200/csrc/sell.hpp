@@ -40,7 +40,8 @@ bool build_sell(const HostCsr& a, int tpr, HostSell& out);
 template <class T>
 std::vector<T> sell_values(const HostSell& s, const std::vector<double>& v) {
   std::vector<T> out(s.src.size());
-  for (size_t k = 0; k < s.src.size(); ++k) out[k] = s.src[k] >= 0 ? (T)v[s.src[k]] : (T)0.0;
+#pragma omp parallel for schedule(static)
+  for (long k = 0; k < (long)s.src.size(); ++k) out[k] = s.src[k] >= 0 ? (T)v[s.src[k]] : (T)0.0;
   return out;
 }
 
