@@ -431,7 +431,7 @@ def run_b200(args):
     # roofline of the dominant kernel class (TimeClass in gpu_system.hpp): per-class
     # device time from CUDA events on the library stream, algorithmic bytes per launch
     names = ["stiffness K(x)x", "pcg spmv+vectors", "v-cycle", "rkc stage/error", "spe estimator", "boundary"]
-    kernels = {0: "K(x)x two-pass stiffness operator (k_kx_p1 + k_kx_gather)",
+    kernels = {0: "K(x)x blocked stiffness operator (k_kx_block<4> + k_kx_partials)",
                1: "PCG fine-level M_II SpMV+dot (fp64 SELL-16, k_sell_red) and fused x/r update (k_pcg_update)",
                2: "AMG V-cycle graph: packed SELL-P bf16 smoother/residual/transfer row kernels, all levels"}
 

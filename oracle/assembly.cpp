@@ -290,6 +290,35 @@ CsrMatrix multiply(const CsrMatrix& a, const CsrMatrix& b) {
   }
   return c;
 }
+// proj/src/csr.cpp:168-195 (pattern union, values alpha a + beta b)
+CsrMatrix add(double alpha, const CsrMatrix& a, double beta, const CsrMatrix& b) {
+  if (a.n_rows != b.n_rows || a.n_cols != b.n_cols) throw NumericalError("csr add: dimension mismatch");
+  CsrMatrix c;
+  c.n_rows = a.n_rows;
+  c.n_cols = a.n_cols;
+  c.row_ptr.assign(a.n_rows + 1, 0);
+  for (int i = 0; i < a.n_rows; ++i) {
+    int ka = a.row_ptr[i], kb = b.row_ptr[i];
+    const int ea = a.row_ptr[i + 1], eb = b.row_ptr[i + 1];
+    while (ka < ea || kb < eb) {
+      const int ja = ka < ea ? a.col_idx[ka] : c.n_cols;
+      const int jb = kb < eb ? b.col_idx[kb] : c.n_cols;
+      if (ja == jb) {
+        c.col_idx.push_back(ja);
+        c.values.push_back(alpha * a.values[ka++] + beta * b.values[kb++]);
+      } else if (ja < jb) {
+        c.col_idx.push_back(ja);
+        c.values.push_back(alpha * a.values[ka++]);
+      } else {
+        c.col_idx.push_back(jb);
+        c.values.push_back(beta * b.values[kb++]);
+      }
+    }
+    c.row_ptr[i + 1] = (int)c.col_idx.size();
+  }
+  return c;
+}
+
 // proj/src/csr.cpp:197-229
 CsrMatrix extract_block(const CsrMatrix& a, const std::vector<int>& rows, const std::vector<int>& cols) {
   std::vector<int> col_map(a.n_cols, -1);

@@ -444,6 +444,20 @@ int ora_pod_build(int n, int k, const double* snaps, int rank, double* basis, in
     if (sigma) std::memcpy(sigma, sv.data(), sizeof(double) * sv.size());
   });
 }
+
+// sdirk_advance_fixed (integrators.cpp:329-341), nsteps fixed steps; returns
+// NumericalError when a Newton iteration fails
+int ora_sdirk_advance_fixed(void* h, double t, double* x, double dt, int nsteps) {
+  return guard([&] {
+    auto* p = static_cast<Problem*>(h);
+    IntegratorState st;
+    st.t = t;
+    st.x.assign(x, x + p->sys->size());
+    for (int i = 0; i < nsteps; ++i)
+      if (!sdirk_advance_fixed(st, *p->sys, dt, SdirkOptions{})) throw NumericalError("sdirk: Newton failed");
+    std::memcpy(x, st.x.data(), sizeof(double) * st.x.size());
+  });
+}
 }  // extern "C"
 
 extern "C" {

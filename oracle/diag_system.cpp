@@ -36,6 +36,12 @@ struct DiagonalSystem final : OdeSystem {
     for (size_t i = 0; i < v.size(); ++i) y[i] = stiffness[i] * v[i] / mass[i];
     ++stats_.rho_solves;
   }
+  void shifted_solve(double, const Vec&, double gdt, const Vec& rhs, Vec& delta, bool refresh) override {
+    if (refresh) ++stats_.precond_setups;  // test_helpers.hpp:67-72
+    delta.resize(rhs.size());
+    for (size_t i = 0; i < rhs.size(); ++i) delta[i] = rhs[i] / (mass[i] + gdt * stiffness[i]);
+    ++stats_.newton_linear_solves;
+  }
 };
 }  // namespace
 
@@ -63,7 +69,8 @@ int ora_diag_advance(void* h, int method, int s, double t, double dt, int nsteps
     st.x.assign(x, x + d->size());
     for (int i = 0; i < nsteps; ++i) {
       if (method == 0) euler_step(st, *d, dt);
-      else rkc_advance_fixed(st, *d, dt, s);
+      else if (method == 1) rkc_advance_fixed(st, *d, dt, s);
+      else if (!sdirk_advance_fixed(st, *d, dt, SdirkOptions{})) throw NumericalError("sdirk: Newton failed");
     }
     std::memcpy(x, st.x.data(), sizeof(double) * st.x.size());
     return 0;
@@ -95,6 +102,34 @@ int ora_diag_rkc_step(void* h, double t, double dt, double rtol, double atol, in
     out[4] = a.rho;
     out[5] = a.dt_next;
     out[6] = st.t;
+    return 0;
+  } catch (const std::exception& e) {
+    d_err = e.what();
+    return 7;
+  }
+}
+
+// one sdirk_step (integrators.cpp:297-327); out[0..6] = accepted, newton_iterations, dt, error, dt_next, t,
+// precond_setups
+int ora_diag_sdirk_step(void* h, double t, double dt, double rtol, double atol, double* x, double* out) {
+  auto* d = static_cast<DiagonalSystem*>(h);
+  try {
+    IntegratorState st;
+    st.t = t;
+    st.dt = dt;
+    st.x.assign(x, x + d->size());
+    SdirkOptions o;
+    o.control.rtol = rtol;
+    o.control.atol = atol;
+    const StepAttempt a = sdirk_step(st, *d, o);
+    std::memcpy(x, st.x.data(), sizeof(double) * st.x.size());
+    out[0] = a.accepted;
+    out[1] = a.newton_iterations;
+    out[2] = a.dt;
+    out[3] = a.error;
+    out[4] = a.dt_next;
+    out[5] = st.t;
+    out[6] = (double)d->stats().precond_setups;
     return 0;
   } catch (const std::exception& e) {
     d_err = e.what();

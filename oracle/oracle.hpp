@@ -134,6 +134,7 @@ struct CsrMatrix {
 };
 CsrMatrix multiply(const CsrMatrix& a, const CsrMatrix& b);
 CsrMatrix extract_block(const CsrMatrix& a, const std::vector<int>& rows, const std::vector<int>& cols);
+CsrMatrix add(double alpha, const CsrMatrix& a, double beta, const CsrMatrix& b);  // csr.cpp:168-195
 
 // ---------------------------------------------------------------- assembly
 struct TetGeometry {
@@ -347,6 +348,8 @@ class OdeSystem {
   virtual void eval_residual(double t, const Vec& x, Vec& r) = 0;
   virtual void mass_apply(const Vec& v, Vec& y) const = 0;
   virtual void apply_minv_stiffness(double t, const Vec& x_state, const Vec& v, Vec& y) = 0;
+  // (M + gdt K(z)) delta = rhs (ode_system.hpp:63-68, the SDIRK Newton matrix)
+  virtual void shifted_solve(double t, const Vec& z, double gdt, const Vec& rhs, Vec& delta, bool refresh_precond) = 0;
   SolveStats& stats() { return stats_; }
  protected:
   SolveStats stats_;
@@ -361,6 +364,7 @@ class FemSystem : public OdeSystem {
   void eval_residual(double t, const Vec& x, Vec& r) override;
   void mass_apply(const Vec& v, Vec& y) const override { mass_.AII.apply(v, y); }
   void apply_minv_stiffness(double t, const Vec& x_state, const Vec& v, Vec& y) override;
+  void shifted_solve(double t, const Vec& z, double gdt, const Vec& rhs, Vec& delta, bool refresh_precond) override;
   Vec lift_full(double t, const Vec& x_free) const;
   const CsrMatrix& mass_free() const { return mass_.AII; }
   const CsrMatrix& mass_ib() const { return mass_.AIB; }
@@ -381,6 +385,8 @@ class FemSystem : public OdeSystem {
   DirichletBlocks mass_;
   MatFreeStiffness matfree_;
   std::unique_ptr<LinearOperator> mass_precond_;
+  std::unique_ptr<LinearOperator> shifted_precond_;
+  std::unique_ptr<LinearOperator> make_preconditioner(const CsrMatrix& a);
   std::vector<SolveRecord> solve_records_;
 };
 
@@ -414,12 +420,16 @@ struct RkcCoefficients {
 struct RkcOptions { StepControl control; int max_stages = 200; int rho_refresh_every = 25; };
 StepAttempt rkc_step(IntegratorState& state, OdeSystem& system, const RkcOptions& options);
 void rkc_advance_fixed(IntegratorState& state, OdeSystem& system, double dt, int s);
+// proj/include/eqs/integrators.hpp:106-120
+struct SdirkOptions { StepControl control; double newton_tol = 1e-8; int max_newton = 25; };
+StepAttempt sdirk_step(IntegratorState& state, OdeSystem& system, const SdirkOptions& options);
+bool sdirk_advance_fixed(IntegratorState& state, OdeSystem& system, double dt, const SdirkOptions& options);
 
 // ---------------------------------------------------------------- helpers
 Vec random_vec(int n, unsigned seed);  // proj/tests/support/test_helpers.hpp:15-21
 
 // ---------------------------------------------------------------- scenario
-enum class IntegratorKind { Euler, Rkc };
+enum class IntegratorKind { Euler, Rkc, Sdirk32 };
 struct BoxSpec {
   int nx = 1, ny = 1, nz = 1;
   double lx = 1, ly = 1, lz = 1;

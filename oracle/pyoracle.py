@@ -255,6 +255,12 @@ class Problem:
         d["stages"] = int(d["stages"])
         return x, d
 
+    def sdirk_advance_fixed(self, t, x, dt, nsteps=1):
+        """sdirk_advance_fixed (integrators.cpp:329-341)."""
+        x = np.array(x, dtype=np.float64, copy=True)
+        _check(lib().ora_sdirk_advance_fixed(self._h, C.c_double(t), _ptr(x), C.c_double(dt), C.c_int(nsteps)))
+        return x
+
     def euler_step(self, t, x, dt):
         x = np.array(x, dtype=np.float64, copy=True)
         _check(lib().ora_euler_step(self._h, C.c_double(t), _ptr(x), C.c_double(dt)))
@@ -342,7 +348,8 @@ class DiagonalSystem:
 
     def advance(self, method: str, x, dt, nsteps=1, s=2, t=0.0):
         x = np.array(x, dtype=float, copy=True)
-        rc = lib().ora_diag_advance(self._h, C.c_int(0 if method == "euler" else 1), C.c_int(s), C.c_double(t),
+        code = {"euler": 0, "rkc": 1, "sdirk": 2}[method]
+        rc = lib().ora_diag_advance(self._h, C.c_int(code), C.c_int(s), C.c_double(t),
                                     C.c_double(dt), C.c_int(nsteps), _ptr(x))
         if rc:
             raise OracleError(rc, lib().ora_diag_last_error().decode())
@@ -359,6 +366,20 @@ class DiagonalSystem:
         d = dict(zip(keys, out.tolist()))
         d["accepted"] = bool(d["accepted"])
         d["stages"] = int(d["stages"])
+        return x, d
+
+    def sdirk_step(self, x, dt, rtol=1e-2, atol=1e-8, t=0.0):
+        x = np.array(x, dtype=float, copy=True)
+        out = np.zeros(7)
+        rc = lib().ora_diag_sdirk_step(self._h, C.c_double(t), C.c_double(dt), C.c_double(rtol), C.c_double(atol),
+                                       _ptr(x), _ptr(out))
+        if rc:
+            raise OracleError(rc, lib().ora_diag_last_error().decode())
+        d = dict(zip(("accepted", "newton_iterations", "dt", "error", "dt_next", "t", "precond_setups"),
+                     out.tolist()))
+        d["accepted"] = bool(d["accepted"])
+        d["newton_iterations"] = int(d["newton_iterations"])
+        d["precond_setups"] = int(d["precond_setups"])
         return x, d
 
     def spectral_radius(self):

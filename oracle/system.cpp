@@ -313,17 +313,44 @@ FemSystem::FemSystem(const TetMesh& mesh, const DofMap& dm, const MaterialTable&
 }
 
 // proj/src/fem_system.cpp:38-54
+std::unique_ptr<LinearOperator> FemSystem::make_preconditioner(const CsrMatrix& a) {  // fem_system.cpp:38-46
+  ++stats_.precond_setups;
+  switch (solver_.precond) {
+    case PrecondKind::Jacobi: return std::make_unique<JacobiPreconditioner>(a);
+    case PrecondKind::Ssor: return std::make_unique<SsorPreconditioner>(a);
+    case PrecondKind::Amg: return std::make_unique<AmgPreconditioner>(a, solver_.amg);
+  }
+  throw ConfigError("unknown preconditioner kind");
+}
+
 const LinearOperator& FemSystem::mass_preconditioner() {
   if (!mass_precond_) {
     PhaseTimer timer(stats_.timers.setup);
-    ++stats_.precond_setups;
-    switch (solver_.precond) {
-      case PrecondKind::Jacobi: mass_precond_ = std::make_unique<JacobiPreconditioner>(mass_.AII); break;
-      case PrecondKind::Ssor: mass_precond_ = std::make_unique<SsorPreconditioner>(mass_.AII); break;
-      case PrecondKind::Amg: mass_precond_ = std::make_unique<AmgPreconditioner>(mass_.AII, solver_.amg); break;
-    }
+    mass_precond_ = make_preconditioner(mass_.AII);
   }
   return *mass_precond_;
+}
+
+// proj/src/fem_system.cpp:124-145
+void FemSystem::shifted_solve(double t, const Vec& z_lin, double gdt, const Vec& rhs, Vec& delta,
+                              bool refresh_precond) {
+  CsrMatrix shifted;
+  {
+    PhaseTimer timer(stats_.timers.setup);
+    const Vec z_full = lift_full(t, z_lin);
+    const CsrMatrix k_full = assemble_stiffness(mesh_, dm_, materials_, z_full);
+    ++stats_.assemblies;
+    const CsrMatrix k_ii = extract_block(k_full, dm_.free_dofs, dm_.free_dofs);
+    shifted = add(1.0, mass_.AII, gdt, k_ii);
+    if (refresh_precond || !shifted_precond_) shifted_precond_ = make_preconditioner(shifted);
+  }
+  PhaseTimer timer(stats_.timers.solve);
+  CsrOperator op(shifted);
+  PcgResult res = pcg_solve(op, *shifted_precond_, rhs, Vec(), solver_.rel_tol, solver_.max_iter);
+  if (!res.converged) throw NumericalError("shifted-system solve failed to converge");
+  ++stats_.newton_linear_solves;
+  stats_.newton_pcg_iterations += res.iterations;
+  delta = std::move(res.x);
 }
 
 // proj/src/fem_system.cpp:56-60
@@ -615,6 +642,115 @@ void rkc_advance_fixed(IntegratorState& state, OdeSystem& system, double dt, int
   state.t += dt;
   ++state.stats.accepted;
   state.stats.stages += s;
+}
+
+
+// ---------------------------------------------------------------- SDIRK3(2)
+// proj/src/integrators.cpp:237-343: stiffly accurate SDIRK3(2), gamma the real
+// root of g^3 - 3g^2 + 3g/2 - 1/6; Newton per stage with M + gamma dt K(z).
+namespace {
+constexpr double kGamma = 0.435866521508459;
+constexpr double kSdC[3] = {kGamma, (1.0 + kGamma) / 2.0, 1.0};
+constexpr double kB1 = -1.5 * kGamma * kGamma + 4.0 * kGamma - 0.25;
+constexpr double kB2 = 1.5 * kGamma * kGamma - 5.0 * kGamma + 1.25;
+constexpr double kSdA[3][3] = {{kGamma, 0.0, 0.0}, {(1.0 - kGamma) / 2.0, kGamma, 0.0}, {kB1, kB2, kGamma}};
+constexpr double kBhat1 = kGamma / (1.0 - kGamma);
+constexpr double kBhat2 = 1.0 - kBhat1;
+
+bool sdirk_stages(IntegratorState& state, OdeSystem& system, double dt, const SdirkOptions& options, Vec& x_new,
+                  Vec& est, int& newton_iters) {
+  const double t = state.t;
+  const double gdt = kGamma * dt;
+  const size_t n = state.x.size();
+  Vec k[3];
+  Vec w, z, g(n), mz, r_ode, delta, zw(n), neg(n);
+  newton_iters = 0;
+  for (int stage = 0; stage < 3; ++stage) {
+    w = state.x;
+    for (int j = 0; j < stage; ++j) {
+      const double c = dt * kSdA[stage][j];
+      for (size_t i = 0; i < n; ++i) w[i] += c * k[j][i];
+    }
+    const double ts = t + kSdC[stage] * dt;
+    z = w;
+    double scale = -1.0;
+    bool converged = false;
+    for (int it = 0;; ++it) {
+      system.eval_residual(ts, z, r_ode);
+      for (size_t i = 0; i < n; ++i) zw[i] = z[i] - w[i];
+      system.mass_apply(zw, mz);
+      for (size_t i = 0; i < n; ++i) g[i] = mz[i] - gdt * r_ode[i];
+      const double gn = norm(g);
+      if (!std::isfinite(gn)) return false;
+      if (scale < 0.0) scale = gn;
+      if (gn <= options.newton_tol * scale || gn == 0.0) {
+        converged = true;
+        break;
+      }
+      if (it >= options.max_newton) break;
+      for (size_t i = 0; i < n; ++i) neg[i] = -g[i];
+      try {
+        system.shifted_solve(ts, z, gdt, neg, delta, stage == 0 && it == 0);
+      } catch (const NumericalError&) {
+        return false;
+      }
+      for (size_t i = 0; i < n; ++i) z[i] += delta[i];
+      ++newton_iters;
+    }
+    if (!converged) return false;
+    k[stage].resize(n);
+    for (size_t i = 0; i < n; ++i) k[stage][i] = (z[i] - w[i]) / gdt;
+  }
+  x_new = std::move(z);
+  est.assign(n, 0.0);
+  const double e0 = kSdA[2][0] - kBhat1, e1 = kSdA[2][1] - kBhat2;
+  for (size_t i = 0; i < n; ++i) est[i] = dt * (e0 * k[0][i] + e1 * k[1][i] + kGamma * k[2][i]);
+  return true;
+}
+}  // namespace
+
+StepAttempt sdirk_step(IntegratorState& state, OdeSystem& system, const SdirkOptions& options) {
+  StepAttempt att;
+  att.t_start = state.t;
+  att.dt = state.dt;
+  Vec x_new, est;
+  int newton_iters = 0;
+  const bool ok = sdirk_stages(state, system, state.dt, options, x_new, est, newton_iters);
+  att.newton_iterations = newton_iters;
+  state.stats.newton_iterations += newton_iters;
+  if (!ok) {
+    att.accepted = false;
+    att.dt_next = 0.5 * state.dt;
+    ++state.stats.rejected;
+    state.dt = att.dt_next;
+    return att;
+  }
+  att.error = weighted_rms(est, state.x, x_new, options.control.atol, options.control.rtol);
+  const ControllerDecision dec = step_controller(att.error, state.dt, 3);
+  bool finite = true;
+  for (double v : x_new) finite = finite && std::isfinite(v);
+  att.accepted = dec.accept && finite;
+  att.dt_next = dec.dt_next;
+  if (att.accepted) {
+    state.x = std::move(x_new);
+    state.t += state.dt;
+    ++state.stats.accepted;
+  } else {
+    ++state.stats.rejected;
+  }
+  state.dt = dec.dt_next;
+  return att;
+}
+
+bool sdirk_advance_fixed(IntegratorState& state, OdeSystem& system, double dt, const SdirkOptions& options) {
+  Vec x_new, est;
+  int newton_iters = 0;
+  if (!sdirk_stages(state, system, dt, options, x_new, est, newton_iters)) return false;
+  state.stats.newton_iterations += newton_iters;
+  state.x = std::move(x_new);
+  state.t += dt;
+  ++state.stats.accepted;
+  return true;
 }
 
 }  // namespace ora

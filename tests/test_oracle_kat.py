@@ -151,7 +151,7 @@ def test_convergence_orders():  # test_integrators.cpp:153-190
         p2 = 0.5 * (k * math.cos(b * t) + b * math.sin(b * t)) / (k * k + b * b)
         return p1 + p2 - (-a / (k * k + a * a) + 0.5 * k / (k * k + b * b)) * math.exp(-k * t)
 
-    for method, order, tol in (("euler", 1.0, 0.1), ("rkc", 2.0, 0.15)):
+    for method, order, tol in (("euler", 1.0, 0.1), ("rkc", 2.0, 0.15), ("sdirk", 3.0, 0.2)):
         errs = []
         for dt in (1 / 40, 1 / 80, 1 / 160, 1 / 320):
             sys_ = po.DiagonalSystem([1.0], [k], c1=1.0, w1=a, c2=0.5, w2=b)
@@ -160,6 +160,25 @@ def test_convergence_orders():  # test_integrators.cpp:153-190
         xs = -np.arange(4.0)
         slope = np.polyfit(xs, np.log2(errs), 1)[0]
         assert abs(slope - order) <= tol
+
+
+def test_sdirk_linear_one_newton_per_stage():  # test_integrators.cpp:192-203
+    sys_ = po.DiagonalSystem([1.0, 1.0, 1.0], [1.0, 5.0, 9.0])
+    _, att = sys_.sdirk_step(po.random_vec(3, 2), 0.05)
+    assert att["accepted"]
+    assert att["newton_iterations"] == 3
+    assert att["precond_setups"] == 1
+
+
+def test_embedded_error_scales_like_dt3():  # test_integrators.cpp:205-234 (sdirk branch)
+    est = []
+    for dt in (0.02, 0.01, 0.005, 0.0025):
+        sys_ = po.DiagonalSystem([1.0], [3.0], c2=1.0, w2=2.0)  # drive cos(2t)
+        _, att = sys_.sdirk_step([1.0], dt, rtol=0.0, atol=1.0)
+        assert att["accepted"]
+        est.append(att["error"])
+    slope = np.polyfit(-np.arange(4.0), np.log2(est), 1)[0]
+    assert abs(slope - 3.0) <= 0.3
 
 
 def test_spectral_radius_diag():  # test_integrators.cpp:73-85

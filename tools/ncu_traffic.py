@@ -6,7 +6,7 @@
 
 A "launch" of a class is what bench.py's roofline divides by: one V-cycle
 (graph replay), one PCG iteration (SpMV+dot and x/r update), one K(x)x
-(two passes). The V-cycle count is the number of fine-level post-smoother
+(k_kx_block + k_kx_partials, or the two-pass p1 + gather). The V-cycle count is the number of fine-level post-smoother
 launches (k_sellp_red<1, float, 3, ...>, once per V-cycle)."""
 import csv
 import json
@@ -36,7 +36,7 @@ def main():
             n_vc += 1
         if "k_sell_red<1, double, double, 0>" in n:
             n_pcg += 1
-        if "k_kx_p1" in n or "k_kx_p2" in n:
+        if "k_kx_p1" in n or "k_kx_p2" in n or "k_kx_block" in n:  # one per K(x)x apply
             n_kx += 1
         if "k_sell_red<1, double, double, 0>" in n or "k_pcg_update" in n or "k_pcg_direction" in n:
             cls["pcg spmv+vectors"] += b
