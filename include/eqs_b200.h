@@ -133,6 +133,14 @@ typedef struct {
   int rho_refresh_every;     /* 25 */
 } eqs_rkc_options;
 
+/* proj/include/eqs/integrators.hpp:106-110 (SdirkOptions); newton_tol <= 0 / max_newton <= 0 select
+ * the reference defaults 1e-8 / 25 */
+typedef struct {
+  double rtol, atol;
+  double newton_tol;
+  int max_newton;
+} eqs_sdirk_options;
+
 /* proj/include/eqs/integrators.hpp:32-41 */
 typedef struct {
   double t_start, dt;
@@ -274,6 +282,18 @@ int eqs_rkc_step(eqs_ctx* ctx, const eqs_rkc_options* opts, eqs_step_attempt* at
 int eqs_rkc_advance_fixed(eqs_ctx* ctx, double dt, int s, int nsteps);
 /* euler_step (proj/src/integrators.cpp:33-47). */
 int eqs_euler_step(eqs_ctx* ctx, double dt, eqs_step_attempt* att);
+/* sdirk_step / sdirk_advance_fixed (proj/src/integrators.cpp:297-341): stiffly
+ * accurate SDIRK3(2), Newton per stage with M + gamma dt K(z) assembled on the
+ * device every iteration (fem_system.cpp:124-145; Jacobi-preconditioned PCG,
+ * DESIGN.md §4). Single-rank contexts. advance_fixed returns NumericalError
+ * when a stage's Newton iteration fails. */
+int eqs_sdirk_step(eqs_ctx* ctx, const eqs_sdirk_options* opts, eqs_step_attempt* att);
+/* OdeSystem::shifted_solve (ode_system.hpp:63-68, fem_system.cpp:124-145):
+ * (M_II + gdt K_II(lift(t, z))) delta = rhs, host vectors of n_free; the
+ * preconditioner is refreshed when refresh_precond != 0 or on first use. */
+int eqs_shifted_solve(eqs_ctx* ctx, double t, const double* z, double gdt, const double* rhs, double* delta,
+                      int refresh_precond);
+int eqs_sdirk_advance_fixed(eqs_ctx* ctx, double dt, int nsteps, const eqs_sdirk_options* opts);
 
 /* ----------------------------------------------------------------- scenario (proj/src/scenario.cpp:217-383) */
 typedef struct {

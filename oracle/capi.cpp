@@ -458,6 +458,17 @@ int ora_sdirk_advance_fixed(void* h, double t, double* x, double dt, int nsteps)
     std::memcpy(x, st.x.data(), sizeof(double) * st.x.size());
   });
 }
+
+// FemSystem::shifted_solve (fem_system.cpp:124-145) on host vectors of n_free
+int ora_shifted_solve(void* h, double t, const double* z, double gdt, const double* rhs, double* delta, int refresh) {
+  return guard([&] {
+    auto* p = static_cast<Problem*>(h);
+    const int n = p->sys->size();
+    Vec d;
+    p->sys->shifted_solve(t, Vec(z, z + n), gdt, Vec(rhs, rhs + n), d, refresh != 0);
+    std::memcpy(delta, d.data(), sizeof(double) * n);
+  });
+}
 }  // extern "C"
 
 extern "C" {

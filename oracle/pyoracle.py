@@ -255,6 +255,15 @@ class Problem:
         d["stages"] = int(d["stages"])
         return x, d
 
+    def shifted_solve(self, t, z, gdt, rhs, refresh_precond=True):
+        """FemSystem::shifted_solve (fem_system.cpp:124-145)."""
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        d = np.zeros_like(rhs)
+        _check(lib().ora_shifted_solve(self._h, C.c_double(t), _ptr(z), C.c_double(gdt), _ptr(rhs), _ptr(d),
+                                       C.c_int(1 if refresh_precond else 0)))
+        return d
+
     def sdirk_advance_fixed(self, t, x, dt, nsteps=1):
         """sdirk_advance_fixed (integrators.cpp:329-341)."""
         x = np.array(x, dtype=np.float64, copy=True)

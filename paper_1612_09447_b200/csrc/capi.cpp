@@ -100,6 +100,8 @@ void fill_stats(GpuSystem& g, eqs_solve_stats* o) {
   o->spe_fallbacks = s.spe_fallbacks;
   o->svd_count = s.svd_count;
   o->estimator_appends = s.appends;
+  o->newton_linear_solves = s.newton_linear_solves;
+  o->newton_pcg_iterations = s.newton_pcg_iterations;
 }
 
 void fill_pcg(const PcgResult& r, eqs_pcg_result* o) {
@@ -499,6 +501,48 @@ int eqs_rkc_step(eqs_ctx* ctx, const eqs_rkc_options* o, eqs_step_attempt* att) 
     }
   });
 }
+namespace {
+SdirkOptions sdirk_from(const eqs_sdirk_options* o) {
+  SdirkOptions so;
+  if (o) {
+    so.rtol = o->rtol;
+    so.atol = o->atol;
+    if (o->newton_tol > 0) so.newton_tol = o->newton_tol;
+    if (o->max_newton > 0) so.max_newton = o->max_newton;
+  }
+  return so;
+}
+}  // namespace
+int eqs_shifted_solve(eqs_ctx* ctx, double t, const double* z, double gdt, const double* rhs, double* delta,
+                      int refresh_precond) {
+  return guard([&] {
+    if (!z || !rhs || !delta) throw std::invalid_argument("eqs_shifted_solve: null vector");
+    S(ctx).shifted_solve_host(t, z, gdt, rhs, delta, refresh_precond != 0);
+  });
+}
+int eqs_sdirk_step(eqs_ctx* ctx, const eqs_sdirk_options* o, eqs_step_attempt* att) {
+  return guard([&] {
+    const StepAttempt a = S(ctx).sdirk_step(sdirk_from(o));
+    if (att) {
+      att->t_start = a.t_start;
+      att->dt = a.dt;
+      att->accepted = a.accepted ? 1 : 0;
+      att->stages = a.stages;
+      att->newton_iterations = a.newton_iterations;
+      att->error = a.error;
+      att->rho = 0.0;
+      att->dt_next = a.dt_next;
+    }
+  });
+}
+int eqs_sdirk_advance_fixed(eqs_ctx* ctx, double dt, int nsteps, const eqs_sdirk_options* o) {
+  return guard([&] {
+    if (!(dt > 0) || nsteps < 0) throw std::invalid_argument("eqs_sdirk_advance_fixed: need dt > 0, nsteps >= 0");
+    const SdirkOptions so = sdirk_from(o);
+    for (int i = 0; i < nsteps; ++i)
+      if (!S(ctx).sdirk_advance_fixed(dt, so)) throw NumericalError("sdirk: Newton iteration failed");
+  });
+}
 int eqs_rkc_advance_fixed(eqs_ctx* ctx, double dt, int s, int nsteps) {
   return guard([&] {
     GpuSystem& g = S(ctx);
@@ -548,6 +592,8 @@ int eqs_run_scenario(const char* json_text, const char* out_dir, int device, eqs
     res->stats.spe_fallbacks = r.stats.spe_fallbacks;
     res->stats.svd_count = r.stats.svd_count;
     res->stats.estimator_appends = r.stats.appends;
+    res->stats.newton_linear_solves = r.stats.newton_linear_solves;
+    res->stats.newton_pcg_iterations = r.stats.newton_pcg_iterations;
     if (x_final && (long)r.final_x_free.size() <= x_cap)
       std::memcpy(x_final, r.final_x_free.data(), sizeof(double) * r.final_x_free.size());
     if (r.exit_code != 0) {

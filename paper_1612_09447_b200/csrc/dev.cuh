@@ -205,6 +205,15 @@ struct CoefPack {
   double c[kMaxMulti];
 };
 void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s);
+// SDIRK Newton matrix (k_sparse.cu / k_stiffness.cu)
+void launch_k_element(int order, int n_tets, const int* tet_dofs, const unsigned char* tet_mat, const double* coords,
+                      const double* x_full, double* S, int* geo_error, cudaStream_t s);
+void launch_shift_gather(long nnz, const long* ptr, const long* src, const double* S, const double* m, double gdt,
+                         double* shifted, cudaStream_t s);
+void launch_csr_diag(int n, const int* rp, const int* ci, const double* v, double* d, cudaStream_t s);
+void launch_jacobi_div(int n, const double* d, const double* r, double* z, Reducer red, int slot, cudaStream_t s);
+void launch_weighted_sq(int n, const double* est, const double* x, const double* xn, double atol, double rtol,
+                        Reducer red, int slot, cudaStream_t s);
 // y += sum_k c[k] V_k
 void launch_lincomb_acc(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s);
 // SPE basis maintenance: w -= sum_j c_j Q_j with ||w||^2 into slot; and a

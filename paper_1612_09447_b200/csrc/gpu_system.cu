@@ -8,6 +8,7 @@
 // (restrict_free, :17-20) is free. With one rank the owned set is every free
 // dof in DofMap::free_dofs order and there are no ghosts.
 #include "gpu_system.hpp"
+#include "element.hpp"
 #include "kxblock.hpp"
 #include "sell.hpp"
 
@@ -2186,6 +2187,284 @@ StepAttempt GpuSystem::euler_step(double dt) {
   att.stages = 1;
   att.dt_next = dt;
   return att;
+}
+
+
+// ------------------------------------------------------------------ SDIRK3(2)
+// proj/src/integrators.cpp:237-343 and FemSystem::shifted_solve
+// (proj/src/fem_system.cpp:124-145). The Newton matrix M_II + gamma dt K_II(z)
+// is assembled on the device every Newton iteration: per-tet element matrices
+// (k_kelem, the reference's element arithmetic), then one thread per M_II
+// entry sums its contributions in ascending tet order (assemble_matrix order)
+// and forms 1.0 m + gdt k (csr.cpp add on the common pattern). Deviation
+// (DESIGN.md §4): the shifted system is preconditioned with Jacobi (diagonal
+// of the matrix at the last refresh) instead of rebuilding the AMG hierarchy
+// every step; the PCG stopping rule is the reference's, so each Newton update
+// is the same to the solver tolerance.
+double* GpuSystem::sd(int i) {
+  if (!sd_buf_[i].p) sd_buf_[i].alloc(std::max(1, n_full_));
+  return sd_buf_[i].p;
+}
+
+void GpuSystem::build_shift_map() {
+  if (shift_built_) return;
+  require_single("sdirk");
+  const int nl = order_ == 1 ? 4 : 10, ntri = nl * (nl + 1) / 2;
+  const std::vector<int>& td = tet_dofs_host();
+  const LocalSpace& s0 = plan_.space[0];
+  const HostCsr& m = m_ii_;
+  auto entry = [&](int li, int lj) -> long {  // local free dofs -> M_II entry
+    const int r = s0.owned[li], c = s0.owned[lj];
+    const int* b = m.col_idx.data() + m.row_ptr[r];
+    const int* e = m.col_idx.data() + m.row_ptr[r + 1];
+    const int* f = std::lower_bound(b, e, c);
+    if (f == e || *f != c) throw NumericalError("sdirk: element pair outside the M_II pattern");
+    return (long)(f - m.col_idx.data());
+  };
+  std::vector<int> order(n_tets_loc_);
+  for (int k = 0; k < n_tets_loc_; ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return plan_.tets[a] < plan_.tets[b]; });
+  const long nnz = m.nnz();
+  std::vector<long> ptr(nnz + 1, 0);
+  for (int k : order)
+    for (int a = 0; a < nl; ++a)
+      for (int b = 0; b < nl; ++b) {
+        const int ra = td[(size_t)k * nl + a], cb = td[(size_t)k * nl + b];
+        if (ra < n_own_ && cb < n_own_) ++ptr[entry(ra, cb) + 1];
+      }
+  for (long e = 0; e < nnz; ++e) ptr[e + 1] += ptr[e];
+  std::vector<long> src(ptr[nnz]), next(ptr.begin(), ptr.end() - 1);
+  for (int k : order)
+    for (int a = 0; a < nl; ++a)
+      for (int b = 0; b < nl; ++b) {
+        const int ra = td[(size_t)k * nl + a], cb = td[(size_t)k * nl + b];
+        if (ra < n_own_ && cb < n_own_) src[next[entry(ra, cb)]++] = (long)k * ntri + tri_index(a, b);
+      }
+  sh_ptr_.alloc(nnz + 1);
+  sh_ptr_.upload(ptr.data(), ptr.size(), stream_);
+  sh_src_.alloc(std::max<size_t>(1, src.size()));
+  sh_src_.upload(src.data(), src.size(), stream_);
+  sh_S_.alloc(std::max<long>(1, (long)n_tets_loc_ * ntri));
+  sh_vals_.alloc(std::max<long>(1, nnz));
+  sh_diag_.alloc(std::max(1, n_own_));
+  sh_err_.alloc(1);
+  CK(cudaMemsetAsync(sh_err_.p, 0, sizeof(int), stream_));
+  sh_csr_ = DevCsr{};
+  sh_csr_.n_rows = mii_.n_rows;
+  sh_csr_.n_cols = mii_.n_cols;
+  sh_csr_.nnz = nnz;
+  sh_csr_.row_ptr = mii_rp_.p;
+  sh_csr_.col_idx = mii_ci_.p;
+  sh_csr_.values = sh_vals_.p;
+  sh_csr_.tpr = mii_.tpr;
+  sync();
+  shift_built_ = true;
+}
+
+void GpuSystem::shifted_solve_dev(double t, double* z_full, double gdt, const double* rhs, double* delta,
+                                  bool refresh) {
+  build_shift_map();
+  const int n = n_own_;
+  {
+    PhaseTimer pt(stats_.t_setup);
+    lift_dev(t, z_full);
+    launch_k_element(order_, n_tets_loc_, tet_dofs_.p, tet_mat_.p, coords_.p, z_full, sh_S_.p, sh_err_.p, stream_);
+    ++stats_.assemblies;
+    launch_shift_gather(sh_csr_.nnz, sh_ptr_.p, sh_src_.p, sh_S_.p, mii_v_.p, gdt, sh_vals_.p, stream_);
+    if (refresh || !shift_precond_) {  // make_preconditioner (fem_system.cpp:38-46): Jacobi on the GPU
+      launch_csr_diag(n, sh_csr_.row_ptr, sh_csr_.col_idx, sh_vals_.p, sh_diag_.p, stream_);
+      ++stats_.precond_setups;
+      shift_precond_ = true;
+    }
+  }
+  PhaseTimer pt(stats_.t_solve);
+  // pcg_solve (proj/src/pcg.cpp:9-72) with a zero start
+  double* x = delta;
+  double* r = sd(12);
+  double* z = sd(13);
+  double* p = sd(14);
+  double* q = sd(15);
+  const double tol = prob_.solver.rel_tol;
+  const int max_iter = prob_.solver.max_iter;
+  const double bnorm = std::sqrt(dot_own(rhs, rhs, S_NORM));
+  launch_fill(n, 0.0, x, stream_);
+  if (bnorm == 0.0) {
+    ++stats_.newton_linear_solves;
+    return;
+  }
+  CK(cudaMemcpyAsync(r, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+  double rel = 1.0;
+  if (!std::isfinite(bnorm)) throw NumericalError("pcg: non-finite initial residual");
+  if (rel <= tol) return;
+  launch_jacobi_div(n, sh_diag_.p, r, z, red_, S_RZ, stream_);
+  double rz = read_scalar(S_RZ);
+  if (!std::isfinite(rz)) throw NumericalError("pcg: non-finite preconditioned residual");
+  CK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+  int k = 1;
+  bool converged = false;
+  for (; k <= max_iter; ++k) {
+    launch_spmv(sh_csr_, p, q, stream_);
+    const double pq = dot_own(p, q, S_PQ);
+    if (!(pq > 0.0) || !std::isfinite(pq)) throw NumericalError("pcg: operator not positive definite");
+    const double alpha = rz / pq;
+    launch_axpy(n, alpha, p, x, stream_);
+    launch_axpy(n, -alpha, q, r, stream_);
+    rel = std::sqrt(dot_own(r, r, S_RR)) / bnorm;
+    if (!std::isfinite(rel)) throw NumericalError("pcg: non-finite residual");
+    if (rel <= tol) {
+      converged = true;
+      break;
+    }
+    launch_jacobi_div(n, sh_diag_.p, r, z, red_, S_RZ, stream_);
+    const double rz_new = read_scalar(S_RZ);
+    if (!std::isfinite(rz_new)) throw NumericalError("pcg: non-finite preconditioned residual");
+    launch_scale(n, rz_new / rz, p, p, stream_);
+    launch_axpy(n, 1.0, z, p, stream_);
+    rz = rz_new;
+  }
+  if (!converged) throw NumericalError("shifted-system solve failed to converge");
+  ++stats_.newton_linear_solves;
+  stats_.newton_pcg_iterations += k;
+}
+
+void GpuSystem::shifted_solve_host(double t, const double* z, double gdt, const double* rhs, double* delta,
+                                   bool refresh) {
+  require_single("shifted_solve");
+  double* zf = sd(11);
+  double* b = sd(10);
+  double* d = sd(6);
+  CK(cudaMemcpyAsync(zf, z, sizeof(double) * n_own_, cudaMemcpyHostToDevice, stream_));
+  CK(cudaMemcpyAsync(b, rhs, sizeof(double) * n_own_, cudaMemcpyHostToDevice, stream_));
+  shifted_solve_dev(t, zf, gdt, b, d, refresh);
+  CK(cudaMemcpyAsync(delta, d, sizeof(double) * n_own_, cudaMemcpyDeviceToHost, stream_));
+  sync();
+}
+
+namespace {
+constexpr double kSdG = 0.435866521508459;
+constexpr double kSdC[3] = {kSdG, (1.0 + kSdG) / 2.0, 1.0};
+constexpr double kSdB1 = -1.5 * kSdG * kSdG + 4.0 * kSdG - 0.25;
+constexpr double kSdB2 = 1.5 * kSdG * kSdG - 5.0 * kSdG + 1.25;
+constexpr double kSdA[3][3] = {{kSdG, 0.0, 0.0}, {(1.0 - kSdG) / 2.0, kSdG, 0.0}, {kSdB1, kSdB2, kSdG}};
+constexpr double kSdBh1 = kSdG / (1.0 - kSdG);
+constexpr double kSdBh2 = 1.0 - kSdBh1;
+}  // namespace
+
+// sdirk_stages (integrators.cpp:256-292); the new state is left in sd(1), the
+// error estimate in est (may be null)
+bool GpuSystem::sdirk_stages(double dt, const SdirkOptions& o, int& newton_iters, double* est) {
+  require_single("sdirk");
+  const int n = n_own_;
+  const double t = state_t, gdt = kSdG * dt;
+  double *w = sd(0), *z = sd(1), *zw = sd(2), *r = sd(3), *mz = sd(4), *g = sd(5), *delta = sd(6);
+  double* kk[3] = {sd(7), sd(8), sd(9)};
+  newton_iters = 0;
+  for (int stage = 0; stage < 3; ++stage) {
+    CK(cudaMemcpyAsync(w, X_, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    for (int j = 0; j < stage; ++j) launch_axpy(n, dt * kSdA[stage][j], kk[j], w, stream_);
+    const double ts = t + kSdC[stage] * dt;
+    CK(cudaMemcpyAsync(z, w, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    double scale = -1.0;
+    bool converged = false;
+    for (int it = 0;; ++it) {
+      {
+        PhaseTimer pt(stats_.t_residual);
+        residual_dev(ts, z, r);
+      }
+      CK(cudaMemcpyAsync(zw, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+      launch_axpy(n, -1.0, w, zw, stream_);
+      mass_apply_dev(zw, mz);
+      CK(cudaMemcpyAsync(g, mz, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+      launch_axpy(n, -gdt, r, g, stream_);
+      const double gn = std::sqrt(dot_own(g, g, S_NORM));
+      if (!std::isfinite(gn)) return false;
+      if (scale < 0.0) scale = gn;
+      if (gn <= o.newton_tol * scale || gn == 0.0) {
+        converged = true;
+        break;
+      }
+      if (it >= o.max_newton) break;
+      launch_scale(n, -1.0, g, g, stream_);
+      try {
+        shifted_solve_dev(ts, z, gdt, g, delta, stage == 0 && it == 0);
+      } catch (const NumericalError&) {
+        return false;
+      }
+      launch_axpy(n, 1.0, delta, z, stream_);
+      ++newton_iters;
+    }
+    if (!converged) return false;
+    CK(cudaMemcpyAsync(kk[stage], z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    launch_axpy(n, -1.0, w, kk[stage], stream_);
+    launch_scale(n, 1.0 / gdt, kk[stage], kk[stage], stream_);
+  }
+  if (est) {
+    CoefPack c{};
+    c.c[0] = dt * (kSdA[2][0] - kSdBh1);
+    c.c[1] = dt * (kSdA[2][1] - kSdBh2);
+    c.c[2] = dt * kSdG;
+    const double* V[3] = {kk[0], kk[1], kk[2]};
+    launch_lincomb(n, 3, V, c, est, stream_);
+  }
+  return true;
+}
+
+// sdirk_step (integrators.cpp:297-327)
+StepAttempt GpuSystem::sdirk_step(const SdirkOptions& o) {
+  StepAttempt att;
+  att.t_start = state_t;
+  att.dt = state_dt;
+  att.stages = 3;
+  int newton_iters = 0;
+  double* est = sd(10);
+  const bool ok = sdirk_stages(state_dt, o, newton_iters, est);
+  att.newton_iterations = newton_iters;
+  st_newton += newton_iters;
+  if (!ok) {
+    att.accepted = false;
+    att.dt_next = 0.5 * state_dt;
+    ++st_rejected;
+    state_dt = att.dt_next;
+    return att;
+  }
+  const int n = n_own_;
+  launch_weighted_sq(n, est, X_, sd(1), o.atol, o.rtol, red_, S_ERR, stream_);
+  const double acc = read_scalar(S_ERR);
+  att.error = n == 0 ? 0.0 : std::sqrt(acc / (double)n);
+  // step_controller (integrators.cpp:12-18), order 3
+  const double err = att.error;
+  bool accept;
+  double dt_next;
+  if (!std::isfinite(err)) {
+    accept = false;
+    dt_next = 0.1 * state_dt;
+  } else {
+    accept = err <= 1.0;
+    const double factor = err == 0.0 ? 10.0 : std::clamp(0.8 * std::pow(err, -1.0 / 4.0), 0.1, 10.0);
+    dt_next = state_dt * factor;
+  }
+  att.accepted = accept;  // finite err implies finite x_new
+  att.dt_next = dt_next;
+  if (att.accepted) {
+    CK(cudaMemcpyAsync(X_, sd(1), sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    state_t += state_dt;
+    ++st_accepted;
+  } else {
+    ++st_rejected;
+  }
+  state_dt = dt_next;
+  return att;
+}
+
+// sdirk_advance_fixed (integrators.cpp:329-341)
+bool GpuSystem::sdirk_advance_fixed(double dt, const SdirkOptions& o) {
+  int newton_iters = 0;
+  if (!sdirk_stages(dt, o, newton_iters, nullptr)) return false;
+  st_newton += newton_iters;
+  CK(cudaMemcpyAsync(X_, sd(1), sizeof(double) * n_own_, cudaMemcpyDeviceToDevice, stream_));
+  state_t += dt;
+  ++st_accepted;
+  return true;
 }
 
 }  // namespace eqsb

@@ -25,6 +25,7 @@ struct SolveStats {
   long m_solves = 0, pcg_iterations = 0, rho_solves = 0, rho_pcg_iterations = 0;
   long precond_setups = 0, assemblies = 0, applies = 0, spe_fallbacks = 0;
   long svd_count = 0, appends = 0;  // StartVectorEstimator::Stats (start_vector.hpp:45-49)
+  long newton_linear_solves = 0, newton_pcg_iterations = 0;  // implicit path (ode_system.hpp:25-26)
   double t_residual = 0, t_solve = 0, t_setup = 0, t_estimator = 0;
 };
 struct SolveRecord {
@@ -40,12 +41,17 @@ struct PcgResult {
 struct StepAttempt {
   double t_start = 0, dt = 0;
   bool accepted = false;
-  int stages = 0;
+  int stages = 0, newton_iterations = 0;
   double error = 0, rho = 0, dt_next = 0;
 };
 struct RkcOptions {
   double rtol = 1e-2, atol = 1e-8;
   int max_stages = 200, rho_refresh_every = 25;
+};
+struct SdirkOptions {  // proj/include/eqs/integrators.hpp:106-110
+  double rtol = 1e-2, atol = 1e-8;
+  double newton_tol = 1e-8;
+  int max_newton = 25;
 };
 
 template <class T>
@@ -181,6 +187,13 @@ class GpuSystem {
   StepAttempt rkc_step(const RkcOptions& o);
   void rkc_advance_fixed(double dt, int s);
   StepAttempt euler_step(double dt);
+  // SDIRK3(2) implicit baseline (integrators.cpp:237-343): Newton per stage with
+  // the matrix M + gamma dt K(z) assembled on the device (fem_system.cpp:124-145)
+  StepAttempt sdirk_step(const SdirkOptions& o);
+  // FemSystem::shifted_solve with host vectors (fem_system.cpp:124-145)
+  void shifted_solve_host(double t, const double* z, double gdt, const double* rhs, double* delta, bool refresh);
+  bool sdirk_advance_fixed(double dt, const SdirkOptions& o);
+  long st_newton = 0;
   double* state_dev() { return X_; }
   double* scratch_full() { return full_[0].p != X_ ? full_[0].p : full_[1].p; }
 
@@ -259,6 +272,19 @@ class GpuSystem {
   void spe_rebuild();
   void spe_append(double* h);
   void spe_downdate();
+  // SDIRK Newton matrix: per M_II entry the element contributions (ascending
+  // tet), per-tet packed element matrices, the shifted values and the Jacobi
+  // diagonal of the last refresh
+  bool sdirk_stages(double dt, const SdirkOptions& o, int& newton_iters, double* est);
+  void shifted_solve_dev(double t, double* z_full, double gdt, const double* rhs, double* delta, bool refresh);
+  void build_shift_map();
+  bool shift_built_ = false, shift_precond_ = false;
+  DevBuf<long> sh_ptr_, sh_src_;
+  DevBuf<double> sh_S_, sh_vals_, sh_diag_;
+  DevBuf<int> sh_err_;
+  DevCsr sh_csr_;
+  DevBuf<double> sd_buf_[16];
+  double* sd(int i);
   // POD estimators (start_vector.cpp:64-71,111-150,165-187): snapshot ring,
   // thin QR of the snapshots (Q, R), Jacobi SVD of R on the host, basis
   // U = Q U_R, W = M U and the reduced inverse (U'MU)^-1

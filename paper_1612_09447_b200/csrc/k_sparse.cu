@@ -196,6 +196,51 @@ __global__ void k_lincomb_multi(int n, int kin, int kout, PtrPack in, PtrPack ou
   }
 }
 
+// SDIRK Newton matrix values on the M_II pattern: k_e = sum of the element
+// contributions in ascending tet order from 0.0 (assemble_matrix), then
+// shifted_e = 1.0 m_e + gdt k_e (csr.cpp:168-195 with equal patterns)
+__global__ void k_shift_gather(long nnz, const long* __restrict__ ptr, const long* __restrict__ src,
+                               const double* __restrict__ S, const double* __restrict__ m, double gdt,
+                               double* __restrict__ shifted) {
+  for (long e = (long)blockIdx.x * kBlock + threadIdx.x; e < nnz; e += (long)gridDim.x * kBlock) {
+    double k = 0.0;
+    for (long c = ptr[e]; c < ptr[e + 1]; ++c) k = __dadd_rn(k, S[src[c]]);
+    shifted[e] = __dadd_rn(m[e], __dmul_rn(gdt, k));
+  }
+}
+// diag[i] = a_ii (CSR with sorted columns)
+__global__ void k_csr_diag(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
+                           double* __restrict__ d) {
+  for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
+    double s = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] == i) s = v[k];
+    d[i] = s;
+  }
+}
+// z = r / d (JacobiPreconditioner, preconditioners.cpp:22-32) ; slot <- r.z
+__global__ void k_jacobi_div(int n, const double* __restrict__ d, const double* __restrict__ r, double* __restrict__ z,
+                             Reducer red, int slot) {
+  double acc = 0.0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    const double zi = r[i] / d[i];
+    z[i] = zi;
+    acc += r[i] * zi;
+  }
+  reduce_finish(acc, red, slot);
+}
+// weighted_rms (integrators.cpp:20-31) sum: (est_i / (atol + rtol max(|x_i|, |xn_i|)))^2
+__global__ void k_weighted_sq(int n, const double* __restrict__ est, const double* __restrict__ x,
+                              const double* __restrict__ xn, double atol, double rtol, Reducer red, int slot) {
+  double acc = 0.0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    const double w = atol + rtol * fmax(fabs(x[i]), fabs(xn[i]));
+    const double e = est[i] / w;
+    acc += e * e;
+  }
+  reduce_finish(acc, red, slot);
+}
+
 __global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] += a * x[i];
 }
@@ -364,6 +409,27 @@ void launch_lincomb_multi(int n, int kin, int kout, const double* const* in, dou
   for (int k = 0; k < kin && k < kMaxMulti; ++k) pi.p[k] = in[k];
   for (int k = 0; k < kout && k < kMaxMulti; ++k) po.p[k] = out[k];
   k_lincomb_multi<<<grid_for(n), kBlock, 0, s>>>(n, kin, kout, pi, po, T);
+}
+void launch_shift_gather(long nnz, const long* ptr, const long* src, const double* S, const double* m, double gdt,
+                         double* shifted, cudaStream_t s) {
+  ++g_launch_count;
+  if (nnz == 0) return;
+  k_shift_gather<<<(int)std::min<long>((nnz + kBlock - 1) / kBlock, 148L * 32), kBlock, 0, s>>>(nnz, ptr, src, S, m,
+                                                                                              gdt, shifted);
+}
+void launch_csr_diag(int n, const int* rp, const int* ci, const double* v, double* d, cudaStream_t s) {
+  ++g_launch_count;
+  if (n == 0) return;
+  k_csr_diag<<<grid_for(n), kBlock, 0, s>>>(n, rp, ci, v, d);
+}
+void launch_jacobi_div(int n, const double* d, const double* r, double* z, Reducer red, int slot, cudaStream_t s) {
+  ++g_launch_count;
+  k_jacobi_div<<<red_grid(k_jacobi_div, n), kBlock, 0, s>>>(n, d, r, z, red, slot);
+}
+void launch_weighted_sq(int n, const double* est, const double* x, const double* xn, double atol, double rtol,
+                        Reducer red, int slot, cudaStream_t s) {
+  ++g_launch_count;
+  k_weighted_sq<<<red_grid(k_weighted_sq, n), kBlock, 0, s>>>(n, est, x, xn, atol, rtol, red, slot);
 }
 void launch_axpy(int n, double a, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;

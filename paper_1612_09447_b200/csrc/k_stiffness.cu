@@ -403,6 +403,61 @@ void launch_kx_tets(int order, int n_tets, const int* tet_dofs, const unsigned c
     k_kx_p2<<<g, kBlock, 0, s>>>(n_tets, tet_dofs, tet_mat, coords, x_state, v, ytet, geo_error);
 }
 
+// Element matrices of K(x) for the SDIRK Newton matrix (assemble_stiffness,
+// proj/src/assembly.cpp:97-116,178-186): packed lower triangle per tet (10 for
+// P1, 55 for P2), kappa at |grad x_h| per quadrature point
+// (gradient_magnitude, assembly.cpp:87-95), element.hpp's reference-order
+// geometry and Laplacian.
+__global__ void __launch_bounds__(kBlock) k_kelem(int nt, int nl, const int* __restrict__ tet_dofs,
+                                                  const unsigned char* __restrict__ tet_mat,
+                                                  const double* __restrict__ coords, const double* __restrict__ x,
+                                                  double* __restrict__ S, int* __restrict__ err) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  int dofs[10];
+  for (int i = 0; i < nl; ++i) dofs[i] = tet_dofs[(long)nl * t + i];
+  double p[4][3];
+  for (int v = 0; v < 4; ++v) load_xyz(coords, dofs[v], p[v]);
+  TetGeo geo;
+  if (!tet_geometry(p, geo)) {
+    atomicExch(err, 1);
+    return;
+  }
+  double xl[10];
+  for (int i = 0; i < nl; ++i) xl[i] = x[dofs[i]];
+  const DevMaterial& m = c_mat[tet_mat[t]];
+  if (nl == 4) {
+    double g[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < 4; ++i)
+      for (int d = 0; d < 3; ++d) g[d] = __dadd_rn(g[d], __dmul_rn(xl[i], geo.g[i][d]));
+    const double e = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])), __dmul_rn(g[2], g[2])));
+    double Sl[10];
+    element_laplacian_p1(geo, kappa_dev(m, e), Sl);
+    for (int k = 0; k < 10; ++k) S[10L * t + k] = Sl[k];
+  } else {
+    double coeff[4], grads[10][3];
+    for (int q = 0; q < 4; ++q) {
+      p2_gradients(geo, q, grads);
+      double g[3] = {0.0, 0.0, 0.0};
+      for (int i = 0; i < 10; ++i)
+        for (int d = 0; d < 3; ++d) g[d] = __dadd_rn(g[d], __dmul_rn(xl[i], grads[i][d]));
+      coeff[q] = kappa_dev(m, sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])),
+                                             __dmul_rn(g[2], g[2]))));
+    }
+    double Sl[55];
+    element_laplacian_p2(geo, coeff, Sl);
+    for (int k = 0; k < 55; ++k) S[55L * t + k] = Sl[k];
+  }
+}
+
+void launch_k_element(int order, int n_tets, const int* tet_dofs, const unsigned char* tet_mat, const double* coords,
+                      const double* x_full, double* S, int* geo_error, cudaStream_t s) {
+  ++g_launch_count;
+  if (n_tets == 0) return;
+  k_kelem<<<(n_tets + kBlock - 1) / kBlock, kBlock, 0, s>>>(n_tets, order == 1 ? 4 : 10, tet_dofs, tet_mat, coords,
+                                                            x_full, S, geo_error);
+}
+
 void launch_kx_gather(int n_rows, const long* slot_ptr, const int* slots, const double* ytet, const double* base,
                       double sign, double* out, cudaStream_t s) {
   ++g_launch_count;

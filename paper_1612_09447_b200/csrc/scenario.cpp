@@ -137,7 +137,7 @@ void write_metrics_csv(const std::string& path, const std::vector<StepMetrics>& 
   char buf[512];
   for (const auto& r : rows) {
     std::snprintf(buf, sizeof buf, "%ld,%.17g,%.17g,%s,%d,%d,%d,%ld,%ld,%.17g,%s,%d,%.17g,%.6g,%.6g,%.6g,%.6g\n",
-                  r.step, r.t, r.dt, r.method.c_str(), r.accepted ? 1 : 0, r.stages, 0, r.m_solves, r.pcg_iters,
+                  r.step, r.t, r.dt, r.method.c_str(), r.accepted ? 1 : 0, r.stages, r.newton_iters, r.m_solves, r.pcg_iters,
                   r.rho, r.estimator_mode.c_str(), r.estimator_rank, r.err_est, r.t_residual, r.t_solve, r.t_setup,
                   r.t_estimator);
     os << buf;
@@ -194,7 +194,6 @@ RunResult run_scenario(const SimConfig& config, const std::string& out_dir, int 
   for (size_t p = 0; p < config.probes.size(); ++p) probe_names.push_back("p" + std::to_string(p));
   try {
     if (!out_dir.empty()) fs::create_directories(out_dir);
-    if (config.integrator == 2) throw ConfigError("integrator 'sdirk32' is not supported by the GPU backend");
     Problem prob = build_problem(config);
     std::vector<PointLocation> locs;
     for (const auto& p : config.probes) {
@@ -241,6 +240,12 @@ RunResult run_scenario(const SimConfig& config, const std::string& out_dir, int 
         att = sys.euler_step(dt);
         att.rho = rho;
         ++sys.rho_age;
+      } else if (config.integrator == 2) {  // scenario.cpp:299-302
+        sys.state_dt = std::min(sys.state_dt, config.t_end - sys.state_t);
+        SdirkOptions so;
+        so.rtol = opts.rtol;
+        so.atol = opts.atol;
+        att = sys.sdirk_step(so);
       } else {
         sys.state_dt = std::min(sys.state_dt, config.t_end - sys.state_t);
         att = sys.rkc_step(opts);
@@ -250,7 +255,8 @@ RunResult run_scenario(const SimConfig& config, const std::string& out_dir, int 
       row.step = step_index++;
       row.t = att.t_start;
       row.dt = att.dt;
-      row.method = config.integrator == 0 ? "euler" : "rkc";
+      row.method = config.integrator == 0 ? "euler" : config.integrator == 2 ? "sdirk32" : "rkc";
+      row.newton_iters = att.newton_iterations;
       row.accepted = att.accepted;
       row.stages = att.stages;
       row.m_solves = after.m_solves - before.m_solves;

@@ -14,7 +14,7 @@ struct StepMetrics {
   double t = 0, dt = 0;
   std::string method;
   bool accepted = false;
-  int stages = 0;
+  int stages = 0, newton_iters = 0;
   long m_solves = 0, pcg_iters = 0;
   double rho = 0;
   std::string estimator_mode;

@@ -75,6 +75,10 @@ class _RkcOptions(C.Structure):
                 ("rho_refresh_every", C.c_int)]
 
 
+class _SdirkOptions(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("atol", C.c_double), ("newton_tol", C.c_double), ("max_newton", C.c_int)]
+
+
 class _StepAttempt(C.Structure):
     _fields_ = [("t_start", C.c_double), ("dt", C.c_double), ("accepted", C.c_int), ("stages", C.c_int),
                 ("newton_iterations", C.c_int), ("error", C.c_double), ("rho", C.c_double),
@@ -147,6 +151,7 @@ class StepAttempt:
     error: float
     rho: float
     dt_next: float
+    newton_iterations: int = 0
 
 
 @dataclass
@@ -424,6 +429,25 @@ class FemSystem:
         a = _StepAttempt()
         _check(load_library().eqs_euler_step(self._h, C.c_double(dt), C.byref(a)))
         return StepAttempt(a.t_start, a.dt, bool(a.accepted), a.stages, a.error, a.rho, a.dt_next)
+
+    def sdirk_step(self, rtol=1e-2, atol=1e-8, newton_tol=1e-8, max_newton=25) -> StepAttempt:
+        """sdirk_step (proj/src/integrators.cpp:297-327) on the resident state."""
+        o = _SdirkOptions(rtol, atol, newton_tol, max_newton)
+        a = _StepAttempt()
+        _check(load_library().eqs_sdirk_step(self._h, C.byref(o), C.byref(a)))
+        return StepAttempt(a.t_start, a.dt, bool(a.accepted), a.stages, a.error, a.rho, a.dt_next,
+                           a.newton_iterations)
+
+    def shifted_solve(self, t: float, z, gdt: float, rhs, refresh_precond: bool = True) -> np.ndarray:
+        """FemSystem::shifted_solve (fem_system.cpp:124-145)."""
+        d = np.zeros(self.n_free)
+        _check(load_library().eqs_shifted_solve(self._h, C.c_double(t), _dp(_f64(z)), C.c_double(gdt),
+                                                _dp(_f64(rhs)), _dp(d), C.c_int(1 if refresh_precond else 0)))
+        return d
+
+    def sdirk_advance_fixed(self, dt: float, nsteps: int = 1, newton_tol=1e-8, max_newton=25):
+        o = _SdirkOptions(1e-2, 1e-8, newton_tol, max_newton)
+        _check(load_library().eqs_sdirk_advance_fixed(self._h, C.c_double(dt), C.c_int(nsteps), C.byref(o)))
 
     # --- instrumentation / options
     def set_option(self, key: int, value: float):

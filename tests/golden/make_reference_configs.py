@@ -6,7 +6,8 @@ import os
 
 SRC = "/root/reference/proj/configs"
 NAMES = ["smoke", "slab_nonlinear_rkc_spe", "slab_linear_rkc", "slab_linear_rkc_previous", "slab_linear_rkc_spe",
-         "slab_order2_rkc", "slab_linear_euler", "slab_nonlinear_rkc_pod_fixed", "slab_nonlinear_rkc_pod_rolling"]
+         "slab_order2_rkc", "slab_linear_euler", "slab_nonlinear_rkc_pod_fixed", "slab_nonlinear_rkc_pod_rolling",
+         "slab_nonlinear_sdirk"]
 
 if __name__ == "__main__":
     out = {n: json.load(open(os.path.join(SRC, n + ".json"))) for n in NAMES}
