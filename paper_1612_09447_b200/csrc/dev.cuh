@@ -205,6 +205,9 @@ struct CoefPack {
   double c[kMaxMulti];
 };
 void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s);
+// per-cell kappa (VTK dump)
+void launch_cell_kappa(int order, int n_tets, const int* tet_dofs, const unsigned char* tet_mat, const double* coords,
+                       const double* x_full, double* kappa, cudaStream_t s);
 // SDIRK Newton matrix (k_sparse.cu / k_stiffness.cu)
 void launch_k_element(int order, int n_tets, const int* tet_dofs, const unsigned char* tet_mat, const double* coords,
                       const double* x_full, double* S, int* geo_error, cudaStream_t s);

@@ -200,6 +200,7 @@ struct SimConfig {
   std::vector<std::array<double, 3>> probes;
   std::string metrics_csv = "metrics.csv", probe_csv = "probe.csv", solves_csv, vtk_prefix;
   int vtk_every = 0;
+  bool vtk_binary = false;  // additive: legacy binary VTK instead of ASCII
   int workers = 1;
   double effective_atol() const;  // proj/src/scenario.cpp:90-100
 };

@@ -2327,6 +2327,20 @@ void GpuSystem::shifted_solve_dev(double t, double* z_full, double gdt, const do
   stats_.newton_pcg_iterations += k;
 }
 
+void GpuSystem::cell_kappa_host(double* kappa) {
+  require_single("cell_kappa");
+  double* xf = sd(11);
+  CK(cudaMemcpyAsync(xf, X_, sizeof(double) * n_own_, cudaMemcpyDeviceToDevice, stream_));
+  lift_dev(state_t, xf);
+  DevBuf<double> kd;
+  kd.alloc(std::max(1, n_tets_loc_));
+  launch_cell_kappa(order_, n_tets_loc_, tet_dofs_.p, tet_mat_.p, coords_.p, xf, kd.p, stream_);
+  std::vector<double> loc(n_tets_loc_);
+  kd.download(loc.data(), loc.size(), stream_);
+  sync();
+  for (int k = 0; k < n_tets_loc_; ++k) kappa[plan_.tets[k]] = loc[k];
+}
+
 void GpuSystem::shifted_solve_host(double t, const double* z, double gdt, const double* rhs, double* delta,
                                    bool refresh) {
   require_single("shifted_solve");

@@ -190,6 +190,8 @@ class GpuSystem {
   // SDIRK3(2) implicit baseline (integrators.cpp:237-343): Newton per stage with
   // the matrix M + gamma dt K(z) assembled on the device (fem_system.cpp:124-145)
   StepAttempt sdirk_step(const SdirkOptions& o);
+  // per-cell kappa of the resident state at state_t, reference tet order (VTK dump)
+  void cell_kappa_host(double* kappa);
   // FemSystem::shifted_solve with host vectors (fem_system.cpp:124-145)
   void shifted_solve_host(double t, const double* z, double gdt, const double* rhs, double* delta, bool refresh);
   bool sdirk_advance_fixed(double dt, const SdirkOptions& o);

@@ -166,6 +166,7 @@ SimConfig parse_config(const std::string& text) {
       c.solves_csv = jo.value("solves_csv", c.solves_csv);
       c.vtk_prefix = jo.value("vtk_prefix", c.vtk_prefix);
       c.vtk_every = jo.value("vtk_every", c.vtk_every);
+      c.vtk_binary = jo.value("vtk_binary", c.vtk_binary);  // additive key
     }
     c.max_steps = j.value("max_steps", -1L);
     c.workers = j.value("workers", 1);

@@ -450,6 +450,44 @@ __global__ void __launch_bounds__(kBlock) k_kelem(int nt, int nl, const int* __r
   }
 }
 
+// per-cell kappa of the VTK dump (vtk_writer.cpp:38-46): kappa at |grad x_h|
+// of the first quadrature point
+__global__ void __launch_bounds__(kBlock) k_cell_kappa(int nt, int nl, const int* __restrict__ tet_dofs,
+                                                       const unsigned char* __restrict__ tet_mat,
+                                                       const double* __restrict__ coords, const double* __restrict__ x,
+                                                       double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  int dofs[10];
+  for (int i = 0; i < nl; ++i) dofs[i] = tet_dofs[(long)nl * t + i];
+  double p[4][3];
+  for (int v = 0; v < 4; ++v) load_xyz(coords, dofs[v], p[v]);
+  TetGeo geo;
+  tet_geometry(p, geo);
+  double grads[10][3];
+  if (nl == 4) {
+    for (int i = 0; i < 4; ++i)
+      for (int d = 0; d < 3; ++d) grads[i][d] = geo.g[i][d];
+  } else {
+    p2_gradients(geo, 0, grads);
+  }
+  double g[3] = {0.0, 0.0, 0.0};
+  for (int i = 0; i < nl; ++i) {
+    const double xi = x[dofs[i]];
+    for (int d = 0; d < 3; ++d) g[d] = __dadd_rn(g[d], __dmul_rn(xi, grads[i][d]));
+  }
+  out[t] = kappa_dev(c_mat[tet_mat[t]],
+                     sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])), __dmul_rn(g[2], g[2]))));
+}
+
+void launch_cell_kappa(int order, int n_tets, const int* tet_dofs, const unsigned char* tet_mat, const double* coords,
+                       const double* x_full, double* kappa, cudaStream_t s) {
+  ++g_launch_count;
+  if (n_tets == 0) return;
+  k_cell_kappa<<<(n_tets + kBlock - 1) / kBlock, kBlock, 0, s>>>(n_tets, order == 1 ? 4 : 10, tet_dofs, tet_mat,
+                                                                 coords, x_full, kappa);
+}
+
 void launch_k_element(int order, int n_tets, const int* tet_dofs, const unsigned char* tet_mat, const double* coords,
                       const double* x_full, double* S, int* geo_error, cudaStream_t s) {
   ++g_launch_count;

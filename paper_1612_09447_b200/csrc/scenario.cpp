@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
@@ -32,25 +34,43 @@ struct PointLocation {
 
 // proj/src/probes.cpp:7-27 (brute-force scan)
 bool locate_point(const Mesh& mesh, const std::array<double, 3>& p, PointLocation& loc) {
+  // proj/src/probes.cpp:9-25: the first tet (ascending id) whose barycentric
+  // coordinates are all >= -1e-12. Scanned in parallel with a min-reduction
+  // over the containing ids, so the result is the sequential one.
+  int best = INT_MAX;
+  bool degenerate = false;
+#pragma omp parallel for schedule(static) reduction(min : best) reduction(|| : degenerate)
   for (int t = 0; t < mesh.n_tets; ++t) {
     double x[4][3];
     for (int v = 0; v < 4; ++v)
       for (int d = 0; d < 3; ++d) x[v][d] = mesh.nodes[3L * mesh.tets[4L * t + v] + d];
     TetGeo g;
-    if (!tet_geometry(x, g)) throw GeometryError("degenerate tetrahedron in element kernel");
+    if (!tet_geometry(x, g)) {
+      degenerate = true;
+      continue;
+    }
     double min_lambda = 1.0;
     for (int i = 0; i < 4; ++i) {
       double l = i == 0 ? 1.0 : 0.0;
       for (int d = 0; d < 3; ++d) l += g.g[i][d] * (p[d] - x[0][d]);
-      loc.lambda[i] = l;
       min_lambda = std::min(min_lambda, l);
     }
-    if (min_lambda >= -1e-12) {
-      loc.tet = t;
-      return true;
-    }
+    if (min_lambda >= -1e-12 && t < best) best = t;
   }
-  return false;
+  if (degenerate) throw GeometryError("degenerate tetrahedron in element kernel");
+  if (best == INT_MAX) return false;
+  double x[4][3];
+  for (int v = 0; v < 4; ++v)
+    for (int d = 0; d < 3; ++d) x[v][d] = mesh.nodes[3L * mesh.tets[4L * best + v] + d];
+  TetGeo g;
+  tet_geometry(x, g);
+  for (int i = 0; i < 4; ++i) {
+    double l = i == 0 ? 1.0 : 0.0;
+    for (int d = 0; d < 3; ++d) l += g.g[i][d] * (p[d] - x[0][d]);
+    loc.lambda[i] = l;
+  }
+  loc.tet = best;
+  return true;
 }
 
 // proj/src/probes.cpp:29-43 on the element's dof values
@@ -69,62 +89,78 @@ double interpolate(int order, const double* vals, const PointLocation& loc) {
   return value;
 }
 
-double kappa_host(const Material& m, double e) {  // proj/src/materials.cpp:25-33
-  if (!(e >= 0.0)) throw std::invalid_argument("kappa_of_e: negative field magnitude");
-  if (m.kind == 0) return m.kappa;
-  const double lo = std::log10(m.kappa_lo), hi = std::log10(m.kappa_hi);
-  const double s = 0.5 * (1.0 + std::tanh((e - m.e_switch) / m.width));
-  return std::pow(10.0, lo + (hi - lo) * s);
-}
-
 }  // namespace
 
-// proj/src/vtk_writer.cpp:11-49 (ASCII VTK 2.0, potential + per-cell kappa)
-void write_vtk(const std::string& path, const Problem& p, const std::vector<double>& x_full) {
-  std::ofstream os(path);
+// proj/src/vtk_writer.cpp:11-49 (VTK 2.0 unstructured grid, potential + per-cell
+// kappa). kappa comes from the device (GpuSystem::cell_kappa_host). binary
+// (additive key output.vtk_binary): legacy BINARY, big-endian, same arrays.
+namespace {
+template <class T>
+void put_be(std::ostream& os, T v) {
+  unsigned char b[sizeof(T)];
+  std::memcpy(b, &v, sizeof(T));
+  std::reverse(b, b + sizeof(T));
+  os.write(reinterpret_cast<const char*>(b), sizeof(T));
+}
+}  // namespace
+
+void write_vtk(const std::string& path, const Problem& p, const std::vector<double>& x_full,
+               const std::vector<double>& kappa, bool binary) {
+  std::ofstream os(path, std::ios::binary);
   if (!os) throw ConfigError("cannot open for writing: " + path);
   const Mesh& mesh = p.mesh;
-  const Dofs& dm = p.dm;
   char buf[128];
-  os << "# vtk DataFile Version 2.0\npotential\nASCII\nDATASET UNSTRUCTURED_GRID\n";
+  os << "# vtk DataFile Version 2.0\npotential\n" << (binary ? "BINARY" : "ASCII") << "\nDATASET UNSTRUCTURED_GRID\n";
   os << "POINTS " << mesh.n_nodes << " double\n";
-  for (int n = 0; n < mesh.n_nodes; ++n) {
-    std::snprintf(buf, sizeof buf, "%.9g %.9g %.9g\n", mesh.nodes[3L * n], mesh.nodes[3L * n + 1],
-                  mesh.nodes[3L * n + 2]);
-    os << buf;
+  if (binary) {
+    for (long k = 0; k < 3L * mesh.n_nodes; ++k) put_be(os, mesh.nodes[k]);
+    os << "\n";
+  } else {
+    for (int n = 0; n < mesh.n_nodes; ++n) {
+      std::snprintf(buf, sizeof buf, "%.9g %.9g %.9g\n", mesh.nodes[3L * n], mesh.nodes[3L * n + 1],
+                    mesh.nodes[3L * n + 2]);
+      os << buf;
+    }
   }
   os << "CELLS " << mesh.n_tets << " " << 5L * mesh.n_tets << "\n";
-  for (int t = 0; t < mesh.n_tets; ++t)
-    os << "4 " << mesh.tets[4L * t] << " " << mesh.tets[4L * t + 1] << " " << mesh.tets[4L * t + 2] << " "
-       << mesh.tets[4L * t + 3] << "\n";
-  os << "CELL_TYPES " << mesh.n_tets << "\n";
-  for (int t = 0; t < mesh.n_tets; ++t) os << "10\n";
-  os << "POINT_DATA " << mesh.n_nodes << "\nSCALARS potential double 1\nLOOKUP_TABLE default\n";
-  for (int n = 0; n < mesh.n_nodes; ++n) {
-    std::snprintf(buf, sizeof buf, "%.9g\n", x_full[n]);
-    os << buf;
+  if (binary) {
+    for (int t = 0; t < mesh.n_tets; ++t) {
+      put_be<int32_t>(os, 4);
+      for (int v = 0; v < 4; ++v) put_be<int32_t>(os, mesh.tets[4L * t + v]);
+    }
+    os << "\n";
+  } else {
+    for (int t = 0; t < mesh.n_tets; ++t)
+      os << "4 " << mesh.tets[4L * t] << " " << mesh.tets[4L * t + 1] << " " << mesh.tets[4L * t + 2] << " "
+         << mesh.tets[4L * t + 3] << "\n";
   }
+  os << "CELL_TYPES " << mesh.n_tets << "\n";
+  if (binary) {
+    for (int t = 0; t < mesh.n_tets; ++t) put_be<int32_t>(os, 10);
+    os << "\n";
+  } else {
+    for (int t = 0; t < mesh.n_tets; ++t) os << "10\n";
+  }
+  os << "POINT_DATA " << mesh.n_nodes << "\nSCALARS potential double 1\nLOOKUP_TABLE default\n";
+  for (int n = 0; n < mesh.n_nodes; ++n) {  // vertex dofs lead
+    if (binary) {
+      put_be(os, x_full[n]);
+    } else {
+      std::snprintf(buf, sizeof buf, "%.9g\n", x_full[n]);
+      os << buf;
+    }
+  }
+  if (binary) os << "\n";
   os << "CELL_DATA " << mesh.n_tets << "\nSCALARS kappa double 1\nLOOKUP_TABLE default\n";
   for (int t = 0; t < mesh.n_tets; ++t) {
-    double x[4][3];
-    for (int v = 0; v < 4; ++v)
-      for (int d = 0; d < 3; ++d) x[v][d] = mesh.nodes[3L * mesh.tets[4L * t + v] + d];
-    TetGeo g;
-    tet_geometry(x, g);
-    double gr[10][3];
-    if (dm.order == 1) {
-      for (int i = 0; i < 4; ++i)
-        for (int d = 0; d < 3; ++d) gr[i][d] = g.g[i][d];
+    if (binary) {
+      put_be(os, kappa[t]);
     } else {
-      p2_gradients(g, 0, gr);
+      std::snprintf(buf, sizeof buf, "%.9g\n", kappa[t]);
+      os << buf;
     }
-    double gx[3] = {0, 0, 0};
-    for (int i = 0; i < dm.n_local; ++i)
-      for (int d = 0; d < 3; ++d) gx[d] += x_full[dm.element_dofs[(size_t)dm.n_local * t + i]] * gr[i][d];
-    const double e = std::sqrt(gx[0] * gx[0] + gx[1] * gx[1] + gx[2] * gx[2]);
-    std::snprintf(buf, sizeof buf, "%.9g\n", kappa_host(p.materials.at(mesh.region[t]), e));
-    os << buf;
   }
+  if (binary) os << "\n";
 }
 
 // proj/src/metrics.cpp:20-35
@@ -280,7 +316,9 @@ RunResult run_scenario(const SimConfig& config, const std::string& out_dir, int 
           x_full.resize(P.dm.n_dofs);
           sys.get_state(x_host.data());
           sys.lift_full_host(sys.state_t, x_host.data(), x_full.data());
-          write_vtk(join_path(out_dir, name), P, x_full);
+          std::vector<double> kappa(P.mesh.n_tets);
+          sys.cell_kappa_host(kappa.data());
+          write_vtk(join_path(out_dir, name), P, x_full, kappa, config.vtk_binary);
         }
       } else if (++consecutive_rejections > 40) {
         throw NumericalError("no accepted step after 40 attempts");

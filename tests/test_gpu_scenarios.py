@@ -169,3 +169,57 @@ def test_pod_estimators_nonlinear_scenario_c7():  # acceptance_main.cpp:272-299 
     print("C7 PCG iterations: spe %d, pod_fixed %d (%d SVDs), pod_rolling %d (%d SVDs)" % (
         spe["stats"]["pcg_iterations"], fixed["stats"]["pcg_iterations"], fixed["stats"]["svd_count"],
         rolling["stats"]["pcg_iterations"], rolling["stats"]["svd_count"]))
+
+
+def _vtk_arrays(path, n_nodes, n_tets):
+    data = open(path, "rb").read()
+    pot_tag = b"SCALARS potential double 1\nLOOKUP_TABLE default\n"
+    kap_tag = b"SCALARS kappa double 1\nLOOKUP_TABLE default\n"
+    if b"\nBINARY\n" in data[:80]:
+        i = data.index(pot_tag) + len(pot_tag)
+        pot = np.frombuffer(data[i:i + 8 * n_nodes], dtype=">f8")
+        j = data.index(kap_tag) + len(kap_tag)
+        kap = np.frombuffer(data[j:j + 8 * n_tets], dtype=">f8")
+        k = data.index(b"POINTS") + len(b"POINTS %d double\n" % n_nodes)
+        pts = np.frombuffer(data[k:k + 24 * n_nodes], dtype=">f8").reshape(-1, 3)
+    else:
+        text = data.decode()
+        pot = np.array(text.split(pot_tag.decode())[1].split("CELL_DATA")[0].split(), float)
+        kap = np.array(text.split(kap_tag.decode())[1].split(), float)
+        pts = np.array(text.split("double\n", 1)[1].split("CELLS")[0].split(), float).reshape(-1, 3)
+    return pts, pot, kap
+
+
+def test_vtk_dump_ascii_binary_and_device_kappa(tmp_path):  # vtk_writer.cpp:11-49 (+ additive vtk_binary)
+    cfg = slab_reference("slab_nonlinear_rkc_spe")
+    cfg["max_steps"] = 30
+    arrays = {}
+    for binary in (False, True):
+        cfg["output"] = {"metrics_csv": "", "probe_csv": "", "solves_csv": "", "vtk_prefix": "v", "vtk_every": 1,
+                         "vtk_binary": binary}
+        out = tmp_path / ("bin" if binary else "asc")
+        r = eb.run_scenario(cfg, out_dir=str(out))
+        assert r["exit_code"] == 0, r.get("error")
+        last = sorted(out.glob("v_*.vtk"))[-1]
+        g = eb.FemSystem(cfg, device=-1)
+        nodes, tets, region = g.mesh()
+        arrays[binary] = _vtk_arrays(str(last), len(nodes), len(tets)), r
+    (pa, va, ka), ra = arrays[False]
+    (pb, vb, kb), rb = arrays[True]
+    assert np.array_equal(ra["x"], rb["x"])
+    assert np.allclose(pa, pb, rtol=1e-8, atol=0) and np.array_equal(pb.ravel(), nodes.ravel())
+    assert np.allclose(va, vb, rtol=1e-8, atol=1e-12 * np.abs(vb).max())
+    assert np.allclose(ka, kb, rtol=1e-8, atol=0)
+    # device kappa = kappa_of_e(|grad x_h|) of the final state (materials.cpp:25-33)
+    o = po.Problem(cfg)
+    full = o.lift_full(rb["final_t"], rb["x"])
+    assert np.allclose(full[:len(nodes)], vb, rtol=1e-12, atol=1e-9 * np.abs(vb).max())
+    P = nodes[tets]  # [t][4][3]
+    E = P[:, 1:, :] - P[:, :1, :]
+    G = np.linalg.inv(E)  # rows: grad(lambda_1..3) as columns of inv(E)
+    grads = np.concatenate([-G.sum(axis=2, keepdims=True), G], axis=2)  # [t][3][4]
+    gx = np.einsum("tdi,ti->td", grads, full[tets])
+    e = np.linalg.norm(gx, axis=1)
+    mats = cfg["materials"]
+    ref = np.array([po.kappa_of_e(mats[str(rg)], ee) for rg, ee in zip(region, e)])
+    assert np.allclose(kb, ref, rtol=1e-9, atol=0)
