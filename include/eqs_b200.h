@@ -322,7 +322,8 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * 12 = start-vector estimator (0 zero, 1 previous, 2 spe, 3 pod_fixed, 4 pod_rolling;
  * resets its history), 15/16/17/18 = POD snapshots / rank / capacity / threshold
  * (estimator config keys "snapshots", "rank", "capacity", "threshold"; take effect
- * at the next reset),
+ * at the next reset), 19 = stencil-coded fine-level V-cycle operator (0/1; default 1
+ * where the rows share at most 255 column-offset patterns),
  * 13 = smoother polynomial (0 first-kind Chebyshev, 1 fourth-kind, 2 fourth-kind
  * with optimised weights), 14 = lambda_max safety factor (default 1.1).
  * The PCG operator and vectors are fp64 in every setting. */

@@ -63,6 +63,15 @@ struct DevSellP {
   const uint4* words = nullptr;
 };
 
+// Stencil-coded SELL (sell.hpp HostSellS): per row a pattern id, per entry the
+// bf16 value; column = row + pat[pid][slot]
+struct DevSellS {
+  int n_chunks = 0, G = 0, P = 0;
+  const uint4* vals = nullptr;           // [n_chunks][G][32] x 8 bf16
+  const unsigned char* pid = nullptr;    // [n_chunks * 32]
+  const int* pat = nullptr;              // [P][8 G]
+};
+
 // CSR matrix resident in HBM (int32 indices, fp64 values, sorted columns),
 // optionally with reduced-precision value copies and a SELL copy that the
 // kernels use instead when `use_sell` is set.
@@ -78,7 +87,10 @@ struct DevCsr {
   bool use_sell = false;
   DevSell sell;
   DevSellP pk;  // used instead of `sell` for bf16 values (prec 2) when present
+  DevSellS st;  // used instead of `pk` when present and use_stencil (fine level, structured meshes)
+  bool use_stencil = true;
   bool packed() const { return use_sell && prec == 2 && pk.tpr > 0; }
+  bool stencil() const { return use_sell && prec == 2 && use_stencil && st.G > 0; }
   bool sell16() const { return use_sell && sell.tpr > 0 && !packed(); }
   int lanes() const { return packed() ? pk.tpr : sell16() ? sell.tpr : tpr; }
 };

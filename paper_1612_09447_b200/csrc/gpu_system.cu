@@ -166,6 +166,27 @@ void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.pk.words = reinterpret_cast<const uint4*>(b.pk_words.p);
 }
 
+// stencil-coded bf16 copy (sell.hpp SELL-S) for the fine-level V-cycle
+// operator; absent when the rows need too many patterns (unstructured meshes)
+void upload_stencil(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
+  d.st = DevSellS{};
+  HostSellS hs;
+  if (h.n_rows == 0 || !build_sell_stencil(h, hs)) return;
+  b.st_vals.alloc(hs.vals.size());
+  b.st_vals.upload(hs.vals.data(), hs.vals.size(), s);
+  b.st_pid.alloc(hs.pid.size());
+  b.st_pid.upload(hs.pid.data(), hs.pid.size(), s);
+  b.st_pat.alloc(hs.pat.size());
+  b.st_pat.upload(hs.pat.data(), hs.pat.size(), s);
+  CK(cudaStreamSynchronize(s));
+  d.st.n_chunks = hs.n_chunks;
+  d.st.G = hs.G;
+  d.st.P = hs.P;
+  d.st.vals = reinterpret_cast<const uint4*>(b.st_vals.p);
+  d.st.pid = b.st_pid.p;
+  d.st.pat = b.st_pat.p;
+}
+
 // 1/diag of the owned rows (local row i <-> local column i)
 // EQS_MEMTRACE=1: host RSS / peak at setup checkpoints (stderr)
 void memtrace(const char* tag) {
@@ -486,6 +507,7 @@ void GpuSystem::build_device() {
   // M_II (owned rows, local columns) + level-0 halo
   upload_csr(plan_.mii, mii_, mii_rp_, mii_ci_, mii_v_, s);
   upload_sell(plan_.mii, mii_, mii_s_, s);
+  upload_stencil(plan_.mii, mii_, mii_s_, s);
   set_sell(sell_on_);
   build_halo(plan_.space[0], halo0_);
   {
@@ -707,6 +729,12 @@ void GpuSystem::set_vcycle_precision(int prec) {
     lv.R.values_f = lv.r_vf.p;
     lv.A.prec = lv.P.prec = lv.R.prec = prec;
   }
+}
+
+void GpuSystem::set_stencil(bool on) {
+  invalidate_graphs();
+  mii_.use_stencil = on;
+  for (auto& lv : levels_) lv.A.use_stencil = on;
 }
 
 void GpuSystem::set_sell(bool on) {

@@ -95,6 +95,9 @@ struct SellBufs {
   DevBuf<uint16_t> v16;
   DevBuf<int> pk_cp, pk_bases;  // packed bf16 copy (sell.hpp SELL-P)
   DevBuf<uint32_t> pk_words;
+  DevBuf<uint16_t> st_vals;     // stencil-coded bf16 copy (sell.hpp SELL-S)
+  DevBuf<unsigned char> st_pid;
+  DevBuf<int> st_pat;
 };
 
 struct DevLevel {
@@ -211,6 +214,7 @@ class GpuSystem {
   void set_cheb(double ratio);
   void set_vcycle_precision(int prec);  // V-cycle matrix values: 0 fp64, 1 fp32, 2 bf16
   void set_sell(bool on);               // SELL-16 copies instead of CSR where available
+  void set_stencil(bool on);            // stencil-coded fine-level V-cycle operator where available
   void set_vcycle_vectors_f32(bool on) {  // V-cycle vectors fp32 (default) or fp64
     invalidate_graphs();
     vcycle_f32_ = on;

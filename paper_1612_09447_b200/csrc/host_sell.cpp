@@ -182,4 +182,71 @@ bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out) {
   return false;
 }
 
+
+bool build_sell_stencil(const HostCsr& a, HostSellS& out) {
+  const int n = a.n_rows;
+  int lmax = 0;
+  for (int r = 0; r < n; ++r) lmax = std::max(lmax, a.row_ptr[r + 1] - a.row_ptr[r]);
+  const int L = std::max(8, (lmax + 7) / 8 * 8);
+  if (L > 32 || n == 0) return false;
+  // row signature hash (length + offsets), then ids in row order with an exact check
+  std::vector<uint64_t> h(n);
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < n; ++r) {
+    uint64_t x = 1469598103934665603ull ^ (uint64_t)(a.row_ptr[r + 1] - a.row_ptr[r]);
+    for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
+      x ^= (uint64_t)(uint32_t)(a.col_idx[k] - r);
+      x *= 1099511628211ull;
+    }
+    h[r] = x;
+  }
+  HostSellS s;
+  s.n_rows = n;
+  s.n_chunks = (n + 31) / 32;
+  s.G = L / 8;
+  s.pid.assign((size_t)s.n_chunks * 32, 0);
+  std::vector<uint64_t> keys;
+  std::vector<int> rep;  // representative row per pattern
+  auto same = [&](int r, int q) {
+    const int lr = a.row_ptr[r + 1] - a.row_ptr[r];
+    if (lr != a.row_ptr[q + 1] - a.row_ptr[q]) return false;
+    for (int k = 0; k < lr; ++k)
+      if (a.col_idx[a.row_ptr[r] + k] - r != a.col_idx[a.row_ptr[q] + k] - q) return false;
+    return true;
+  };
+  for (int r = 0; r < n; ++r) {
+    int id = -1;
+    if (r > 0 && keys[s.pid[r - 1]] == h[r] && same(r, rep[s.pid[r - 1]])) id = s.pid[r - 1];  // common case
+    for (size_t p = 0; p < keys.size() && id < 0; ++p)
+      if (keys[p] == h[r] && same(r, rep[p])) {
+        id = (int)p;
+        break;
+      }
+    if (id < 0) {
+      if (keys.size() == 255) return false;
+      id = (int)keys.size();
+      keys.push_back(h[r]);
+      rep.push_back(r);
+    }
+    s.pid[r] = (uint8_t)id;
+  }
+  s.P = (int)keys.size();
+  s.pat.assign((size_t)s.P * L, 0);
+  for (int p = 0; p < s.P; ++p) {
+    const int r = rep[p];
+    for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) s.pat[(size_t)p * L + (k - a.row_ptr[r])] = a.col_idx[k] - r;
+  }
+  s.vals.assign((size_t)s.n_chunks * 32 * L, 0);
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < n; ++r) {
+    const int c = r / 32, lane = r % 32;
+    for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
+      const int j = k - a.row_ptr[r];
+      s.vals[(((size_t)c * s.G + j / 8) * 32 + lane) * 8 + j % 8] = to_bf16(a.values[k]);
+    }
+  }
+  out = std::move(s);
+  return true;
+}
+
 }  // namespace eqsb

@@ -24,7 +24,9 @@ namespace eqsb {
 // (n_cols each) and the streamed row vectors (n_rows each).
 double matrix_pass_bytes(const DevCsr& a, int gathered, int streamed, int xbytes) {
   double m;
-  if (a.packed()) {
+  if (a.stencil()) {
+    m = 16.0 * 32.0 * a.st.G * a.st.n_chunks + 32.0 * a.st.n_chunks + 32.0 * a.st.G * a.st.P;
+  } else if (a.packed()) {
     m = 4.0 * (double)a.pk.padded + (4.0 + 4.0 * a.pk.windows) * a.pk.n_chunks;
   } else if (a.sell16()) {
     const double vs = a.prec == 2 ? 2.0 : a.prec == 1 ? 4.0 : 8.0;
@@ -167,6 +169,43 @@ __device__ __forceinline__ XT sellp_dot(const DevSellP& m, int chunk, int lane, 
   return s;
 }
 
+// Stencil-coded rows (TPR 1, one row per lane): the pattern table is staged in
+// shared memory (spat); slot j of the row holds the value of its j-th CSR
+// entry, so the products are summed in the same order as the TPR-1 SELL-P pass.
+template <class XT, bool SCALED, bool CG = false>
+__device__ __forceinline__ XT sells_dot(const DevSellS& m, const int* __restrict__ spat, int chunk, int lane,
+                                        int row, const XT* __restrict__ x, const XT* __restrict__ w) {
+  const int G = m.G;
+  const int* off = spat + (int)__ldcs(m.pid + 32L * chunk + lane) * (8 * G);
+  const uint4* v = m.vals + (long)chunk * G * 32 + lane;
+  uint4 qs[4];  // all value groups in flight before the gathers (G <= 4)
+#pragma unroll
+  for (int g = 0; g < 4; ++g) qs[g] = g < G ? __ldcs(v + 32 * g) : make_uint4(0u, 0u, 0u, 0u);
+  XT s = 0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (g >= G) break;
+    const uint4 q = qs[g];
+    const unsigned wd[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+#pragma unroll
+      for (int hbit = 0; hbit < 2; ++hbit) {
+        const int c = row + off[8 * g + 2 * e + hbit];
+        const XT a = (XT)__uint_as_float(hbit ? (wd[e] & 0xffff0000u) : (wd[e] << 16));
+        const XT xv = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
+        s += a * xv;
+      }
+    }
+  }
+  return s;
+}
+
+__device__ __forceinline__ void stage_patterns(const DevSellS& m, int* spat) {
+  for (int i = threadIdx.x; i < m.P * 8 * m.G; i += blockDim.x) spat[i] = __ldg(m.pat + i);
+  __syncthreads();
+}
+
 // Row epilogues (load before the pass, store after).
 // Row ops (MODE < 0):
 // OP 0: y = A x                       (restriction, plain SpMV)
@@ -305,6 +344,46 @@ __global__ void __launch_bounds__(kBlock) k_sellp(int n, DevSellP m, const XT* _
   if (act) e.store(row, s, y, y2, nullptr, c, 0);
 }
 
+template <class XT, int OP, bool PRE>
+__global__ void __launch_bounds__(kBlock) k_sells(int n, DevSellS m, const XT* __restrict__ x,
+                                                  const XT* __restrict__ b, const XT* __restrict__ invd,
+                                                  XT* __restrict__ y, XT* __restrict__ y2, ChebCoef c,
+                                                  const XT* __restrict__ pre) {
+  extern __shared__ int spat[];
+  stage_patterns(m, spat);
+  const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (chunk >= m.n_chunks) return;  // warp-uniform exit
+  constexpr bool SC = kScaled<OP, -1>;
+  const int row = chunk * 32 + lane;
+  const bool act = row < n;
+  Epi<OP, -1, XT> e;
+  if (act) e.load(row, x, b, invd, y, nullptr, 0);
+  const XT s = sells_dot<XT, SC && !PRE>(m, spat, chunk, lane, act ? row : 0, SC ? (PRE ? pre : b) : x, invd);
+  if (act) e.store(row, s, y, y2, nullptr, c, 0);
+}
+
+template <class XT, int MODE, bool PRE>
+__global__ void __launch_bounds__(kBlock) k_sells_red(int n, DevSellS m, const XT* __restrict__ x,
+                                                      const XT* __restrict__ b, const XT* __restrict__ invd,
+                                                      XT* __restrict__ y, double* __restrict__ out64,
+                                                      const double* __restrict__ b64, ChebCoef c, Reducer red,
+                                                      int slot, int do_red, const XT* __restrict__ pre) {
+  extern __shared__ int spat[];
+  stage_patterns(m, spat);
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (kBlock / 32);
+  double acc = 0.0;
+  for (int chunk = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); chunk < m.n_chunks; chunk += warps) {
+    const int row = chunk * 32 + lane;
+    const bool act = row < n;
+    Epi<0, MODE, XT> e;
+    if (act) e.load(row, x, b, invd, y, b64, do_red);
+    const XT s = sells_dot<XT, kScaled<0, MODE> && !PRE>(m, spat, chunk, lane, act ? row : 0, PRE ? pre : x, invd);
+    if (act) acc += e.store(row, s, y, nullptr, out64, c, do_red);
+  }
+  reduce_finish(acc, red, slot);
+}
+
 template <int TPR, class XT, int MODE, bool PRE>
 __global__ void __launch_bounds__(kBlock) k_sellp_red(int n, DevSellP m, const XT* __restrict__ x,
                                                       const XT* __restrict__ b, const XT* __restrict__ invd,
@@ -400,6 +479,19 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
   const int p = eff_prec<XT>(a);
   DevCsr view = a;
   view.prec = p;
+  if (view.stencil()) {
+    const DevSellS& m = a.st;
+    const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
+    const size_t smem = sizeof(int) * m.P * 8 * m.G;
+    if (pre && kScaled<OP, -1>) {
+      g_algo_bytes += matrix_pass_bytes(view, 1, kS[OP] + 2, sizeof(XT));
+      k_sells<XT, OP, true><<<g, kBlock, smem, s>>>(a.n_rows, m, x, b, invd, y, y2, c, pre);
+    } else {
+      g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
+      k_sells<XT, OP, false><<<g, kBlock, smem, s>>>(a.n_rows, m, x, b, invd, y, y2, c, nullptr);
+    }
+    return;
+  }
   if (view.packed()) {
     const DevSellP& m = a.pk;
     const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
@@ -453,12 +545,24 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
   const int p = eff_prec<XT>(a);
   DevCsr view = a;
   view.prec = p;
-  const bool use_pre = pre && kScaled<0, MODE> && view.packed();
+  const bool use_pre = pre && kScaled<0, MODE> && (view.packed() || view.stencil());
   double bytes = use_pre ? matrix_pass_bytes(view, 1, kS[MODE] + 2, sizeof(XT))
                          : matrix_pass_bytes(view, kG[MODE], kS[MODE], sizeof(XT));
   if (MODE == 2 && red) bytes += sizeof(XT) * (double)a.n_rows;
   if (MODE == 3) bytes += (red ? 16.0 : 8.0) * a.n_rows;
   g_algo_bytes += bytes;
+  if (view.stencil()) {
+    const DevSellS& m = a.st;
+    const long work = (long)m.n_chunks * 32;
+    const size_t smem = sizeof(int) * m.P * 8 * m.G;
+    if (use_pre)
+      k_sells_red<XT, MODE, true><<<red_grid(k_sells_red<XT, MODE, true>, work), kBlock, smem, s>>>(
+          a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, pre);
+    else
+      k_sells_red<XT, MODE, false><<<red_grid(k_sells_red<XT, MODE, false>, work), kBlock, smem, s>>>(
+          a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, nullptr);
+    return;
+  }
   if (view.packed()) {
     const DevSellP& m = a.pk;
     const long work = (long)m.n_chunks * 32;

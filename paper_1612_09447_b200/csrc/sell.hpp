@@ -70,6 +70,23 @@ struct HostSellP {
   long padded() const { return chunk_ptr.empty() ? 0 : 4L * chunk_ptr.back(); }
 };
 
+// Stencil-coded SELL ("SELL-S") for operators whose rows share a few
+// column-offset lists (the fine level of structured meshes): pattern table
+// [P][L] of offsets col - row (P <= 255, L = 8 G <= 32 slots, padding offset
+// 0 with value 0), one pattern id per row and only the bf16 values, row r
+// (chunk c = r / 32, lane r % 32) slot j at ((c G + j / 8) 32 + lane) 8 + j % 8:
+// one 16-byte load gives a lane 8 values. Entries keep the CSR (column) order,
+// so a TPR-1 SELL-P pass and a SELL-S pass sum the same products in the same
+// order. 2 B per entry + 1 B per row instead of 4 B per entry.
+struct HostSellS {
+  int n_rows = 0, n_chunks = 0, G = 0, P = 0;
+  std::vector<uint16_t> vals;   // [n_chunks][G][32][8]
+  std::vector<uint8_t> pid;     // [n_chunks * 32]
+  std::vector<int> pat;         // [P][8 G]
+};
+// false when the rows need more than 255 patterns or more than 32 slots
+bool build_sell_stencil(const HostCsr& a, HostSellS& out);
+
 uint16_t to_bf16(double d);  // round to nearest even
 // lanes per row of the packed format: about 32 entries per lane (fewer
 // shuffle-reduction steps and more loads in flight per lane on coarse levels)

@@ -69,6 +69,53 @@ static int check_sell16(const HostCsr& a, const HostSell& h) {
   return 0;
 }
 
+// SELL-S: slot j of row r decodes to the row's j-th CSR entry (column row +
+// pat[pid][j], bf16 value), padding slots to value 0 at column row
+static int check_stencil(const HostCsr& a, const HostSellS& h) {
+  const int L = 8 * h.G;
+  int bad = 0;
+  for (int r = 0; r < a.n_rows; ++r) {
+    const int c = r / 32, lane = r % 32, len = a.row_ptr[r + 1] - a.row_ptr[r];
+    for (int j = 0; j < L; ++j) {
+      const uint16_t v = h.vals[(((size_t)c * h.G + j / 8) * 32 + lane) * 8 + j % 8];
+      const int col = r + h.pat[(size_t)h.pid[r] * L + j];
+      if (j < len) {
+        const int k = a.row_ptr[r] + j;
+        bad += col != a.col_idx[k] || v != to_bf16(a.values[k]);
+      } else {
+        bad += v != 0 || col != r;
+      }
+    }
+  }
+  return bad;
+}
+
+// structured 15-point rows (Kuhn-box M_II-like): 3D grid with offsets
+// (di, dj, dk) in {-1,0,1}^3 restricted to the 15 Kuhn-mesh neighbours
+static HostCsr kuhn_like(int nx, int ny, int nz) {
+  const int off[15][3] = {{0, 0, 0},  {1, 0, 0},   {-1, 0, 0}, {0, 1, 0},  {0, -1, 0}, {0, 0, 1},  {0, 0, -1}, {1, 1, 0},
+                          {-1, -1, 0}, {1, 0, 1},  {-1, 0, -1}, {0, 1, 1}, {0, -1, -1}, {1, 1, 1}, {-1, -1, -1}};
+  HostCsr a;
+  a.n_rows = a.n_cols = nx * ny * nz;
+  a.row_ptr.push_back(0);
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        std::vector<int> cols;
+        for (auto& o : off) {
+          const int ii = i + o[0], jj = j + o[1], kk = k + o[2];
+          if (ii >= 0 && ii < nx && jj >= 0 && jj < ny && kk >= 0 && kk < nz) cols.push_back((kk * ny + jj) * nx + ii);
+        }
+        std::sort(cols.begin(), cols.end());
+        for (int col : cols) {
+          a.col_idx.push_back(col);
+          a.values.push_back(0.25 + 1e-3 * (col % 97) - (col == (int)a.row_ptr.size() - 1 ? 0.0 : 0.5));
+        }
+        a.row_ptr.push_back((int)a.col_idx.size());
+      }
+  return a;
+}
+
 int main() {
   std::mt19937 g(20261017u);
   int fails = 0;
@@ -135,6 +182,35 @@ int main() {
     printf("clusters %d tpr %d packed %d shift %d -> %s\n", nclus, tpr, okp, p.shift,
            fp || p.shift != want_shift ? "FAIL" : "ok");
     fails += fp + (p.shift != want_shift);
+  }
+  // SELL-S on structured rows (27 patterns for a box interior + faces/edges/corners)
+  {
+    const HostCsr a = kuhn_like(13, 11, 9);
+    HostSellS h;
+    const bool ok = build_sell_stencil(a, h);
+    const int fs = ok ? check_stencil(a, h) : 1;
+    printf("stencil kuhn-like %d rows: ok %d patterns %d G %d -> %s\n", a.n_rows, ok, h.P, h.G,
+           fs || h.P != 27 || h.G != 2 ? "FAIL" : "ok");
+    fails += fs + (h.P != 27) + (h.G != 2);
+  }
+  {  // random columns: too many patterns -> no stencil copy
+    HostCsr a;
+    a.n_rows = a.n_cols = 5000;
+    a.row_ptr.push_back(0);
+    for (int i = 0; i < a.n_rows; ++i) {
+      std::vector<int> cols = {i, (int)(g() % 5000), (int)(g() % 5000)};
+      std::sort(cols.begin(), cols.end());
+      cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+      for (int col : cols) {
+        a.col_idx.push_back(col);
+        a.values.push_back(1.0);
+      }
+      a.row_ptr.push_back((int)a.col_idx.size());
+    }
+    HostSellS h;
+    const bool ok = build_sell_stencil(a, h);
+    printf("stencil random rows: built %d -> %s\n", ok, ok ? "FAIL" : "ok");
+    fails += ok;
   }
   return fails ? 1 : 0;
 }

@@ -267,3 +267,18 @@ def test_dense_coarse_truncation():
     assert r1.iterations <= r0.iterations + 1
     for x in (x0, x1):
         assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+
+
+def test_stencil_vcycle_matches_packed():
+    """The stencil-coded fine-level V-cycle operator (SELL-S, option 19) sums
+    the same bf16 products in the same order as the packed SELL-P pass, so
+    the M-solve takes the same iterations and lands on the same solution (the
+    reduction grids differ, so dot products may differ in the last bits)."""
+    g = eb.FemSystem(cube(16, jitter=0.1, planes=(0.45, 0.55)))
+    b = po.random_vec(g.n_free, 77)
+    x1, r1 = g.mass_solve(b)
+    g.set_option(19, 0)
+    x0, r0 = g.mass_solve(b)
+    g.set_option(19, 1)
+    assert r1.iterations == r0.iterations
+    assert np.linalg.norm(x1 - x0) <= 1e-13 * np.linalg.norm(x0)
