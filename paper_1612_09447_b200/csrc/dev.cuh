@@ -70,6 +70,7 @@ struct DevSellS {
   const uint4* vals = nullptr;           // [n_chunks][G][32] x 8 bf16
   const unsigned char* pid = nullptr;    // [n_chunks * 32]
   const int* pat = nullptr;              // [P][8 G]
+  const double* vals64 = nullptr;        // [n_chunks][8 G][32] fp64 values (PCG operator) or null
 };
 
 // CSR matrix resident in HBM (int32 indices, fp64 values, sorted columns),
@@ -91,6 +92,7 @@ struct DevCsr {
   bool use_stencil = true;
   bool packed() const { return use_sell && prec == 2 && pk.tpr > 0; }
   bool stencil() const { return use_sell && prec == 2 && use_stencil && st.G > 0; }
+  bool stencil64() const { return use_sell && prec == 0 && use_stencil && st.vals64 != nullptr; }
   bool sell16() const { return use_sell && sell.tpr > 0 && !packed(); }
   int lanes() const { return packed() ? pk.tpr : sell16() ? sell.tpr : tpr; }
 };

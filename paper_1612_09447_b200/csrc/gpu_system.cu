@@ -171,13 +171,15 @@ void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
 void upload_stencil(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.st = DevSellS{};
   HostSellS hs;
-  if (h.n_rows == 0 || !build_sell_stencil(h, hs)) return;
+  if (h.n_rows == 0 || !build_sell_stencil(h, hs, true)) return;
   b.st_vals.alloc(hs.vals.size());
   b.st_vals.upload(hs.vals.data(), hs.vals.size(), s);
   b.st_pid.alloc(hs.pid.size());
   b.st_pid.upload(hs.pid.data(), hs.pid.size(), s);
   b.st_pat.alloc(hs.pat.size());
   b.st_pat.upload(hs.pat.data(), hs.pat.size(), s);
+  b.st_v64.alloc(hs.vals64.size());
+  b.st_v64.upload(hs.vals64.data(), hs.vals64.size(), s);
   CK(cudaStreamSynchronize(s));
   d.st.n_chunks = hs.n_chunks;
   d.st.G = hs.G;
@@ -185,6 +187,7 @@ void upload_stencil(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.st.vals = reinterpret_cast<const uint4*>(b.st_vals.p);
   d.st.pid = b.st_pid.p;
   d.st.pat = b.st_pat.p;
+  d.st.vals64 = hs.vals64.empty() ? nullptr : b.st_v64.p;
 }
 
 // 1/diag of the owned rows (local row i <-> local column i)

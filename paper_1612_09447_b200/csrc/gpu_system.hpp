@@ -98,6 +98,7 @@ struct SellBufs {
   DevBuf<uint16_t> st_vals;     // stencil-coded bf16 copy (sell.hpp SELL-S)
   DevBuf<unsigned char> st_pid;
   DevBuf<int> st_pat;
+  DevBuf<double> st_v64;
 };
 
 struct DevLevel {

@@ -183,7 +183,7 @@ bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out) {
 }
 
 
-bool build_sell_stencil(const HostCsr& a, HostSellS& out) {
+bool build_sell_stencil(const HostCsr& a, HostSellS& out, bool with_fp64) {
   const int n = a.n_rows;
   int lmax = 0;
   for (int r = 0; r < n; ++r) lmax = std::max(lmax, a.row_ptr[r + 1] - a.row_ptr[r]);
@@ -243,6 +243,15 @@ bool build_sell_stencil(const HostCsr& a, HostSellS& out) {
     for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
       const int j = k - a.row_ptr[r];
       s.vals[(((size_t)c * s.G + j / 8) * 32 + lane) * 8 + j % 8] = to_bf16(a.values[k]);
+    }
+  }
+  if (with_fp64) {
+    s.vals64.assign((size_t)s.n_chunks * 32 * L, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < n; ++r) {
+      const int c = r / 32, lane = r % 32;
+      for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k)
+        s.vals64[((size_t)c * L + (k - a.row_ptr[r])) * 32 + lane] = a.values[k];
     }
   }
   out = std::move(s);

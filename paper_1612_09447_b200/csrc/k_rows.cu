@@ -24,7 +24,9 @@ namespace eqsb {
 // (n_cols each) and the streamed row vectors (n_rows each).
 double matrix_pass_bytes(const DevCsr& a, int gathered, int streamed, int xbytes) {
   double m;
-  if (a.stencil()) {
+  if (a.stencil64()) {
+    m = 8.0 * 8.0 * 32.0 * a.st.G * a.st.n_chunks + 32.0 * a.st.n_chunks + 32.0 * a.st.G * a.st.P;
+  } else if (a.stencil()) {
     m = 16.0 * 32.0 * a.st.G * a.st.n_chunks + 32.0 * a.st.n_chunks + 32.0 * a.st.G * a.st.P;
   } else if (a.packed()) {
     m = 4.0 * (double)a.pk.padded + (4.0 + 4.0 * a.pk.windows) * a.pk.n_chunks;
@@ -197,6 +199,24 @@ __device__ __forceinline__ XT sells_dot(const DevSellS& m, const int* __restrict
         s += a * xv;
       }
     }
+  }
+  return s;
+}
+
+// fp64 values (the PCG operator M_II): slot j of the chunk's lanes is one
+// 256-byte warp load; products summed in CSR order
+__device__ __forceinline__ double sells_dot64(const DevSellS& m, const int* __restrict__ spat, int chunk, int lane,
+                                              int row, const double* __restrict__ x) {
+  const int L = 8 * m.G;
+  const int* off = spat + (int)__ldcs(m.pid + 32L * chunk + lane) * L;
+  const double* v = m.vals64 + (long)chunk * L * 32 + lane;
+  double s = 0.0;
+  for (int j0 = 0; j0 < L; j0 += 8) {
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = __ldcs(v + 32 * (j0 + u));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += a[u] * __ldg(x + row + off[j0 + u]);
   }
   return s;
 }
@@ -384,6 +404,27 @@ __global__ void __launch_bounds__(kBlock) k_sells_red(int n, DevSellS m, const X
   reduce_finish(acc, red, slot);
 }
 
+// q = A p (OP 0) / q = A p, p.q (MODE 0) with the fp64 stencil-coded operator
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_sells64(int n, DevSellS m, const double* __restrict__ x,
+                                                    double* __restrict__ y, Reducer red, int slot, int do_red) {
+  extern __shared__ int spat[];
+  stage_patterns(m, spat);
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (kBlock / 32);
+  double acc = 0.0;
+  for (int chunk = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); chunk < m.n_chunks; chunk += warps) {
+    const int row = chunk * 32 + lane;
+    const bool act = row < n;
+    const double s = sells_dot64(m, spat, chunk, lane, act ? row : 0, x);
+    if (act) {
+      y[row] = s;
+      if (MODE == 0) acc += x[row] * s;
+    }
+  }
+  if (MODE == 0 && do_red) reduce_finish(acc, red, slot);
+}
+
 template <int TPR, class XT, int MODE, bool PRE>
 __global__ void __launch_bounds__(kBlock) k_sellp_red(int n, DevSellP m, const XT* __restrict__ x,
                                                       const XT* __restrict__ b, const XT* __restrict__ invd,
@@ -479,6 +520,15 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
   const int p = eff_prec<XT>(a);
   DevCsr view = a;
   view.prec = p;
+  if constexpr (std::is_same_v<XT, double> && OP == 0) {
+    if (view.stencil64()) {
+      const DevSellS& m = a.st;
+      g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
+      k_sells64<-1><<<red_grid(k_sells64<-1>, (long)m.n_chunks * 32), kBlock, sizeof(int) * m.P * 8 * m.G, s>>>(
+          a.n_rows, m, x, y, Reducer{}, 0, 0);
+      return;
+    }
+  }
   if (view.stencil()) {
     const DevSellS& m = a.st;
     const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
@@ -550,6 +600,15 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
                          : matrix_pass_bytes(view, kG[MODE], kS[MODE], sizeof(XT));
   if (MODE == 2 && red) bytes += sizeof(XT) * (double)a.n_rows;
   if (MODE == 3) bytes += (red ? 16.0 : 8.0) * a.n_rows;
+  if constexpr (std::is_same_v<XT, double> && MODE == 0) {
+    if (view.stencil64()) {
+      const DevSellS& m = a.st;
+      g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
+      k_sells64<0><<<red_grid(k_sells64<0>, (long)m.n_chunks * 32), kBlock, sizeof(int) * m.P * 8 * m.G, s>>>(
+          a.n_rows, m, x, y, r, slot, dr);
+      return;
+    }
+  }
   g_algo_bytes += bytes;
   if (view.stencil()) {
     const DevSellS& m = a.st;

@@ -81,11 +81,12 @@ struct HostSellP {
 struct HostSellS {
   int n_rows = 0, n_chunks = 0, G = 0, P = 0;
   std::vector<uint16_t> vals;   // [n_chunks][G][32][8]
+  std::vector<double> vals64;   // [n_chunks][8 G][32] fp64 values (the PCG operator), slot-major per chunk
   std::vector<uint8_t> pid;     // [n_chunks * 32]
   std::vector<int> pat;         // [P][8 G]
 };
 // false when the rows need more than 255 patterns or more than 32 slots
-bool build_sell_stencil(const HostCsr& a, HostSellS& out);
+bool build_sell_stencil(const HostCsr& a, HostSellS& out, bool with_fp64 = false);
 
 uint16_t to_bf16(double d);  // round to nearest even
 // lanes per row of the packed format: about 32 entries per lane (fewer

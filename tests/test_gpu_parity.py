@@ -270,15 +270,18 @@ def test_dense_coarse_truncation():
 
 
 def test_stencil_vcycle_matches_packed():
-    """The stencil-coded fine-level V-cycle operator (SELL-S, option 19) sums
-    the same bf16 products in the same order as the packed SELL-P pass, so
-    the M-solve takes the same iterations and lands on the same solution (the
-    reduction grids differ, so dot products may differ in the last bits)."""
+    """The stencil-coded fine-level operators (SELL-S, option 19): the bf16
+    V-cycle copy sums the same products in the same order as the packed
+    SELL-P pass; the fp64 PCG copy sums the CSR products in row order. The
+    M-solve lands on the same solution to rounding (reduction grids and the
+    PCG operator's summation order differ, so the last bits may)."""
     g = eb.FemSystem(cube(16, jitter=0.1, planes=(0.45, 0.55)))
     b = po.random_vec(g.n_free, 77)
     x1, r1 = g.mass_solve(b)
     g.set_option(19, 0)
     x0, r0 = g.mass_solve(b)
     g.set_option(19, 1)
-    assert r1.iterations == r0.iterations
-    assert np.linalg.norm(x1 - x0) <= 1e-13 * np.linalg.norm(x0)
+    assert abs(r1.iterations - r0.iterations) <= 1
+    assert np.linalg.norm(x1 - x0) <= 1e-11 * np.linalg.norm(x0)
+    xo = po.Problem(cube(16, jitter=0.1, planes=(0.45, 0.55))).mass_solve(b)[0]
+    assert np.linalg.norm(x1 - xo) <= 1e-10 * np.linalg.norm(xo)
