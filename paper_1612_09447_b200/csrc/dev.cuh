@@ -66,7 +66,8 @@ struct DevSellP {
 // Stencil-coded SELL (sell.hpp HostSellS): per row a pattern id, per entry the
 // bf16 value; column = row + pat[pid][slot]
 struct DevSellS {
-  int n_chunks = 0, G = 0, P = 0;
+  int n_chunks = 0, G = 0, P = 0, common = 0;
+  int n_cols = 0;                        // length of the gathered vectors (speculative gathers are clamped to it)
   const uint4* vals = nullptr;           // [n_chunks][G][32] x 8 bf16
   const unsigned char* pid = nullptr;    // [n_chunks * 32]
   const int* pat = nullptr;              // [P][8 G]

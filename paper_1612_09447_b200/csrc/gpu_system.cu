@@ -184,6 +184,8 @@ void upload_stencil(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.st.n_chunks = hs.n_chunks;
   d.st.G = hs.G;
   d.st.P = hs.P;
+  d.st.common = hs.common;
+  d.st.n_cols = h.n_cols;
   d.st.vals = reinterpret_cast<const uint4*>(b.st_vals.p);
   d.st.pid = b.st_pid.p;
   d.st.pat = b.st_pat.p;

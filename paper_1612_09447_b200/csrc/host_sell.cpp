@@ -231,6 +231,11 @@ bool build_sell_stencil(const HostCsr& a, HostSellS& out, bool with_fp64) {
     s.pid[r] = (uint8_t)id;
   }
   s.P = (int)keys.size();
+  {
+    std::vector<long> freq(s.P, 0);
+    for (int r = 0; r < n; ++r) ++freq[s.pid[r]];
+    s.common = (int)(std::max_element(freq.begin(), freq.end()) - freq.begin());
+  }
   s.pat.assign((size_t)s.P * L, 0);
   for (int p = 0; p < s.P; ++p) {
     const int r = rep[p];

@@ -174,9 +174,46 @@ __device__ __forceinline__ XT sellp_dot(const DevSellP& m, int chunk, int lane, 
 // Stencil-coded rows (TPR 1, one row per lane): the pattern table is staged in
 // shared memory (spat); slot j of the row holds the value of its j-th CSR
 // entry, so the products are summed in the same order as the TPR-1 SELL-P pass.
+// G = 2 (up to 16 slots, the Kuhn-box fine level): the columns of the most
+// frequent pattern are gathered speculatively together with the pattern id
+// and the values, so no load waits on another; rows with another pattern
+// gather again. Same products, same order.
+template <class XT, bool SCALED, bool CG = false>
+__device__ __forceinline__ XT sells_dot_g2(const DevSellS& m, const int* __restrict__ spat, int chunk, int lane,
+                                           int row, const XT* __restrict__ x, const XT* __restrict__ w) {
+  const int p = (int)__ldcs(m.pid + 32L * chunk + lane);
+  const uint4* v = m.vals + (long)chunk * 2 * 32 + lane;
+  const uint4 q0 = __ldcs(v), q1 = __ldcs(v + 32);
+  const int* offc = spat + m.common * 16;
+  const int cmax = m.n_cols - 1;
+  XT xs[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {  // clamped: rows with another pattern may point outside
+    const int c = min(max(row + offc[j], 0), cmax);
+    xs[j] = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
+  }
+  if (p != m.common) {
+    const int* off = spat + p * 16;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = row + off[j];
+      xs[j] = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
+    }
+  }
+  const unsigned wd[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+  XT s = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    s += (XT)__uint_as_float(wd[e] << 16) * xs[2 * e];
+    s += (XT)__uint_as_float(wd[e] & 0xffff0000u) * xs[2 * e + 1];
+  }
+  return s;
+}
+
 template <class XT, bool SCALED, bool CG = false>
 __device__ __forceinline__ XT sells_dot(const DevSellS& m, const int* __restrict__ spat, int chunk, int lane,
                                         int row, const XT* __restrict__ x, const XT* __restrict__ w) {
+  if (m.G == 2) return sells_dot_g2<XT, SCALED, CG>(m, spat, chunk, lane, row, x, w);
   const int G = m.G;
   const int* off = spat + (int)__ldcs(m.pid + 32L * chunk + lane) * (8 * G);
   const uint4* v = m.vals + (long)chunk * G * 32 + lane;
@@ -208,6 +245,26 @@ __device__ __forceinline__ XT sells_dot(const DevSellS& m, const int* __restrict
 __device__ __forceinline__ double sells_dot64(const DevSellS& m, const int* __restrict__ spat, int chunk, int lane,
                                               int row, const double* __restrict__ x) {
   const int L = 8 * m.G;
+  if (L == 16) {  // speculative gathers of the most frequent pattern (see sells_dot_g2)
+    const int p = (int)__ldcs(m.pid + 32L * chunk + lane);
+    const double* v = m.vals64 + (long)chunk * 16 * 32 + lane;
+    double a[16], xs[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = __ldcs(v + 32 * j);
+    const int* offc = spat + m.common * 16;
+    const int cmax = m.n_cols - 1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) xs[j] = __ldg(x + min(max(row + offc[j], 0), cmax));
+    if (p != m.common) {
+      const int* off = spat + p * 16;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) xs[j] = __ldg(x + row + off[j]);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s += a[j] * xs[j];
+    return s;
+  }
   const int* off = spat + (int)__ldcs(m.pid + 32L * chunk + lane) * L;
   const double* v = m.vals64 + (long)chunk * L * 32 + lane;
   double s = 0.0;

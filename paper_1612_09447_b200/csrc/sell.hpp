@@ -80,6 +80,7 @@ struct HostSellP {
 // order. 2 B per entry + 1 B per row instead of 4 B per entry.
 struct HostSellS {
   int n_rows = 0, n_chunks = 0, G = 0, P = 0;
+  int common = 0;               // most frequent pattern (the kernels gather its columns speculatively)
   std::vector<uint16_t> vals;   // [n_chunks][G][32][8]
   std::vector<double> vals64;   // [n_chunks][8 G][32] fp64 values (the PCG operator), slot-major per chunk
   std::vector<uint8_t> pid;     // [n_chunks * 32]
