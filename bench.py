@@ -487,6 +487,12 @@ def run_b200(args):
         "gpu_launches": launches,
         "roofline": dom,
         "roofline_other_classes": others,
+        # whole step: all classes' algorithmic bytes of the
+        # instrumented pass / the un-instrumented step time (both K steps)
+        "roofline_full_step": {"bound": "hbm", "achieved": sum(timing["bytes"][:6]) / (ms / 1e3) / 1e9,
+                               "peak": hbm, "unit": "GB/s",
+                               "frac": sum(timing["bytes"][:6]) / (ms / 1e3) / 1e9 / hbm,
+                               "frac_vs_8tbs_spec": sum(timing["bytes"][:6]) / (ms / 1e3) / 8e12},
         "time_by_class_ms": {names[c]: timing["ms"][c] for c in range(6)},
         "time_by_class_source": "CUDA events per kernel class in a second pass of K steps after the timed region",
         "bytes_by_class": {names[c]: timing["bytes"][c] for c in range(6)},

@@ -1442,18 +1442,13 @@ void GpuSystem::spe_downdate() {
   RotPack T{};
   for (int a = 0; a < k; ++a)
     for (int b = 0; b + 1 < k; ++b) T.t[a][b] = J[b][a];
-  std::vector<const double*> qi(k), wi(k);
-  std::vector<double*> qo(k - 1), wo(k - 1);
-  for (int i = 0; i < k; ++i) {
-    qi[i] = spe_q(spe_set_, i);
-    wi[i] = spe_w(spe_set_, i);
-  }
-  for (int j = 0; j + 1 < k; ++j) {
-    qo[j] = spe_q(1 - spe_set_, j);
-    wo[j] = spe_w(1 - spe_set_, j);
-  }
+  // W = M Q is only read for the newest column (spe_g_column right after its
+  // SpMV), and G is rotated below on the host, so W is not rotated
+  std::vector<const double*> qi(k);
+  std::vector<double*> qo(k - 1);
+  for (int i = 0; i < k; ++i) qi[i] = spe_q(spe_set_, i);
+  for (int j = 0; j + 1 < k; ++j) qo[j] = spe_q(1 - spe_set_, j);
   launch_lincomb_multi(n_own_, k, k - 1, qi.data(), qo.data(), T, stream_);
-  launch_lincomb_multi(n_own_, k, k - 1, wi.data(), wo.data(), T, stream_);
   // G' = T' G T, R' = rows 0..k-2 of the rotated Rh
   std::vector<double> G2((size_t)kMaxMulti * kMaxMulti, 0.0);
   for (int a = 0; a + 1 < k; ++a)
