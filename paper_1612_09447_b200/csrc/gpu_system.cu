@@ -137,16 +137,21 @@ void upload_sell16(const HostCsr& h, const HostSell& hs, DevCsr& d, SellBufs& b,
 }
 
 // SELL copies of h (sell.hpp): SELL-16 with fp64/fp32/bf16 values and the
-// packed bf16 SELL-P; each stays absent when some chunk cannot be encoded
-void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
+// packed bf16 SELL-P; each stays absent when some chunk cannot be encoded.
+// sell16_always = false (V-cycle operators): SELL-16 only when the packed
+// encoding fails; the non-default fp64/fp32 V-cycles then read CSR.
+void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s, bool sell16_always = true) {
   d.sell = DevSell{};
   d.pk = DevSellP{};
   if (h.n_rows == 0) return;
-  HostSell hs;
-  if (build_sell(h, choose_sell_tpr(h), hs)) upload_sell16(h, hs, d, b, s);
   // packed bf16 copy for the V-cycle kernels (sell.hpp "SELL-P")
   HostSellP hp;
-  if (!build_sell_packed(h, choose_sellp_tpr(h), hp)) return;
+  const bool packed = build_sell_packed(h, choose_sellp_tpr(h), hp);
+  if (sell16_always || !packed) {
+    HostSell hs;
+    if (build_sell(h, choose_sell_tpr(h), hs)) upload_sell16(h, hs, d, b, s);
+  }
+  if (!packed) return;
   std::vector<int> pcp = hp.chunk_ptr;
   b.pk_cp.alloc(pcp.size());
   b.pk_cp.upload(pcp.data(), pcp.size(), s);
@@ -572,7 +577,7 @@ void GpuSystem::build_levels() {
       lv.A = mii_;  // shares indices / fp64 values with the PCG operator
     } else {
       upload_csr(plan_.A[l], lv.A, lv.a_rp, lv.a_ci, lv.a_v, s);
-      if (l + 1 < L) upload_sell(plan_.A[l], lv.A, lv.a_s, s);
+      if (l + 1 < L) upload_sell(plan_.A[l], lv.A, lv.a_s, s, false);
     }
     build_halo(sp, lv.halo);
     const size_t nloc = std::max(1, lv.n_loc);
@@ -594,8 +599,8 @@ void GpuSystem::build_levels() {
       upload_csr(plan_.R[l], lv.R, lv.r_rp, lv.r_ci, lv.r_v, s);
       f32(plan_.P[l].values, lv.p_vf);
       f32(plan_.R[l].values, lv.r_vf);
-      upload_sell(plan_.P[l], lv.P, lv.p_s, s);
-      upload_sell(plan_.R[l], lv.R, lv.r_s, s);
+      upload_sell(plan_.P[l], lv.P, lv.p_s, s, false);
+      upload_sell(plan_.R[l], lv.R, lv.r_s, s, false);
       std::vector<double> invd = inv_diagonal(plan_.A[l]);
       invd.resize(nloc, 0.0);
       lv.invd.alloc(nloc);

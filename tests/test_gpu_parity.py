@@ -285,3 +285,18 @@ def test_stencil_vcycle_matches_packed():
     assert np.linalg.norm(x1 - x0) <= 1e-11 * np.linalg.norm(x0)
     xo = po.Problem(cube(16, jitter=0.1, planes=(0.45, 0.55))).mass_solve(b)[0]
     assert np.linalg.norm(x1 - xo) <= 1e-10 * np.linalg.norm(xo)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_vcycle_precision_options_converge(prec):
+    """Non-default V-cycle value precisions (option 4: fp64 / fp32) read the
+    CSR copies of the transfer and coarse operators; the M-solve converges
+    to the same solution."""
+    g = eb.FemSystem(cube(12, jitter=0.1))
+    b = po.random_vec(g.n_free, 78)
+    x2, r2 = g.mass_solve(b)
+    g.set_option(4, prec)
+    xp, rp = g.mass_solve(b)
+    g.set_option(4, 2)
+    assert rp.converged and abs(rp.iterations - r2.iterations) <= 3
+    assert np.linalg.norm(xp - x2) <= 1e-10 * np.linalg.norm(x2)
