@@ -323,7 +323,9 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * resets its history), 15/16/17/18 = POD snapshots / rank / capacity / threshold
  * (estimator config keys "snapshots", "rank", "capacity", "threshold"; take effect
  * at the next reset), 19 = stencil-coded fine-level V-cycle operator (0/1; default 1
- * where the rows share at most 255 column-offset patterns),
+ * where the rows share at most 255 column-offset patterns), 20 = graph-resident
+ * PCG iteration loop (0/1; default 1: iterations 2.. run inside one CUDA graph
+ * with a device-side stopping rule, no host round trip per iteration),
  * 13 = smoother polynomial (0 first-kind Chebyshev, 1 fourth-kind, 2 fourth-kind
  * with optimised weights), 14 = lambda_max safety factor (default 1.1).
  * The PCG operator and vectors are fp64 in every setting. */

@@ -195,6 +195,13 @@ void launch_pcg_update(int n, double* x, double* r, const double* p, const doubl
                        float* r32 = nullptr, const float* invd32 = nullptr, float* d32 = nullptr);
 // p = z + beta p, beta = scal[S_RZ]/scal[S_RZ_OLD]
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s);
+// Device-side PCG stopping rule (pcg.cpp:40-66) for the graph-resident
+// iteration loop. stat = [k, status, rel, pq, bnorm, tol, max_iter]: advances
+// k, sets status 0 continue / 1 converged / 2 rz non-finite / 3 p'Ap <= 0 or
+// non-finite / 4 rel non-finite / 5 max_iter reached, copies r.z to S_RZ_OLD
+// when continuing and sets the loop's conditional handle to (status == 0).
+enum PcgStatus : int { PCG_CONTINUE = 0, PCG_CONVERGED, PCG_BAD_RZ, PCG_BAD_PQ, PCG_BAD_REL, PCG_MAX_ITER };
+void launch_pcg_check(double* scal, double* stat, cudaGraphConditionalHandle h, cudaStream_t s);
 // z = Ainv b (dense, n <= 1024, fp64 inverse)
 template <class XT>
 void launch_dense_solve(int n, const double* ainv, const float* ainv32, const XT* b, XT* z, cudaStream_t s);

@@ -234,6 +234,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     CK(cudaSetDevice(device_));
     CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     CK(cudaMallocHost(&pinned_, sizeof(double) * (S_COUNT + 8)));
+    CK(cudaMallocHost(&pcg_pinned_, sizeof(double) * 8));
   }
   const Dofs& dm = prob_.dm;
   n_dofs_ = dm.n_dofs;
@@ -324,6 +325,7 @@ GpuSystem::~GpuSystem() {
   }
   for (auto e : ev_pool_) cudaEventDestroy(e);
   if (pinned_) cudaFreeHost(pinned_);
+  if (pcg_pinned_) cudaFreeHost(pcg_pinned_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -533,6 +535,7 @@ void GpuSystem::build_device() {
   // reductions + work vectors
   red_partials_.alloc((size_t)S_COUNT * kRedGrid);
   red_scal_.alloc(S_COUNT);
+  pcg_stat_.alloc(8);
   red_counters_.alloc(S_COUNT);
   CK(cudaMemsetAsync(red_counters_.p, 0, sizeof(unsigned) * S_COUNT, s));
   CK(cudaMemsetAsync(red_scal_.p, 0, sizeof(double) * S_COUNT, s));
@@ -717,6 +720,8 @@ void GpuSystem::set_cheb(double ratio) {
 void GpuSystem::invalidate_graphs() {
   if (vcycle_graph_) cudaGraphExecDestroy(vcycle_graph_);
   vcycle_graph_ = nullptr;
+  for (auto& kv : pcg_graphs_) cudaGraphExecDestroy(kv.second);
+  pcg_graphs_.clear();
 }
 
 void GpuSystem::set_level_tpr(int level, int tpr) {
@@ -1186,6 +1191,59 @@ double* GpuSystem::precondition(double* r, bool prepared) {
   return z;
 }
 
+// One PCG iteration k >= 2 as the body of a WHILE conditional node: V-cycle
+// on r (z, r.z), p = z + beta p, q = A p with p.q, the x/r update with r.r
+// (and the next V-cycle's fp32 inputs), then k_pcg_check evaluates the
+// stopping rule and sets the loop condition. Kernels and arguments are those
+// of the host loop, so every iteration computes the same values.
+cudaGraphExec_t GpuSystem::pcg_loop_graph(double* x, bool f32) {
+  auto it = pcg_graphs_.find(x);
+  if (it != pcg_graphs_.end()) return it->second;
+  if (pcg_graphs_.size() >= 8) {  // bounded cache (callers with many distinct x buffers)
+    for (auto& kv : pcg_graphs_) cudaGraphExecDestroy(kv.second);
+    pcg_graphs_.clear();
+  }
+  const int n = n_own_;
+  double* r = w_r_.p;
+  double* p = w_p_.p;
+  double* q = w_q_.p;
+  cudaGraph_t graph;
+  CK(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle handle;
+  CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  const long before = g_launch_count;
+  const double bytes_before = g_algo_bytes;
+  CK(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  if (!f32) vcycle_prepare(r);
+  double* z = vcycle(r);
+  launch_pcg_direction(n, p, z, red_scal_.p, stream_);
+  launch_spmv_dot(mii_, p, q, red_, S_PQ, stream_);
+  DevLevel& f0 = levels_.empty() ? dummy_level_ : levels_[0];
+  if (f32)
+    launch_pcg_update(n, x, r, p, q, red_, stream_, f0.b32.p, f0.invd32.p, f0.db32.p);
+  else
+    launch_pcg_update(n, x, r, p, q, red_, stream_);
+  launch_pcg_check(red_scal_.p, pcg_stat_.p, handle, stream_);
+  CK(cudaStreamEndCapture(stream_, &body));
+  pcg_body_kernels_ = g_launch_count - before;
+  pcg_body_bytes_ = g_algo_bytes - bytes_before;
+  g_launch_count = before;
+  g_algo_bytes = bytes_before;
+  cudaGraphExec_t exec;
+  CK(cudaGraphInstantiate(&exec, graph, 0));
+  CK(cudaGraphDestroy(graph));
+  pcg_graphs_[x] = exec;
+  return exec;
+}
+
 // pcg_solve (proj/src/pcg.cpp:9-72) with device vectors; host reads three
 // scalars per iteration for the stopping rule and the breakdown checks.
 // b, x: owned entries; x0 may be null.
@@ -1241,6 +1299,11 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
   read_scalars(S_RZ, 1, sc);
   if (!std::isfinite(sc[0])) throw NumericalError("pcg: non-finite preconditioned residual");
   CK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));  // p = z
+  // The loop runs in one CUDA graph (pcg_loop_graph) when the V-cycle is
+  // capturable and no per-class timing is requested; the decisions are the
+  // same tests on the same scalars, evaluated on the device.
+  const bool graph_loop = pcg_graph_loop && use_graphs && !timing_on && prob_.solver.precond == 2 &&
+                          comm_->size() == 1 && comm_->capturable() && device_ >= 0;
   for (int k = 1; k <= max_iter; ++k) {
     tic(TC_PCG);
     halo(halo0_, p);
@@ -1269,6 +1332,43 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
     }
     CK(cudaMemcpyAsync(red_scal_.p + S_RZ_OLD, red_scal_.p + S_RZ, sizeof(double), cudaMemcpyDeviceToDevice,
                        stream_));
+    if (k < max_iter && graph_loop) {
+      // iterations k+1 .. run inside one graph launch; the host reads the
+      // device stopping rule's verdict once at the end
+      cudaGraphExec_t loop = pcg_loop_graph(x, f32);
+      pcg_pinned_[0] = k;
+      pcg_pinned_[1] = 0.0;
+      pcg_pinned_[2] = rel;
+      pcg_pinned_[3] = 0.0;
+      pcg_pinned_[4] = bnorm;
+      pcg_pinned_[5] = tol;
+      pcg_pinned_[6] = max_iter;
+      CK(cudaMemcpyAsync(pcg_stat_.p, pcg_pinned_, sizeof(double) * 7, cudaMemcpyHostToDevice, stream_));
+      CK(cudaGraphLaunch(loop, stream_));
+      CK(cudaMemcpyAsync(pcg_pinned_, pcg_stat_.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, stream_));
+      sync();
+      const int k_end = (int)pcg_pinned_[0];
+      const int status = (int)pcg_pinned_[1];
+      const long body_runs = k_end - k;
+      g_launch_count += body_runs * pcg_body_kernels_;
+      g_algo_bytes += body_runs * pcg_body_bytes_;
+      res.iterations = k_end;
+      res.rel_residual = pcg_pinned_[2];
+      switch (status) {
+        case PCG_CONVERGED: res.converged = true; return res;
+        case PCG_BAD_RZ: throw NumericalError("pcg: non-finite preconditioned residual");
+        case PCG_BAD_PQ:
+          throw NumericalError("pcg: operator not positive definite (p'Ap = " + std::to_string(pcg_pinned_[3]) +
+                               ")");
+        case PCG_BAD_REL: throw NumericalError("pcg: non-finite residual");
+        default: break;  // PCG_MAX_ITER: the host loop's last precondition + direction
+      }
+      CK(cudaMemcpyAsync(red_scal_.p + S_RZ_OLD, red_scal_.p + S_RZ, sizeof(double), cudaMemcpyDeviceToDevice,
+                         stream_));
+      z = precondition(r, f32);
+      launch_pcg_direction(n, p, z, red_scal_.p, stream_);
+      break;
+    }
     z = precondition(r, f32);
     tic(TC_PCG);
     launch_pcg_direction(n, p, z, red_scal_.p, stream_);

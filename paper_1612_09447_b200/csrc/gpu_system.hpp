@@ -12,6 +12,7 @@
 #include <deque>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "comm.hpp"
@@ -211,6 +212,7 @@ class GpuSystem {
   int cheb_kind = 0;          // 0 first-kind Chebyshev on [lmax/ratio, lmax], 1 fourth-kind
   double cheb_scale = 1.1;    // lmax = cheb_scale x the power estimate of lambda_max(D^-1 A)
   bool use_graphs = true;
+  bool pcg_graph_loop = true;  // eqs_set_option 20
   bool spe_incremental = true;  // false: the reference's full MGS rebuild on every solve
   void set_cheb(double ratio);
   void set_vcycle_precision(int prec);  // V-cycle matrix values: 0 fp64, 1 fp32, 2 bf16
@@ -321,6 +323,15 @@ class GpuSystem {
   double* vcycle_out_ = nullptr;
   long vcycle_graph_kernels_ = 0;
   double vcycle_graph_bytes_ = 0.0;
+  // graph-resident PCG loops (pcg_dev), one per solution pointer x: a WHILE
+  // conditional node whose body is one iteration (V-cycle, direction, SpMV+dot,
+  // update, device stopping rule)
+  std::unordered_map<double*, cudaGraphExec_t> pcg_graphs_;
+  long pcg_body_kernels_ = 0;
+  double pcg_body_bytes_ = 0.0;
+  DevBuf<double> pcg_stat_;
+  double* pcg_pinned_ = nullptr;  // host pinned [8]: stat in / out
+  cudaGraphExec_t pcg_loop_graph(double* x, bool f32);
 
   Problem prob_;
   int device_ = 0;

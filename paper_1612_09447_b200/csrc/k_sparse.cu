@@ -139,6 +139,31 @@ __global__ void k_pcg_direction(int n, double* __restrict__ p, const double* __r
     p[i] = z[i] + beta * p[i];
 }
 
+// Same tests, same order and same arithmetic as the host loop in
+// GpuSystem::pcg_dev (sqrt and division are correctly rounded on both sides).
+__global__ void k_pcg_check(double* __restrict__ scal, double* __restrict__ stat, cudaGraphConditionalHandle h) {
+  const double pq = scal[S_PQ], rr = scal[S_RR], rz = scal[S_RZ];
+  const double k = stat[0] + 1.0;
+  const double rel = sqrt(rr) / stat[4];
+  int status = PCG_CONTINUE;
+  if (!isfinite(rz))
+    status = PCG_BAD_RZ;
+  else if (!(pq > 0.0) || !isfinite(pq))
+    status = PCG_BAD_PQ;
+  else if (!isfinite(rel))
+    status = PCG_BAD_REL;
+  else if (rel <= stat[5])
+    status = PCG_CONVERGED;
+  else if (k >= stat[6])
+    status = PCG_MAX_ITER;
+  stat[0] = k;
+  stat[1] = status;
+  stat[2] = rel;
+  stat[3] = pq;
+  if (status == PCG_CONTINUE) scal[S_RZ_OLD] = rz;
+  cudaGraphSetConditional(h, status == PCG_CONTINUE ? 1u : 0u);
+}
+
 __global__ void k_dot(int n, const double* __restrict__ a, const double* __restrict__ b, Reducer red, int slot) {
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) acc += a[i] * b[i];
@@ -348,6 +373,10 @@ void launch_to_f64_dot(int n, const float* z32, double* z64, const double* b, Re
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s) {
   ++g_launch_count;
   k_pcg_direction<<<grid_for(n), kBlock, 0, s>>>(n, p, z, scal);
+}
+void launch_pcg_check(double* scal, double* stat, cudaGraphConditionalHandle h, cudaStream_t s) {
+  ++g_launch_count;
+  k_pcg_check<<<1, 1, 0, s>>>(scal, stat, h);
 }
 template <class XT>
 void launch_dense_solve(int n, const double* ainv, const float* ainv32, const XT* b, XT* z, cudaStream_t s) {

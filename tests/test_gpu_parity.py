@@ -300,3 +300,44 @@ def test_vcycle_precision_options_converge(prec):
     g.set_option(4, 2)
     assert rp.converged and abs(rp.iterations - r2.iterations) <= 3
     assert np.linalg.norm(xp - x2) <= 1e-10 * np.linalg.norm(x2)
+
+
+@pytest.mark.parametrize("f32_vectors", [1, 0])
+def test_graph_pcg_loop_bit_identical(f32_vectors):
+    """Option 20: PCG iterations 2.. run inside one CUDA graph (WHILE
+    conditional node) with the stopping rule evaluated on the device
+    (k_pcg_check). Same kernels, same scalars, same tests as the host loop:
+    solutions, iteration counts and residuals are bit-identical, including a
+    solve stopped by max_iter (pcg.cpp:66-71: reported, not thrown)."""
+    g = eb.FemSystem(cube(16, jitter=0.1, planes=(0.45, 0.55)))
+    g.set_option(11, f32_vectors)
+    b = po.random_vec(g.n_free, 91)
+    x0 = 1e-3 * po.random_vec(g.n_free, 92)
+    out = {}
+    for loop in (1, 0):
+        g.set_option(20, loop)
+        out[loop] = [g.mass_solve(b), g.mass_solve(b, x0=x0), g.mass_solve(b, max_iter=3),
+                     g.mass_solve(b, tol=1e-6)]
+    for (xa, ra), (xb, rb) in zip(out[1], out[0]):
+        assert np.array_equal(xa, xb)
+        assert ra.iterations == rb.iterations and ra.converged == rb.converged
+        assert ra.rel_residual == rb.rel_residual
+    assert out[1][0][1].iterations > 3 and not out[1][2][1].converged and out[1][2][1].iterations == 3
+
+
+def test_graph_pcg_loop_rkc_steps_bit_identical():
+    """Fixed RKC steps (fused residual, SPE starts, AMG-PCG M-solves) with the
+    graph-resident PCG loop on and off: identical potentials and counters."""
+    cfg = cube(12, jitter=0.1, planes=(0.45, 0.55))
+    res = {}
+    for loop in (1, 0):
+        g = eb.FemSystem(cfg)
+        g.set_option(20, loop)
+        x0 = 2e4 * po.random_vec(g.n_free, 93)
+        g.set_state(0.0, x0, 1e-4)
+        g.rkc_advance_fixed(1e-4, 4, 3)
+        x, _ = g.get_state()
+        s = g.stats()
+        res[loop] = (x, s["pcg_iterations"], s["m_solves"])
+    assert np.array_equal(res[1][0], res[0][0])
+    assert res[1][1:] == res[0][1:]
