@@ -326,6 +326,8 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * where the rows share at most 255 column-offset patterns), 20 = graph-resident
  * PCG iteration loop (0/1; default 1: iterations 2.. run inside one CUDA graph
  * with a device-side stopping rule, no host round trip per iteration),
+ * 21 = programmatic dependent launch of the row/vector kernels (0/1; default 1;
+ * process-wide),
  * 13 = smoother polynomial (0 first-kind Chebyshev, 1 fourth-kind, 2 fourth-kind
  * with optimised weights), 14 = lambda_max safety factor (default 1.1).
  * The PCG operator and vectors are fp64 in every setting. */

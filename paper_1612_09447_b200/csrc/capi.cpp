@@ -641,6 +641,7 @@ int eqs_set_option(eqs_ctx* ctx, int key, double value) {
       case 18: g.set_pod_params(0, 0, 0, std::max(0.0, value)); break;
       case 19: g.set_stencil(value != 0.0); break;
       case 20: g.pcg_graph_loop = value != 0.0; g.invalidate_graphs(); break;
+      case 21: g_pdl = value != 0.0; g.invalidate_graphs(); break;
       default: throw std::invalid_argument("eqs_set_option: unknown key");
     }
   });

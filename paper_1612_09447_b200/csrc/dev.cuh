@@ -14,6 +14,8 @@ constexpr int kBlock = 256;
 extern long g_launch_count;
 // algorithmic HBM bytes of the sparse row kernels launched so far (roofline accounting)
 extern double g_algo_bytes;
+// programmatic dependent launch on for the row/vector kernels (eqs_set_option 21)
+extern bool g_pdl;
 // Reduction kernels run grid-stride on a fixed grid so that the partial-sum
 // count (and therefore the summation order) is fixed: deterministic results.
 constexpr int kRedGrid = 148 * 8;

@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(kBlock) k_row(int n, const int* __restrict__ r
                                                 const VT* __restrict__ v, const XT* __restrict__ x,
                                                 const XT* __restrict__ b, const XT* __restrict__ invd,
                                                 XT* __restrict__ y, XT* __restrict__ y2, ChebCoef c) {
+  pdl_entry();
   const long tid = (long)blockIdx.x * kBlock + threadIdx.x;
   const int row = (int)(tid / TPR), lane = (int)(tid % TPR);
   if ((tid & ~31L) / TPR >= n) return;  // warp-uniform exit
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(kBlock, SELL_MINB) k_sell(int n, DevSell m, co
                                                  const XT* __restrict__ x, const XT* __restrict__ b,
                                                  const XT* __restrict__ invd, XT* __restrict__ y,
                                                  XT* __restrict__ y2, ChebCoef c) {
+  pdl_entry();
   const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (chunk >= m.n_chunks) return;  // warp-uniform exit
   constexpr bool SC = kScaled<OP, -1>;
@@ -410,6 +412,7 @@ __global__ void __launch_bounds__(kBlock) k_sellp(int n, DevSellP m, const XT* _
                                                   const XT* __restrict__ b, const XT* __restrict__ invd,
                                                   XT* __restrict__ y, XT* __restrict__ y2, ChebCoef c,
                                                   const XT* __restrict__ pre) {
+  pdl_entry();
   const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (chunk >= m.n_chunks) return;  // warp-uniform exit
   constexpr bool SC = kScaled<OP, -1>;
@@ -428,6 +431,7 @@ __global__ void __launch_bounds__(kBlock) k_sells(int n, DevSellS m, const XT* _
                                                   const XT* __restrict__ pre) {
   extern __shared__ int spat[];
   stage_patterns(m, spat);
+  pdl_entry();
   const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (chunk >= m.n_chunks) return;  // warp-uniform exit
   constexpr bool SC = kScaled<OP, -1>;
@@ -447,6 +451,7 @@ __global__ void __launch_bounds__(kBlock) k_sells_red(int n, DevSellS m, const X
                                                       int slot, int do_red, const XT* __restrict__ pre) {
   extern __shared__ int spat[];
   stage_patterns(m, spat);
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kBlock / 32);
   double acc = 0.0;
@@ -467,6 +472,7 @@ __global__ void __launch_bounds__(kBlock) k_sells64(int n, DevSellS m, const dou
                                                     double* __restrict__ y, Reducer red, int slot, int do_red) {
   extern __shared__ int spat[];
   stage_patterns(m, spat);
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kBlock / 32);
   double acc = 0.0;
@@ -488,6 +494,7 @@ __global__ void __launch_bounds__(kBlock) k_sellp_red(int n, DevSellP m, const X
                                                       XT* __restrict__ y, double* __restrict__ out64,
                                                       const double* __restrict__ b64, ChebCoef c, Reducer red,
                                                       int slot, int do_red, const XT* __restrict__ pre) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kBlock / 32);
   double acc = 0.0;
@@ -510,6 +517,7 @@ __global__ void __launch_bounds__(kBlock) k_row_red(int n, const int* __restrict
                                                     XT* __restrict__ y, double* __restrict__ out64,
                                                     const double* __restrict__ b64, ChebCoef c, Reducer red,
                                                     int slot, int do_red) {
+  pdl_entry();
   const int lane = threadIdx.x % TPR;
   const long groups_per_grid = (long)gridDim.x * (kBlock / TPR);
   // every group iterates the same number of times (shuffles need full warps)
@@ -531,6 +539,7 @@ __global__ void __launch_bounds__(kBlock) k_sell_red(int n, DevSell m, const VT*
                                                      const XT* __restrict__ invd, XT* __restrict__ y,
                                                      double* __restrict__ out64, const double* __restrict__ b64,
                                                      ChebCoef c, Reducer red, int slot, int do_red) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kBlock / 32);
   double acc = 0.0;
@@ -581,7 +590,7 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
     if (view.stencil64()) {
       const DevSellS& m = a.st;
       g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
-      k_sells64<-1><<<red_grid(k_sells64<-1>, (long)m.n_chunks * 32), kBlock, sizeof(int) * m.P * 8 * m.G, s>>>(
+      launch_pdl(k_sells64<-1>, red_grid(k_sells64<-1>, (long)m.n_chunks * 32), kBlock, sizeof(int) * m.P * 8 * m.G, s, 
           a.n_rows, m, x, y, Reducer{}, 0, 0);
       return;
     }
@@ -592,10 +601,10 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
     const size_t smem = sizeof(int) * m.P * 8 * m.G;
     if (pre && kScaled<OP, -1>) {
       g_algo_bytes += matrix_pass_bytes(view, 1, kS[OP] + 2, sizeof(XT));
-      k_sells<XT, OP, true><<<g, kBlock, smem, s>>>(a.n_rows, m, x, b, invd, y, y2, c, pre);
+      launch_pdl(k_sells<XT, OP, true>, g, kBlock, smem, s, a.n_rows, m, x, b, invd, y, y2, c, pre);
     } else {
       g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
-      k_sells<XT, OP, false><<<g, kBlock, smem, s>>>(a.n_rows, m, x, b, invd, y, y2, c, nullptr);
+      launch_pdl(k_sells<XT, OP, false>, g, kBlock, smem, s, a.n_rows, m, x, b, invd, y, y2, c, nullptr);
     }
     return;
   }
@@ -604,13 +613,13 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
     const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
     if (pre && kScaled<OP, -1>) {  // one prescaled gather; b and D^-1 read per row
       g_algo_bytes += matrix_pass_bytes(view, 1, kS[OP] + 2, sizeof(XT));
-#define P_(T, VT, V) k_sellp<T, XT, OP, true><<<g, kBlock, 0, s>>>(a.n_rows, m, x, b, invd, y, y2, c, pre)
+#define P_(T, VT, V) launch_pdl(k_sellp<T, XT, OP, true>, g, kBlock, 0, s, a.n_rows, m, x, b, invd, y, y2, c, pre)
       TPR_SWITCH_(m.tpr, P_, void, 0)
 #undef P_
       return;
     }
     g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
-#define P_(T, VT, V) k_sellp<T, XT, OP, false><<<g, kBlock, 0, s>>>(a.n_rows, m, x, b, invd, y, y2, c, nullptr)
+#define P_(T, VT, V) launch_pdl(k_sellp<T, XT, OP, false>, g, kBlock, 0, s, a.n_rows, m, x, b, invd, y, y2, c, nullptr)
     TPR_SWITCH_(m.tpr, P_, void, 0)
 #undef P_
     return;
@@ -619,7 +628,7 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
     const DevSell& m = a.sell;
     g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
     const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
-#define S_(T, VT, V) k_sell<T, VT, XT, OP><<<g, kBlock, 0, s>>>(a.n_rows, m, V, x, b, invd, y, y2, c)
+#define S_(T, VT, V) launch_pdl(k_sell<T, VT, XT, OP>, g, kBlock, 0, s, a.n_rows, m, V, x, b, invd, y, y2, c)
     if (p == 2) {
       TPR_SWITCH_(m.tpr, S_, uint16_t, m.v16)
     } else if (p == 1 || std::is_same_v<XT, float>) {
@@ -632,7 +641,7 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
   }
   g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
   const int g = grid_rows(a.n_rows, a.tpr);
-#define L_(T, VT, V) k_row<T, VT, XT, OP><<<g, kBlock, 0, s>>>(a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, y2, c)
+#define L_(T, VT, V) launch_pdl(k_row<T, VT, XT, OP>, g, kBlock, 0, s, a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, y2, c)
   if (p >= 1 || std::is_same_v<XT, float>) {
     TPR_SWITCH_(a.tpr, L_, float, a.values_f)
   } else {
@@ -661,7 +670,7 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
     if (view.stencil64()) {
       const DevSellS& m = a.st;
       g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
-      k_sells64<0><<<red_grid(k_sells64<0>, (long)m.n_chunks * 32), kBlock, sizeof(int) * m.P * 8 * m.G, s>>>(
+      launch_pdl(k_sells64<0>, red_grid(k_sells64<0>, (long)m.n_chunks * 32), kBlock, sizeof(int) * m.P * 8 * m.G, s, 
           a.n_rows, m, x, y, r, slot, dr);
       return;
     }
@@ -672,10 +681,10 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
     const long work = (long)m.n_chunks * 32;
     const size_t smem = sizeof(int) * m.P * 8 * m.G;
     if (use_pre)
-      k_sells_red<XT, MODE, true><<<red_grid(k_sells_red<XT, MODE, true>, work), kBlock, smem, s>>>(
+      launch_pdl(k_sells_red<XT, MODE, true>, red_grid(k_sells_red<XT, MODE, true>, work), kBlock, smem, s, 
           a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, pre);
     else
-      k_sells_red<XT, MODE, false><<<red_grid(k_sells_red<XT, MODE, false>, work), kBlock, smem, s>>>(
+      launch_pdl(k_sells_red<XT, MODE, false>, red_grid(k_sells_red<XT, MODE, false>, work), kBlock, smem, s, 
           a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, nullptr);
     return;
   }
@@ -684,14 +693,14 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
     const long work = (long)m.n_chunks * 32;
     if (use_pre) {
 #define P_(T, VT, V)                                                                                   \
-  k_sellp_red<T, XT, MODE, true><<<red_grid(k_sellp_red<T, XT, MODE, true>, work), kBlock, 0, s>>>(     \
+  launch_pdl(k_sellp_red<T, XT, MODE, true>, red_grid(k_sellp_red<T, XT, MODE, true>, work), kBlock, 0, s,      \
       a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, pre)
       TPR_SWITCH_(m.tpr, P_, void, 0)
 #undef P_
       return;
     }
 #define P_(T, VT, V)                                                                                   \
-  k_sellp_red<T, XT, MODE, false><<<red_grid(k_sellp_red<T, XT, MODE, false>, work), kBlock, 0, s>>>(   \
+  launch_pdl(k_sellp_red<T, XT, MODE, false>, red_grid(k_sellp_red<T, XT, MODE, false>, work), kBlock, 0, s,    \
       a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, nullptr)
     TPR_SWITCH_(m.tpr, P_, void, 0)
 #undef P_
@@ -701,7 +710,7 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
     const DevSell& m = a.sell;
     const long work = (long)m.n_chunks * 32;
 #define S_(T, VT, V)                                                                                              \
-  k_sell_red<T, VT, XT, MODE><<<red_grid(k_sell_red<T, VT, XT, MODE>, work), kBlock, 0, s>>>(                      \
+  launch_pdl(k_sell_red<T, VT, XT, MODE>, red_grid(k_sell_red<T, VT, XT, MODE>, work), kBlock, 0, s,                       \
       a.n_rows, m, V, x, b, invd, y, out64, b64, c, r, slot, dr)
     if (p == 2) {
       TPR_SWITCH_(m.tpr, S_, uint16_t, m.v16)
@@ -715,7 +724,7 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
   }
   const long work = (long)a.n_rows * a.tpr;
 #define L_(T, VT, V)                                                                                             \
-  k_row_red<T, VT, XT, MODE><<<red_grid(k_row_red<T, VT, XT, MODE>, work), kBlock, 0, s>>>(                       \
+  launch_pdl(k_row_red<T, VT, XT, MODE>, red_grid(k_row_red<T, VT, XT, MODE>, work), kBlock, 0, s,                        \
       a.n_rows, a.row_ptr, a.col_idx, V, x, b, invd, y, out64, b64, c, r, slot, dr)
   if (p >= 1 || std::is_same_v<XT, float>) {
     TPR_SWITCH_(a.tpr, L_, float, a.values_f)

@@ -15,12 +15,14 @@ namespace eqsb {
 
 long g_launch_count = 0;
 double g_algo_bytes = 0.0;
+bool g_pdl = true;
 
 namespace {
 
 template <class XT>
 __global__ void k_dense_solve(int n, const double* __restrict__ ainv, const XT* __restrict__ b,
                               XT* __restrict__ z) {
+  pdl_entry();
   extern __shared__ double sb[];
   for (int i = threadIdx.x; i < n; i += blockDim.x) sb[i] = (double)b[i];
   __syncthreads();
@@ -38,6 +40,7 @@ __global__ void k_dense_solve(int n, const double* __restrict__ ainv, const XT* 
 template <class MT, class XT>
 __global__ void __launch_bounds__(kBlock) k_dense_gemv(int n, const MT* __restrict__ a, const XT* __restrict__ b,
                                                       XT* __restrict__ z) {
+  pdl_entry();
   const int row = (int)((blockIdx.x * (long)kBlock + threadIdx.x) >> 5), l = threadIdx.x & 31;
   if (row >= n) return;
   const MT* ar = a + (size_t)row * n;
@@ -50,6 +53,7 @@ __global__ void __launch_bounds__(kBlock) k_dense_gemv(int n, const MT* __restri
 
 __global__ void k_jacobi(int n, const double* __restrict__ invd, const double* __restrict__ r,
                          double* __restrict__ z, Reducer red, int slot, int do_red) {
+  pdl_entry();
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     const double zi = invd[i] * r[i];
@@ -69,6 +73,7 @@ __global__ void __launch_bounds__(kBlock, 6)
     k_pcg_update(int n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                  const double* __restrict__ q, float* __restrict__ r32, const float* __restrict__ invd32,
                  float* __restrict__ d32, Reducer red) {
+  pdl_entry();
   const double alpha = red.scal[S_RZ] / red.scal[S_PQ];
   double acc = 0.0;
   auto one = [&](long i) {
@@ -110,10 +115,12 @@ __global__ void __launch_bounds__(kBlock, 6)
 }
 
 __global__ void k_to_f32(long n, const double* __restrict__ x, float* __restrict__ y) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = (float)x[i];
 }
 __global__ void k_to_f32_scaled(long n, const double* __restrict__ x, const float* __restrict__ invd,
                                 float* __restrict__ y, float* __restrict__ d) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     const float f = (float)x[i];
     y[i] = f;
@@ -123,6 +130,7 @@ __global__ void k_to_f32_scaled(long n, const double* __restrict__ x, const floa
 // z64 = z32 ; slot <- b.z64
 __global__ void k_to_f64_dot(int n, const float* __restrict__ z32, double* __restrict__ z64,
                              const double* __restrict__ b, Reducer red, int slot, int do_red) {
+  pdl_entry();
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     const double zi = (double)z32[i];
@@ -134,6 +142,7 @@ __global__ void k_to_f64_dot(int n, const float* __restrict__ z32, double* __res
 
 __global__ void k_pcg_direction(int n, double* __restrict__ p, const double* __restrict__ z,
                                 const double* __restrict__ scal) {
+  pdl_entry();
   const double beta = scal[S_RZ] / scal[S_RZ_OLD];
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
     p[i] = z[i] + beta * p[i];
@@ -165,6 +174,7 @@ __global__ void k_pcg_check(double* __restrict__ scal, double* __restrict__ stat
 }
 
 __global__ void k_dot(int n, const double* __restrict__ a, const double* __restrict__ b, Reducer red, int slot) {
+  pdl_entry();
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) acc += a[i] * b[i];
   reduce_finish(acc, red, slot);
@@ -175,6 +185,7 @@ struct PtrPack {
 };
 
 __global__ void k_multi_dot(int n, int m, PtrPack V, const double* __restrict__ w, Reducer red, int slot0) {
+  pdl_entry();
   double acc[kMaxMulti];
 #pragma unroll
   for (int k = 0; k < kMaxMulti; ++k) acc[k] = 0.0;
@@ -189,6 +200,7 @@ __global__ void k_multi_dot(int n, int m, PtrPack V, const double* __restrict__ 
 
 template <bool ACC>
 __global__ void k_lincomb(int n, int m, PtrPack V, CoefPack c, double* __restrict__ y) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     double s = ACC ? y[i] : 0.0;
     for (int k = 0; k < m; ++k) s += V.p[k][i] * c.c[k];
@@ -198,6 +210,7 @@ __global__ void k_lincomb(int n, int m, PtrPack V, CoefPack c, double* __restric
 
 // w -= sum_j c_j Q_j ; slot <- w.w   (one Gram-Schmidt projection pass)
 __global__ void k_orth_update(int n, int m, PtrPack Q, CoefPack c, double* __restrict__ w, Reducer red, int slot) {
+  pdl_entry();
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     double s = w[i];
@@ -210,6 +223,7 @@ __global__ void k_orth_update(int n, int m, PtrPack Q, CoefPack c, double* __res
 
 // out_j = sum_i T[i][j] in_i  (basis rotation of the SPE window, T by value)
 __global__ void k_lincomb_multi(int n, int kin, int kout, PtrPack in, PtrPack out, RotPack T) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     double v[kMaxMulti];
     for (int a = 0; a < kin; ++a) v[a] = in.p[a][i];
@@ -227,6 +241,7 @@ __global__ void k_lincomb_multi(int n, int kin, int kout, PtrPack in, PtrPack ou
 __global__ void k_shift_gather(long nnz, const long* __restrict__ ptr, const long* __restrict__ src,
                                const double* __restrict__ S, const double* __restrict__ m, double gdt,
                                double* __restrict__ shifted) {
+  pdl_entry();
   for (long e = (long)blockIdx.x * kBlock + threadIdx.x; e < nnz; e += (long)gridDim.x * kBlock) {
     double k = 0.0;
     for (long c = ptr[e]; c < ptr[e + 1]; ++c) k = __dadd_rn(k, S[src[c]]);
@@ -236,6 +251,7 @@ __global__ void k_shift_gather(long nnz, const long* __restrict__ ptr, const lon
 // diag[i] = a_ii (CSR with sorted columns)
 __global__ void k_csr_diag(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
                            double* __restrict__ d) {
+  pdl_entry();
   for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) {
     double s = 0.0;
     for (int k = rp[i]; k < rp[i + 1]; ++k)
@@ -246,6 +262,7 @@ __global__ void k_csr_diag(int n, const int* __restrict__ rp, const int* __restr
 // z = r / d (JacobiPreconditioner, preconditioners.cpp:22-32) ; slot <- r.z
 __global__ void k_jacobi_div(int n, const double* __restrict__ d, const double* __restrict__ r, double* __restrict__ z,
                              Reducer red, int slot) {
+  pdl_entry();
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     const double zi = r[i] / d[i];
@@ -257,6 +274,7 @@ __global__ void k_jacobi_div(int n, const double* __restrict__ d, const double* 
 // weighted_rms (integrators.cpp:20-31) sum: (est_i / (atol + rtol max(|x_i|, |xn_i|)))^2
 __global__ void k_weighted_sq(int n, const double* __restrict__ est, const double* __restrict__ x,
                               const double* __restrict__ xn, double atol, double rtol, Reducer red, int slot) {
+  pdl_entry();
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     const double w = atol + rtol * fmax(fabs(x[i]), fabs(xn[i]));
@@ -267,23 +285,28 @@ __global__ void k_weighted_sq(int n, const double* __restrict__ est, const doubl
 }
 
 __global__ void k_axpy(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] += a * x[i];
 }
 __global__ void k_axpy_dev(int n, const double* __restrict__ coef, double sign, const double* __restrict__ x,
                            double* __restrict__ y) {
+  pdl_entry();
   const double a = sign * coef[0];
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] += a * x[i];
 }
 template <class XT>
 __global__ void k_diag_scale(int n, const XT* __restrict__ invd, const XT* __restrict__ b, double a,
                              XT* __restrict__ z) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
     z[i] = (XT)(a * invd[i] * b[i]);
 }
 __global__ void k_scale(int n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = a * x[i];
 }
 __global__ void k_fill(long n, double v, double* __restrict__ y) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = v;
 }
 
@@ -291,17 +314,20 @@ __global__ void k_rkc_stage(int n, double a0, double mu, double nu, double mt, d
                             const double* __restrict__ y0, const double* __restrict__ y1,
                             const double* __restrict__ y2, const double* __restrict__ f,
                             const double* __restrict__ f0, double* __restrict__ y) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
     y[i] = a0 * y0[i] + mu * y1[i] + nu * y2[i] + mt * f[i] + gt * f0[i];
 }
 __global__ void k_axpby_into(int n, const double* __restrict__ y0, double c, const double* __restrict__ f,
                              double* __restrict__ y) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = y0[i] + c * f[i];
 }
 
 __global__ void k_rkc_error(int n, const double* __restrict__ x, const double* __restrict__ xn,
                             const double* __restrict__ f0, const double* __restrict__ fn, double dt, double atol,
                             double rtol, Reducer red, int slot) {
+  pdl_entry();
   const double c = 0.4 * dt;
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
@@ -316,17 +342,21 @@ __global__ void k_rkc_error(int n, const double* __restrict__ x, const double* _
 
 template <class T>
 __global__ void k_gather(int n, const int* __restrict__ idx, const T* __restrict__ x, T* __restrict__ y) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = x[idx[i]];
 }
 __global__ void k_scatter(int n, const int* __restrict__ idx, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[idx[i]] = x[i];
 }
 __global__ void k_lift_fixed(int n, const int* __restrict__ set_of, SetVals vals, double* __restrict__ out) {
+  pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
     out[i] = vals.v[set_of[i]];
 }
 __global__ void k_boundary_load(int n, const int* __restrict__ rows, const double* __restrict__ coef, int ns,
                                 SetVals rates, double* __restrict__ r) {
+  pdl_entry();
   for (long k = (long)blockIdx.x * kBlock + threadIdx.x; k < n; k += (long)gridDim.x * kBlock) {
     double s = 0.0;
     for (int j = 0; j < ns; ++j) s += coef[k * ns + j] * rates.v[j];
@@ -344,7 +374,7 @@ void launch_pcg_update(int n, double* x, double* r, const double* p, const doubl
                    (!r32 || (al(r32, 8) && al(invd32, 8) && al(d32, 8)));
   const long work = vec ? std::max(1, n / 2) : n;
 #define U_(F, V) \
-  k_pcg_update<F, V><<<red_grid(k_pcg_update<F, V>, work), kBlock, 0, s>>>(n, x, r, p, q, r32, invd32, d32, red)
+  launch_pdl(k_pcg_update<F, V>, red_grid(k_pcg_update<F, V>, work), kBlock, 0, s, n, x, r, p, q, r32, invd32, d32, red)
   if (r32) {
     if (vec) U_(true, true); else U_(true, false);
   } else {
@@ -356,23 +386,23 @@ void launch_to_f32_scaled(long n, const double* x, const float* invd, float* y, 
   if (n <= 0) return;
   ++g_launch_count;
   g_algo_bytes += 20.0 * n;
-  k_to_f32_scaled<<<grid_for(n), kBlock, 0, s>>>(n, x, invd, y, d);
+  launch_pdl(k_to_f32_scaled, grid_for(n), kBlock, 0, s, n, x, invd, y, d);
 }
 void launch_to_f32(long n, const double* x, float* y, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launch_count;
   g_algo_bytes += 12.0 * n;
-  k_to_f32<<<grid_for(n), kBlock, 0, s>>>(n, x, y);
+  launch_pdl(k_to_f32, grid_for(n), kBlock, 0, s, n, x, y);
 }
 void launch_to_f64_dot(int n, const float* z32, double* z64, const double* b, Reducer* red, int slot, cudaStream_t s) {
   ++g_launch_count;
   g_algo_bytes += (red ? 20.0 : 12.0) * n;
   Reducer rr = red ? *red : Reducer{};
-  k_to_f64_dot<<<red_grid(k_to_f64_dot, n), kBlock, 0, s>>>(n, z32, z64, b, rr, slot, red ? 1 : 0);
+  launch_pdl(k_to_f64_dot, red_grid(k_to_f64_dot, n), kBlock, 0, s, n, z32, z64, b, rr, slot, red ? 1 : 0);
 }
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s) {
   ++g_launch_count;
-  k_pcg_direction<<<grid_for(n), kBlock, 0, s>>>(n, p, z, scal);
+  launch_pdl(k_pcg_direction, grid_for(n), kBlock, 0, s, n, p, z, scal);
 }
 void launch_pcg_check(double* scal, double* stat, cudaGraphConditionalHandle h, cudaStream_t s) {
   ++g_launch_count;
@@ -383,16 +413,16 @@ void launch_dense_solve(int n, const double* ainv, const float* ainv32, const XT
   ++g_launch_count;
   if (n <= 256) {  // the hierarchy's own <= 64-row coarsest (amg.hpp:17): one block
     g_algo_bytes += 8.0 * n * n;
-    k_dense_solve<XT><<<1, 1024, n * sizeof(double), s>>>(n, ainv, b, z);
+    launch_pdl(k_dense_solve<XT>, 1, 1024, n * sizeof(double), s, n, ainv, b, z);
     return;
   }
   const int g = (int)(((long)n * 32 + kBlock - 1) / kBlock);
   if (std::is_same_v<XT, float> && ainv32) {
     g_algo_bytes += 4.0 * n * n + 8.0 * n;
-    k_dense_gemv<float, XT><<<g, kBlock, 0, s>>>(n, ainv32, b, z);
+    launch_pdl(k_dense_gemv<float, XT>, g, kBlock, 0, s, n, ainv32, b, z);
   } else {
     g_algo_bytes += 8.0 * n * n + 2.0 * sizeof(XT) * n;
-    k_dense_gemv<double, XT><<<g, kBlock, 0, s>>>(n, ainv, b, z);
+    launch_pdl(k_dense_gemv<double, XT>, g, kBlock, 0, s, n, ainv, b, z);
   }
 }
 template void launch_dense_solve<double>(int, const double*, const float*, const double*, double*, cudaStream_t);
@@ -400,36 +430,36 @@ template void launch_dense_solve<float>(int, const double*, const float*, const 
 void launch_jacobi(int n, const double* invd, const double* r, double* z, Reducer* red, int slot, cudaStream_t s) {
   ++g_launch_count;
   Reducer rr = red ? *red : Reducer{};
-  k_jacobi<<<red_grid(k_jacobi, n), kBlock, 0, s>>>(n, invd, r, z, rr, slot, red ? 1 : 0);
+  launch_pdl(k_jacobi, red_grid(k_jacobi, n), kBlock, 0, s, n, invd, r, z, rr, slot, red ? 1 : 0);
 }
 void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, cudaStream_t s) {
   ++g_launch_count;
-  k_dot<<<red_grid(k_dot, n), kBlock, 0, s>>>(n, a, b, red, slot);
+  launch_pdl(k_dot, red_grid(k_dot, n), kBlock, 0, s, n, a, b, red, slot);
 }
 void launch_multi_dot(int n, int m, const double* const* V, const double* w, Reducer red, int slot0, cudaStream_t s) {
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
-  k_multi_dot<<<red_grid(k_multi_dot, n), kBlock, 0, s>>>(n, m, pk, w, red, slot0);
+  launch_pdl(k_multi_dot, red_grid(k_multi_dot, n), kBlock, 0, s, n, m, pk, w, red, slot0);
 }
 void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s) {
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
-  k_lincomb<false><<<grid_for(n), kBlock, 0, s>>>(n, m, pk, c, y);
+  launch_pdl(k_lincomb<false>, grid_for(n), kBlock, 0, s, n, m, pk, c, y);
 }
 void launch_lincomb_acc(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s) {
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
-  k_lincomb<true><<<grid_for(n), kBlock, 0, s>>>(n, m, pk, c, y);
+  launch_pdl(k_lincomb<true>, grid_for(n), kBlock, 0, s, n, m, pk, c, y);
 }
 void launch_orth_update(int n, int m, const double* const* Q, CoefPack c, double* w, Reducer red, int slot,
                         cudaStream_t s) {
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = Q[k];
-  k_orth_update<<<red_grid(k_orth_update, n), kBlock, 0, s>>>(n, m, pk, c, w, red, slot);
+  launch_pdl(k_orth_update, red_grid(k_orth_update, n), kBlock, 0, s, n, m, pk, c, w, red, slot);
 }
 void launch_lincomb_multi(int n, int kin, int kout, const double* const* in, double* const* out, const RotPack& T,
                           cudaStream_t s) {
@@ -437,95 +467,95 @@ void launch_lincomb_multi(int n, int kin, int kout, const double* const* in, dou
   PtrPack pi{}, po{};
   for (int k = 0; k < kin && k < kMaxMulti; ++k) pi.p[k] = in[k];
   for (int k = 0; k < kout && k < kMaxMulti; ++k) po.p[k] = out[k];
-  k_lincomb_multi<<<grid_for(n), kBlock, 0, s>>>(n, kin, kout, pi, po, T);
+  launch_pdl(k_lincomb_multi, grid_for(n), kBlock, 0, s, n, kin, kout, pi, po, T);
 }
 void launch_shift_gather(long nnz, const long* ptr, const long* src, const double* S, const double* m, double gdt,
                          double* shifted, cudaStream_t s) {
   ++g_launch_count;
   if (nnz == 0) return;
-  k_shift_gather<<<(int)std::min<long>((nnz + kBlock - 1) / kBlock, 148L * 32), kBlock, 0, s>>>(nnz, ptr, src, S, m,
+  launch_pdl(k_shift_gather, (int)std::min<long>((nnz + kBlock - 1) / kBlock, 148L * 32), kBlock, 0, s, nnz, ptr, src, S, m,
                                                                                               gdt, shifted);
 }
 void launch_csr_diag(int n, const int* rp, const int* ci, const double* v, double* d, cudaStream_t s) {
   ++g_launch_count;
   if (n == 0) return;
-  k_csr_diag<<<grid_for(n), kBlock, 0, s>>>(n, rp, ci, v, d);
+  launch_pdl(k_csr_diag, grid_for(n), kBlock, 0, s, n, rp, ci, v, d);
 }
 void launch_jacobi_div(int n, const double* d, const double* r, double* z, Reducer red, int slot, cudaStream_t s) {
   ++g_launch_count;
-  k_jacobi_div<<<red_grid(k_jacobi_div, n), kBlock, 0, s>>>(n, d, r, z, red, slot);
+  launch_pdl(k_jacobi_div, red_grid(k_jacobi_div, n), kBlock, 0, s, n, d, r, z, red, slot);
 }
 void launch_weighted_sq(int n, const double* est, const double* x, const double* xn, double atol, double rtol,
                         Reducer red, int slot, cudaStream_t s) {
   ++g_launch_count;
-  k_weighted_sq<<<red_grid(k_weighted_sq, n), kBlock, 0, s>>>(n, est, x, xn, atol, rtol, red, slot);
+  launch_pdl(k_weighted_sq, red_grid(k_weighted_sq, n), kBlock, 0, s, n, est, x, xn, atol, rtol, red, slot);
 }
 void launch_axpy(int n, double a, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;
-  k_axpy<<<grid_for(n), kBlock, 0, s>>>(n, a, x, y);
+  launch_pdl(k_axpy, grid_for(n), kBlock, 0, s, n, a, x, y);
 }
 void launch_axpy_dev(int n, const double* coef, double sign, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;
-  k_axpy_dev<<<grid_for(n), kBlock, 0, s>>>(n, coef, sign, x, y);
+  launch_pdl(k_axpy_dev, grid_for(n), kBlock, 0, s, n, coef, sign, x, y);
 }
 template <class XT>
 void launch_diag_scale(int n, const XT* invd, const XT* b, double a, XT* z, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launch_count;
   g_algo_bytes += 3.0 * sizeof(XT) * n;
-  k_diag_scale<XT><<<grid_for(n), kBlock, 0, s>>>(n, invd, b, a, z);
+  launch_pdl(k_diag_scale<XT>, grid_for(n), kBlock, 0, s, n, invd, b, a, z);
 }
 template void launch_diag_scale<double>(int, const double*, const double*, double, double*, cudaStream_t);
 template void launch_diag_scale<float>(int, const float*, const float*, double, float*, cudaStream_t);
 void launch_scale(int n, double a, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;
-  k_scale<<<grid_for(n), kBlock, 0, s>>>(n, a, x, y);
+  launch_pdl(k_scale, grid_for(n), kBlock, 0, s, n, a, x, y);
 }
 void launch_fill(long n, double v, double* y, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launch_count;
-  k_fill<<<grid_for(n), kBlock, 0, s>>>(n, v, y);
+  launch_pdl(k_fill, grid_for(n), kBlock, 0, s, n, v, y);
 }
 void launch_rkc_stage(int n, double a0, double mu, double nu, double mt, double gt, const double* y0,
                       const double* y1, const double* y2, const double* f, const double* f0, double* y,
                       cudaStream_t s) {
   ++g_launch_count;
-  k_rkc_stage<<<grid_for(n), kBlock, 0, s>>>(n, a0, mu, nu, mt, gt, y0, y1, y2, f, f0, y);
+  launch_pdl(k_rkc_stage, grid_for(n), kBlock, 0, s, n, a0, mu, nu, mt, gt, y0, y1, y2, f, f0, y);
 }
 void launch_axpby_into(int n, const double* y0, double c, const double* f, double* y, cudaStream_t s) {
   ++g_launch_count;
-  k_axpby_into<<<grid_for(n), kBlock, 0, s>>>(n, y0, c, f, y);
+  launch_pdl(k_axpby_into, grid_for(n), kBlock, 0, s, n, y0, c, f, y);
 }
 void launch_rkc_error(int n, const double* x, const double* xn, const double* f0, const double* fn, double dt,
                       double atol, double rtol, Reducer red, int slot, cudaStream_t s) {
   ++g_launch_count;
-  k_rkc_error<<<red_grid(k_rkc_error, n), kBlock, 0, s>>>(n, x, xn, f0, fn, dt, atol, rtol, red, slot);
+  launch_pdl(k_rkc_error, red_grid(k_rkc_error, n), kBlock, 0, s, n, x, xn, f0, fn, dt, atol, rtol, red, slot);
 }
 void launch_gather(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launch_count;
-  k_gather<double><<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
+  launch_pdl(k_gather<double>, grid_for(n), kBlock, 0, s, n, idx, x, y);
 }
 void launch_gather_f(int n, const int* idx, const float* x, float* y, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launch_count;
-  k_gather<float><<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
+  launch_pdl(k_gather<float>, grid_for(n), kBlock, 0, s, n, idx, x, y);
 }
 void launch_scatter(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
   if (n <= 0) return;
   ++g_launch_count;
-  k_scatter<<<grid_for(n), kBlock, 0, s>>>(n, idx, x, y);
+  launch_pdl(k_scatter, grid_for(n), kBlock, 0, s, n, idx, x, y);
 }
 void launch_lift_fixed(int n_fixed, const int* set_of_fixed, SetVals set_vals, double* fixed_part, cudaStream_t s) {
   if (n_fixed <= 0) return;
   ++g_launch_count;
-  k_lift_fixed<<<grid_for(n_fixed), kBlock, 0, s>>>(n_fixed, set_of_fixed, set_vals, fixed_part);
+  launch_pdl(k_lift_fixed, grid_for(n_fixed), kBlock, 0, s, n_fixed, set_of_fixed, set_vals, fixed_part);
 }
 void launch_boundary_load(int n_rows, const int* rows, const double* coef, int n_sets, SetVals rates, double* r,
                           cudaStream_t s) {
   if (n_rows <= 0) return;
   ++g_launch_count;
-  k_boundary_load<<<grid_for(n_rows), kBlock, 0, s>>>(n_rows, rows, coef, n_sets, rates, r);
+  launch_pdl(k_boundary_load, grid_for(n_rows), kBlock, 0, s, n_rows, rows, coef, n_sets, rates, r);
 }
 
 }  // namespace eqsb

@@ -6,10 +6,40 @@
 
 #include <algorithm>
 #include <unordered_map>
+#include <utility>
 
 #include "dev.cuh"
 
 namespace eqsb {
+
+// Programmatic dependent launch (PDL). Every kernel of k_rows.cu / k_sparse.cu
+// starts with pdl_entry(): griddepcontrol.wait blocks until the preceding
+// kernel on the stream has completed and its writes are visible (a no-op
+// when the launch carried no PDL attribute), then launch_dependents lets the
+// next PDL launch start its CTAs on SMs freed by this grid's last wave. The
+// next kernel's launch latency and ramp thus overlap this kernel's tail;
+// ordering and results are unchanged (each wait covers the whole chain).
+
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 namespace {
 
 

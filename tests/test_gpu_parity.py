@@ -325,19 +325,25 @@ def test_graph_pcg_loop_bit_identical(f32_vectors):
     assert out[1][0][1].iterations > 3 and not out[1][2][1].converged and out[1][2][1].iterations == 3
 
 
-def test_graph_pcg_loop_rkc_steps_bit_identical():
+def test_graph_pcg_loop_and_pdl_rkc_steps_bit_identical():
     """Fixed RKC steps (fused residual, SPE starts, AMG-PCG M-solves) with the
-    graph-resident PCG loop on and off: identical potentials and counters."""
+    graph-resident PCG loop (option 20) and programmatic dependent launch
+    (option 21) on and off: identical potentials and counters."""
     cfg = cube(12, jitter=0.1, planes=(0.45, 0.55))
     res = {}
-    for loop in (1, 0):
-        g = eb.FemSystem(cfg)
-        g.set_option(20, loop)
-        x0 = 2e4 * po.random_vec(g.n_free, 93)
-        g.set_state(0.0, x0, 1e-4)
-        g.rkc_advance_fixed(1e-4, 4, 3)
-        x, _ = g.get_state()
-        s = g.stats()
-        res[loop] = (x, s["pcg_iterations"], s["m_solves"])
-    assert np.array_equal(res[1][0], res[0][0])
-    assert res[1][1:] == res[0][1:]
+    try:
+        for loop, pdl in ((1, 1), (0, 0), (1, 0), (0, 1)):
+            g = eb.FemSystem(cfg)
+            g.set_option(20, loop)
+            g.set_option(21, pdl)
+            x0 = 2e4 * po.random_vec(g.n_free, 93)
+            g.set_state(0.0, x0, 1e-4)
+            g.rkc_advance_fixed(1e-4, 4, 3)
+            x, _ = g.get_state()
+            s = g.stats()
+            res[(loop, pdl)] = (x, s["pcg_iterations"], s["m_solves"])
+    finally:
+        g.set_option(21, 1)
+    for key, val in res.items():
+        assert np.array_equal(val[0], res[(0, 0)][0]), key
+        assert val[1:] == res[(0, 0)][1:], key
