@@ -33,7 +33,13 @@ enum Slot : int {
   S_NORM,     // generic norm^2
   S_MDOT,     // first of kMaxMulti multi-dot slots
   kMaxMulti = 16,
-  S_COUNT = S_MDOT + kMaxMulti
+  // SPE append (one host read per append): |h|^2, |w|^2 after each
+  // Gram-Schmidt pass, the two passes' coefficients, the new G column
+  S_APP = S_MDOT + kMaxMulti,
+  S_APP_NRM = S_APP + 1,
+  S_APP_C = S_APP + 3,
+  S_APP_G = S_APP_C + 2 * kMaxMulti,
+  S_COUNT = S_APP_G + kMaxMulti
 };
 
 struct Reducer {
@@ -195,15 +201,26 @@ void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, do
 // and d32 = invd32 .* r32 (the next fp32 V-cycle's inputs)
 void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s,
                        float* r32 = nullptr, const float* invd32 = nullptr, float* d32 = nullptr);
-// p = z + beta p, beta = scal[S_RZ]/scal[S_RZ_OLD]
-void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s);
+// w -= sum_j dcoef[j] Q_j ; slot <- w.w   (coefficients read from device memory)
+void launch_orth_update_dev(int n, int m, const double* const* Q, const double* dcoef, double* w, Reducer red,
+                            int slot, cudaStream_t s);
+// y = x / sqrt(*nrm2)  (device-resident norm^2)
+void launch_scale_rsqrt(int n, const double* nrm2, const double* x, double* y, cudaStream_t s);
+// p = z + beta p, beta = scal[S_RZ]/scal[S_RZ_OLD]; p = z when stat && stat[0] == 0
+void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s,
+                          const double* stat = nullptr);
 // Device-side PCG stopping rule (pcg.cpp:40-66) for the graph-resident
-// iteration loop. stat = [k, status, rel, pq, bnorm, tol, max_iter]: advances
+// iteration loop. stat = [k, status, rel, pq, bnorm, tol, max_iter, rr0 (< 0:
+// read S_RR), initial rel]: advances
 // k, sets status 0 continue / 1 converged / 2 rz non-finite / 3 p'Ap <= 0 or
 // non-finite / 4 rel non-finite / 5 max_iter reached, copies r.z to S_RZ_OLD
 // when continuing and sets the loop's conditional handle to (status == 0).
-enum PcgStatus : int { PCG_CONTINUE = 0, PCG_CONVERGED, PCG_BAD_RZ, PCG_BAD_PQ, PCG_BAD_REL, PCG_MAX_ITER };
+enum PcgStatus : int {
+  PCG_CONTINUE = 0, PCG_CONVERGED, PCG_BAD_RZ, PCG_BAD_PQ, PCG_BAD_REL, PCG_MAX_ITER, PCG_BAD_INIT
+};
 void launch_pcg_check(double* scal, double* stat, cudaGraphConditionalHandle h, cudaStream_t s);
+// initial residual test (status PCG_BAD_INIT / PCG_CONVERGED / PCG_CONTINUE), sets the loop condition
+void launch_pcg_check0(double* scal, double* stat, cudaGraphConditionalHandle h, cudaStream_t s);
 // z = Ainv b (dense, n <= 1024, fp64 inverse)
 template <class XT>
 void launch_dense_solve(int n, const double* ainv, const float* ainv32, const XT* b, XT* z, cudaStream_t s);

@@ -234,7 +234,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     CK(cudaSetDevice(device_));
     CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     CK(cudaMallocHost(&pinned_, sizeof(double) * (S_COUNT + 8)));
-    CK(cudaMallocHost(&pcg_pinned_, sizeof(double) * 8));
+    CK(cudaMallocHost(&pcg_pinned_, sizeof(double) * 9));
   }
   const Dofs& dm = prob_.dm;
   n_dofs_ = dm.n_dofs;
@@ -535,7 +535,7 @@ void GpuSystem::build_device() {
   // reductions + work vectors
   red_partials_.alloc((size_t)S_COUNT * kRedGrid);
   red_scal_.alloc(S_COUNT);
-  pcg_stat_.alloc(8);
+  pcg_stat_.alloc(9);
   red_counters_.alloc(S_COUNT);
   CK(cudaMemsetAsync(red_counters_.p, 0, sizeof(unsigned) * S_COUNT, s));
   CK(cudaMemsetAsync(red_scal_.p, 0, sizeof(double) * S_COUNT, s));
@@ -1191,11 +1191,13 @@ double* GpuSystem::precondition(double* r, bool prepared) {
   return z;
 }
 
-// One PCG iteration k >= 2 as the body of a WHILE conditional node: V-cycle
-// on r (z, r.z), p = z + beta p, q = A p with p.q, the x/r update with r.r
-// (and the next V-cycle's fp32 inputs), then k_pcg_check evaluates the
-// stopping rule and sets the loop condition. Kernels and arguments are those
-// of the host loop, so every iteration computes the same values.
+// The whole PCG iteration of pcg_dev as one CUDA graph: k_pcg_check0 tests
+// the initial residual and sets the condition of a WHILE node whose body is
+// one iteration (V-cycle on r with r.z, p = z (first) or z + beta p, q = A p
+// with p.q, the x/r update with r.r and the next V-cycle's fp32 inputs), closed
+// by k_pcg_check (the stopping rule and breakdown tests on the device).
+// Kernels and arguments are those of the host loop, so every iteration
+// computes the same values; the host reads the verdict once per solve.
 cudaGraphExec_t GpuSystem::pcg_loop_graph(double* x, bool f32) {
   auto it = pcg_graphs_.find(x);
   if (it != pcg_graphs_.end()) return it->second;
@@ -1210,21 +1212,29 @@ cudaGraphExec_t GpuSystem::pcg_loop_graph(double* x, bool f32) {
   cudaGraph_t graph;
   CK(cudaGraphCreate(&graph, 0));
   cudaGraphConditionalHandle handle;
-  CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+  CK(cudaGraphConditionalHandleCreate(&handle, graph, 0, cudaGraphCondAssignDefault));
+  const long before = g_launch_count;
+  const double bytes_before = g_algo_bytes;
+  CK(cudaStreamBeginCaptureToGraph(stream_, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  launch_pcg_check0(red_scal_.p, pcg_stat_.p, handle, stream_);
+  CK(cudaStreamEndCapture(stream_, &graph));
+  cudaGraphNode_t check0;
+  size_t n_nodes = 1;
+  CK(cudaGraphGetNodes(graph, &check0, &n_nodes));
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = handle;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
   cudaGraphNode_t node;
-  CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+  CK(cudaGraphAddNode(&node, graph, &check0, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
-  const long before = g_launch_count;
-  const double bytes_before = g_algo_bytes;
+  const long body_before = g_launch_count;
+  const double body_bytes_before = g_algo_bytes;
   CK(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   if (!f32) vcycle_prepare(r);
   double* z = vcycle(r);
-  launch_pcg_direction(n, p, z, red_scal_.p, stream_);
+  launch_pcg_direction(n, p, z, red_scal_.p, stream_, pcg_stat_.p);
   launch_spmv_dot(mii_, p, q, red_, S_PQ, stream_);
   DevLevel& f0 = levels_.empty() ? dummy_level_ : levels_[0];
   if (f32)
@@ -1233,8 +1243,8 @@ cudaGraphExec_t GpuSystem::pcg_loop_graph(double* x, bool f32) {
     launch_pcg_update(n, x, r, p, q, red_, stream_);
   launch_pcg_check(red_scal_.p, pcg_stat_.p, handle, stream_);
   CK(cudaStreamEndCapture(stream_, &body));
-  pcg_body_kernels_ = g_launch_count - before;
-  pcg_body_bytes_ = g_algo_bytes - bytes_before;
+  pcg_body_kernels_ = g_launch_count - body_before;
+  pcg_body_bytes_ = g_algo_bytes - body_bytes_before;
   g_launch_count = before;
   g_algo_bytes = bytes_before;
   cudaGraphExec_t exec;
@@ -1244,26 +1254,96 @@ cudaGraphExec_t GpuSystem::pcg_loop_graph(double* x, bool f32) {
   return exec;
 }
 
+// pcg_dev with the iteration in one graph launch (pcg_loop_graph): the
+// start (x = x0 and r = b - A x0, or x = 0 and r = b) is enqueued, then the
+// graph; one host read of the verdict per solve.
+PcgResult GpuSystem::pcg_dev_graph(const double* b, bool use_x0, const double* x0, double* x, double tol,
+                                   int max_iter, double bnorm) {
+  const int n = n_own_;
+  PcgResult res;
+  double* r = w_r_.p;
+  double* p = w_p_.p;
+  if (use_x0) {
+    if (x0 != x) CK(cudaMemcpyAsync(x, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    CK(cudaMemcpyAsync(p, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    halo(halo0_, p);
+    Reducer rd = red_;
+    launch_residual(mii_, b, p, r, &rd, S_RR, stream_);
+    allreduce(S_RR);
+  } else {
+    launch_fill(n, 0.0, x, stream_);
+    CK(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+  }
+  const bool f32 = vcycle_f32_ && levels_.size() >= 2;
+  if (f32) vcycle_prepare(r);  // the first V-cycle's fp32 inputs (later ones come out of the update)
+  cudaGraphExec_t loop = pcg_loop_graph(x, f32);
+  double* st = pcg_pinned_;
+  st[0] = 0.0;
+  st[1] = 0.0;
+  st[2] = 0.0;
+  st[3] = 0.0;
+  st[4] = bnorm;
+  st[5] = tol;
+  st[6] = max_iter;
+  st[7] = use_x0 ? -1.0 : bnorm * bnorm;
+  st[8] = 0.0;
+  CK(cudaMemcpyAsync(pcg_stat_.p, st, sizeof(double) * 9, cudaMemcpyHostToDevice, stream_));
+  CK(cudaGraphLaunch(loop, stream_));
+  CK(cudaMemcpyAsync(st, pcg_stat_.p, sizeof(double) * 9, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  const int k_end = (int)st[0];
+  const int status = (int)st[1];
+  g_launch_count += 1 + (long)k_end * pcg_body_kernels_;
+  g_algo_bytes += (double)k_end * pcg_body_bytes_;
+  res.iterations = k_end;
+  res.initial_rel_residual = st[8];
+  res.rel_residual = st[2];
+  switch (status) {
+    case PCG_CONVERGED: res.converged = true; return res;
+    case PCG_BAD_INIT: throw NumericalError("pcg: non-finite initial residual");
+    case PCG_BAD_RZ: throw NumericalError("pcg: non-finite preconditioned residual");
+    case PCG_BAD_PQ:
+      throw NumericalError("pcg: operator not positive definite (p'Ap = " + std::to_string(st[3]) + ")");
+    case PCG_BAD_REL: throw NumericalError("pcg: non-finite residual");
+    default: break;
+  }
+  // PCG_MAX_ITER: the host loop's last precondition + direction, then its check
+  CK(cudaMemcpyAsync(red_scal_.p + S_RZ_OLD, red_scal_.p + S_RZ, sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+  double* z = precondition(r, f32);
+  launch_pcg_direction(n, p, z, red_scal_.p, stream_);
+  double sc[1];
+  read_scalars(S_RZ, 1, sc);
+  if (!std::isfinite(sc[0])) throw NumericalError("pcg: non-finite preconditioned residual");
+  return res;
+}
+
 // pcg_solve (proj/src/pcg.cpp:9-72) with device vectors; host reads three
 // scalars per iteration for the stopping rule and the breakdown checks.
 // b, x: owned entries; x0 may be null.
 PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, double tol, int max_iter) {
   const int n = n_own_;
   PcgResult res;
+  // The iteration runs as one CUDA graph (pcg_loop_graph) when the V-cycle
+  // is capturable and no per-class timing is requested; the decisions are the
+  // same tests on the same scalars, evaluated on the device.
+  const bool graph_loop = pcg_graph_loop && use_graphs && !timing_on && prob_.solver.precond == 2 &&
+                          comm_->size() == 1 && comm_->capturable() && device_ >= 0 && max_iter >= 1;
   launch_dot(n, b, b, red_, S_BB, stream_);
   allreduce(S_BB);
-  const double bnorm = std::sqrt(read_scalar(S_BB));
+  if (x0) {  // S_X0X0 follows S_BB: one read for both
+    launch_dot(n, x0, x0, red_, S_X0X0, stream_);
+    allreduce(S_X0X0);
+  }
+  double bx[2] = {0.0, 0.0};
+  read_scalars(S_BB, x0 ? 2 : 1, bx);
+  const double bnorm = std::sqrt(bx[0]);
   if (bnorm == 0.0) {
     launch_fill(n, 0.0, x, stream_);
     res.converged = true;
     return res;
   }
-  bool use_x0 = false;
-  if (x0) {
-    launch_dot(n, x0, x0, red_, S_X0X0, stream_);
-    allreduce(S_X0X0);
-    use_x0 = read_scalar(S_X0X0) != 0.0;
-  }
+  const bool use_x0 = x0 && bx[1] != 0.0;
+  if (graph_loop) return pcg_dev_graph(b, use_x0, x0, x, tol, max_iter, bnorm);
   double* r = w_r_.p;
   double* z = nullptr;
   double* p = w_p_.p;
@@ -1299,11 +1379,6 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
   read_scalars(S_RZ, 1, sc);
   if (!std::isfinite(sc[0])) throw NumericalError("pcg: non-finite preconditioned residual");
   CK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));  // p = z
-  // The loop runs in one CUDA graph (pcg_loop_graph) when the V-cycle is
-  // capturable and no per-class timing is requested; the decisions are the
-  // same tests on the same scalars, evaluated on the device.
-  const bool graph_loop = pcg_graph_loop && use_graphs && !timing_on && prob_.solver.precond == 2 &&
-                          comm_->size() == 1 && comm_->capturable() && device_ >= 0;
   for (int k = 1; k <= max_iter; ++k) {
     tic(TC_PCG);
     halo(halo0_, p);
@@ -1332,43 +1407,6 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
     }
     CK(cudaMemcpyAsync(red_scal_.p + S_RZ_OLD, red_scal_.p + S_RZ, sizeof(double), cudaMemcpyDeviceToDevice,
                        stream_));
-    if (k < max_iter && graph_loop) {
-      // iterations k+1 .. run inside one graph launch; the host reads the
-      // device stopping rule's verdict once at the end
-      cudaGraphExec_t loop = pcg_loop_graph(x, f32);
-      pcg_pinned_[0] = k;
-      pcg_pinned_[1] = 0.0;
-      pcg_pinned_[2] = rel;
-      pcg_pinned_[3] = 0.0;
-      pcg_pinned_[4] = bnorm;
-      pcg_pinned_[5] = tol;
-      pcg_pinned_[6] = max_iter;
-      CK(cudaMemcpyAsync(pcg_stat_.p, pcg_pinned_, sizeof(double) * 7, cudaMemcpyHostToDevice, stream_));
-      CK(cudaGraphLaunch(loop, stream_));
-      CK(cudaMemcpyAsync(pcg_pinned_, pcg_stat_.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, stream_));
-      sync();
-      const int k_end = (int)pcg_pinned_[0];
-      const int status = (int)pcg_pinned_[1];
-      const long body_runs = k_end - k;
-      g_launch_count += body_runs * pcg_body_kernels_;
-      g_algo_bytes += body_runs * pcg_body_bytes_;
-      res.iterations = k_end;
-      res.rel_residual = pcg_pinned_[2];
-      switch (status) {
-        case PCG_CONVERGED: res.converged = true; return res;
-        case PCG_BAD_RZ: throw NumericalError("pcg: non-finite preconditioned residual");
-        case PCG_BAD_PQ:
-          throw NumericalError("pcg: operator not positive definite (p'Ap = " + std::to_string(pcg_pinned_[3]) +
-                               ")");
-        case PCG_BAD_REL: throw NumericalError("pcg: non-finite residual");
-        default: break;  // PCG_MAX_ITER: the host loop's last precondition + direction
-      }
-      CK(cudaMemcpyAsync(red_scal_.p + S_RZ_OLD, red_scal_.p + S_RZ, sizeof(double), cudaMemcpyDeviceToDevice,
-                         stream_));
-      z = precondition(r, f32);
-      launch_pcg_direction(n, p, z, red_scal_.p, stream_);
-      break;
-    }
     z = precondition(r, f32);
     tic(TC_PCG);
     launch_pcg_direction(n, p, z, red_scal_.p, stream_);
@@ -1473,47 +1511,61 @@ void GpuSystem::spe_rebuild() {
 }
 
 // append h (newest) with two classical Gram-Schmidt passes and the MGS drop test
+// Append h to the basis: the device runs both Gram-Schmidt passes (the
+// coefficients go from the multi-dot slots straight into the update), the
+// normalisation, W_m = M q_m and the new G column back to back; the host reads
+// all their scalars once and replays the reference's drop decisions
+// (start_vector.cpp:10-28) on them. A dropped vector only leaves scratch in
+// the unused slot m, so the committed state equals the step-by-step version.
 void GpuSystem::spe_append(double* h) {
   const int n = n_own_;
   const double drop = prob_.solver.mgs_drop_tol;
   const int m = spe_k_;
-  const double norm0 = std::sqrt(dot_own(h, h, S_NORM));
+  double* w = spe_q(spe_set_, m);
+  launch_dot(n, h, h, red_, S_APP, stream_);
+  allreduce(S_APP);
+  CK(cudaMemcpyAsync(w, h, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+  std::vector<const double*> Q(m);
+  for (int i = 0; i < m; ++i) Q[i] = spe_q(spe_set_, i);
+  if (m > 0)
+    for (int pass = 0; pass < 2; ++pass) {
+      const int cs = S_APP_C + pass * kMaxMulti;
+      launch_multi_dot(n, m, Q.data(), w, red_, cs, stream_);
+      allreduce(cs, m);
+      launch_orth_update_dev(n, m, Q.data(), red_scal_.p + cs, w, red_, S_APP_NRM + pass, stream_);
+      allreduce(S_APP_NRM + pass);
+    }
+  launch_scale_rsqrt(n, red_scal_.p + (m > 0 ? S_APP_NRM + 1 : S_APP), w, w, stream_);
+  double* wm = spe_w(spe_set_, m);
+  mass_apply_dev(w, wm);
+  Q.push_back(w);
+  launch_multi_dot(n, m + 1, Q.data(), wm, red_, S_APP_G, stream_);
+  allreduce(S_APP_G, m + 1);
+  double sc[S_COUNT - S_APP];
+  read_scalars(S_APP, S_COUNT - S_APP, sc);
+  const double norm0 = std::sqrt(sc[0]);
   if (norm0 == 0.0) {
     spe_clean_ = false;
     return;
   }
-  double* w = spe_q(spe_set_, m);
-  CK(cudaMemcpyAsync(w, h, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
-  std::vector<const double*> Q(m);
-  for (int i = 0; i < m; ++i) Q[i] = spe_q(spe_set_, i);
   std::vector<double> r(m + 1, 0.0);
   double nrm = norm0;
   for (int pass = 0; pass < 2; ++pass) {
     if (m > 0) {
-      launch_multi_dot(n, m, Q.data(), w, red_, S_MDOT, stream_);
-      allreduce(S_MDOT, m);
-      double c[kMaxMulti];
-      read_scalars(S_MDOT, m, c);
-      CoefPack cp{};
-      for (int i = 0; i < m; ++i) {
-        cp.c[i] = c[i];
-        r[i] += c[i];
-      }
-      launch_orth_update(n, m, Q.data(), cp, w, red_, S_NORM, stream_);
-      allreduce(S_NORM);
-      nrm = std::sqrt(read_scalar(S_NORM));
+      for (int i = 0; i < m; ++i) r[i] += sc[S_APP_C - S_APP + pass * kMaxMulti + i];
+      nrm = std::sqrt(sc[S_APP_NRM - S_APP + pass]);
     }
     if (nrm <= drop * norm0) {
       spe_clean_ = false;
       return;
     }
   }
-  launch_scale(n, 1.0 / nrm, w, w, stream_);
   r[m] = nrm;
   for (int i = 0; i <= m; ++i) spe_R_[(size_t)i * kMaxWin + m] = r[i];
-  mass_apply_dev(w, spe_w(spe_set_, m));
   spe_k_ = m + 1;
-  spe_g_column(m);
+  spe_G_.resize((size_t)kMaxMulti * kMaxMulti);
+  for (int i = 0; i <= m; ++i)
+    spe_G_[(size_t)i * kMaxMulti + m] = spe_G_[(size_t)m * kMaxMulti + i] = sc[S_APP_G - S_APP + i];
 }
 
 // remove the oldest window vector: Givens downdate of R[:,1:], rotate Q and W

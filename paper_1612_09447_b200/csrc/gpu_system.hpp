@@ -330,8 +330,10 @@ class GpuSystem {
   long pcg_body_kernels_ = 0;
   double pcg_body_bytes_ = 0.0;
   DevBuf<double> pcg_stat_;
-  double* pcg_pinned_ = nullptr;  // host pinned [8]: stat in / out
+  double* pcg_pinned_ = nullptr;  // host pinned [9]: stat in / out
   cudaGraphExec_t pcg_loop_graph(double* x, bool f32);
+  PcgResult pcg_dev_graph(const double* b, bool use_x0, const double* x0, double* x, double tol, int max_iter,
+                          double bnorm);
 
   Problem prob_;
   int device_ = 0;

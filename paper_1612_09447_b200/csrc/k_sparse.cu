@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <stdexcept>
 #include <type_traits>
 #include <unordered_map>
 
@@ -141,11 +142,33 @@ __global__ void k_to_f64_dot(int n, const float* __restrict__ z32, double* __res
 }
 
 __global__ void k_pcg_direction(int n, double* __restrict__ p, const double* __restrict__ z,
-                                const double* __restrict__ scal) {
+                                const double* __restrict__ scal, const double* __restrict__ stat) {
   pdl_entry();
+  // graph-resident loop: before the first iteration (stat[0] == 0) p = z,
+  // exactly the host loop's copy
+  if (stat && stat[0] == 0.0) {
+    for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) p[i] = z[i];
+    return;
+  }
   const double beta = scal[S_RZ] / scal[S_RZ_OLD];
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
     p[i] = z[i] + beta * p[i];
+}
+
+// Initial residual test of the graph-resident loop (pcg.cpp:19-31): rr from
+// stat[7] (zero start: b.b) or S_RR (x0 start), rel = sqrt(rr) / bnorm.
+__global__ void k_pcg_check0(double* __restrict__ scal, double* __restrict__ stat, cudaGraphConditionalHandle h) {
+  const double rr = stat[7] < 0.0 ? scal[S_RR] : stat[7];
+  const double rel = sqrt(rr) / stat[4];
+  int status = PCG_CONTINUE;
+  if (!isfinite(rel))
+    status = PCG_BAD_INIT;
+  else if (rel <= stat[5])
+    status = PCG_CONVERGED;
+  stat[1] = status;
+  stat[2] = rel;
+  stat[8] = rel;
+  cudaGraphSetConditional(h, status == PCG_CONTINUE ? 1u : 0u);
 }
 
 // Same tests, same order and same arithmetic as the host loop in
@@ -184,26 +207,43 @@ struct PtrPack {
   const double* p[kMaxMulti];
 };
 
-__global__ void k_multi_dot(int n, int m, PtrPack V, const double* __restrict__ w, Reducer red, int slot0) {
+// 16-byte loads over element pairs; an odd last element goes to thread 0 of block 0
+__global__ void k_multi_dot(int n, int m, PtrPack V, const double* __restrict__ w, Reducer red, int slot0,
+                            int vec) {
   pdl_entry();
   double acc[kMaxMulti];
 #pragma unroll
   for (int k = 0; k < kMaxMulti; ++k) acc[k] = 0.0;
-  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+  const long n2 = vec ? n / 2 : 0;  // vec: every vector 16-byte aligned
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (long)gridDim.x * kBlock) {
+    const double2 wi = w2[i];
+#pragma unroll
+    for (int k = 0; k < kMaxMulti; ++k)
+      if (k < m) {
+        const double2 v = reinterpret_cast<const double2*>(V.p[k])[i];
+        acc[k] += v.x * wi.x;
+        acc[k] += v.y * wi.y;
+      }
+  }
+  for (long i = 2 * n2 + (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     const double wi = w[i];
 #pragma unroll
     for (int k = 0; k < kMaxMulti; ++k)
       if (k < m) acc[k] += V.p[k][i] * wi;
   }
-  for (int k = 0; k < m; ++k) reduce_finish(acc[k], red, slot0 + k);
+#pragma unroll
+  for (int k = 0; k < kMaxMulti; ++k)  // constant indices keep acc in registers
+    if (k < m) reduce_finish(acc[k], red, slot0 + k);
 }
-
 template <bool ACC>
 __global__ void k_lincomb(int n, int m, PtrPack V, CoefPack c, double* __restrict__ y) {
   pdl_entry();
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     double s = ACC ? y[i] : 0.0;
-    for (int k = 0; k < m; ++k) s += V.p[k][i] * c.c[k];
+#pragma unroll
+    for (int k = 0; k < kMaxMulti; ++k)  // constant indices: the packs stay in parameter space
+      if (k < m) s += V.p[k][i] * c.c[k];
     y[i] = s;
   }
 }
@@ -214,24 +254,77 @@ __global__ void k_orth_update(int n, int m, PtrPack Q, CoefPack c, double* __res
   double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
     double s = w[i];
-    for (int k = 0; k < m; ++k) s -= c.c[k] * Q.p[k][i];
+#pragma unroll
+    for (int k = 0; k < kMaxMulti; ++k)
+      if (k < m) s -= c.c[k] * Q.p[k][i];
     w[i] = s;
     acc += s * s;
   }
   reduce_finish(acc, red, slot);
 }
 
-// out_j = sum_i T[i][j] in_i  (basis rotation of the SPE window, T by value)
-__global__ void k_lincomb_multi(int n, int kin, int kout, PtrPack in, PtrPack out, RotPack T) {
+// the same pass with the coefficients read from device memory (the multi-dot
+// slots), so no host round trip sits between the two kernels
+__global__ void k_orth_update_dev(int n, int m, PtrPack Q, const double* __restrict__ dcoef,
+                                  double* __restrict__ w, Reducer red, int slot) {
   pdl_entry();
+  double c[kMaxMulti];
+#pragma unroll
+  for (int k = 0; k < kMaxMulti; ++k) c[k] = k < m ? dcoef[k] : 0.0;
+  double acc = 0.0;
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
-    double v[kMaxMulti];
-    for (int a = 0; a < kin; ++a) v[a] = in.p[a][i];
-    for (int b = 0; b < kout; ++b) {
-      double s = 0.0;
-      for (int a = 0; a < kin; ++a) s += T.t[a][b] * v[a];
-      const_cast<double*>(out.p[b])[i] = s;
-    }
+    double s = w[i];
+#pragma unroll
+    for (int k = 0; k < kMaxMulti; ++k)
+      if (k < m) s -= c[k] * Q.p[k][i];
+    w[i] = s;
+    acc += s * s;
+  }
+  reduce_finish(acc, red, slot);
+}
+
+__global__ void k_scale_rsqrt(int n, const double* __restrict__ nrm2, const double* __restrict__ x,
+                              double* __restrict__ y) {
+  pdl_entry();
+  const double a = 1.0 / sqrt(*nrm2);  // the host's 1.0 / std::sqrt(.)
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) y[i] = a * x[i];
+}
+
+// out_j = sum_i T[i][j] in_i  (basis rotation of the SPE window, T by value)
+// KIN inputs held in registers (a runtime-indexed array would live in local
+// memory); element pairs with 16-byte loads and stores
+template <int KIN>
+__global__ void k_lincomb_multi(int n, int kout, PtrPack in, PtrPack out, RotPack T, int vec) {
+  pdl_entry();
+  const long n2 = vec ? n / 2 : 0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (long)gridDim.x * kBlock) {
+    double2 v[KIN];
+#pragma unroll
+    for (int a = 0; a < KIN; ++a) v[a] = reinterpret_cast<const double2*>(in.p[a])[i];
+#pragma unroll
+    for (int b = 0; b < KIN; ++b)
+      if (b < kout) {
+        double sx = 0.0, sy = 0.0;
+#pragma unroll
+        for (int a = 0; a < KIN; ++a) {
+          sx += T.t[a][b] * v[a].x;
+          sy += T.t[a][b] * v[a].y;
+        }
+        reinterpret_cast<double2*>(const_cast<double*>(out.p[b]))[i] = make_double2(sx, sy);
+      }
+  }
+  for (long i = 2 * n2 + (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    double v[KIN];
+#pragma unroll
+    for (int a = 0; a < KIN; ++a) v[a] = in.p[a][i];
+#pragma unroll
+    for (int b = 0; b < KIN; ++b)
+      if (b < kout) {
+        double sv = 0.0;
+#pragma unroll
+        for (int a = 0; a < KIN; ++a) sv += T.t[a][b] * v[a];
+        const_cast<double*>(out.p[b])[i] = sv;
+      }
   }
 }
 
@@ -400,9 +493,14 @@ void launch_to_f64_dot(int n, const float* z32, double* z64, const double* b, Re
   Reducer rr = red ? *red : Reducer{};
   launch_pdl(k_to_f64_dot, red_grid(k_to_f64_dot, n), kBlock, 0, s, n, z32, z64, b, rr, slot, red ? 1 : 0);
 }
-void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s) {
+void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s,
+                          const double* stat) {
   ++g_launch_count;
-  launch_pdl(k_pcg_direction, grid_for(n), kBlock, 0, s, n, p, z, scal);
+  launch_pdl(k_pcg_direction, grid_for(n), kBlock, 0, s, n, p, z, scal, stat);
+}
+void launch_pcg_check0(double* scal, double* stat, cudaGraphConditionalHandle h, cudaStream_t s) {
+  ++g_launch_count;
+  k_pcg_check0<<<1, 1, 0, s>>>(scal, stat, h);
 }
 void launch_pcg_check(double* scal, double* stat, cudaGraphConditionalHandle h, cudaStream_t s) {
   ++g_launch_count;
@@ -440,7 +538,9 @@ void launch_multi_dot(int n, int m, const double* const* V, const double* w, Red
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
-  launch_pdl(k_multi_dot, red_grid(k_multi_dot, n), kBlock, 0, s, n, m, pk, w, red, slot0);
+  bool vec = aligned16(w);
+  for (int k = 0; k < m; ++k) vec = vec && aligned16(V[k]);
+  launch_pdl(k_multi_dot, red_grid(k_multi_dot, n), kBlock, 0, s, n, m, pk, w, red, slot0, vec ? 1 : 0);
 }
 void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s) {
   ++g_launch_count;
@@ -461,13 +561,34 @@ void launch_orth_update(int n, int m, const double* const* Q, CoefPack c, double
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = Q[k];
   launch_pdl(k_orth_update, red_grid(k_orth_update, n), kBlock, 0, s, n, m, pk, c, w, red, slot);
 }
+void launch_orth_update_dev(int n, int m, const double* const* Q, const double* dcoef, double* w, Reducer red,
+                            int slot, cudaStream_t s) {
+  ++g_launch_count;
+  PtrPack pk{};
+  for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = Q[k];
+  launch_pdl(k_orth_update_dev, red_grid(k_orth_update_dev, n), kBlock, 0, s, n, m, pk, dcoef, w, red, slot);
+}
+void launch_scale_rsqrt(int n, const double* nrm2, const double* x, double* y, cudaStream_t s) {
+  ++g_launch_count;
+  launch_pdl(k_scale_rsqrt, grid_for(n), kBlock, 0, s, n, nrm2, x, y);
+}
 void launch_lincomb_multi(int n, int kin, int kout, const double* const* in, double* const* out, const RotPack& T,
                           cudaStream_t s) {
   ++g_launch_count;
   PtrPack pi{}, po{};
   for (int k = 0; k < kin && k < kMaxMulti; ++k) pi.p[k] = in[k];
   for (int k = 0; k < kout && k < kMaxMulti; ++k) po.p[k] = out[k];
-  launch_pdl(k_lincomb_multi, grid_for(n), kBlock, 0, s, n, kin, kout, pi, po, T);
+  bool vec = true;
+  for (int k = 0; k < kin; ++k) vec = vec && aligned16(in[k]);
+  for (int k = 0; k < kout; ++k) vec = vec && aligned16(out[k]);
+  const int g = grid_for(vec ? n / 2 + 1 : n);
+  switch (kin) {
+#define LM_(K) \
+  case K: launch_pdl(k_lincomb_multi<K>, g, kBlock, 0, s, n, kout, pi, po, T, vec ? 1 : 0); break;
+    LM_(1) LM_(2) LM_(3) LM_(4) LM_(5) LM_(6) LM_(7) LM_(8) LM_(9)
+#undef LM_
+    default: throw std::invalid_argument("lincomb_multi: at most kMaxWin inputs");
+  }
 }
 void launch_shift_gather(long nnz, const long* ptr, const long* src, const double* S, const double* m, double gdt,
                          double* shifted, cudaStream_t s) {

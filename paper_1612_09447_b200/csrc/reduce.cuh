@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <unordered_map>
 #include <utility>
 
@@ -116,6 +117,7 @@ int red_grid(K kernel, long work_items) {
   return (int)std::max<long>(g, 1);
 }
 
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 inline int grid_for(long n) {
   long g = (n + kBlock - 1) / kBlock;
   const long cap = 148L * 32;

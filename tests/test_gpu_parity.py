@@ -316,13 +316,19 @@ def test_graph_pcg_loop_bit_identical(f32_vectors):
     out = {}
     for loop in (1, 0):
         g.set_option(20, loop)
+        xs = g.mass_solve(b)[0]
         out[loop] = [g.mass_solve(b), g.mass_solve(b, x0=x0), g.mass_solve(b, max_iter=3),
-                     g.mass_solve(b, tol=1e-6)]
+                     g.mass_solve(b, tol=1e-6), g.mass_solve(b, tol=1.0), g.mass_solve(b, x0=xs),
+                     g.mass_solve(b, max_iter=1), g.mass_solve(np.zeros_like(b))]
     for (xa, ra), (xb, rb) in zip(out[1], out[0]):
         assert np.array_equal(xa, xb)
         assert ra.iterations == rb.iterations and ra.converged == rb.converged
         assert ra.rel_residual == rb.rel_residual
+        assert ra.initial_rel_residual == rb.initial_rel_residual
     assert out[1][0][1].iterations > 3 and not out[1][2][1].converged and out[1][2][1].iterations == 3
+    assert out[1][4][1].iterations == 0 and out[1][4][1].converged  # rel = 1 <= tol at the start
+    assert out[1][6][1].iterations == 1 and not out[1][6][1].converged
+    assert out[1][7][1].iterations == 0 and out[1][7][1].converged and not out[1][7][0].any()
 
 
 def test_graph_pcg_loop_and_pdl_rkc_steps_bit_identical():
