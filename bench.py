@@ -56,6 +56,7 @@ CPU_SAMPLE = dict(n=48, steps=2)
 
 
 COARSE_FILTER = None  # --coarse-filter: solver.amg_coarse_filter override (additive key)
+DENSE_COARSE = None  # --dense-coarse: solver.amg_dense_coarse override (additive key)
 
 
 def scenario(n, jitter, planes, estimator="spe"):
@@ -68,7 +69,8 @@ def scenario(n, jitter, planes, estimator="spe"):
         "excitations": {"hv": {"kind": "sinusoid", "amplitude": 4e4 / 0.012, "frequency": 50.0},
                         "ground": {"kind": "constant", "value": 0.0}},
         "solver": dict({"preconditioner": "amg", "rel_tol": 1e-12, "max_iter": 500},
-                       **({} if COARSE_FILTER is None else {"amg_coarse_filter": COARSE_FILTER})),
+                       **({} if COARSE_FILTER is None else {"amg_coarse_filter": COARSE_FILTER}),
+                       **({} if DENSE_COARSE is None else {"amg_dense_coarse": DENSE_COARSE})),
         "estimator": {"mode": estimator, "window": 8},
     }
 
@@ -512,6 +514,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--coarse-filter", type=float, default=None,
                     help="solver.amg_coarse_filter (V-cycle coarse-operator filter, DESIGN.md §4)")
+    ap.add_argument("--dense-coarse", type=int, default=None,
+                    help="solver.amg_dense_coarse (dense explicit-inverse solve from the first level with at "
+                         "most this many rows, DESIGN.md §4)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the in-run CPU baseline sample")
     ap.add_argument("--estimator", default="spe", choices=["zero", "previous", "spe"],
                     help="MRHS start vectors (proj/src/start_vector.cpp); the reference nonlinear scenario uses spe")
@@ -521,8 +526,9 @@ def main():
                     help="rkc: the headline line (default); euler: config 2 Euler vs RKC on --config (c2); "
                          "mrhs: config 5 multiple-right-hand-side sequence on --config")
     args = ap.parse_args()
-    global COARSE_FILTER
+    global COARSE_FILTER, DENSE_COARSE
     COARSE_FILTER = args.coarse_filter
+    DENSE_COARSE = args.dense_coarse
     if args.impl == "reference":
         run_reference(args)
     elif args.mode == "euler":

@@ -67,7 +67,7 @@ typedef struct {
   double mgs_drop_tol;    /* 1e-8 */
   double amg_coarse_filter; /* additive: V-cycle coarse-operator filter eps (0 = off; configs default 0.0025) */
   int amg_dense_coarse;     /* additive: direct (dense) solve of the first coarse level with at most this many
-                               rows in the device V-cycle; <= 0 (default) = recurse to the coarsest */
+                               rows in the device V-cycle; <= 0 = recurse to the coarsest (configs default 512) */
   /* start_vector.hpp:31-35 (POD modes); <= 0 selects the reference default */
   int pod_snapshots;        /* 40: pod_fixed solves collected before the basis is built */
   int pod_rank;             /* 10 */

@@ -79,9 +79,9 @@ struct SolverParams {
   int amg_sweeps = 1, amg_max_levels = 10, amg_coarse_limit = 64;
   double amg_coarse_filter = 0.0025;  // additive: V-cycle coarse-operator filter (0 = off)
   int amg_replicate_rows = 32768;     // additive: coarse levels up to this size are replicated on every rank
-  int amg_dense_coarse = 0;           // additive: the device V-cycle solves the first coarse level with at most
-                                      // this many rows directly (dense inverse); <= 0 (default): recurse to the
-                                      // hierarchy's coarsest
+  int amg_dense_coarse = 512;         // additive: the device V-cycle solves the first coarse level with at most
+                                      // this many rows directly (dense inverse); <= 0: recurse to the
+                                      // hierarchy's coarsest (configs default 512)
   int estimator_mode = 0;  // 0 zero, 1 previous, 2 spe, 3 pod_fixed, 4 pod_rolling
   int spe_window = 8;
   int pod_snapshots = 40;    // start_vector.hpp:31-35

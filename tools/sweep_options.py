@@ -29,8 +29,10 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--dense-coarse", type=int, default=None)
     ap.add_argument("variants", nargs="*", default=["default"])
     args = ap.parse_args()
+    bench.DENSE_COARSE = args.dense_coarse
     import torch
     import paper_1612_09447_b200 as eb
     import ctypes as C
