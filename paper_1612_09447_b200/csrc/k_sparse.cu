@@ -328,6 +328,95 @@ __global__ void k_lincomb_multi(int n, int kout, PtrPack in, PtrPack out, RotPac
   }
 }
 
+
+// Window kernels of the SPE / POD estimators, templated on the window size M
+// (loads unpredicated, accumulators and coefficients in registers) and run on
+// element pairs with 16-byte accesses when every vector is 16-byte aligned
+// (vec); the remaining elements take a scalar grid-stride loop.
+template <int M>
+__global__ void k_multi_dot_t(int n, PtrPack V, const double* __restrict__ w, Reducer red, int slot0, int vec) {
+  pdl_entry();
+  double acc[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) acc[k] = 0.0;
+  const long n2 = vec ? n / 2 : 0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (long)gridDim.x * kBlock) {
+    const double2 wi = reinterpret_cast<const double2*>(w)[i];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double2 v = reinterpret_cast<const double2*>(V.p[k])[i];
+      acc[k] += v.x * wi.x;
+      acc[k] += v.y * wi.y;
+    }
+  }
+  for (long i = 2 * n2 + (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    const double wi = w[i];
+#pragma unroll
+    for (int k = 0; k < M; ++k) acc[k] += V.p[k][i] * wi;
+  }
+#pragma unroll
+  for (int k = 0; k < M; ++k) reduce_finish(acc[k], red, slot0 + k);
+}
+
+template <int M, bool ACC>
+__global__ void k_lincomb_t(int n, PtrPack V, CoefPack c, double* __restrict__ y, int vec) {
+  pdl_entry();
+  const long n2 = vec ? n / 2 : 0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (long)gridDim.x * kBlock) {
+    double2 sacc = ACC ? reinterpret_cast<const double2*>(y)[i] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double2 v = reinterpret_cast<const double2*>(V.p[k])[i];
+      sacc.x += v.x * c.c[k];
+      sacc.y += v.y * c.c[k];
+    }
+    reinterpret_cast<double2*>(y)[i] = sacc;
+  }
+  for (long i = 2 * n2 + (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    double sv = ACC ? y[i] : 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) sv += V.p[k][i] * c.c[k];
+    y[i] = sv;
+  }
+}
+
+template <int M>
+__global__ void k_orth_update_t(int n, PtrPack Q, const double* __restrict__ dcoef, double* __restrict__ w,
+                                Reducer red, int slot, int vec) {
+  pdl_entry();
+  double c[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) c[k] = dcoef[k];
+  double acc = 0.0;
+  const long n2 = vec ? n / 2 : 0;
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (long)gridDim.x * kBlock) {
+    double2 sv = reinterpret_cast<const double2*>(w)[i];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double2 q = reinterpret_cast<const double2*>(Q.p[k])[i];
+      sv.x -= c[k] * q.x;
+      sv.y -= c[k] * q.y;
+    }
+    reinterpret_cast<double2*>(w)[i] = sv;
+    acc += sv.x * sv.x;
+    acc += sv.y * sv.y;
+  }
+  for (long i = 2 * n2 + (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    double sv = w[i];
+#pragma unroll
+    for (int k = 0; k < M; ++k) sv -= c[k] * Q.p[k][i];
+    w[i] = sv;
+    acc += sv * sv;
+  }
+  reduce_finish(acc, red, slot);
+}
+
+#define WIN_SWITCH_(m, X) \
+  switch (m) {            \
+    X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) \
+    default: throw std::invalid_argument("estimator window kernels: at most kMaxMulti vectors"); \
+  }
+
 // SDIRK Newton matrix values on the M_II pattern: k_e = sum of the element
 // contributions in ascending tet order from 0.0 (assemble_matrix), then
 // shifted_e = 1.0 m_e + gdt k_e (csr.cpp:168-195 with equal patterns)
@@ -535,24 +624,41 @@ void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, 
   launch_pdl(k_dot, red_grid(k_dot, n), kBlock, 0, s, n, a, b, red, slot);
 }
 void launch_multi_dot(int n, int m, const double* const* V, const double* w, Reducer red, int slot0, cudaStream_t s) {
+  if (m <= 0) return;
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
   bool vec = aligned16(w);
   for (int k = 0; k < m; ++k) vec = vec && aligned16(V[k]);
-  launch_pdl(k_multi_dot, red_grid(k_multi_dot, n), kBlock, 0, s, n, m, pk, w, red, slot0, vec ? 1 : 0);
+#define MD_(M)                                                                                                 \
+  case M:                                                                                                      \
+    launch_pdl(k_multi_dot_t<M>, red_grid(k_multi_dot_t<M>, n), kBlock, 0, s, n, pk, w, red, slot0, vec ? 1 : 0); \
+    break;
+  WIN_SWITCH_(m, MD_)
+#undef MD_
+}
+template <bool ACC>
+static void lincomb_any(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s) {
+  if (m <= 0) {
+    if (!ACC) launch_fill(n, 0.0, y, s);
+    return;
+  }
+  ++g_launch_count;
+  PtrPack pk{};
+  for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
+  bool vec = aligned16(y);
+  for (int k = 0; k < m; ++k) vec = vec && aligned16(V[k]);
+  const int g = grid_for(vec ? n / 2 + 1 : n);
+#define LC_(M)                                                                   \
+  case M: launch_pdl(k_lincomb_t<M, ACC>, g, kBlock, 0, s, n, pk, c, y, vec ? 1 : 0); break;
+  WIN_SWITCH_(m, LC_)
+#undef LC_
 }
 void launch_lincomb(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s) {
-  ++g_launch_count;
-  PtrPack pk{};
-  for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
-  launch_pdl(k_lincomb<false>, grid_for(n), kBlock, 0, s, n, m, pk, c, y);
+  lincomb_any<false>(n, m, V, c, y, s);
 }
 void launch_lincomb_acc(int n, int m, const double* const* V, CoefPack c, double* y, cudaStream_t s) {
-  ++g_launch_count;
-  PtrPack pk{};
-  for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
-  launch_pdl(k_lincomb<true>, grid_for(n), kBlock, 0, s, n, m, pk, c, y);
+  lincomb_any<true>(n, m, V, c, y, s);
 }
 void launch_orth_update(int n, int m, const double* const* Q, CoefPack c, double* w, Reducer red, int slot,
                         cudaStream_t s) {
@@ -566,7 +672,19 @@ void launch_orth_update_dev(int n, int m, const double* const* Q, const double* 
   ++g_launch_count;
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = Q[k];
-  launch_pdl(k_orth_update_dev, red_grid(k_orth_update_dev, n), kBlock, 0, s, n, m, pk, dcoef, w, red, slot);
+  if (m <= 0) {  // no projection: the pass only produces w.w
+    launch_pdl(k_orth_update_dev, red_grid(k_orth_update_dev, n), kBlock, 0, s, n, m, pk, dcoef, w, red, slot);
+    return;
+  }
+  bool vec = aligned16(w);
+  for (int k = 0; k < m; ++k) vec = vec && aligned16(Q[k]);
+#define OU_(M)                                                                                                  \
+  case M:                                                                                                       \
+    launch_pdl(k_orth_update_t<M>, red_grid(k_orth_update_t<M>, n), kBlock, 0, s, n, pk, dcoef, w, red, slot, \
+               vec ? 1 : 0);                                                                                    \
+    break;
+  WIN_SWITCH_(m, OU_)
+#undef OU_
 }
 void launch_scale_rsqrt(int n, const double* nrm2, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;
