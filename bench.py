@@ -440,8 +440,10 @@ def run_b200(args):
     # device time from CUDA events on the library stream, algorithmic bytes per launch
     names = ["stiffness K(x)x", "pcg spmv+vectors", "v-cycle", "rkc stage/error", "spe estimator", "boundary"]
     kernels = {0: "K(x)x blocked stiffness operator (k_kx_block<4> + k_kx_partials)",
-               1: "PCG fine-level M_II SpMV+dot (fp64 SELL-16, k_sell_red) and fused x/r update (k_pcg_update)",
-               2: "AMG V-cycle graph: packed SELL-P bf16 smoother/residual/transfer row kernels, all levels"}
+               1: "PCG fine-level M_II SpMV+dot (fp64 stencil-coded SELL-S k_sells64<0>; SELL-16 k_sell_red on "
+                  "unstructured meshes) and fused x/r update (k_pcg_update)",
+               2: "AMG V-cycle: stencil-coded SELL-S (fine level) and packed SELL-P (transfers, coarse levels) bf16 "
+                  "smoother/residual/transfer row kernels, dense coarse GEMV"}
 
     def roof(c):
         if not (timing["launches"][c] and timing["bytes"][c]):
