@@ -197,7 +197,8 @@ void launch_prolong_add(const DevCsr& p, const XT* zc, XT* z, cudaStream_t s);
 void launch_scaled_spmv(const DevCsr& a, const double* invd, const double* v, double* w, cudaStream_t s);
 
 // ---- PCG / dense (k_sparse.cu)
-// x += alpha p ; r -= alpha q ; slot_rr <- r.r ; alpha = scal[S_RZ]/scal[S_PQ]; r32 (optional) = (float) r
+// x += alpha p (skipped for x == nullptr) ; r -= alpha q ; slot_rr <- r.r ; alpha = scal[S_RZ]/scal[S_PQ];
+// r32 (optional) = (float) r
 // and d32 = invd32 .* r32 (the next fp32 V-cycle's inputs)
 void launch_pcg_update(int n, double* x, double* r, const double* p, const double* q, Reducer red, cudaStream_t s,
                        float* r32 = nullptr, const float* invd32 = nullptr, float* d32 = nullptr);
@@ -206,9 +207,13 @@ void launch_orth_update_dev(int n, int m, const double* const* Q, const double* 
                             int slot, cudaStream_t s);
 // y = x / sqrt(*nrm2)  (device-resident norm^2)
 void launch_scale_rsqrt(int n, const double* nrm2, const double* x, double* y, cudaStream_t s);
-// p = z + beta p, beta = scal[S_RZ]/scal[S_RZ_OLD]; p = z when stat && stat[0] == 0
+// p = z + beta p, beta = scal[S_RZ]/scal[S_RZ_OLD]; p = z when stat && stat[0] == 0;
+// x (optional): first x += (scal[S_RZ_OLD]/scal[S_PQ]) p, the update deferred from
+// the previous iteration (launch_pcg_update with x == nullptr)
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s,
-                          const double* stat = nullptr);
+                          const double* stat = nullptr, double* x = nullptr);
+// x += (scal[S_RZ]/scal[S_PQ]) p: the deferred update of the last iteration
+void launch_pcg_xfinal(int n, double* x, const double* p, const double* scal, cudaStream_t s);
 // Device-side PCG stopping rule (pcg.cpp:40-66) for the graph-resident
 // iteration loop. stat = [k, status, rel, pq, bnorm, tol, max_iter, rr0 (< 0:
 // read S_RR), initial rel]: advances

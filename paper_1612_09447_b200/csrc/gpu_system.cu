@@ -1234,13 +1234,15 @@ cudaGraphExec_t GpuSystem::pcg_loop_graph(double* x, bool f32) {
   CK(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   if (!f32) vcycle_prepare(r);
   double* z = vcycle(r);
-  launch_pcg_direction(n, p, z, red_scal_.p, stream_, pcg_stat_.p);
+  // x += alpha p of iteration k is applied by the direction kernel of
+  // iteration k+1 (which reads p anyway) or by k_pcg_xfinal after the loop
+  launch_pcg_direction(n, p, z, red_scal_.p, stream_, pcg_stat_.p, x);
   launch_spmv_dot(mii_, p, q, red_, S_PQ, stream_);
   DevLevel& f0 = levels_.empty() ? dummy_level_ : levels_[0];
   if (f32)
-    launch_pcg_update(n, x, r, p, q, red_, stream_, f0.b32.p, f0.invd32.p, f0.db32.p);
+    launch_pcg_update(n, nullptr, r, p, q, red_, stream_, f0.b32.p, f0.invd32.p, f0.db32.p);
   else
-    launch_pcg_update(n, x, r, p, q, red_, stream_);
+    launch_pcg_update(n, nullptr, r, p, q, red_, stream_);
   launch_pcg_check(red_scal_.p, pcg_stat_.p, handle, stream_);
   CK(cudaStreamEndCapture(stream_, &body));
   pcg_body_kernels_ = g_launch_count - body_before;
@@ -1298,6 +1300,9 @@ PcgResult GpuSystem::pcg_dev_graph(const double* b, bool use_x0, const double* x
   res.iterations = k_end;
   res.initial_rel_residual = st[8];
   res.rel_residual = st[2];
+  if (k_end >= 1 && (status == PCG_CONVERGED || status == PCG_MAX_ITER)) {
+    launch_pcg_xfinal(n, x, p, red_scal_.p, stream_);
+  }
   switch (status) {
     case PCG_CONVERGED: res.converged = true; return res;
     case PCG_BAD_INIT: throw NumericalError("pcg: non-finite initial residual");

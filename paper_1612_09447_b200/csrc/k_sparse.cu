@@ -69,7 +69,10 @@ __global__ void k_jacobi(int n, const double* __restrict__ invd, const double* _
 // d32 = invd32 .* r32 (its fine-level b and D^-1 b). VEC: pairs of entries per
 // thread with 16-byte loads (all arrays 16-byte aligned); the odd tail entry
 // is handled by thread 0.
-template <bool F32, bool VEC>
+// WX false (graph-resident loop): x is not touched here; its update by this
+// iteration's alpha p happens in the next direction kernel (or k_pcg_xfinal),
+// which reads p anyway.
+template <bool F32, bool VEC, bool WX>
 __global__ void __launch_bounds__(kBlock, 6)
     k_pcg_update(int n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                  const double* __restrict__ q, float* __restrict__ r32, const float* __restrict__ invd32,
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(kBlock, 6)
   const double alpha = red.scal[S_RZ] / red.scal[S_PQ];
   double acc = 0.0;
   auto one = [&](long i) {
-    x[i] += alpha * p[i];
+    if constexpr (WX) x[i] += alpha * p[i];
     const double ri = r[i] - alpha * q[i];
     r[i] = ri;
     if constexpr (F32) {
@@ -91,13 +94,17 @@ __global__ void __launch_bounds__(kBlock, 6)
   if constexpr (VEC) {
     const long n2 = n / 2;
     for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (long)gridDim.x * kBlock) {
-      const double2 pi = reinterpret_cast<const double2*>(p)[i], qi = reinterpret_cast<const double2*>(q)[i];
-      double2 xi = reinterpret_cast<double2*>(x)[i], ri = reinterpret_cast<double2*>(r)[i];
-      xi.x += alpha * pi.x;
-      xi.y += alpha * pi.y;
+      const double2 qi = reinterpret_cast<const double2*>(q)[i];
+      double2 ri = reinterpret_cast<double2*>(r)[i];
+      if constexpr (WX) {
+        const double2 pi = reinterpret_cast<const double2*>(p)[i];
+        double2 xi = reinterpret_cast<double2*>(x)[i];
+        xi.x += alpha * pi.x;
+        xi.y += alpha * pi.y;
+        reinterpret_cast<double2*>(x)[i] = xi;
+      }
       ri.x -= alpha * qi.x;
       ri.y -= alpha * qi.y;
-      reinterpret_cast<double2*>(x)[i] = xi;
       reinterpret_cast<double2*>(r)[i] = ri;
       if constexpr (F32) {
         const float2 w = reinterpret_cast<const float2*>(invd32)[i];
@@ -142,7 +149,8 @@ __global__ void k_to_f64_dot(int n, const float* __restrict__ z32, double* __res
 }
 
 __global__ void k_pcg_direction(int n, double* __restrict__ p, const double* __restrict__ z,
-                                const double* __restrict__ scal, const double* __restrict__ stat) {
+                                const double* __restrict__ scal, const double* __restrict__ stat,
+                                double* __restrict__ x) {
   pdl_entry();
   // graph-resident loop: before the first iteration (stat[0] == 0) p = z,
   // exactly the host loop's copy
@@ -151,8 +159,25 @@ __global__ void k_pcg_direction(int n, double* __restrict__ p, const double* __r
     return;
   }
   const double beta = scal[S_RZ] / scal[S_RZ_OLD];
+  if (x) {  // the previous iteration's x += alpha p (alpha = rz_old / pq), deferred from its update
+    const double alpha = scal[S_RZ_OLD] / scal[S_PQ];
+    for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+      const double pi = p[i];
+      x[i] += alpha * pi;
+      p[i] = z[i] + beta * pi;
+    }
+    return;
+  }
   for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock)
     p[i] = z[i] + beta * p[i];
+}
+
+// the last iteration's deferred x += alpha p (alpha = rz / pq)
+__global__ void k_pcg_xfinal(int n, double* __restrict__ x, const double* __restrict__ p,
+                             const double* __restrict__ scal) {
+  pdl_entry();
+  const double alpha = scal[S_RZ] / scal[S_PQ];
+  for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) x[i] += alpha * p[i];
 }
 
 // Initial residual test of the graph-resident loop (pcg.cpp:19-31): rr from
@@ -552,16 +577,20 @@ void launch_pcg_update(int n, double* x, double* r, const double* p, const doubl
                        float* r32, const float* invd32, float* d32) {
   ++g_launch_count;
   auto al = [](const void* ptr, int a) { return ((uintptr_t)ptr % a) == 0; };
-  const bool vec = al(x, 16) && al(r, 16) && al(p, 16) && al(q, 16) &&
+  const bool vec = (!x || al(x, 16)) && al(r, 16) && al(p, 16) && al(q, 16) &&
                    (!r32 || (al(r32, 8) && al(invd32, 8) && al(d32, 8)));
   const long work = vec ? std::max(1, n / 2) : n;
-#define U_(F, V) \
-  launch_pdl(k_pcg_update<F, V>, red_grid(k_pcg_update<F, V>, work), kBlock, 0, s, n, x, r, p, q, r32, invd32, d32, red)
+#define U_(F, V, W)                                                                                              \
+  launch_pdl(k_pcg_update<F, V, W>, red_grid(k_pcg_update<F, V, W>, work), kBlock, 0, s, n, x, r, p, q, r32, invd32, \
+             d32, red)
+#define UW_(F, V) \
+  if (x) U_(F, V, true); else U_(F, V, false);
   if (r32) {
-    if (vec) U_(true, true); else U_(true, false);
+    if (vec) { UW_(true, true) } else { UW_(true, false) }
   } else {
-    if (vec) U_(false, true); else U_(false, false);
+    if (vec) { UW_(false, true) } else { UW_(false, false) }
   }
+#undef UW_
 #undef U_
 }
 void launch_to_f32_scaled(long n, const double* x, const float* invd, float* y, float* d, cudaStream_t s) {
@@ -583,9 +612,13 @@ void launch_to_f64_dot(int n, const float* z32, double* z64, const double* b, Re
   launch_pdl(k_to_f64_dot, red_grid(k_to_f64_dot, n), kBlock, 0, s, n, z32, z64, b, rr, slot, red ? 1 : 0);
 }
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s,
-                          const double* stat) {
+                          const double* stat, double* x) {
   ++g_launch_count;
-  launch_pdl(k_pcg_direction, grid_for(n), kBlock, 0, s, n, p, z, scal, stat);
+  launch_pdl(k_pcg_direction, grid_for(n), kBlock, 0, s, n, p, z, scal, stat, x);
+}
+void launch_pcg_xfinal(int n, double* x, const double* p, const double* scal, cudaStream_t s) {
+  ++g_launch_count;
+  launch_pdl(k_pcg_xfinal, grid_for(n), kBlock, 0, s, n, x, p, scal);
 }
 void launch_pcg_check0(double* scal, double* stat, cudaGraphConditionalHandle h, cudaStream_t s) {
   ++g_launch_count;
