@@ -150,7 +150,7 @@ __global__ void k_to_f64_dot(int n, const float* __restrict__ z32, double* __res
 
 __global__ void k_pcg_direction(int n, double* __restrict__ p, const double* __restrict__ z,
                                 const double* __restrict__ scal, const double* __restrict__ stat,
-                                double* __restrict__ x) {
+                                double* __restrict__ x, int vec) {
   pdl_entry();
   // graph-resident loop: before the first iteration (stat[0] == 0) p = z,
   // exactly the host loop's copy
@@ -161,7 +161,16 @@ __global__ void k_pcg_direction(int n, double* __restrict__ p, const double* __r
   const double beta = scal[S_RZ] / scal[S_RZ_OLD];
   if (x) {  // the previous iteration's x += alpha p (alpha = rz_old / pq), deferred from its update
     const double alpha = scal[S_RZ_OLD] / scal[S_PQ];
-    for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
+    const long n2 = vec ? n / 2 : 0;  // element pairs, 16-byte accesses
+    for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (long)gridDim.x * kBlock) {
+      const double2 pi = reinterpret_cast<const double2*>(p)[i], zi = reinterpret_cast<const double2*>(z)[i];
+      double2 xi = reinterpret_cast<const double2*>(x)[i];
+      xi.x += alpha * pi.x;
+      xi.y += alpha * pi.y;
+      reinterpret_cast<double2*>(x)[i] = xi;
+      reinterpret_cast<double2*>(p)[i] = make_double2(zi.x + beta * pi.x, zi.y + beta * pi.y);
+    }
+    for (long i = 2 * n2 + (long)blockIdx.x * kBlock + threadIdx.x; i < n; i += (long)gridDim.x * kBlock) {
       const double pi = p[i];
       x[i] += alpha * pi;
       p[i] = z[i] + beta * pi;
@@ -614,7 +623,8 @@ void launch_to_f64_dot(int n, const float* z32, double* z64, const double* b, Re
 void launch_pcg_direction(int n, double* p, const double* z, const double* scal, cudaStream_t s,
                           const double* stat, double* x) {
   ++g_launch_count;
-  launch_pdl(k_pcg_direction, grid_for(n), kBlock, 0, s, n, p, z, scal, stat, x);
+  const bool vec = x && aligned16(x) && aligned16(p) && aligned16(z);
+  launch_pdl(k_pcg_direction, grid_for(vec ? n / 2 + 1 : n), kBlock, 0, s, n, p, z, scal, stat, x, vec ? 1 : 0);
 }
 void launch_pcg_xfinal(int n, double* x, const double* p, const double* scal, cudaStream_t s) {
   ++g_launch_count;
