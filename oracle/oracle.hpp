@@ -31,6 +31,43 @@
 
 namespace ora {
 
+// Sum of f(0..n-1) in the order of Eigen 3.4's LinearVectorizedTraversal
+// redux with SSE2 packets of 2 doubles (the default x86-64 build of the
+// reference, proj/CMakeLists.txt: Release, no -march): two packet
+// accumulators over blocks of 4, then the leftover packet, the horizontal
+// add and the scalar tail. Used for every Eigen dot/norm/squaredNorm the
+// reference calls (pcg.cpp, amg.cpp:28-45, integrators.cpp:56-65,
+// start_vector.cpp) so the restatement matches the compiled reference
+// (oracle/_ref, built against the same order in oracle/ref_shim/Eigen/Core)
+// bit for bit where it matters: the AMG hierarchy depends on omega through
+// borderline strength decisions.
+template <class F>
+inline double eigen_redux_sum(size_t n, F&& c) {
+  if (n == 0) return 0.0;
+  const size_t a2 = n / 4 * 4, a1 = n / 2 * 2;
+  if (a1 == 0) return c(0);
+  double p00 = c(0), p01 = c(1);
+  if (a1 > 2) {
+    double p10 = c(2), p11 = c(3);
+    for (size_t i = 4; i < a2; i += 4) {
+      p00 = p00 + c(i);
+      p01 = p01 + c(i + 1);
+      p10 = p10 + c(i + 2);
+      p11 = p11 + c(i + 3);
+    }
+    p00 = p00 + p10;
+    p01 = p01 + p11;
+    if (a1 > a2) {
+      p00 = p00 + c(a2);
+      p01 = p01 + c(a2 + 1);
+    }
+  }
+  double r = p00 + p01;
+  for (size_t i = a1; i < n; ++i) r = r + c(i);
+  return r;
+}
+
+
 using Vec = std::vector<double>;
 
 // proj/include/eqs/types.hpp:12

@@ -11,10 +11,8 @@
 namespace ora {
 
 namespace {
-double dot(const Vec& a, const Vec& b) {
-  double s = 0.0;
-  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
-  return s;
+double dot(const Vec& a, const Vec& b) {  // Eigen's a.dot(b) summation order
+  return eigen_redux_sum(a.size(), [&](size_t i) { return a[i] * b[i]; });
 }
 double norm(const Vec& a) { return std::sqrt(dot(a, a)); }
 }  // namespace
