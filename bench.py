@@ -12,10 +12,15 @@ summed over ranks); steps_per_s is reported beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4] [--impl b200|reference]
 
---impl reference times the CPU restatement of the reference (oracle/, the
-reference itself needs Eigen and cannot be built here) on a
-bounded sample of the same mesh family, with all host threads for the element
-kernel exactly like the reference (PCG/AMG serial, proj/src/matfree.cpp:105).
+--impl reference times the reference's own CPU implementation of the path:
+the unmodified reference sources compiled against an Eigen-API shim
+(oracle/_ref/libeqsref.so, built by `make -C oracle ref`; the oracle/ port is
+the fallback when that library is absent) on a bounded sample of the same mesh
+family, with all host threads for the element kernel exactly like the
+reference (PCG/AMG serial, proj/src/matfree.cpp:105).
+
+--gpus N outside torchrun re-launches itself under torch.distributed.run with N
+ranks (one per GPU, NCCL).
 """
 from __future__ import annotations
 
@@ -144,26 +149,124 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-# ------------------------------------------------------------------ CPU (oracle) leg
-def cpu_sample(steps, cores):
-    """Time the CPU restatement of the reference on the bounded sample; returns
-    (DOF-stage-updates/s, steps/s, description)."""
-    from oracle import pyoracle as po  # checker / baseline only (never the measured product)
+# ------------------------------------------------------------------ CPU (reference) leg
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return None
 
+
+class CpuArm:
+    """The reference's CPU path: oracle/_ref (unmodified reference sources,
+    kind "reference") when built, else the oracle/ restatement (kind "port").
+    Checker / baseline only, never the measured product."""
+
+    def __init__(self, cfg, cores):
+        from oracle import pyref as pr  # checker / baseline only
+        if pr.available():
+            self.kind, self.p = "reference", pr.RefProblem(cfg, workers=cores)
+        else:
+            from oracle import pyoracle as po
+            self.kind, self.p = "port", po.Problem(cfg, workers=cores)
+        self.n_free = self.p.n_free
+        self.t = 0.0
+        self.x = None
+
+    def spectral_radius(self, x):
+        return self.p.spectral_radius(0.0, x)
+
+    def set_state(self, t, x, dt):
+        self.t, self.x = t, np.array(x, dtype=np.float64, copy=True)
+        if self.kind == "reference":
+            self.p.set_state(t, self.x, dt)
+
+    def advance(self, dt, s, steps):
+        if self.kind == "reference":
+            self.p.rkc_advance_fixed(dt, s, steps)
+            self.x, self.t, _ = self.p.get_state()
+        else:
+            self.x = self.p.rkc_advance_fixed(self.t, self.x, dt, s, steps)
+            self.t += steps * dt
+
+    def iters_per_solve(self):
+        st = self.p.stats()
+        return st["pcg_iterations"] / max(1, st["m_solves"])
+
+    def describe(self, cores):
+        what = ("unmodified reference sources (proj/src) compiled against the Eigen-API shim oracle/ref_shim "
+                "(oracle/_ref/libeqsref.so, -O3, no -march)" if self.kind == "reference" else
+                "oracle/ C++ restatement of the reference (oracle/_ref not built)")
+        return (f"{what}; OpenMP element kernel with {cores} threads, serial PCG with the SGS-smoothed SA-AMG V-cycle "
+                f"as in the reference (proj/src/matfree.cpp:105-115)")
+
+
+def sample_x0_dt(arm):
+    from oracle import pyoracle as po  # random_vec: mt19937 uniform[-1,1) (test_helpers.hpp:15-21)
+    x0 = 2e4 * po.random_vec(arm.n_free, 31)
+    rho = arm.spectral_radius(x0)
+    return x0, 0.9 * 0.653 * (S_STAGES ** 2 - 1) / rho, rho
+
+
+def cpu_sample(steps, cores):
+    """Time the reference's CPU path on the bounded sample (48^3 cube of the C3
+    family) and keep its state for the parity check against the GPU."""
     cfg = scenario(CPU_SAMPLE["n"], 0.1, [0.45, 0.55])
-    cfg["workers"] = cores
-    o = po.Problem(cfg)
-    x = 2e4 * po.random_vec(o.n_free, 31)
-    rho = o.spectral_radius(0.0, x)
-    dt = 0.9 * 0.653 * (S_STAGES ** 2 - 1) / rho
+    arm = CpuArm(cfg, cores)
+    x0, dt, rho = sample_x0_dt(arm)
+    arm.set_state(0.0, x0, dt)
     t0 = time.perf_counter()
-    x = o.rkc_advance_fixed(0.0, x, dt, S_STAGES, steps)
+    arm.advance(dt, S_STAGES, steps)
     wall = time.perf_counter() - t0
-    dof_updates = o.n_free * S_STAGES * steps / wall
-    desc = (f"oracle (C++ restatement of the reference, -O3, OpenMP element kernel with {cores} threads, serial "
-            f"PCG/SGS-AMG as in the reference) on {CPU_SAMPLE['n']}^3 jittered cube of the C3 family "
-            f"({o.n_free} free dofs), {steps} RKC steps path B (s=4), stepping time only")
-    return dof_updates, steps / wall, desc
+    return {"value": arm.n_free * S_STAGES * steps / wall, "steps_per_s": steps / wall, "arm": arm, "x0": x0,
+            "dt": dt, "x": arm.x.copy(), "cfg": cfg, "iters": arm.iters_per_solve(),
+            "desc": (f"{arm.describe(cores)}; {CPU_SAMPLE['n']}^3 jittered cube of the C3 family ({arm.n_free} "
+                     f"free dofs), {steps} RKC steps path B (s=4, dt=0.9 beta(4)/rho), stepping time only")}
+
+
+def sample_parity(sample, steps, cores):
+    """GPU vs the reference on the CPU sample: same x0, dt and steps; the gate is
+    10x the reference's own response to a 1e-12 perturbation of x0 and to a
+    PCG tolerance of 1e-13 (tests/test_gpu_ref_parity.py)."""
+    import copy
+
+    import paper_1612_09447_b200 as eb
+    g = eb.FemSystem(sample["cfg"], device=0)
+    g.set_state(0.0, sample["x0"], sample["dt"])
+    g.rkc_advance_fixed(sample["dt"], S_STAGES, steps)
+    xg = g.get_state()[0]
+    g.close()
+    xr = sample["x"]
+    rel = float(np.linalg.norm(xg - xr) / np.linalg.norm(xr))
+    pert = CpuArm(sample["cfg"], cores)
+    pert.set_state(0.0, sample["x0"] * (1 + 1e-12), sample["dt"])
+    pert.advance(sample["dt"], S_STAGES, steps)
+    sens = float(np.linalg.norm(pert.x - xr) / np.linalg.norm(xr))
+    tight_cfg = copy.deepcopy(sample["cfg"])
+    tight_cfg["solver"]["rel_tol"] = 1e-13
+    tight = CpuArm(tight_cfg, cores)
+    tight.set_state(0.0, sample["x0"], sample["dt"])
+    tight.advance(sample["dt"], S_STAGES, steps)
+    sens_tol = float(np.linalg.norm(tight.x - xr) / np.linalg.norm(xr))
+    gate = 10.0 * max(sens, sens_tol, 1e-13)
+    return {"sample": f"{CPU_SAMPLE['n']}^3 C3-family cube, x0 = 2e4 random_vec(31), {steps} RKC steps path B",
+            "against": sample["arm"].kind, "rel_l2_gpu_vs_reference": rel,
+            "reference_response_1e-12_x0": sens, "reference_response_tol_1e-13": sens_tol, "gate": gate,
+            "pass": rel <= gate}
+
+
+def c3_cpu_record():
+    """The committed full-size C3 measurement of the reference's CPU path
+    (tools/cpu_c3_baseline.py -> profiles/CPU_r2_c3.json), if present."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "CPU_r2_c3.json")) as f:
+            return json.load(f)
+    except OSError:
+        return None
 
 
 def run_reference(args):
@@ -171,33 +274,32 @@ def run_reference(args):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    from oracle import pyoracle as po
     cfg = scenario(CPU_SAMPLE["n"], 0.1, [0.45, 0.55])
-    cfg["workers"] = cores
-    o = po.Problem(cfg)
-    x = 2e4 * po.random_vec(o.n_free, 31)
-    rho = o.spectral_radius(0.0, x)
-    dt = 0.9 * 0.653 * (S_STAGES ** 2 - 1) / rho
-    t = 0.0
+    arm = CpuArm(cfg, cores)
+    x0, dt, _ = sample_x0_dt(arm)
+    arm.set_state(0.0, x0, dt)
     for _ in range(args.warmup):
-        x = o.rkc_advance_fixed(t, x, dt, S_STAGES, 1)
-        t += dt
+        arm.advance(dt, S_STAGES, 1)
+    it0 = arm.p.stats()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        x = o.rkc_advance_fixed(t, x, dt, S_STAGES, 1)
-        t += dt
+        arm.advance(dt, S_STAGES, 1)
     wall = time.perf_counter() - t0
-    value = o.n_free * S_STAGES * args.steps / wall
-    sample = (f"{CPU_SAMPLE['n']}^3 jittered cube of the C3 family ({o.n_free} free dofs), RKC path B s=4, "
+    it1 = arm.p.stats()
+    value = arm.n_free * S_STAGES * args.steps / wall
+    sample = (f"{CPU_SAMPLE['n']}^3 jittered cube of the C3 family ({arm.n_free} free dofs), RKC path B s=4, "
               f"{args.steps} timed steps after {args.warmup} warm-up")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "steps_per_s": args.steps / wall, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cpu sample of {args.config}: {sample}", "n_free": o.n_free},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": "oracle/ C++ restatement (reference unbuildable: Eigen3 absent); " + sample},
+        "config": {"workload": f"cpu sample of {args.config}: {sample}", "n_free": arm.n_free},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": arm.kind, "cpu_model": cpu_model(),
+                         "sample": arm.describe(cores) + "; " + sample,
+                         "pcg_iters_per_solve": (it1["pcg_iterations"] - it0["pcg_iterations"])
+                         / max(1, it1["m_solves"] - it0["m_solves"])},
+        "c3_full_size_record": c3_cpu_record(),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -462,23 +564,37 @@ def run_b200(args):
     cls = max(range(3), key=lambda c: timing["ms"][c])
     dom = roof(cls)
     others = {names[c]: roof(c) for c in range(3) if c != cls}
-    cpu = None
+    n_tets, nnz_mass, amg_levels = g.n_tets, g.nnz_mass_free, g.amg_levels()
+    cpu = parity = None
     if world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
-        cv, csps, desc = cpu_sample(CPU_SAMPLE["steps"], cores)
-        cpu = {"value": cv, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
+        g.close()  # free the C3 system before the sample's GPU parity run
+        smp = cpu_sample(CPU_SAMPLE["steps"], cores)
+        cpu = {"value": smp["value"], "unit": UNIT, "cores": cores, "kind": smp["arm"].kind,
+               "cpu_model": cpu_model(), "pcg_iters_per_solve": smp["iters"], "sample": smp["desc"],
+               "c3_full_size_record": c3_cpu_record()}
+        parity = sample_parity(smp, CPU_SAMPLE["steps"], cores)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "steps_per_s": 1e3 * args.steps / ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated mesh + mt19937 initial state; no dataset)",
         "config": {"workload": f"{args.config}: {spec['n']}^3 {'jittered ' if spec['jitter'] else ''}unit cube, "
-                               f"{n} free dofs, {g.n_tets} tets, microvaristor layer z in {spec['planes']}, "
+                               f"{n} free dofs, {n_tets} tets, microvaristor layer z in {spec['planes']}, "
                                f"RKC path B s={S_STAGES} dt=0.9*beta(4)/rho (={dt:.4g}s), "
                                f"estimator {args.estimator} + AMG-PCG 1e-12",
                    "estimator": args.estimator,
-                   "n_free": n, "n_tets": g.n_tets, "nnz_mass_free": g.nnz_mass_free,
-                   "amg_levels": g.amg_levels(),
+                   "n_free": n, "n_tets": n_tets, "nnz_mass_free": nnz_mass,
+                   "amg_levels": amg_levels,
+                   "precision": {
+                       "operator_pcg_and_result": "fp64: M_II (fp64 stencil-coded SELL-S, same products and row "
+                                                  "order as CsrMatrix::apply), PCG vectors, dots, stopping rule "
+                                                  "rel_tol 1e-12, K(x)x, RKC stages",
+                       "vcycle_preconditioner": "bf16 matrix values (packed SELL-S/SELL-P), fp32 vectors, "
+                                                "Chebyshev(2) fine / (1) coarse smoothing instead of SGS (DESIGN.md "
+                                                "§4.1-4.2)",
+                       "coarse_filter_eps": COARSE_FILTER if COARSE_FILTER is not None else 0.0025,
+                       "dense_coarse_rows": DENSE_COARSE if DENSE_COARSE is not None else 512},
                    "parallelism": (f"node-ownership partition over {world} GPUs (owner-computes K(x)x, halo "
                                    f"SpMV + NCCL allreduce per level, small coarse levels replicated)")
                    if world > 1 else "single GPU",
@@ -501,6 +617,8 @@ def run_b200(args):
         "time_by_class_source": "CUDA events per kernel class in a second pass of K steps after the timed region",
         "bytes_by_class": {names[c]: timing["bytes"][c] for c in range(6)},
         "cpu_baseline": cpu,
+        "parity": parity,
+        "parity_rel": parity["rel_l2_gpu_vs_reference"] if parity else None,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -528,6 +646,15 @@ def main():
                     help="rkc: the headline line (default); euler: config 2 Euler vs RKC on --config (c2); "
                          "mrhs: config 5 multiple-right-hand-side sequence on --config")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (127.0.0.1 rendezvous)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     global COARSE_FILTER, DENSE_COARSE
     COARSE_FILTER = args.coarse_filter
     DENSE_COARSE = args.dense_coarse
