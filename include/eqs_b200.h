@@ -190,6 +190,21 @@ int eqs_get_sizes(eqs_ctx* ctx, eqs_sizes* out);
 int eqs_nccl_unique_id(char* id128);
 int eqs_create_distributed(const char* json_text, int device, int nranks, int rank, const char* id128,
                            eqs_ctx** out);
+/* One process per rank on one node, halos and allreduces host-staged through
+ * a POSIX shared-memory segment `shm_name` (same name on every rank, e.g.
+ * "/eqs_<uuid>"): the backend for ranks that share a GPU or where NCCL is
+ * unavailable. Deterministic (rank-order sums, bit-identical to the
+ * virtual-rank group). Not graph-capturable: PCG keeps the host loop. */
+int eqs_create_distributed_shm(const char* json_text, int device, int nranks, int rank, const char* shm_name,
+                               eqs_ctx** out);
+/* The same transport on host buffers, without a GPU (tests of the protocol). */
+typedef struct eqs_comm eqs_comm;
+int eqs_comm_open_shm(const char* shm_name, int nranks, int rank, eqs_comm** out);
+void eqs_comm_close(eqs_comm* c);
+int eqs_comm_barrier(eqs_comm* c);
+int eqs_comm_allreduce_host(eqs_comm* c, double* buf, int count);
+int eqs_comm_exchange_host(eqs_comm* c, int n_msgs, const int* peers, const double* const* send,
+                           const int* send_counts, double* const* recv, const int* recv_counts);
 /* nranks virtual ranks in one process (threads, device-to-device halos);
  * every later call on these contexts must be made concurrently from one
  * thread per rank. Used to test the partitioned path on a single GPU. */
@@ -327,7 +342,8 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * PCG iteration loop (0/1; default 1: iterations 2.. run inside one CUDA graph
  * with a device-side stopping rule, no host round trip per iteration),
  * 21 = programmatic dependent launch of the row/vector kernels (0/1; default 1;
- * process-wide),
+ * process-wide), 22 = the graph-resident PCG loop on multi-rank NCCL contexts
+ * too (0/1; default 0: halo and allreduce calls captured into the loop body),
  * 13 = smoother polynomial (0 first-kind Chebyshev, 1 fourth-kind, 2 fourth-kind
  * with optimised weights), 14 = lambda_max safety factor (default 1.1).
  * The PCG operator and vectors are fp64 in every setting. */

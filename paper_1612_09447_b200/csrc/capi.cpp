@@ -202,6 +202,48 @@ int eqs_create_distributed(const char* json_text, int device, int nranks, int ra
   });
 }
 
+int eqs_create_distributed_shm(const char* json_text, int device, int nranks, int rank, const char* shm_name,
+                               eqs_ctx** out) {
+  return guard([&] {
+    if (!json_text || !out || !shm_name) throw std::invalid_argument("eqs_create_distributed_shm: null argument");
+    SimConfig c = parse_config(json_text);
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    std::unique_ptr<Comm> comm = make_shm_comm(shm_name, nranks, rank);
+    auto ctx = std::make_unique<eqs_ctx>();
+    ctx->sys = std::make_unique<GpuSystem>(build_problem(c), device, std::move(comm));
+    *out = ctx.release();
+  });
+}
+
+struct eqs_comm {
+  std::unique_ptr<Comm> comm;
+};
+
+int eqs_comm_open_shm(const char* shm_name, int nranks, int rank, eqs_comm** out) {
+  return guard([&] {
+    if (!shm_name || !out) throw std::invalid_argument("eqs_comm_open_shm: null argument");
+    auto c = std::make_unique<eqs_comm>();
+    c->comm = make_shm_comm(shm_name, nranks, rank);
+    *out = c.release();
+  });
+}
+void eqs_comm_close(eqs_comm* c) { delete c; }
+int eqs_comm_barrier(eqs_comm* c) {
+  return guard([&] { c->comm->barrier(); });
+}
+int eqs_comm_allreduce_host(eqs_comm* c, double* buf, int count) {
+  return guard([&] { shm_allreduce_host(*c->comm, buf, count); });
+}
+int eqs_comm_exchange_host(eqs_comm* c, int n_msgs, const int* peers, const double* const* send,
+                           const int* send_counts, double* const* recv, const int* recv_counts) {
+  return guard([&] {
+    std::vector<HaloMsg> msgs;
+    for (int k = 0; k < n_msgs; ++k)
+      msgs.push_back({peers[k], send[k], send_counts[k], recv[k], recv_counts[k], 8});
+    shm_exchange_host(*c->comm, msgs);
+  });
+}
+
 int eqs_create_virtual_group(const char* json_text, int device, int nranks, eqs_ctx** out) {
   return guard([&] {
     if (!json_text || !out || nranks < 1) throw std::invalid_argument("eqs_create_virtual_group: bad argument");
@@ -642,6 +684,7 @@ int eqs_set_option(eqs_ctx* ctx, int key, double value) {
       case 19: g.set_stencil(value != 0.0); break;
       case 20: g.pcg_graph_loop = value != 0.0; g.invalidate_graphs(); break;
       case 21: g_pdl = value != 0.0; g.invalidate_graphs(); break;
+      case 22: g.pcg_graph_multi = value != 0.0; g.invalidate_graphs(); break;
       default: throw std::invalid_argument("eqs_set_option: unknown key");
     }
   });

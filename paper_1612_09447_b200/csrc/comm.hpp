@@ -6,6 +6,12 @@
 //  * ThreadComm — P "virtual ranks" (threads) in one process, partitions on
 //                 any devices, exchange by device-to-device copies with host
 //                 barriers. Used to test the partitioned algorithm on one GPU.
+//  * ShmComm    — P processes on one node, host-staged through a POSIX shared
+//                 memory segment (process-shared atomics for the barrier).
+//                 Not capturable; runs where NCCL cannot (several ranks on one
+//                 GPU, no GPU at all for the host-buffer test entry points).
+//                 Allreduces sum in rank order, like ThreadComm, so the two
+//                 give bit-identical results.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -75,6 +81,13 @@ class StaticComm final : public Comm {
 struct ThreadGroup;
 std::shared_ptr<ThreadGroup> make_thread_group(int nranks);
 std::unique_ptr<Comm> make_thread_comm(std::shared_ptr<ThreadGroup> g, int rank);
+
+// host-staged multi-process backend; every rank passes the same segment name
+// (rank 0 creates it, all ranks attach, rank 0 unlinks once all attached)
+std::unique_ptr<Comm> make_shm_comm(const std::string& name, int nranks, int rank);
+// the same transport on host buffers (CPU tests of the exchange protocol)
+void shm_allreduce_host(Comm& c, double* buf, int count);
+void shm_exchange_host(Comm& c, const std::vector<HaloMsg>& msgs);
 
 // NCCL: id is the 128-byte ncclUniqueId from nccl_unique_id() on rank 0
 std::string nccl_unique_id();

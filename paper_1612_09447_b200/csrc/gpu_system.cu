@@ -1233,16 +1233,19 @@ cudaGraphExec_t GpuSystem::pcg_loop_graph(double* x, bool f32) {
   const double body_bytes_before = g_algo_bytes;
   CK(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   if (!f32) vcycle_prepare(r);
-  double* z = vcycle(r);
+  double* z = vcycle(r);  // r.z allreduced inside on several ranks
   // x += alpha p of iteration k is applied by the direction kernel of
   // iteration k+1 (which reads p anyway) or by k_pcg_xfinal after the loop
   launch_pcg_direction(n, p, z, red_scal_.p, stream_, pcg_stat_.p, x);
+  halo(halo0_, p);  // no-ops on one rank; NCCL calls on a multi-rank context
   launch_spmv_dot(mii_, p, q, red_, S_PQ, stream_);
+  allreduce(S_PQ);
   DevLevel& f0 = levels_.empty() ? dummy_level_ : levels_[0];
   if (f32)
     launch_pcg_update(n, nullptr, r, p, q, red_, stream_, f0.b32.p, f0.invd32.p, f0.db32.p);
   else
     launch_pcg_update(n, nullptr, r, p, q, red_, stream_);
+  allreduce(S_RR);
   launch_pcg_check(red_scal_.p, pcg_stat_.p, handle, stream_);
   CK(cudaStreamEndCapture(stream_, &body));
   pcg_body_kernels_ = g_launch_count - body_before;
@@ -1331,8 +1334,11 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
   // The iteration runs as one CUDA graph (pcg_loop_graph) when the V-cycle
   // is capturable and no per-class timing is requested; the decisions are the
   // same tests on the same scalars, evaluated on the device.
+  // multi-rank: only on capturable (NCCL) communicators, whose halo and
+  // allreduce calls are captured into the loop body
   const bool graph_loop = pcg_graph_loop && use_graphs && !timing_on && prob_.solver.precond == 2 &&
-                          comm_->size() == 1 && comm_->capturable() && device_ >= 0 && max_iter >= 1;
+                          comm_->capturable() && device_ >= 0 && max_iter >= 1 &&
+                          (comm_->size() == 1 || pcg_graph_multi);
   launch_dot(n, b, b, red_, S_BB, stream_);
   allreduce(S_BB);
   if (x0) {  // S_X0X0 follows S_BB: one read for both

@@ -213,6 +213,10 @@ class GpuSystem {
   double cheb_scale = 1.1;    // lmax = cheb_scale x the power estimate of lambda_max(D^-1 A)
   bool use_graphs = true;
   bool pcg_graph_loop = true;  // eqs_set_option 20
+  // eqs_set_option 22: the graph-resident PCG loop also on multi-rank NCCL
+  // contexts (halo + allreduces captured into the WHILE body). Off by default:
+  // NCCL inside a conditional graph body has not run on multi-GPU hardware.
+  bool pcg_graph_multi = false;
   bool spe_incremental = true;  // false: the reference's full MGS rebuild on every solve
   void set_cheb(double ratio);
   void set_vcycle_precision(int prec);  // V-cycle matrix values: 0 fp64, 1 fp32, 2 bf16

@@ -116,6 +116,8 @@ def load_library():
         L.eqs_destroy.restype = None
         L.eqs_destroy.argtypes = [C.c_void_p]
         L.eqs_launch_count.restype = C.c_long
+        L.eqs_comm_close.restype = None
+        L.eqs_comm_close.argtypes = [C.c_void_p]
         for fn in ("eqs_eval_rhs", "eqs_eval_residual", "eqs_apply_minv_stiffness", "eqs_lift_full",
                    "eqs_set_state", "eqs_mass_solve", "eqs_rkc_advance_fixed", "eqs_euler_step",
                    "eqs_set_option"):
@@ -202,6 +204,16 @@ class FemSystem:
         _check(load_library().eqs_create_distributed(text.encode(), C.c_int(device), C.c_int(nranks),
                                                      C.c_int(rank), C.create_string_buffer(nccl_id, 128),
                                                      C.byref(h)))
+        return cls(None, _handle=h)
+
+    @classmethod
+    def distributed_shm(cls, config, device: int, nranks: int, rank: int, shm_name: str):
+        """One rank of a multi-process run whose halos and allreduces are host-staged
+        through the POSIX shared-memory segment `shm_name` (same on every rank)."""
+        text = config if isinstance(config, str) else json.dumps(config)
+        h = C.c_void_p()
+        _check(load_library().eqs_create_distributed_shm(text.encode(), C.c_int(device), C.c_int(nranks),
+                                                         C.c_int(rank), shm_name.encode(), C.byref(h)))
         return cls(None, _handle=h)
 
     @classmethod
@@ -464,6 +476,42 @@ class FemSystem:
 
     def timing_reset(self):
         _check(load_library().eqs_timing_reset(self._h))
+
+
+class ShmComm:
+    """The shared-memory transport on host buffers (no GPU needed): the
+    exchange/allreduce protocol of eqs_create_distributed_shm."""
+
+    def __init__(self, shm_name: str, nranks: int, rank: int):
+        self._h = C.c_void_p()
+        _check(load_library().eqs_comm_open_shm(shm_name.encode(), C.c_int(nranks), C.c_int(rank),
+                                                C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            load_library().eqs_comm_close(self._h)
+            self._h = None
+
+    def barrier(self):
+        _check(load_library().eqs_comm_barrier(self._h))
+
+    def allreduce(self, a: np.ndarray) -> np.ndarray:
+        a = np.ascontiguousarray(a, dtype=np.float64).copy()
+        _check(load_library().eqs_comm_allreduce_host(self._h, _dp(a), C.c_int(a.size)))
+        return a
+
+    def exchange(self, sends: dict, recv_counts: dict) -> dict:
+        """sends: peer -> float64 array; recv_counts: peer -> count. Returns peer -> received array."""
+        peers = sorted(set(sends) | set(recv_counts))
+        recv = {p: np.zeros(recv_counts.get(p, 0)) for p in peers}
+        snd = [np.ascontiguousarray(sends.get(p, np.zeros(0)), dtype=np.float64) for p in peers]
+        n = len(peers)
+        P = C.POINTER(C.c_double)
+        _check(load_library().eqs_comm_exchange_host(
+            self._h, C.c_int(n), (C.c_int * n)(*peers), (P * n)(*[_dp(a) for a in snd]),
+            (C.c_int * n)(*[a.size for a in snd]), (P * n)(*[_dp(recv[p]) for p in peers]),
+            (C.c_int * n)(*[recv[p].size for p in peers])))
+        return recv
 
 
 def nccl_unique_id() -> bytes:

@@ -135,3 +135,60 @@ def test_world_size_2_gloo_halo_lists_agree():
     out = mgr.dict()
     mp.spawn(_gloo_worker, args=(2, port, cube(8, jitter=0.1), out), nprocs=2, join=True)
     assert out[0] and out[1]
+
+
+def _shm_worker(rank, world, port, name, cfg, out):
+    """One OS process per rank: the partition plan's numeric halo exchange and
+    the dot-product allreduce through the shared-memory transport of
+    eqs_create_distributed_shm (host buffers, no GPU), checked against the
+    global vector and against a gloo allreduce of the same partials."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = eb.eqs.ShmComm(name, world, rank)
+    try:
+        plan = eb.FemSystem.partition_host(cfg, world, rank).partition(0)
+        owner, owned, ghosts = plan["owner"], plan["owned"], plan["ghosts"]
+        g = np.sin(0.37 * np.arange(owner.size)) * 1e3  # the global vector
+        sends = {q: g[ids] for q, ids in plan["sends"].items()}
+        recv_counts = {q: int(np.sum(owner[ghosts] == q)) for q in range(world) if q != rank}
+        got = comm.exchange(sends, recv_counts)
+        ok = True
+        for q, vals in got.items():
+            ok = ok and np.array_equal(vals, g[ghosts[owner[ghosts] == q]])
+        # allreduce: rank-order sum of the owned partial dots (deterministic)
+        part = np.array([float(np.dot(g[owned], g[owned])), float(owned.size)])
+        tot = comm.allreduce(part)
+        allp = [None] * world
+        dist.all_gather_object(allp, part.tolist())
+        expect = np.zeros(2)
+        for p in allp:
+            expect += np.array(p)
+        ok = ok and np.array_equal(tot, expect) and tot[1] == owner.size
+        t = torch.tensor(part)
+        dist.all_reduce(t)  # gloo: the same sum up to summation order
+        ok = ok and abs(float(t[0]) - tot[0]) <= 1e-12 * tot[0] and np.isclose(tot[0], np.dot(g, g), rtol=1e-12)
+        comm.barrier()
+        out[rank] = bool(ok)
+    finally:
+        comm.close()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shm_transport_halo_and_allreduce_multiprocess(world):
+    import uuid
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    name = f"/eqs_test_{uuid.uuid4().hex[:12]}"
+    mp.spawn(_shm_worker, args=(world, port, name, cube(8, jitter=0.1), out), nprocs=world, join=True)
+    assert all(out[r] for r in range(world))
