@@ -722,6 +722,7 @@ void GpuSystem::invalidate_graphs() {
   vcycle_graph_ = nullptr;
   for (auto& kv : pcg_graphs_) cudaGraphExecDestroy(kv.second);
   pcg_graphs_.clear();
+  pcg_graph_use_.clear();
 }
 
 void GpuSystem::set_level_tpr(int level, int tpr) {
@@ -1200,11 +1201,24 @@ double* GpuSystem::precondition(double* r, bool prepared) {
 // computes the same values; the host reads the verdict once per solve.
 cudaGraphExec_t GpuSystem::pcg_loop_graph(double* x, bool f32) {
   auto it = pcg_graphs_.find(x);
-  if (it != pcg_graphs_.end()) return it->second;
-  if (pcg_graphs_.size() >= 8) {  // bounded cache (callers with many distinct x buffers)
-    for (auto& kv : pcg_graphs_) cudaGraphExecDestroy(kv.second);
-    pcg_graphs_.clear();
+  if (it != pcg_graphs_.end()) {
+    pcg_graph_use_[x] = ++pcg_graph_clock_;
+    return it->second;
   }
+  if (pcg_graphs_.size() >= 8) {  // bounded cache: evict the least recently used graph
+    double* lru = nullptr;
+    long oldest = -1;
+    for (auto& kv : pcg_graph_use_)
+      if (oldest < 0 || kv.second < oldest) {
+        oldest = kv.second;
+        lru = kv.first;
+      }
+    cudaGraphExecDestroy(pcg_graphs_[lru]);
+    pcg_graphs_.erase(lru);
+    pcg_graph_use_.erase(lru);
+  }
+  ++pcg_graph_captures;  // counted: a caller cycling through many x buffers re-captures
+  pcg_graph_use_[x] = ++pcg_graph_clock_;
   const int n = n_own_;
   double* r = w_r_.p;
   double* p = w_p_.p;
@@ -1967,6 +1981,9 @@ void GpuSystem::estimator_feedback(const double* x, int iterations) {
   }
   CK(cudaMemcpyAsync(buf, x, sizeof(double) * n_own_, cudaMemcpyDeviceToDevice, stream_));
   history_.push_back(buf);
+  // with the incremental basis switched off the window changed without the
+  // basis following it: the next next() must rebuild
+  if (mode == 2 && !spe_incremental) spe_clean_ = false;
   if (mode == 2 && spe_clean_ && spe_incremental) {
     if (window > (size_t)(kMaxWin - 1)) {
       spe_clean_ = false;  // large windows always use the full rebuild

@@ -331,6 +331,13 @@ class GpuSystem {
   // conditional node whose body is one iteration (V-cycle, direction, SpMV+dot,
   // update, device stopping rule)
   std::unordered_map<double*, cudaGraphExec_t> pcg_graphs_;
+  std::unordered_map<double*, long> pcg_graph_use_;  // LRU clock per cached graph
+  long pcg_graph_clock_ = 0;
+
+ public:
+  long pcg_graph_captures = 0;  // whole-PCG graph (re)captures (stats: a cache-thrash signal)
+
+ private:
   long pcg_body_kernels_ = 0;
   double pcg_body_bytes_ = 0.0;
   DevBuf<double> pcg_stat_;

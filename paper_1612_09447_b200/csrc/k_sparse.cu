@@ -93,15 +93,21 @@ __global__ void __launch_bounds__(kBlock, 6)
   };
   if constexpr (VEC) {
     const long n2 = n / 2;
+    const bool x_al = ((uintptr_t)x & 15) == 0;
     for (long i = (long)blockIdx.x * kBlock + threadIdx.x; i < n2; i += (long)gridDim.x * kBlock) {
       const double2 qi = reinterpret_cast<const double2*>(q)[i];
       double2 ri = reinterpret_cast<double2*>(r)[i];
       if constexpr (WX) {
         const double2 pi = reinterpret_cast<const double2*>(p)[i];
-        double2 xi = reinterpret_cast<double2*>(x)[i];
-        xi.x += alpha * pi.x;
-        xi.y += alpha * pi.y;
-        reinterpret_cast<double2*>(x)[i] = xi;
+        if (x_al) {
+          double2 xi = reinterpret_cast<double2*>(x)[i];
+          xi.x += alpha * pi.x;
+          xi.y += alpha * pi.y;
+          reinterpret_cast<double2*>(x)[i] = xi;
+        } else {  // a caller's 8-byte-aligned x: same values, scalar accesses
+          x[2 * i] += alpha * pi.x;
+          x[2 * i + 1] += alpha * pi.y;
+        }
       }
       ri.x -= alpha * qi.x;
       ri.y -= alpha * qi.y;
@@ -586,8 +592,10 @@ void launch_pcg_update(int n, double* x, double* r, const double* p, const doubl
                        float* r32, const float* invd32, float* d32) {
   ++g_launch_count;
   auto al = [](const void* ptr, int a) { return ((uintptr_t)ptr % a) == 0; };
-  const bool vec = (!x || al(x, 16)) && al(r, 16) && al(p, 16) && al(q, 16) &&
-                   (!r32 || (al(r32, 8) && al(invd32, 8) && al(d32, 8)));
+  // the paired path (and so the r.r summation order) is chosen from r/p/q
+  // only: the host loop (x given) and the graph loop (x deferred) must sum
+  // r.r identically whatever the caller's x alignment
+  const bool vec = al(r, 16) && al(p, 16) && al(q, 16) && (!r32 || (al(r32, 8) && al(invd32, 8) && al(d32, 8)));
   const long work = vec ? std::max(1, n / 2) : n;
 #define U_(F, V, W)                                                                                              \
   launch_pdl(k_pcg_update<F, V, W>, red_grid(k_pcg_update<F, V, W>, work), kBlock, 0, s, n, x, r, p, q, r32, invd32, \
