@@ -80,6 +80,12 @@ struct DevSellS {
   const unsigned char* pid = nullptr;    // [n_chunks * 32]
   const int* pat = nullptr;              // [P][8 G]
   const double* vals64 = nullptr;        // [n_chunks][8 G][32] fp64 values (PCG operator) or null
+  // symmetric half storage (sell.hpp SELL-SH); used instead of vals/vals64 when sym
+  bool sym = false;
+  const uint16_t* u16 = nullptr;         // [n_chunks][8][32] bf16 upper values
+  const double* u64 = nullptr;           // [n_chunks][8][32] fp64 upper values
+  const unsigned char* spid = nullptr;   // [n_chunks * 32] pattern | 0x80 (fast row)
+  const int* sinfo = nullptr;            // [P][16] slot kinds
 };
 
 // CSR matrix resident in HBM (int32 indices, fp64 values, sorted columns),

@@ -110,6 +110,11 @@ struct Problem {
 // ----------------------------------------------------------------- setup
 // color_elements (proj/src/matfree.cpp:11-38), bit-exact, returns colour per tet.
 std::vector<int> color_elements(const Dofs& dm, int n_tets, int* n_colors);
+// the same colouring on a GPU (k_setup.cu: topological waves over the earlier-neighbour DAG)
+std::vector<int> dev_color_elements(const Dofs& dm, int n_tets, int* n_colors, int device, int* waves = nullptr);
+// owner rank of every free dof from its partition-axis coordinate: stable radix
+// sort on the GPU, contiguous equal chunks (partition_free_dofs, k_setup.cu)
+std::vector<int> dev_partition_owner(const std::vector<double>& key, int nranks, int device);
 // assemble_mass (proj/src/assembly.cpp:130-176) + split_dirichlet (:188-193).
 void assemble_mass_blocks(const Problem& p, HostCsr& m_ii, HostCsr& m_ib);
 
@@ -143,6 +148,12 @@ class AmgDeviceBuilder {
                       long long batch);
   // R (A P) with A and P resident; the result becomes the next fine operator
   HostCsr galerkin(const HostCsr& r, long long batch);
+  // One whole level of build_amg on the device (amg.cpp:99-137): strength
+  // graph + aggregation, P_tent, lambda_max, smoothed P, R = P^T, R (A P) and
+  // the diagonal check, all bit-identical to the host build. The fine
+  // operator is uploaded on the first call and the coarse one stays resident.
+  // Returns false when coarsening stalls (n_agg >= rows).
+  bool next_level(const HostCsr& fine, const SolverParams& sp, long long batch, AmgHostLevel& lv, HostCsr& coarse);
 
  private:
   struct Impl;
@@ -158,6 +169,8 @@ std::vector<double> dense_inverse(const HostCsr& a);
 // levels >= 1 uses this.
 HostCsr filter_lumped(const HostCsr& a, double eps);
 double estimate_lambda_max_scaled(const HostCsr& a, int iters, unsigned seed);
+// Eigen 3.4 v.norm() in its SSE2 reduction order (host_setup.cpp)
+double seq_norm(const std::vector<double>& v);
 
 // symmetric LDLT with diagonal pivoting (Eigen::LDLT semantics)
 struct DenseLdlt {

@@ -176,7 +176,7 @@ void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s, bool 
 void upload_stencil(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.st = DevSellS{};
   HostSellS hs;
-  if (h.n_rows == 0 || !build_sell_stencil(h, hs, true)) return;
+  if (h.n_rows == 0 || !build_sell_stencil(h, hs, true, true)) return;
   b.st_vals.alloc(hs.vals.size());
   b.st_vals.upload(hs.vals.data(), hs.vals.size(), s);
   b.st_pid.alloc(hs.pid.size());
@@ -195,6 +195,22 @@ void upload_stencil(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.st.pid = b.st_pid.p;
   d.st.pat = b.st_pat.p;
   d.st.vals64 = hs.vals64.empty() ? nullptr : b.st_v64.p;
+  if (hs.sym) {
+    b.sh_u16.alloc(hs.uvals.size());
+    b.sh_u16.upload(hs.uvals.data(), hs.uvals.size(), s);
+    b.sh_u64.alloc(hs.uvals64.size());
+    b.sh_u64.upload(hs.uvals64.data(), hs.uvals64.size(), s);
+    b.sh_spid.alloc(hs.spid.size());
+    b.sh_spid.upload(hs.spid.data(), hs.spid.size(), s);
+    b.sh_sinfo.alloc(hs.sinfo.size());
+    b.sh_sinfo.upload(hs.sinfo.data(), hs.sinfo.size(), s);
+    CK(cudaStreamSynchronize(s));
+    d.st.u16 = b.sh_u16.p;
+    d.st.u64 = b.sh_u64.p;
+    d.st.spid = b.sh_spid.p;
+    d.st.sinfo = b.sh_sinfo.p;
+    d.st.sym = true;
+  }
 }
 
 // 1/diag of the owned rows (local row i <-> local column i)
@@ -288,7 +304,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     }
     memtrace("coarse filter");
     plan_ = build_plan(prob_, m_ii_, m_ib_, amg_, comm_->size(), comm_->rank(), prob_.solver.amg_replicate_rows,
-                       &filtered, dev_levels_);
+                       &filtered, dev_levels_, device_);
   }
   memtrace("plan");
   const LocalSpace& s0 = plan_.space[0];
@@ -753,6 +769,13 @@ void GpuSystem::set_stencil(bool on) {
   for (auto& lv : levels_) lv.A.use_stencil = on;
 }
 
+// symmetric half storage of the stencil-coded fine operator (SELL-SH) where built
+void GpuSystem::set_stencil_sym(bool on) {
+  invalidate_graphs();
+  mii_.st.sym = on && mii_.st.u64 != nullptr;
+  if (!levels_.empty()) levels_[0].A.st.sym = mii_.st.sym;
+}
+
 void GpuSystem::set_sell(bool on) {
   invalidate_graphs();
   sell_on_ = on;
@@ -764,7 +787,11 @@ void GpuSystem::set_sell(bool on) {
 }
 
 const std::vector<int>& GpuSystem::colors() {
-  if (n_colors_ < 0) colors_ = color_elements(prob_.dm, n_tets_, &n_colors_);
+  // device waves (k_setup.cu) on a GPU context; EQS_HOST_COLOR=1 keeps the sequential host loop
+  static const bool host_color = getenv("EQS_HOST_COLOR") != nullptr && atoi(getenv("EQS_HOST_COLOR")) != 0;
+  if (n_colors_ < 0)
+    colors_ = device_ >= 0 && !host_color ? dev_color_elements(prob_.dm, n_tets_, &n_colors_, device_)
+                                          : color_elements(prob_.dm, n_tets_, &n_colors_);
   return colors_;
 }
 int GpuSystem::n_colors() {

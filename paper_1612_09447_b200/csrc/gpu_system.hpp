@@ -100,6 +100,10 @@ struct SellBufs {
   DevBuf<unsigned char> st_pid;
   DevBuf<int> st_pat;
   DevBuf<double> st_v64;
+  DevBuf<uint16_t> sh_u16;      // symmetric half storage (SELL-SH)
+  DevBuf<double> sh_u64;
+  DevBuf<unsigned char> sh_spid;
+  DevBuf<int> sh_sinfo;
 };
 
 struct DevLevel {
@@ -222,6 +226,7 @@ class GpuSystem {
   void set_vcycle_precision(int prec);  // V-cycle matrix values: 0 fp64, 1 fp32, 2 bf16
   void set_sell(bool on);               // SELL-16 copies instead of CSR where available
   void set_stencil(bool on);            // stencil-coded fine-level V-cycle operator where available
+  void set_stencil_sym(bool on);        // its symmetric half storage (SELL-SH) where built
   void set_vcycle_vectors_f32(bool on) {  // V-cycle vectors fp32 (default) or fp64
     invalidate_graphs();
     vcycle_f32_ = on;

@@ -74,7 +74,7 @@ HostCsr local_rows(const HostCsr& a, const std::vector<int>* rows, const std::ve
 
 }  // namespace
 
-std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out) {
+std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out, int device) {
   const Dofs& dm = p.dm;
   const int nf = dm.n_free();
   const std::vector<double> c = dof_coords(p);
@@ -90,6 +90,11 @@ std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out
   if (axis_out) *axis_out = axis;
   std::vector<int> owner(nf, 0);
   if (nranks == 1) return owner;
+  if (device >= 0) {
+    std::vector<double> key(nf);
+    for (int a = 0; a < nf; ++a) key[a] = c[3L * dm.free_dofs[a] + axis];
+    return dev_partition_owner(key, nranks, device);
+  }
   std::vector<int> order(nf);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
@@ -101,7 +106,7 @@ std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out
 
 PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m_ib, const AmgHierarchy& h,
                          int nranks, int rank, int rep_threshold, const std::vector<HostCsr>* level_A,
-                         int max_levels) {
+                         int max_levels, int device) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("build_plan: bad rank/nranks");
   PartitionPlan plan;
   plan.nranks = nranks;
@@ -126,7 +131,7 @@ PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m
   plan.rep_level = rep;
   // ownership per level
   plan.owner.resize(L);
-  plan.owner[0] = partition_free_dofs(p, nranks, &plan.axis);
+  plan.owner[0] = partition_free_dofs(p, nranks, &plan.axis, device);
   for (int l = 0; l + 1 < L; ++l) {
     const std::vector<int>& agg = h.levels[l].aggregates;
     const int nc = A_of(l + 1).n_rows;

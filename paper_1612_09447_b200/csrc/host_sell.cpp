@@ -183,7 +183,86 @@ bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out) {
 }
 
 
-bool build_sell_stencil(const HostCsr& a, HostSellS& out, bool with_fp64) {
+// SELL-SH (sell.hpp): upper slots only, lower slots read from the mirror row.
+// Leaves s.sym false when the operator does not qualify (not square, more than
+// 127 patterns, not 16 slots wide, more than kSymSlots upper slots in a
+// pattern, or not bitwise symmetric).
+void build_stencil_sym(const HostCsr& a, HostSellS& s) {
+  const int n = a.n_rows, L = 8 * s.G;
+  s.sym = false;
+  if (a.n_cols != n || s.P > 127 || L != 16) return;
+  std::vector<int> uslot((size_t)s.P * L, -1);
+  for (int p = 0; p < s.P; ++p) {
+    int nu = 0;
+    for (int j = 0; j < s.plen[p]; ++j)
+      if (s.pat[(size_t)p * L + j] >= 0) uslot[(size_t)p * L + j] = nu++;
+    if (nu > kSymSlots) return;
+  }
+  // slot j' of pattern p holding offset `off` (upper slots only), -1 if none
+  auto find_upper = [&](int p, int off) {
+    for (int j = 0; j < s.plen[p]; ++j)
+      if (s.pat[(size_t)p * L + j] == off) return uslot[(size_t)p * L + j];
+    return -1;
+  };
+  const int cm = s.common;
+  s.sinfo.assign((size_t)s.P * L, -1);
+  std::vector<int> mirror_common((size_t)s.P * L, -1);
+  for (int p = 0; p < s.P; ++p)
+    for (int j = 0; j < s.plen[p]; ++j) {
+      const int off = s.pat[(size_t)p * L + j];
+      if (off >= 0) {
+        s.sinfo[(size_t)p * L + j] = uslot[(size_t)p * L + j];
+      } else {
+        const int m = find_upper(cm, -off);
+        mirror_common[(size_t)p * L + j] = m;
+        s.sinfo[(size_t)p * L + j] = m >= 0 ? 8 + m : 16;
+      }
+    }
+  std::vector<uint16_t> uv((size_t)s.n_chunks * kSymSlots * 32, 0);
+  std::vector<double> uv64((size_t)s.n_chunks * kSymSlots * 32, 0.0);
+  std::vector<uint8_t> spid(s.pid.size(), 0);
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < n; ++r) {
+    const int p = s.pid[r], c = r / 32, lane = r % 32;
+    for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
+      const int u = uslot[(size_t)p * L + (k - a.row_ptr[r])];
+      if (u < 0) continue;
+      const size_t at = ((size_t)c * kSymSlots + u) * 32 + lane;
+      uv[at] = to_bf16(a.values[k]);
+      uv64[at] = a.values[k];
+    }
+  }
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+  for (int r = 0; r < n; ++r) {
+    const int p = s.pid[r];
+    bool fast = true;
+    for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
+      const int j = k - a.row_ptr[r], off = s.pat[(size_t)p * L + j];
+      if (off >= 0) continue;
+      const int col = r + off, pc = s.pid[col];
+      const int m = find_upper(pc, -off);
+      if (m < 0) {
+        bad = 1;
+        continue;
+      }
+      const double mirror = uv64[((size_t)(col / 32) * kSymSlots + m) * 32 + col % 32];
+      if (std::memcmp(&mirror, &a.values[k], sizeof(double)) != 0) bad = 1;  // not bitwise symmetric
+      if (pc != cm || mirror_common[(size_t)p * L + j] < 0) fast = false;
+    }
+    spid[r] = (uint8_t)(p | (fast ? 0x80 : 0));
+  }
+  if (bad) {
+    s.sinfo.clear();
+    return;
+  }
+  s.uvals = std::move(uv);
+  s.uvals64 = std::move(uv64);
+  s.spid = std::move(spid);
+  s.sym = true;
+}
+
+bool build_sell_stencil(const HostCsr& a, HostSellS& out, bool with_fp64, bool with_sym) {
   const int n = a.n_rows;
   int lmax = 0;
   for (int r = 0; r < n; ++r) lmax = std::max(lmax, a.row_ptr[r + 1] - a.row_ptr[r]);
@@ -237,8 +316,10 @@ bool build_sell_stencil(const HostCsr& a, HostSellS& out, bool with_fp64) {
     s.common = (int)(std::max_element(freq.begin(), freq.end()) - freq.begin());
   }
   s.pat.assign((size_t)s.P * L, 0);
+  s.plen.assign(s.P, 0);
   for (int p = 0; p < s.P; ++p) {
     const int r = rep[p];
+    s.plen[p] = a.row_ptr[r + 1] - a.row_ptr[r];
     for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) s.pat[(size_t)p * L + (k - a.row_ptr[r])] = a.col_idx[k] - r;
   }
   s.vals.assign((size_t)s.n_chunks * 32 * L, 0);
@@ -259,6 +340,7 @@ bool build_sell_stencil(const HostCsr& a, HostSellS& out, bool with_fp64) {
         s.vals64[((size_t)c * L + (k - a.row_ptr[r])) * 32 + lane] = a.values[k];
     }
   }
+  if (with_sym) build_stencil_sym(a, s);
   out = std::move(s);
   return true;
 }

@@ -258,43 +258,6 @@ void spmv(const HostCsr& a, const std::vector<double>& x, std::vector<double>& y
   }
 }
 
-// Eigen's v.norm() = sqrt(squaredNorm()) in the summation order of Eigen 3.4's
-// vectorised redux with SSE2 packets of 2 doubles (the reference's default
-// x86-64 build): four interleaved accumulators (two packets) over blocks of 4,
-// then the leftover packet, the horizontal add and the scalar tail. The
-// coarse AMG hierarchy depends on omega = (4/3)/lambda_max through borderline
-// strength decisions, so this order is what makes the hierarchy bit-exact to
-// the compiled reference (tests/test_ref_pinning.py).
-double seq_norm(const std::vector<double>& v) {
-  const size_t n = v.size();
-  if (n == 0) return 0.0;
-  const size_t a2 = n / 4 * 4, a1 = n / 2 * 2;
-  double r;
-  if (a1 == 0) {
-    r = v[0] * v[0];
-  } else {
-    double p00 = v[0] * v[0], p01 = v[1] * v[1];
-    if (a1 > 2) {
-      double p10 = v[2] * v[2], p11 = v[3] * v[3];
-      for (size_t i = 4; i < a2; i += 4) {
-        p00 = p00 + v[i] * v[i];
-        p01 = p01 + v[i + 1] * v[i + 1];
-        p10 = p10 + v[i + 2] * v[i + 2];
-        p11 = p11 + v[i + 3] * v[i + 3];
-      }
-      p00 = p00 + p10;
-      p01 = p01 + p11;
-      if (a1 > a2) {
-        p00 = p00 + v[a2] * v[a2];
-        p01 = p01 + v[a2 + 1] * v[a2 + 1];
-      }
-    }
-    r = p00 + p01;
-    for (size_t i = a1; i < n; ++i) r = r + v[i] * v[i];
-  }
-  return std::sqrt(r);
-}
-
 // proj/src/csr.cpp:133-166, row-parallel: each thread owns a contiguous row
 // range and its own accumulator; per-row arithmetic order is unchanged.
 HostCsr multiply(const HostCsr& a, const HostCsr& b) {
@@ -449,6 +412,43 @@ std::vector<int> aggregate(const HostCsr& a, double theta) {
 
 }  // namespace
 
+// Eigen's v.norm() = sqrt(squaredNorm()) in the summation order of Eigen 3.4's
+// vectorised redux with SSE2 packets of 2 doubles (the reference's default
+// x86-64 build): four interleaved accumulators (two packets) over blocks of 4,
+// then the leftover packet, the horizontal add and the scalar tail. The
+// coarse AMG hierarchy depends on omega = (4/3)/lambda_max through borderline
+// strength decisions, so this order is what makes the hierarchy bit-exact to
+// the compiled reference (tests/test_ref_pinning.py).
+double seq_norm(const std::vector<double>& v) {
+  const size_t n = v.size();
+  if (n == 0) return 0.0;
+  const size_t a2 = n / 4 * 4, a1 = n / 2 * 2;
+  double r;
+  if (a1 == 0) {
+    r = v[0] * v[0];
+  } else {
+    double p00 = v[0] * v[0], p01 = v[1] * v[1];
+    if (a1 > 2) {
+      double p10 = v[2] * v[2], p11 = v[3] * v[3];
+      for (size_t i = 4; i < a2; i += 4) {
+        p00 = p00 + v[i] * v[i];
+        p01 = p01 + v[i + 1] * v[i + 1];
+        p10 = p10 + v[i + 2] * v[i + 2];
+        p11 = p11 + v[i + 3] * v[i + 3];
+      }
+      p00 = p00 + p10;
+      p01 = p01 + p11;
+      if (a1 > a2) {
+        p00 = p00 + v[a2] * v[a2];
+        p01 = p01 + v[a2 + 1] * v[a2 + 1];
+      }
+    }
+    r = p00 + p01;
+    for (size_t i = a1; i < n; ++i) r = r + v[i] * v[i];
+  }
+  return std::sqrt(r);
+}
+
 // proj/src/amg.cpp:28-45 (seed 20240811, 10 iterations, sequential norms)
 double estimate_lambda_max_scaled(const HostCsr& a, int iters, unsigned seed) {
   const std::vector<double> d = diagonal(a);
@@ -476,6 +476,8 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device) {
   check_diagonal(a);
   AmgHierarchy h;
   std::unique_ptr<AmgDeviceBuilder> dev_builder;
+  // EQS_HOST_AMG=1: aggregation and lambda_max on the host, products on the device (the round-1 path)
+  static const bool host_amg = getenv("EQS_HOST_AMG") != nullptr && atoi(getenv("EQS_HOST_AMG")) != 0;
   h.levels.push_back({a, {}, {}, {}, 0.0});
   while ((int)h.levels.size() < sp.amg_max_levels && h.levels.back().A.n_rows > sp.amg_coarse_limit) {
     AmgHostLevel& lv = h.levels.back();
@@ -488,6 +490,16 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device) {
                       std::chrono::duration<double>(now - T0).count());
       T0 = now;
     };
+    const long long batch = getenv("EQS_SPGEMM_BATCH") ? atoll(getenv("EQS_SPGEMM_BATCH")) : (1ll << 28);
+    if (device >= 0 && !host_amg) {
+      // the whole level on the device (k_amgsetup.cu + k_spgemm.cu), bit-identical
+      if (!dev_builder) dev_builder = std::make_unique<AmgDeviceBuilder>(device);
+      HostCsr coarse;
+      if (!dev_builder->next_level(fine, sp, batch, lv, coarse)) break;
+      lap("device level");
+      h.levels.push_back({std::move(coarse), {}, {}, {}, 0.0});
+      continue;
+    }
     std::vector<int> agg = aggregate(fine, sp.amg_theta);
     lap("aggregate");
     const int n_agg = *std::max_element(agg.begin(), agg.end()) + 1;
@@ -512,7 +524,6 @@ AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device) {
     const double omega = sp.amg_omega / lv.lambda_max_scaled;
     const std::vector<double> d = diagonal(fine);
     // EQS_SPGEMM_BATCH: products per device batch (tests force many batches)
-    const long long batch = getenv("EQS_SPGEMM_BATCH") ? atoll(getenv("EQS_SPGEMM_BATCH")) : (1ll << 28);
     HostCsr p;
     if (device >= 0) {
       if (!dev_builder) dev_builder = std::make_unique<AmgDeviceBuilder>(device);

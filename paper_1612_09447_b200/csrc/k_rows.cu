@@ -24,8 +24,12 @@ namespace eqsb {
 // (n_cols each) and the streamed row vectors (n_rows each).
 double matrix_pass_bytes(const DevCsr& a, int gathered, int streamed, int xbytes) {
   double m;
-  if (a.stencil64()) {
+  if (a.stencil64() && a.st.sym) {  // upper slots only (lower values are re-reads of them)
+    m = 8.0 * 8.0 * 32.0 * a.st.n_chunks + 32.0 * a.st.n_chunks + 128.0 * a.st.P;
+  } else if (a.stencil64()) {
     m = 8.0 * 8.0 * 32.0 * a.st.G * a.st.n_chunks + 32.0 * a.st.n_chunks + 32.0 * a.st.G * a.st.P;
+  } else if (a.stencil() && a.st.sym) {
+    m = 2.0 * 8.0 * 32.0 * a.st.n_chunks + 32.0 * a.st.n_chunks + 128.0 * a.st.P;
   } else if (a.stencil()) {
     m = 16.0 * 32.0 * a.st.G * a.st.n_chunks + 32.0 * a.st.n_chunks + 32.0 * a.st.G * a.st.P;
   } else if (a.packed()) {
@@ -50,6 +54,7 @@ constexpr int kUnroll = 8;  // independent entries in flight per lane
 #define SELL_MINB 1
 #endif
 constexpr int kSellUnroll1 = SELL_UNROLL1;
+constexpr int kSymSlotsDev = 8;  // sell.hpp kSymSlots
 
 // matrix entries are streamed once per pass: evict-first loads keep L2 for
 // the gathered vectors (ld.global.cs). bf16 values are stored as uint16 bit
@@ -283,6 +288,79 @@ __device__ __forceinline__ void stage_patterns(const DevSellS& m, int* spat) {
   __syncthreads();
 }
 
+// SELL-SH (sell.hpp, symmetric half storage; 16 slots): the pattern offsets
+// [P][16] and slot kinds [P][16] in shared memory
+__device__ __forceinline__ void stage_sym(const DevSellS& m, int* spat) {
+  const int np = m.P * 16;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    spat[i] = __ldg(m.pat + i);
+    spat[np + i] = __ldg(m.sinfo + i);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float sym_cvt(uint16_t v) { return __uint_as_float((unsigned)v << 16); }
+__device__ __forceinline__ double sym_cvt(double v) { return v; }
+
+// slot value of a row outside the speculative (common pattern) path: own upper
+// slot, or the mirror row's upper slot for -offset, found in that row's pattern
+template <class T>
+__device__ __forceinline__ T sym_slot(const DevSellS& m, const int* spat, const T* __restrict__ U, int row, int off,
+                                      int kind, int chunk, int lane) {
+  if (kind < 0) return T(0);
+  if (kind < 8) return U[((long)chunk * kSymSlotsDev + kind) * 32 + lane];
+  const int c = row + off;
+  const int pc = __ldg(m.spid + c) & 127;
+  const int* po = spat + pc * 16;
+  const int* pk = spat + m.P * 16 + pc * 16;
+  int u = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (po[j] == -off && pk[j] >= 0 && pk[j] < 8) u = pk[j];
+  return __ldg(U + ((long)(c >> 5) * kSymSlotsDev + u) * 32 + (c & 31));
+}
+
+// sum over the 16 slots in CSR order of a[j] * x[row + off_j] (x_j w_j when
+// SCALED); a lower slot's value is the mirror row's upper value. Rows of the
+// common pattern whose lower neighbours all have it too (spid bit 7) take the
+// warp-uniform slot kinds; the others redo their slots (boundary rows).
+template <class T, class XT, bool SCALED, bool CG>
+__device__ __forceinline__ XT sym_dot(const DevSellS& m, const T* __restrict__ U, const int* spat, int chunk, int lane,
+                                      int row, const XT* __restrict__ x, const XT* __restrict__ w) {
+  const unsigned pf = __ldcs(m.spid + 32L * chunk + lane);
+  const int p = pf & 127;
+  const int* offc = spat + m.common * 16;
+  const int* kc = spat + m.P * 16 + m.common * 16;
+  const int cmax = m.n_cols - 1;
+  XT a[16], xs[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int off = offc[j], kind = kc[j];
+    const int c = min(max(row + off, 0), cmax);
+    xs[j] = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
+    if (kind >= 0 && kind < 8)
+      a[j] = (XT)sym_cvt(U[((long)chunk * kSymSlotsDev + kind) * 32 + lane]);  // own upper slot (stays in L2)
+    else if (kind >= 8 && kind < 16)
+      a[j] = (XT)sym_cvt(__ldg(U + ((long)(c >> 5) * kSymSlotsDev + (kind - 8)) * 32 + (c & 31)));  // mirror row
+    else
+      a[j] = (XT)0;
+  }
+  if (p != m.common || !(pf & 0x80u)) {
+    const int* po = spat + p * 16;
+    const int* pk = spat + m.P * 16 + p * 16;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = row + po[j];
+      xs[j] = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
+      a[j] = (XT)sym_cvt(sym_slot<T>(m, spat, U, row, po[j], pk[j], chunk, lane));
+    }
+  }
+  XT s = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) s += a[j] * xs[j];
+  return s;
+}
+
 // Row epilogues (load before the pass, store after).
 // Row ops (MODE < 0):
 // OP 0: y = A x                       (restriction, plain SpMV)
@@ -424,13 +502,14 @@ __global__ void __launch_bounds__(kBlock) k_sellp(int n, DevSellP m, const XT* _
   if (act) e.store(row, s, y, y2, nullptr, c, 0);
 }
 
-template <class XT, int OP, bool PRE>
+template <class XT, int OP, bool PRE, bool SYM>
 __global__ void __launch_bounds__(kBlock) k_sells(int n, DevSellS m, const XT* __restrict__ x,
                                                   const XT* __restrict__ b, const XT* __restrict__ invd,
                                                   XT* __restrict__ y, XT* __restrict__ y2, ChebCoef c,
                                                   const XT* __restrict__ pre) {
   extern __shared__ int spat[];
-  stage_patterns(m, spat);
+  if (SYM) stage_sym(m, spat);
+  else stage_patterns(m, spat);
   pdl_entry();
   const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (chunk >= m.n_chunks) return;  // warp-uniform exit
@@ -439,18 +518,24 @@ __global__ void __launch_bounds__(kBlock) k_sells(int n, DevSellS m, const XT* _
   const bool act = row < n;
   Epi<OP, -1, XT> e;
   if (act) e.load(row, x, b, invd, y, nullptr, 0);
-  const XT s = sells_dot<XT, SC && !PRE>(m, spat, chunk, lane, act ? row : 0, SC ? (PRE ? pre : b) : x, invd);
+  XT s;
+  if constexpr (SYM)
+    s = sym_dot<uint16_t, XT, SC && !PRE, false>(m, m.u16, spat, chunk, lane, act ? row : 0,
+                                                 SC ? (PRE ? pre : b) : x, invd);
+  else
+    s = sells_dot<XT, SC && !PRE>(m, spat, chunk, lane, act ? row : 0, SC ? (PRE ? pre : b) : x, invd);
   if (act) e.store(row, s, y, y2, nullptr, c, 0);
 }
 
-template <class XT, int MODE, bool PRE>
+template <class XT, int MODE, bool PRE, bool SYM>
 __global__ void __launch_bounds__(kBlock) k_sells_red(int n, DevSellS m, const XT* __restrict__ x,
                                                       const XT* __restrict__ b, const XT* __restrict__ invd,
                                                       XT* __restrict__ y, double* __restrict__ out64,
                                                       const double* __restrict__ b64, ChebCoef c, Reducer red,
                                                       int slot, int do_red, const XT* __restrict__ pre) {
   extern __shared__ int spat[];
-  stage_patterns(m, spat);
+  if (SYM) stage_sym(m, spat);
+  else stage_patterns(m, spat);
   pdl_entry();
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kBlock / 32);
@@ -460,18 +545,24 @@ __global__ void __launch_bounds__(kBlock) k_sells_red(int n, DevSellS m, const X
     const bool act = row < n;
     Epi<0, MODE, XT> e;
     if (act) e.load(row, x, b, invd, y, b64, do_red);
-    const XT s = sells_dot<XT, kScaled<0, MODE> && !PRE>(m, spat, chunk, lane, act ? row : 0, PRE ? pre : x, invd);
+    XT s;
+    if constexpr (SYM)
+      s = sym_dot<uint16_t, XT, kScaled<0, MODE> && !PRE, false>(m, m.u16, spat, chunk, lane, act ? row : 0,
+                                                                 PRE ? pre : x, invd);
+    else
+      s = sells_dot<XT, kScaled<0, MODE> && !PRE>(m, spat, chunk, lane, act ? row : 0, PRE ? pre : x, invd);
     if (act) acc += e.store(row, s, y, nullptr, out64, c, do_red);
   }
   reduce_finish(acc, red, slot);
 }
 
 // q = A p (OP 0) / q = A p, p.q (MODE 0) with the fp64 stencil-coded operator
-template <int MODE>
+template <int MODE, bool SYM>
 __global__ void __launch_bounds__(kBlock) k_sells64(int n, DevSellS m, const double* __restrict__ x,
                                                     double* __restrict__ y, Reducer red, int slot, int do_red) {
   extern __shared__ int spat[];
-  stage_patterns(m, spat);
+  if (SYM) stage_sym(m, spat);
+  else stage_patterns(m, spat);
   pdl_entry();
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kBlock / 32);
@@ -479,7 +570,8 @@ __global__ void __launch_bounds__(kBlock) k_sells64(int n, DevSellS m, const dou
   for (int chunk = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); chunk < m.n_chunks; chunk += warps) {
     const int row = chunk * 32 + lane;
     const bool act = row < n;
-    const double s = sells_dot64(m, spat, chunk, lane, act ? row : 0, x);
+    const double s = SYM ? sym_dot<double, double, false, false>(m, m.u64, spat, chunk, lane, act ? row : 0, x, nullptr)
+                         : sells_dot64(m, spat, chunk, lane, act ? row : 0, x);
     if (act) {
       y[row] = s;
       if (MODE == 0) acc += x[row] * s;
@@ -590,21 +682,29 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
     if (view.stencil64()) {
       const DevSellS& m = a.st;
       g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
-      launch_pdl(k_sells64<-1>, red_grid(k_sells64<-1>, (long)m.n_chunks * 32), kBlock, sizeof(int) * m.P * 8 * m.G, s, 
-          a.n_rows, m, x, y, Reducer{}, 0, 0);
+      if (m.sym)
+        launch_pdl(k_sells64<-1, true>, red_grid(k_sells64<-1, true>, (long)m.n_chunks * 32), kBlock,
+                   sizeof(int) * m.P * 32, s, a.n_rows, m, x, y, Reducer{}, 0, 0);
+      else
+        launch_pdl(k_sells64<-1, false>, red_grid(k_sells64<-1, false>, (long)m.n_chunks * 32), kBlock,
+                   sizeof(int) * m.P * 8 * m.G, s, a.n_rows, m, x, y, Reducer{}, 0, 0);
       return;
     }
   }
   if (view.stencil()) {
     const DevSellS& m = a.st;
     const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
-    const size_t smem = sizeof(int) * m.P * 8 * m.G;
+    const size_t smem = m.sym ? sizeof(int) * m.P * 32 : sizeof(int) * m.P * 8 * m.G;
     if (pre && kScaled<OP, -1>) {
       g_algo_bytes += matrix_pass_bytes(view, 1, kS[OP] + 2, sizeof(XT));
-      launch_pdl(k_sells<XT, OP, true>, g, kBlock, smem, s, a.n_rows, m, x, b, invd, y, y2, c, pre);
+      if (m.sym) launch_pdl(k_sells<XT, OP, true, true>, g, kBlock, smem, s, a.n_rows, m, x, b, invd, y, y2, c, pre);
+      else launch_pdl(k_sells<XT, OP, true, false>, g, kBlock, smem, s, a.n_rows, m, x, b, invd, y, y2, c, pre);
     } else {
       g_algo_bytes += matrix_pass_bytes(view, kG[OP], kS[OP], sizeof(XT));
-      launch_pdl(k_sells<XT, OP, false>, g, kBlock, smem, s, a.n_rows, m, x, b, invd, y, y2, c, nullptr);
+      if (m.sym)
+        launch_pdl(k_sells<XT, OP, false, true>, g, kBlock, smem, s, a.n_rows, m, x, b, invd, y, y2, c, nullptr);
+      else
+        launch_pdl(k_sells<XT, OP, false, false>, g, kBlock, smem, s, a.n_rows, m, x, b, invd, y, y2, c, nullptr);
     }
     return;
   }
@@ -670,8 +770,12 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
     if (view.stencil64()) {
       const DevSellS& m = a.st;
       g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
-      launch_pdl(k_sells64<0>, red_grid(k_sells64<0>, (long)m.n_chunks * 32), kBlock, sizeof(int) * m.P * 8 * m.G, s, 
-          a.n_rows, m, x, y, r, slot, dr);
+      if (m.sym)
+        launch_pdl(k_sells64<0, true>, red_grid(k_sells64<0, true>, (long)m.n_chunks * 32), kBlock,
+                   sizeof(int) * m.P * 32, s, a.n_rows, m, x, y, r, slot, dr);
+      else
+        launch_pdl(k_sells64<0, false>, red_grid(k_sells64<0, false>, (long)m.n_chunks * 32), kBlock,
+                   sizeof(int) * m.P * 8 * m.G, s, a.n_rows, m, x, y, r, slot, dr);
       return;
     }
   }
@@ -679,13 +783,18 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
   if (view.stencil()) {
     const DevSellS& m = a.st;
     const long work = (long)m.n_chunks * 32;
-    const size_t smem = sizeof(int) * m.P * 8 * m.G;
-    if (use_pre)
-      launch_pdl(k_sells_red<XT, MODE, true>, red_grid(k_sells_red<XT, MODE, true>, work), kBlock, smem, s, 
-          a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, pre);
-    else
-      launch_pdl(k_sells_red<XT, MODE, false>, red_grid(k_sells_red<XT, MODE, false>, work), kBlock, smem, s, 
-          a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, nullptr);
+    const size_t smem = m.sym ? sizeof(int) * m.P * 32 : sizeof(int) * m.P * 8 * m.G;
+#define R_(PRE, SYM, PP)                                                                                      \
+  launch_pdl(k_sells_red<XT, MODE, PRE, SYM>, red_grid(k_sells_red<XT, MODE, PRE, SYM>, work), kBlock, smem, s, \
+             a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, PP)
+    if (use_pre) {
+      if (m.sym) R_(true, true, pre);
+      else R_(true, false, pre);
+    } else {
+      if (m.sym) R_(false, true, nullptr);
+      else R_(false, false, nullptr);
+    }
+#undef R_
     return;
   }
   if (view.packed()) {

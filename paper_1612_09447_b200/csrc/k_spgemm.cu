@@ -20,11 +20,12 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
-#include "eqs_internal.hpp"
-#include "gpu_system.hpp"
+#include "amg_device.hpp"
 
 namespace eqsb {
 
@@ -111,28 +112,7 @@ void up(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
 }
 template void up(DevBuf<double>&, const std::vector<double>&, cudaStream_t);
 
-// ---------------------------------------------------------------- device CSR products
-struct DCsr {
-  int rows = 0, cols = 0;
-  long long nnz = 0;
-  DevBuf<int> rp, ci;
-  DevBuf<double> v;
-};
-class SpgemmDevice {
- public:
-  SpgemmDevice() = default;
-  ~SpgemmDevice();
-  void init(int device);
-  cudaStream_t stream() const { return s_; }
-  void upload(const HostCsr& h, DCsr& d);
-  void download(const DCsr& d, HostCsr& h);
-  void multiply(const DCsr& a, const DCsr& b, DCsr& c, const double* diag_dev, double omega, long long batch);
-
- private:
-  int device_ = -1;
-  cudaStream_t s_ = nullptr;
-};
-
+// ---------------------------------------------------------------- device CSR products (amg_device.hpp)
 void SpgemmDevice::init(int device) {
   device_ = device;
   ck(cudaSetDevice(device), "set device");
@@ -316,6 +296,44 @@ HostCsr AmgDeviceBuilder::galerkin(const HostCsr& r, long long batch) {
   m.sd.download(coarse, c);
   m.fine = std::move(coarse);  // next level's fine operator stays resident
   return c;
+}
+
+bool AmgDeviceBuilder::next_level(const HostCsr& fine, const SolverParams& sp, long long batch, AmgHostLevel& lv,
+                                  HostCsr& coarse_out) {
+  Impl& m = *impl_;
+  cudaStream_t s = m.sd.stream();
+  if (!m.has_fine) m.sd.upload(fine, m.fine);
+  m.has_fine = true;
+  const int n = m.fine.rows;
+  DevBuf<double> d;
+  dev_diagonal(m.fine, d, s);
+  DevBuf<int> agg;
+  DevAggStats st;
+  const int n_agg = dev_aggregate(m.fine, d.p, sp.amg_theta, agg, s, &st);
+  if (getenv("EQS_MEMTRACE"))
+    fprintf(stderr, "[amg] device aggregation: %d rows -> %d aggregates (%d roots in %d rounds, %d attached in %d rounds, %d new)\n",
+            n, n_agg, st.roots, st.rounds_pass1, st.pass2, st.rounds_pass2, st.pass3);
+  if (n_agg >= n) return false;  // coarsening stalled (amg.cpp:102)
+  lv.aggregates.resize(n);
+  agg.download(lv.aggregates.data(), n, s);
+  DCsr pt;
+  dev_tentative(agg, n, n_agg, pt, s);
+  lv.lambda_max_scaled = dev_lambda_max(m.fine, d.p, 10, 20240811u, s);
+  const double omega = sp.amg_omega / lv.lambda_max_scaled;
+  m.sd.multiply(m.fine, pt, m.p, d.p, omega, batch);  // P = (I - omega D^-1 A) P_tent
+  pt = DCsr();
+  DCsr r, ap, coarse;
+  dev_transpose(m.p, r, s);
+  m.sd.multiply(m.fine, m.p, ap, nullptr, 0.0, batch);
+  m.sd.multiply(r, ap, coarse, nullptr, 0.0, batch);
+  ap = DCsr();
+  dev_check_diagonal(coarse, s);
+  m.sd.download(m.p, lv.P);
+  m.sd.download(r, lv.R);
+  m.sd.download(coarse, coarse_out);
+  m.p = DCsr();
+  m.fine = std::move(coarse);
+  return true;
 }
 
 HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std::vector<double>* diag,

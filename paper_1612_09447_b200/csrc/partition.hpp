@@ -44,7 +44,8 @@ struct PartitionPlan {
 // owner rank of every free dof: stable sort by (coordinate along the longest
 // bounding-box axis, preferring z then y then x on ties; free index), then
 // contiguous equal chunks
-std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out = nullptr);
+// (device >= 0: the sort runs on that GPU, k_setup.cu, same result)
+std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out = nullptr, int device = -1);
 
 // full plan for `rank` (levels from the AMG hierarchy; a single level when h
 // is empty). Coarse levels with at most rep_threshold rows, and always the
@@ -54,6 +55,6 @@ std::vector<int> partition_free_dofs(const Problem& p, int nranks, int* axis_out
 // level_A (optional): replacement operators per level (entries with n_rows == 0 keep h's)
 PartitionPlan build_plan(const Problem& p, const HostCsr& m_ii, const HostCsr& m_ib, const AmgHierarchy& h,
                          int nranks, int rank, int rep_threshold, const std::vector<HostCsr>* level_A = nullptr,
-                         int max_levels = 1 << 30);
+                         int max_levels = 1 << 30, int device = -1);
 
 }  // namespace eqsb

@@ -85,9 +85,26 @@ struct HostSellS {
   std::vector<double> vals64;   // [n_chunks][8 G][32] fp64 values (the PCG operator), slot-major per chunk
   std::vector<uint8_t> pid;     // [n_chunks * 32]
   std::vector<int> pat;         // [P][8 G]
+  std::vector<int> plen;        // [P] entries per pattern (slots >= plen are padding)
+  // Symmetric half storage ("SELL-SH"), built when the operator
+  // is square, bitwise symmetric, 16 slots wide and has <= 127 patterns: a row
+  // stores only its upper slots (offset >= 0, at most kSymSlots) and reads the
+  // value of a lower slot (column c = row + offset < row) from row c's upper
+  // slot for -offset, i.e. from data streamed shortly before (L2). Products
+  // are still summed in CSR order, so a pass is bit-identical to the full
+  // stencil-coded pass.
+  bool sym = false;
+  std::vector<uint16_t> uvals;  // [n_chunks][kSymSlots][32] bf16 upper values (slot-major)
+  std::vector<double> uvals64;  // [n_chunks][kSymSlots][32] fp64 upper values
+  std::vector<uint8_t> spid;    // [n_chunks * 32] pattern id | 0x80 when every lower slot's row has the
+                                // common pattern and the common pattern holds the mirror slot
+  std::vector<int> sinfo;       // [P][16] slot kind: u (0..7) own upper slot u; 8 + m lower slot whose
+                                // mirror is upper slot m of the common pattern; 16 lower slot without
+                                // such a mirror; -1 padding
 };
+constexpr int kSymSlots = 8;
 // false when the rows need more than 255 patterns or more than 32 slots
-bool build_sell_stencil(const HostCsr& a, HostSellS& out, bool with_fp64 = false);
+bool build_sell_stencil(const HostCsr& a, HostSellS& out, bool with_fp64 = false, bool with_sym = false);
 
 uint16_t to_bf16(double d);  // round to nearest even
 // lanes per row of the packed format: about 32 entries per lane (fewer

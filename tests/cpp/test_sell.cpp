@@ -90,6 +90,57 @@ static int check_stencil(const HostCsr& a, const HostSellS& h) {
   return bad;
 }
 
+// SELL-SH: emulate the kernel's slot resolution (sym_dot in k_rows.cu): the
+// common pattern's slot kinds for fast rows, the row's own pattern plus a
+// search of the mirror row's pattern otherwise; every slot must decode to the
+// row's CSR value (fp64 bitwise, bf16 rounded) and padding to 0
+static int check_sym(const HostCsr& a, const HostSellS& h, long* fast_rows) {
+  int bad = 0;
+  long fast = 0;
+  auto U64 = [&](int row, int u) { return h.uvals64[((size_t)(row / 32) * kSymSlots + u) * 32 + row % 32]; };
+  auto U16 = [&](int row, int u) { return h.uvals[((size_t)(row / 32) * kSymSlots + u) * 32 + row % 32]; };
+  for (int r = 0; r < a.n_rows; ++r) {
+    const int pf = h.spid[r], p = pf & 127, len = a.row_ptr[r + 1] - a.row_ptr[r];
+    const bool spec = p == h.common && (pf & 0x80);
+    fast += spec;
+    for (int j = 0; j < 16; ++j) {
+      const int off = h.pat[(size_t)p * 16 + j], kind = h.sinfo[(size_t)(spec ? h.common : p) * 16 + j];
+      double v64 = 0.0;
+      uint16_t v16 = 0;
+      if (kind >= 0 && kind < 8) {
+        v64 = U64(r, kind);
+        v16 = U16(r, kind);
+      } else if (kind >= 8) {
+        const int c = r + off;
+        int u = -1;
+        if (spec) {
+          u = kind - 8;
+        } else {
+          const int pc = h.spid[c] & 127;
+          for (int q = 0; q < 16; ++q)
+            if (h.pat[(size_t)pc * 16 + q] == -off && h.sinfo[(size_t)pc * 16 + q] >= 0 &&
+                h.sinfo[(size_t)pc * 16 + q] < 8)
+              u = h.sinfo[(size_t)pc * 16 + q];
+        }
+        if (u < 0) {
+          ++bad;
+          continue;
+        }
+        v64 = U64(c, u);
+        v16 = U16(c, u);
+      }
+      if (j < len) {
+        const int k = a.row_ptr[r] + j;
+        bad += std::memcmp(&v64, &a.values[k], 8) != 0 || v16 != to_bf16(a.values[k]) || r + off != a.col_idx[k];
+      } else {
+        bad += v64 != 0.0 || v16 != 0;
+      }
+    }
+  }
+  *fast_rows = fast;
+  return bad;
+}
+
 // structured 15-point rows (Kuhn-box M_II-like): 3D grid with offsets
 // (di, dj, dk) in {-1,0,1}^3 restricted to the 15 Kuhn-mesh neighbours
 static HostCsr kuhn_like(int nx, int ny, int nz) {
@@ -192,6 +243,23 @@ int main() {
     printf("stencil kuhn-like %d rows: ok %d patterns %d G %d -> %s\n", a.n_rows, ok, h.P, h.G,
            fs || h.P != 27 || h.G != 2 ? "FAIL" : "ok");
     fails += fs + (h.P != 27) + (h.G != 2);
+  }
+  // SELL-SH on symmetric structured rows; an asymmetric value set keeps the full copy
+  for (int symmetric : {1, 0}) {
+    HostCsr a = kuhn_like(13, 11, 9);
+    for (int r = 0; r < a.n_rows; ++r)
+      for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
+        const int c = a.col_idx[k], lo = std::min(r, c), hi = std::max(r, c);
+        a.values[k] = (c == r ? 6.0 : -0.1) + 1e-3 * ((lo * 31 + hi * 7) % 101) + (symmetric ? 0.0 : 1e-9 * (r > c));
+      }
+    HostSellS h;
+    const bool ok = build_sell_stencil(a, h, true, true);
+    long fast = 0;
+    const int fs = ok && h.sym ? check_sym(a, h, &fast) : 0;
+    const bool pass = ok && (symmetric ? h.sym && fs == 0 && fast > a.n_rows / 4 : !h.sym);
+    printf("stencil sym (symmetric %d): built %d sym %d fast rows %ld -> %s\n", symmetric, ok, (int)h.sym, fast,
+           pass ? "ok" : "FAIL");
+    fails += !pass;
   }
   {  // random columns: too many patterns -> no stencil copy
     HostCsr a;
