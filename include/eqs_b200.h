@@ -344,10 +344,11 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * 21 = programmatic dependent launch of the row/vector kernels (0/1; default 1;
  * process-wide), 22 = the graph-resident PCG loop on multi-rank NCCL contexts
  * too (0/1; default 0: halo and allreduce calls captured into the loop body),
- * 23 = symmetric half storage of the stencil-coded fine operator (0/1; default 1
- * where the operator is single-rank, bitwise symmetric and 16 slots wide: rows
- * store their upper slots only and read lower values from the mirror rows;
- * bit-identical results, about half the matrix bytes),
+ * 23 = symmetric half storage of the stencil-coded fine operator (0/1; only when
+ * the context was created with EQS_SELL_SH=1 in the environment and the operator
+ * is single-rank, bitwise symmetric and 16 slots wide: rows store their upper
+ * slots only and read lower values from the mirror rows; bit-identical products,
+ * about half the matrix bytes, but slower on B200: DESIGN.md §8),
  * 13 = smoother polynomial (0 first-kind Chebyshev, 1 fourth-kind, 2 fourth-kind
  * with optimised weights), 14 = lambda_max safety factor (default 1.1).
  * The PCG operator and vectors are fp64 in every setting. */

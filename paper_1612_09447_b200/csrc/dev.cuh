@@ -86,6 +86,8 @@ struct DevSellS {
   const double* u64 = nullptr;           // [n_chunks][8][32] fp64 upper values
   const unsigned char* spid = nullptr;   // [n_chunks * 32] pattern | 0x80 (fast row)
   const int* sinfo = nullptr;            // [P][16] slot kinds
+  const uint4* slow_code = nullptr;      // [n_slow] 16 mirror slots of each slow row
+  const int* slow_base = nullptr;        // [n_chunks + 1] slow rows before each chunk
 };
 
 // CSR matrix resident in HBM (int32 indices, fp64 values, sorted columns),

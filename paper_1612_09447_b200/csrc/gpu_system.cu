@@ -176,7 +176,10 @@ void upload_sell(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s, bool 
 void upload_stencil(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.st = DevSellS{};
   HostSellS hs;
-  if (h.n_rows == 0 || !build_sell_stencil(h, hs, true, true)) return;
+  // SELL-SH (symmetric half storage) is built only on request (EQS_SELL_SH=1):
+  // measured slower than the full stencil copy on B200
+  const bool want_sym = getenv("EQS_SELL_SH") != nullptr && atoi(getenv("EQS_SELL_SH")) != 0;
+  if (h.n_rows == 0 || !build_sell_stencil(h, hs, true, want_sym)) return;
   b.st_vals.alloc(hs.vals.size());
   b.st_vals.upload(hs.vals.data(), hs.vals.size(), s);
   b.st_pid.alloc(hs.pid.size());
@@ -204,11 +207,17 @@ void upload_stencil(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
     b.sh_spid.upload(hs.spid.data(), hs.spid.size(), s);
     b.sh_sinfo.alloc(hs.sinfo.size());
     b.sh_sinfo.upload(hs.sinfo.data(), hs.sinfo.size(), s);
+    b.sh_slow.alloc(hs.slow_code.size() + 32 * 16);  // padded lanes of the last chunk may index past the table
+    if (!hs.slow_code.empty()) b.sh_slow.upload(hs.slow_code.data(), hs.slow_code.size(), s);
+    b.sh_slow_base.alloc(hs.slow_base.size());
+    b.sh_slow_base.upload(hs.slow_base.data(), hs.slow_base.size(), s);
     CK(cudaStreamSynchronize(s));
     d.st.u16 = b.sh_u16.p;
     d.st.u64 = b.sh_u64.p;
     d.st.spid = b.sh_spid.p;
     d.st.sinfo = b.sh_sinfo.p;
+    d.st.slow_code = reinterpret_cast<const uint4*>(b.sh_slow.p);
+    d.st.slow_base = b.sh_slow_base.p;
     d.st.sym = true;
   }
 }

@@ -104,6 +104,8 @@ struct SellBufs {
   DevBuf<double> sh_u64;
   DevBuf<unsigned char> sh_spid;
   DevBuf<int> sh_sinfo;
+  DevBuf<unsigned char> sh_slow;
+  DevBuf<int> sh_slow_base;
 };
 
 struct DevLevel {

@@ -256,6 +256,23 @@ void build_stencil_sym(const HostCsr& a, HostSellS& s) {
     s.sinfo.clear();
     return;
   }
+  s.slow_base.assign(s.n_chunks + 1, 0);
+  for (int r = 0; r < n; ++r) s.slow_base[r / 32 + 1] += !(spid[r] & 0x80);
+  for (int c = 0; c < s.n_chunks; ++c) s.slow_base[c + 1] += s.slow_base[c];
+  s.slow_code.assign((size_t)s.slow_base[s.n_chunks] * 16, 0);
+#pragma omp parallel for schedule(static)
+  for (int c = 0; c < s.n_chunks; ++c) {
+    long at = s.slow_base[c];
+    for (int r = 32 * c; r < std::min(n, 32 * c + 32); ++r) {
+      if (spid[r] & 0x80) continue;
+      const int p = s.pid[r];
+      for (int j = 0; j < s.plen[p]; ++j) {
+        const int off = s.pat[(size_t)p * L + j];
+        if (off < 0) s.slow_code[at * 16 + j] = (uint8_t)find_upper(s.pid[r + off], -off);
+      }
+      ++at;
+    }
+  }
   s.uvals = std::move(uv);
   s.uvals64 = std::move(uv64);
   s.spid = std::move(spid);

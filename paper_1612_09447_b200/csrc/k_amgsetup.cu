@@ -19,8 +19,9 @@
 //   in index order by a scan, which is the order the sequential loop uses.
 // * Pass 2 attaches a leftover node to the aggregate of its strongest
 //   aggregated neighbour (first maximum in row order). Earlier leftovers count
-//   as aggregated once they are attached, so node i is resolved in the first
-//   round in which all of its smaller leftover neighbours are resolved.
+//   as aggregated once they are attached. Node i is resolved in the first
+//   round in which none of its unresolved smaller leftover neighbours could
+//   still be the first maximum of its row scan.
 // * Pass 3 numbers the remaining nodes in index order (scan).
 //
 // The round loops run until their worklists are empty; the result does not
@@ -185,15 +186,20 @@ __global__ void k_pass1_agg(int n, const int* __restrict__ taken, const int* __r
 
 // pass 2 (amg.cpp:69-83). code[j] of a leftover j: 0 unresolved, 1 resolved
 // without an aggregate, a + 2 attached to aggregate a. Earlier leftovers are
-// visible to i only once resolved; later ones are not aggregated yet.
+// visible to i only once resolved; later ones are not aggregated yet. Row i is
+// decided as soon as no unresolved earlier leftover could be its first
+// maximum (mu_k, mu below), so chains resolve in a few rounds.
 __global__ void k_pass2(int nl, const int* __restrict__ list, const int* __restrict__ rp, const int* __restrict__ ci,
                         const double* __restrict__ v, const int* __restrict__ agg1, int* code, int* __restrict__ next,
                         int* __restrict__ count) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nl) return;
   const int i = list[t];
-  int best = -1;
+  int best = -1, best_k = INT_MAX;
   double best_w = -1.0;
+  // unresolved earlier leftovers: the largest weight and its first position
+  double mu = -1.0;
+  int mu_k = INT_MAX;
   for (int k = rp[i]; k < rp[i + 1]; ++k) {
     const int j = ci[k];
     if (j == i) continue;
@@ -201,9 +207,13 @@ __global__ void k_pass2(int nl, const int* __restrict__ list, const int* __restr
     if (aj < 0) {
       if (j > i) continue;
       const int c = ((volatile int*)code)[j];
-      if (c == 0) {  // an earlier leftover is unresolved: retry next round
-        next[atomicAdd(count, 1)] = i;
-        return;
+      if (c == 0) {
+        const double w = fabs(v[k]);
+        if (w > mu) {
+          mu = w;
+          mu_k = k;
+        }
+        continue;
       }
       aj = c - 2;
       if (aj < 0) continue;
@@ -212,7 +222,14 @@ __global__ void k_pass2(int nl, const int* __restrict__ list, const int* __restr
     if (w > best_w) {
       best_w = w;
       best = aj;
+      best_k = k;
     }
+  }
+  // the row scan keeps the first maximum: an unresolved leftover changes the
+  // outcome only if it could be that maximum; otherwise i is decided now
+  if (mu > best_w || (mu == best_w && mu_k < best_k)) {
+    next[atomicAdd(count, 1)] = i;
+    return;
   }
   ((volatile int*)code)[i] = best >= 0 ? best + 2 : 1;
 }

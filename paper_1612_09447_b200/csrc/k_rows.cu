@@ -289,12 +289,33 @@ __device__ __forceinline__ void stage_patterns(const DevSellS& m, int* spat) {
 }
 
 // SELL-SH (sell.hpp, symmetric half storage; 16 slots): the pattern offsets
-// [P][16] and slot kinds [P][16] in shared memory
+// [P][16] and slot kinds [P][16] in shared memory, then for the common
+// pattern the element index of every (slot, lane) relative to the lane's
+// chunk base (own upper slot: u 32 + lane; lower slot: the mirror row's upper
+// slot in its chunk) and the pattern's padding mask
+constexpr int kSymSmemInts(int P) { return P * 32 + 16 * 32 + 1; }
 __device__ __forceinline__ void stage_sym(const DevSellS& m, int* spat) {
   const int np = m.P * 16;
   for (int i = threadIdx.x; i < np; i += blockDim.x) {
     spat[i] = __ldg(m.pat + i);
     spat[np + i] = __ldg(m.sinfo + i);
+  }
+  int* dtab = spat + 2 * np;
+  for (int i = threadIdx.x; i < 16 * 32; i += blockDim.x) {
+    const int j = i >> 5, lane = i & 31;
+    const int off = __ldg(m.pat + m.common * 16 + j), kind = __ldg(m.sinfo + m.common * 16 + j);
+    int d = lane;  // padding: the row's first upper value (masked out)
+    if (kind >= 0 && kind < 8) d = kind * 32 + lane;
+    if (kind >= 8) {
+      const int t = lane + off;  // mirror row = chunk * 32 + t
+      d = (t >> 5) * (kSymSlotsDev * 32) + (kind - 8) * 32 + (t & 31);
+    }
+    dtab[i] = d;
+  }
+  if (threadIdx.x == 0) {
+    unsigned pad = 0;
+    for (int j = 0; j < 16; ++j) pad |= (__ldg(m.sinfo + m.common * 16 + j) < 0 ? 1u : 0u) << j;
+    spat[2 * np + 16 * 32] = (int)pad;
   }
   __syncthreads();
 }
@@ -302,62 +323,68 @@ __device__ __forceinline__ void stage_sym(const DevSellS& m, int* spat) {
 __device__ __forceinline__ float sym_cvt(uint16_t v) { return __uint_as_float((unsigned)v << 16); }
 __device__ __forceinline__ double sym_cvt(double v) { return v; }
 
-// slot value of a row outside the speculative (common pattern) path: own upper
-// slot, or the mirror row's upper slot for -offset, found in that row's pattern
-template <class T>
-__device__ __forceinline__ T sym_slot(const DevSellS& m, const int* spat, const T* __restrict__ U, int row, int off,
-                                      int kind, int chunk, int lane) {
-  if (kind < 0) return T(0);
-  if (kind < 8) return U[((long)chunk * kSymSlotsDev + kind) * 32 + lane];
-  const int c = row + off;
-  const int pc = __ldg(m.spid + c) & 127;
-  const int* po = spat + pc * 16;
-  const int* pk = spat + m.P * 16 + pc * 16;
-  int u = 0;
-#pragma unroll
-  for (int j = 0; j < 16; ++j)
-    if (po[j] == -off && pk[j] >= 0 && pk[j] < 8) u = pk[j];
-  return __ldg(U + ((long)(c >> 5) * kSymSlotsDev + u) * 32 + (c & 31));
-}
-
-// sum over the 16 slots in CSR order of a[j] * x[row + off_j] (x_j w_j when
-// SCALED); a lower slot's value is the mirror row's upper value. Rows of the
-// common pattern whose lower neighbours all have it too (spid bit 7) take the
-// warp-uniform slot kinds; the others redo their slots (boundary rows).
+// SELL-SH row dot: the 16 slots summed in CSR order, a[j] x[row + off_j]
+// (x_j w_j when SCALED); a lower slot's value is the mirror row's upper value.
+// Warps whose rows all have the common pattern and common-pattern lower
+// neighbours (spid bit 7) use the warp-uniform slot kinds of the common
+// pattern. Other warps take each lane's own pattern; a lane whose row lacks
+// bit 7 reads its mirror slots from the slow-row table (16 bytes per row,
+// located by a ballot over the chunk).
 template <class T, class XT, bool SCALED, bool CG>
 __device__ __forceinline__ XT sym_dot(const DevSellS& m, const T* __restrict__ U, const int* spat, int chunk, int lane,
                                       int row, const XT* __restrict__ x, const XT* __restrict__ w) {
   const unsigned pf = __ldcs(m.spid + 32L * chunk + lane);
-  const int p = pf & 127;
-  const int* offc = spat + m.common * 16;
-  const int* kc = spat + m.P * 16 + m.common * 16;
-  const int cmax = m.n_cols - 1;
-  XT a[16], xs[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int off = offc[j], kind = kc[j];
-    const int c = min(max(row + off, 0), cmax);
-    xs[j] = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
-    if (kind >= 0 && kind < 8)
-      a[j] = (XT)sym_cvt(U[((long)chunk * kSymSlotsDev + kind) * 32 + lane]);  // own upper slot (stays in L2)
-    else if (kind >= 8 && kind < 16)
-      a[j] = (XT)sym_cvt(__ldg(U + ((long)(c >> 5) * kSymSlotsDev + (kind - 8)) * 32 + (c & 31)));  // mirror row
-    else
-      a[j] = (XT)0;
-  }
-  if (p != m.common || !(pf & 0x80u)) {
-    const int* po = spat + p * 16;
-    const int* pk = spat + m.P * 16 + p * 16;
+  // speculative pass with the common pattern, issued before the pattern id
+  // arrives (no pid -> address -> load chain); indices are clamped because a
+  // row of another pattern may point outside the arrays, and such a warp
+  // redoes its slots below. Every load is issued before the first use.
+  T raw[16];
+  XT xs[16];
+  {
+    const int* offc = spat + m.common * 16;
+    const int* dtab = spat + m.P * 32 + lane;
+    const long base = (long)chunk * kSymSlotsDev * 32;
+    const long emax = (long)m.n_chunks * kSymSlotsDev * 32 - 1;
+    const int cmax = m.n_cols - 1;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
+      const int c = min(max(row + offc[j], 0), cmax);
+      xs[j] = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
+      raw[j] = __ldg(U + min(max(base + dtab[32 * j], 0L), emax));
+    }
+  }
+  unsigned pad = (unsigned)spat[m.P * 32 + 16 * 32];
+  const int p = pf & 127;
+  const bool fast = p == m.common && (pf & 0x80u);
+  const unsigned slow = __ballot_sync(0xffffffffu, !fast);
+  if (slow != 0) {
+    // rows of another pattern or next to one: each lane's own pattern; a lane
+    // whose row lacks bit 7 reads its mirror slots from the slow-row table
+    const unsigned tab = __ballot_sync(0xffffffffu, !(pf & 0x80u));
+    const T* own = U + (long)chunk * kSymSlotsDev * 32 + lane;
+    const int* po = spat + p * 16;
+    const int* pk = spat + m.P * 16 + p * 16;
+    uint4 sc = make_uint4(0u, 0u, 0u, 0u);
+    if (!(pf & 0x80u)) sc = __ldg(m.slow_code + __ldg(m.slow_base + chunk) + __popc(tab & ((1u << lane) - 1u)));
+    const unsigned scw[4] = {sc.x, sc.y, sc.z, sc.w};
+    pad = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int kind = pk[j];
       const int c = row + po[j];
       xs[j] = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
-      a[j] = (XT)sym_cvt(sym_slot<T>(m, spat, U, row, po[j], pk[j], chunk, lane));
+      const int u = (pf & 0x80u) ? kind - 8 : (int)((scw[j >> 2] >> (8 * (j & 3))) & 0xffu);
+      const T* mirror = U + ((long)(c >> 5) * kSymSlotsDev + u) * 32 + (c & 31);
+      raw[j] = __ldg(kind >= 8 ? mirror : own + 32 * max(kind, 0));
+      pad |= (kind < 0 ? 1u : 0u) << j;
     }
   }
   XT s = 0;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) s += a[j] * xs[j];
+  for (int j = 0; j < 16; ++j) {
+    const XT a = (pad >> j) & 1u ? (XT)0 : (XT)sym_cvt(raw[j]);
+    s += a * xs[j];
+  }
   return s;
 }
 
@@ -684,7 +711,7 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
       g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
       if (m.sym)
         launch_pdl(k_sells64<-1, true>, red_grid(k_sells64<-1, true>, (long)m.n_chunks * 32), kBlock,
-                   sizeof(int) * m.P * 32, s, a.n_rows, m, x, y, Reducer{}, 0, 0);
+                   sizeof(int) * kSymSmemInts(m.P), s, a.n_rows, m, x, y, Reducer{}, 0, 0);
       else
         launch_pdl(k_sells64<-1, false>, red_grid(k_sells64<-1, false>, (long)m.n_chunks * 32), kBlock,
                    sizeof(int) * m.P * 8 * m.G, s, a.n_rows, m, x, y, Reducer{}, 0, 0);
@@ -694,7 +721,7 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
   if (view.stencil()) {
     const DevSellS& m = a.st;
     const int g = (int)(((long)m.n_chunks * 32 + kBlock - 1) / kBlock);
-    const size_t smem = m.sym ? sizeof(int) * m.P * 32 : sizeof(int) * m.P * 8 * m.G;
+    const size_t smem = m.sym ? sizeof(int) * kSymSmemInts(m.P) : sizeof(int) * m.P * 8 * m.G;
     if (pre && kScaled<OP, -1>) {
       g_algo_bytes += matrix_pass_bytes(view, 1, kS[OP] + 2, sizeof(XT));
       if (m.sym) launch_pdl(k_sells<XT, OP, true, true>, g, kBlock, smem, s, a.n_rows, m, x, b, invd, y, y2, c, pre);
@@ -772,7 +799,7 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
       g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
       if (m.sym)
         launch_pdl(k_sells64<0, true>, red_grid(k_sells64<0, true>, (long)m.n_chunks * 32), kBlock,
-                   sizeof(int) * m.P * 32, s, a.n_rows, m, x, y, r, slot, dr);
+                   sizeof(int) * kSymSmemInts(m.P), s, a.n_rows, m, x, y, r, slot, dr);
       else
         launch_pdl(k_sells64<0, false>, red_grid(k_sells64<0, false>, (long)m.n_chunks * 32), kBlock,
                    sizeof(int) * m.P * 8 * m.G, s, a.n_rows, m, x, y, r, slot, dr);
@@ -783,7 +810,7 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
   if (view.stencil()) {
     const DevSellS& m = a.st;
     const long work = (long)m.n_chunks * 32;
-    const size_t smem = m.sym ? sizeof(int) * m.P * 32 : sizeof(int) * m.P * 8 * m.G;
+    const size_t smem = m.sym ? sizeof(int) * kSymSmemInts(m.P) : sizeof(int) * m.P * 8 * m.G;
 #define R_(PRE, SYM, PP)                                                                                      \
   launch_pdl(k_sells_red<XT, MODE, PRE, SYM>, red_grid(k_sells_red<XT, MODE, PRE, SYM>, work), kBlock, smem, s, \
              a.n_rows, m, x, b, invd, y, out64, b64, c, r, slot, dr, PP)

@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -302,6 +303,15 @@ bool AmgDeviceBuilder::next_level(const HostCsr& fine, const SolverParams& sp, l
                                   HostCsr& coarse_out) {
   Impl& m = *impl_;
   cudaStream_t s = m.sd.stream();
+  static const bool trace = getenv("EQS_MEMTRACE") != nullptr;
+  auto T0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[amg]   %-10s %.3f s\n", what, std::chrono::duration<double>(now - T0).count());
+    T0 = now;
+  };
   if (!m.has_fine) m.sd.upload(fine, m.fine);
   m.has_fine = true;
   const int n = m.fine.rows;
@@ -309,7 +319,9 @@ bool AmgDeviceBuilder::next_level(const HostCsr& fine, const SolverParams& sp, l
   dev_diagonal(m.fine, d, s);
   DevBuf<int> agg;
   DevAggStats st;
+  lap("upload");
   const int n_agg = dev_aggregate(m.fine, d.p, sp.amg_theta, agg, s, &st);
+  lap("aggregate");
   if (getenv("EQS_MEMTRACE"))
     fprintf(stderr, "[amg] device aggregation: %d rows -> %d aggregates (%d roots in %d rounds, %d attached in %d rounds, %d new)\n",
             n, n_agg, st.roots, st.rounds_pass1, st.pass2, st.rounds_pass2, st.pass3);
@@ -318,19 +330,26 @@ bool AmgDeviceBuilder::next_level(const HostCsr& fine, const SolverParams& sp, l
   agg.download(lv.aggregates.data(), n, s);
   DCsr pt;
   dev_tentative(agg, n, n_agg, pt, s);
+  lap("p_tent");
   lv.lambda_max_scaled = dev_lambda_max(m.fine, d.p, 10, 20240811u, s);
+  lap("lambda");
   const double omega = sp.amg_omega / lv.lambda_max_scaled;
   m.sd.multiply(m.fine, pt, m.p, d.p, omega, batch);  // P = (I - omega D^-1 A) P_tent
   pt = DCsr();
+  lap("P");
   DCsr r, ap, coarse;
   dev_transpose(m.p, r, s);
+  lap("R");
   m.sd.multiply(m.fine, m.p, ap, nullptr, 0.0, batch);
+  lap("AP");
   m.sd.multiply(r, ap, coarse, nullptr, 0.0, batch);
   ap = DCsr();
   dev_check_diagonal(coarse, s);
+  lap("RAP");
   m.sd.download(m.p, lv.P);
   m.sd.download(r, lv.R);
   m.sd.download(coarse, coarse_out);
+  lap("download");
   m.p = DCsr();
   m.fine = std::move(coarse);
   return true;

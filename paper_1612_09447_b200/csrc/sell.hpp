@@ -101,6 +101,11 @@ struct HostSellS {
   std::vector<int> sinfo;       // [P][16] slot kind: u (0..7) own upper slot u; 8 + m lower slot whose
                                 // mirror is upper slot m of the common pattern; 16 lower slot without
                                 // such a mirror; -1 padding
+  // rows without bit 0x80 ("slow" rows, next to faces/edges): the mirror
+  // upper slot of each lower slot, 16 bytes per row, rows in order;
+  // slow_base[c] = slow rows before chunk c (a lane finds its row by a ballot)
+  std::vector<uint8_t> slow_code;  // [n_slow][16]
+  std::vector<int> slow_base;      // [n_chunks + 1]
 };
 constexpr int kSymSlots = 8;
 // false when the rows need more than 255 patterns or more than 32 slots

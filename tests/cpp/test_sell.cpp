@@ -99,10 +99,13 @@ static int check_sym(const HostCsr& a, const HostSellS& h, long* fast_rows) {
   long fast = 0;
   auto U64 = [&](int row, int u) { return h.uvals64[((size_t)(row / 32) * kSymSlots + u) * 32 + row % 32]; };
   auto U16 = [&](int row, int u) { return h.uvals[((size_t)(row / 32) * kSymSlots + u) * 32 + row % 32]; };
+  long slow_rank = -1;
   for (int r = 0; r < a.n_rows; ++r) {
     const int pf = h.spid[r], p = pf & 127, len = a.row_ptr[r + 1] - a.row_ptr[r];
     const bool spec = p == h.common && (pf & 0x80);
     fast += spec;
+    if (r % 32 == 0 && h.slow_base[r / 32] != slow_rank + 1) ++bad;
+    if (!(pf & 0x80)) ++slow_rank;
     for (int j = 0; j < 16; ++j) {
       const int off = h.pat[(size_t)p * 16 + j], kind = h.sinfo[(size_t)(spec ? h.common : p) * 16 + j];
       double v64 = 0.0;
@@ -113,14 +116,10 @@ static int check_sym(const HostCsr& a, const HostSellS& h, long* fast_rows) {
       } else if (kind >= 8) {
         const int c = r + off;
         int u = -1;
-        if (spec) {
-          u = kind - 8;
-        } else {
-          const int pc = h.spid[c] & 127;
-          for (int q = 0; q < 16; ++q)
-            if (h.pat[(size_t)pc * 16 + q] == -off && h.sinfo[(size_t)pc * 16 + q] >= 0 &&
-                h.sinfo[(size_t)pc * 16 + q] < 8)
-              u = h.sinfo[(size_t)pc * 16 + q];
+        if (pf & 0x80) {
+          u = kind - 8;  // every lower neighbour has the common pattern
+        } else {         // slow-row table: rows without bit 7 in order (k_rows.cu sym_dot)
+          u = h.slow_code[(size_t)slow_rank * 16 + j];
         }
         if (u < 0) {
           ++bad;

@@ -287,7 +287,7 @@ def test_stencil_vcycle_matches_packed():
     assert np.linalg.norm(x1 - xo) <= 1e-10 * np.linalg.norm(xo)
 
 
-def test_symmetric_half_storage_matches_full_stencil():
+def test_symmetric_half_storage_matches_full_stencil(monkeypatch):
     """SELL-SH (option 23): the fine operator stores upper slots only and reads
     each lower value from the mirror row. The PCG operator's products and their
     row order are unchanged, so q = M_II p is bit-identical to the full
@@ -295,6 +295,7 @@ def test_symmetric_half_storage_matches_full_stencil():
     rounding (the reduction grids of the two kernels differ). Boundary rows
     (x/y faces, edges, corners next to the Dirichlet planes) take the
     per-row path."""
+    monkeypatch.setenv("EQS_SELL_SH", "1")  # read at context creation
     cfg = cube(18, jitter=0.1, planes=(0.45, 0.55))
     g = eb.FemSystem(cfg)
     o = po.Problem(cfg)
