@@ -141,6 +141,55 @@ def ncu_traffic(config_name):
         return {}
 
 
+def fp64_csr_equivalent(g, iters, ms, steps, hbm, other_bytes, dense_rows):
+    """SURVEY.md §8d bytes of the same V-cycle passes if every operator were
+    fp64 CSR (12 B/entry + 4 B/row) with fp64 vectors, on the reference's
+    (unfiltered) Galerkin hierarchy: fine level 4 smoother/residual passes
+    (Chebyshev(2) pre and post), coarse levels 2 (Chebyshev(1)), restriction
+    and prolongation per level, dense solve of the first level with at most
+    `dense_rows` rows. Single-rank contexts only (host copies of P, R)."""
+    try:
+        L = len(g.amg_levels())
+        dims = [[tuple(int(v) for v in _level_dims(g, l, w)) for w in range(3)] for l in range(L)]
+    except Exception as e:  # noqa: BLE001 - reported in the line
+        return {"unavailable": str(e)}
+    total = 0.0
+    for l in range(L):
+        n_l, _, nnz_a = dims[l][0]
+        if n_l <= dense_rows or l == L - 1:
+            total += 8.0 * n_l * n_l + 16.0 * n_l
+            break
+        passes = 4 if l == 0 else 2
+        total += passes * (12.0 * nnz_a + 4.0 * (n_l + 1) + 32.0 * n_l)
+        nr, nc, nnz_r = dims[l][2]
+        total += 12.0 * nnz_r + 4.0 * (nr + 1) + 8.0 * nc + 8.0 * nr
+        npr, npc, nnz_p = dims[l][1]
+        total += 12.0 * nnz_p + 4.0 * (npr + 1) + 8.0 * npc + 16.0 * npr
+    n = dims[0][0][0]
+    nnz_m = dims[0][0][2]
+    spmv = 12.0 * nnz_m + 4.0 * (n + 1) + 16.0 * n
+    per_iter_pcg = spmv + 16.0 * n + 48.0 * n + 16.0 * n + 24.0 * n
+    vc_total = iters * total
+    step_bytes = (vc_total + iters * per_iter_pcg + other_bytes) / steps
+    return {"vcycle_bytes": total, "pcg_iteration_vector_and_spmv_bytes": per_iter_pcg,
+            "step_bytes": step_bytes,
+            "achieved_full_step": step_bytes * steps / (ms / 1e3) / 1e9,
+            "frac_full_step": step_bytes * steps / (ms / 1e3) / 1e9 / hbm,
+            "rule": "SURVEY.md §8d fp64-CSR formulas on the reference hierarchy (unfiltered A_l, explicit P/R), "
+                    "this V-cycle's pass counts, PCG canonical fused form; K(x)x/RKC/SPE bytes as counted"}
+
+
+def _level_dims(g, level, which):
+    import ctypes as C
+    dims = np.zeros(3, dtype=np.int32)
+    import paper_1612_09447_b200 as eb
+    rc = eb.load_library().eqs_amg_level_csr(g._h, C.c_int(level), C.c_int(which),
+                                             dims.ctypes.data_as(C.POINTER(C.c_int)), None, None, None)
+    if rc != 0:
+        raise RuntimeError(f"eqs_amg_level_csr rc {rc}")
+    return dims
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -309,6 +358,9 @@ def run_reference(args):
 def apply_options(g, args):
     if args.vcycle_values:
         g.set_option(4, {"fp64": 0, "fp32": 1, "bf16": 2}[args.vcycle_values])
+    for kv in args.opt or []:  # eqs_set_option keys (include/eqs_b200.h), for sweeps
+        k, v = kv.split("=")
+        g.set_option(int(k), float(v))
 
 
 def single_gpu_system(args, estimator=None):
@@ -376,6 +428,65 @@ def run_euler_vs_rkc(args):
             / out["euler"]["simulated_s_per_wall_s"],
             "config": {"workload": f"{args.config} cube, x0 = 2e4*random_vec(31), {n} free dofs",
                        "n_free": n}, "setup_s": t_setup, **out}
+    print(json.dumps(line), flush=True)
+
+
+def run_sdirk_vs_rkc(args):
+    """Explicit vs implicit time to t_end (§V, Fig. 2): adaptive RKC
+    (rkc_step, tol 1e-2, integrators.cpp:177-225) against adaptive SDIRK3(2)
+    (sdirk_step, tol 1e-2, Newton 1e-8, integrators.cpp:297-327) whose shifted
+    system M + gamma dt K(z) is re-assembled every Newton iteration and
+    preconditioned with the SA-AMG rebuilt on the device once per step (the
+    reference's make_preconditioner refresh, fem_system.cpp:124-145), and with
+    Jacobi as a third arm. Same state, one GPU, device time (CUDA events)."""
+    import ctypes as C
+    import torch
+
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    g, t_setup, eb = single_gpu_system(args)
+    n = g.n_free
+    lib = eb.load_library()
+    x0 = np.zeros(n)
+    lib.eqs_random_vec(C.c_int(n), C.c_uint(31), x0.ctypes.data_as(C.POINTER(C.c_double)))
+    x0 *= 2e4
+    sp = C.c_void_p()
+    lib.eqs_get_stream(g._h, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value, device=torch.device("cuda", 0))
+    t_end, cap = args.t_end, 2000
+    out = {}
+    for name, step, opt in (("rkc", lambda: g.rkc_step(rtol=1e-2, atol=1e-8), None),
+                            ("sdirk_amg", lambda: g.sdirk_step(rtol=1e-2, atol=1e-8, newton_tol=1e-8), 1),
+                            ("sdirk_jacobi", lambda: g.sdirk_step(rtol=1e-2, atol=1e-8, newton_tol=1e-8), 0)):
+        if opt is not None:
+            g.set_option(26, opt)
+        g.set_state(0.0, x0, 1e-5)
+        st0 = g.stats()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        ev0.record(stream)
+        t, acc, rej = 0.0, 0, 0
+        while t < t_end and acc + rej < cap:
+            a = step()
+            acc += a.accepted
+            rej += not a.accepted
+            t = a.t_start + (a.dt if a.accepted else 0.0)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        st1 = g.stats()
+        d = {k: st1[k] - st0[k] for k in ("m_solves", "pcg_iterations", "newton_linear_solves",
+                                            "newton_pcg_iterations", "precond_setups", "assemblies")}
+        out[name] = {"t_reached": t, "accepted": acc, "rejected": rej, "device_s": ev0.elapsed_time(ev1) / 1e3,
+                     "wall_s": wall, **d}
+    line = {"metric": "explicit RKC vs implicit SDIRK3(2): time to t_end (PAPER.md Fig. 2)",
+            "value": out["sdirk_amg"]["wall_s"] / out["rkc"]["wall_s"], "unit": "speed-up of RKC over SDIRK+AMG",
+            "n_gpus": 1, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} cube, x0 = 2e4*random_vec(31), {n} free dofs, t_end {t_end}",
+                       "n_free": n}, "setup_s": t_setup,
+            "rkc_over_sdirk_jacobi": out["sdirk_jacobi"]["wall_s"] / out["rkc"]["wall_s"], **out}
     print(json.dumps(line), flush=True)
 
 
@@ -499,6 +610,19 @@ def run_b200(args):
     torch.cuda.synchronize()
     timing = g.timing()
     g.timing(False)
+    # third pass, graph path: the graph-resident PCG (the timed region's code
+    # path) as one event region per solve (class 6), the other classes as above
+    g.set_option(24, 1)
+    st_g0 = g.stats()
+    g.timing(True)
+    g.timing_reset()
+    for _ in range(args.steps):
+        g.rkc_advance_fixed(dt, S_STAGES, 1)
+    torch.cuda.synchronize()
+    timing_g = g.timing()
+    g.timing(False)
+    g.set_option(24, 0)
+    iters_g = g.stats()["pcg_iterations"] - st_g0["pcg_iterations"]
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -547,7 +671,7 @@ def run_b200(args):
                2: "AMG V-cycle: stencil-coded SELL-S (fine level) and packed SELL-P (transfers, coarse levels) bf16 "
                   "smoother/residual/transfer row kernels, dense coarse GEMV"}
 
-    def roof(c):
+    def roof(c, timing=timing):
         if not (timing["launches"][c] and timing["bytes"][c]):
             return None
         avg_ms = timing["ms"][c] / timing["launches"][c]
@@ -560,11 +684,40 @@ def run_b200(args):
                 "share_of_step": timing["ms"][c] / sum(timing["ms"][:6]),
                 "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"}
 
+    # graph path (what the timed region runs): the whole PCG loop per solve is
+    # one event region (class 6); its V-cycle / SpMV+vectors split is the
+    # host-loop pass's time ratio, its bytes are the captured body's bytes
+    # (iterations x (V-cycle + direction + SpMV + update)), the V-cycle part
+    # is iterations x the V-cycle's algorithmic bytes
+    v_per = timing["bytes"][2] / max(1, timing["launches"][2])
+    host_vp = timing["ms"][1] + timing["ms"][2]
+    vshare = timing["ms"][2] / host_vp if host_vp else 0.0
+    g_ms = list(timing_g["ms"])
+    g_by = list(timing_g["bytes"])
+    g_ms[2] = g_ms[2] + vshare * g_ms[6]
+    g_ms[1] = g_ms[1] + (1.0 - vshare) * g_ms[6]
+    g_by[2] = g_by[2] + iters_g * v_per
+    g_by[1] = g_by[1] + max(0.0, g_by[6] - iters_g * v_per)
+    g_n = list(timing_g["launches"])
+    g_n[2] = g_n[2] + iters_g
+    g_n[1] = g_n[1] + 2 * iters_g
+    timing_graph = {"ms": g_ms[:6], "bytes": g_by[:6], "launches": g_n[:6]}
+
+    def roof_g(c):
+        r = roof(c, timing_graph)
+        if r:
+            r["time_source"] = ("graph path: CUDA events around each graph-resident PCG solve; its V-cycle share "
+                                f"({vshare:.3f}) from the host-loop pass")
+        return r
+
     # the dominant class (largest device time) is the headline roofline
-    cls = max(range(3), key=lambda c: timing["ms"][c])
-    dom = roof(cls)
-    others = {names[c]: roof(c) for c in range(3) if c != cls}
+    cls = max(range(3), key=lambda c: timing_graph["ms"][c])
+    dom = roof_g(cls)
+    others = {names[c]: roof_g(c) for c in range(3) if c != cls}
+    host_loop = {names[c]: roof(c) for c in range(3)}
     n_tets, nnz_mass, amg_levels = g.n_tets, g.nnz_mass_free, g.amg_levels()
+    csr64 = (fp64_csr_equivalent(g, iters_g, ms, args.steps, hbm, g_by[0] + g_by[3] + g_by[4] + g_by[5],
+                                 DENSE_COARSE if DENSE_COARSE is not None else 512) if world == 1 else None)
     cpu = parity = None
     if world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
@@ -607,15 +760,24 @@ def run_b200(args):
         "gpu_launches": launches,
         "roofline": dom,
         "roofline_other_classes": others,
+        "roofline_host_loop": host_loop,
         # whole step: all classes' algorithmic bytes of the
-        # instrumented pass / the un-instrumented step time (both K steps)
-        "roofline_full_step": {"bound": "hbm", "achieved": sum(timing["bytes"][:6]) / (ms / 1e3) / 1e9,
+        # graph-path pass / the un-instrumented step time (both K steps)
+        "roofline_full_step": {"bound": "hbm", "achieved": sum(timing_graph["bytes"]) / (ms / 1e3) / 1e9,
                                "peak": hbm, "unit": "GB/s",
-                               "frac": sum(timing["bytes"][:6]) / (ms / 1e3) / 1e9 / hbm,
-                               "frac_vs_8tbs_spec": sum(timing["bytes"][:6]) / (ms / 1e3) / 8e12},
-        "time_by_class_ms": {names[c]: timing["ms"][c] for c in range(6)},
-        "time_by_class_source": "CUDA events per kernel class in a second pass of K steps after the timed region",
-        "bytes_by_class": {names[c]: timing["bytes"][c] for c in range(6)},
+                               "frac": sum(timing_graph["bytes"]) / (ms / 1e3) / 1e9 / hbm,
+                               "frac_vs_8tbs_spec": sum(timing_graph["bytes"]) / (ms / 1e3) / 8e12,
+                               "bytes_per_step": sum(timing_graph["bytes"]) / args.steps},
+        "bytes_counted_as": ("algorithmic bytes of the stored formats: bf16 SELL-S at 2 B/entry + 1 B/row and "
+                             "packed SELL-P at 4 B/entry in the V-cycle, fp64 SELL-S at 8 B/entry for M_II, "
+                             "SURVEY.md §8d per-tet/per-dof figures for K(x)x; fp32 V-cycle vectors"),
+        "fp64_csr_equivalent": csr64,
+        "time_by_class_ms": {names[c]: timing_graph["ms"][c] for c in range(6)},
+        "time_by_class_source": ("graph path (third pass of K steps): CUDA events around K(x)x, SPE, RKC and each "
+                                 "whole graph-resident PCG solve; PCG split into V-cycle / SpMV+vectors by the "
+                                 "host-loop pass (second pass, per-class events)"),
+        "time_by_class_host_loop_ms": {names[c]: timing["ms"][c] for c in range(6)},
+        "bytes_by_class": {names[c]: timing_graph["bytes"][c] for c in range(6)},
         "cpu_baseline": cpu,
         "parity": parity,
         "parity_rel": parity["rel_l2_gpu_vs_reference"] if parity else None,
@@ -642,7 +804,9 @@ def main():
                     help="MRHS start vectors (proj/src/start_vector.cpp); the reference nonlinear scenario uses spe")
     ap.add_argument("--vcycle-values", default=None, choices=["fp64", "fp32", "bf16"],
                     help="V-cycle matrix value precision (library default when omitted)")
-    ap.add_argument("--mode", default="rkc", choices=["rkc", "euler", "mrhs"],
+    ap.add_argument("--opt", action="append", help="KEY=VALUE eqs_set_option before the run (repeatable)")
+    ap.add_argument("--t-end", type=float, default=1e-3, help="--mode sdirk: simulated interval")
+    ap.add_argument("--mode", default="rkc", choices=["rkc", "euler", "mrhs", "sdirk"],
                     help="rkc: the headline line (default); euler: config 2 Euler vs RKC on --config (c2); "
                          "mrhs: config 5 multiple-right-hand-side sequence on --config")
     args = ap.parse_args()
@@ -664,6 +828,8 @@ def main():
         run_euler_vs_rkc(args)
     elif args.mode == "mrhs":
         run_mrhs(args)
+    elif args.mode == "sdirk":
+        run_sdirk_vs_rkc(args)
     else:
         run_b200(args)
 

@@ -160,7 +160,9 @@ typedef struct {
 /* Device time per kernel class (CUDA events on the context stream), ms and
  * launches, accumulated since the last eqs_timing_reset. Classes:
  * 0 stiffness K(x)v, 1 PCG SpMV+vectors, 2 V-cycle, 3 RKC stage/error,
- * 4 SPE estimator, 5 boundary/lift. Only collected when enabled. */
+ * 4 SPE estimator, 5 boundary/lift, 6 whole graph-resident PCG loop (V-cycle +
+ * SpMV + vectors; only with option 24, which keeps the graph loop while timing).
+ * Only collected when enabled. */
 typedef struct {
   double ms[8];
   long launches[8];
@@ -350,7 +352,12 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * slots only and read lower values from the mirror rows; bit-identical products,
  * about half the matrix bytes, but slower on B200: DESIGN.md §8),
  * 13 = smoother polynomial (0 first-kind Chebyshev, 1 fourth-kind, 2 fourth-kind
- * with optimised weights), 14 = lambda_max safety factor (default 1.1).
+ * with optimised weights), 14 = lambda_max safety factor (default 1.1),
+ * 24 = per-class timing keeps the graph-resident PCG loop (0/1; default 0: the
+ * whole loop is timed as class 6 instead of classes 1 and 2), 26 = SDIRK shifted
+ * solves preconditioned by an SA-AMG of the shifted matrix rebuilt on the device
+ * at every preconditioner refresh (1, default, with solver.preconditioner amg) or
+ * by Jacobi (0).
  * The PCG operator and vectors are fp64 in every setting. */
 int eqs_set_option(eqs_ctx* ctx, int key, double value);
 /* The CUDA stream (cudaStream_t) every device call of this context runs on. */

@@ -686,6 +686,8 @@ int eqs_set_option(eqs_ctx* ctx, int key, double value) {
       case 21: g_pdl = value != 0.0; g.invalidate_graphs(); break;
       case 22: g.pcg_graph_multi = value != 0.0; g.invalidate_graphs(); break;
       case 23: g.set_stencil_sym(value != 0.0); break;
+      case 24: g.timing_graph = value != 0.0; break;
+      case 26: g.shift_amg = value != 0.0; break;
       default: throw std::invalid_argument("eqs_set_option: unknown key");
     }
   });

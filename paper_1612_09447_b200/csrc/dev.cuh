@@ -150,6 +150,7 @@ struct KxDev {
   const int* lout = nullptr;
   double* partials = nullptr;
   const int *bdof = nullptr, *bptr = nullptr, *bpart = nullptr;
+  const double *bxy = nullptr, *bz = nullptr;  // P1: coordinates per block-dof entry ({x, y} pairs, z)
 };
 void launch_kx_blocked(const KxDev& k, const double* coords, const double* x_state, const double* v,
                        const double* base, double sign, int n_out, double* out, int* geo_error, cudaStream_t s);
@@ -268,6 +269,8 @@ void launch_k_element(int order, int n_tets, const int* tet_dofs, const unsigned
 void launch_shift_gather(long nnz, const long* ptr, const long* src, const double* S, const double* m, double gdt,
                          double* shifted, cudaStream_t s);
 void launch_csr_diag(int n, const int* rp, const int* ci, const double* v, double* d, cudaStream_t s);
+void launch_recip(int n, const double* d, double* inv, cudaStream_t s);  // inv = 1 / d
+
 void launch_jacobi_div(int n, const double* d, const double* r, double* z, Reducer red, int slot, cudaStream_t s);
 void launch_weighted_sq(int n, const double* est, const double* x, const double* xn, double atol, double rtol,
                         Reducer red, int slot, cudaStream_t s);

@@ -8,6 +8,7 @@
 // (restrict_free, :17-20) is free. With one rank the owned set is every free
 // dof in DofMap::free_dofs order and there are no ghosts.
 #include "gpu_system.hpp"
+#include "amg_device.hpp"
 #include "element.hpp"
 #include "kxblock.hpp"
 #include "sell.hpp"
@@ -20,7 +21,19 @@
 #include <random>
 #include <type_traits>
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace eqsb {
+
+struct GpuSystem::ShiftAmg {
+  SpgemmDevice sd;
+  std::vector<DCsr> A, P, R;
+  std::vector<DevLevel> levels;
+  int coarse_n = 0;
+  DevBuf<double> inv;
+  DevBuf<float> inv32;
+  int builds = 0;
+};
 
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
@@ -57,11 +70,22 @@ template struct DevBuf<unsigned long long>;
 
 namespace {
 using clk = std::chrono::steady_clock;
+// Host wall time of a phase bucket (the reference's metrics.cpp phases:
+// residual / estimator / solve / setup) plus an NVTX range of the same name,
+// so profilers can attribute kernels to the buckets.
 struct PhaseTimer {
   double& slot;
   clk::time_point t0;
-  explicit PhaseTimer(double& s) : slot(s), t0(clk::now()) {}
-  ~PhaseTimer() { slot += std::chrono::duration<double>(clk::now() - t0).count(); }
+  PhaseTimer(double& s, const char* name) : slot(s), t0(clk::now()) { nvtxRangePushA(name); }
+  ~PhaseTimer() {
+    nvtxRangePop();
+    slot += std::chrono::duration<double>(clk::now() - t0).count();
+  }
+};
+
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 // threads per row: enough that each thread handles <= 8 entries (one batch of
@@ -254,7 +278,7 @@ std::vector<double> inv_diagonal(const HostCsr& a) {
 
 GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     : prob_(std::move(p)), device_(device), comm_(comm ? std::move(comm) : std::make_unique<SelfComm>()) {
-  PhaseTimer timer(stats_.t_setup);
+  PhaseTimer timer(stats_.t_setup, "setup");
   if (device_ >= 0) {
     CK(cudaSetDevice(device_));
     CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -464,7 +488,7 @@ void GpuSystem::build_device() {
     CK(cudaMemcpy(c4.data(), coords_.p, sizeof(double) * c4.size(), cudaMemcpyDeviceToHost));
     KxBlocks kb = build_kx_blocks(td, nl, n_tets_loc_, c4, n_full_, bt);
     std::vector<int> btd((size_t)std::max(1, n_tets_loc_) * nl);
-    std::vector<unsigned char> btm(std::max(1, n_tets_loc_));
+    std::vector<unsigned char> btm(std::max(1, n_tets_loc_) + 4, 0);  // k_kx_block4 copies whole words
     for (int k = 0; k < n_tets_loc_; ++k) {
       const int t = kb.tet_perm[k];
       for (int i = 0; i < nl; ++i) btd[(size_t)nl * k + i] = td[(size_t)nl * t + i];
@@ -476,6 +500,15 @@ void GpuSystem::build_device() {
     };
     if (nl == 4) {
       up(kb_tloc_, kb.tet_local);
+      // coordinates per block-dof entry, streamed by k_kx_block4 instead of gathered
+      const size_t nld = kb.ldof_dof.size();
+      std::vector<double> bc(3 * std::max<size_t>(1, nld));
+      for (size_t i = 0; i < nld; ++i) {  // [nld] {x, y} pairs, then [nld] z
+        bc[2 * i] = c4[4 * (size_t)kb.ldof_dof[i]];
+        bc[2 * i + 1] = c4[4 * (size_t)kb.ldof_dof[i] + 1];
+        bc[2 * nld + i] = c4[4 * (size_t)kb.ldof_dof[i] + 2];
+      }
+      up(kb_bxyz_, bc);
     } else {
       up(kb_tets_, btd);
     }
@@ -509,6 +542,11 @@ void GpuSystem::build_device() {
     kxd_.bdof = kb_bdof_.p;
     kxd_.bptr = kb_bptr_.p;
     kxd_.bpart = kb_bpart_.p;
+    if (nl == 4 && !getenv("EQS_KX_GENERIC")) {
+      const size_t nld = kb.ldof_dof.size();
+      kxd_.bxy = kb_bxyz_.p;
+      kxd_.bz = kb_bxyz_.p + 2 * nld;
+    }
     kx_partials_ = kb.n_partials;
     kx_ldofs_ = (long)kb.ldof_out.size();
     kx_slots_ = (long)kb.slots.size();
@@ -732,14 +770,19 @@ void GpuSystem::set_cheb(double ratio) {
       lv.cheb1 = ChebCoef{0.0, 0.0, b11 * 4.0 / (3.0 * lmax)};
       continue;
     }
-    const double lmin = lmax / ratio;
-    const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
-    const double sigma = theta / delta, rho0 = 1.0 / sigma, rho1 = 1.0 / (2.0 * sigma - rho0);
-    lv.cheb.c0 = (1.0 + rho1 * rho0) / theta;
-    lv.cheb.c1 = 2.0 * rho1 / delta;
-    lv.cheb.inv_theta = 1.0 / theta;
-    lv.cheb1 = ChebCoef{0.0, 0.0, 1.0 / theta};
+    cheb_first_kind(lmax, ratio, lv);
   }
+}
+
+// first-kind Chebyshev on [lmax/ratio, lmax]: degree-2 and degree-1 coefficients
+void cheb_first_kind(double lmax, double ratio, DevLevel& lv) {
+  const double lmin = lmax / ratio;
+  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
+  const double sigma = theta / delta, rho0 = 1.0 / sigma, rho1 = 1.0 / (2.0 * sigma - rho0);
+  lv.cheb.c0 = (1.0 + rho1 * rho0) / theta;
+  lv.cheb.c1 = 2.0 * rho1 / delta;
+  lv.cheb.inv_theta = 1.0 / theta;
+  lv.cheb1 = ChebCoef{0.0, 0.0, 1.0 / theta};
 }
 
 void GpuSystem::invalidate_graphs() {
@@ -859,6 +902,7 @@ void GpuSystem::tic(int cls) {
     return;
   }
   open_cls_ = cls;
+  open_bytes_ = g_algo_bytes;
   open_ev_ = get_event();
   CK(cudaEventRecord(open_ev_, stream_));
 }
@@ -869,6 +913,7 @@ void GpuSystem::toc(int cls, double bytes) {
     return;
   }
   (void)cls;
+  if (bytes < 0.0) bytes = g_algo_bytes - open_bytes_;  // launchers' own byte counts since tic
   cudaEvent_t b = get_event();
   CK(cudaEventRecord(b, stream_));
   events_.push_back({open_ev_, b, open_cls_, bytes});
@@ -1343,10 +1388,14 @@ PcgResult GpuSystem::pcg_dev_graph(const double* b, bool use_x0, const double* x
   st[7] = use_x0 ? -1.0 : bnorm * bnorm;
   st[8] = 0.0;
   CK(cudaMemcpyAsync(pcg_stat_.p, st, sizeof(double) * 9, cudaMemcpyHostToDevice, stream_));
+  tic(TC_PCG_GRAPH);
   CK(cudaGraphLaunch(loop, stream_));
+  toc(TC_PCG_GRAPH, 0.0);
   CK(cudaMemcpyAsync(st, pcg_stat_.p, sizeof(double) * 9, cudaMemcpyDeviceToHost, stream_));
   sync();
   const int k_end = (int)st[0];
+  if (timing_on && !events_.empty() && events_.back().cls == TC_PCG_GRAPH)
+    events_.back().bytes = (double)k_end * pcg_body_bytes_;
   const int status = (int)st[1];
   g_launch_count += 1 + (long)k_end * pcg_body_kernels_;
   g_algo_bytes += (double)k_end * pcg_body_bytes_;
@@ -1386,7 +1435,7 @@ PcgResult GpuSystem::pcg_dev(const double* b, const double* x0, double* x, doubl
   // same tests on the same scalars, evaluated on the device.
   // multi-rank: only on capturable (NCCL) communicators, whose halo and
   // allreduce calls are captured into the loop body
-  const bool graph_loop = pcg_graph_loop && use_graphs && !timing_on && prob_.solver.precond == 2 &&
+  const bool graph_loop = pcg_graph_loop && use_graphs && (!timing_on || timing_graph) && prob_.solver.precond == 2 &&
                           comm_->capturable() && device_ >= 0 && max_iter >= 1 &&
                           (comm_->size() == 1 || pcg_graph_multi);
   launch_dot(n, b, b, red_, S_BB, stream_);
@@ -1919,7 +1968,7 @@ bool GpuSystem::estimator_next(const double* b, double* x0) {
   if (mode >= 3) {
     tic(TC_SPE);
     const bool nz = pod_start(b, x0);
-    toc(TC_SPE, 0.0);
+    toc(TC_SPE, -1.0);
     return nz;
   }
   if (history_.empty()) return false;
@@ -1932,7 +1981,7 @@ bool GpuSystem::estimator_next(const double* b, double* x0) {
   const int m = spe_k_;
   estimator_rank_ = m;
   if (m == 0) {
-    toc(TC_SPE, 0.0);
+    toc(TC_SPE, -1.0);
     return false;
   }
   // spe_start (start_vector.cpp:33-62): x0 = V (V'MV)^-1 V' b with the pivoted LDLT of G
@@ -1950,7 +1999,7 @@ bool GpuSystem::estimator_next(const double* b, double* x0) {
   if (!ok) {
     ++stats_.spe_fallbacks;
     std::fprintf(stderr, "start_vector: singular reduced system, zero start used\n");
-    toc(TC_SPE, 0.0);
+    toc(TC_SPE, -1.0);
     return false;
   }
   std::vector<double> ginv((size_t)m * m), e(m), col(m);
@@ -1973,7 +2022,7 @@ bool GpuSystem::estimator_next(const double* b, double* x0) {
     y.c[r] = s;
   }
   launch_lincomb(n, m, V.data(), y, x0, stream_);
-  toc(TC_SPE, 0.0);
+  toc(TC_SPE, -1.0);
   return true;
 }
 
@@ -2027,7 +2076,7 @@ void GpuSystem::estimator_feedback(const double* x, int iterations) {
       tic(TC_SPE);
       spe_alloc((int)window);
       spe_append(buf);
-      toc(TC_SPE, 0.0);
+      toc(TC_SPE, -1.0);
     }
   }
 }
@@ -2036,17 +2085,17 @@ void GpuSystem::estimator_feedback(const double* x, int iterations) {
 PcgResult GpuSystem::eval_rhs_dev(double t, double* x_full, double* f) {
   double* b = w_free_a_.p;
   {
-    PhaseTimer pt(stats_.t_residual);
+    PhaseTimer pt(stats_.t_residual, "residual");
     residual_dev(t, x_full, b);
   }
   bool has_x0;
   {
-    PhaseTimer pt(stats_.t_estimator);
+    PhaseTimer pt(stats_.t_estimator, "estimator");
     has_x0 = estimator_next(b, f);
   }
   PcgResult res;
   {
-    PhaseTimer pt(stats_.t_solve);
+    PhaseTimer pt(stats_.t_solve, "solve");
     res = pcg_dev(b, has_x0 ? f : nullptr, f, prob_.solver.rel_tol, prob_.solver.max_iter);
   }
   if (!res.converged) {
@@ -2055,7 +2104,7 @@ PcgResult GpuSystem::eval_rhs_dev(double t, double* x_full, double* f) {
     throw NumericalError(buf);
   }
   {
-    PhaseTimer pt(stats_.t_estimator);
+    PhaseTimer pt(stats_.t_estimator, "estimator");
     estimator_feedback(f, res.iterations);
   }
   ++stats_.m_solves;
@@ -2069,7 +2118,7 @@ void GpuSystem::apply_minv_stiffness_dev(double t, double* x_full, const double*
   double* vfull = w_full_b_.p;
   double* kv = w_free_b_.p;
   {
-    PhaseTimer pt(stats_.t_residual);
+    PhaseTimer pt(stats_.t_residual, "residual");
     lift_dev(t, x_full);
     halo(halo0_, x_full);
     CK(cudaMemcpyAsync(vfull, v_own, sizeof(double) * n_own_, cudaMemcpyDeviceToDevice, stream_));
@@ -2085,7 +2134,7 @@ void GpuSystem::apply_minv_stiffness_dev(double t, double* x_full, const double*
     toc(TC_STIFF, kx_bytes());
     check_kernel_flags();
   }
-  PhaseTimer pt(stats_.t_solve);
+  PhaseTimer pt(stats_.t_solve, "solve");
   PcgResult res = pcg_dev(kv, nullptr, y, prob_.solver.rho_solve_tol, prob_.solver.max_iter);
   ++stats_.rho_solves;
   stats_.rho_pcg_iterations += res.iterations;
@@ -2163,7 +2212,7 @@ void GpuSystem::kx_residual_host(const double* x_full, const double* b_mass, dou
 
 void GpuSystem::eval_residual_host(double t, const double* x, double* r) {
   require_single("eval_residual");
-  PhaseTimer pt(stats_.t_residual);
+  PhaseTimer pt(stats_.t_residual, "residual");
   double* xf = w_full_b_.p;
   CK(cudaMemcpyAsync(xf, x, sizeof(double) * n_own_, cudaMemcpyHostToDevice, stream_));
   residual_dev(t, xf, w_free_b_.p);
@@ -2185,7 +2234,7 @@ PcgResult GpuSystem::mass_solve_host(const double* b, const double* x0, double t
   require_single("mass_solve");
   F0_.upload(b, n_own_, stream_);
   if (x0) Fn_.upload(x0, n_own_, stream_);
-  PhaseTimer pt(stats_.t_solve);
+  PhaseTimer pt(stats_.t_solve, "solve");
   PcgResult r = pcg_dev(F0_.p, x0 ? Fn_.p : nullptr, F_.p, tol, max_iter);
   F_.download(x, n_own_, stream_);
   sync();
@@ -2198,7 +2247,7 @@ int GpuSystem::estimator_next_host(const double* b, double* x0) {
   F0_.upload(b, n_own_, stream_);
   int rank = 0;
   {
-    PhaseTimer pt(stats_.t_estimator);
+    PhaseTimer pt(stats_.t_estimator, "estimator");
     estimator_next_dev(F0_.p, F_.p, &rank);
   }
   F_.download(x0, n_own_, stream_);
@@ -2208,7 +2257,7 @@ int GpuSystem::estimator_next_host(const double* b, double* x0) {
 void GpuSystem::estimator_feedback_host(const double* x, int iterations) {
   require_single("estimator_feedback");
   F_.upload(x, n_own_, stream_);
-  PhaseTimer pt(stats_.t_estimator);
+  PhaseTimer pt(stats_.t_estimator, "estimator");
   estimator_feedback(F_.p, iterations);
   sync();
 }
@@ -2344,6 +2393,7 @@ static double* rkc_stages(GpuSystem& g, double t, double dt, const RkcCoefficien
 
 // rkc_step (proj/src/integrators.cpp:177-225)
 StepAttempt GpuSystem::rkc_step(const RkcOptions& o) {
+  NvtxRange nv("rkc_step");
   StepAttempt att;
   att.t_start = state_t;
   const double rho = spectral_radius_cached(o.rho_refresh_every);
@@ -2409,6 +2459,7 @@ StepAttempt GpuSystem::rkc_step(const RkcOptions& o) {
 
 // rkc_advance_fixed (proj/src/integrators.cpp:227-235)
 void GpuSystem::rkc_advance_fixed(double dt, int s) {
+  NvtxRange nv("rkc_step");
   const RkcCoefficients& k = rkc_coefficients(s);
   double* bufs[3];
   int bi = 0;
@@ -2510,23 +2561,158 @@ void GpuSystem::build_shift_map() {
   shift_built_ = true;
 }
 
+// SA-AMG of the shifted matrix M_II + gdt K_II(z) (make_preconditioner,
+// proj/src/fem_system.cpp:38-46 -> AmgPreconditioner, proj/src/amg.cpp:90-143),
+// rebuilt on the device at every refresh: strength graph, greedy aggregation,
+// P_tent, lambda_max, P = (I - omega/lambda D^-1 A) P_tent, R = P^T and
+// R (A P) with the k_amgsetup.cu / k_spgemm.cu kernels (bit-identical to the
+// host algorithm), the coarsest level (<= amg_coarse_limit rows) as an explicit
+// inverse of its pivoted LDLT. Nothing leaves the device but the coarsest
+// matrix. The V-cycle is vcycle_t<double> over fp64 CSR levels with the
+// Chebyshev smoothers of the mass V-cycle.
+
+void GpuSystem::build_shift_amg() {
+  if (!sh_amg_) {
+    sh_amg_ = std::make_unique<ShiftAmg>();
+    sh_amg_->sd.init(device_);
+  }
+  ShiftAmg& S = *sh_amg_;
+  cudaStream_t s = S.sd.stream();
+  CK(cudaStreamSynchronize(stream_));  // the shifted values were written on the context stream
+  S.levels.clear();
+  S.A.clear();
+  S.P.clear();
+  S.R.clear();
+  const SolverParams& sp = prob_.solver;
+  const long long batch = 1ll << 28;
+  {
+    S.A.emplace_back();
+    DCsr& a0 = S.A.back();
+    a0.rows = a0.cols = sh_csr_.n_rows;
+    a0.nnz = sh_csr_.nnz;
+    a0.rp.alloc(a0.rows + 1);
+    a0.ci.alloc(std::max<long long>(1, a0.nnz));
+    a0.v.alloc(std::max<long long>(1, a0.nnz));
+    CK(cudaMemcpyAsync(a0.rp.p, sh_csr_.row_ptr, sizeof(int) * (a0.rows + 1), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(a0.ci.p, sh_csr_.col_idx, sizeof(int) * a0.nnz, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(a0.v.p, sh_csr_.values, sizeof(double) * a0.nnz, cudaMemcpyDeviceToDevice, s));
+  }
+  dev_check_diagonal(S.A[0], s);
+  std::vector<double> lam;
+  while ((int)S.A.size() < sp.amg_max_levels && S.A.back().rows > sp.amg_coarse_limit) {
+    const DCsr& a = S.A.back();
+    DevBuf<double> d;
+    dev_diagonal(a, d, s);
+    DevBuf<int> agg;
+    const int n_agg = dev_aggregate(a, d.p, sp.amg_theta, agg, s);
+    if (n_agg >= a.rows) break;  // coarsening stalled (amg.cpp:102)
+    DCsr pt, p, r, ap, c;
+    dev_tentative(agg, a.rows, n_agg, pt, s);
+    const double lm = dev_lambda_max(a, d.p, 10, 20240811u, s);
+    S.sd.multiply(a, pt, p, d.p, sp.amg_omega / lm, batch);
+    dev_transpose(p, r, s);
+    S.sd.multiply(a, p, ap, nullptr, 0.0, batch);
+    S.sd.multiply(r, ap, c, nullptr, 0.0, batch);
+    dev_check_diagonal(c, s);
+    lam.push_back(lm);
+    S.P.push_back(std::move(p));
+    S.R.push_back(std::move(r));
+    S.A.push_back(std::move(c));
+  }
+  // coarsest: explicit inverse of the pivoted LDLT (amg.cpp:138-141 + DESIGN.md §4.5)
+  HostCsr hc;
+  S.sd.download(S.A.back(), hc);
+  const std::vector<double> inv = dense_inverse(hc);
+  S.coarse_n = hc.n_rows;
+  S.inv.alloc(std::max<size_t>(1, inv.size()));
+  S.inv.upload(inv.data(), inv.size(), s);
+  S.inv32.alloc(1);
+  const int L = (int)S.A.size();
+  S.levels.resize(L);
+  auto view = [](DCsr& m) {
+    DevCsr v;
+    v.n_rows = m.rows;
+    v.n_cols = m.cols;
+    v.nnz = m.nnz;
+    v.row_ptr = m.rp.p;
+    v.col_idx = m.ci.p;
+    v.values = m.v.p;
+    const double avg = m.rows ? (double)m.nnz / m.rows : 0.0;
+    int t = 1;
+    while (t < 32 && t * 8 < avg) t <<= 1;
+    v.tpr = t;
+    return v;
+  };
+  for (int l = 0; l < L; ++l) {
+    DevLevel& lv = S.levels[l];
+    const int n = S.A[l].rows;
+    lv.n_own = lv.n_loc = lv.n_global = n;
+    lv.A = view(S.A[l]);
+    const size_t nb = std::max(1, n);
+    lv.b.alloc(nb);
+    lv.z.alloc(nb);
+    lv.z2.alloc(nb);
+    lv.t.alloc(nb);
+    if (l + 1 < L) {
+      lv.P = view(S.P[l]);
+      lv.R = view(S.R[l]);
+      DevBuf<double> d;
+      dev_diagonal(S.A[l], d, s);
+      lv.invd.alloc(nb);
+      launch_recip(n, d.p, lv.invd.p, s);
+      CK(cudaStreamSynchronize(s));
+      // smoother bound: the setup's 10-step lambda_max(D^-1 A) estimate (amg.cpp:28-45)
+      lv.lambda_smoother = lam[l];
+      cheb_first_kind(cheb_scale * lv.lambda_smoother, cheb_ratio, lv);
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  ++S.builds;
+}
+
+// one V-cycle of the shifted hierarchy on r (fp64): z, and r.z in S_RZ
+double* GpuSystem::shift_vcycle(const double* r) {
+  ShiftAmg& S = *sh_amg_;
+  std::swap(levels_, S.levels);
+  std::swap(coarse_n_, S.coarse_n);
+  std::swap(coarse_inv_, S.inv);
+  std::swap(coarse_inv32_, S.inv32);
+  double* z = nullptr;
+  try {
+    z = vcycle_t<double>(0, r, true, nullptr, nullptr, nullptr);
+  } catch (...) {
+    std::swap(levels_, S.levels);
+    std::swap(coarse_n_, S.coarse_n);
+    std::swap(coarse_inv_, S.inv);
+    std::swap(coarse_inv32_, S.inv32);
+    throw;
+  }
+  std::swap(levels_, S.levels);
+  std::swap(coarse_n_, S.coarse_n);
+  std::swap(coarse_inv_, S.inv);
+  std::swap(coarse_inv32_, S.inv32);
+  return z;
+}
+
 void GpuSystem::shifted_solve_dev(double t, double* z_full, double gdt, const double* rhs, double* delta,
                                   bool refresh) {
   build_shift_map();
   const int n = n_own_;
   {
-    PhaseTimer pt(stats_.t_setup);
+    PhaseTimer pt(stats_.t_setup, "setup");
     lift_dev(t, z_full);
     launch_k_element(order_, n_tets_loc_, tet_dofs_.p, tet_mat_.p, coords_.p, z_full, sh_S_.p, sh_err_.p, stream_);
     ++stats_.assemblies;
     launch_shift_gather(sh_csr_.nnz, sh_ptr_.p, sh_src_.p, sh_S_.p, mii_v_.p, gdt, sh_vals_.p, stream_);
-    if (refresh || !shift_precond_) {  // make_preconditioner (fem_system.cpp:38-46): Jacobi on the GPU
+    if (refresh || !shift_precond_) {  // make_preconditioner (fem_system.cpp:38-46)
       launch_csr_diag(n, sh_csr_.row_ptr, sh_csr_.col_idx, sh_vals_.p, sh_diag_.p, stream_);
+      shift_amg_on_ = shift_amg && prob_.solver.precond == 2;
+      if (shift_amg_on_) build_shift_amg();
       ++stats_.precond_setups;
       shift_precond_ = true;
     }
   }
-  PhaseTimer pt(stats_.t_solve);
+  PhaseTimer pt(stats_.t_solve, "solve");
   // pcg_solve (proj/src/pcg.cpp:9-72) with a zero start
   double* x = delta;
   double* r = sd(12);
@@ -2545,7 +2731,15 @@ void GpuSystem::shifted_solve_dev(double t, double* z_full, double gdt, const do
   double rel = 1.0;
   if (!std::isfinite(bnorm)) throw NumericalError("pcg: non-finite initial residual");
   if (rel <= tol) return;
-  launch_jacobi_div(n, sh_diag_.p, r, z, red_, S_RZ, stream_);
+  auto precond = [&]() {  // z = B r and r.z in S_RZ
+    if (shift_amg_on_) {
+      const double* zv = shift_vcycle(r);
+      CK(cudaMemcpyAsync(z, zv, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
+    } else {
+      launch_jacobi_div(n, sh_diag_.p, r, z, red_, S_RZ, stream_);
+    }
+  };
+  precond();
   double rz = read_scalar(S_RZ);
   if (!std::isfinite(rz)) throw NumericalError("pcg: non-finite preconditioned residual");
   CK(cudaMemcpyAsync(p, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));
@@ -2564,7 +2758,7 @@ void GpuSystem::shifted_solve_dev(double t, double* z_full, double gdt, const do
       converged = true;
       break;
     }
-    launch_jacobi_div(n, sh_diag_.p, r, z, red_, S_RZ, stream_);
+    precond();
     const double rz_new = read_scalar(S_RZ);
     if (!std::isfinite(rz_new)) throw NumericalError("pcg: non-finite preconditioned residual");
     launch_scale(n, rz_new / rz, p, p, stream_);
@@ -2631,7 +2825,7 @@ bool GpuSystem::sdirk_stages(double dt, const SdirkOptions& o, int& newton_iters
     bool converged = false;
     for (int it = 0;; ++it) {
       {
-        PhaseTimer pt(stats_.t_residual);
+        PhaseTimer pt(stats_.t_residual, "residual");
         residual_dev(ts, z, r);
       }
       CK(cudaMemcpyAsync(zw, z, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_));

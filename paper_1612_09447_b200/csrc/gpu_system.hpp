@@ -126,7 +126,10 @@ struct DevLevel {
 };
 
 // timing classes (eqs_timing in include/eqs_b200.h)
-enum TimeClass { TC_STIFF = 0, TC_PCG = 1, TC_VCYCLE = 2, TC_RKC = 3, TC_SPE = 4, TC_BOUNDARY = 5, TC_COUNT = 8 };
+enum TimeClass { TC_STIFF = 0, TC_PCG = 1, TC_VCYCLE = 2, TC_RKC = 3, TC_SPE = 4, TC_BOUNDARY = 5, TC_PCG_GRAPH = 6, TC_COUNT = 8 };
+
+struct DevLevel;
+void cheb_first_kind(double lmax, double ratio, DevLevel& lv);
 
 class GpuSystem {
  public:
@@ -238,6 +241,8 @@ class GpuSystem {
   int vcycle_precision() const { return vcycle_prec_; }
   bool sell_on() const { return sell_on_; }
   bool timing_on = false;
+  bool timing_graph = false;  // timing keeps the graph-resident PCG (one TC_PCG_GRAPH region per solve)
+  bool shift_amg = true;      // SDIRK shifted solves: SA-AMG rebuilt per refresh (default) or Jacobi (option 26)
   void tic(int cls);
   void toc(int cls, double bytes);
   void timing_resolve(double ms[TC_COUNT], long launches[TC_COUNT], double bytes[TC_COUNT]);
@@ -298,7 +303,11 @@ class GpuSystem {
   bool sdirk_stages(double dt, const SdirkOptions& o, int& newton_iters, double* est);
   void shifted_solve_dev(double t, double* z_full, double gdt, const double* rhs, double* delta, bool refresh);
   void build_shift_map();
-  bool shift_built_ = false, shift_precond_ = false;
+  bool shift_built_ = false, shift_precond_ = false, shift_amg_on_ = false;
+  struct ShiftAmg;
+  std::unique_ptr<ShiftAmg> sh_amg_;
+  void build_shift_amg();
+  double* shift_vcycle(const double* r);
   DevBuf<long> sh_ptr_, sh_src_;
   DevBuf<double> sh_S_, sh_vals_, sh_diag_;
   DevBuf<int> sh_err_;
@@ -382,7 +391,7 @@ class GpuSystem {
   DevBuf<unsigned char> kb_mat_;
   DevBuf<uint16_t> kb_slots_, kb_tloc_;
   DevBuf<int> kb_ldof_;
-  DevBuf<double> kb_partials_;
+  DevBuf<double> kb_partials_, kb_bxyz_;
   KxDev kxd_;
   long kx_partials_ = 0, kx_ldofs_ = 0, kx_slots_ = 0;
   DevBuf<int> err_;  // kernel error flags
@@ -429,6 +438,7 @@ class GpuSystem {
   std::vector<cudaEvent_t> ev_pool_;
   int open_cls_ = -1, nest_ = 0;
   cudaEvent_t open_ev_ = nullptr;
+  double open_bytes_ = 0.0;
   double acc_ms_[TC_COUNT] = {}, acc_bytes_[TC_COUNT] = {};
   long acc_n_[TC_COUNT] = {};
   cudaEvent_t get_event();

@@ -597,6 +597,8 @@ void launch_pcg_update(int n, double* x, double* r, const double* p, const doubl
   // r.r identically whatever the caller's x alignment
   const bool vec = al(r, 16) && al(p, 16) && al(q, 16) && (!r32 || (al(r32, 8) && al(invd32, 8) && al(d32, 8)));
   const long work = vec ? std::max(1, n / 2) : n;
+  // r, q in, r out (+ x, p in, x out; + invd32 in, r32 and D^-1 r32 out)
+  g_algo_bytes += (24.0 + (x ? 24.0 : 0.0) + (r32 ? 12.0 : 0.0)) * n;
 #define U_(F, V, W)                                                                                              \
   launch_pdl(k_pcg_update<F, V, W>, red_grid(k_pcg_update<F, V, W>, work), kBlock, 0, s, n, x, r, p, q, r32, invd32, \
              d32, red)
@@ -632,10 +634,12 @@ void launch_pcg_direction(int n, double* p, const double* z, const double* scal,
                           const double* stat, double* x) {
   ++g_launch_count;
   const bool vec = x && aligned16(x) && aligned16(p) && aligned16(z);
+  g_algo_bytes += (24.0 + (x ? 16.0 : 0.0)) * n;  // z, p in, p out (+ the deferred x += alpha p: x in and out)
   launch_pdl(k_pcg_direction, grid_for(vec ? n / 2 + 1 : n), kBlock, 0, s, n, p, z, scal, stat, x, vec ? 1 : 0);
 }
 void launch_pcg_xfinal(int n, double* x, const double* p, const double* scal, cudaStream_t s) {
   ++g_launch_count;
+  g_algo_bytes += 24.0 * n;
   launch_pdl(k_pcg_xfinal, grid_for(n), kBlock, 0, s, n, x, p, scal);
 }
 void launch_pcg_check0(double* scal, double* stat, cudaGraphConditionalHandle h, cudaStream_t s) {
@@ -670,6 +674,14 @@ void launch_jacobi(int n, const double* invd, const double* r, double* z, Reduce
   Reducer rr = red ? *red : Reducer{};
   launch_pdl(k_jacobi, red_grid(k_jacobi, n), kBlock, 0, s, n, invd, r, z, rr, slot, red ? 1 : 0);
 }
+__global__ void __launch_bounds__(kBlock) k_recip(int n, const double* __restrict__ d, double* __restrict__ inv) {
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i < n) inv[i] = 1.0 / d[i];
+}
+void launch_recip(int n, const double* d, double* inv, cudaStream_t s) {
+  ++g_launch_count;
+  if (n > 0) k_recip<<<(n + kBlock - 1) / kBlock, kBlock, 0, s>>>(n, d, inv);
+}
 void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, cudaStream_t s) {
   ++g_launch_count;
   launch_pdl(k_dot, red_grid(k_dot, n), kBlock, 0, s, n, a, b, red, slot);
@@ -677,6 +689,7 @@ void launch_dot(int n, const double* a, const double* b, Reducer red, int slot, 
 void launch_multi_dot(int n, int m, const double* const* V, const double* w, Reducer red, int slot0, cudaStream_t s) {
   if (m <= 0) return;
   ++g_launch_count;
+  g_algo_bytes += 8.0 * n * (m + 1);
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
   bool vec = aligned16(w);
@@ -695,6 +708,7 @@ static void lincomb_any(int n, int m, const double* const* V, CoefPack c, double
     return;
   }
   ++g_launch_count;
+  g_algo_bytes += 8.0 * n * (m + (ACC ? 2 : 1));
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = V[k];
   bool vec = aligned16(y);
@@ -714,6 +728,7 @@ void launch_lincomb_acc(int n, int m, const double* const* V, CoefPack c, double
 void launch_orth_update(int n, int m, const double* const* Q, CoefPack c, double* w, Reducer red, int slot,
                         cudaStream_t s) {
   ++g_launch_count;
+  g_algo_bytes += 8.0 * n * (m + 2);
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = Q[k];
   launch_pdl(k_orth_update, red_grid(k_orth_update, n), kBlock, 0, s, n, m, pk, c, w, red, slot);
@@ -721,6 +736,7 @@ void launch_orth_update(int n, int m, const double* const* Q, CoefPack c, double
 void launch_orth_update_dev(int n, int m, const double* const* Q, const double* dcoef, double* w, Reducer red,
                             int slot, cudaStream_t s) {
   ++g_launch_count;
+  g_algo_bytes += 8.0 * n * (m > 0 ? m + 2 : 1);
   PtrPack pk{};
   for (int k = 0; k < m && k < kMaxMulti; ++k) pk.p[k] = Q[k];
   if (m <= 0) {  // no projection: the pass only produces w.w
@@ -739,11 +755,13 @@ void launch_orth_update_dev(int n, int m, const double* const* Q, const double* 
 }
 void launch_scale_rsqrt(int n, const double* nrm2, const double* x, double* y, cudaStream_t s) {
   ++g_launch_count;
+  g_algo_bytes += 16.0 * n;
   launch_pdl(k_scale_rsqrt, grid_for(n), kBlock, 0, s, n, nrm2, x, y);
 }
 void launch_lincomb_multi(int n, int kin, int kout, const double* const* in, double* const* out, const RotPack& T,
                           cudaStream_t s) {
   ++g_launch_count;
+  g_algo_bytes += 8.0 * n * (kin + kout);
   PtrPack pi{}, po{};
   for (int k = 0; k < kin && k < kMaxMulti; ++k) pi.p[k] = in[k];
   for (int k = 0; k < kout && k < kMaxMulti; ++k) po.p[k] = out[k];

@@ -33,6 +33,10 @@ __device__ __forceinline__ double kappa_dev(const DevMaterial& m, double e) {
   return exp10(m.lo + (m.hi - m.lo) * s);
 }
 
+// out-of-line field-dependent branch: keeps the tanh / exp10 registers out
+// of the element loop of k_kx_block4 (linear materials never call it)
+__device__ __noinline__ double kappa_nl(const DevMaterial& m, double e) { return kappa_dev(m, e); }
+
 __device__ __forceinline__ void load_xyz(const double* __restrict__ coords, int d, double p[3]) {
   const double2 a = __ldg(reinterpret_cast<const double2*>(coords + 4L * d));
   const double b = __ldg(coords + 4L * d + 2);
@@ -339,6 +343,161 @@ __global__ void __launch_bounds__(kBlock, NL == 4 ? 4 : 1) k_kx_block(const int*
   }
 }
 
+// P1 blocked K(x)v, latency-lean form. Differences from the
+// generic k_kx_block<4>:
+//  * every global load is issued before the first barrier: the thread's tets
+//    (ushort4 block-local ids + material byte, TPT per thread, in registers),
+//    the dof lists, the block-dof coordinates (stored per block-dof, streamed
+//    instead of gathered) and the x (v) gathers; the element phase reads
+//    registers and shared memory only;
+//  * the element arithmetic uses the unscaled cofactor rows cr_k (g_k =
+//    cr_k / det): w = sum_k (x_k - x_0) cr_k, |grad x_h| = |w| / |det|,
+//    y_k = kappa / (6 det) cr_k . w_v (k = 1..3), y_0 = -(y_1 + y_2 + y_3);
+//    the sqrt runs for field-dependent materials only;
+//  * the per-dof sums load four products ahead of the (sequential, fixed
+//    order) additions.
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+#ifndef KX4_MINB
+#define KX4_MINB 4
+#endif
+template <bool SAME>
+__global__ void __launch_bounds__(kBlock, KX4_MINB) k_kx_block4(const int* __restrict__ blk_tet0, const ushort4* __restrict__ tets,
+                                                        const unsigned char* __restrict__ mat,
+                                                        const double2* __restrict__ bxy, const double* __restrict__ bz,
+                                                        const double* __restrict__ x,
+                                                        const double* __restrict__ v, const int* __restrict__ blk_dof0,
+                                                        const int* __restrict__ sptr, const uint16_t* __restrict__ slots,
+                                                        const int* __restrict__ lout, double* __restrict__ partials,
+                                                        const double* __restrict__ base, double sign, int n_out,
+                                                        double* __restrict__ out, int* err, int max_tets, int max_dofs,
+                                                        const int* __restrict__ ldof_dof) {
+  // shared memory: products [4][max_tets] (the first quarter doubles as the
+  // staged tets: thread-private slot tl is read before it is overwritten),
+  // block-dof records {x, y, z, x_state} (32 B: two 16-byte loads per
+  // vertex), v [max_dofs] when v != x, slot ranges, outputs, material bytes,
+  // slots
+  extern __shared__ double ysm[];
+  ushort4* s_tet = reinterpret_cast<ushort4*>(ysm);
+  double* s_p = ysm + (size_t)max_tets * 4;  // [max_dofs][4]
+  double* s_v = SAME ? nullptr : s_p + 4L * max_dofs;
+  int* s_sptr = reinterpret_cast<int*>(s_p + (SAME ? 4L : 5L) * max_dofs);  // [max_dofs + 1]
+  int* s_out = s_sptr + max_dofs + 1;                      // [max_dofs]
+  unsigned* s_matw = reinterpret_cast<unsigned*>(s_out + max_dofs);  // [max_tets / 4 + 2] words
+  uint16_t* s_slot = reinterpret_cast<uint16_t*>(s_matw + max_tets / 4 + 2);
+  const int b = blockIdx.x;
+  const int t0 = __ldg(blk_tet0 + b), nt = __ldg(blk_tet0 + b + 1) - t0;
+  const int d0 = __ldg(blk_dof0 + b), nd = __ldg(blk_dof0 + b + 1) - d0;
+  // asynchronous copies of the streamed per-tet data (no registers held)
+  for (int tl = threadIdx.x; tl < nt; tl += kBlock) cp_async8(s_tet + tl, tets + t0 + tl);
+  {
+    const unsigned* mw = reinterpret_cast<const unsigned*>(mat);
+    const int w0 = t0 >> 2, w1 = (t0 + nt + 3) >> 2;
+    for (int w = w0 + threadIdx.x; w < w1; w += kBlock) cp_async4(s_matw + (w - w0), mw + w);
+  }
+  const int sbase = __ldg(sptr + d0);
+  const int nsl = __ldg(sptr + d0 + nd) - sbase;
+  for (int i = threadIdx.x; i < nd; i += kBlock) {
+    const int gd = __ldcs(ldof_dof + d0 + i);
+    cp_async16(s_p + 4 * i, bxy + d0 + i);
+    cp_async8(s_p + 4 * i + 2, bz + d0 + i);
+    cp_async4(s_sptr + i, sptr + d0 + i);
+    cp_async4(s_out + i, lout + d0 + i);
+    cp_async8(s_p + 4 * i + 3, x + gd);
+    if (!SAME) cp_async8(s_v + i, v + gd);
+  }
+  for (int i = threadIdx.x; i < nsl; i += kBlock) s_slot[i] = __ldcs(slots + sbase + i);
+  if (threadIdx.x == 0) s_sptr[nd] = sbase + nsl;
+  cp_async_wait_all();
+  __syncthreads();
+  const unsigned char* s_mat = reinterpret_cast<const unsigned char*>(s_matw) + (t0 & 3);
+  for (int tl = threadIdx.x; tl < nt; tl += kBlock) {
+    const ushort4 q = s_tet[tl];
+    const int li[4] = {q.x, q.y, q.z, q.w};
+    double2 pa[4], pb[4];  // {x, y}, {z, x_state} of the four vertices
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      pa[k] = reinterpret_cast<const double2*>(s_p)[2 * li[k]];
+      pb[k] = reinterpret_cast<const double2*>(s_p)[2 * li[k] + 1];
+    }
+    double e[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      e[c][0] = pa[c + 1].x - pa[0].x;
+      e[c][1] = pa[c + 1].y - pa[0].y;
+      e[c][2] = pb[c + 1].x - pb[0].x;
+    }
+    double cr[3][3];
+    cr[0][0] = e[1][1] * e[2][2] - e[1][2] * e[2][1];
+    cr[0][1] = e[1][2] * e[2][0] - e[1][0] * e[2][2];
+    cr[0][2] = e[1][0] * e[2][1] - e[1][1] * e[2][0];
+    cr[1][0] = e[2][1] * e[0][2] - e[2][2] * e[0][1];
+    cr[1][1] = e[2][2] * e[0][0] - e[2][0] * e[0][2];
+    cr[1][2] = e[2][0] * e[0][1] - e[2][1] * e[0][0];
+    cr[2][0] = e[0][1] * e[1][2] - e[0][2] * e[1][1];
+    cr[2][1] = e[0][2] * e[1][0] - e[0][0] * e[1][2];
+    cr[2][2] = e[0][0] * e[1][1] - e[0][1] * e[1][0];
+    const double det = e[0][0] * cr[0][0] + e[0][1] * cr[0][1] + e[0][2] * cr[0][2];
+    if (det == 0.0) atomicOr(err, 1);
+    const double x0 = pb[0].y;
+    const double dx[3] = {pb[1].y - x0, pb[2].y - x0, pb[3].y - x0};
+    double w[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) w[d] = dx[0] * cr[0][d] + dx[1] * cr[1][d] + dx[2] * cr[2][d];
+    const double s2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+    if (!(s2 >= 0.0)) atomicOr(err, 2);  // kappa_of_e: invalid_argument (materials.cpp:26)
+    const double inv = 1.0 / det;
+    const DevMaterial& m = c_mat[s_mat[tl]];
+    const double kap = m.kind == 0 ? m.kappa : kappa_nl(m, sqrt(s2) * fabs(inv));
+    double wv[3] = {w[0], w[1], w[2]};
+    if (!SAME) {
+      const double v0 = s_v[li[0]];
+      const double dv[3] = {s_v[li[1]] - v0, s_v[li[2]] - v0, s_v[li[3]] - v0};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) wv[d] = dv[0] * cr[0][d] + dv[1] * cr[1][d] + dv[2] * cr[2][d];
+    }
+    const double c = kap * inv * (1.0 / 6.0);
+    double y[4];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) y[i + 1] = c * (cr[i][0] * wv[0] + cr[i][1] * wv[1] + cr[i][2] * wv[2]);
+    y[0] = -(y[1] + y[2] + y[3]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ysm[i * max_tets + tl] = y[i];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nd; e += kBlock) {
+    int k = s_sptr[e] - sbase;
+    const int k1 = s_sptr[e + 1] - sbase;
+    double s = 0.0;
+    for (; k + 4 <= k1; k += 4) {
+      const double a0 = ysm[s_slot[k]], a1 = ysm[s_slot[k + 1]], a2 = ysm[s_slot[k + 2]], a3 = ysm[s_slot[k + 3]];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; k < k1; ++k) s += ysm[s_slot[k]];
+    const int o = s_out[e];
+    if (o >= 0) {
+      if (o < n_out) out[o] = base ? base[o] + sign * s : sign * s;
+    } else {
+      partials[-o - 1] = s;
+    }
+  }
+}
+
 // pass 2: boundary dofs, partials summed in block order
 __global__ void __launch_bounds__(kBlock) k_kx_partials(int nb, const int* __restrict__ bdof,
                                                         const int* __restrict__ bptr, const int* __restrict__ bpart,
@@ -363,7 +522,23 @@ void launch_kx_blocked(const KxDev& k, const double* coords, const double* x_sta
   size_t smem = sizeof(double) * k.nl * k.max_block_tets + sizeof(int) * (2L * k.max_block_dofs + 1) +
                 sizeof(uint16_t) * k.max_block_slots + 16;
   if (k.nl == 4) smem += sizeof(double) * 5L * k.max_block_dofs;  // staged coordinates, x, v
-  if (k.nl == 4) {
+  if (k.nl == 4 && k.bxy) {
+    const bool same = x_state == v;
+    const size_t sm4 = sizeof(double) * (4L * k.max_block_tets + (same ? 4L : 5L) * k.max_block_dofs) +
+                       sizeof(int) * (2L * k.max_block_dofs + 1) + sizeof(unsigned) * (k.max_block_tets / 4 + 2) +
+                       sizeof(uint16_t) * k.max_block_slots + 16;
+    static bool attr4 = false;
+    if (!attr4) {
+      cudaFuncSetAttribute(k_kx_block4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_kx_block4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr4 = true;
+    }
+    auto kern = same ? k_kx_block4<true> : k_kx_block4<false>;
+    kern<<<k.n_blocks, kBlock, sm4, s>>>(k.blk_tet0, reinterpret_cast<const ushort4*>(k.tets), k.mat,
+                                         reinterpret_cast<const double2*>(k.bxy), k.bz, x_state, v, k.blk_dof0,
+                                         k.sptr, k.slots, k.lout, k.partials, base, sign, n_out, out, geo_error,
+                                         k.max_block_tets, k.max_block_dofs, k.ldof_dof);
+  } else if (k.nl == 4) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_kx_block<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -95,3 +95,48 @@ def test_sdirk_scenario_runs():  # proj/configs/slab_nonlinear_sdirk.json (accep
     assert st["newton_linear_solves"] > 0 and st["newton_pcg_iterations"] > 0
     assert st["precond_setups"] >= r["accepted"]  # one refresh per attempted step (+1 for the mass AMG)
     assert np.isfinite(r["x"]).all()
+
+
+@pytest.mark.parametrize("jitter", [0.1, 0.0])
+def test_shifted_amg_matches_jacobi_with_fewer_iterations(jitter):
+    """The shifted system (M_II + gdt K_II(z)) preconditioned with the SA-AMG
+    rebuilt on the device (make_preconditioner -> AmgPreconditioner,
+    fem_system.cpp:38-46, amg.cpp:90-143; option 26 = 1, the default) and with
+    Jacobi (option 26 = 0): same solution to the solver tolerance, and the AMG
+    needs far fewer PCG iterations, as the reference's per-step AMG would."""
+    cfg = cube(20, jitter=jitter)
+    z = 3e4 * po.random_vec(cube_free(cfg), 5)
+    rhs = po.random_vec(cube_free(cfg), 6)
+    gdt = 0.435866521508459 * 2e-4
+    out = {}
+    for amg in (1, 0):
+        g = eb.FemSystem(cfg)
+        g.set_option(26, amg)
+        d = g.shifted_solve(1e-3, z, gdt, rhs)
+        out[amg] = (d, g.stats()["newton_pcg_iterations"])
+        g.close()
+    (d_amg, it_amg), (d_jac, it_jac) = out[1], out[0]
+    assert np.linalg.norm(d_amg - d_jac) <= 1e-9 * np.linalg.norm(d_jac)
+    assert it_amg * 3 <= it_jac, (it_amg, it_jac)
+
+
+def test_sdirk_steps_with_shifted_amg_match_jacobi():
+    """Two fixed SDIRK steps: AMG- and Jacobi-preconditioned Newton solves give
+    the same potentials (Newton tolerance 1e-8, PCG 1e-12) and Newton counts."""
+    cfg = cube(12, jitter=0.1)
+    x0 = 200 * po.random_vec(cube_free(cfg), 31)
+    res = {}
+    for amg in (1, 0):
+        g = eb.FemSystem(cfg)
+        g.set_option(26, amg)
+        g.set_state(0.0, x0, 5e-5)
+        g.sdirk_advance_fixed(5e-5, 2)
+        res[amg] = (g.get_state()[0], g.stats()["assemblies"], g.stats()["precond_setups"])
+        g.close()
+    assert np.linalg.norm(res[1][0] - res[0][0]) <= 1e-8 * np.linalg.norm(res[0][0])
+    assert res[1][1] == res[0][1] and res[1][2] == res[0][2]
+
+
+def cube_free(cfg):
+    n = cfg["mesh"]["box"]["nx"]
+    return (n + 1) ** 2 * (n - 1)  # z = 0 and z = 1 planes are Dirichlet

@@ -28,21 +28,24 @@ def main():
                 r["Metric Unit"], 1)
             d["bytes"] = d.get("bytes", 0.0) + v
     cls = defaultdict(float)
-    n_vc = n_pcg = n_kx = 0
+    n_vc = n_pcg = n_kx = n_spe_dot = 0
     for d in rows.values():
         n = d["name"]
         b = d.get("bytes", 0.0)
-        if "k_sellp_red<1, float, 3" in n or "k_sells_red<float, 3" in n:  # fine-level post-smoother
+        # fine-level post-smoother: once per V-cycle
+        if "k_sellp_red<1, float, 3" in n or "k_sells_red<float, 3" in n or "k_sells_pair<2>" in n:
             n_vc += 1
-        if "k_sell_red<1, double, double, 0>" in n or "k_sells64<0>" in n:  # PCG q = A p, p.q
+        if "k_sell_red<1, double, double, 0>" in n or "k_sells64<0" in n:  # PCG q = A p, p.q
             n_pcg += 1
         if "k_kx_p1" in n or "k_kx_p2" in n or "k_kx_block" in n:  # one per K(x)x apply
             n_kx += 1
-        if ("k_sell_red<1, double, double, 0>" in n or "k_sells64<0>" in n or "k_pcg_update" in n
+        if ("k_sell_red<1, double, double, 0>" in n or "k_sells64<0" in n or "k_pcg_update" in n
                 or "k_pcg_direction" in n):
             cls["pcg spmv+vectors"] += b
         elif "k_kx_" in n:
             cls["stiffness K(x)x"] += b
+        elif any(k in n for k in ("k_multi_dot", "k_orth_update", "k_lincomb", "k_scale_rsqrt")):
+            cls["spe estimator"] += b
         elif any(k in n for k in ("k_sellp", "k_sells", "k_row<", "k_sell<", "k_dense_", "k_diag_scale", "k_to_f64")):
             cls["v-cycle"] += b
     out = {"source": sys.argv[1], "launches": {"v-cycle": n_vc, "pcg spmv+vectors": n_pcg, "stiffness K(x)x": n_kx},
@@ -50,7 +53,8 @@ def main():
                "v-cycle": cls["v-cycle"] / max(1, n_vc),
                # bench.py times a PCG iteration as two regions (SpMV+update, direction)
                "pcg spmv+vectors": cls["pcg spmv+vectors"] / max(1, 2 * n_pcg),
-               "stiffness K(x)x": cls["stiffness K(x)x"] / max(1, n_kx)}}
+               "stiffness K(x)x": cls["stiffness K(x)x"] / max(1, n_kx)},
+           "dram_bytes_total": dict(cls)}
     print(json.dumps(out, indent=1))
 
 
