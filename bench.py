@@ -55,6 +55,10 @@ CONFIGS = {
     "c2": dict(n=99, jitter=0.0, planes=[1 / 3, 2 / 3]),
     "c3": dict(n=215, jitter=0.1, planes=[0.45, 0.55]),
     "c4": dict(n=367, jitter=0.1, planes=[0.45, 0.55]),
+    # config 4 weak scaling: 183 x 183 x (183 g) cubic cells on
+    # [0,1]^2 x [0,g] for g GPUs (~6.2 M free dofs per GPU), the coating layer
+    # repeated in every unit slab and the hv amplitude scaled by g (same fields)
+    "c4w": dict(n=183, jitter=0.1, planes=[0.45, 0.55], weak=True),
 }
 # bounded CPU sample of the same family (same physics/planes/jitter, 48^3 cells)
 CPU_SAMPLE = dict(n=48, steps=2)
@@ -64,14 +68,18 @@ COARSE_FILTER = None  # --coarse-filter: solver.amg_coarse_filter override (addi
 DENSE_COARSE = None  # --dense-coarse: solver.amg_dense_coarse override (additive key)
 
 
-def scenario(n, jitter, planes, estimator="spe"):
+def scenario(n, jitter, planes, estimator="spe", slabs=1):
+    """Unit cube (slabs = 1) or [0,1]^2 x [0,slabs] with n x n x (n slabs)
+    cells, the coating layer repeated per unit slab (weak scaling)."""
+    zp = [k + p for k in range(slabs) for p in planes]
+    regions = [1] + [2, 1] * (slabs - 1) + [2, 3]
     return {
-        "name": f"bench_cube{n}",
-        "mesh": {"box": {"nx": n, "ny": n, "nz": n, "lx": 1.0, "ly": 1.0, "lz": 1.0, "z_planes": planes,
-                         "regions": [1, 2, 3], "jitter": jitter}},
+        "name": f"bench_cube{n}" + (f"x{slabs}" if slabs > 1 else ""),
+        "mesh": {"box": {"nx": n, "ny": n, "nz": n * slabs, "lx": 1.0, "ly": 1.0, "lz": float(slabs),
+                         "z_planes": zp, "regions": regions, "jitter": jitter}},
         "order": 1,
         "materials": MATERIALS,
-        "excitations": {"hv": {"kind": "sinusoid", "amplitude": 4e4 / 0.012, "frequency": 50.0},
+        "excitations": {"hv": {"kind": "sinusoid", "amplitude": slabs * 4e4 / 0.012, "frequency": 50.0},
                         "ground": {"kind": "constant", "value": 0.0}},
         "solver": dict({"preconditioner": "amg", "rel_tol": 1e-12, "max_iter": 500},
                        **({} if COARSE_FILTER is None else {"amg_coarse_filter": COARSE_FILTER}),
@@ -371,7 +379,7 @@ def single_gpu_system(args, estimator=None):
         raise RuntimeError("bench.py needs a CUDA device (no CPU fallback)")
     spec = CONFIGS[args.config]
     cfg = scenario(spec["n"], spec["jitter"], spec["planes"], estimator=estimator or args.estimator)
-    t0 = time.perf_counter()
+    t0 = time.perf_counter()  # (weak configs: one slab on one GPU)
     g = eb.FemSystem(cfg, device=0)
     apply_options(g, args)
     return g, time.perf_counter() - t0, eb
@@ -553,7 +561,8 @@ def run_b200(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     spec = CONFIGS[args.config]
-    cfg = scenario(spec["n"], spec["jitter"], spec["planes"], estimator=args.estimator)
+    weak = bool(spec.get("weak"))
+    cfg = scenario(spec["n"], spec["jitter"], spec["planes"], estimator=args.estimator, slabs=world if weak else 1)
     t_setup = time.perf_counter()
     if world > 1:
         # one C3 problem partitioned by node ownership over the ranks (strong
@@ -689,6 +698,7 @@ def run_b200(args):
     # host-loop pass's time ratio, its bytes are the captured body's bytes
     # (iterations x (V-cycle + direction + SpMV + update)), the V-cycle part
     # is iterations x the V-cycle's algorithmic bytes
+    n_tets_all = g.n_tets
     v_per = timing["bytes"][2] / max(1, timing["launches"][2])
     host_vp = timing["ms"][1] + timing["ms"][2]
     vshare = timing["ms"][2] / host_vp if host_vp else 0.0
@@ -714,6 +724,17 @@ def run_b200(args):
     cls = max(range(3), key=lambda c: timing_graph["ms"][c])
     dom = roof_g(cls)
     others = {names[c]: roof_g(c) for c in range(3) if c != cls}
+    # K(x)x: SURVEY.md §8d asks for both fractions (HBM and FP64 pipe). fp64
+    # operations per P1 tet of k_kx_block4's residual form (linear material:
+    # 9 edge differences, 3 cofactor rows 27, det 5, x differences 3, w 15,
+    # |w|^2 5, 1/det 1, kappa/(6 det) 2, y_1..3 18, y_0 3); the peak is the
+    # spec-derived B200 vector FP64 rate (148 SMs x 64 FMA/clk x 2 x 1.965 GHz)
+    kx = others.get(names[0]) or (dom if cls == 0 else None)
+    if kx:
+        flops = 88.0 * n_tets_all
+        kx["fp64"] = {"flops_per_tet": 88, "achieved_tflops": flops / (kx["avg_launch_ms"] / 1e3) / 1e12,
+                      "peak_tflops": 37.2, "frac": flops / (kx["avg_launch_ms"] / 1e3) / 37.2e12,
+                      "peak_source": "spec-derived (148 SMs x 64 FP64 FMA/clk x 2 flops x 1.965 GHz), not measured"}
     host_loop = {names[c]: roof(c) for c in range(3)}
     n_tets, nnz_mass, amg_levels = g.n_tets, g.nnz_mass_free, g.amg_levels()
     csr64 = (fp64_csr_equivalent(g, iters_g, ms, args.steps, hbm, g_by[0] + g_by[3] + g_by[4] + g_by[5],
@@ -730,10 +751,13 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "steps_per_s": 1e3 * args.steps / ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generated mesh + mt19937 initial state; no dataset)",
-        "config": {"workload": f"{args.config}: {spec['n']}^3 {'jittered ' if spec['jitter'] else ''}unit cube, "
-                               f"{n} free dofs, {n_tets} tets, microvaristor layer z in {spec['planes']}, "
+        "config": {"workload": (f"{args.config}: {spec['n']}x{spec['n']}x{spec['n'] * world} "
+                                f"{'jittered ' if spec['jitter'] else ''}box [0,1]^2x[0,{world}] (weak scaling), "
+                                if weak else
+                                f"{args.config}: {spec['n']}^3 {'jittered ' if spec['jitter'] else ''}unit cube, ")
+                               + f"{n} free dofs, {n_tets} tets, microvaristor layer z in {spec['planes']}, "
                                f"RKC path B s={S_STAGES} dt=0.9*beta(4)/rho (={dt:.4g}s), "
                                f"estimator {args.estimator} + AMG-PCG 1e-12",
                    "estimator": args.estimator,

@@ -69,6 +69,7 @@ struct DevSellP {
   const int* chunk_ptr = nullptr;   // [n_chunks + 1] in 16-byte groups
   const int* bases = nullptr;       // [n_chunks][windows]
   const uint4* words = nullptr;
+  const int* perm = nullptr;        // [n_rows] slot row -> matrix row (sell.hpp HostSellP::perm) or null
 };
 
 // Stencil-coded SELL (sell.hpp HostSellS): per row a pattern id, per entry the

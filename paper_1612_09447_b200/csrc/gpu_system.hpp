@@ -94,7 +94,7 @@ struct SellBufs {
   DevBuf<double> v64;
   DevBuf<float> v32;
   DevBuf<uint16_t> v16;
-  DevBuf<int> pk_cp, pk_bases;  // packed bf16 copy (sell.hpp SELL-P)
+  DevBuf<int> pk_cp, pk_bases, pk_perm;  // packed bf16 copy (sell.hpp SELL-P)
   DevBuf<uint32_t> pk_words;
   DevBuf<uint16_t> st_vals;     // stencil-coded bf16 copy (sell.hpp SELL-S)
   DevBuf<unsigned char> st_pid;

@@ -112,9 +112,22 @@ bool chunk_windows(std::vector<int>& cols, int span, int max_w, int* out) {
 }
 }  // namespace
 
-bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out) {
+bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out, int sigma) {
   const int rows_per_chunk = 32 / tpr;
   const int n_chunks = (a.n_rows + rows_per_chunk - 1) / rows_per_chunk;
+  // slot row -> matrix row (identity unless sorted)
+  std::vector<int> perm;
+  if (sigma > 0) {
+    perm.resize(a.n_rows);
+    for (int i = 0; i < a.n_rows; ++i) perm[i] = i;
+    for (int w0 = 0; w0 < a.n_rows; w0 += sigma) {
+      const int w1 = std::min(a.n_rows, w0 + sigma);
+      std::stable_sort(perm.begin() + w0, perm.begin() + w1, [&](int x, int y) {
+        return a.row_ptr[x + 1] - a.row_ptr[x] > a.row_ptr[y + 1] - a.row_ptr[y];
+      });
+    }
+  }
+  auto row_of = [&](int i) { return perm.empty() ? i : perm[i]; };
   for (int shift = 13; shift >= 11; --shift) {
     const int windows = 1 << (16 - shift), span = 1 << shift;
     std::vector<int> len(n_chunks + 1, 0);
@@ -127,8 +140,12 @@ bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out) {
       for (int c = 0; c < n_chunks; ++c) {
         const int r0 = c * rows_per_chunk, r1 = std::min(a.n_rows, r0 + rows_per_chunk);
         int maxlen = 0;
-        for (int r = r0; r < r1; ++r) maxlen = std::max(maxlen, a.row_ptr[r + 1] - a.row_ptr[r]);
-        cols.assign(a.col_idx.begin() + a.row_ptr[r0], a.col_idx.begin() + a.row_ptr[r1]);
+        cols.clear();
+        for (int i = r0; i < r1; ++i) {
+          const int r = row_of(i);
+          maxlen = std::max(maxlen, a.row_ptr[r + 1] - a.row_ptr[r]);
+          cols.insert(cols.end(), a.col_idx.begin() + a.row_ptr[r], a.col_idx.begin() + a.row_ptr[r + 1]);
+        }
         if (!chunk_windows(cols, span, windows, &bases[(size_t)c * windows])) fail = 1;
         const int groups = (maxlen + kPackGroup - 1) / kPackGroup;
         len[c + 1] = 32 * ((groups + tpr - 1) / tpr);
@@ -155,13 +172,14 @@ bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out) {
     s.windows = windows;
     s.chunk_ptr = std::move(len);
     s.bases = std::move(bases);
+    s.perm = perm;
     s.words.assign(s.padded(), 0u);
 #pragma omp parallel for schedule(static)
     for (int c = 0; c < n_chunks; ++c) {
       const int* wb = &s.bases[(size_t)c * windows];
       const int r0 = c * rows_per_chunk, r1 = std::min(a.n_rows, r0 + rows_per_chunk);
-      for (int r = r0; r < r1; ++r) {
-        const int q = r - r0;
+      for (int i = r0; i < r1; ++i) {
+        const int q = i - r0, r = row_of(i);
         for (int k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
           const int j = k - a.row_ptr[r], col = a.col_idx[k];
           // entry j of the (column-sorted) row goes to lane j % tpr, slot

@@ -33,7 +33,7 @@ double matrix_pass_bytes(const DevCsr& a, int gathered, int streamed, int xbytes
   } else if (a.stencil()) {
     m = 16.0 * 32.0 * a.st.G * a.st.n_chunks + 32.0 * a.st.n_chunks + 32.0 * a.st.G * a.st.P;
   } else if (a.packed()) {
-    m = 4.0 * (double)a.pk.padded + (4.0 + 4.0 * a.pk.windows) * a.pk.n_chunks;
+    m = 4.0 * (double)a.pk.padded + (4.0 + 4.0 * a.pk.windows) * a.pk.n_chunks + (a.pk.perm ? 4.0 * a.n_rows : 0.0);
   } else if (a.sell16()) {
     const double vs = a.prec == 2 ? 2.0 : a.prec == 1 ? 4.0 : 8.0;
     m = (double)a.sell.padded * (2.0 + vs) + 40.0 * a.sell.n_chunks;  // padded entries are read too
@@ -521,8 +521,9 @@ __global__ void __launch_bounds__(kBlock) k_sellp(int n, DevSellP m, const XT* _
   const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (chunk >= m.n_chunks) return;  // warp-uniform exit
   constexpr bool SC = kScaled<OP, -1>;
-  const int row = chunk * (32 / TPR) + lane / TPR;
-  const bool act = lane % TPR == 0 && row < n;
+  const int slot = chunk * (32 / TPR) + lane / TPR;
+  const bool act = lane % TPR == 0 && slot < n;
+  const int row = act && m.perm ? __ldg(m.perm + slot) : slot;  // sorted rows (SELL-C-sigma)
   Epi<OP, -1, XT> e;
   if (act) e.load(row, x, b, invd, y, nullptr, 0);
   const XT s = sellp_dot<TPR, XT, SC && !PRE>(m, chunk, lane, SC ? (PRE ? pre : b) : x, invd);
@@ -618,8 +619,9 @@ __global__ void __launch_bounds__(kBlock) k_sellp_red(int n, DevSellP m, const X
   const int warps = gridDim.x * (kBlock / 32);
   double acc = 0.0;
   for (int chunk = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); chunk < m.n_chunks; chunk += warps) {
-    const int row = chunk * (32 / TPR) + lane / TPR;
-    const bool act = lane % TPR == 0 && row < n;
+    const int slot = chunk * (32 / TPR) + lane / TPR;
+    const bool act = lane % TPR == 0 && slot < n;
+    const int row = act && m.perm ? __ldg(m.perm + slot) : slot;  // sorted rows (SELL-C-sigma)
     Epi<0, MODE, XT> e;
     if (act) e.load(row, x, b, invd, y, b64, do_red);
     const XT s = sellp_dot<TPR, XT, kScaled<0, MODE> && !PRE>(m, chunk, lane, PRE ? pre : x, invd);

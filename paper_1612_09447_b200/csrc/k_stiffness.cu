@@ -377,7 +377,7 @@ template <bool SAME>
 __global__ void __launch_bounds__(kBlock, KX4_MINB) k_kx_block4(const int* __restrict__ blk_tet0, const ushort4* __restrict__ tets,
                                                         const unsigned char* __restrict__ mat,
                                                         const double2* __restrict__ bxy, const double* __restrict__ bz,
-                                                        const double* __restrict__ x,
+                                                        const double* __restrict__ coords, const double* __restrict__ x,
                                                         const double* __restrict__ v, const int* __restrict__ blk_dof0,
                                                         const int* __restrict__ sptr, const uint16_t* __restrict__ slots,
                                                         const int* __restrict__ lout, double* __restrict__ partials,
@@ -411,8 +411,13 @@ __global__ void __launch_bounds__(kBlock, KX4_MINB) k_kx_block4(const int* __res
   const int nsl = __ldg(sptr + d0 + nd) - sbase;
   for (int i = threadIdx.x; i < nd; i += kBlock) {
     const int gd = __ldcs(ldof_dof + d0 + i);
-    cp_async16(s_p + 4 * i, bxy + d0 + i);
-    cp_async8(s_p + 4 * i + 2, bz + d0 + i);
+    if (bz) {  // coordinates streamed from the per-block-dof copy
+      cp_async16(s_p + 4 * i, bxy + d0 + i);
+      cp_async8(s_p + 4 * i + 2, bz + d0 + i);
+    } else {  // gathered from the padded [x, y, z, 0] rows (fewer DRAM bytes, longer chain)
+      cp_async16(s_p + 4 * i, coords + 4L * gd);
+      cp_async8(s_p + 4 * i + 2, coords + 4L * gd + 2);
+    }
     cp_async4(s_sptr + i, sptr + d0 + i);
     cp_async4(s_out + i, lout + d0 + i);
     cp_async8(s_p + 4 * i + 3, x + gd);
@@ -535,7 +540,7 @@ void launch_kx_blocked(const KxDev& k, const double* coords, const double* x_sta
     }
     auto kern = same ? k_kx_block4<true> : k_kx_block4<false>;
     kern<<<k.n_blocks, kBlock, sm4, s>>>(k.blk_tet0, reinterpret_cast<const ushort4*>(k.tets), k.mat,
-                                         reinterpret_cast<const double2*>(k.bxy), k.bz, x_state, v, k.blk_dof0,
+                                         reinterpret_cast<const double2*>(k.bxy), k.bz, coords, x_state, v, k.blk_dof0,
                                          k.sptr, k.slots, k.lout, k.partials, base, sign, n_out, out, geo_error,
                                          k.max_block_tets, k.max_block_dofs, k.ldof_dof);
   } else if (k.nl == 4) {

@@ -67,6 +67,11 @@ struct HostSellP {
   std::vector<int> chunk_ptr;    // [n_chunks + 1] offsets in 16-byte groups (multiples of 32)
   std::vector<int> bases;        // [n_chunks][windows]
   std::vector<uint32_t> words;   // 4 * chunk_ptr.back() packed entries (padding: 0)
+  // row sorting (SELL-C-sigma): slot row i of the chunks holds matrix row
+  // perm[i]; rows are sorted by length (descending, stable) within windows of
+  // sigma rows, so a chunk's rows have similar lengths and little padding.
+  // Empty: identity. The kernels read and write the epilogue rows at perm[i].
+  std::vector<int> perm;
   long padded() const { return chunk_ptr.empty() ? 0 : 4L * chunk_ptr.back(); }
 };
 
@@ -115,7 +120,8 @@ uint16_t to_bf16(double d);  // round to nearest even
 // lanes per row of the packed format: about 32 entries per lane (fewer
 // shuffle-reduction steps and more loads in flight per lane on coarse levels)
 int choose_sellp_tpr(const HostCsr& a);
-// false when some chunk's columns need more than 32 windows
-bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out);
+// false when some chunk's columns need more than 32 windows; sigma > 0 sorts
+// the rows by length within windows of sigma rows (HostSellP::perm)
+bool build_sell_packed(const HostCsr& a, int tpr, HostSellP& out, int sigma = 0);
 
 }  // namespace eqsb

@@ -26,7 +26,8 @@ static int check_packed(const HostCsr& a, const HostSellP& p) {
   for (int c = 0; c < p.n_chunks; ++c) {
     const int S = (p.chunk_ptr[c + 1] - p.chunk_ptr[c]) / 32;
     for (int lane = 0; lane < 32; ++lane) {
-      const int q = lane / p.tpr, sub = lane % p.tpr, r = c * rpc + q;
+      const int q = lane / p.tpr, sub = lane % p.tpr, i = c * rpc + q;
+      const int r = i < a.n_rows && !p.perm.empty() ? p.perm[i] : i;  // sorted rows (SELL-C-sigma)
       for (int st = 0; st < S; ++st)
         for (int e = 0; e < 4; ++e) {
           const uint32_t w = p.words[4L * (p.chunk_ptr[c] + 32L * st + lane) + e];
@@ -205,6 +206,39 @@ int main() {
       if (okp && p.uniform && p.padded() != 128L * p.uniform * p.n_chunks) ++fails, printf("uniform size\n");
       if (!okp && spreads[si] <= 30000) ++fails, printf("packed encoding unexpectedly failed\n");
     }
+  // rows of irregular length (transfer-operator-like): sorting within windows
+  // of 256 rows (SELL-C-sigma) keeps every entry and cuts the padding
+  {
+    HostCsr a;
+    a.n_rows = 5000;
+    a.n_cols = 40000;
+    a.row_ptr.push_back(0);
+    for (int i = 0; i < a.n_rows; ++i) {
+      const int len = 2 + (int)(g() % 11);
+      std::vector<int> cols;
+      for (int k = 0; k < len; ++k) cols.push_back(8 * i + (int)(g() % 64));
+      std::sort(cols.begin(), cols.end());
+      cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+      for (int col : cols) {
+        a.col_idx.push_back(col);
+        a.values.push_back(0.5 + col % 5);
+      }
+      a.row_ptr.push_back((int)a.col_idx.size());
+    }
+    HostSellP p0, p1;
+    const bool ok0 = build_sell_packed(a, 1, p0), ok1 = build_sell_packed(a, 1, p1, 256);
+    int bad = !ok0 || !ok1 || p1.perm.size() != (size_t)a.n_rows;
+    if (!bad) {
+      std::vector<int> seen(a.n_rows, 0);
+      for (int r : p1.perm) bad |= r < 0 || r >= a.n_rows || seen[r]++;
+      for (int w0 = 0; w0 < a.n_rows && !bad; w0 += 256)  // a permutation within each window
+        for (int i = w0; i < std::min(a.n_rows, w0 + 256); ++i) bad |= p1.perm[i] / 256 != w0 / 256;
+      bad |= check_packed(a, p0) + check_packed(a, p1);
+    }
+    printf("irregular rows: padded %ld unsorted, %ld sorted (nnz %ld) -> %s\n", p0.padded(), p1.padded(), a.nnz(),
+           bad || p1.padded() >= p0.padded() ? "FAIL" : "ok");
+    fails += bad || p1.padded() >= p0.padded();
+  }
   // clustered columns (restriction-like rows: a few node planes each): 12
   // clusters 20000 apart need 16 windows of 4096 (shift 12), 24 need 32 (shift 11)
   for (int nclus : {12, 24}) {
