@@ -486,7 +486,8 @@ def run_sdirk_vs_rkc(args):
         wall = time.perf_counter() - w0
         st1 = g.stats()
         d = {k: st1[k] - st0[k] for k in ("m_solves", "pcg_iterations", "newton_linear_solves",
-                                            "newton_pcg_iterations", "precond_setups", "assemblies")}
+                                            "newton_pcg_iterations", "precond_setups", "assemblies",
+                                            "time_residual", "time_solve", "time_setup", "time_estimator")}
         out[name] = {"t_reached": t, "accepted": acc, "rejected": rej, "device_s": ev0.elapsed_time(ev1) / 1e3,
                      "wall_s": wall, **d}
     line = {"metric": "explicit RKC vs implicit SDIRK3(2): time to t_end (PAPER.md Fig. 2)",

@@ -28,11 +28,31 @@ namespace eqsb {
 struct GpuSystem::ShiftAmg {
   SpgemmDevice sd;
   std::vector<DCsr> A, P, R;
+  std::vector<DevBuf<float>> vals32;  // fp32 copies of the level values (the fp32 V-cycle reads them)
   std::vector<DevLevel> levels;
   int coarse_n = 0;
   DevBuf<double> inv;
   DevBuf<float> inv32;
   int builds = 0;
+  // the mass solve's operator / graph state, swapped in while a shifted
+  // system is solved through pcg_dev (shift_swap)
+  DevCsr op;
+  cudaGraphExec_t vgraph = nullptr;
+  double* vout = nullptr;
+  long vkern = 0;
+  double vbytes = 0.0;
+  std::unordered_map<double*, cudaGraphExec_t> graphs;
+  std::unordered_map<double*, long> graph_use;
+  long graph_clock = 0, body_kernels = 0;
+  double body_bytes = 0.0;
+  void drop_graphs() {
+    if (vgraph) cudaGraphExecDestroy(vgraph);
+    vgraph = nullptr;
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    graphs.clear();
+    graph_use.clear();
+  }
+  ~ShiftAmg() { drop_graphs(); }
 };
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -2603,6 +2623,8 @@ void GpuSystem::build_shift_amg() {
   ShiftAmg& S = *sh_amg_;
   cudaStream_t s = S.sd.stream();
   CK(cudaStreamSynchronize(stream_));  // the shifted values were written on the context stream
+  S.drop_graphs();  // the level buffers are reallocated below
+  S.vals32.clear();
   S.levels.clear();
   S.A.clear();
   S.P.clear();
@@ -2650,7 +2672,11 @@ void GpuSystem::build_shift_amg() {
   S.coarse_n = hc.n_rows;
   S.inv.alloc(std::max<size_t>(1, inv.size()));
   S.inv.upload(inv.data(), inv.size(), s);
-  S.inv32.alloc(1);
+  {
+    std::vector<float> f(inv.begin(), inv.end());
+    S.inv32.alloc(std::max<size_t>(1, f.size()));
+    S.inv32.upload(f.data(), f.size(), s);
+  }
   const int L = (int)S.A.size();
   S.levels.resize(L);
   auto view = [](DCsr& m) {
@@ -2677,13 +2703,24 @@ void GpuSystem::build_shift_amg() {
     lv.z.alloc(nb);
     lv.z2.alloc(nb);
     lv.t.alloc(nb);
+    for (DevBuf<float>* v : {&lv.b32, &lv.z32, &lv.z2_32, &lv.t32, &lv.db32, &lv.dt32, &lv.invd32}) v->alloc(nb);
+    auto f32 = [&](DCsr& m, DevCsr& v) {  // fp32 value copy read by the fp32 V-cycle (CSR kernels)
+      S.vals32.emplace_back();
+      S.vals32.back().alloc(std::max<long long>(1, m.nnz));
+      launch_to_f32(m.nnz, m.v.p, S.vals32.back().p, s);
+      v.values_f = S.vals32.back().p;
+    };
+    if (l + 1 < L) f32(S.A[l], lv.A);
     if (l + 1 < L) {
       lv.P = view(S.P[l]);
       lv.R = view(S.R[l]);
+      f32(S.P[l], lv.P);
+      f32(S.R[l], lv.R);
       DevBuf<double> d;
       dev_diagonal(S.A[l], d, s);
       lv.invd.alloc(nb);
       launch_recip(n, d.p, lv.invd.p, s);
+      launch_to_f32(n, lv.invd.p, lv.invd32.p, s);
       CK(cudaStreamSynchronize(s));
       // smoother bound: the setup's 10-step lambda_max(D^-1 A) estimate (amg.cpp:28-45)
       lv.lambda_smoother = lam[l];
@@ -2692,6 +2729,27 @@ void GpuSystem::build_shift_amg() {
   }
   CK(cudaStreamSynchronize(s));
   ++S.builds;
+}
+
+// Exchange the mass solve's operator, hierarchy and captured graphs with the
+// shifted system's, so pcg_dev (graph-resident loop, fp32 V-cycle) solves
+// the shifted system; called in pairs around the solve.
+void GpuSystem::shift_swap() {
+  ShiftAmg& S = *sh_amg_;
+  std::swap(mii_, S.op);
+  std::swap(levels_, S.levels);
+  std::swap(coarse_n_, S.coarse_n);
+  std::swap(coarse_inv_, S.inv);
+  std::swap(coarse_inv32_, S.inv32);
+  std::swap(vcycle_graph_, S.vgraph);
+  std::swap(vcycle_out_, S.vout);
+  std::swap(vcycle_graph_kernels_, S.vkern);
+  std::swap(vcycle_graph_bytes_, S.vbytes);
+  std::swap(pcg_graphs_, S.graphs);
+  std::swap(pcg_graph_use_, S.graph_use);
+  std::swap(pcg_graph_clock_, S.graph_clock);
+  std::swap(pcg_body_kernels_, S.body_kernels);
+  std::swap(pcg_body_bytes_, S.body_bytes);
 }
 
 // one V-cycle of the shifted hierarchy on r (fp64): z, and r.z in S_RZ
@@ -2718,6 +2776,14 @@ double* GpuSystem::shift_vcycle(const double* r) {
   return z;
 }
 
+// the shifted operator as the PCG operator of pcg_dev (fp64 CSR on M_II's pattern)
+void GpuSystem::S_op_view() {
+  DevCsr& o = sh_amg_->op;
+  o = sh_csr_;
+  o.use_sell = false;
+  o.prec = 0;
+}
+
 void GpuSystem::shifted_solve_dev(double t, double* z_full, double gdt, const double* rhs, double* delta,
                                   bool refresh) {
   build_shift_map();
@@ -2737,6 +2803,24 @@ void GpuSystem::shifted_solve_dev(double t, double* z_full, double gdt, const do
     }
   }
   PhaseTimer pt(stats_.t_solve, "solve");
+  if (shift_amg_on_ && shift_pcg_graph) {
+    // pcg_solve (proj/src/pcg.cpp:9-72) with a zero start through pcg_dev:
+    // the graph-resident loop with the fp32 V-cycle of the shifted hierarchy
+    S_op_view();
+    shift_swap();
+    PcgResult res;
+    try {
+      res = pcg_dev(rhs, nullptr, delta, prob_.solver.rel_tol, prob_.solver.max_iter);
+    } catch (...) {
+      shift_swap();
+      throw;
+    }
+    shift_swap();
+    if (!res.converged) throw NumericalError("shifted-system solve failed to converge");
+    ++stats_.newton_linear_solves;
+    stats_.newton_pcg_iterations += res.iterations;
+    return;
+  }
   // pcg_solve (proj/src/pcg.cpp:9-72) with a zero start
   double* x = delta;
   double* r = sd(12);

@@ -243,6 +243,7 @@ class GpuSystem {
   bool timing_on = false;
   bool timing_graph = false;  // timing keeps the graph-resident PCG (one TC_PCG_GRAPH region per solve)
   bool shift_amg = true;      // SDIRK shifted solves: SA-AMG rebuilt per refresh (default) or Jacobi (option 26)
+  bool shift_pcg_graph = true;  // shifted AMG solves through pcg_dev (graph loop, fp32 V-cycle; option 27)
   void tic(int cls);
   void toc(int cls, double bytes);
   void timing_resolve(double ms[TC_COUNT], long launches[TC_COUNT], double bytes[TC_COUNT]);
@@ -308,6 +309,8 @@ class GpuSystem {
   std::unique_ptr<ShiftAmg> sh_amg_;
   void build_shift_amg();
   double* shift_vcycle(const double* r);
+  void shift_swap();
+  void S_op_view();
   DevBuf<long> sh_ptr_, sh_src_;
   DevBuf<double> sh_S_, sh_vals_, sh_diag_;
   DevBuf<int> sh_err_;

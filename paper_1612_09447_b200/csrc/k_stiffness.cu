@@ -391,7 +391,11 @@ __global__ void __launch_bounds__(kBlock, KX4_MINB) k_kx_block4(const int* __res
   // slots
   extern __shared__ double ysm[];
   ushort4* s_tet = reinterpret_cast<ushort4*>(ysm);
-  double* s_p = ysm + (size_t)max_tets * 4;  // [max_dofs][4]
+  // {x, y} and {z, x_state} of each block-dof in two arrays of 16-byte
+  // records: a 16-byte load then starts on one of 8 bank groups (one of 4
+  // with 32-byte records), halving the structural bank conflicts
+  double* s_p = ysm + (size_t)max_tets * 4;  // [max_dofs][2] {x, y}, then [max_dofs][2] {z, x_state}
+  double* s_q = s_p + 2L * max_dofs;
   double* s_v = SAME ? nullptr : s_p + 4L * max_dofs;
   int* s_sptr = reinterpret_cast<int*>(s_p + (SAME ? 4L : 5L) * max_dofs);  // [max_dofs + 1]
   int* s_out = s_sptr + max_dofs + 1;                      // [max_dofs]
@@ -412,15 +416,15 @@ __global__ void __launch_bounds__(kBlock, KX4_MINB) k_kx_block4(const int* __res
   for (int i = threadIdx.x; i < nd; i += kBlock) {
     const int gd = __ldcs(ldof_dof + d0 + i);
     if (bz) {  // coordinates streamed from the per-block-dof copy
-      cp_async16(s_p + 4 * i, bxy + d0 + i);
-      cp_async8(s_p + 4 * i + 2, bz + d0 + i);
+      cp_async16(s_p + 2 * i, bxy + d0 + i);
+      cp_async8(s_q + 2 * i, bz + d0 + i);
     } else {  // gathered from the padded [x, y, z, 0] rows (fewer DRAM bytes, longer chain)
-      cp_async16(s_p + 4 * i, coords + 4L * gd);
-      cp_async8(s_p + 4 * i + 2, coords + 4L * gd + 2);
+      cp_async16(s_p + 2 * i, coords + 4L * gd);
+      cp_async8(s_q + 2 * i, coords + 4L * gd + 2);
     }
     cp_async4(s_sptr + i, sptr + d0 + i);
     cp_async4(s_out + i, lout + d0 + i);
-    cp_async8(s_p + 4 * i + 3, x + gd);
+    cp_async8(s_q + 2 * i + 1, x + gd);
     if (!SAME) cp_async8(s_v + i, v + gd);
   }
   for (int i = threadIdx.x; i < nsl; i += kBlock) s_slot[i] = __ldcs(slots + sbase + i);
@@ -434,8 +438,8 @@ __global__ void __launch_bounds__(kBlock, KX4_MINB) k_kx_block4(const int* __res
     double2 pa[4], pb[4];  // {x, y}, {z, x_state} of the four vertices
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      pa[k] = reinterpret_cast<const double2*>(s_p)[2 * li[k]];
-      pb[k] = reinterpret_cast<const double2*>(s_p)[2 * li[k] + 1];
+      pa[k] = reinterpret_cast<const double2*>(s_p)[li[k]];
+      pb[k] = reinterpret_cast<const double2*>(s_q)[li[k]];
     }
     double e[3][3];
 #pragma unroll

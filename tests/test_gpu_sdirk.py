@@ -137,6 +137,31 @@ def test_sdirk_steps_with_shifted_amg_match_jacobi():
     assert res[1][1] == res[0][1] and res[1][2] == res[0][2]
 
 
+def test_shifted_solve_graph_loop_matches_host_loop():
+    """Shifted AMG solves through pcg_dev (graph-resident loop, fp32 V-cycle
+    of the shifted hierarchy; option 27 = 1, default) against the
+    host-driven fp64 V-cycle loop (option 27 = 0): same update to the solver
+    tolerance, and the oracle's shifted solve."""
+    cfg = cube(16, jitter=0.1)
+    n = cube_free(cfg)
+    z = 3e4 * po.random_vec(n, 5)
+    rhs = po.random_vec(n, 6)
+    gdt = 0.435866521508459 * 2e-4
+    res = {}
+    for graph in (1, 0):
+        g = eb.FemSystem(cfg)
+        g.set_option(27, graph)
+        d = g.shifted_solve(1e-3, z, gdt, rhs)
+        d2 = g.shifted_solve(1e-3, z, gdt, 2 * rhs, refresh_precond=False)  # captured graph reused
+        res[graph] = (d, d2, g.stats()["newton_pcg_iterations"])
+        g.close()
+    do = po.Problem(cfg).shifted_solve(1e-3, z, gdt, rhs)
+    for graph in (1, 0):
+        assert np.linalg.norm(res[graph][0] - do) <= 1e-9 * np.linalg.norm(do)
+        assert np.linalg.norm(res[graph][1] - 2 * do) <= 1e-9 * np.linalg.norm(2 * do)
+    assert abs(res[1][2] - res[0][2]) <= 4
+
+
 def cube_free(cfg):
     n = cfg["mesh"]["box"]["nx"]
     return (n + 1) ** 2 * (n - 1)  # z = 0 and z = 1 planes are Dirichlet
