@@ -88,6 +88,18 @@ def scenario(n, jitter, planes, estimator="spe", slabs=1):
     }
 
 
+def host_mem_available():
+    """MemAvailable of /proc/meminfo in bytes (0 when unknown)."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
@@ -551,6 +563,16 @@ def run_b200(args):
     if world > 1 and "OMP_NUM_THREADS" not in os.environ:
         # host setup of every rank runs concurrently: share the cores
         os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // world))
+    if world > 1 and "EQS_SETUP_CONCURRENCY" not in os.environ:
+        # every rank builds the global problem before extracting its partition
+        # (~2.5 kB of host memory per global free dof at the peak): bound how
+        # many ranks of the node do so at once (capi.cpp SetupGate)
+        spec0 = CONFIGS[args.config]
+        slabs = world if spec0.get("weak") else 1
+        n_glob = (spec0["n"] + 1) ** 2 * (spec0["n"] * slabs - 1)
+        avail = host_mem_available()
+        k = max(1, int(0.8 * avail / (2.5e3 * n_glob))) if avail else world
+        os.environ["EQS_SETUP_CONCURRENCY"] = str(min(world, k))
     import torch
     import paper_1612_09447_b200 as eb
 
@@ -610,6 +632,27 @@ def run_b200(args):
     launches = lib.eqs_launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     st1 = g.stats()
+    # e2e: the same step through the public API with host buffers: every step
+    # copies the state in from pinned host memory (H2D) and back out (D2H);
+    # measured right after the timed region (same thermal / power-cap state)
+    x_host = torch.empty(g.n_own, dtype=torch.float64, pin_memory=True).numpy()
+    g.get_state(out=x_host)
+    t_host = g.get_state(want_x=False)[1]["t"]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    e_steps = max(1, min(args.steps, 5))
+    for _ in range(e_steps):
+        g.set_state(t_host, x_host, dt)
+        g.rkc_advance_fixed(dt, S_STAGES, 1)
+        t_host = g.get_state(out=x_host)[1]["t"]
+    e_wall = time.perf_counter() - e0
+    if dist:
+        t = torch.tensor([e_wall], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_wall = float(t.item())
+    e2e_value = n * S_STAGES * e_steps / e_wall
     # per-class breakdown for the roofline: CUDA events around every kernel
     # class on the library stream, in a second pass of K steps after the
     # timed region (the events add host work, so they stay out of `value`)
@@ -642,26 +685,6 @@ def run_b200(args):
     iters = st1["pcg_iterations"] - st0["pcg_iterations"]
     value = n * f_evals / (ms / 1e3)  # n = global free dofs: all ranks together
 
-    # e2e: the same step through the public API with host buffers: every step
-    # copies the state in from pinned host memory (H2D) and back out (D2H)
-    x_host = torch.empty(g.n_own, dtype=torch.float64, pin_memory=True).numpy()
-    g.get_state(out=x_host)
-    t_host = g.get_state(want_x=False)[1]["t"]
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0 = time.perf_counter()
-    e_steps = max(1, min(args.steps, 5))
-    for _ in range(e_steps):
-        g.set_state(t_host, x_host, dt)
-        g.rkc_advance_fixed(dt, S_STAGES, 1)
-        t_host = g.get_state(out=x_host)[1]["t"]
-    e_wall = time.perf_counter() - e0
-    if dist:
-        t = torch.tensor([e_wall], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_wall = float(t.item())
-    e2e_value = n * S_STAGES * e_steps / e_wall
     import resource
     rss_gb = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6
 
@@ -774,7 +797,8 @@ def run_b200(args):
                        "coarse_filter_eps": COARSE_FILTER if COARSE_FILTER is not None else 0.0025,
                        "dense_coarse_rows": DENSE_COARSE if DENSE_COARSE is not None else 512},
                    "parallelism": (f"node-ownership partition over {world} GPUs (owner-computes K(x)x, halo "
-                                   f"SpMV + NCCL allreduce per level, small coarse levels replicated)")
+                                   f"SpMV + NCCL allreduce per level, small coarse levels replicated; host setup "
+                                   f"{os.environ.get('EQS_SETUP_CONCURRENCY', world)} ranks at a time)")
                    if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (matrices + vectors >> 126 MB), no flush needed"},
         "pcg_iters_per_solve": iters / max(1, f_evals), "f_evals_per_step": f_evals / args.steps,

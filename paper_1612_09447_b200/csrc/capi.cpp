@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <fcntl.h>
+#include <semaphore.h>
 #include <memory>
 #include <random>
 #include <string>
@@ -186,6 +188,43 @@ int eqs_nccl_unique_id(char* id128) {
   });
 }
 
+// Host setup of the ranks of one node, at most EQS_SETUP_CONCURRENCY at a
+// time (default: all): every rank builds the global mesh, M and AMG
+// hierarchy before extracting its partition, so the node's peak host memory
+// is (concurrency) x (one global build) + the others' partitions. A POSIX
+// semaphore named after the job's NCCL id gates the phase from before
+// build_problem to the release of the global hierarchy (GpuSystem ctor,
+// setup_gate_release); the collective device build runs after it.
+struct SetupGate {
+  sem_t* sem = nullptr;
+  bool held = false;
+  SetupGate(const std::string& key, int nranks) {
+    const char* e = getenv("EQS_SETUP_CONCURRENCY");
+    const int k = e ? atoi(e) : 0;
+    if (k <= 0 || k >= nranks) return;
+    unsigned long h = 1469598103934665603ul;
+    for (unsigned char ch : key) h = (h ^ ch) * 1099511628211ul;
+    char name[64];
+    std::snprintf(name, sizeof name, "/eqs_setup_%016lx", h);
+    sem = sem_open(name, O_CREAT, 0600, (unsigned)k);
+    if (sem == SEM_FAILED) {
+      sem = nullptr;
+      return;
+    }
+    while (sem_wait(sem) != 0) {
+    }
+    held = true;
+  }
+  void release() {
+    if (held) sem_post(sem);
+    held = false;
+  }
+  ~SetupGate() {
+    release();
+    if (sem) sem_close(sem);
+  }
+};
+
 int eqs_create_distributed(const char* json_text, int device, int nranks, int rank, const char* id128,
                            eqs_ctx** out) {
   return guard([&] {
@@ -196,8 +235,16 @@ int eqs_create_distributed(const char* json_text, int device, int nranks, int ra
       cuda_check(cudaSetDevice(device), "cudaSetDevice");
       comm = make_nccl_comm(std::string(id128, 128), nranks, rank);
     }
+    SetupGate gate(std::string(id128, 128), nranks);
+    setup_gate_release = [&gate] { gate.release(); };
     auto ctx = std::make_unique<eqs_ctx>();
-    ctx->sys = std::make_unique<GpuSystem>(build_problem(c), device, std::move(comm));
+    try {
+      ctx->sys = std::make_unique<GpuSystem>(build_problem(c), device, std::move(comm));
+    } catch (...) {
+      setup_gate_release = nullptr;
+      throw;
+    }
+    setup_gate_release = nullptr;
     *out = ctx.release();
   });
 }
@@ -209,8 +256,16 @@ int eqs_create_distributed_shm(const char* json_text, int device, int nranks, in
     SimConfig c = parse_config(json_text);
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     std::unique_ptr<Comm> comm = make_shm_comm(shm_name, nranks, rank);
+    SetupGate gate(shm_name, nranks);
+    setup_gate_release = [&gate] { gate.release(); };
     auto ctx = std::make_unique<eqs_ctx>();
-    ctx->sys = std::make_unique<GpuSystem>(build_problem(c), device, std::move(comm));
+    try {
+      ctx->sys = std::make_unique<GpuSystem>(build_problem(c), device, std::move(comm));
+    } catch (...) {
+      setup_gate_release = nullptr;
+      throw;
+    }
+    setup_gate_release = nullptr;
     *out = ctx.release();
   });
 }

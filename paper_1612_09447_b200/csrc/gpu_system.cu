@@ -21,9 +21,12 @@
 #include <random>
 #include <type_traits>
 
+#include <malloc.h>
 #include <nvtx3/nvToolsExt.h>
 
 namespace eqsb {
+
+thread_local std::function<void()> setup_gate_release;
 
 struct GpuSystem::ShiftAmg {
   SpgemmDevice sd;
@@ -381,6 +384,19 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
                        &filtered, dev_levels_, device_);
   }
   memtrace("plan");
+  if (comm_->size() > 1) {
+    // the rank's plan holds its operators: the global hierarchy's matrices
+    // are only needed for single-rank API queries; release them before the
+    // device build, then let the next rank of the node start its host setup
+    // (setup_gate: bounded concurrency of the host phase, capi.cpp)
+    for (auto& lv : amg_.levels) lv.A = lv.P = lv.R = HostCsr{};
+    malloc_trim(0);
+    memtrace("global hierarchy released");
+  }
+  if (setup_gate_release) {
+    setup_gate_release();
+    setup_gate_release = nullptr;
+  }
   const LocalSpace& s0 = plan_.space[0];
   n_own_ = s0.n_own();
   n_ghost_ = s0.n_ghost();
@@ -399,10 +415,6 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     plan_.mii = HostCsr{};
     plan_.mib = HostCsr{};
     std::vector<int>().swap(plan_.tet_dofs);
-    if (comm_->size() > 1) {
-      // the global hierarchy is only needed for single-rank API queries
-      for (auto& lv : amg_.levels) lv.A = lv.P = lv.R = HostCsr{};
-    }
   }
   memtrace("device built");
 }

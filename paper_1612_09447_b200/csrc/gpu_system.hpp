@@ -10,6 +10,7 @@
 
 #include <chrono>
 #include <deque>
+#include <functional>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -130,6 +131,10 @@ enum TimeClass { TC_STIFF = 0, TC_PCG = 1, TC_VCYCLE = 2, TC_RKC = 3, TC_SPE = 4
 
 struct DevLevel;
 void cheb_first_kind(double lmax, double ratio, DevLevel& lv);
+// set by the C-ABI around the construction of a multi-rank context: called
+// once the rank's host setup (problem, M, AMG, partition plan) is done and the
+// global hierarchy released, before the collective device build
+extern thread_local std::function<void()> setup_gate_release;
 
 class GpuSystem {
  public:

@@ -60,9 +60,14 @@ def _virtual(world, x0, dt):
     return res
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_processes_match_virtual_ranks_and_single_partition(world):
+@pytest.mark.parametrize("world,gate", [(2, None), (3, None), (3, "1")])
+def test_processes_match_virtual_ranks_and_single_partition(world, gate, monkeypatch):
+    """gate "1": EQS_SETUP_CONCURRENCY=1, the ranks' host setups run one at a
+    time (capi.cpp SetupGate) before the collective device build."""
     import torch.multiprocessing as mp
+
+    if gate:
+        monkeypatch.setenv("EQS_SETUP_CONCURRENCY", gate)  # inherited by the spawned ranks
 
     single = eb.FemSystem(CFG)
     x0 = 2e4 * po.random_vec(single.n_free, 31)
