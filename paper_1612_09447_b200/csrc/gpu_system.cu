@@ -384,7 +384,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
                        &filtered, dev_levels_, device_);
   }
   memtrace("plan");
-  if (comm_->size() > 1) {
+  if (comm_->size() > 1 && device_ >= 0) {
     // the rank's plan holds its operators: the global hierarchy's matrices
     // are only needed for single-rank API queries; release them before the
     // device build, then let the next rank of the node start its host setup
