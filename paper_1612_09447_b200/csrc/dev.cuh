@@ -80,6 +80,8 @@ struct DevSellS {
   const uint4* vals = nullptr;           // [n_chunks][G][32] x 8 bf16
   const unsigned char* pid = nullptr;    // [n_chunks * 32]
   const int* pat = nullptr;              // [P][8 G]
+  int coff[16] = {};                     // G = 2: offsets of the common pattern (kernel parameters)
+  int stage = 1;                         // G = 2: 1 = pattern table staged in shared memory, 0 = parameters + L1
   const double* vals64 = nullptr;        // [n_chunks][8 G][32] fp64 values (PCG operator) or null
   // symmetric half storage (sell.hpp SELL-SH); used instead of vals/vals64 when sym
   bool sym = false;

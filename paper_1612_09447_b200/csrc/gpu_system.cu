@@ -261,6 +261,13 @@ void upload_stencil(const HostCsr& h, DevCsr& d, SellBufs& b, cudaStream_t s) {
   d.st.G = hs.G;
   d.st.P = hs.P;
   d.st.common = hs.common;
+  if (hs.G == 2)
+    for (int j = 0; j < 16; ++j) d.st.coff[j] = hs.pat[(size_t)hs.common * 16 + j];
+  // the common pattern's offsets as kernel parameters, other patterns through L1 (no
+  // per-CTA staging barrier; interleaved A/B at C3: 112.4 vs 115.2 ms per step);
+  // EQS_SELLS_STAGE=1 stages the table in shared memory
+  static const int stage = getenv("EQS_SELLS_STAGE") ? atoi(getenv("EQS_SELLS_STAGE")) : 0;
+  d.st.stage = stage;
   d.st.n_cols = h.n_cols;
   d.st.vals = reinterpret_cast<const uint4*>(b.st_vals.p);
   d.st.pid = b.st_pid.p;

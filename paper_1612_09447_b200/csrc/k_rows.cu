@@ -189,16 +189,15 @@ __device__ __forceinline__ XT sells_dot_g2(const DevSellS& m, const int* __restr
   const int p = (int)__ldcs(m.pid + 32L * chunk + lane);
   const uint4* v = m.vals + (long)chunk * 2 * 32 + lane;
   const uint4 q0 = __ldcs(v), q1 = __ldcs(v + 32);
-  const int* offc = spat + m.common * 16;
   const int cmax = m.n_cols - 1;
   XT xs[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {  // clamped: rows with another pattern may point outside
-    const int c = min(max(row + offc[j], 0), cmax);
+    const int c = min(max(row + (m.stage ? spat[m.common * 16 + j] : m.coff[j]), 0), cmax);
     xs[j] = SCALED ? ldvec<CG>(x + c) * ldvec<CG>(w + c) : ldvec<CG>(x + c);
   }
   if (p != m.common) {
-    const int* off = spat + p * 16;
+    const int* off = (m.stage ? spat : m.pat) + p * 16;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int c = row + off[j];
@@ -256,12 +255,12 @@ __device__ __forceinline__ double sells_dot64(const DevSellS& m, const int* __re
     double a[16], xs[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) a[j] = __ldcs(v + 32 * j);
-    const int* offc = spat + m.common * 16;
     const int cmax = m.n_cols - 1;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) xs[j] = __ldg(x + min(max(row + offc[j], 0), cmax));
+    for (int j = 0; j < 16; ++j)
+      xs[j] = __ldg(x + min(max(row + (m.stage ? spat[m.common * 16 + j] : m.coff[j]), 0), cmax));
     if (p != m.common) {
-      const int* off = spat + p * 16;
+      const int* off = (m.stage ? spat : m.pat) + p * 16;
 #pragma unroll
       for (int j = 0; j < 16; ++j) xs[j] = __ldg(x + row + off[j]);
     }
@@ -537,7 +536,7 @@ __global__ void __launch_bounds__(kBlock) k_sells(int n, DevSellS m, const XT* _
                                                   const XT* __restrict__ pre) {
   extern __shared__ int spat[];
   if (SYM) stage_sym(m, spat);
-  else stage_patterns(m, spat);
+  else if (m.G != 2 || m.stage) stage_patterns(m, spat);  // m.stage = 0: offsets from the parameters
   pdl_entry();
   const int chunk = (int)(((long)blockIdx.x * kBlock + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (chunk >= m.n_chunks) return;  // warp-uniform exit
@@ -563,7 +562,7 @@ __global__ void __launch_bounds__(kBlock) k_sells_red(int n, DevSellS m, const X
                                                       int slot, int do_red, const XT* __restrict__ pre) {
   extern __shared__ int spat[];
   if (SYM) stage_sym(m, spat);
-  else stage_patterns(m, spat);
+  else if (m.G != 2 || m.stage) stage_patterns(m, spat);  // m.stage = 0: offsets from the parameters
   pdl_entry();
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kBlock / 32);
@@ -590,7 +589,7 @@ __global__ void __launch_bounds__(kBlock) k_sells64(int n, DevSellS m, const dou
                                                     double* __restrict__ y, Reducer red, int slot, int do_red) {
   extern __shared__ int spat[];
   if (SYM) stage_sym(m, spat);
-  else stage_patterns(m, spat);
+  else if (m.G != 2 || m.stage) stage_patterns(m, spat);  // m.stage = 0: offsets from the parameters
   pdl_entry();
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (kBlock / 32);
