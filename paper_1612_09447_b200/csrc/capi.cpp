@@ -198,13 +198,13 @@ int eqs_nccl_unique_id(char* id128) {
 struct SetupGate {
   sem_t* sem = nullptr;
   bool held = false;
+  char name[64] = {};
   SetupGate(const std::string& key, int nranks) {
     const char* e = getenv("EQS_SETUP_CONCURRENCY");
     const int k = e ? atoi(e) : 0;
     if (k <= 0 || k >= nranks) return;
     unsigned long h = 1469598103934665603ul;
     for (unsigned char ch : key) h = (h ^ ch) * 1099511628211ul;
-    char name[64];
     std::snprintf(name, sizeof name, "/eqs_setup_%016lx", h);
     sem = sem_open(name, O_CREAT, 0600, (unsigned)k);
     if (sem == SEM_FAILED) {
@@ -218,6 +218,11 @@ struct SetupGate {
   void release() {
     if (held) sem_post(sem);
     held = false;
+  }
+  // once any rank's context is built every rank has passed the gate (the
+  // device build's collectives need all of them): the name can go
+  void unlink() {
+    if (sem) sem_unlink(name);
   }
   ~SetupGate() {
     release();
@@ -245,6 +250,7 @@ int eqs_create_distributed(const char* json_text, int device, int nranks, int ra
       throw;
     }
     setup_gate_release = nullptr;
+    if (rank == 0) gate.unlink();
     *out = ctx.release();
   });
 }
@@ -266,6 +272,7 @@ int eqs_create_distributed_shm(const char* json_text, int device, int nranks, in
       throw;
     }
     setup_gate_release = nullptr;
+    if (rank == 0) gate.unlink();
     *out = ctx.release();
   });
 }

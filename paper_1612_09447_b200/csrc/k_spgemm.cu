@@ -149,6 +149,16 @@ void SpgemmDevice::multiply(const DCsr& a, const DCsr& b, DCsr& c, const double*
   if (a.cols != b.rows) throw NumericalError("csr multiply: dimension mismatch");
   cudaStream_t s = s_;
   const int m = a.rows;
+  static const bool trace = getenv("EQS_SPGEMM_TRACE") != nullptr;
+  auto T0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what, long long v) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[spgemm] %dx%d * %dx%d %-10s %.3f s (%lld)\n", a.rows, a.cols, b.rows, b.cols, what,
+            std::chrono::duration<double>(now - T0).count(), v);
+    T0 = now;
+  };
   c.rows = m;
   c.cols = b.cols;
   // per-row product counts -> offsets
@@ -176,6 +186,7 @@ void SpgemmDevice::multiply(const DCsr& a, const DCsr& b, DCsr& c, const double*
     max_batch = std::max<long long>(max_batch, hoff[r1] - hoff[r0]);
     r0 = r1;
   }
+  lap("offsets", hoff[m]);
   if (max_batch >= (1ll << 31)) throw CudaError("spgemm: a single row has more than 2^31 products");
   const size_t cap = std::max<long long>(1, max_batch);
   DevBuf<unsigned long long> k_in, k_out;
@@ -194,6 +205,7 @@ void SpgemmDevice::multiply(const DCsr& a, const DCsr& b, DCsr& c, const double*
      "sort size");
   ck(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, head.p, idx.p, (int)cap, s), "scan size");
   tmp.alloc(std::max<size_t>({1, sort_bytes, scan_bytes}));
+  lap("alloc", (long long)batches.size());
   // batch outputs (compressed entries in row-major, column-sorted order)
   std::vector<DevBuf<int>> out_c;
   std::vector<DevBuf<double>> out_v;
@@ -214,9 +226,11 @@ void SpgemmDevice::multiply(const DCsr& a, const DCsr& b, DCsr& c, const double*
                                                                      a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, nullptr,
                                                                      0.0, jbits, k_in.p, v_in.p);
     ck(cudaGetLastError(), "expand");
+    lap("expand", n);
     const int end_bit = jbits + bits_for(std::max(1, nr - 1));
     size_t tb = tmp.n;
     ck(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in.p, k_out.p, v_in.p, v_out.p, (int)n, 0, end_bit, s), "sort");
+    lap("sort", end_bit);
     const int grid = (int)std::min<long long>((n + 255) / 256, 148 * 16);
     k_spgemm_heads<<<grid, 256, 0, s>>>(n, k_out.p, head.p);
     tb = tmp.n;
@@ -233,6 +247,7 @@ void SpgemmDevice::multiply(const DCsr& a, const DCsr& b, DCsr& c, const double*
     k_spgemm_reduce<<<grid, 256, 0, s>>>(n, k_out.p, v_out.p, head.p, idx.p, jbits, out_c.back().p, out_v.back().p,
                                          rcnt.p + 1 + r0);
     ck(cudaGetLastError(), "reduce");
+    lap("reduce", nu);
     out_n.push_back(nu);
     total += nu;
   }
