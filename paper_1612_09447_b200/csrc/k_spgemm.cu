@@ -48,20 +48,29 @@ __global__ void k_spgemm_count(int m, const int* __restrict__ arp, const int* __
   cnt[i] = s;
 }
 
+// wpr warps per row of A (rows with many products, e.g. the dense coarse
+// Galerkin products, would otherwise leave most SMs idle): warp w of a row
+// takes the w-th contiguous share of its A entries and starts writing after
+// the products of the entries before it (same positions as one warp).
 template <bool SCALED>
 __global__ void k_spgemm_expand(int r0, int r1, long long base, const long long* __restrict__ off,
                                 const int* __restrict__ arp, const int* __restrict__ aci,
                                 const double* __restrict__ av, const int* __restrict__ brp,
                                 const int* __restrict__ bci, const double* __restrict__ bv,
                                 const double* __restrict__ diag, double neg_omega, int jbits,
-                                unsigned long long* __restrict__ keys, double* __restrict__ vals) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                                unsigned long long* __restrict__ keys, double* __restrict__ vals, int wpr) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int i = r0 + warp;
+  const int i = r0 + gw / wpr, w = gw % wpr;
   if (i >= r1) return;
-  long long pos = off[i] - base;
+  const int a0 = arp[i], a1 = arp[i + 1], share = (a1 - a0 + wpr - 1) / wpr;
+  const int kb = min(a1, a0 + w * share), ke = min(a1, kb + share);
+  long long pre = 0;  // products of the row's A entries before this warp's share
+  for (int ka = a0 + lane; ka < kb; ka += 32) pre += brp[aci[ka] + 1] - brp[aci[ka]];
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  long long pos = off[i] - base + pre;
   const unsigned long long rowkey = (unsigned long long)(i - r0) << jbits;
-  for (int ka = arp[i]; ka < arp[i + 1]; ++ka) {
+  for (int ka = kb; ka < ke; ++ka) {
     const int k = aci[ka];
     double a = av[ka];
     if (SCALED) {
@@ -87,14 +96,27 @@ __global__ void k_spgemm_reduce(long long n, const unsigned long long* __restric
                                 const int* __restrict__ idx, int jbits, int* __restrict__ out_col,
                                 double* __restrict__ out_val, int* __restrict__ row_cnt) {
   const unsigned long long jmask = (1ull << jbits) - 1;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-    if (!head[t]) continue;
-    const unsigned long long key = keys[t];
-    double s = 0.0;
-    for (long long u = t; u < n && keys[u] == key; ++u) s = __dadd_rn(s, vals[u]);
-    out_col[idx[t]] = (int)(key & jmask);
-    out_val[idx[t]] = s;
-    atomicAdd(&row_cnt[key >> jbits], 1);  // row_cnt points at the batch's first row
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // warp-uniform trip count (the per-row output counts are aggregated per warp)
+  for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < n; t0 += stride) {
+    const long long t = t0 + threadIdx.x;
+    const bool h = t < n && head[t];
+    unsigned row = 0;
+    if (h) {
+      const unsigned long long key = keys[t];
+      double s = 0.0;
+      for (long long u = t; u < n && keys[u] == key; ++u) s = __dadd_rn(s, vals[u]);
+      out_col[idx[t]] = (int)(key & jmask);
+      out_val[idx[t]] = s;
+      row = (unsigned)(key >> jbits);
+    }
+    // one atomic per row and warp (dense coarse rows have thousands of
+    // outputs: one atomic per output serialised on the row's counter)
+    const unsigned act = __ballot_sync(0xffffffffu, h);
+    if (h) {
+      const unsigned peers = __match_any_sync(act, row);
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&row_cnt[row], __popc(peers));  // batch-relative row
+    }
   }
 }
 
@@ -216,15 +238,19 @@ void SpgemmDevice::multiply(const DCsr& a, const DCsr& b, DCsr& c, const double*
     const int nr = r1 - r0;
     if (n == 0) continue;
     const int warps_per_block = 8;
-    const int blocks = (nr + warps_per_block - 1) / warps_per_block;
+    // enough warps to fill the GPU when the batch has few (heavy) rows
+    int wpr = 1;
+    while (wpr < 32 && (long long)nr * wpr < 148L * 48) wpr <<= 1;
+    const long long warps = (long long)nr * wpr;
+    const int blocks = (int)((warps + warps_per_block - 1) / warps_per_block);
     if (diag_dev)
       k_spgemm_expand<true><<<blocks, 32 * warps_per_block, 0, s>>>(r0, r1, base, (const long long*)off.p, a.rp.p,
                                                                     a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, diag_dev,
-                                                                    -omega, jbits, k_in.p, v_in.p);
+                                                                    -omega, jbits, k_in.p, v_in.p, wpr);
     else
       k_spgemm_expand<false><<<blocks, 32 * warps_per_block, 0, s>>>(r0, r1, base, (const long long*)off.p, a.rp.p,
                                                                      a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, nullptr,
-                                                                     0.0, jbits, k_in.p, v_in.p);
+                                                                     0.0, jbits, k_in.p, v_in.p, wpr);
     ck(cudaGetLastError(), "expand");
     lap("expand", n);
     const int end_bit = jbits + bits_for(std::max(1, nr - 1));
