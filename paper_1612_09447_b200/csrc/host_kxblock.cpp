@@ -23,14 +23,22 @@ KxBlocks build_kx_blocks(const std::vector<int>& tet_dofs, int nl, int n_tets, c
   // centroid buckets: a uniform grid with ~0.75 block_tets tets per bucket
   std::vector<double> cen(3L * std::max(1, n_tets));
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int t = 0; t < n_tets; ++t)
+  double lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY;
+#pragma omp parallel for schedule(static) reduction(min : lo0, lo1, lo2) reduction(max : hi0, hi1, hi2)
+  for (int t = 0; t < n_tets; ++t) {
     for (int d = 0; d < 3; ++d) {
       double c = 0.0;
       for (int k = 0; k < 4; ++k) c += coords4[4L * tet_dofs[(long)nl * t + k] + d];
       cen[3L * t + d] = 0.25 * c;
-      lo[d] = std::min(lo[d], cen[3L * t + d]);
-      hi[d] = std::max(hi[d], cen[3L * t + d]);
     }
+    lo0 = std::min(lo0, cen[3L * t]);
+    lo1 = std::min(lo1, cen[3L * t + 1]);
+    lo2 = std::min(lo2, cen[3L * t + 2]);
+    hi0 = std::max(hi0, cen[3L * t]);
+    hi1 = std::max(hi1, cen[3L * t + 1]);
+    hi2 = std::max(hi2, cen[3L * t + 2]);
+  }
+  lo[0] = lo0, lo[1] = lo1, lo[2] = lo2, hi[0] = hi0, hi[1] = hi1, hi[2] = hi2;
   int dims[3] = {1, 1, 1};
   if (n_tets > 0) {
     const double nb = std::max(1.0, n_tets / (0.75 * block_tets));
@@ -49,6 +57,7 @@ KxBlocks build_kx_blocks(const std::vector<int>& tet_dofs, int nl, int n_tets, c
   const long nbk = (long)dims[0] * dims[1] * dims[2];
   std::vector<long> bucket(std::max(1, n_tets));
   std::vector<long> cnt(nbk + 1, 0);
+#pragma omp parallel for schedule(static)
   for (int t = 0; t < n_tets; ++t) {
     long id = 0;
     for (int d = 2; d >= 0; --d) {
@@ -58,8 +67,8 @@ KxBlocks build_kx_blocks(const std::vector<int>& tet_dofs, int nl, int n_tets, c
       id = id * dims[d] + i;
     }
     bucket[t] = id;
-    ++cnt[id + 1];
   }
+  for (int t = 0; t < n_tets; ++t) ++cnt[bucket[t] + 1];
   for (long b = 0; b < nbk; ++b) cnt[b + 1] += cnt[b];
   kb.tet_perm.assign(n_tets, 0);
   {
