@@ -155,55 +155,16 @@ void SpgemmDevice::upload(const HostCsr& h, DCsr& d) {
   up(d.v, h.values, s_);
 }
 
-// Device -> pageable host copy through two pinned 64 MB staging buffers: the
-// DMA of one chunk overlaps the (threaded) host copy of the previous one
-// (pageable cudaMemcpy of the GB-sized level matrices ran at a few GB/s).
-static void staged_download(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  constexpr size_t kChunk = 64u << 20;
-  if (bytes < (8u << 20)) {
-    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "d2h");
-    ck(cudaStreamSynchronize(s), "d2h");
-    return;
-  }
-  static char* stage[2] = {nullptr, nullptr};
-  static cudaEvent_t done[2];
-  if (!stage[0]) {
-    for (int b = 0; b < 2; ++b) {
-      ck(cudaMallocHost(reinterpret_cast<void**>(&stage[b]), kChunk), "pinned staging");
-      ck(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming), "event");
-    }
-  }
-  const size_t n = (bytes + kChunk - 1) / kChunk;
-  auto issue = [&](size_t c) {
-    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
-    ck(cudaMemcpyAsync(stage[c & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, s), "d2h");
-    ck(cudaEventRecord(done[c & 1], s), "event");
-  };
-  issue(0);
-  for (size_t c = 0; c < n; ++c) {
-    if (c + 1 < n) issue(c + 1);
-    ck(cudaEventSynchronize(done[c & 1]), "d2h chunk");
-    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
-    char* d = static_cast<char*>(dst) + off;
-    const char* from = stage[c & 1];
-#pragma omp parallel for schedule(static)
-    for (long q = 0; q < 16; ++q) {
-      const size_t a = len * q / 16, b = len * (q + 1) / 16;
-      std::memcpy(d + a, from + a, b - a);
-    }
-  }
-}
-
 void SpgemmDevice::download(const DCsr& d, HostCsr& h) {
   h.n_rows = d.rows;
   h.n_cols = d.cols;
   h.row_ptr.resize(d.rows + 1);
   h.col_idx.resize(d.nnz);
   h.values.resize(d.nnz);
+  d.rp.download(h.row_ptr.data(), d.rows + 1, s_);
+  d.ci.download(h.col_idx.data(), d.nnz, s_);
+  d.v.download(h.values.data(), d.nnz, s_);
   ck(cudaStreamSynchronize(s_), "download");
-  staged_download(h.row_ptr.data(), d.rp.p, sizeof(int) * (d.rows + 1), s_);
-  staged_download(h.col_idx.data(), d.ci.p, sizeof(int) * d.nnz, s_);
-  staged_download(h.values.data(), d.v.p, sizeof(double) * d.nnz, s_);
 }
 
 void SpgemmDevice::multiply(const DCsr& a, const DCsr& b, DCsr& c, const double* diag_dev, double omega,
