@@ -14,6 +14,7 @@
 #include "sell.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -2642,6 +2643,15 @@ void GpuSystem::build_shift_amg() {
   ShiftAmg& S = *sh_amg_;
   cudaStream_t s = S.sd.stream();
   CK(cudaStreamSynchronize(stream_));  // the shifted values were written on the context stream
+  static const bool trace = getenv("EQS_MEMTRACE") != nullptr;
+  auto T0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[shift-amg] %-12s %.4f s\n", what, std::chrono::duration<double>(now - T0).count());
+    T0 = now;
+  };
   S.drop_graphs();  // the level buffers are reallocated below
   S.vals32.clear();
   S.levels.clear();
@@ -2663,6 +2673,7 @@ void GpuSystem::build_shift_amg() {
     CK(cudaMemcpyAsync(a0.v.p, sh_csr_.values, sizeof(double) * a0.nnz, cudaMemcpyDeviceToDevice, s));
   }
   dev_check_diagonal(S.A[0], s);
+  lap("copy A0");
   std::vector<double> lam;
   while ((int)S.A.size() < sp.amg_max_levels && S.A.back().rows > sp.amg_coarse_limit) {
     const DCsr& a = S.A.back();
@@ -2670,15 +2681,19 @@ void GpuSystem::build_shift_amg() {
     dev_diagonal(a, d, s);
     DevBuf<int> agg;
     const int n_agg = dev_aggregate(a, d.p, sp.amg_theta, agg, s);
+    lap("aggregate");
     if (n_agg >= a.rows) break;  // coarsening stalled (amg.cpp:102)
     DCsr pt, p, r, ap, c;
     dev_tentative(agg, a.rows, n_agg, pt, s);
     const double lm = dev_lambda_max(a, d.p, 10, 20240811u, s);
+    lap("lambda");
     S.sd.multiply(a, pt, p, d.p, sp.amg_omega / lm, batch);
     dev_transpose(p, r, s);
+    lap("P, R");
     S.sd.multiply(a, p, ap, nullptr, 0.0, batch);
     S.sd.multiply(r, ap, c, nullptr, 0.0, batch);
     dev_check_diagonal(c, s);
+    lap("RAP");
     lam.push_back(lm);
     S.P.push_back(std::move(p));
     S.R.push_back(std::move(r));
@@ -2688,6 +2703,7 @@ void GpuSystem::build_shift_amg() {
   HostCsr hc;
   S.sd.download(S.A.back(), hc);
   const std::vector<double> inv = dense_inverse(hc);
+  lap("coarse inv");
   S.coarse_n = hc.n_rows;
   S.inv.alloc(std::max<size_t>(1, inv.size()));
   S.inv.upload(inv.data(), inv.size(), s);
@@ -2747,6 +2763,7 @@ void GpuSystem::build_shift_amg() {
     }
   }
   CK(cudaStreamSynchronize(s));
+  lap("levels");
   ++S.builds;
 }
 
