@@ -29,6 +29,10 @@ def run(order, n):
     if os.environ.get("SAN_NOGRAPH") == "1":  # host-driven PCG, no V-cycle graph, no PDL
         for key in (8, 20, 21):
             g.set_option(key, 0)
+    if os.environ.get("SAN_NOPDL") == "1":  # graphs on, programmatic dependent launch off
+        g.set_option(21, 0)
+    if os.environ.get("SAN_NOLOOP") == "1":  # V-cycle graphs + PDL on, no conditional (WHILE) PCG graph
+        g.set_option(20, 0)
     rng = np.random.default_rng(5)
     x = 2e4 * rng.standard_normal(g.n_dofs)
     v = rng.standard_normal(g.n_dofs)
