@@ -357,7 +357,10 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * whole loop is timed as class 6 instead of classes 1 and 2), 26 = SDIRK shifted
  * solves preconditioned by an SA-AMG of the shifted matrix rebuilt on the device
  * at every preconditioner refresh (1, default, with solver.preconditioner amg) or
- * by Jacobi (0).
+ * by Jacobi (0), 27 = SDIRK shifted AMG solves through the graph-resident PCG
+ * loop with an fp32 V-cycle (1, default) or the host-driven fp64 loop (0),
+ * 28 = W-cycle (two coarse-grid corrections) on levels >= value (0 = V-cycle,
+ * the default; slower at C3).
  * The PCG operator and vectors are fp64 in every setting. */
 int eqs_set_option(eqs_ctx* ctx, int key, double value);
 /* The CUDA stream (cudaStream_t) every device call of this context runs on. */

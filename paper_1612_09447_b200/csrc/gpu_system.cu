@@ -1229,6 +1229,18 @@ XT* GpuSystem::vcycle_t(int l, const XT* b_in, bool dot_into_rz, const double* r
   halo(nx.halo, zc);  // no-op on replicated levels
   launch_prolong_add<XT>(lv.P, zc, z, stream_);
   halo(lv.halo, z);
+  if (wcycle_from > 0 && l >= wcycle_from && l + 2 < L && comm_->size() == 1) {
+    // W-cycle on the coarse levels (option 28): a second coarse-grid
+    // correction from the updated residual before the post-smoother; the
+    // cycle stays symmetric (same correction twice between the smoothers)
+    launch_residual<XT>(lv.A, b, z, t, nullptr, 0, stream_);
+    if (prec)
+      launch_spmv_scaled<XT>(lv.R, t, V::invd(nx), bc, prec, stream_);
+    else
+      launch_spmv<XT>(lv.R, t, bc, stream_);
+    zc = vcycle_t<XT>(l + 1, bc, false, nullptr, nullptr, prec);
+    launch_prolong_add<XT>(lv.P, zc, z, stream_);
+  }
   const bool to64 = out64 != nullptr;  // fine level of an fp32 V-cycle
   Reducer r = red_;
   if (deg >= 2) {

@@ -248,6 +248,7 @@ class GpuSystem {
   bool timing_on = false;
   bool timing_graph = false;  // timing keeps the graph-resident PCG (one TC_PCG_GRAPH region per solve)
   bool shift_amg = true;      // SDIRK shifted solves: SA-AMG rebuilt per refresh (default) or Jacobi (option 26)
+  int wcycle_from = 0;  // > 0: W-cycle (two coarse-grid corrections) on levels >= this (option 28; 0 = V-cycle)
   bool shift_pcg_graph = true;  // shifted AMG solves through pcg_dev (graph loop, fp32 V-cycle; option 27)
   void tic(int cls);
   void toc(int cls, double bytes);
