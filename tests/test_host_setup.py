@@ -141,3 +141,20 @@ def test_amg_hierarchy_values_bit_exact(cfg):
             assert a[:2] == b[:2]
             for x, y in zip(a[2:], b[2:]):
                 assert np.array_equal(x, y), (lvl, which)
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include"), reason="reference headers absent")
+def test_cpp_shim_compiles_against_reference_headers():
+    """integration/eqs_gpu_shim.hpp (the INTEGRATION.md shim) compiles against
+    the unmodified reference headers and include/eqs_b200.h."""
+    import subprocess
+    import sysconfig
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    site = sysconfig.get_paths()["purelib"]
+    src = '#include "eqs_gpu_shim.hpp"\nint main() { return 0; }\n'
+    cmd = ["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror", "-x", "c++", "-",
+           "-I" + os.path.join(root, "integration"), "-I" + os.path.join(root, "oracle", "ref_shim"),
+           "-I/root/reference/proj/include", "-I" + os.path.join(root, "include"),
+           "-I" + os.path.join(site, "include", "cudnn_frontend", "thirdparty")]
+    r = subprocess.run(cmd, input=src, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
