@@ -4,7 +4,8 @@
 // own FemSystem on the same mesh, dof map, materials and excitation, all built
 // by the reference (SimConfig, generate_box_mesh, build_dof_map;
 // proj/src/scenario.cpp:229-253). Compares eval_rhs, the spectral-radius
-// estimate, 10 fixed RKC steps (path B) and 3 adaptive rkc_step attempts.
+// estimate, 10 fixed RKC steps (path B), 3 adaptive rkc_step attempts and
+// 2 fixed SDIRK3(2) steps.
 //
 //   dropin_main [config.json]      (default: the 14^3 three-layer slab cube)
 // prints one JSON line; exit code 0 when every relative difference is within
@@ -95,14 +96,31 @@ int main(int argc, char** argv) {
       same_decisions &= a.accepted == b.accepted && a.stages == b.stages;
     }
     const double rel_adaptive = rel(ag.x, ar.x);
+    // the implicit baseline through the same interface: 2 fixed SDIRK3(2)
+    // steps (integrators.cpp:237-296) with Newton on the shifted systems
+    IntegratorState ir, ig;  // milder start (the reference's Picard-type Newton needs it; test_gpu_sdirk.py)
+    ir.x = x0;
+    ir.x *= 0.01;
+    ig.x = ir.x;
+    const double dts = 5e-5;
+    SdirkOptions so;
+    bool okr = true, okg = true;
+    for (int k = 0; k < 2; ++k) {
+      okr = sdirk_advance_fixed(ir, ref, dts, so) && okr;
+      okg = sdirk_advance_fixed(ig, gpu, dts, so) && okg;
+    }
+    const double rel_sdirk = rel(ig.x, ir.x);
     const bool ok = rel_rhs <= 1e-9 && std::fabs(rho_g - rho_r) <= 0.05 * rho_r && rel_fixed <= 1e-9 &&
-                    rel_adaptive <= 1e-6 && same_decisions;
+                    rel_adaptive <= 1e-6 && same_decisions && okr && okg && rel_sdirk <= 1e-7;
     std::printf(
         "{\"n_free\": %d, \"rel_eval_rhs\": %.3e, \"rho_reference\": %.6e, \"rho_gpu\": %.6e, \"dt\": %.6e, "
         "\"rel_10_fixed_rkc_steps\": %.3e, \"rel_3_adaptive_rkc_steps\": %.3e, \"same_accept_and_stages\": %d, "
-        "\"gpu_m_solves\": %ld, \"reference_m_solves\": %ld, \"pass\": %s}\n",
+        "\"gpu_m_solves\": %ld, \"reference_m_solves\": %ld, \"rel_2_fixed_sdirk_steps\": %.3e, "
+        "\"sdirk_converged\": [%d, %d], \"sdirk_newton_solves_gpu\": %ld, \"sdirk_newton_solves_reference\": %ld, "
+        "\"pass\": %s}\n",
         n, rel_rhs, rho_r, rho_g, dt, rel_fixed, rel_adaptive, same_decisions, gpu.stats().m_solves,
-        ref.stats().m_solves, ok ? "true" : "false");
+        ref.stats().m_solves, rel_sdirk, (int)okr, (int)okg, gpu.stats().newton_linear_solves, ref.stats().newton_linear_solves,
+        ok ? "true" : "false");
     return ok ? 0 : 1;
   } catch (const std::exception& e) {
     std::printf("{\"error\": \"%s\", \"pass\": false}\n", e.what());

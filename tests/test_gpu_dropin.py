@@ -26,3 +26,5 @@ def test_reference_integrators_through_the_shim():
     assert r["rel_eval_rhs"] <= 1e-9
     assert r["rel_10_fixed_rkc_steps"] <= 1e-9
     assert r["same_accept_and_stages"] == 1
+    assert r["sdirk_converged"] == [1, 1] and r["rel_2_fixed_sdirk_steps"] <= 1e-7
+    assert r["sdirk_newton_solves_gpu"] == r["sdirk_newton_solves_reference"]
