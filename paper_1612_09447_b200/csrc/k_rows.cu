@@ -53,6 +53,9 @@ constexpr int kUnroll = 8;  // independent entries in flight per lane
 #ifndef SELL_MINB
 #define SELL_MINB 1
 #endif
+#ifndef SELLS_MINB
+#define SELLS_MINB 6  // k_sells: 40 registers, 6 CTAs per SM (A/B at C3: V-cycle -2.8%)
+#endif
 constexpr int kSellUnroll1 = SELL_UNROLL1;
 constexpr int kSymSlotsDev = 8;  // sell.hpp kSymSlots
 
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(kBlock) k_sellp(int n, DevSellP m, const XT* _
 }
 
 template <class XT, int OP, bool PRE, bool SYM>
-__global__ void __launch_bounds__(kBlock) k_sells(int n, DevSellS m, const XT* __restrict__ x,
+__global__ void __launch_bounds__(kBlock, SELLS_MINB) k_sells(int n, DevSellS m, const XT* __restrict__ x,
                                                   const XT* __restrict__ b, const XT* __restrict__ invd,
                                                   XT* __restrict__ y, XT* __restrict__ y2, ChebCoef c,
                                                   const XT* __restrict__ pre) {
