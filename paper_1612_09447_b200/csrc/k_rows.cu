@@ -53,6 +53,9 @@ constexpr int kUnroll = 8;  // independent entries in flight per lane
 #ifndef SELL_MINB
 #define SELL_MINB 1
 #endif
+#ifndef SELLS_RED_MINB
+#define SELLS_RED_MINB 5  // k_sells_red: 48 registers, 5 CTAs per SM (A/B at C3: V-cycle -1.9%)
+#endif
 #ifndef SELLS_MINB
 #define SELLS_MINB 6  // k_sells: 40 registers, 6 CTAs per SM (A/B at C3: V-cycle -2.8%)
 #endif
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(kBlock, SELLS_MINB) k_sells(int n, DevSellS m,
 }
 
 template <class XT, int MODE, bool PRE, bool SYM>
-__global__ void __launch_bounds__(kBlock) k_sells_red(int n, DevSellS m, const XT* __restrict__ x,
+__global__ void __launch_bounds__(kBlock, SELLS_RED_MINB) k_sells_red(int n, DevSellS m, const XT* __restrict__ x,
                                                       const XT* __restrict__ b, const XT* __restrict__ invd,
                                                       XT* __restrict__ y, double* __restrict__ out64,
                                                       const double* __restrict__ b64, ChebCoef c, Reducer red,
