@@ -361,6 +361,11 @@ int eqs_timing_reset(eqs_ctx* ctx);
  * loop with an fp32 V-cycle (1, default) or the host-driven fp64 loop (0),
  * 28 = W-cycle (two coarse-grid corrections) on levels >= value (0 = V-cycle,
  * the default; slower at C3).
+ * 29 = fine-level pre-smoother degree (0 = option 1's degree, the default;
+ *      1 = one fused Jacobi-type pass; the cycle is then not symmetric).
+ * 30 = row-sum correction of the stencil-coded bf16 fine-level V-cycle
+ *      operator (1, the default: the bf16 rounding error of each row sum is
+ *      stored in the row's first padded slot on the diagonal; 0 = plain bf16).
  * The PCG operator and vectors are fp64 in every setting. */
 int eqs_set_option(eqs_ctx* ctx, int key, double value);
 /* The CUDA stream (cudaStream_t) every device call of this context runs on. */

@@ -752,6 +752,8 @@ int eqs_set_option(eqs_ctx* ctx, int key, double value) {
       case 26: g.shift_amg = value != 0.0; break;
       case 27: g.shift_pcg_graph = value != 0.0; break;
       case 28: g.wcycle_from = (int)value; g.invalidate_graphs(); break;
+      case 29: g.fine_pre_degree = (int)value; g.invalidate_graphs(); break;
+      case 30: g.set_stencil_rowsum(value != 0.0); break;
       default: throw std::invalid_argument("eqs_set_option: unknown key");
     }
   });

@@ -168,6 +168,12 @@ void launch_kx_colored(int order, int n_batch, const int* batch_tets, const int*
 // algorithmic bytes of one pass over `a` (resident format) with `gathered`
 // column vectors and `streamed` row vectors of `xbytes` each
 double matrix_pass_bytes(const DevCsr& a, int gathered, int streamed, int xbytes = 8);
+// Row-sum correction of the stencil-coded bf16 V-cycle operator (DESIGN.md
+// §4.12): writes sum_k (a_k - bf16(a_k)) of each row (from the fp64 copy) as
+// bf16 into the row's first padded slot (column offset 0, the diagonal), or 0
+// when on = false. vals is the mutable [n_chunks][G][32] x 8 bf16 array of m.
+void launch_sells_rowsum(int n_rows, const DevSellS& m, uint16_t* vals, bool on, cudaStream_t s);
+
 template <class XT>
 void launch_spmv(const DevCsr& a, const XT* x, XT* y, cudaStream_t s);
 // y = b - A x, and (if red) ||y||^2 into slot

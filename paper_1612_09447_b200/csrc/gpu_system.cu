@@ -647,6 +647,7 @@ void GpuSystem::build_device() {
   upload_csr(plan_.mii, mii_, mii_rp_, mii_ci_, mii_v_, s);
   upload_sell(plan_.mii, mii_, mii_s_, s);
   upload_stencil(plan_.mii, mii_, mii_s_, s);
+  if (mii_.st.vals) launch_sells_rowsum(mii_.n_rows, mii_.st, mii_s_.st_vals.p, stencil_rowsum, s);
   set_sell(sell_on_);
   build_halo(plan_.space[0], halo0_);
   {
@@ -886,6 +887,14 @@ void GpuSystem::set_stencil(bool on) {
 }
 
 // symmetric half storage of the stencil-coded fine operator (SELL-SH) where built
+void GpuSystem::set_stencil_rowsum(bool on) {
+  stencil_rowsum = on;
+  if (device_ >= 0 && mii_.st.vals) {
+    launch_sells_rowsum(mii_.n_rows, mii_.st, mii_s_.st_vals.p, on, stream_);
+    CK(cudaStreamSynchronize(stream_));
+  }
+}
+
 void GpuSystem::set_stencil_sym(bool on) {
   invalidate_graphs();
   mii_.st.sym = on && mii_.st.u64 != nullptr;
@@ -1195,12 +1204,13 @@ XT* GpuSystem::vcycle_t(int l, const XT* b_in, bool dot_into_rz, const double* r
   }
   DevLevel& nx = levels_[l + 1];
   const int deg = l == 0 ? cheb_degree : coarse_degree;
+  const int deg_pre = (l == 0 && fine_pre_degree > 0) ? fine_pre_degree : deg;
   XT* z = V::z(lv);
   XT* t = V::t(lv);
   XT* invd = V::invd(lv);
   // pre: D^-1 b, written by the producer of b (PCG update or the restriction),
   // gathered by the smoother instead of b and D^-1 (k_rows.cu OP 8/9)
-  if (deg >= 2) {
+  if (deg_pre >= 2) {
     halo(lv.halo, pre ? const_cast<XT*>(pre) : b);
     launch_cheb_pre<XT>(lv.A, invd, b, z, lv.cheb, stream_, pre);
     halo(lv.halo, z);

@@ -222,6 +222,8 @@ class GpuSystem {
   int stiffness_mode = 0;  // 0 blocked scatter, 1 coloured, 2 two-pass gather
   int cheb_degree = 2;     // fine level (1 or 2)
   int coarse_degree = 1;   // levels >= 1 (1 or 2)
+  int fine_pre_degree = 0; // fine pre-smoother degree override (option 29; 0 = cheb_degree)
+  bool stencil_rowsum = true;  // bf16 row-sum correction in the stencil copy's padding (option 30)
   double cheb_ratio = 6.0;
   int cheb_kind = 0;          // 0 first-kind Chebyshev on [lmax/ratio, lmax], 1 fourth-kind
   double cheb_scale = 1.1;    // lmax = cheb_scale x the power estimate of lambda_max(D^-1 A)
@@ -237,6 +239,7 @@ class GpuSystem {
   void set_sell(bool on);               // SELL-16 copies instead of CSR where available
   void set_stencil(bool on);            // stencil-coded fine-level V-cycle operator where available
   void set_stencil_sym(bool on);        // its symmetric half storage (SELL-SH) where built
+  void set_stencil_rowsum(bool on);     // row-sum correction slot of the stencil copy (option 30)
   void set_vcycle_vectors_f32(bool on) {  // V-cycle vectors fp32 (default) or fp64
     invalidate_graphs();
     vcycle_f32_ = on;

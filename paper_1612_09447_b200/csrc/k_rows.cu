@@ -9,6 +9,7 @@
 // fp64 for the PCG operator and fp32 (default) or fp64 inside the V-cycle.
 // Row operands of the epilogue are loaded before the matrix pass so that
 // their latency overlaps it.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -878,6 +879,39 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
 }
 
 }  // namespace
+
+namespace {
+// one thread per row; the first padded slot is the second slot whose column
+// offset is 0 (a row's real entries have distinct columns, padding follows them)
+__global__ void __launch_bounds__(kBlock) k_sells_rowsum(int n, DevSellS m, uint16_t* __restrict__ vals, int on) {
+  const int row = blockIdx.x * kBlock + threadIdx.x;
+  if (row >= n) return;
+  const int L = 8 * m.G, chunk = row / 32, lane = row % 32;
+  const int* off = m.pat + (int)m.pid[row] * L;
+  double e = 0.0;
+  int slot = -1;
+  bool diag = false;
+  for (int j = 0; j < L; ++j) {
+    const size_t at = (((size_t)chunk * m.G + j / 8) * 32 + lane) * 8 + j % 8;
+    if (off[j] == 0) {
+      if (diag && slot < 0) slot = (int)j;
+      diag = true;
+    }
+    const double a = m.vals64[((size_t)chunk * L + j) * 32 + lane];
+    if (a != 0.0) e += a - (double)__uint_as_float((unsigned)vals[at] << 16);
+  }
+  if (slot >= 0) {
+    const size_t at = (((size_t)chunk * m.G + slot / 8) * 32 + lane) * 8 + slot % 8;
+    vals[at] = on ? __bfloat16_as_ushort(__float2bfloat16_rn((float)e)) : (uint16_t)0;
+  }
+}
+}  // namespace
+
+void launch_sells_rowsum(int n_rows, const DevSellS& m, uint16_t* vals, bool on, cudaStream_t s) {
+  if (n_rows == 0 || !m.vals64 || m.sym) return;
+  ++g_launch_count;
+  k_sells_rowsum<<<(n_rows + kBlock - 1) / kBlock, kBlock, 0, s>>>(n_rows, m, vals, on ? 1 : 0);
+}
 
 template <class XT>
 void launch_spmv(const DevCsr& a, const XT* x, XT* y, cudaStream_t s) {

@@ -21,7 +21,7 @@ import numpy as np  # noqa: E402
 
 import bench  # noqa: E402
 
-DEFAULTS = {1: 2, 2: 6.0, 3: 1, 9: 1, 13: 0, 14: 1.1, 19: 1, 20: 1, 21: 1}
+DEFAULTS = {1: 2, 2: 6.0, 3: 1, 4: 2, 9: 1, 13: 0, 14: 1.1, 19: 1, 20: 1, 21: 1, 28: 0, 29: 0, 30: 1}
 
 
 def main():
