@@ -590,10 +590,12 @@ __global__ void __launch_bounds__(kBlock, SELLS_RED_MINB) k_sells_red(int n, Dev
   reduce_finish(acc, red, slot);
 }
 
-// q = A p (OP 0) / q = A p, p.q (MODE 0) with the fp64 stencil-coded operator
+// q = A p (MODE -1) / q = A p, p.q (MODE 0) / r = b - A x, r.r (MODE 1) with
+// the fp64 stencil-coded operator
 template <int MODE, bool SYM>
 __global__ void __launch_bounds__(kBlock) k_sells64(int n, DevSellS m, const double* __restrict__ x,
-                                                    double* __restrict__ y, Reducer red, int slot, int do_red) {
+                                                    double* __restrict__ y, Reducer red, int slot, int do_red,
+                                                    const double* __restrict__ b) {
   extern __shared__ int spat[];
   if (SYM) stage_sym(m, spat);
   else if (m.G != 2 || m.stage) stage_patterns(m, spat);  // m.stage = 0: offsets from the parameters
@@ -607,11 +609,17 @@ __global__ void __launch_bounds__(kBlock) k_sells64(int n, DevSellS m, const dou
     const double s = SYM ? sym_dot<double, double, false, false>(m, m.u64, spat, chunk, lane, act ? row : 0, x, nullptr)
                          : sells_dot64(m, spat, chunk, lane, act ? row : 0, x);
     if (act) {
-      y[row] = s;
-      if (MODE == 0) acc += x[row] * s;
+      if (MODE == 1) {
+        const double r = b[row] - s;
+        y[row] = r;
+        acc += r * r;
+      } else {
+        y[row] = s;
+        if (MODE == 0) acc += x[row] * s;
+      }
     }
   }
-  if (MODE == 0 && do_red) reduce_finish(acc, red, slot);
+  if (MODE >= 0 && do_red) reduce_finish(acc, red, slot);
 }
 
 template <int TPR, class XT, int MODE, bool PRE>
@@ -719,10 +727,10 @@ void row_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, XT* y
       g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
       if (m.sym)
         launch_pdl(k_sells64<-1, true>, red_grid(k_sells64<-1, true>, (long)m.n_chunks * 32), kBlock,
-                   sizeof(int) * kSymSmemInts(m.P), s, a.n_rows, m, x, y, Reducer{}, 0, 0);
+                   sizeof(int) * kSymSmemInts(m.P), s, a.n_rows, m, x, y, Reducer{}, 0, 0, (const double*)nullptr);
       else
         launch_pdl(k_sells64<-1, false>, red_grid(k_sells64<-1, false>, (long)m.n_chunks * 32), kBlock,
-                   sizeof(int) * m.P * 8 * m.G, s, a.n_rows, m, x, y, Reducer{}, 0, 0);
+                   sizeof(int) * m.P * 8 * m.G, s, a.n_rows, m, x, y, Reducer{}, 0, 0, (const double*)nullptr);
       return;
     }
   }
@@ -801,16 +809,29 @@ void row_red_launch(const DevCsr& a, const XT* x, const XT* b, const XT* invd, X
                          : matrix_pass_bytes(view, kG[MODE], kS[MODE], sizeof(XT));
   if (MODE == 2 && red) bytes += sizeof(XT) * (double)a.n_rows;
   if (MODE == 3) bytes += (red ? 16.0 : 8.0) * a.n_rows;
+  if constexpr (std::is_same_v<XT, double> && MODE == 1) {
+    if (view.stencil64()) {  // fp64 residual + r.r (PCG start with x0 != 0)
+      const DevSellS& m = a.st;
+      g_algo_bytes += matrix_pass_bytes(view, 1, 2, 8);
+      if (m.sym)
+        launch_pdl(k_sells64<1, true>, red_grid(k_sells64<1, true>, (long)m.n_chunks * 32), kBlock,
+                   sizeof(int) * kSymSmemInts(m.P), s, a.n_rows, m, x, y, r, slot, dr, b);
+      else
+        launch_pdl(k_sells64<1, false>, red_grid(k_sells64<1, false>, (long)m.n_chunks * 32), kBlock,
+                   sizeof(int) * m.P * 8 * m.G, s, a.n_rows, m, x, y, r, slot, dr, b);
+      return;
+    }
+  }
   if constexpr (std::is_same_v<XT, double> && MODE == 0) {
     if (view.stencil64()) {
       const DevSellS& m = a.st;
       g_algo_bytes += matrix_pass_bytes(view, 1, 1, 8);
       if (m.sym)
         launch_pdl(k_sells64<0, true>, red_grid(k_sells64<0, true>, (long)m.n_chunks * 32), kBlock,
-                   sizeof(int) * kSymSmemInts(m.P), s, a.n_rows, m, x, y, r, slot, dr);
+                   sizeof(int) * kSymSmemInts(m.P), s, a.n_rows, m, x, y, r, slot, dr, (const double*)nullptr);
       else
         launch_pdl(k_sells64<0, false>, red_grid(k_sells64<0, false>, (long)m.n_chunks * 32), kBlock,
-                   sizeof(int) * m.P * 8 * m.G, s, a.n_rows, m, x, y, r, slot, dr);
+                   sizeof(int) * m.P * 8 * m.G, s, a.n_rows, m, x, y, r, slot, dr, (const double*)nullptr);
       return;
     }
   }
