@@ -65,6 +65,7 @@ CPU_SAMPLE = dict(n=48, steps=2)
 
 
 COARSE_FILTER = None  # --coarse-filter: solver.amg_coarse_filter override (additive key)
+VCYCLE_TRUNCATE = None  # --vcycle-truncate: solver.amg_vcycle_truncate override (additive key)
 DENSE_COARSE = None  # --dense-coarse: solver.amg_dense_coarse override (additive key)
 
 
@@ -83,6 +84,7 @@ def scenario(n, jitter, planes, estimator="spe", slabs=1):
                         "ground": {"kind": "constant", "value": 0.0}},
         "solver": dict({"preconditioner": "amg", "rel_tol": 1e-12, "max_iter": 500},
                        **({} if COARSE_FILTER is None else {"amg_coarse_filter": COARSE_FILTER}),
+                       **({} if VCYCLE_TRUNCATE is None else {"amg_vcycle_truncate": VCYCLE_TRUNCATE}),
                        **({} if DENSE_COARSE is None else {"amg_dense_coarse": DENSE_COARSE})),
         "estimator": {"mode": estimator, "window": 8},
     }
@@ -791,9 +793,13 @@ def run_b200(args):
                        "operator_pcg_and_result": "fp64: M_II (fp64 stencil-coded SELL-S, same products and row "
                                                   "order as CsrMatrix::apply), PCG vectors, dots, stopping rule "
                                                   "rel_tol 1e-12, K(x)x, RKC stages",
-                       "vcycle_preconditioner": "bf16 matrix values (packed SELL-S/SELL-P), fp32 vectors, "
-                                                "Chebyshev(2) fine / (1) coarse smoothing instead of SGS (DESIGN.md "
-                                                "§4.1-4.2)",
+                       "vcycle_preconditioner": "bf16 matrix values (packed SELL-S/SELL-P; fine-level rows carry "
+                                                "their bf16 row-sum correction), fp32 vectors, Chebyshev(2) fine / "
+                                                "(1) coarse smoothing instead of SGS, level-1 prolongator truncated "
+                                                "for the V-cycle with its coarser Galerkin operators recomputed "
+                                                "(DESIGN.md §4.1-4.2, 4.12-4.13; the reported amg_levels are the "
+                                                "reference hierarchy)",
+                       "vcycle_truncate": VCYCLE_TRUNCATE if VCYCLE_TRUNCATE is not None else 0.15,
                        "coarse_filter_eps": COARSE_FILTER if COARSE_FILTER is not None else 0.0025,
                        "dense_coarse_rows": DENSE_COARSE if DENSE_COARSE is not None else 512},
                    "parallelism": (f"node-ownership partition over {world} GPUs (owner-computes K(x)x, halo "
@@ -845,6 +851,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--coarse-filter", type=float, default=None,
                     help="solver.amg_coarse_filter (V-cycle coarse-operator filter, DESIGN.md §4)")
+    ap.add_argument("--vcycle-truncate", type=float, default=None,
+                    help="solver.amg_vcycle_truncate (V-cycle truncation of the level-1 prolongator, DESIGN.md §4.13)")
     ap.add_argument("--dense-coarse", type=int, default=None,
                     help="solver.amg_dense_coarse (dense explicit-inverse solve from the first level with at "
                          "most this many rows, DESIGN.md §4)")
@@ -868,8 +876,9 @@ def main():
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
         sys.exit(subprocess.call(cmd))
-    global COARSE_FILTER, DENSE_COARSE
+    global COARSE_FILTER, DENSE_COARSE, VCYCLE_TRUNCATE
     COARSE_FILTER = args.coarse_filter
+    VCYCLE_TRUNCATE = args.vcycle_truncate
     DENSE_COARSE = args.dense_coarse
     if args.impl == "reference":
         run_reference(args)

@@ -78,6 +78,7 @@ struct SolverParams {
   double amg_theta = 0.08, amg_omega = 4.0 / 3.0;
   int amg_sweeps = 1, amg_max_levels = 10, amg_coarse_limit = 64;
   double amg_coarse_filter = 0.0025;  // additive: V-cycle coarse-operator filter (0 = off)
+  double amg_vcycle_truncate = 0.15;   // additive: V-cycle truncation of the level-1 prolongator (0 = off)
   int amg_replicate_rows = 32768;     // additive: coarse levels up to this size are replicated on every rank
   int amg_dense_coarse = 512;         // additive: the device V-cycle solves the first coarse level with at most
                                       // this many rows directly (dense inverse); <= 0: recurse to the
@@ -163,6 +164,9 @@ class AmgDeviceBuilder {
 // below (the coarsest-level solve, amg.cpp:140); threaded for the larger
 // dense coarse levels of the device V-cycle (SolverParams::amg_dense_coarse)
 std::vector<double> dense_inverse(const HostCsr& a);
+// host CSR product / transpose of build_amg (proj/src/csr.cpp:133-166, 52-70)
+HostCsr csr_multiply(const HostCsr& a, const HostCsr& b);
+HostCsr csr_transposed(const HostCsr& a);
 // V-cycle operator of a coarse level: entries with |a_ij| < eps sqrt(|a_ii a_jj|)
 // dropped and lumped onto the diagonal (row sums kept). The hierarchy itself
 // (P, R, Galerkin A_l) is untouched; only the smoother/residual operator of

@@ -328,6 +328,85 @@ std::vector<double> inv_diagonal(const HostCsr& a) {
 }
 }  // namespace
 
+// V-cycle truncation of the level-1 prolongator (additive
+// key solver.amg_vcycle_truncate = theta): P_1 keeps the entries with
+// |p_ij| >= theta max_j |p_ij| of its row, rescaled to the row's sum (so
+// constants are still interpolated exactly), R_1 = P_1^T, and every coarser
+// Galerkin operator A_{m+1} = R_m A_m P_m is recomputed from there (device
+// SpGEMM). The reference hierarchy is stashed and restored once the device
+// levels are built, so the hierarchy the API reports stays the reference's.
+void GpuSystem::truncate_vcycle_prolongators() {
+  const double theta = prob_.solver.amg_vcycle_truncate;
+  auto& L = amg_.levels;
+  const int nl = (int)L.size();
+  if (!(theta > 0.0) || nl < 3) return;
+  const int l0 = 1;
+  amg_stash_.assign(nl, AmgHostLevel{});
+  amg_stash_coarse_inv_ = amg_.coarse_inverse;
+  {
+    HostCsr& P = L[l0].P;
+    HostCsr q;
+    q.n_rows = P.n_rows;
+    q.n_cols = P.n_cols;
+    q.row_ptr.assign(P.n_rows + 1, 0);
+    for (int i = 0; i < P.n_rows; ++i) {
+      double mx = 0.0, s0 = 0.0, s1 = 0.0;
+      for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k) {
+        mx = std::max(mx, std::fabs(P.values[k]));
+        s0 += P.values[k];
+      }
+      const size_t start = q.col_idx.size();
+      for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k)
+        if (std::fabs(P.values[k]) >= theta * mx) {
+          q.col_idx.push_back(P.col_idx[k]);
+          q.values.push_back(P.values[k]);
+          s1 += P.values[k];
+        }
+      const double f = s1 != 0.0 ? s0 / s1 : 0.0;
+      if (f >= 0.5 && f <= 2.0) {
+        for (size_t k = start; k < q.values.size(); ++k) q.values[k] *= f;
+      } else {  // the kept entries cannot carry the row sum: keep the row whole
+        q.col_idx.resize(start);
+        q.values.resize(start);
+        for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k) {
+          q.col_idx.push_back(P.col_idx[k]);
+          q.values.push_back(P.values[k]);
+        }
+      }
+      q.row_ptr[i + 1] = (int)q.col_idx.size();
+    }
+    amg_stash_[l0].P = std::move(P);
+    amg_stash_[l0].R = std::move(L[l0].R);
+    P = std::move(q);
+    L[l0].R = csr_transposed(P);
+  }
+  for (int l = l0; l + 1 < nl; ++l) {
+    HostCsr ap = device_ >= 0 ? spgemm_device(L[l].A, L[l].P, device_) : csr_multiply(L[l].A, L[l].P);
+    HostCsr ac = device_ >= 0 ? spgemm_device(L[l].R, ap, device_) : csr_multiply(L[l].R, ap);
+    amg_stash_[l + 1].A = std::move(L[l + 1].A);
+    L[l + 1].A = std::move(ac);
+  }
+  if (amg_.coarse_n > 0) amg_.coarse_inverse = dense_inverse(L.back().A);
+  memtrace("v-cycle P_1 truncated");
+}
+
+// puts the reference hierarchy back (or drops the stash when the global
+// hierarchy has been released on a multi-rank context)
+void GpuSystem::restore_reference_hierarchy() {
+  if (amg_stash_.empty()) return;
+  auto& L = amg_.levels;
+  const bool released = L.size() > 1 && L[1].A.n_rows == 0 && L[1].P.n_rows == 0;
+  if (!released)
+    for (size_t l = 1; l < L.size() && l < amg_stash_.size(); ++l) {
+      if (amg_stash_[l].P.n_rows) L[l].P = std::move(amg_stash_[l].P);
+      if (amg_stash_[l].R.n_rows) L[l].R = std::move(amg_stash_[l].R);
+      if (amg_stash_[l].A.n_rows) L[l].A = std::move(amg_stash_[l].A);
+    }
+  if (!released) amg_.coarse_inverse = std::move(amg_stash_coarse_inv_);
+  std::vector<AmgHostLevel>().swap(amg_stash_);
+  std::vector<double>().swap(amg_stash_coarse_inv_);
+}
+
 GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     : prob_(std::move(p)), device_(device), comm_(comm ? std::move(comm) : std::make_unique<SelfComm>()) {
   PhaseTimer timer(stats_.t_setup, "setup");
@@ -359,6 +438,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
   if (prob_.solver.precond == 2) amg_ = build_amg(m_ii_, prob_.solver, device_);
   ++stats_.precond_setups;
   memtrace("amg built");
+  if (prob_.solver.precond == 2) truncate_vcycle_prolongators();
   // device V-cycle depth: the first coarse level with at most amg_dense_coarse
   // rows is solved directly (explicit inverse of its Galerkin operator) instead
   // of recursing through the remaining latency-bound levels
@@ -398,6 +478,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     // device build, then let the next rank of the node start its host setup
     // (setup_gate: bounded concurrency of the host phase, capi.cpp)
     for (auto& lv : amg_.levels) lv.A = lv.P = lv.R = HostCsr{};
+    restore_reference_hierarchy();  // drops the stash
     malloc_trim(0);
     memtrace("global hierarchy released");
   }
@@ -424,6 +505,7 @@ GpuSystem::GpuSystem(Problem&& p, int device, std::unique_ptr<Comm> comm)
     plan_.mib = HostCsr{};
     std::vector<int>().swap(plan_.tet_dofs);
   }
+  restore_reference_hierarchy();
   memtrace("device built");
 }
 

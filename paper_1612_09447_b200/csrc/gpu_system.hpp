@@ -240,6 +240,8 @@ class GpuSystem {
   void set_stencil(bool on);            // stencil-coded fine-level V-cycle operator where available
   void set_stencil_sym(bool on);        // its symmetric half storage (SELL-SH) where built
   void set_stencil_rowsum(bool on);     // row-sum correction slot of the stencil copy (option 30)
+  void truncate_vcycle_prolongators();  // solver.amg_vcycle_truncate
+  void restore_reference_hierarchy();
   void set_vcycle_vectors_f32(bool on) {  // V-cycle vectors fp32 (default) or fp64
     invalidate_graphs();
     vcycle_f32_ = on;
@@ -386,6 +388,8 @@ class GpuSystem {
   int n_colors_ = -1;
   HostCsr m_ii_, m_ib_;
   AmgHierarchy amg_;
+  std::vector<AmgHostLevel> amg_stash_;  // reference P_1/R_1/A_l (l >= 2) while the V-cycle's are built
+  std::vector<double> amg_stash_coarse_inv_;
   SolveStats stats_;
   std::vector<SolveRecord> records_;
 

@@ -132,6 +132,9 @@ SimConfig parse_config(const std::string& text) {
       c.solver.amg_theta = js.value("amg_strength_threshold", c.solver.amg_theta);
       c.solver.amg_coarse_limit = js.value("amg_coarse_limit", c.solver.amg_coarse_limit);
       c.solver.amg_coarse_filter = js.value("amg_coarse_filter", c.solver.amg_coarse_filter);  // additive key
+      c.solver.amg_vcycle_truncate = js.value("amg_vcycle_truncate", c.solver.amg_vcycle_truncate);  // additive key
+      if (c.solver.amg_vcycle_truncate < 0.0 || c.solver.amg_vcycle_truncate >= 1.0)
+        throw ConfigError("solver amg_vcycle_truncate must be in [0, 1)");
       c.solver.amg_replicate_rows = js.value("amg_replicate_rows", c.solver.amg_replicate_rows);  // additive key
       c.solver.amg_dense_coarse = js.value("amg_dense_coarse", c.solver.amg_dense_coarse);        // additive key
       if (!(c.solver.rel_tol > 0)) throw ConfigError("solver rel_tol must be positive");

@@ -723,4 +723,7 @@ RkcCoefficients RkcCoefficients::compute(int s) {
   return k;
 }
 
+HostCsr csr_multiply(const HostCsr& a, const HostCsr& b) { return multiply(a, b); }
+HostCsr csr_transposed(const HostCsr& a) { return transposed(a); }
+
 }  // namespace eqsb

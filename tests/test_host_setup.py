@@ -68,6 +68,26 @@ def test_config_errors_map_to_reference_classes():
         eb.FemSystem(unknown_set, device=-1)
     with pytest.raises(eb.ParseError):
         eb.FemSystem({**cube(3), "mesh": {"file": "/nonexistent.msh"}}, device=-1)
+    trunc = cube(3)
+    trunc["solver"]["amg_vcycle_truncate"] = 1.5  # additive key, [0, 1)
+    with pytest.raises(eb.ConfigError):
+        eb.FemSystem(trunc, device=-1)
+
+
+def test_vcycle_truncation_keeps_the_reference_hierarchy():
+    """solver.amg_vcycle_truncate changes only the V-cycle's
+    copy of P_1 and the coarser Galerkin operators: the hierarchy a context
+    reports stays the reference algorithm's, bit for bit."""
+    cfg = cube(10, jitter=0.1)
+    off = dict(cfg, solver=dict(cfg["solver"], amg_vcycle_truncate=0.0))
+    g_on, g_off = eb.FemSystem(cfg, device=-1), eb.FemSystem(off, device=-1)
+    assert g_on.amg_levels() == g_off.amg_levels()
+    for lvl in range(len(g_on.amg_levels())):
+        for which in (0, 1, 2):
+            if lvl + 1 == len(g_on.amg_levels()) and which > 0:
+                continue
+            a, b = g_on.amg_level_csr(lvl, which), g_off.amg_level_csr(lvl, which)
+            assert all(np.array_equal(x, y) for x, y in zip(a, b))
     with pytest.raises(eb.InvalidArgument):
         c = cube(3)
         c["mesh"]["box"]["z_planes"] = [1.5, 2.0]

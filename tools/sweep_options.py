@@ -30,9 +30,13 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--dense-coarse", type=int, default=None)
+    ap.add_argument("--vcycle-truncate", type=float, default=None)
+    ap.add_argument("--coarse-filter", type=float, default=None)
     ap.add_argument("variants", nargs="*", default=["default"])
     args = ap.parse_args()
     bench.DENSE_COARSE = args.dense_coarse
+    bench.VCYCLE_TRUNCATE = args.vcycle_truncate
+    bench.COARSE_FILTER = args.coarse_filter
     import torch
     import paper_1612_09447_b200 as eb
     import ctypes as C
