@@ -795,11 +795,12 @@ def run_b200(args):
                                                   "rel_tol 1e-12, K(x)x, RKC stages",
                        "vcycle_preconditioner": "bf16 matrix values (packed SELL-S/SELL-P; fine-level rows carry "
                                                 "their bf16 row-sum correction), fp32 vectors, Chebyshev(2) fine / "
-                                                "(1) coarse smoothing instead of SGS, level-1 prolongator truncated "
-                                                "for the V-cycle with its coarser Galerkin operators recomputed "
+                                                "(1) coarse smoothing instead of SGS, prolongators of levels 0-2 "
+                                                "truncated for the V-cycle with the coarser Galerkin operators "
+                                                "recomputed "
                                                 "(DESIGN.md §4.1-4.2, 4.12-4.13; the reported amg_levels are the "
                                                 "reference hierarchy)",
-                       "vcycle_truncate": VCYCLE_TRUNCATE if VCYCLE_TRUNCATE is not None else 0.15,
+                       "vcycle_truncate": VCYCLE_TRUNCATE if VCYCLE_TRUNCATE is not None else [0.1, 0.15, 0.03],
                        "coarse_filter_eps": COARSE_FILTER if COARSE_FILTER is not None else 0.0025,
                        "dense_coarse_rows": DENSE_COARSE if DENSE_COARSE is not None else 512},
                    "parallelism": (f"node-ownership partition over {world} GPUs (owner-computes K(x)x, halo "
@@ -851,8 +852,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--coarse-filter", type=float, default=None,
                     help="solver.amg_coarse_filter (V-cycle coarse-operator filter, DESIGN.md §4)")
-    ap.add_argument("--vcycle-truncate", type=float, default=None,
-                    help="solver.amg_vcycle_truncate (V-cycle truncation of the level-1 prolongator, DESIGN.md §4.13)")
+    ap.add_argument("--vcycle-truncate", default=None,
+                    help="solver.amg_vcycle_truncate: comma-separated per-level prolongator truncation thresholds "
+                         "for the V-cycle, or 0 = off (DESIGN.md §4.13; default 0.1,0.15,0.03)")
     ap.add_argument("--dense-coarse", type=int, default=None,
                     help="solver.amg_dense_coarse (dense explicit-inverse solve from the first level with at "
                          "most this many rows, DESIGN.md §4)")
@@ -878,7 +880,9 @@ def main():
         sys.exit(subprocess.call(cmd))
     global COARSE_FILTER, DENSE_COARSE, VCYCLE_TRUNCATE
     COARSE_FILTER = args.coarse_filter
-    VCYCLE_TRUNCATE = args.vcycle_truncate
+    if args.vcycle_truncate is not None:
+        vt = [float(v) for v in str(args.vcycle_truncate).split(",")]
+        VCYCLE_TRUNCATE = 0 if vt == [0.0] else vt
     DENSE_COARSE = args.dense_coarse
     if args.impl == "reference":
         run_reference(args)

@@ -78,7 +78,8 @@ struct SolverParams {
   double amg_theta = 0.08, amg_omega = 4.0 / 3.0;
   int amg_sweeps = 1, amg_max_levels = 10, amg_coarse_limit = 64;
   double amg_coarse_filter = 0.0025;  // additive: V-cycle coarse-operator filter (0 = off)
-  double amg_vcycle_truncate = 0.15;   // additive: V-cycle truncation of the level-1 prolongator (0 = off)
+  std::vector<double> amg_vcycle_truncate = {0.1, 0.15, 0.03};  // additive: per-level V-cycle prolongator
+                                                                // truncation thresholds ({} / 0 = off)
   int amg_replicate_rows = 32768;     // additive: coarse levels up to this size are replicated on every rank
   int amg_dense_coarse = 512;         // additive: the device V-cycle solves the first coarse level with at most
                                       // this many rows directly (dense inverse); <= 0: recurse to the

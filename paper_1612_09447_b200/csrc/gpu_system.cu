@@ -328,66 +328,77 @@ std::vector<double> inv_diagonal(const HostCsr& a) {
 }
 }  // namespace
 
-// V-cycle truncation of the level-1 prolongator (additive
-// key solver.amg_vcycle_truncate = theta): P_1 keeps the entries with
-// |p_ij| >= theta max_j |p_ij| of its row, rescaled to the row's sum (so
-// constants are still interpolated exactly), R_1 = P_1^T, and every coarser
-// Galerkin operator A_{m+1} = R_m A_m P_m is recomputed from there (device
-// SpGEMM). The reference hierarchy is stashed and restored once the device
+// V-cycle truncation of the prolongators (additive key
+// solver.amg_vcycle_truncate = [theta_0, theta_1, ...], default [0.1, 0.15,
+// 0.03]): P_l keeps the entries with |p_ij| >= theta_l max_j |p_ij| of its
+// row, rescaled to the row's sum (so constants are still interpolated
+// exactly; rows whose kept entries cannot carry the sum stay whole),
+// R_l = P_l^T, and every coarser Galerkin operator A_{m+1} = R_m A_m P_m is
+// recomputed from the first truncated level on (device SpGEMM). The reference hierarchy is stashed and restored once the device
 // levels are built, so the hierarchy the API reports stays the reference's.
 void GpuSystem::truncate_vcycle_prolongators() {
-  const double theta = prob_.solver.amg_vcycle_truncate;
   auto& L = amg_.levels;
   const int nl = (int)L.size();
-  if (!(theta > 0.0) || nl < 3) return;
-  const int l0 = 1;
+  // theta per level: solver.amg_vcycle_truncate; the coarsest level's P is
+  // never truncated below a 3-level hierarchy
+  std::vector<double> theta(nl, 0.0);
+  for (int l = 0; l + 1 < nl && l < (int)prob_.solver.amg_vcycle_truncate.size(); ++l)
+    if (nl >= 3) theta[l] = prob_.solver.amg_vcycle_truncate[l];
+  for (int l = 0; l + 1 < nl; ++l) {  // EQS_VCYCLE_TRUNCATE_L<l>=theta overrides level l (experiments)
+    const std::string key = "EQS_VCYCLE_TRUNCATE_L" + std::to_string(l);
+    if (getenv(key.c_str())) theta[l] = atof(getenv(key.c_str()));
+  }
+  int l0 = -1;
+  for (int l = 0; l + 1 < nl && l0 < 0; ++l)
+    if (theta[l] > 0.0) l0 = l;
+  if (l0 < 0) return;
   amg_stash_.assign(nl, AmgHostLevel{});
   amg_stash_coarse_inv_ = amg_.coarse_inverse;
-  {
-    HostCsr& P = L[l0].P;
-    HostCsr q;
-    q.n_rows = P.n_rows;
-    q.n_cols = P.n_cols;
-    q.row_ptr.assign(P.n_rows + 1, 0);
-    for (int i = 0; i < P.n_rows; ++i) {
-      double mx = 0.0, s0 = 0.0, s1 = 0.0;
-      for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k) {
-        mx = std::max(mx, std::fabs(P.values[k]));
-        s0 += P.values[k];
-      }
-      const size_t start = q.col_idx.size();
-      for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k)
-        if (std::fabs(P.values[k]) >= theta * mx) {
-          q.col_idx.push_back(P.col_idx[k]);
-          q.values.push_back(P.values[k]);
-          s1 += P.values[k];
-        }
-      const double f = s1 != 0.0 ? s0 / s1 : 0.0;
-      if (f >= 0.5 && f <= 2.0) {
-        for (size_t k = start; k < q.values.size(); ++k) q.values[k] *= f;
-      } else {  // the kept entries cannot carry the row sum: keep the row whole
-        q.col_idx.resize(start);
-        q.values.resize(start);
-        for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k) {
-          q.col_idx.push_back(P.col_idx[k]);
-          q.values.push_back(P.values[k]);
-        }
-      }
-      q.row_ptr[i + 1] = (int)q.col_idx.size();
-    }
-    amg_stash_[l0].P = std::move(P);
-    amg_stash_[l0].R = std::move(L[l0].R);
-    P = std::move(q);
-    L[l0].R = csr_transposed(P);
-  }
   for (int l = l0; l + 1 < nl; ++l) {
+    if (theta[l] > 0.0) {
+      HostCsr& P = L[l].P;
+      HostCsr q;
+      q.n_rows = P.n_rows;
+      q.n_cols = P.n_cols;
+      q.row_ptr.assign(P.n_rows + 1, 0);
+      for (int i = 0; i < P.n_rows; ++i) {
+        double mx = 0.0, s0 = 0.0, s1 = 0.0;
+        for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k) {
+          mx = std::max(mx, std::fabs(P.values[k]));
+          s0 += P.values[k];
+        }
+        const size_t start = q.col_idx.size();
+        for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k)
+          if (std::fabs(P.values[k]) >= theta[l] * mx) {
+            q.col_idx.push_back(P.col_idx[k]);
+            q.values.push_back(P.values[k]);
+            s1 += P.values[k];
+          }
+        const double f = s1 != 0.0 ? s0 / s1 : 0.0;
+        if (f >= 0.5 && f <= 2.0) {
+          for (size_t k = start; k < q.values.size(); ++k) q.values[k] *= f;
+        } else {  // the kept entries cannot carry the row sum: keep the row whole
+          q.col_idx.resize(start);
+          q.values.resize(start);
+          for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k) {
+            q.col_idx.push_back(P.col_idx[k]);
+            q.values.push_back(P.values[k]);
+          }
+        }
+        q.row_ptr[i + 1] = (int)q.col_idx.size();
+      }
+      amg_stash_[l].P = std::move(P);
+      amg_stash_[l].R = std::move(L[l].R);
+      P = std::move(q);
+      L[l].R = csr_transposed(P);
+    }
     HostCsr ap = device_ >= 0 ? spgemm_device(L[l].A, L[l].P, device_) : csr_multiply(L[l].A, L[l].P);
     HostCsr ac = device_ >= 0 ? spgemm_device(L[l].R, ap, device_) : csr_multiply(L[l].R, ap);
-    amg_stash_[l + 1].A = std::move(L[l + 1].A);
+    if (!amg_stash_[l + 1].A.n_rows) amg_stash_[l + 1].A = std::move(L[l + 1].A);
     L[l + 1].A = std::move(ac);
   }
   if (amg_.coarse_n > 0) amg_.coarse_inverse = dense_inverse(L.back().A);
-  memtrace("v-cycle P_1 truncated");
+  memtrace("v-cycle prolongators truncated");
 }
 
 // puts the reference hierarchy back (or drops the stash when the global
@@ -395,9 +406,9 @@ void GpuSystem::truncate_vcycle_prolongators() {
 void GpuSystem::restore_reference_hierarchy() {
   if (amg_stash_.empty()) return;
   auto& L = amg_.levels;
-  const bool released = L.size() > 1 && L[1].A.n_rows == 0 && L[1].P.n_rows == 0;
+  const bool released = L.size() > 1 && L[0].A.n_rows == 0 && L[1].A.n_rows == 0;
   if (!released)
-    for (size_t l = 1; l < L.size() && l < amg_stash_.size(); ++l) {
+    for (size_t l = 0; l < L.size() && l < amg_stash_.size(); ++l) {
       if (amg_stash_[l].P.n_rows) L[l].P = std::move(amg_stash_[l].P);
       if (amg_stash_[l].R.n_rows) L[l].R = std::move(amg_stash_[l].R);
       if (amg_stash_[l].A.n_rows) L[l].A = std::move(amg_stash_[l].A);

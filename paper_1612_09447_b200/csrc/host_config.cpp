@@ -132,9 +132,19 @@ SimConfig parse_config(const std::string& text) {
       c.solver.amg_theta = js.value("amg_strength_threshold", c.solver.amg_theta);
       c.solver.amg_coarse_limit = js.value("amg_coarse_limit", c.solver.amg_coarse_limit);
       c.solver.amg_coarse_filter = js.value("amg_coarse_filter", c.solver.amg_coarse_filter);  // additive key
-      c.solver.amg_vcycle_truncate = js.value("amg_vcycle_truncate", c.solver.amg_vcycle_truncate);  // additive key
-      if (c.solver.amg_vcycle_truncate < 0.0 || c.solver.amg_vcycle_truncate >= 1.0)
-        throw ConfigError("solver amg_vcycle_truncate must be in [0, 1)");
+      if (js.contains("amg_vcycle_truncate")) {  // additive key: per-level thresholds, or 0 = off
+        const json& jt = js.at("amg_vcycle_truncate");
+        if (jt.is_number()) {
+          if (jt.get<double>() != 0.0) throw ConfigError("solver amg_vcycle_truncate: a list of per-level thresholds or 0");
+          c.solver.amg_vcycle_truncate.clear();
+        } else if (jt.is_array()) {
+          c.solver.amg_vcycle_truncate = jt.get<std::vector<double>>();
+        } else {
+          throw ConfigError("solver amg_vcycle_truncate: a list of per-level thresholds or 0");
+        }
+        for (double t : c.solver.amg_vcycle_truncate)
+          if (!(t >= 0.0 && t < 1.0)) throw ConfigError("solver amg_vcycle_truncate thresholds must be in [0, 1)");
+      }
       c.solver.amg_replicate_rows = js.value("amg_replicate_rows", c.solver.amg_replicate_rows);  // additive key
       c.solver.amg_dense_coarse = js.value("amg_dense_coarse", c.solver.amg_dense_coarse);        // additive key
       if (!(c.solver.rel_tol > 0)) throw ConfigError("solver rel_tol must be positive");

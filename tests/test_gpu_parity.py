@@ -407,8 +407,8 @@ def test_graph_pcg_loop_and_pdl_rkc_steps_bit_identical():
 
 
 def test_vcycle_truncation_solves_to_the_oracle():
-    """The V-cycle with the truncated level-1 prolongator (default
-    solver.amg_vcycle_truncate = 0.15) is a different
+    """The V-cycle with truncated prolongators (default
+    solver.amg_vcycle_truncate = [0.1, 0.15, 0.03]) is a different
     preconditioner, not a different solve: the M-solve lands on the oracle's
     solution to the solver tolerance with at most one more PCG iteration than
     the reference hierarchy's V-cycle, and a short RKC run matches the oracle."""

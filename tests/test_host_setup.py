@@ -69,9 +69,10 @@ def test_config_errors_map_to_reference_classes():
     with pytest.raises(eb.ParseError):
         eb.FemSystem({**cube(3), "mesh": {"file": "/nonexistent.msh"}}, device=-1)
     trunc = cube(3)
-    trunc["solver"]["amg_vcycle_truncate"] = 1.5  # additive key, [0, 1)
-    with pytest.raises(eb.ConfigError):
-        eb.FemSystem(trunc, device=-1)
+    for bad_t in (1.5, [0.1, 1.5], "x"):  # additive key: per-level thresholds in [0, 1), or 0
+        trunc["solver"]["amg_vcycle_truncate"] = bad_t
+        with pytest.raises(eb.ConfigError):
+            eb.FemSystem(trunc, device=-1)
 
 
 def test_vcycle_truncation_keeps_the_reference_hierarchy():

@@ -30,12 +30,14 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--dense-coarse", type=int, default=None)
-    ap.add_argument("--vcycle-truncate", type=float, default=None)
+    ap.add_argument("--vcycle-truncate", default=None, help="comma-separated per-level thresholds or 0")
     ap.add_argument("--coarse-filter", type=float, default=None)
     ap.add_argument("variants", nargs="*", default=["default"])
     args = ap.parse_args()
     bench.DENSE_COARSE = args.dense_coarse
-    bench.VCYCLE_TRUNCATE = args.vcycle_truncate
+    if args.vcycle_truncate is not None:
+        vt = [float(v) for v in args.vcycle_truncate.split(",")]
+        bench.VCYCLE_TRUNCATE = 0 if vt == [0.0] else vt
     bench.COARSE_FILTER = args.coarse_filter
     import torch
     import paper_1612_09447_b200 as eb
