@@ -42,6 +42,8 @@ def main():
         if ("k_sell_red<1, double, double, 0>" in n or "k_sells64<0" in n or "k_pcg_update" in n
                 or "k_pcg_direction" in n):
             cls["pcg spmv+vectors"] += b
+        elif "k_sells64" in n or "k_sell_red<1, double, double, 1>" in n or "k_sell_red<1, double, double, -1>" in n:
+            cls["fp64 spmv (start residual, SPE basis)"] += b  # not V-cycle kernels
         elif "k_kx_" in n:
             cls["stiffness K(x)x"] += b
         elif any(k in n for k in ("k_multi_dot", "k_orth_update", "k_lincomb", "k_scale_rsqrt")):
