@@ -137,6 +137,9 @@ struct AmgHierarchy {
 AmgHierarchy build_amg(const HostCsr& a, const SolverParams& sp, int device = -1);
 // C = A B on the GPU with the host product's per-row arithmetic order
 // (k_spgemm.cu). With diag, A is replaced by I - omega D^-1 A on the fly.
+// A_{k+1} = R_k (A_k P_k) for k = 0.. with A_0 = fine, operands resident on the GPU
+std::vector<HostCsr> galerkin_chain_device(const HostCsr& fine, const std::vector<const HostCsr*>& p,
+                                           const std::vector<const HostCsr*>& r, int device);
 HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std::vector<double>* diag = nullptr,
                       double omega = 0.0, long long batch_products = 1ll << 28);
 // Device-resident Galerkin chain of build_amg: the fine operator and P stay on

@@ -392,10 +392,27 @@ void GpuSystem::truncate_vcycle_prolongators() {
       P = std::move(q);
       L[l].R = csr_transposed(P);
     }
-    HostCsr ap = device_ >= 0 ? spgemm_device(L[l].A, L[l].P, device_) : csr_multiply(L[l].A, L[l].P);
-    HostCsr ac = device_ >= 0 ? spgemm_device(L[l].R, ap, device_) : csr_multiply(L[l].R, ap);
-    if (!amg_stash_[l + 1].A.n_rows) amg_stash_[l + 1].A = std::move(L[l + 1].A);
-    L[l + 1].A = std::move(ac);
+  }
+  // Galerkin operators below the first truncated level
+  std::vector<const HostCsr*> ps, rs;
+  for (int l = l0; l + 1 < nl; ++l) {
+    ps.push_back(&L[l].P);
+    rs.push_back(&L[l].R);
+  }
+  std::vector<HostCsr> ac;
+  if (device_ >= 0) {
+    ac = galerkin_chain_device(L[l0].A, ps, rs, device_);
+  } else {
+    ac.reserve(ps.size());
+    const HostCsr* a = &L[l0].A;
+    for (size_t k = 0; k < ps.size(); ++k) {
+      ac.push_back(csr_multiply(*rs[k], csr_multiply(*a, *ps[k])));
+      a = &ac.back();
+    }
+  }
+  for (int l = l0; l + 1 < nl; ++l) {
+    amg_stash_[l + 1].A = std::move(L[l + 1].A);
+    L[l + 1].A = std::move(ac[l - l0]);
   }
   if (amg_.coarse_n > 0) amg_.coarse_inverse = dense_inverse(L.back().A);
   memtrace("v-cycle prolongators truncated");

@@ -412,4 +412,28 @@ HostCsr spgemm_device(const HostCsr& a, const HostCsr& b, int device, const std:
   return c;
 }
 
+// Galerkin chain A_{k+1} = R_k (A_k P_k) with every operand and the running
+// coarse operator resident on the device; only the coarse operators return
+std::vector<HostCsr> galerkin_chain_device(const HostCsr& fine, const std::vector<const HostCsr*>& p,
+                                           const std::vector<const HostCsr*>& r, int device) {
+  SpgemmDevice sd;
+  sd.init(device);
+  DCsr a;
+  sd.upload(fine, a);
+  std::vector<HostCsr> out;
+  for (size_t k = 0; k < p.size(); ++k) {
+    DCsr dp, dr, ap, c;
+    sd.upload(*p[k], dp);
+    sd.multiply(a, dp, ap, nullptr, 0.0, 1ll << 28);
+    dp = DCsr();
+    sd.upload(*r[k], dr);
+    sd.multiply(dr, ap, c, nullptr, 0.0, 1ll << 28);
+    HostCsr hc;
+    sd.download(c, hc);
+    out.push_back(std::move(hc));
+    a = std::move(c);
+  }
+  return out;
+}
+
 }  // namespace eqsb
